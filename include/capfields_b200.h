@@ -1,0 +1,154 @@
+/*
+ * capfields_b200 — C-ABI of the B200-native Instant-NVR render back-end hot path.
+ *
+ * Every entry point takes plain device pointers + sizes and a caller-supplied
+ * stream (`void* stream` = cudaStream_t, NULL = legacy default stream). All calls
+ * are stream-ordered and asynchronous unless stated; none allocate on the hot
+ * call (handles own their storage, sized at create time). No torch types.
+ *
+ * Status codes map 1:1 onto the reference's exception classes (the Python shim
+ * re-raises them):
+ *   CF_E_OUT_OF_SUPPORT  -> capfields.edgraph.OutOfSupportError   (edgraph.py:27)
+ *   CF_E_DUPLICATE_FRAME -> ValueError "frame already registered"  (knnfield.py:132-133)
+ *   CF_E_BAD_ARG         -> ValueError                             (knnfield.py:56-57,134-135)
+ *   CF_E_DEGENERATE      -> capfields.transforms.DegenerateWeightsError (transforms.py:15)
+ *   CF_E_CUDA            -> RuntimeError (device fault / launch failure)
+ * cf_last_error() returns a thread-local message for the last non-zero status.
+ *
+ * Reference interfaces replaced (the reference has no FFI; these are the Python
+ * functions whose bodies the calls stand in for — see INTEGRATION.md):
+ *   cf_deform_nodes            <- edgraph.deformed_nodes            edgraph.py:134-136
+ *   cf_knn_warp                <- edgraph.warp_backward_batch       edgraph.py:174-183
+ *                                 edgraph.warp_forward_batch        edgraph.py:154-162
+ *                                 knnfield.brute_force_query        knnfield.py:32-42
+ *                                 knnfield.brute_force_neighbors_batch knnfield.py:25-29
+ *   cf_knnfield_build          <- KnnField._build_canonical_field   knnfield.py:93-120
+ *   cf_knnfield_update         <- KnnField.update_live_map          knnfield.py:124-167
+ *                                 KnnField._dilate_once             knnfield.py:169-188
+ *   cf_knnfield_query          <- KnnField.query_motion_batch       knnfield.py:197-222
+ *   cf_lbs_forward             <- skeleton.lbs_batch                skeleton.py:142-149
+ *   cf_lbs_backward            <- (builder-defined inverse of lbs_batch)
+ *   cf_hashgrid_encode(_bwd)   <- SPEC nrf.hash_encode
+ *   cf_field_forward           <- SPEC nrf E_g/E_c/DeformNet
+ *   cf_render_*                <- SPEC nrf.volume_render/render_view SPEC.md:381-407
+ */
+#ifndef CAPFIELDS_B200_H
+#define CAPFIELDS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CF_OK 0
+#define CF_E_BAD_ARG 1
+#define CF_E_OUT_OF_SUPPORT 2
+#define CF_E_DUPLICATE_FRAME 3
+#define CF_E_DEGENERATE 4
+#define CF_E_CUDA 5
+
+int cf_version(void);
+const char* cf_last_error(void);
+/* number of SMs of the current device (grid sizing helper for hosts) */
+int cf_device_sm_count(void);
+
+/* ---------------------------------------------------------------- deformation */
+
+/* anchors[i] = dq_apply(dqs[i], nodes[i]) in float64, bit-identical to the
+ * reference's numpy evaluation order (edgraph.py:134-136). */
+int cf_deform_nodes(const double* nodes, const double* dqs, int64_t n, double* anchors, void* stream);
+
+/* Coarse voxel buckets over a point set (ED anchors or posed skin vertices):
+ * counting sort of point ids into a uniform grid, rebuilt per frame into
+ * storage sized at create time. */
+typedef struct cf_buckets cf_buckets_t;
+int cf_buckets_create(int64_t max_points, int max_grid_res, cf_buckets_t** out);
+int cf_buckets_destroy(cf_buckets_t* b);
+/* grid_res <= 0 picks a resolution from n (~4 points per occupied cell). */
+int cf_buckets_build(cf_buckets_t* b, const double* pts, int64_t n, int grid_res, void* stream);
+
+/* Exact k-NN (ties by index, squared distance evaluated as the reference's
+ * sum((p - a)**2)) over `anchors` followed by the dual-quaternion blend.
+ *   mode CF_WARP_BACKWARD  : warp_backward_batch  (safe_w = valid ? w : 1, DQB^-1 applied)
+ *   mode CF_WARP_FORWARD   : warp_forward_batch   (safe_w = valid ? w : 1, DQB applied)
+ *   mode CF_BRUTE_QUERY    : brute_force_query    (max(w,1e-300), DQB^-1 applied)
+ *   mode CF_NEIGHBORS_ONLY : brute_force_neighbors_batch (idx only)
+ * `buckets` NULL -> exhaustive scan (trivially-correct brute-force kernel);
+ * otherwise the hierarchical bucket ring search (bit-identical results).
+ * Any of idx_out (int64, N*k), w_out (N*k), pc_out (N*3), valid_out (N) may be NULL. */
+#define CF_WARP_BACKWARD 0
+#define CF_WARP_FORWARD 1
+#define CF_BRUTE_QUERY 2
+#define CF_NEIGHBORS_ONLY 3
+int cf_knn_warp(const cf_buckets_t* buckets, const double* anchors, const double* dqs, int64_t n_nodes,
+                int k, double radius, int mode, const double* pts, int64_t n_pts,
+                int64_t* idx_out, double* w_out, double* pc_out, uint8_t* valid_out, void* stream);
+
+/* ------------------------------------------------------------------ KnnField */
+
+/* neighbor_idx (res^3, s) int32, -1 outside support (knnfield.py:93-120). */
+int cf_knnfield_build(const double* nodes, int64_t n, int s, int res, const double* bbox_min,
+                      double voxel_size, double support_radius, int32_t* neighbor_idx, void* stream);
+/* live map of one frame (knnfield.py:124-188). scratch_u64: res^3 uint64;
+ * scratch_i32: res^3 int32 (pre-dilation map). */
+int cf_knnfield_update(const double* nodes, const double* dqs, int64_t n, const int32_t* neighbor_idx, int s,
+                       int res, const double* bbox_min, double voxel_size, double radius, int32_t* live_out,
+                       uint64_t* scratch_u64, int32_t* scratch_i32, void* stream);
+/* O(1) query (knnfield.py:197-222): anchors_frame = deformed nodes of the frame,
+ * dqs_frame = the frame's LUT block. nbr_out int64 (N,s). */
+int cf_knnfield_query(const int32_t* live, const int32_t* neighbor_idx, const double* dqs_frame,
+                      const double* anchors_frame, int s, int res, const double* bbox_min, double voxel_size,
+                      double radius, const double* pts, int64_t n_pts, int64_t* nbr_out, double* w_out,
+                      double* pc_out, uint8_t* valid_out, void* stream);
+
+/* ------------------------------------------------------------------ skeleton */
+
+/* forward LBS (skeleton.py:142-149): A (J,4,4) float64, weights (N,J). */
+int cf_lbs_forward(const double* A, int J, const double* pts, const double* weights, int64_t n_pts, double* out,
+                   void* stream);
+/* per-frame vertex transforms for the backward warp: T_v = sum_j W[v,j] A_j[:3,:],
+ * Tinv_v its inverse, both (V,3,4) row-major; T_out may be NULL. */
+int cf_lbs_vertex_transforms(const double* A, int J, const double* vert_weights, int64_t n_verts, double* T_out,
+                             double* Tinv_out, void* stream);
+/* backward LBS (builder-defined): nearest posed skin vertex
+ * v* (exact 1-NN, ties by index; vert_buckets built over verts_posed, or NULL
+ * for an exhaustive scan) -> p_c = Tinv_{v*} [p, 1];
+ * valid = |p - v*|^2 <= max_dist^2. */
+int cf_lbs_backward(const cf_buckets_t* vert_buckets, const double* verts_posed, const double* vert_Tinv,
+                    int64_t n_verts, double max_dist, const double* pts, int64_t n_pts, int64_t* vert_out,
+                    double* pc_out, uint8_t* valid_out, void* stream);
+
+/* ------------------------------------------------------------------ hash grid */
+
+#define CF_MAX_LEVELS 16
+typedef struct cf_hashgrid_desc {
+  int n_levels;       /* L */
+  int n_features;     /* F (2 or 4) */
+  int log2_table;     /* log2 T */
+  int base_resolution;
+  int max_resolution;
+  int resolution[CF_MAX_LEVELS]; /* N_l */
+  int dense[CF_MAX_LEVELS];      /* 1: dense (N_l+1)^3 indexing */
+  int64_t offset[CF_MAX_LEVELS + 1]; /* entry offsets of each level, offset[L] = total entries */
+} cf_hashgrid_desc;
+
+/* fill desc from (L, F, log2T, N_min, N_max) */
+int cf_hashgrid_init(cf_hashgrid_desc* desc, int n_levels, int n_features, int log2_table, int base_res,
+                     int max_res);
+/* pts (N,3) float32 in [0,1]^3 (clamped); table (entries, F) float32;
+ * feat_out (N, L*F) float32. */
+int cf_hashgrid_encode(const cf_hashgrid_desc* desc, const float* table, const float* pts, int64_t n_pts,
+                       float* feat_out, void* stream);
+/* table_grad += dL/dtable, atomics (dfeat (N, L*F)). */
+int cf_hashgrid_encode_bwd(const cf_hashgrid_desc* desc, const float* pts, const float* dfeat, int64_t n_pts,
+                           float* table_grad, void* stream);
+/* parity probe: idx_out (N, L, 8) uint32 entry indices within each level,
+ * w_out (N, L, 8) float32 trilinear weights. */
+int cf_hashgrid_indices(const cf_hashgrid_desc* desc, const float* pts, int64_t n_pts, uint32_t* idx_out,
+                        float* w_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CAPFIELDS_B200_H */

@@ -1,0 +1,137 @@
+"""ctypes binding of the C-ABI library (include/capfields_b200.h).
+
+The library is the product: if it is missing or CUDA is unavailable, every
+entry point raises — there is no CPU fallback on any path.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import torch
+
+from .errors import DegenerateWeightsError, OutOfSupportError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libcapfields_b200.so")
+
+CF_OK = 0
+CF_E_BAD_ARG = 1
+CF_E_OUT_OF_SUPPORT = 2
+CF_E_DUPLICATE_FRAME = 3
+CF_E_DEGENERATE = 4
+CF_E_CUDA = 5
+
+CF_WARP_BACKWARD = 0
+CF_WARP_FORWARD = 1
+CF_BRUTE_QUERY = 2
+CF_NEIGHBORS_ONLY = 3
+
+CF_MAX_LEVELS = 16
+
+_p = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_i32 = ctypes.c_int
+_f64 = ctypes.c_double
+
+
+class HashGridDesc(ctypes.Structure):
+    _fields_ = [
+        ("n_levels", ctypes.c_int),
+        ("n_features", ctypes.c_int),
+        ("log2_table", ctypes.c_int),
+        ("base_resolution", ctypes.c_int),
+        ("max_resolution", ctypes.c_int),
+        ("resolution", ctypes.c_int * CF_MAX_LEVELS),
+        ("dense", ctypes.c_int * CF_MAX_LEVELS),
+        ("offset", ctypes.c_int64 * (CF_MAX_LEVELS + 1)),
+    ]
+
+
+# name -> argtypes (all return int status)
+_SIGS = {
+    "cf_device_sm_count": [],
+    "cf_deform_nodes": [_p, _p, _i64, _p, _p],
+    "cf_buckets_create": [_i64, _i32, ctypes.POINTER(_p)],
+    "cf_buckets_destroy": [_p],
+    "cf_buckets_build": [_p, _p, _i64, _i32, _p],
+    "cf_knn_warp": [_p, _p, _p, _i64, _i32, _f64, _i32, _p, _i64, _p, _p, _p, _p, _p],
+    "cf_knnfield_build": [_p, _i64, _i32, _i32, _p, _f64, _f64, _p, _p],
+    "cf_knnfield_update": [_p, _p, _i64, _p, _i32, _i32, _p, _f64, _f64, _p, _p, _p, _p],
+    "cf_knnfield_query": [_p, _p, _p, _p, _i32, _i32, _p, _f64, _f64, _p, _i64, _p, _p, _p, _p, _p],
+    "cf_lbs_forward": [_p, _i32, _p, _p, _i64, _p, _p],
+    "cf_lbs_vertex_transforms": [_p, _i32, _p, _i64, _p, _p, _p],
+    "cf_lbs_backward": [_p, _p, _p, _i64, _f64, _p, _i64, _p, _p, _p, _p],
+    "cf_hashgrid_init": [ctypes.POINTER(HashGridDesc), _i32, _i32, _i32, _i32, _i32],
+    "cf_hashgrid_encode": [ctypes.POINTER(HashGridDesc), _p, _p, _i64, _p, _p],
+    "cf_hashgrid_encode_bwd": [ctypes.POINTER(HashGridDesc), _p, _p, _i64, _p, _p],
+    "cf_hashgrid_indices": [ctypes.POINTER(HashGridDesc), _p, _i64, _p, _p, _p],
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+def lib():
+    """Load the library (once). Raises if it was not built or CUDA is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"capfields_b200 CUDA library not built ({LIB_PATH}); run `python -m paper_2304_03184_b200.build`"
+            )
+        handle = ctypes.CDLL(LIB_PATH)
+        for name, args in _SIGS.items():
+            fn = getattr(handle, name, None)
+            if fn is None:
+                continue
+            fn.argtypes = args
+            fn.restype = ctypes.c_int
+        handle.cf_last_error.restype = ctypes.c_char_p
+        handle.cf_last_error.argtypes = []
+        _lib = handle
+    return _lib
+
+
+def exported_symbols() -> list[str]:
+    return list(_SIGS.keys()) + ["cf_version", "cf_last_error"]
+
+
+def require_cuda() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("capfields_b200 needs a CUDA device (sm_100a); there is no CPU path")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_ptr() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == CF_OK:
+        return
+    msg = lib().cf_last_error().decode(errors="replace")
+    text = f"{what}: {msg}" if what else msg
+    if rc == CF_E_OUT_OF_SUPPORT:
+        raise OutOfSupportError(text)
+    if rc == CF_E_DEGENERATE:
+        raise DegenerateWeightsError(text)
+    if rc in (CF_E_BAD_ARG, CF_E_DUPLICATE_FRAME):
+        raise ValueError(msg)
+    raise RuntimeError(text)
+
+
+def call(name: str, *args) -> None:
+    check(getattr(lib(), name)(*args), name)
+
+
+def ptr(t) -> int | None:
+    """Device pointer of a tensor (None -> NULL)."""
+    if t is None:
+        return None
+    return t.data_ptr()

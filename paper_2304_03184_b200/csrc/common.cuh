@@ -1,0 +1,63 @@
+// Shared helpers: status plumbing, launch sizing, IEEE-exact fp64 arithmetic.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+
+#include "../../include/capfields_b200.h"
+
+namespace cf {
+
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int check_launch(const char* what);
+int sm_count();
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// grid for a grid-stride kernel: enough CTAs for `per_sm` resident CTAs on every SM
+inline unsigned grid_for(int64_t n, int block, int per_sm = 8) {
+  int64_t need = (n + block - 1) / block;
+  int64_t cap = (int64_t)sm_count() * per_sm;
+  if (need < 1) need = 1;
+  return (unsigned)(need < cap ? need : cap);
+}
+
+}  // namespace cf
+
+#define CF_CHECK_CUDA(call)                                                                 \
+  do {                                                                                      \
+    cudaError_t _e = (call);                                                                \
+    if (_e != cudaSuccess) return cf::fail(CF_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// IEEE round-to-nearest fp64 ops that ptxas may not contract into FMAs. The
+// reference evaluates every expression as separate numpy ufunc calls, each a
+// correctly rounded binary op; using these keeps the device result bit-equal.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double x_mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double x_add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double x_sub(double a, double b) { return __dadd_rn(a, -b); }
+__device__ __forceinline__ double x_div(double a, double b) { return __ddiv_rn(a, b); }
+
+__device__ __forceinline__ float f_mul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float f_add(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float f_sub(float a, float b) { return __fadd_rn(a, -b); }
+
+struct d3 {
+  double x, y, z;
+};
+
+__device__ __forceinline__ d3 load_d3(const double* p) { return d3{p[0], p[1], p[2]}; }
+__device__ __forceinline__ void store_d3(double* p, d3 v) {
+  p[0] = v.x;
+  p[1] = v.y;
+  p[2] = v.z;
+}
+
+// sum((a - b)**2) with numpy's sequential reduction order: (dx*dx + dy*dy) + dz*dz
+__device__ __forceinline__ double sqdist(d3 a, d3 b) {
+  double dx = x_sub(a.x, b.x), dy = x_sub(a.y, b.y), dz = x_sub(a.z, b.z);
+  return x_add(x_add(x_mul(dx, dx), x_mul(dy, dy)), x_mul(dz, dz));
+}

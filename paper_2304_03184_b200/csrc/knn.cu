@@ -1,0 +1,328 @@
+// Per-frame node deformation, coarse node buckets, and the fused exact
+// k-NN + dual-quaternion blend kernels behind
+//   edgraph.warp_backward_batch / warp_forward_batch  (edgraph.py:139-183)
+//   knnfield.brute_force_query / brute_force_neighbors_batch (knnfield.py:20-42)
+// All geometry is float64 in the reference's evaluation order (dq.cuh), so the
+// k-NN indices are bit-identical and the positions match to the last bits of exp().
+#include <algorithm>
+#include <cmath>
+
+#include "buckets.cuh"
+#include "dq.cuh"
+
+namespace {
+
+constexpr double kWeightFloor = 1e-6;  // edgraph.py:24
+
+__global__ void deform_nodes_kernel(const double* __restrict__ nodes, const double* __restrict__ dqs, int64_t n,
+                                    double* __restrict__ anchors) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    dq8 q = load_dq(dqs + 8 * i);
+    store_d3(anchors + 3 * i, dq_apply(q, load_d3(nodes + 3 * i)));
+  }
+}
+
+// ------------------------------------------------------------------ buckets
+
+__global__ void bucket_params_kernel(const double* __restrict__ pts, int n, int G, BucketParams* P) {
+  __shared__ double smin[3][32], smax[3][32];
+  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    for (int a = 0; a < 3; ++a) {
+      double v = pts[3 * i + a];
+      lo[a] = fmin(lo[a], v);
+      hi[a] = fmax(hi[a], v);
+    }
+  for (int a = 0; a < 3; ++a)
+    for (int o = 16; o > 0; o >>= 1) {
+      lo[a] = fmin(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+      hi[a] = fmax(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+    }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0)
+    for (int a = 0; a < 3; ++a) {
+      smin[a][w] = lo[a];
+      smax[a][w] = hi[a];
+    }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int nw = blockDim.x >> 5;
+    double mn[3], mx[3], ext = 0.0, scale = 0.0;
+    for (int a = 0; a < 3; ++a) {
+      mn[a] = smin[a][0];
+      mx[a] = smax[a][0];
+      for (int j = 1; j < nw; ++j) {
+        mn[a] = fmin(mn[a], smin[a][j]);
+        mx[a] = fmax(mx[a], smax[a][j]);
+      }
+      ext = fmax(ext, mx[a] - mn[a]);
+      scale = fmax(scale, fmax(fabs(mn[a]), fabs(mx[a])));
+    }
+    if (!(ext > 0.0)) ext = fmax(scale, 1.0) * 1e-3;
+    const double h = ext * (1.0 + 1e-9) / G;
+    for (int a = 0; a < 3; ++a) {
+      P->origin[a] = mn[a] - 1e-12 * (fabs(mn[a]) + ext);
+      int g = (int)ceil((mx[a] - P->origin[a]) / h);
+      P->g[a] = g < 1 ? 1 : (g > G ? G : g);
+    }
+    P->h = h;
+    P->margin = 1e-10 * (scale + ext) + 1e-300;
+    P->n = n;
+  }
+}
+
+__global__ void bucket_count_kernel(const double* __restrict__ pts, int n, const BucketParams* __restrict__ Pp,
+                                    int* __restrict__ counts, int* __restrict__ point_cell,
+                                    int* __restrict__ point_slot) {
+  const BucketParams P = *Pp;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    int c[3];
+    bucket_cell(P, load_d3(pts + 3 * i), c);
+    const int cell = (c[2] * P.g[1] + c[1]) * P.g[0] + c[0];
+    point_cell[i] = cell;
+    point_slot[i] = atomicAdd(counts + cell, 1);
+  }
+}
+
+// single-CTA exclusive scan, in place: counts[0..ncells] -> starts
+__global__ void bucket_scan_kernel(int* __restrict__ cells, const BucketParams* __restrict__ Pp) {
+  __shared__ int warp_tot[32];
+  __shared__ int carry;
+  const int ncells = Pp->g[0] * Pp->g[1] * Pp->g[2];
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base <= ncells; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    const int v = (i < ncells) ? cells[i] : 0;
+    int x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, x, o);
+      if ((threadIdx.x & 31) >= o) x += y;
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 31) warp_tot[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      int t = (threadIdx.x < (blockDim.x >> 5)) ? warp_tot[threadIdx.x] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, t, o);
+        if (threadIdx.x >= o) t += y;
+      }
+      if (threadIdx.x < (blockDim.x >> 5)) warp_tot[threadIdx.x] = t;
+    }
+    __syncthreads();
+    const int excl = carry + (w > 0 ? warp_tot[w - 1] : 0) + x - v;
+    if (i <= ncells) cells[i] = excl;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = excl + v;
+    __syncthreads();
+  }
+}
+
+__global__ void bucket_scatter_kernel(const double* __restrict__ pts, int n, const int* __restrict__ cell_start,
+                                      const int* __restrict__ point_cell, const int* __restrict__ point_slot,
+                                      double4* __restrict__ sorted) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int dst = cell_start[point_cell[i]] + point_slot[i];
+    sorted[dst] = make_double4(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2], (double)i);
+  }
+}
+
+// ------------------------------------------------------------------ k-NN + blend
+
+struct WarpArgs {
+  const double* anchors;
+  const double* dqs;
+  int n_nodes;
+  int k;
+  double r2;  // radius * radius
+  int mode;
+  const double* pts;
+  int64_t n_pts;
+  int64_t* idx_out;
+  double* w_out;
+  double* pc_out;
+  uint8_t* valid_out;
+};
+
+template <int K>
+__device__ __forceinline__ void finish_query(const WarpArgs& A, int64_t q, d3 p, const TopK<K>& top) {
+  double w[K];
+  bool valid = false;
+#pragma unroll
+  for (int j = 0; j < K; ++j)
+    if (j < A.k) {
+      // np.exp(-d2 / (r * r))
+      w[j] = exp(x_div(-top.d[j], A.r2));
+      valid |= w[j] > kWeightFloor;
+    }
+#pragma unroll
+  for (int j = 0; j < K; ++j)
+    if (j < A.k) {
+      if (A.idx_out) A.idx_out[q * A.k + j] = top.i[j];
+      if (A.w_out) A.w_out[q * A.k + j] = w[j];
+    }
+  if (A.valid_out) A.valid_out[q] = valid ? 1 : 0;
+  if (A.mode == CF_NEIGHBORS_ONLY || !A.pc_out) return;
+  DqbAcc acc;
+#pragma unroll
+  for (int j = 0; j < K; ++j)
+    if (j < A.k) {
+      double wj;
+      if (A.mode == CF_BRUTE_QUERY)
+        wj = fmax(w[j], 1e-300);  // knnfield.py:41
+      else
+        wj = valid ? w[j] : 1.0;  // edgraph.py:149
+      acc.add(wj, load_dq(A.dqs + 8 * (int64_t)top.i[j]));
+    }
+  dq8 b = acc.result();
+  if (A.mode != CF_WARP_FORWARD) b = dq_conj(b);
+  store_d3(A.pc_out + 3 * q, dq_apply(b, p));
+}
+
+template <int K>
+__global__ void __launch_bounds__(128) knn_brute_kernel(WarpArgs A) {
+  constexpr int TILE = 512;
+  __shared__ double4 tile[TILE];
+  const int64_t nblk = (A.n_pts + blockDim.x - 1) / blockDim.x;
+  for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    const int64_t q = blk * blockDim.x + threadIdx.x;
+    const bool live = q < A.n_pts;
+    d3 p = live ? load_d3(A.pts + 3 * q) : d3{0.0, 0.0, 0.0};
+    TopK<K> top;
+    top.init(A.k);
+    for (int base = 0; base < A.n_nodes; base += TILE) {
+      const int cnt = min(TILE, A.n_nodes - base);
+      __syncthreads();
+      for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
+        const double* a = A.anchors + 3 * (int64_t)(base + t);
+        tile[t] = make_double4(a[0], a[1], a[2], 0.0);
+      }
+      __syncthreads();
+      if (live)
+        for (int t = 0; t < cnt; ++t) {
+          const double4 s = tile[t];
+          top.insert(sqdist(p, d3{s.x, s.y, s.z}), base + t);
+        }
+    }
+    if (live) finish_query<K>(A, q, p, top);
+  }
+}
+
+template <int K>
+__global__ void __launch_bounds__(128) knn_bucket_kernel(WarpArgs A, const BucketParams* __restrict__ Pp,
+                                                         const int* __restrict__ cell_start,
+                                                         const double4* __restrict__ sorted) {
+  __shared__ BucketParams sP;
+  if (threadIdx.x == 0) sP = *Pp;
+  __syncthreads();
+  const BucketParams P = sP;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < A.n_pts; q += (int64_t)gridDim.x * blockDim.x) {
+    const d3 p = load_d3(A.pts + 3 * q);
+    TopK<K> top;
+    top.init(A.k);
+    bucket_knn<K>(P, cell_start, sorted, p, top);
+    finish_query<K>(A, q, p, top);
+  }
+}
+
+template <int K>
+int launch_knn(const cf_buckets* b, const WarpArgs& A, cudaStream_t st) {
+  const int block = 128;
+  if (b) {
+    knn_bucket_kernel<K><<<cf::grid_for(A.n_pts, block, 8), block, 0, st>>>(A, b->params, b->cell_start, b->sorted);
+  } else {
+    knn_brute_kernel<K><<<cf::grid_for(A.n_pts, block, 8), block, 0, st>>>(A);
+  }
+  return cf::check_launch("knn_warp");
+}
+
+}  // namespace
+
+namespace cf {
+
+int buckets_build(cf_buckets* b, const double* pts, int64_t n, int grid_res, cudaStream_t st) {
+  if (!b || n < 1 || n > b->max_points) return fail(CF_E_BAD_ARG, "buckets_build: bad handle or point count");
+  int G = grid_res;
+  if (G <= 0) G = (int)std::ceil(std::cbrt((double)n / 2.0) * 2.0);
+  G = std::max(1, std::min(G, b->max_grid_res));
+  b->grid_res = G;
+  const int64_t cells = (int64_t)G * G * G;
+  CF_CHECK_CUDA(cudaMemsetAsync(b->cell_start, 0, sizeof(int) * (cells + 1), st));
+  bucket_params_kernel<<<1, 1024, 0, st>>>(pts, (int)n, G, b->params);
+  bucket_count_kernel<<<grid_for(n, 256, 4), 256, 0, st>>>(pts, (int)n, b->params, b->cell_start, b->point_cell,
+                                                             b->point_slot);
+  bucket_scan_kernel<<<1, 1024, 0, st>>>(b->cell_start, b->params);
+  bucket_scatter_kernel<<<grid_for(n, 256, 4), 256, 0, st>>>(pts, (int)n, b->cell_start, b->point_cell,
+                                                               b->point_slot, b->sorted);
+  return check_launch("buckets_build");
+}
+
+}  // namespace cf
+
+extern "C" {
+
+int cf_deform_nodes(const double* nodes, const double* dqs, int64_t n, double* anchors, void* stream) {
+  if (n < 0 || (n > 0 && (!nodes || !dqs || !anchors))) return cf::fail(CF_E_BAD_ARG, "cf_deform_nodes: bad args");
+  if (n == 0) return CF_OK;
+  deform_nodes_kernel<<<cf::grid_for(n, 128, 4), 128, 0, cf::as_stream(stream)>>>(nodes, dqs, n, anchors);
+  return cf::check_launch("cf_deform_nodes");
+}
+
+int cf_buckets_create(int64_t max_points, int max_grid_res, cf_buckets_t** out) {
+  if (!out || max_points < 1 || max_grid_res < 1 || max_grid_res > 256)
+    return cf::fail(CF_E_BAD_ARG, "cf_buckets_create: bad args");
+  cf_buckets* b = new cf_buckets();
+  b->max_points = max_points;
+  b->max_grid_res = max_grid_res;
+  const int64_t cells = (int64_t)max_grid_res * max_grid_res * max_grid_res;
+  cudaError_t e = cudaMalloc(&b->params, sizeof(BucketParams));
+  if (e == cudaSuccess) e = cudaMalloc(&b->cell_start, sizeof(int) * (cells + 1));
+  if (e == cudaSuccess) e = cudaMalloc(&b->point_cell, sizeof(int) * max_points);
+  if (e == cudaSuccess) e = cudaMalloc(&b->point_slot, sizeof(int) * max_points);
+  if (e == cudaSuccess) e = cudaMalloc(&b->sorted, sizeof(double4) * max_points);
+  if (e != cudaSuccess) {
+    cf_buckets_destroy(b);
+    return cf::fail(CF_E_CUDA, std::string("cf_buckets_create: ") + cudaGetErrorString(e));
+  }
+  *out = b;
+  return CF_OK;
+}
+
+int cf_buckets_destroy(cf_buckets_t* b) {
+  if (!b) return CF_OK;
+  cudaFree(b->params);
+  cudaFree(b->cell_start);
+  cudaFree(b->point_cell);
+  cudaFree(b->point_slot);
+  cudaFree(b->sorted);
+  delete b;
+  return CF_OK;
+}
+
+int cf_buckets_build(cf_buckets_t* b, const double* pts, int64_t n, int grid_res, void* stream) {
+  return cf::buckets_build(b, pts, n, grid_res, cf::as_stream(stream));
+}
+
+int cf_knn_warp(const cf_buckets_t* buckets, const double* anchors, const double* dqs, int64_t n_nodes, int k,
+                double radius, int mode, const double* pts, int64_t n_pts, int64_t* idx_out, double* w_out,
+                double* pc_out, uint8_t* valid_out, void* stream) {
+  if (n_nodes < 1 || n_nodes > (1LL << 30)) return cf::fail(CF_E_BAD_ARG, "cf_knn_warp: graph needs at least one node");
+  if (mode < CF_WARP_BACKWARD || mode > CF_NEIGHBORS_ONLY) return cf::fail(CF_E_BAD_ARG, "cf_knn_warp: bad mode");
+  if (!(radius > 0.0)) return cf::fail(CF_E_BAD_ARG, "influence radius must be positive");
+  if (k < 1) return cf::fail(CF_E_BAD_ARG, "cf_knn_warp: k must be >= 1");
+  if (k > n_nodes) k = (int)n_nodes;  // edgraph.py:43, knnfield.py:27
+  if (k > 16) return cf::fail(CF_E_BAD_ARG, "cf_knn_warp: k > 16 unsupported");
+  if (mode != CF_NEIGHBORS_ONLY && !dqs) return cf::fail(CF_E_BAD_ARG, "cf_knn_warp: dqs required");
+  if (buckets && buckets->grid_res == 0) return cf::fail(CF_E_BAD_ARG, "cf_knn_warp: buckets not built");
+  if (n_pts == 0) return CF_OK;
+  WarpArgs A{anchors, dqs, (int)n_nodes, k, radius * radius, mode, pts, n_pts, idx_out, w_out, pc_out, valid_out};
+  cudaStream_t st = cf::as_stream(stream);
+  if (k <= 1) return launch_knn<1>(buckets, A, st);
+  if (k <= 2) return launch_knn<2>(buckets, A, st);
+  if (k <= 4) return launch_knn<4>(buckets, A, st);
+  if (k <= 8) return launch_knn<8>(buckets, A, st);
+  return launch_knn<16>(buckets, A, st);
+}
+
+}  // extern "C"
