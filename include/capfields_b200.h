@@ -148,6 +148,17 @@ int cf_hashgrid_encode_bwd(const cf_hashgrid_desc* desc, const float* pts, const
 int cf_hashgrid_indices(const cf_hashgrid_desc* desc, const float* pts, int64_t n_pts, uint32_t* idx_out,
                         float* w_out, void* stream);
 
+/* ------------------------------------------------------------------ tiny MLPs */
+
+/* Fused MLP chain on tcgen05 (fp16 operands, fp32 TMEM accumulation):
+ * y = L_n(relu(...relu(L_1(x)))). widths[0..n_layers]; layer l weight is the
+ * (N_l x K_l) fp16 matrix (K_l, N_l = widths padded to 16, <= 128) packed in the
+ * UMMA canonical K-major layout, concatenated into wblob;
+ * bias (n_layers x 128) fp32, row l used where has_bias[l] (host array).
+ * x (N, widths[0]) fp32, y (N, widths[n_layers]) fp32. */
+int cf_mlp_forward(int n_layers, const int* widths, const uint8_t* wblob, int w_bytes, const float* bias,
+                   const int* has_bias, const float* x, int64_t n_rows, float* y, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

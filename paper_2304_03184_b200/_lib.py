@@ -67,6 +67,7 @@ _SIGS = {
     "cf_hashgrid_encode": [ctypes.POINTER(HashGridDesc), _p, _p, _i64, _p, _p],
     "cf_hashgrid_encode_bwd": [ctypes.POINTER(HashGridDesc), _p, _p, _i64, _p, _p],
     "cf_hashgrid_indices": [ctypes.POINTER(HashGridDesc), _p, _i64, _p, _p, _p],
+    "cf_mlp_forward": [_i32, ctypes.POINTER(_i32), _p, _i32, _p, ctypes.POINTER(_i32), _p, _i64, _p, _p],
 }
 
 _lock = threading.Lock()
