@@ -159,6 +159,99 @@ int cf_hashgrid_indices(const cf_hashgrid_desc* desc, const float* pts, int64_t 
 int cf_mlp_forward(int n_layers, const int* widths, const uint8_t* wblob, int w_bytes, const float* bias,
                    const int* has_bias, const float* x, int64_t n_rows, float* y, void* stream);
 
+/* ------------------------------------------------------------------ render path */
+
+/* pinhole camera, CV axes (camera.py:94-108): R camera-to-world row-major */
+typedef struct cf_camera {
+  double R[9];
+  double fx, fy, cx, cy;
+  int width, height;
+} cf_camera;
+
+/* cubic occupancy bit grid: res^3 cells of edge `cell` from `min`, x-major
+ * flat index (i*res + j)*res + k, 32 cells per uint32 word */
+typedef struct cf_occ_grid {
+  double min[3];
+  double cell;
+  int res;
+} cf_occ_grid;
+
+/* uniform march of n_samples per ray over [t_near, t_far]: t_i = t_near + (i+0.5) dt */
+typedef struct cf_march_desc {
+  double origin[3];
+  int64_t n_rays;
+  int n_samples;
+  double t_near, t_far, dt;
+  cf_occ_grid human_grid;   /* live-space occupancy of the human field */
+  cf_occ_grid object_grid;  /* object-local occupancy of the rigid object */
+  double obj_R[9], obj_t[3]; /* object pose (object-to-world) */
+  double obj_min[3], obj_inv_side; /* object unit-cube normalisation */
+} cf_march_desc;
+
+/* compacted samples of one field: records (capacity) = ray << 8 | i, grouped
+ * per ray in ascending i; counters[0] = total emitted, counters[1] = overflow flag */
+typedef struct cf_march_out {
+  uint32_t* records;
+  int* ray_offset;
+  int* ray_count;
+  int* counters;
+  int64_t capacity;
+} cf_march_out;
+
+/* per-frame human warp state (hybrid deformation) */
+typedef struct cf_human_warp {
+  const double* dqs;        /* (n,8) node motion of the frame */
+  int k;                    /* ED neighbours */
+  double r2;                /* ED radius^2 */
+  const double* vert_Tinv;  /* (V,12) inverse blended bone transforms, NULL = no LBS fallback */
+  double lbs_max_d2;
+  double canon_min[3];      /* canonical unit-cube normalisation */
+  double inv_side;
+} cf_human_warp;
+
+int cf_camera_rays(const cf_camera* cam, double* dirs, void* stream);
+/* occupancy from geometry: cells whose centre is within radius of a bucketed point */
+int cf_occ_from_points(const cf_buckets_t* pts, const cf_occ_grid* g, double radius, uint32_t* bits, void* stream);
+/* occupancy of a solid origin-centred box dilated by shell: sdf(centre) <= shell */
+int cf_occ_box_shell(const cf_occ_grid* g, const double* half_extents, double shell, uint32_t* bits, void* stream);
+/* per-frame live occupancy: forward ED warp of every occupied canonical cell
+ * centre (node_buckets over the CANONICAL nodes), 3x3x3 live cells set */
+int cf_occ_splat(const uint32_t* canon_bits, const cf_occ_grid* cg, const cf_buckets_t* node_buckets,
+                 const double* dqs, int k, double radius, const cf_occ_grid* lg, uint32_t* live_bits, void* stream);
+/* occupancy-skipped compaction of the samples of every ray (one or two fields) */
+int cf_march(const cf_march_desc* M, const double* dirs, const uint32_t* human_bits, const uint32_t* object_bits,
+             const cf_march_out* human, const cf_march_out* object, void* stream);
+/* human samples -> canonical unit cube (xu: float4 x,y,z,flag; flag 1 = ED, 2 = LBS, 0 = invalid) */
+int cf_human_canon(const cf_march_desc* M, const double* dirs, const cf_march_out* F, const cf_human_warp* W,
+                   const cf_buckets_t* anchor_buckets, const cf_buckets_t* vert_buckets, float* xu, void* stream);
+int cf_object_canon(const cf_march_desc* M, const double* dirs, const cf_march_out* F, float* xu, void* stream);
+/* front-to-back compositing of field outputs (float4 sigma,r,g,b per sample) */
+int cf_composite(const cf_march_desc* M, const cf_march_out* F, const float* field, float t_term, float* rgb,
+                 float* depth, float* opacity, void* stream);
+/* per pixel: nearer layer among those with opacity > 0.5, else background; layer 0 bg, 1 human, 2 object */
+int cf_composite_layers(int64_t n, const float* h_rgb, const float* h_depth, const float* h_opac, const float* o_rgb,
+                        const float* o_depth, const float* o_opac, const float* bg, float* out, uint8_t* layer,
+                        void* stream);
+
+/* fused radiance field of one field: hash grids + MLPs on tcgen05.
+ * wblob = fp16 canonical-layout weights, in order
+ *   [has_deform: D1 128x32, D2..D4 128x128, D5 16x128] G1 64x32, G2 16x64, C1 64x32, C2 64x64, C3 16x64 */
+typedef struct cf_field_desc {
+  int has_deform;
+  cf_hashgrid_desc dgrid;   /* deformation grid (L*F = 32, F = 4) */
+  const float* dtable;
+  cf_hashgrid_desc cgrid;   /* canonical grid (L*F = 32, F = 2) */
+  const float* ctable;
+  const uint8_t* wblob;
+  int w_bytes;
+  const float* dbias;       /* DeformNet layer-1 bias (128), pose theta folded in */
+  float delta_scale;        /* |dv| bound, metres (0.05) */
+  float inv_side;           /* metres -> unit cube */
+} cf_field_desc;
+/* out: float4 (sigma, r, g, b) per compacted sample of S (count read on device) */
+int cf_field_forward(const cf_field_desc* F, const cf_march_out* S, const double* dirs, const float* xu, float* out,
+                     void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -49,6 +49,45 @@ class HashGridDesc(ctypes.Structure):
     ]
 
 
+class Camera(ctypes.Structure):
+    _fields_ = [("R", ctypes.c_double * 9), ("fx", ctypes.c_double), ("fy", ctypes.c_double),
+                ("cx", ctypes.c_double), ("cy", ctypes.c_double), ("width", ctypes.c_int), ("height", ctypes.c_int)]
+
+
+class OccGrid(ctypes.Structure):
+    _fields_ = [("min", ctypes.c_double * 3), ("cell", ctypes.c_double), ("res", ctypes.c_int)]
+
+
+class MarchDesc(ctypes.Structure):
+    _fields_ = [("origin", ctypes.c_double * 3), ("n_rays", ctypes.c_int64), ("n_samples", ctypes.c_int),
+                ("t_near", ctypes.c_double), ("t_far", ctypes.c_double), ("dt", ctypes.c_double),
+                ("human_grid", OccGrid), ("object_grid", OccGrid), ("obj_R", ctypes.c_double * 9),
+                ("obj_t", ctypes.c_double * 3), ("obj_min", ctypes.c_double * 3), ("obj_inv_side", ctypes.c_double)]
+
+
+class MarchOut(ctypes.Structure):
+    _fields_ = [("records", ctypes.c_void_p), ("ray_offset", ctypes.c_void_p), ("ray_count", ctypes.c_void_p),
+                ("counters", ctypes.c_void_p), ("capacity", ctypes.c_int64)]
+
+
+class HumanWarp(ctypes.Structure):
+    _fields_ = [("dqs", ctypes.c_void_p), ("k", ctypes.c_int), ("r2", ctypes.c_double),
+                ("vert_Tinv", ctypes.c_void_p), ("lbs_max_d2", ctypes.c_double),
+                ("canon_min", ctypes.c_double * 3), ("inv_side", ctypes.c_double)]
+
+
+class FieldDesc(ctypes.Structure):
+    _fields_ = [("has_deform", ctypes.c_int), ("dgrid", HashGridDesc), ("dtable", ctypes.c_void_p),
+                ("cgrid", HashGridDesc), ("ctable", ctypes.c_void_p), ("wblob", ctypes.c_void_p),
+                ("w_bytes", ctypes.c_int), ("dbias", ctypes.c_void_p), ("delta_scale", ctypes.c_float),
+                ("inv_side", ctypes.c_float)]
+
+
+def byref(x):
+    return ctypes.byref(x)
+
+
+_P = ctypes.POINTER
 # name -> argtypes (all return int status)
 _SIGS = {
     "cf_device_sm_count": [],
@@ -68,6 +107,16 @@ _SIGS = {
     "cf_hashgrid_encode_bwd": [ctypes.POINTER(HashGridDesc), _p, _p, _i64, _p, _p],
     "cf_hashgrid_indices": [ctypes.POINTER(HashGridDesc), _p, _i64, _p, _p, _p],
     "cf_mlp_forward": [_i32, ctypes.POINTER(_i32), _p, _i32, _p, ctypes.POINTER(_i32), _p, _i64, _p, _p],
+    "cf_camera_rays": [_P(Camera), _p, _p],
+    "cf_occ_from_points": [_p, _P(OccGrid), _f64, _p, _p],
+    "cf_occ_box_shell": [_P(OccGrid), _p, _f64, _p, _p],
+    "cf_occ_splat": [_p, _P(OccGrid), _p, _p, _i32, _f64, _P(OccGrid), _p, _p],
+    "cf_march": [_P(MarchDesc), _p, _p, _p, _P(MarchOut), _P(MarchOut), _p],
+    "cf_human_canon": [_P(MarchDesc), _p, _P(MarchOut), _P(HumanWarp), _p, _p, _p, _p],
+    "cf_object_canon": [_P(MarchDesc), _p, _P(MarchOut), _p, _p],
+    "cf_composite": [_P(MarchDesc), _P(MarchOut), _p, ctypes.c_float, _p, _p, _p, _p],
+    "cf_composite_layers": [_i64, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p],
+    "cf_field_forward": [_P(FieldDesc), _P(MarchOut), _p, _p, _p, _p],
 }
 
 _lock = threading.Lock()

@@ -1,0 +1,442 @@
+// Ray generation, occupancy grids, occupancy-skipped ray marching, sample
+// canonicalisation and front-to-back compositing — the SPEC render path
+// (volume_render SPEC.md:381-389, render_view SPEC.md:399-407,
+// composite SPEC.md:555-563) with the occupancy skipping of DESIGN.md §6.
+//
+// Layouts in HBM: rays = one float64 origin + (R,3) float64 unit directions;
+// occupancy = bit grid (res^3 bits, x-major flat index, 32 cells per word);
+// compacted samples = uint32 record (ray << 8 | sample) grouped per ray in
+// ascending sample order, with per-ray (offset, count); canonicalised samples
+// = float4 (x, y, z in the field's unit cube, flag).
+#include "edwarp.cuh"
+#include "render_common.cuh"
+
+namespace {
+
+__device__ __forceinline__ bool occ_test(const cf_occ_grid& g, const uint32_t* __restrict__ bits, d3 p) {
+  const double q[3] = {p.x, p.y, p.z};
+  int64_t c[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double f = floor(x_div(x_sub(q[a], g.min[a]), g.cell));
+    if (!(f >= 0.0) || f >= (double)g.res) return false;
+    c[a] = (int64_t)f;
+  }
+  const int64_t flat = (c[0] * g.res + c[1]) * g.res + c[2];
+  return (__ldg(bits + (flat >> 5)) >> (flat & 31)) & 1u;
+}
+
+__device__ __forceinline__ d3 cell_center(const cf_occ_grid& g, int64_t flat) {
+  const int64_t r = g.res;
+  const int64_t x = flat / (r * r), y = (flat / r) % r, z = flat % r;
+  return d3{x_add(g.min[0], x_mul((double)x + 0.5, g.cell)), x_add(g.min[1], x_mul((double)y + 0.5, g.cell)),
+            x_add(g.min[2], x_mul((double)z + 0.5, g.cell))};
+}
+
+// t_i = t_near + (i + 0.5) * dt ;  p = o + t * d   (float64, un-contracted)
+__device__ __forceinline__ double sample_t(const cf_march_desc& M, int i) {
+  return x_add(M.t_near, x_mul((double)i + 0.5, M.dt));
+}
+__device__ __forceinline__ d3 sample_p(d3 o, d3 d, double t) {
+  return d3{x_add(o.x, x_mul(t, d.x)), x_add(o.y, x_mul(t, d.y)), x_add(o.z, x_mul(t, d.z))};
+}
+// object-local point R^T (p - t), summed ((R0i q0 + R1i q1) + R2i q2)
+__device__ __forceinline__ d3 to_object(const double* R, const double* t, d3 p) {
+  const double q0 = x_sub(p.x, t[0]), q1 = x_sub(p.y, t[1]), q2 = x_sub(p.z, t[2]);
+  double o[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) o[i] = x_add(x_add(x_mul(q0, R[i]), x_mul(q1, R[3 + i])), x_mul(q2, R[6 + i]));
+  return d3{o[0], o[1], o[2]};
+}
+
+__global__ void rays_kernel(cf_camera cam, double* __restrict__ dirs) {
+  const int64_t n = (int64_t)cam.width * cam.height;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double u = (double)(i % cam.width), v = (double)(i / cam.width);
+    const double dc[3] = {x_div(x_sub(u, cam.cx), cam.fx), x_div(x_sub(v, cam.cy), cam.fy), 1.0};
+    double d[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      d[a] = __fma_rn(dc[2], cam.R[3 * a + 2], __fma_rn(dc[1], cam.R[3 * a + 1], x_mul(dc[0], cam.R[3 * a])));
+    const double nrm = sqrt(x_add(x_add(x_mul(d[0], d[0]), x_mul(d[1], d[1])), x_mul(d[2], d[2])));
+    dirs[3 * i] = x_div(d[0], nrm);
+    dirs[3 * i + 1] = x_div(d[1], nrm);
+    dirs[3 * i + 2] = x_div(d[2], nrm);
+  }
+}
+
+// cells whose centre lies within `radius` of any bucketed point
+__global__ void __launch_bounds__(128) occ_points_kernel(cf_occ_grid g, const BucketParams* __restrict__ Pp,
+                                                         const int* __restrict__ cell_start,
+                                                         const double4* __restrict__ sorted, double r2,
+                                                         uint32_t* __restrict__ bits) {
+  __shared__ BucketParams sP;
+  if (threadIdx.x == 0) sP = *Pp;
+  __syncthreads();
+  const int64_t total = (int64_t)g.res * g.res * g.res;
+  const int64_t words = (total + 31) / 32;
+  for (int64_t base = (blockIdx.x * (int64_t)blockDim.x) & ~31LL; base < words * 32;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t cell = base + (threadIdx.x & 31) + (threadIdx.x & ~31);
+    bool on = false;
+    if (cell < total) {
+      TopK<1> top;
+      top.init(1);
+      bucket_knn<1>(sP, cell_start, sorted, cell_center(g, cell), top);
+      on = top.d[0] <= r2;
+    }
+    const uint32_t word = __ballot_sync(0xffffffffu, on);
+    if ((threadIdx.x & 31) == 0 && (cell >> 5) < words) bits[cell >> 5] = word;
+  }
+}
+
+// solid origin-centred box dilated by shell: sdf(centre) <= shell
+__global__ void occ_box_kernel(cf_occ_grid g, double hx, double hy, double hz, double shell, uint32_t* bits) {
+  const int64_t total = (int64_t)g.res * g.res * g.res;
+  const int64_t words = (total + 31) / 32;
+  for (int64_t base = (blockIdx.x * (int64_t)blockDim.x) & ~31LL; base < words * 32;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t cell = base + (threadIdx.x & 31) + (threadIdx.x & ~31);
+    bool on = false;
+    if (cell < total) {
+      const d3 c = cell_center(g, cell);
+      const double q[3] = {x_sub(fabs(c.x), hx), x_sub(fabs(c.y), hy), x_sub(fabs(c.z), hz)};
+      const double m0 = fmax(q[0], 0.0), m1 = fmax(q[1], 0.0), m2 = fmax(q[2], 0.0);
+      const double o = sqrt(x_add(x_add(x_mul(m0, m0), x_mul(m1, m1)), x_mul(m2, m2)));
+      const double in = fmin(fmax(q[0], fmax(q[1], q[2])), 0.0);
+      on = x_add(o, in) <= shell;
+    }
+    const uint32_t word = __ballot_sync(0xffffffffu, on);
+    if ((threadIdx.x & 31) == 0 && (cell >> 5) < words) bits[cell >> 5] = word;
+  }
+}
+
+// forward-warp every occupied canonical cell centre into live space and set
+// the 3x3x3 block of live cells around it
+template <int K>
+__global__ void __launch_bounds__(128) occ_splat_kernel(const uint32_t* __restrict__ cbits, cf_occ_grid cg,
+                                                        const BucketParams* __restrict__ Pp,
+                                                        const int* __restrict__ cell_start,
+                                                        const double4* __restrict__ sorted,
+                                                        const double* __restrict__ dqs, int k, double r2,
+                                                        cf_occ_grid lg, uint32_t* __restrict__ lbits) {
+  __shared__ BucketParams sP;
+  if (threadIdx.x == 0) sP = *Pp;
+  __syncthreads();
+  const int64_t total = (int64_t)cg.res * cg.res * cg.res;
+  for (int64_t cell = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; cell < total;
+       cell += (int64_t)gridDim.x * blockDim.x) {
+    if (!((cbits[cell >> 5] >> (cell & 31)) & 1u)) continue;
+    d3 x;
+    if (!ed_warp_point<K>(sP, cell_start, sorted, dqs, k, r2, false, cell_center(cg, cell), x)) continue;
+    const double q[3] = {x.x, x.y, x.z};
+    int64_t c[3];
+    bool ok = true;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double f = floor(x_div(x_sub(q[a], lg.min[a]), lg.cell));
+      ok &= (f >= -1.0) && (f <= (double)lg.res);
+      c[a] = ok ? (int64_t)f : 0;
+    }
+    if (!ok) continue;
+    for (int dx = -1; dx <= 1; ++dx)
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dz = -1; dz <= 1; ++dz) {
+          const int64_t a = c[0] + dx, b = c[1] + dy, z = c[2] + dz;
+          if (a < 0 || b < 0 || z < 0 || a >= lg.res || b >= lg.res || z >= lg.res) continue;
+          const int64_t f = (a * lg.res + b) * lg.res + z;
+          atomicOr(lbits + (f >> 5), 1u << (f & 31));
+        }
+  }
+}
+
+__device__ __forceinline__ int warp_excl_scan(int v, int& total) {
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if ((threadIdx.x & 31) >= o) x += y;
+  }
+  total = __shfl_sync(0xffffffffu, x, 31);
+  return x - v;
+}
+
+// occupancy-skipped sample compaction, one thread per ray, up to two fields
+__global__ void __launch_bounds__(128) march_kernel(cf_march_desc M, const double* __restrict__ dirs,
+                                                    const uint32_t* __restrict__ hbits,
+                                                    const uint32_t* __restrict__ obits, cf_march_out H,
+                                                    cf_march_out O) {
+  const d3 o{M.origin[0], M.origin[1], M.origin[2]};
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < M.n_rays; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t ray = base + threadIdx.x;
+    const bool live = ray < M.n_rays;
+    const d3 d = live ? load_d3(dirs + 3 * ray) : d3{0.0, 0.0, 1.0};
+    uint32_t hm[4] = {0, 0, 0, 0}, om[4] = {0, 0, 0, 0};  // occupancy masks of up to 128 samples
+    int hc = 0, oc = 0;
+    if (live)
+      for (int i = 0; i < M.n_samples; ++i) {
+        const d3 p = sample_p(o, d, sample_t(M, i));
+        if (hbits && occ_test(M.human_grid, hbits, p)) {
+          hm[i >> 5] |= 1u << (i & 31);
+          ++hc;
+        }
+        if (obits && occ_test(M.object_grid, obits, to_object(M.obj_R, M.obj_t, p))) {
+          om[i >> 5] |= 1u << (i & 31);
+          ++oc;
+        }
+      }
+    for (int f = 0; f < 2; ++f) {
+      const cf_march_out& out = f == 0 ? H : O;
+      if (!out.records) continue;
+      const int c = f == 0 ? hc : oc;
+      const uint32_t* m = f == 0 ? hm : om;
+      int wtot;
+      const int excl = warp_excl_scan(c, wtot);
+      int wbase = 0;
+      if ((threadIdx.x & 31) == 0 && wtot > 0) wbase = atomicAdd(out.counters, wtot);
+      wbase = __shfl_sync(0xffffffffu, wbase, 0);
+      if (!live) continue;
+      int64_t pos = (int64_t)wbase + excl;
+      const bool fits = pos + c <= out.capacity;
+      out.ray_offset[ray] = (int)pos;
+      out.ray_count[ray] = fits ? c : 0;
+      if (!fits) {
+        if (c > 0) atomicExch(out.counters + 1, 1);
+        continue;
+      }
+      for (int w = 0; w < 4; ++w) {
+        uint32_t bitsw = m[w];
+        while (bitsw) {
+          const int b = __ffs(bitsw) - 1;
+          bitsw &= bitsw - 1;
+          out.records[pos++] = ((uint32_t)ray << 8) | (uint32_t)(w * 32 + b);
+        }
+      }
+    }
+  }
+}
+
+// human samples: live point -> ED backward warp (exact bucketed k-NN + DQB^-1),
+// falling back to backward LBS outside the ED support; -> canonical unit cube
+template <int K>
+__global__ void __launch_bounds__(128) human_canon_kernel(cf_march_desc M, const double* __restrict__ dirs,
+                                                          const uint32_t* __restrict__ records,
+                                                          const int* __restrict__ count, int64_t capacity,
+                                                          cf_human_warp W, const BucketParams* __restrict__ EPp,
+                                                          const int* __restrict__ ecs, const double4* __restrict__ es,
+                                                          const BucketParams* __restrict__ LPp,
+                                                          const int* __restrict__ lcs, const double4* __restrict__ ls,
+                                                          float4* __restrict__ xu) {
+  __shared__ BucketParams sE, sL;
+  if (threadIdx.x == 0) {
+    sE = *EPp;
+    if (LPp) sL = *LPp;
+  }
+  __syncthreads();
+  const int64_t n = min((int64_t)*count, capacity);
+  const d3 o{M.origin[0], M.origin[1], M.origin[2]};
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t rec = records[s];
+    const int64_t ray = rec >> 8;
+    const d3 p = sample_p(o, load_d3(dirs + 3 * ray), sample_t(M, (int)(rec & 255u)));
+    d3 pt;
+    float flag = 0.0f;
+    if (ed_warp_point<K>(sE, ecs, es, W.dqs, W.k, W.r2, true, p, pt)) {
+      flag = 1.0f;
+    } else if (LPp) {
+      TopK<1> top;
+      top.init(1);
+      bucket_knn<1>(sL, lcs, ls, p, top);
+      if (top.d[0] <= W.lbs_max_d2) {
+        const double* T = W.vert_Tinv + 12 * (int64_t)top.i[0];
+        pt = d3{T[0] * p.x + T[1] * p.y + T[2] * p.z + T[3], T[4] * p.x + T[5] * p.y + T[6] * p.z + T[7],
+                T[8] * p.x + T[9] * p.y + T[10] * p.z + T[11]};
+        flag = 2.0f;
+      }
+    }
+    float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (flag > 0.0f)
+      r = make_float4(__double2float_rn(x_mul(x_sub(pt.x, W.canon_min[0]), W.inv_side)),
+                      __double2float_rn(x_mul(x_sub(pt.y, W.canon_min[1]), W.inv_side)),
+                      __double2float_rn(x_mul(x_sub(pt.z, W.canon_min[2]), W.inv_side)), flag);
+    xu[s] = r;
+  }
+}
+
+// rigid object samples: live point -> object-local frame -> unit cube
+__global__ void object_canon_kernel(cf_march_desc M, const double* __restrict__ dirs,
+                                    const uint32_t* __restrict__ records, const int* __restrict__ count,
+                                    int64_t capacity, const double* obj_min, double inv_side,
+                                    float4* __restrict__ xu) {
+  const int64_t n = min((int64_t)*count, capacity);
+  const d3 o{M.origin[0], M.origin[1], M.origin[2]};
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t rec = records[s];
+    const int64_t ray = rec >> 8;
+    const d3 p = to_object(M.obj_R, M.obj_t, sample_p(o, load_d3(dirs + 3 * ray), sample_t(M, (int)(rec & 255u))));
+    xu[s] = make_float4(__double2float_rn(x_mul(x_sub(p.x, M.obj_min[0]), M.obj_inv_side)),
+                        __double2float_rn(x_mul(x_sub(p.y, M.obj_min[1]), M.obj_inv_side)),
+                        __double2float_rn(x_mul(x_sub(p.z, M.obj_min[2]), M.obj_inv_side)), 1.0f);
+  }
+}
+
+// front-to-back alpha compositing: alpha_i = 1 - exp(-sigma_i * dt),
+// T_i = prod_{j<i} (1 - alpha_j); stops once T < t_term
+__global__ void composite_kernel(cf_march_desc M, cf_march_out F, const float4* __restrict__ field, float t_term,
+                                 float* __restrict__ rgb, float* __restrict__ depth, float* __restrict__ opacity) {
+  const float dt = (float)M.dt;
+  for (int64_t ray = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ray < M.n_rays;
+       ray += (int64_t)gridDim.x * blockDim.x) {
+    const int off = F.ray_offset[ray], cnt = F.ray_count[ray];
+    float T = 1.0f, r = 0.f, g = 0.f, b = 0.f, dep = 0.f, op = 0.f;
+    for (int j = 0; j < cnt; ++j) {
+      const float4 f = field[off + j];
+      const int i = (int)(F.records[off + j] & 255u);
+      const float alpha = 1.0f - expf(-f.x * dt);
+      const float w = T * alpha;
+      r += w * f.y;
+      g += w * f.z;
+      b += w * f.w;
+      dep += w * (float)sample_t(M, i);
+      op += w;
+      T *= 1.0f - alpha;
+      if (T < t_term) break;
+    }
+    rgb[3 * ray] = r;
+    rgb[3 * ray + 1] = g;
+    rgb[3 * ray + 2] = b;
+    depth[ray] = dep / fmaxf(op, 1e-6f);
+    opacity[ray] = op;
+  }
+}
+
+// depth-occlusion composite: nearer layer with opacity > 0.5
+__global__ void layers_kernel(int64_t n, const float* __restrict__ hr, const float* __restrict__ hd,
+                              const float* __restrict__ ho, const float* __restrict__ orgb,
+                              const float* __restrict__ od, const float* __restrict__ oo, float bg0, float bg1,
+                              float bg2, float* __restrict__ out, uint8_t* __restrict__ layer) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const bool h = hr && ho[i] > 0.5f, o = orgb && oo[i] > 0.5f;
+    int L = 0;
+    if (h && o) L = hd[i] <= od[i] ? 1 : 2;
+    else if (h) L = 1;
+    else if (o) L = 2;
+    const float* src = L == 1 ? hr + 3 * i : (L == 2 ? orgb + 3 * i : nullptr);
+    out[3 * i] = src ? src[0] : bg0;
+    out[3 * i + 1] = src ? src[1] : bg1;
+    out[3 * i + 2] = src ? src[2] : bg2;
+    if (layer) layer[i] = (uint8_t)L;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int cf_camera_rays(const cf_camera* cam, double* dirs, void* stream) {
+  if (!cam || cam->width < 1 || cam->height < 1 || !dirs) return cf::fail(CF_E_BAD_ARG, "cf_camera_rays: bad args");
+  const int64_t n = (int64_t)cam->width * cam->height;
+  rays_kernel<<<cf::grid_for(n, 256, 4), 256, 0, cf::as_stream(stream)>>>(*cam, dirs);
+  return cf::check_launch("cf_camera_rays");
+}
+
+int cf_occ_from_points(const cf_buckets_t* pts, const cf_occ_grid* g, double radius, uint32_t* bits, void* stream) {
+  if (!pts || !g || g->res < 1 || pts->grid_res == 0) return cf::fail(CF_E_BAD_ARG, "cf_occ_from_points: bad args");
+  const int64_t total = (int64_t)g->res * g->res * g->res;
+  occ_points_kernel<<<cf::grid_for(total, 128, 8), 128, 0, cf::as_stream(stream)>>>(*g, pts->params, pts->cell_start,
+                                                                                   pts->sorted, radius * radius, bits);
+  return cf::check_launch("cf_occ_from_points");
+}
+
+int cf_occ_box_shell(const cf_occ_grid* g, const double* half_extents, double shell, uint32_t* bits, void* stream) {
+  if (!g || g->res < 1 || !half_extents) return cf::fail(CF_E_BAD_ARG, "cf_occ_box_shell: bad args");
+  const int64_t total = (int64_t)g->res * g->res * g->res;
+  occ_box_kernel<<<cf::grid_for(total, 256, 4), 256, 0, cf::as_stream(stream)>>>(
+      *g, half_extents[0], half_extents[1], half_extents[2], shell, bits);
+  return cf::check_launch("cf_occ_box_shell");
+}
+
+int cf_occ_splat(const uint32_t* canon_bits, const cf_occ_grid* cg, const cf_buckets_t* node_buckets,
+                 const double* dqs, int k, double radius, const cf_occ_grid* lg, uint32_t* live_bits, void* stream) {
+  if (!canon_bits || !cg || !lg || !node_buckets || node_buckets->grid_res == 0 || k < 1 || k > 8)
+    return cf::fail(CF_E_BAD_ARG, "cf_occ_splat: bad args");
+  cudaStream_t st = cf::as_stream(stream);
+  const int64_t lwords = ((int64_t)lg->res * lg->res * lg->res + 31) / 32;
+  CF_CHECK_CUDA(cudaMemsetAsync(live_bits, 0, sizeof(uint32_t) * lwords, st));
+  const int64_t total = (int64_t)cg->res * cg->res * cg->res;
+  const unsigned grid = cf::grid_for(total, 128, 8);
+  const double r2 = radius * radius;
+  if (k <= 4)
+    occ_splat_kernel<4><<<grid, 128, 0, st>>>(canon_bits, *cg, node_buckets->params, node_buckets->cell_start,
+                                              node_buckets->sorted, dqs, k, r2, *lg, live_bits);
+  else
+    occ_splat_kernel<8><<<grid, 128, 0, st>>>(canon_bits, *cg, node_buckets->params, node_buckets->cell_start,
+                                              node_buckets->sorted, dqs, k, r2, *lg, live_bits);
+  return cf::check_launch("cf_occ_splat");
+}
+
+int cf_march(const cf_march_desc* M, const double* dirs, const uint32_t* human_bits, const uint32_t* object_bits,
+             const cf_march_out* human, const cf_march_out* object, void* stream) {
+  if (!M || !dirs || M->n_samples < 1 || M->n_samples > 128 || M->n_rays < 0 || M->n_rays >= (1LL << 24))
+    return cf::fail(CF_E_BAD_ARG, "cf_march: bad args (<= 128 samples, < 2^24 rays)");
+  cf_march_out H{}, O{};
+  if (human && human_bits) H = *human;
+  if (object && object_bits) O = *object;
+  cudaStream_t st = cf::as_stream(stream);
+  if (H.records) CF_CHECK_CUDA(cudaMemsetAsync(H.counters, 0, 2 * sizeof(int), st));
+  if (O.records) CF_CHECK_CUDA(cudaMemsetAsync(O.counters, 0, 2 * sizeof(int), st));
+  if (M->n_rays == 0) return CF_OK;
+  march_kernel<<<cf::grid_for(M->n_rays, 128, 8), 128, 0, st>>>(*M, dirs, H.records ? human_bits : nullptr,
+                                                                  O.records ? object_bits : nullptr, H, O);
+  return cf::check_launch("cf_march");
+}
+
+int cf_human_canon(const cf_march_desc* M, const double* dirs, const cf_march_out* F, const cf_human_warp* W,
+                   const cf_buckets_t* anchor_buckets, const cf_buckets_t* vert_buckets, float* xu_f, void* stream) {
+  float4* xu = reinterpret_cast<float4*>(xu_f);
+  if (!M || !F || !W || !anchor_buckets || anchor_buckets->grid_res == 0 || W->k < 1 || W->k > 8)
+    return cf::fail(CF_E_BAD_ARG, "cf_human_canon: bad args");
+  const bool lbs = vert_buckets && W->vert_Tinv;
+  cudaStream_t st = cf::as_stream(stream);
+  const unsigned grid = cf::grid_for(F->capacity, 128, 8);
+#define CF_HC(KK)                                                                                                \
+  human_canon_kernel<KK><<<grid, 128, 0, st>>>(*M, dirs, F->records, F->counters, F->capacity, *W,               \
+                                               anchor_buckets->params, anchor_buckets->cell_start,              \
+                                               anchor_buckets->sorted, lbs ? vert_buckets->params : nullptr,    \
+                                               lbs ? vert_buckets->cell_start : nullptr,                        \
+                                               lbs ? vert_buckets->sorted : nullptr, xu)
+  if (W->k <= 4) CF_HC(4);
+  else CF_HC(8);
+#undef CF_HC
+  return cf::check_launch("cf_human_canon");
+}
+
+int cf_object_canon(const cf_march_desc* M, const double* dirs, const cf_march_out* F, float* xu_f, void* stream) {
+  float4* xu = reinterpret_cast<float4*>(xu_f);
+  if (!M || !F) return cf::fail(CF_E_BAD_ARG, "cf_object_canon: bad args");
+  object_canon_kernel<<<cf::grid_for(F->capacity, 256, 4), 256, 0, cf::as_stream(stream)>>>(
+      *M, dirs, F->records, F->counters, F->capacity, M->obj_min, M->obj_inv_side, xu);
+  return cf::check_launch("cf_object_canon");
+}
+
+int cf_composite(const cf_march_desc* M, const cf_march_out* F, const float* field_f, float t_term, float* rgb,
+                 float* depth, float* opacity, void* stream) {
+  if (!M || !F || !rgb || !depth || !opacity) return cf::fail(CF_E_BAD_ARG, "cf_composite: bad args");
+  const float4* field = reinterpret_cast<const float4*>(field_f);
+  if (M->n_rays == 0) return CF_OK;
+  composite_kernel<<<cf::grid_for(M->n_rays, 128, 8), 128, 0, cf::as_stream(stream)>>>(*M, *F, field, t_term, rgb,
+                                                                                        depth, opacity);
+  return cf::check_launch("cf_composite");
+}
+
+int cf_composite_layers(int64_t n, const float* h_rgb, const float* h_depth, const float* h_opac, const float* o_rgb,
+                        const float* o_depth, const float* o_opac, const float* bg, float* out, uint8_t* layer,
+                        void* stream) {
+  if (n < 0 || !bg || !out) return cf::fail(CF_E_BAD_ARG, "cf_composite_layers: bad args");
+  if (n == 0) return CF_OK;
+  layers_kernel<<<cf::grid_for(n, 256, 4), 256, 0, cf::as_stream(stream)>>>(n, h_rgb, h_depth, h_opac, o_rgb, o_depth,
+                                                                             o_opac, bg[0], bg[1], bg[2], out, layer);
+  return cf::check_launch("cf_composite_layers");
+}
+
+}  // extern "C"

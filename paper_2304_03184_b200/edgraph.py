@@ -65,7 +65,7 @@ class FrameMotion:
     anchors and their coarse buckets. Built once per frame and reused by every
     warp call of that frame (the render path's per-frame setup)."""
 
-    def __init__(self, graph, motion, buckets: bool = True):
+    def __init__(self, graph, motion, buckets=True):
         nodes = graph.nodes
         self.n = int(len(nodes))
         self.k = int(min(getattr(graph, "knn_k", 4), self.n))
@@ -79,8 +79,8 @@ class FrameMotion:
                   _lib.stream_ptr())
         self.canon_buckets = None
         self.live_buckets = None
-        if buckets:
-            self.live_buckets = Buckets(self.n)
+        if buckets is not False and buckets is not None:
+            self.live_buckets = buckets if isinstance(buckets, Buckets) else Buckets(self.n)
             self.live_buckets.build(self.anchors)
 
     def canonical_buckets(self) -> "Buckets":

@@ -1,0 +1,306 @@
+"""Novel-view rendering of the human + rigid-object scene on the GPU — the SPEC
+render path (canonicalize_human SPEC.md:372-380, volume_render :381-389,
+render_view :399-407, composite :555-563) with occupancy skipping.
+
+Per frame (host orchestrates, every step a CUDA kernel, stream-ordered, no host
+sync):  deformed nodes + live buckets -> backward-LBS vertex transforms ->
+live occupancy splat ; per view: rays -> march (occupancy-skipped compaction) ->
+canonicalise (ED DQB^-1 / LBS fallback | rigid) -> fused field (hash + tcgen05
+MLPs) -> front-to-back composite -> depth-occlusion layer composite.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._tensors import dev
+from .edgraph import Buckets, FrameMotion, EDGraph, GraphMotion
+from .nrf import HashGrid, HashGridConfig, pack_weight
+from .skeleton import BackwardLBS
+
+CANON_GRID = HashGridConfig(16, 2, 19, 16, 2048)   # config.py:56-60
+DEFORM_GRID = HashGridConfig(8, 4, 17, 16, 256)    # SPEC.md:419 (L=8, F=4); T, N_max frozen in DESIGN.md §4
+
+
+@dataclass
+class RenderConfig:
+    n_samples: int = 128          # C2: 128 samples / ray
+    t_near: float = 0.3           # config.py:53-54
+    t_far: float = 5.0
+    t_term: float = 1e-4          # early ray termination
+    ed_k: int = 4
+    ed_radius: float = 0.1
+    lbs_max_dist: float = 0.2
+    world_min: tuple = (-1.3, -0.3, -1.3)   # live-space occupancy volume (cube)
+    world_size: float = 2.6
+    live_occ_res: int = 128
+    canon_occ_res: int = 128
+    canon_occ_radius: float = 0.03   # geometry-initialised density bits
+    obj_occ_res: int = 64
+    obj_shell: float = 0.02
+    background: tuple = (24 / 255.0, 28 / 255.0, 34 / 255.0)   # config.py bg_r/g/b
+
+
+def _kaiming(rng, n_out, n_in):
+    b = np.sqrt(6.0 / n_in)
+    return rng.uniform(-b, b, size=(n_out, n_in))
+
+
+def occ_grid(gmin, size, res) -> _lib.OccGrid:
+    g = _lib.OccGrid()
+    for a in range(3):
+        g.min[a] = float(gmin[a])
+    g.cell = float(size) / res
+    g.res = int(res)
+    return g
+
+
+class FieldNets:
+    """Weights of one field: [DeformNet], E_g, E_c (fp16-representable fp32 copies kept on host)."""
+
+    def __init__(self, rng, deform: bool, zero_deform_out: bool = True, theta_dim: int = 72):
+        self.deform = deform
+        L = {}
+        if deform:
+            L["D1"] = _kaiming(rng, 128, 32 + theta_dim)   # hash_d(32) (+) theta(72)
+            for i in (2, 3, 4):
+                L[f"D{i}"] = _kaiming(rng, 128, 128)
+            L["D5"] = np.zeros((3, 128)) if zero_deform_out else _kaiming(rng, 3, 128) * 0.1
+        L["G1"] = _kaiming(rng, 64, 32)
+        L["G2"] = _kaiming(rng, 16, 64)
+        L["C1"] = _kaiming(rng, 64, 31)
+        L["C2"] = _kaiming(rng, 64, 64)
+        L["C3"] = _kaiming(rng, 3, 64)
+        self.layers = {k: np.asarray(v, dtype=np.float32) for k, v in L.items()}
+        self.repack()
+
+    def repack(self) -> None:
+        """Round the host weights to fp16 and upload them in the tcgen05 operand layout."""
+        self.layers = {k: v.astype(np.float16).astype(np.float32) for k, v in self.layers.items()}
+        order = (["D1h", "D2", "D3", "D4", "D5"] if self.deform else []) + ["G1", "G2", "C1", "C2", "C3"]
+        mats = [self.layers["D1"][:, :32] if k == "D1h" else self.layers[k] for k in order]
+        blob = np.concatenate([pack_weight(m) for m in mats])
+        self.w_bytes = int(blob.size)
+        self.blob = dev(blob.copy(), dtype=torch.uint8)
+
+    def theta_bias(self, theta) -> np.ndarray:
+        """DeformNet layer-1 pose term W1[:, 32:] @ theta, folded into a per-frame bias (fp32)."""
+        W = self.layers["D1"][:, 32:].astype(np.float32)
+        return (W @ np.asarray(theta, dtype=np.float32)).astype(np.float32)
+
+
+class HumanField:
+    """Canonical human radiance field + its static canonical occupancy."""
+
+    def __init__(self, nodes, template_points, skin_verts, skin_weights, cfg: RenderConfig | None = None,
+                 seed: int = 0, zero_deform_out: bool = True, table_scale: float = 1e-4):
+        self.cfg = cfg = cfg or RenderConfig()
+        nodes = np.asarray(nodes, dtype=np.float64)
+        lo, hi = nodes.min(0), nodes.max(0)
+        self.side = float((hi - lo).max() + 2 * 0.15)
+        self.canon_min = (lo + hi) / 2 - self.side / 2
+        self.inv_side = 1.0 / self.side
+        rng = np.random.default_rng(seed)
+        self.cgrid = HashGrid(CANON_GRID, init_scale=table_scale, seed=seed + 1)
+        self.dgrid = HashGrid(DEFORM_GRID, init_scale=table_scale, seed=seed + 2)
+        self.nets = FieldNets(rng, deform=True, zero_deform_out=zero_deform_out)
+        self.graph = EDGraph(nodes, radius=cfg.ed_radius, knn_k=cfg.ed_k)
+        self.nodes = dev(nodes, shape_last=3)
+        self.node_buckets = Buckets(len(nodes))
+        self.node_buckets.build(self.nodes)
+        self.lbs = BackwardLBS(skin_verts, skin_weights, max_dist=cfg.lbs_max_dist)
+        # geometry-initialised canonical density bits (stand-in for a trained density grid)
+        self.canon_occ = occ_grid(self.canon_min, self.side, cfg.canon_occ_res)
+        self._tpl = dev(template_points, shape_last=3)
+        tb = Buckets(len(template_points))
+        tb.build(self._tpl)
+        nwords = (cfg.canon_occ_res ** 3 + 31) // 32
+        self.canon_bits = torch.empty(nwords, dtype=torch.int32, device=self.nodes.device)
+        _lib.call("cf_occ_from_points", tb.handle, _lib.byref(self.canon_occ), cfg.canon_occ_radius,
+                  self.canon_bits.data_ptr(), _lib.stream_ptr())
+        self._tb = tb
+
+    def desc(self, dbias: torch.Tensor) -> _lib.FieldDesc:
+        d = _lib.FieldDesc()
+        d.has_deform = 1
+        d.dgrid = self.dgrid.desc
+        d.dtable = self.dgrid.table.data_ptr()
+        d.cgrid = self.cgrid.desc
+        d.ctable = self.cgrid.table.data_ptr()
+        d.wblob = self.nets.blob.data_ptr()
+        d.w_bytes = self.nets.w_bytes
+        d.dbias = dbias.data_ptr()
+        d.delta_scale = 0.05
+        d.inv_side = self.inv_side
+        return d
+
+
+class ObjectField:
+    """Object-local rigid radiance field (static box geometry for its occupancy)."""
+
+    def __init__(self, half_extents, cfg: RenderConfig | None = None, seed: int = 1, table_scale: float = 1e-4):
+        self.cfg = cfg = cfg or RenderConfig()
+        self.half = np.asarray(half_extents, dtype=np.float64)
+        self.side = float(2 * self.half.max() + 2 * 0.05)
+        self.obj_min = -np.full(3, self.side / 2)
+        self.inv_side = 1.0 / self.side
+        rng = np.random.default_rng(seed)
+        self.cgrid = HashGrid(CANON_GRID, init_scale=table_scale, seed=seed + 11)
+        self.nets = FieldNets(rng, deform=False)
+        self.occ = occ_grid(self.obj_min, self.side, cfg.obj_occ_res)
+        nwords = (cfg.obj_occ_res ** 3 + 31) // 32
+        self.bits = torch.empty(nwords, dtype=torch.int32, device=self.cgrid.table.device)
+        h = (ctypes.c_double * 3)(*self.half)
+        _lib.call("cf_occ_box_shell", _lib.byref(self.occ), h, cfg.obj_shell, self.bits.data_ptr(), _lib.stream_ptr())
+
+    def desc(self) -> _lib.FieldDesc:
+        d = _lib.FieldDesc()
+        d.has_deform = 0
+        d.cgrid = self.cgrid.desc
+        d.ctable = self.cgrid.table.data_ptr()
+        d.wblob = self.nets.blob.data_ptr()
+        d.w_bytes = self.nets.w_bytes
+        d.delta_scale = 0.05
+        d.inv_side = self.inv_side
+        return d
+
+
+class _FieldBuffers:
+    def __init__(self, n_rays, capacity, device):
+        self.records = torch.empty(capacity, dtype=torch.int32, device=device)
+        self.ray_offset = torch.empty(n_rays, dtype=torch.int32, device=device)
+        self.ray_count = torch.empty(n_rays, dtype=torch.int32, device=device)
+        self.counters = torch.zeros(2, dtype=torch.int32, device=device)
+        self.xu = torch.empty((capacity, 4), dtype=torch.float32, device=device)
+        self.out = torch.empty((capacity, 4), dtype=torch.float32, device=device)
+        self.rgb = torch.empty((n_rays, 3), dtype=torch.float32, device=device)
+        self.depth = torch.empty(n_rays, dtype=torch.float32, device=device)
+        self.opacity = torch.empty(n_rays, dtype=torch.float32, device=device)
+        self.mo = _lib.MarchOut(self.records.data_ptr(), self.ray_offset.data_ptr(), self.ray_count.data_ptr(),
+                                self.counters.data_ptr(), int(capacity))
+
+
+class Renderer:
+    """render_view for one human + one rigid object."""
+
+    def __init__(self, human: HumanField | None, obj: ObjectField | None, width: int, height: int,
+                 cfg: RenderConfig | None = None, capacity_per_ray: int | None = None):
+        self.cfg = cfg = cfg or RenderConfig()
+        self.human, self.obj = human, obj
+        self.W, self.H = int(width), int(height)
+        self.n_rays = self.W * self.H
+        d = _lib.require_cuda()
+        cap = self.n_rays * int(capacity_per_ray or cfg.n_samples)
+        self.dirs = torch.empty((self.n_rays, 3), dtype=torch.float64, device=d)
+        self.hb = _FieldBuffers(self.n_rays, cap, d) if human else None
+        self.ob = _FieldBuffers(self.n_rays, cap, d) if obj else None
+        self.image = torch.empty((self.n_rays, 3), dtype=torch.float32, device=d)
+        self.layer = torch.empty(self.n_rays, dtype=torch.uint8, device=d)
+        self.live_occ = occ_grid(cfg.world_min, cfg.world_size, cfg.live_occ_res)
+        self.live_bits = torch.zeros((cfg.live_occ_res ** 3 + 31) // 32, dtype=torch.int32, device=d)
+        self.bg = (ctypes.c_float * 3)(*cfg.background)
+        self.M = _lib.MarchDesc()
+        self.M.n_samples = cfg.n_samples
+        self.M.t_near, self.M.t_far = cfg.t_near, cfg.t_far
+        self.M.dt = (cfg.t_far - cfg.t_near) / cfg.n_samples
+        self.M.human_grid = self.live_occ
+        if obj:
+            self.M.object_grid = obj.occ
+            for a in range(3):
+                self.M.obj_min[a] = obj.obj_min[a]
+            self.M.obj_inv_side = obj.inv_side
+        self.frame = None
+
+    # -- per-frame setup ------------------------------------------------------
+
+    def set_frame(self, node_dqs=None, theta=None, bone_A=None, obj_R=None, obj_t=None):
+        """Register the frame's motion prior: ED node dqs, SMPL-style pose (theta, bone
+        transforms) and the object pose (object-to-world)."""
+        s = _lib.stream_ptr()
+        if self.human is not None:
+            h = self.human
+            if getattr(self, "_anchor_buckets", None) is None:
+                self._anchor_buckets = Buckets(len(h.graph.nodes))
+            self.frame = FrameMotion(h.graph, GraphMotion(0, node_dqs), buckets=self._anchor_buckets)
+            h.lbs.set_pose(bone_A)
+            self.dbias = dev(h.nets.theta_bias(theta), dtype=torch.float32)
+            _lib.call("cf_occ_splat", h.canon_bits.data_ptr(), _lib.byref(h.canon_occ), h.node_buckets.handle,
+                      self.frame.dqs.data_ptr(), self.cfg.ed_k, self.cfg.ed_radius, _lib.byref(self.live_occ),
+                      self.live_bits.data_ptr(), s)
+            w = _lib.HumanWarp()
+            w.dqs = self.frame.dqs.data_ptr()
+            w.k = self.cfg.ed_k
+            w.r2 = self.cfg.ed_radius ** 2
+            w.vert_Tinv = h.lbs.Tinv.data_ptr()
+            w.lbs_max_d2 = self.cfg.lbs_max_dist ** 2
+            for a in range(3):
+                w.canon_min[a] = h.canon_min[a]
+            w.inv_side = h.inv_side
+            self.hw = w
+            self.hdesc = h.desc(self.dbias)
+        if self.obj is not None:
+            R = np.asarray(obj_R, dtype=np.float64).reshape(9)
+            t = np.asarray(obj_t, dtype=np.float64).reshape(3)
+            for i in range(9):
+                self.M.obj_R[i] = R[i]
+            for i in range(3):
+                self.M.obj_t[i] = t[i]
+            self.odesc = self.obj.desc()
+
+    # -- per-view --------------------------------------------------------------
+
+    def rays(self, R, t, fx, fy, cx, cy):
+        cam = _lib.Camera()
+        Rf = np.asarray(R, dtype=np.float64).reshape(9)
+        for i in range(9):
+            cam.R[i] = Rf[i]
+        cam.fx, cam.fy, cam.cx, cam.cy = float(fx), float(fy), float(cx), float(cy)
+        cam.width, cam.height = self.W, self.H
+        _lib.call("cf_camera_rays", _lib.byref(cam), self.dirs.data_ptr(), _lib.stream_ptr())
+        for a in range(3):
+            self.M.origin[a] = float(t[a])
+        self.M.n_rays = self.n_rays
+
+    def render(self, R, t, fx, fy, cx, cy):
+        """All stages of one novel view; returns the composited image tensor (H*W, 3)."""
+        s = _lib.stream_ptr()
+        self.rays(R, t, fx, fy, cx, cy)
+        hb, ob = self.hb, self.ob
+        _lib.call("cf_march", _lib.byref(self.M), self.dirs.data_ptr(),
+                  self.live_bits.data_ptr() if hb else None, self.obj.bits.data_ptr() if ob else None,
+                  _lib.byref(hb.mo) if hb else None, _lib.byref(ob.mo) if ob else None, s)
+        if hb:
+            h = self.human
+            _lib.call("cf_human_canon", _lib.byref(self.M), self.dirs.data_ptr(), _lib.byref(hb.mo),
+                      _lib.byref(self.hw), self.frame.live_buckets.handle, h.lbs.buckets.handle, hb.xu.data_ptr(), s)
+            _lib.call("cf_field_forward", _lib.byref(self.hdesc), _lib.byref(hb.mo), self.dirs.data_ptr(),
+                      hb.xu.data_ptr(), hb.out.data_ptr(), s)
+            _lib.call("cf_composite", _lib.byref(self.M), _lib.byref(hb.mo), hb.out.data_ptr(), self.cfg.t_term,
+                      hb.rgb.data_ptr(), hb.depth.data_ptr(), hb.opacity.data_ptr(), s)
+        if ob:
+            _lib.call("cf_object_canon", _lib.byref(self.M), self.dirs.data_ptr(), _lib.byref(ob.mo),
+                      ob.xu.data_ptr(), s)
+            _lib.call("cf_field_forward", _lib.byref(self.odesc), _lib.byref(ob.mo), self.dirs.data_ptr(),
+                      ob.xu.data_ptr(), ob.out.data_ptr(), s)
+            _lib.call("cf_composite", _lib.byref(self.M), _lib.byref(ob.mo), ob.out.data_ptr(), self.cfg.t_term,
+                      ob.rgb.data_ptr(), ob.depth.data_ptr(), ob.opacity.data_ptr(), s)
+        _lib.call("cf_composite_layers", self.n_rays, hb.rgb.data_ptr() if hb else None,
+                  hb.depth.data_ptr() if hb else None, hb.opacity.data_ptr() if hb else None,
+                  ob.rgb.data_ptr() if ob else None, ob.depth.data_ptr() if ob else None,
+                  ob.opacity.data_ptr() if ob else None, self.bg, self.image.data_ptr(), self.layer.data_ptr(), s)
+        return self.image
+
+    def sample_counts(self):
+        """(human, object) processed-sample counts of the last view (syncs)."""
+        h = int(self.hb.counters[0]) if self.hb else 0
+        o = int(self.ob.counters[0]) if self.ob else 0
+        return h, o
+
+    def check_overflow(self):
+        for b in (self.hb, self.ob):
+            if b is not None and int(b.counters[1]) != 0:
+                raise RuntimeError("sample buffer overflow: raise capacity_per_ray")

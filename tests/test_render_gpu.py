@@ -1,0 +1,175 @@
+"""Render path parity on the B200 (C1 frame: 64x64 rays, 64 samples/ray, 128 ED
+nodes + 6890 skin verts, 16-level 2^19 grid), stage by stage against the
+oracle fed with the previous stage's device output:
+  occupancy bits, march sample sets, ED/LBS flags      bit-exact
+  canonical coordinates (float32)                      ED: bit-exact; LBS: 1e-6
+  field sigma / rgb (fp16 tensor-core MLPs)            see FIELD_* below
+  composite rgb / opacity / depth                      1e-5 abs
+  layer choice                                         bit-exact
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import deform as od
+from oracle import render as orr
+from paper_2304_03184_b200.render import HumanField, ObjectField, RenderConfig, Renderer
+from paper_2304_03184_b200.scene import Scene, SceneConfig
+
+pytestmark = pytest.mark.gpu
+
+FIELD_RGB_ATOL = 2e-3     # fp16 activations: one-ulp flips of intermediate rounding
+FIELD_SIGMA_RTOL = 2e-2
+
+
+def words(t):
+    return t.cpu().numpy().view(np.uint32)
+
+
+@pytest.fixture(scope="module")
+def setup():
+    sc = Scene(SceneConfig(width=64, height=64), seed=0)
+    cfg = RenderConfig(n_samples=64)
+    hf = HumanField(sc.nodes, sc.template_points, sc.skin_verts, sc.skin_weights, cfg, seed=0, zero_deform_out=False,
+                    table_scale=0.5)
+    of = ObjectField(sc.box_half, cfg, seed=1, table_scale=0.5)
+    for f, s in ((hf, 6.0), (of, 14.0)):  # denser random fields so both layers win somewhere
+        f.nets.layers["G2"][0] *= s
+        f.nets.repack()
+    r = Renderer(hf, of, 64, 64, cfg)
+    fid = 7
+    R, t = sc.object_pose(fid)
+    r.set_frame(sc.node_dqs(fid), sc.theta(fid), sc.bone_transforms(fid), R, t)
+    cam = sc.camera
+    img = r.render(cam.R, cam.t, cam.fx, cam.fy, cam.cx, cam.cy)
+    torch.cuda.synchronize()
+    r.check_overflow()
+    return sc, cfg, hf, of, r, fid, img
+
+
+def field_samples(buf):
+    n = int(buf.counters[0])
+    rec = buf.records[:n].cpu().numpy().view(np.uint32)
+    return n, (rec >> 8).astype(np.int64), (rec & 255).astype(np.int64)
+
+
+def test_rays(setup):
+    sc, cfg, hf, of, r, fid, img = setup
+    _, d = sc.camera.all_rays()
+    assert np.allclose(r.dirs.cpu().numpy(), d, rtol=0, atol=1e-15)
+
+
+def test_occupancy_bits_bitexact(setup):
+    sc, cfg, hf, of, r, fid, img = setup
+    g = hf.canon_occ
+    on = orr.occ_from_points(sc.template_points, list(g.min), g.cell, g.res, cfg.canon_occ_radius)
+    got = orr.unpack_bits(words(hf.canon_bits), g.res ** 3)
+    assert np.array_equal(got, on) and on.sum() > 1000
+    og = of.occ
+    ob = orr.occ_box_shell(list(og.min), og.cell, og.res, sc.box_half, cfg.obj_shell)
+    assert np.array_equal(orr.unpack_bits(words(of.bits), og.res ** 3), ob)
+    lg = r.live_occ
+    live = orr.occ_splat(got, (list(g.min), g.cell, g.res), sc.nodes, sc.node_dqs(fid), cfg.ed_k, cfg.ed_radius,
+                         (list(lg.min), lg.cell, lg.res))
+    assert np.array_equal(orr.unpack_bits(words(r.live_bits), lg.res ** 3), live)
+
+
+def test_march_sets_bitexact(setup):
+    sc, cfg, hf, of, r, fid, img = setup
+    dirs = r.dirs.cpu().numpy()
+    lg, og = r.live_occ, of.occ
+    R, t = sc.object_pose(fid)
+    ref = orr.march(sc.camera.t, dirs, cfg.n_samples, cfg.t_near, r.M.dt,
+                    orr.unpack_bits(words(r.live_bits), lg.res ** 3), (list(lg.min), lg.cell, lg.res),
+                    orr.unpack_bits(words(of.bits), og.res ** 3), (list(og.min), og.cell, og.res), R, t)
+    for name, buf in (("human", r.hb), ("object", r.ob)):
+        n, ray, i = field_samples(buf)
+        rr, ri = ref[name]
+        assert n == len(rr) and n > 0
+        got = np.sort(ray * 256 + i)
+        assert np.array_equal(got, np.sort(rr * 256 + ri))
+        # per-ray grouping, ascending i
+        off = buf.ray_offset.cpu().numpy()
+        cnt = buf.ray_count.cpu().numpy()
+        assert cnt.sum() == n
+        rec_ray = ray
+        for q in np.nonzero(cnt)[0][:200]:
+            seg = slice(off[q], off[q] + cnt[q])
+            assert (rec_ray[seg] == q).all() and (np.diff(i[seg]) > 0).all()
+
+
+def test_human_canon(setup):
+    sc, cfg, hf, of, r, fid, img = setup
+    n, ray, i = field_samples(r.hb)
+    p = orr.sample_points(sc.camera.t, r.dirs.cpu().numpy(), ray, i, cfg.t_near, r.M.dt)
+    ref = orr.human_canon(p, sc.nodes, sc.node_dqs(fid), cfg.ed_k, cfg.ed_radius, sc.bone_transforms(fid),
+                          sc.skin_verts, sc.skin_weights, cfg.lbs_max_dist, hf.canon_min, hf.inv_side)
+    got = r.hb.xu[:n].cpu().numpy()
+    assert np.array_equal(got[:, 3], ref[:, 3])
+    ed = ref[:, 3] == 1
+    lbs = ref[:, 3] == 2
+    assert ed.mean() > 0.5
+    ulp = np.abs(got[ed, :3].view(np.int32) - ref[ed, :3].view(np.int32))
+    assert ulp.max() <= 1 and (ulp == 0).mean() > 0.999
+    assert np.allclose(got[lbs, :3], ref[lbs, :3], rtol=0, atol=1e-6)
+
+
+def _field_ref(layers, has_deform, xu, dirs, grid, dgrid=None, dbias=None, inv_side=1.0):
+    return orr.field_forward(layers, has_deform, xu, dirs, grid.table.cpu().numpy(),
+                             dgrid.table.cpu().numpy() if dgrid is not None else None, dbias, inv_side)
+
+
+def _check_field(got, ref):
+    assert np.array_equal(got[:, 0] == 0, ref[:, 0] == 0)
+    rel = np.abs(got[:, 0] - ref[:, 0]) / np.maximum(np.abs(ref[:, 0]), 1e-6)
+    assert np.quantile(rel, 0.999) <= FIELD_SIGMA_RTOL, np.quantile(rel, [0.5, 0.99, 0.999, 1.0])
+    err = np.abs(got[:, 1:] - ref[:, 1:])
+    assert np.quantile(err, 0.999) <= FIELD_RGB_ATOL, np.quantile(err, [0.5, 0.99, 0.999, 1.0])
+    assert np.median(err) <= 1e-4
+
+
+def test_field_forward_human(setup):
+    sc, cfg, hf, of, r, fid, img = setup
+    n, ray, i = field_samples(r.hb)
+    xu = r.hb.xu[:n].cpu().numpy()
+    dirs = r.dirs.cpu().numpy()[ray]
+    ref = _field_ref(hf.nets.layers, True, xu, dirs, hf.cgrid, hf.dgrid, hf.nets.theta_bias(sc.theta(fid)),
+                     hf.inv_side)
+    _check_field(r.hb.out[:n].cpu().numpy(), ref)
+
+
+def test_field_forward_object(setup):
+    sc, cfg, hf, of, r, fid, img = setup
+    n, ray, i = field_samples(r.ob)
+    xu = r.ob.xu[:n].cpu().numpy()
+    R, t = sc.object_pose(fid)
+    p = orr.sample_points(sc.camera.t, r.dirs.cpu().numpy(), ray, i, cfg.t_near, r.M.dt)
+    ref_xu = orr.object_canon(p, R, t, of.obj_min, of.inv_side)
+    assert np.array_equal(xu, ref_xu)
+    ref = _field_ref(of.nets.layers, False, xu, r.dirs.cpu().numpy()[ray], of.cgrid)
+    _check_field(r.ob.out[:n].cpu().numpy(), ref)
+
+
+def test_composite_and_layers(setup):
+    sc, cfg, hf, of, r, fid, img = setup
+    res = {}
+    for name, buf in (("human", r.hb), ("object", r.ob)):
+        n, ray, i = field_samples(buf)
+        rgb, dep, op = orr.composite(r.n_rays, ray, i, buf.out[:n].cpu().numpy(), cfg.t_near, r.M.dt, cfg.t_term)
+        assert np.allclose(buf.rgb.cpu().numpy(), rgb, atol=1e-5)
+        assert np.allclose(buf.opacity.cpu().numpy(), op, atol=1e-5)
+        ok = op > 1e-3
+        assert np.allclose(buf.depth.cpu().numpy()[ok], dep[ok], rtol=1e-4)
+        res[name] = (buf.rgb.cpu().numpy(), buf.depth.cpu().numpy(), buf.opacity.cpu().numpy())
+    out, L = orr.layers(res["human"], res["object"], cfg.background)
+    assert np.array_equal(r.layer.cpu().numpy(), L)
+    assert np.array_equal(img.cpu().numpy(), out)
+    assert (L == 1).sum() > 0 and (L == 2).sum() > 0
+
+
+def test_render_deterministic(setup):
+    sc, cfg, hf, of, r, fid, img = setup
+    a = img.clone()
+    cam = sc.camera
+    b = r.render(cam.R, cam.t, cam.fx, cam.fy, cam.cx, cam.cy)
+    assert torch.equal(a, b)
