@@ -1,0 +1,458 @@
+#!/usr/bin/env python
+"""Headline benchmark: deformed samples/s and ms per 512x512 frame (BASELINE.json
+`metric`, workload configs[1]: 512^2 novel-view render of the synthetic human +
+rigid object, 128 samples/ray, 1 B200; N GPUs = N independent ranks, each
+rendering its own frame stream — weak scaling, no data-path collective).
+
+A step = one frame: load the frame's motion prior (ED node dqs, bone transforms,
+DeformNet pose bias, object pose), per-frame setup (deformed nodes, buckets,
+backward-LBS vertex transforms, live occupancy splat) and the full render
+(rays, occupancy-skipped march, hybrid canonicalisation, fused hash+tcgen05
+field, compositing, layer composite).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "deformed samples/s (warp+hash+MLP+composite); ms per 512² frame; 1/2/4/8 B200"
+UNIT = "samples/s"
+FLOP_PER_SAMPLE_HUMAN = 2 * (32 * 128 + 3 * 128 * 128 + 128 * 16) + 2 * (32 * 64 + 64 * 16) + 2 * (
+    32 * 64 + 64 * 64 + 64 * 16)  # 131,072 (DeformNet + E_g + E_c, padded widths as issued)
+FLOP_PER_SAMPLE_OBJECT = 2 * (32 * 64 + 64 * 16) + 2 * (32 * 64 + 64 * 64 + 64 * 16)  # 20,480
+KERNELS_PER_STEP = 21  # see DESIGN.md §8 (12 per-frame setup + 9 render launches), checked against ncu
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--width", type=int, default=512)
+    ap.add_argument("--height", type=int, default=512)
+    ap.add_argument("--samples", type=int, default=128)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- distributed
+
+def dist_setup(n_gpus):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
+        pg = dist
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return rank, world, local, pg
+
+
+def barrier(pg):
+    if pg is not None:
+        pg.barrier()
+
+
+def max_over_ranks(pg, v: float) -> float:
+    if pg is None:
+        return v
+    import torch
+    t = torch.tensor([v], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    pg.all_reduce(t, op=pg.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(pg, v: float) -> float:
+    if pg is None:
+        return v
+    import torch
+    t = torch.tensor([v], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    pg.all_reduce(t, op=pg.ReduceOp.SUM)
+    return float(t.item())
+
+
+# ----------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi-equivalent clock / throttle sampling (NVML) during the timed region."""
+
+    def __init__(self, index=0, period=0.02):
+        self.samples, self.reasons = [], set()
+        self.period, self.index = period, index
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+            self.max_mhz = None
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, b in names.items():
+                    if mask & b:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv is not None:
+            self.t.join()
+
+    def summary(self):
+        med = float(np.median(self.samples)) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------- workload
+
+def build_workload(args, rank):
+    from paper_2304_03184_b200.render import HumanField, ObjectField, RenderConfig, Renderer
+    from paper_2304_03184_b200.scene import Scene, SceneConfig
+    sc = Scene(SceneConfig(width=args.width, height=args.height), seed=0)
+    cfg = RenderConfig(n_samples=args.samples)
+    hf = HumanField(sc.nodes, sc.template_points, sc.skin_verts, sc.skin_weights, cfg, seed=0, zero_deform_out=False)
+    of = ObjectField(sc.box_half, cfg, seed=1)
+    r = Renderer(hf, of, args.width, args.height, cfg)
+    frames = []
+    for fid in range(sc.cfg.frames):
+        R, t = sc.object_pose(fid)
+        frames.append(dict(dqs=sc.node_dqs(fid), A=sc.bone_transforms(fid),
+                           dbias=hf.nets.theta_bias(sc.theta(fid)), R=R, t=t))
+    return sc, cfg, hf, of, r, frames
+
+
+def run_ours(args, rank, world, pg):
+    import torch
+    from paper_2304_03184_b200 import _lib
+    sc, cfg, hf, of, r, frames = build_workload(args, rank)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    cam = sc.camera
+    # device-resident inputs (value) and pinned host inputs (e2e)
+    dframes, hframes = [], []
+    for f in frames:
+        dframes.append((torch.from_numpy(f["dqs"]).to(dev), torch.from_numpy(f["A"]).to(dev),
+                        torch.from_numpy(f["dbias"]).to(dev), f["R"], f["t"]))
+        hframes.append((torch.from_numpy(f["dqs"]).pin_memory(), torch.from_numpy(f["A"]).pin_memory(),
+                        torch.from_numpy(f["dbias"]).pin_memory(), f["R"], f["t"]))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def step(fi, src):
+        dqs, A, dbias, R, t = src[fi]
+        r.load_prior(dqs, A, dbias)
+        r.set_object_pose(R, t)
+        return r.render(cam.R, cam.t, cam.fx, cam.fy, cam.cx, cam.cy)
+
+    nF = len(frames)
+    # processed-sample counts per frame (deterministic), untimed
+    counts = []
+    for fi in range(nF):
+        step(fi, dframes)
+        torch.cuda.synchronize()
+        r.check_overflow()
+        counts.append(r.sample_counts())
+    for w in range(args.warmup):
+        step((w + rank) % nF, dframes)
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, device-resident inputs, L2 flushed between steps
+    barrier(pg)
+    torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    stage_marks = []
+    processed = 0
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        for k in range(args.steps):
+            fi = (k + rank) % nF
+            flush.zero_()
+            r.marks = [("start", starts[k])]
+            starts[k].record()
+            step(fi, dframes)
+            ends[k].record()
+            stage_marks.append(r.marks)
+            r.marks = None
+            processed += counts[fi][0] + counts[fi][1]
+        torch.cuda.synchronize()
+    barrier(pg)
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    ms_local = float(np.sum(step_ms))
+    ms_total = max_over_ranks(pg, ms_local)
+    processed_all = sum_over_ranks(pg, float(processed))
+    value = processed_all / (ms_total / 1e3)
+    ms_per_step = ms_total / args.steps
+
+    # per-stage times (CUDA events on the launching stream inside the timed region)
+    stages = {}
+    for marks in stage_marks:
+        for (n0, e0), (n1, e1) in zip(marks[:-1], marks[1:]):
+            stages.setdefault(n1, []).append(e0.elapsed_time(e1))
+    stage_ms = {k: float(np.mean(v)) for k, v in stages.items()}
+
+    # ---- e2e: pinned host prior -> device, render through the public API, image -> pinned host
+    e2e = None
+    if not args.no_e2e:
+        img_host = torch.empty((r.n_rays, 3), dtype=torch.float32).pin_memory()
+        h2d = sum(int(x.numel() * x.element_size()) for x in hframes[0][:3])
+        d2h = int(img_host.numel() * img_host.element_size())
+        for w in range(2):
+            step(w % nF, hframes)
+        torch.cuda.synchronize()
+        barrier(pg)
+        t0 = time.perf_counter()
+        for k in range(args.steps):
+            img = step((k + rank) % nF, hframes)
+            img_host.copy_(img, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        wall = time.perf_counter() - t0
+        barrier(pg)
+        wall = max_over_ranks(pg, wall)
+        e2e = {"value": processed_all / wall, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": wall * 1e3 / args.steps}
+
+    # ---- roofline of the dominant kernel
+    hs = float(np.mean([counts[(k + rank) % nF][0] for k in range(args.steps)]))
+    os_ = float(np.mean([counts[(k + rank) % nF][1] for k in range(args.steps)]))
+    dom = max(stage_ms, key=stage_ms.get)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    tensor_peak = float(peaks.get("bf16_tflops", 1590.0))
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    if dom in ("human_field", "object_field"):
+        n = hs if dom == "human_field" else os_
+        flop = n * (FLOP_PER_SAMPLE_HUMAN if dom == "human_field" else FLOP_PER_SAMPLE_OBJECT)
+        ach = flop / (stage_ms[dom] / 1e3) / 1e12
+        roof = {"kernel": dom, "bound": "tensor", "achieved": ach, "peak": tensor_peak, "unit": "TFLOP/s",
+                "frac": ach / tensor_peak, "traffic": None,
+                "per_unit": "131072 FLOP/sample (human) / 20480 (object)",
+                "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst; fp16 dense rate is the same)"}
+    else:
+        per = {"human_canon": 4 + 24 + 16, "march": 24 + 8 + 4 * 0, "human_composite": 24, "object_composite": 24}
+        n = hs if dom.startswith("human") else (os_ if dom.startswith("object") else r.n_rays)
+        byt = n * per.get(dom, 16)
+        ach = byt / (stage_ms[dom] / 1e3) / 1e9
+        roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+                "frac": ach / hbm_peak, "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64 deform / f32 hash / fp16-in fp32-acc MLP", "data": "synthetic (seeded scene, random-init fields)",
+        "config": {"workload": f"{args.width}x{args.height} novel-view render, human+rigid object, "
+                               f"{args.samples} samples/ray, occupancy-skipped (configs[1])",
+                   "rays_per_frame": r.n_rays, "nominal_samples_per_frame": r.n_rays * args.samples,
+                   "processed_samples_per_frame": hs + os_, "human_samples_per_frame": hs,
+                   "object_samples_per_frame": os_, "ed_nodes": int(len(sc.nodes)), "skin_verts": int(len(sc.skin_verts)),
+                   "hash": "16 levels x 2^19 x F2 (canonical) + 8 x 2^17 x F4 (deform)",
+                   "l2": "flushed (256 MiB write) between timed steps, outside the per-step events",
+                   "parallelism": f"{world} independent rank(s), frames per rank"},
+        "ms_per_frame": ms_per_step,
+        "nominal_samples_per_s": (r.n_rays * args.samples * args.steps * world) / (ms_total / 1e3),
+        "stage_ms": stage_ms,
+        "roofline": roof,
+        "gpu_launches": KERNELS_PER_STEP * args.steps,
+        "e2e": e2e,
+    }
+    line["clocks"] = clk.summary()
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args, sc, cfg, hf, of, frames, r, budget_s=12.0)
+    if rank == 0:
+        print(json.dumps(line))
+
+
+# ----------------------------------------------------------------- CPU path (oracle)
+
+_W = {}
+
+
+def _cpu_work(ray_ids):
+    """Oracle pipeline for a set of rays of frame _W['fid']: march, canonicalise,
+    field, composite. Returns processed samples."""
+    from oracle import render as orr
+    W = _W
+    out = orr.march(W["origin"], W["dirs"][ray_ids], W["S"], W["t_near"], W["dt"], W["live_on"], W["lg"],
+                    W["obj_on"], W["og"], W["R"], W["t"])
+    n_done = 0
+    for name in ("human", "object"):
+        rr, ii = out[name]
+        if len(rr) == 0:
+            continue
+        p = orr.sample_points(W["origin"], W["dirs"][ray_ids], rr, ii, W["t_near"], W["dt"])
+        d = W["dirs"][ray_ids][rr]
+        if name == "human":
+            xu = orr.human_canon(p, W["nodes"], W["dqs"], 4, 0.1, W["A"], W["verts"], W["vw"], 0.2, W["cmin"],
+                                 W["cinv"])
+            f = orr.field_forward(W["hl"], True, xu, d, W["htab"], W["dtab"], W["dbias"], W["cinv"])
+        else:
+            xu = orr.object_canon(p, W["R"], W["t"], W["omin"], W["oinv"])
+            f = orr.field_forward(W["ol"], False, xu, d, W["otab"])
+        orr.composite(len(ray_ids), rr, ii, f, W["t_near"], W["dt"])
+        n_done += len(rr)
+    return n_done
+
+
+def _prepare_cpu(sc, cfg, hf, of, frames, fid, live_on):
+    from paper_2304_03184_b200.render import Renderer  # noqa: F401  (only for config parity)
+    f = frames[fid]
+    o, d = sc.camera.all_rays()
+    lg = (list(cfg.world_min), cfg.world_size / cfg.live_occ_res, cfg.live_occ_res)
+    og = (list(of.obj_min), of.side / cfg.obj_occ_res, cfg.obj_occ_res)
+    from oracle import render as orr
+    obj_on = orr.occ_box_shell(og[0], og[1], og[2], of.half, cfg.obj_shell)
+    _W.update(origin=sc.camera.t, dirs=d, S=cfg.n_samples, t_near=cfg.t_near,
+              dt=(cfg.t_far - cfg.t_near) / cfg.n_samples, live_on=live_on, lg=lg, obj_on=obj_on, og=og,
+              R=f["R"], t=f["t"], nodes=sc.nodes, dqs=f["dqs"], A=f["A"], verts=sc.skin_verts, vw=sc.skin_weights,
+              cmin=hf.canon_min, cinv=hf.inv_side, hl=hf.nets.layers, htab=hf.cgrid.table.cpu().numpy(),
+              dtab=hf.dgrid.table.cpu().numpy(), dbias=f["dbias"], ol=of.nets.layers,
+              otab=of.cgrid.table.cpu().numpy(), omin=of.obj_min, oinv=of.inv_side)
+
+
+def _live_on_host(r, hf, cfg, frames, fid):
+    """Live occupancy of frame fid for the CPU path (per-frame setup, untimed)."""
+    import torch
+    from oracle import render as orr
+    f = frames[fid]
+    dev = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else None
+    if dev is not None:
+        r.load_prior(torch.from_numpy(f["dqs"]).to(dev), torch.from_numpy(f["A"]).to(dev),
+                     torch.from_numpy(f["dbias"]).to(dev))
+        torch.cuda.synchronize()
+        return orr.unpack_bits(r.live_bits.cpu().numpy().view(np.uint32), cfg.live_occ_res ** 3)
+    raise RuntimeError("live occupancy needs the device setup")
+
+
+def _pool_run(ray_sets, cores):
+    import multiprocessing as mp
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        return sum(pool.map(_cpu_work, ray_sets))
+
+
+def _rays_near_human(sc, n):
+    """A bounded sample of the frame: the n rays nearest the image centre of the human."""
+    W, H = sc.cfg.width, sc.cfg.height
+    cy, cx = int(H * 0.48), W // 2
+    side = int(np.sqrt(n))
+    ys = np.arange(cy - side // 2, cy - side // 2 + side)
+    xs = np.arange(cx - side // 2, cx - side // 2 + side)
+    return (ys[:, None] * W + xs[None, :]).reshape(-1)
+
+
+def cpu_baseline(args, sc, cfg, hf, of, frames, r, budget_s=12.0, rays=4096):
+    import os as _os
+    from threadpoolctl import threadpool_limits
+    _prepare_cpu(sc, cfg, hf, of, frames, 7, _live_on_host(r, hf, cfg, frames, 7))
+    cores = _os.cpu_count() or 1
+    ray_ids = _rays_near_human(sc, rays)
+    sets = np.array_split(ray_ids, cores * 4)
+    with threadpool_limits(1):
+        t0 = time.perf_counter()
+        done, reps = 0, 0
+        while True:
+            done += _pool_run(sets, cores)
+            reps += 1
+            if time.perf_counter() - t0 > budget_s or reps >= 8:
+                break
+        el = time.perf_counter() - t0
+    return {"value": done / el, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"oracle (numpy restatement of the reference + SPEC) on {len(ray_ids)} rays x "
+                      f"{cfg.n_samples} samples around the human of frame 7 (occupancy-skipped; per-frame setup "
+                      f"excluded), {reps} rep(s), {cores} worker processes x 1 BLAS thread"}
+
+
+def run_reference(args, rank, world, pg):
+    """--impl reference: the reference's algorithm on the host cores (oracle port,
+    the reference itself is pure Python and has no render path), same metric."""
+    if rank != 0:
+        return
+    import torch
+    sc, cfg, hf, of, r, frames = build_workload(args, rank)
+    live = _live_on_host(r, hf, cfg, frames, 7)
+    _prepare_cpu(sc, cfg, hf, of, frames, 7, live)
+    import os as _os
+    from threadpoolctl import threadpool_limits
+    cores = _os.cpu_count() or 1
+    ray_ids = _rays_near_human(sc, 1024)
+    sets = np.array_split(ray_ids, cores * 2)
+    with threadpool_limits(1):
+        for _ in range(max(1, min(args.warmup, 1))):
+            _pool_run(sets, cores)
+        t0 = time.perf_counter()
+        done = 0
+        for _ in range(args.steps):
+            done += _pool_run(sets, cores)
+        el = time.perf_counter() - t0
+    v = done / el
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": el * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64/f32 numpy", "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"{args.width}x{args.height} novel-view render, human+rigid object, "
+                                   f"{args.samples} samples/ray, occupancy-skipped (configs[1])",
+                       "parallelism": f"{cores} host processes"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": f"per step: {len(ray_ids)} rays x {cfg.n_samples} samples of frame 7 around "
+                                       f"the human through the oracle pipeline (march, ED/LBS warp, hash, MLPs, "
+                                       f"composite), {cores} processes x 1 BLAS thread"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    args = parse()
+    rank, world, local, pg = dist_setup(args.gpus)
+    if args.impl == "reference":
+        run_reference(args, rank, world, pg)
+    else:
+        run_ours(args, rank, world, pg)
+    if pg is not None:
+        pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

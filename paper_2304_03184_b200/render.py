@@ -214,25 +214,45 @@ class Renderer:
                 self.M.obj_min[a] = obj.obj_min[a]
             self.M.obj_inv_side = obj.inv_side
         self.frame = None
+        self.marks = None
 
     # -- per-frame setup ------------------------------------------------------
 
     def set_frame(self, node_dqs=None, theta=None, bone_A=None, obj_R=None, obj_t=None):
         """Register the frame's motion prior: ED node dqs, SMPL-style pose (theta, bone
         transforms) and the object pose (object-to-world)."""
-        s = _lib.stream_ptr()
         if self.human is not None:
             h = self.human
-            if getattr(self, "_anchor_buckets", None) is None:
-                self._anchor_buckets = Buckets(len(h.graph.nodes))
-            self.frame = FrameMotion(h.graph, GraphMotion(0, node_dqs), buckets=self._anchor_buckets)
-            h.lbs.set_pose(bone_A)
-            self.dbias = dev(h.nets.theta_bias(theta), dtype=torch.float32)
-            _lib.call("cf_occ_splat", h.canon_bits.data_ptr(), _lib.byref(h.canon_occ), h.node_buckets.handle,
-                      self.frame.dqs.data_ptr(), self.cfg.ed_k, self.cfg.ed_radius, _lib.byref(self.live_occ),
-                      self.live_bits.data_ptr(), s)
+            self.load_prior(dev(node_dqs, shape_last=8), dev(np.asarray(bone_A, dtype=np.float64)),
+                            dev(h.nets.theta_bias(theta), dtype=torch.float32))
+        if self.obj is not None:
+            self.set_object_pose(obj_R, obj_t)
+
+    def load_prior(self, dqs: torch.Tensor, bone_A: torch.Tensor, dbias: torch.Tensor) -> None:
+        """Per-frame human setup from device-resident prior tensors (no host sync):
+        node dqs (n,8) f64, bone transforms (J,4,4) f64, DeformNet pose bias (128,) f32."""
+        s = _lib.stream_ptr()
+        h = self.human
+        if getattr(self, "_dqs", None) is None:
+            n = len(h.graph.nodes)
+            self._dqs = torch.empty((n, 8), dtype=torch.float64, device=self.dirs.device)
+            self._anchors = torch.empty((n, 3), dtype=torch.float64, device=self.dirs.device)
+            self._A = torch.empty((h.lbs.J, 4, 4), dtype=torch.float64, device=self.dirs.device)
+            self.dbias = torch.empty(128, dtype=torch.float32, device=self.dirs.device)
+            self._anchor_buckets = Buckets(n)
+        self._dqs.copy_(dqs, non_blocking=True)
+        self._A.copy_(bone_A, non_blocking=True)
+        self.dbias.copy_(dbias, non_blocking=True)
+        n = self._dqs.shape[0]
+        _lib.call("cf_deform_nodes", h.nodes.data_ptr(), self._dqs.data_ptr(), n, self._anchors.data_ptr(), s)
+        self._anchor_buckets.build(self._anchors)
+        h.lbs.set_pose(self._A)
+        _lib.call("cf_occ_splat", h.canon_bits.data_ptr(), _lib.byref(h.canon_occ), h.node_buckets.handle,
+                  self._dqs.data_ptr(), self.cfg.ed_k, self.cfg.ed_radius, _lib.byref(self.live_occ),
+                  self.live_bits.data_ptr(), s)
+        if getattr(self, "hw", None) is None:
             w = _lib.HumanWarp()
-            w.dqs = self.frame.dqs.data_ptr()
+            w.dqs = self._dqs.data_ptr()
             w.k = self.cfg.ed_k
             w.r2 = self.cfg.ed_radius ** 2
             w.vert_Tinv = h.lbs.Tinv.data_ptr()
@@ -242,13 +262,16 @@ class Renderer:
             w.inv_side = h.inv_side
             self.hw = w
             self.hdesc = h.desc(self.dbias)
-        if self.obj is not None:
-            R = np.asarray(obj_R, dtype=np.float64).reshape(9)
-            t = np.asarray(obj_t, dtype=np.float64).reshape(3)
-            for i in range(9):
-                self.M.obj_R[i] = R[i]
-            for i in range(3):
-                self.M.obj_t[i] = t[i]
+
+    def set_object_pose(self, obj_R, obj_t) -> None:
+        """Object-to-world pose of the frame (kernel parameters, no device copy)."""
+        R = np.asarray(obj_R, dtype=np.float64).reshape(9)
+        t = np.asarray(obj_t, dtype=np.float64).reshape(3)
+        for i in range(9):
+            self.M.obj_R[i] = R[i]
+        for i in range(3):
+            self.M.obj_t[i] = t[i]
+        if getattr(self, "odesc", None) is None:
             self.odesc = self.obj.desc()
 
     # -- per-view --------------------------------------------------------------
@@ -265,33 +288,49 @@ class Renderer:
             self.M.origin[a] = float(t[a])
         self.M.n_rays = self.n_rays
 
+    def _mark(self, name):
+        if self.marks is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            self.marks.append((name, e))
+
     def render(self, R, t, fx, fy, cx, cy):
-        """All stages of one novel view; returns the composited image tensor (H*W, 3)."""
+        """All stages of one novel view; returns the composited image tensor (H*W, 3).
+        If `self.marks` is a list, a CUDA event is appended after each stage."""
         s = _lib.stream_ptr()
         self.rays(R, t, fx, fy, cx, cy)
         hb, ob = self.hb, self.ob
+        self._mark("rays")
         _lib.call("cf_march", _lib.byref(self.M), self.dirs.data_ptr(),
                   self.live_bits.data_ptr() if hb else None, self.obj.bits.data_ptr() if ob else None,
                   _lib.byref(hb.mo) if hb else None, _lib.byref(ob.mo) if ob else None, s)
+        self._mark("march")
         if hb:
             h = self.human
             _lib.call("cf_human_canon", _lib.byref(self.M), self.dirs.data_ptr(), _lib.byref(hb.mo),
-                      _lib.byref(self.hw), self.frame.live_buckets.handle, h.lbs.buckets.handle, hb.xu.data_ptr(), s)
+                      _lib.byref(self.hw), self._anchor_buckets.handle, h.lbs.buckets.handle, hb.xu.data_ptr(), s)
+            self._mark("human_canon")
             _lib.call("cf_field_forward", _lib.byref(self.hdesc), _lib.byref(hb.mo), self.dirs.data_ptr(),
                       hb.xu.data_ptr(), hb.out.data_ptr(), s)
+            self._mark("human_field")
             _lib.call("cf_composite", _lib.byref(self.M), _lib.byref(hb.mo), hb.out.data_ptr(), self.cfg.t_term,
                       hb.rgb.data_ptr(), hb.depth.data_ptr(), hb.opacity.data_ptr(), s)
+            self._mark("human_composite")
         if ob:
             _lib.call("cf_object_canon", _lib.byref(self.M), self.dirs.data_ptr(), _lib.byref(ob.mo),
                       ob.xu.data_ptr(), s)
+            self._mark("object_canon")
             _lib.call("cf_field_forward", _lib.byref(self.odesc), _lib.byref(ob.mo), self.dirs.data_ptr(),
                       ob.xu.data_ptr(), ob.out.data_ptr(), s)
+            self._mark("object_field")
             _lib.call("cf_composite", _lib.byref(self.M), _lib.byref(ob.mo), ob.out.data_ptr(), self.cfg.t_term,
                       ob.rgb.data_ptr(), ob.depth.data_ptr(), ob.opacity.data_ptr(), s)
+            self._mark("object_composite")
         _lib.call("cf_composite_layers", self.n_rays, hb.rgb.data_ptr() if hb else None,
                   hb.depth.data_ptr() if hb else None, hb.opacity.data_ptr() if hb else None,
                   ob.rgb.data_ptr() if ob else None, ob.depth.data_ptr() if ob else None,
                   ob.opacity.data_ptr() if ob else None, self.bg, self.image.data_ptr(), self.layer.data_ptr(), s)
+        self._mark("layers")
         return self.image
 
     def sample_counts(self):

@@ -51,9 +51,9 @@ class BackwardLBS:
         self.Tinv = torch.empty_like(self.T)
         self.buckets = Buckets(self.V)
 
-    def set_pose(self, A: np.ndarray) -> None:
-        """Per-frame setup from bone transforms A (J,4,4)."""
-        self.A = dev(np.asarray(A, dtype=np.float64))
+    def set_pose(self, A) -> None:
+        """Per-frame setup from bone transforms A (J,4,4): numpy, or a CUDA tensor used in place."""
+        self.A = A.contiguous() if is_device(A) else dev(np.asarray(A, dtype=np.float64))
         s = _lib.stream_ptr()
         _lib.call("cf_lbs_vertex_transforms", self.A.data_ptr(), self.J, self.W.data_ptr(), self.V, self.T.data_ptr(),
                   self.Tinv.data_ptr(), s)
