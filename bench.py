@@ -31,13 +31,13 @@ UNIT = "samples/s"
 FLOP_PER_SAMPLE_HUMAN = 2 * (32 * 128 + 3 * 128 * 128 + 128 * 16) + 2 * (32 * 64 + 64 * 16) + 2 * (
     32 * 64 + 64 * 64 + 64 * 16)  # 131,072 (DeformNet + E_g + E_c, padded widths as issued)
 FLOP_PER_SAMPLE_OBJECT = 2 * (32 * 64 + 64 * 16) + 2 * (32 * 64 + 64 * 64 + 64 * 16)  # 20,480
-KERNELS_PER_STEP = 21  # see DESIGN.md §8 (12 per-frame setup + 9 render launches), checked against ncu
+KERNELS_PER_STEP = 17  # 7 per-frame setup + 10 render launches, checked against the ncu launch list
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--width", type=int, default=512)
@@ -97,7 +97,7 @@ def sum_over_ranks(pg, v: float) -> float:
 class ClockSampler:
     """nvidia-smi-equivalent clock / throttle sampling (NVML) during the timed region."""
 
-    def __init__(self, index=0, period=0.02):
+    def __init__(self, index=0, period=0.005):
         self.samples, self.reasons = [], set()
         self.period, self.index = period, index
         self._stop = threading.Event()

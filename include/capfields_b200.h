@@ -186,6 +186,7 @@ typedef struct cf_march_desc {
   cf_occ_grid object_grid;  /* object-local occupancy of the rigid object */
   double obj_R[9], obj_t[3]; /* object pose (object-to-world) */
   double obj_min[3], obj_inv_side; /* object unit-cube normalisation */
+  const int* human_cell_bbox;      /* device int[6] (lo xyz, hi xyz) of set live cells, or NULL */
 } cf_march_desc;
 
 /* compacted samples of one field: records (capacity) = ray << 8 | i, grouped
@@ -218,7 +219,25 @@ int cf_occ_box_shell(const cf_occ_grid* g, const double* half_extents, double sh
  * centre (node_buckets over the CANONICAL nodes), 3x3x3 live cells set */
 int cf_occ_splat(const uint32_t* canon_bits, const cf_occ_grid* cg, const cf_buckets_t* node_buckets,
                  const double* dqs, int k, double radius, const cf_occ_grid* lg, uint32_t* live_bits, void* stream);
-/* occupancy-skipped compaction of the samples of every ray (one or two fields) */
+/* once per sequence: the static part of the splat — every occupied canonical
+ * cell whose forward warp is valid, with its exact canonical k-NN (ties by
+ * index) and Gaussian weights (edgraph.canonical_blend_info, edgraph.py:186-195).
+ * cells (cap), nbr (cap*k), w (cap*k); count = cells written (device int). */
+int cf_occ_cache(const uint32_t* canon_bits, const cf_occ_grid* cg, const cf_buckets_t* node_buckets, int k,
+                 double radius, int64_t capacity, int* cells, int* nbr, double* w, int* count, void* stream);
+/* per frame, same live bits as cf_occ_splat from the cache: blend + apply the
+ * frame's dqs, set the centre cells in a 1-padded scratch grid
+ * ((res+2)^3/32 + 3 words), then a word-parallel 3x3x3 dilation; live_bbox (int[6],
+ * may be NULL) receives the cell bbox of the live set as cf_occ_bbox would */
+int cf_occ_splat_cached(const int* cells, const int* nbr, const double* w, const int* count, int64_t capacity, int k,
+                        const double* dqs, const cf_occ_grid* cg, const cf_occ_grid* lg, uint32_t* scratch_bits,
+                        uint32_t* live_bits, int* live_bbox, void* stream);
+/* bounding box (cell coords, int[6] lo xyz, hi xyz; lo > hi if empty) of the set cells */
+int cf_occ_bbox(const uint32_t* bits, const cf_occ_grid* g, int* bbox, void* stream);
+/* occupancy-skipped compaction of the samples of every ray (one or two fields);
+ * each ray only tests the samples inside its entry/exit interval of the
+ * occupied box (the live cell bbox, the object grid box), with a one-sample
+ * margin, so decisions equal a test of every sample */
 int cf_march(const cf_march_desc* M, const double* dirs, const uint32_t* human_bits, const uint32_t* object_bits,
              const cf_march_out* human, const cf_march_out* object, void* stream);
 /* human samples -> canonical unit cube (xu: float4 x,y,z,flag; flag 1 = ED, 2 = LBS, 0 = invalid) */

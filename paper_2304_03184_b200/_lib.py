@@ -62,7 +62,8 @@ class MarchDesc(ctypes.Structure):
     _fields_ = [("origin", ctypes.c_double * 3), ("n_rays", ctypes.c_int64), ("n_samples", ctypes.c_int),
                 ("t_near", ctypes.c_double), ("t_far", ctypes.c_double), ("dt", ctypes.c_double),
                 ("human_grid", OccGrid), ("object_grid", OccGrid), ("obj_R", ctypes.c_double * 9),
-                ("obj_t", ctypes.c_double * 3), ("obj_min", ctypes.c_double * 3), ("obj_inv_side", ctypes.c_double)]
+                ("obj_t", ctypes.c_double * 3), ("obj_min", ctypes.c_double * 3), ("obj_inv_side", ctypes.c_double),
+                ("human_cell_bbox", ctypes.c_void_p)]
 
 
 class MarchOut(ctypes.Structure):
@@ -112,6 +113,9 @@ _SIGS = {
     "cf_occ_box_shell": [_P(OccGrid), _p, _f64, _p, _p],
     "cf_occ_splat": [_p, _P(OccGrid), _p, _p, _i32, _f64, _P(OccGrid), _p, _p],
     "cf_march": [_P(MarchDesc), _p, _p, _p, _P(MarchOut), _P(MarchOut), _p],
+    "cf_occ_bbox": [_p, _P(OccGrid), _p, _p],
+    "cf_occ_cache": [_p, _P(OccGrid), _p, _i32, _f64, _i64, _p, _p, _p, _p, _p],
+    "cf_occ_splat_cached": [_p, _p, _p, _p, _i64, _i32, _p, _P(OccGrid), _P(OccGrid), _p, _p, _p, _p],
     "cf_human_canon": [_P(MarchDesc), _p, _P(MarchOut), _P(HumanWarp), _p, _p, _p, _p],
     "cf_object_canon": [_P(MarchDesc), _p, _P(MarchOut), _p, _p],
     "cf_composite": [_P(MarchDesc), _P(MarchOut), _p, ctypes.c_float, _p, _p, _p, _p],

@@ -24,7 +24,7 @@ __global__ void deform_nodes_kernel(const double* __restrict__ nodes, const doub
 
 // ------------------------------------------------------------------ buckets
 
-__global__ void bucket_params_kernel(const double* __restrict__ pts, int n, int G, BucketParams* P) {
+__device__ __forceinline__ void bucket_params_body(const double* __restrict__ pts, int n, int G, BucketParams* P) {
   __shared__ double smin[3][32], smax[3][32];
   double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
   for (int i = threadIdx.x; i < n; i += blockDim.x)
@@ -71,7 +71,7 @@ __global__ void bucket_params_kernel(const double* __restrict__ pts, int n, int 
   }
 }
 
-__global__ void bucket_count_kernel(const double* __restrict__ pts, int n, const BucketParams* __restrict__ Pp,
+__device__ __forceinline__ void bucket_count_body(const double* __restrict__ pts, int n, const BucketParams* __restrict__ Pp,
                                     int* __restrict__ counts, int* __restrict__ point_cell,
                                     int* __restrict__ point_slot) {
   const BucketParams P = *Pp;
@@ -85,47 +85,83 @@ __global__ void bucket_count_kernel(const double* __restrict__ pts, int n, const
 }
 
 // single-CTA exclusive scan, in place: counts[0..ncells] -> starts
-__global__ void bucket_scan_kernel(int* __restrict__ cells, const BucketParams* __restrict__ Pp) {
+__device__ __forceinline__ void bucket_scan_body(int* __restrict__ cells, const BucketParams* __restrict__ Pp) {
+  // each thread owns a contiguous chunk: serial sum, block scan of the chunk
+  // totals, serial write-back (2 barriers regardless of the cell count)
   __shared__ int warp_tot[32];
-  __shared__ int carry;
   const int ncells = Pp->g[0] * Pp->g[1] * Pp->g[2];
-  if (threadIdx.x == 0) carry = 0;
+  const int n = ncells + 1;
+  const int chunk = (n + blockDim.x - 1) / blockDim.x;
+  const int b = min(n, (int)threadIdx.x * chunk), e = min(n, b + chunk);
+  int v = 0;
+  for (int i = b; i < e; ++i) v += (i < ncells) ? cells[i] : 0;
+  int x = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if ((threadIdx.x & 31) >= o) x += y;
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 31) warp_tot[w] = x;
   __syncthreads();
-  for (int base = 0; base <= ncells; base += blockDim.x) {
-    const int i = base + threadIdx.x;
-    const int v = (i < ncells) ? cells[i] : 0;
-    int x = v;
+  if (w == 0) {
+    int t = (threadIdx.x < (blockDim.x >> 5)) ? warp_tot[threadIdx.x] : 0;
     for (int o = 1; o < 32; o <<= 1) {
-      int y = __shfl_up_sync(0xffffffffu, x, o);
-      if ((threadIdx.x & 31) >= o) x += y;
+      const int y = __shfl_up_sync(0xffffffffu, t, o);
+      if (threadIdx.x >= o) t += y;
     }
-    const int w = threadIdx.x >> 5;
-    if ((threadIdx.x & 31) == 31) warp_tot[w] = x;
-    __syncthreads();
-    if (w == 0) {
-      int t = (threadIdx.x < (blockDim.x >> 5)) ? warp_tot[threadIdx.x] : 0;
-      for (int o = 1; o < 32; o <<= 1) {
-        int y = __shfl_up_sync(0xffffffffu, t, o);
-        if (threadIdx.x >= o) t += y;
-      }
-      if (threadIdx.x < (blockDim.x >> 5)) warp_tot[threadIdx.x] = t;
-    }
-    __syncthreads();
-    const int excl = carry + (w > 0 ? warp_tot[w - 1] : 0) + x - v;
-    if (i <= ncells) cells[i] = excl;
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) carry = excl + v;
-    __syncthreads();
+    if (threadIdx.x < (blockDim.x >> 5)) warp_tot[threadIdx.x] = t;
+  }
+  __syncthreads();
+  int run = (w > 0 ? warp_tot[w - 1] : 0) + x - v;
+  for (int i = b; i < e; ++i) {
+    const int c = (i < ncells) ? cells[i] : 0;
+    cells[i] = run;
+    run += c;
   }
 }
 
-__global__ void bucket_scatter_kernel(const double* __restrict__ pts, int n, const int* __restrict__ cell_start,
+__device__ __forceinline__ void bucket_scatter_body(const double* __restrict__ pts, int n, const int* __restrict__ cell_start,
                                       const int* __restrict__ point_cell, const int* __restrict__ point_slot,
                                       double4* __restrict__ sorted) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int dst = cell_start[point_cell[i]] + point_slot[i];
     sorted[dst] = make_double4(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2], (double)i);
   }
+}
+
+__global__ void bucket_params_kernel(const double* __restrict__ pts, int n, int G, BucketParams* P) {
+  bucket_params_body(pts, n, G, P);
+}
+__global__ void bucket_count_kernel(const double* __restrict__ pts, int n, const BucketParams* __restrict__ Pp,
+                                    int* __restrict__ counts, int* __restrict__ point_cell,
+                                    int* __restrict__ point_slot) {
+  bucket_count_body(pts, n, Pp, counts, point_cell, point_slot);
+}
+__global__ void bucket_scan_kernel(int* __restrict__ cells, const BucketParams* __restrict__ Pp) {
+  bucket_scan_body(cells, Pp);
+}
+__global__ void bucket_scatter_kernel(const double* __restrict__ pts, int n, const int* __restrict__ cell_start,
+                                      const int* __restrict__ point_cell, const int* __restrict__ point_slot,
+                                      double4* __restrict__ sorted) {
+  bucket_scatter_body(pts, n, cell_start, point_cell, point_slot, sorted);
+}
+
+// the whole build in one CTA for small point sets (per-frame ED nodes / skin
+// vertices): one launch instead of four plus a memset
+__global__ void __launch_bounds__(1024) bucket_build_small_kernel(const double* __restrict__ pts, int n, int G,
+                                                                  BucketParams* P, int* __restrict__ cell_start,
+                                                                  int* __restrict__ point_cell,
+                                                                  int* __restrict__ point_slot,
+                                                                  double4* __restrict__ sorted) {
+  const int cells = G * G * G;
+  for (int i = threadIdx.x; i <= cells; i += blockDim.x) cell_start[i] = 0;
+  bucket_params_body(pts, n, G, P);
+  __syncthreads();
+  bucket_count_body(pts, n, P, cell_start, point_cell, point_slot);
+  __syncthreads();
+  bucket_scan_body(cell_start, P);
+  __syncthreads();
+  bucket_scatter_body(pts, n, cell_start, point_cell, point_slot, sorted);
 }
 
 // ------------------------------------------------------------------ k-NN + blend
@@ -248,6 +284,11 @@ int buckets_build(cf_buckets* b, const double* pts, int64_t n, int grid_res, cud
   G = std::max(1, std::min(G, b->max_grid_res));
   b->grid_res = G;
   const int64_t cells = (int64_t)G * G * G;
+  if (n <= 65536 && cells <= (1 << 18)) {
+    bucket_build_small_kernel<<<1, 1024, 0, st>>>(pts, (int)n, G, b->params, b->cell_start, b->point_cell,
+                                                  b->point_slot, b->sorted);
+    return check_launch("buckets_build");
+  }
   CF_CHECK_CUDA(cudaMemsetAsync(b->cell_start, 0, sizeof(int) * (cells + 1), st));
   bucket_params_kernel<<<1, 1024, 0, st>>>(pts, (int)n, G, b->params);
   bucket_count_kernel<<<grid_for(n, 256, 4), 256, 0, st>>>(pts, (int)n, b->params, b->cell_start, b->point_cell,

@@ -150,6 +150,236 @@ __global__ void __launch_bounds__(128) occ_splat_kernel(const uint32_t* __restri
   }
 }
 
+// Sample indices whose t lies in the ray's [t_enter, t_exit] through box
+// [lo, hi], widened by one sample on each side (a conservative superset: any
+// sample outside it is outside the box, hence in no set cell). i0 > i1 = none.
+__device__ __forceinline__ void sample_range(const cf_march_desc& M, d3 o, d3 d, const double* lo, const double* hi,
+                                             int& i0, int& i1) {
+  const double oq[3] = {o.x, o.y, o.z}, dq[3] = {d.x, d.y, d.z};
+  double t0 = -INFINITY, t1 = INFINITY;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if (fabs(dq[a]) < 1e-300) {
+      if (oq[a] < lo[a] || oq[a] > hi[a]) t0 = INFINITY;
+      continue;
+    }
+    const double inv = 1.0 / dq[a];
+    double ta = (lo[a] - oq[a]) * inv, tb = (hi[a] - oq[a]) * inv;
+    if (ta > tb) {
+      const double s = ta;
+      ta = tb;
+      tb = s;
+    }
+    t0 = fmax(t0, ta);
+    t1 = fmin(t1, tb);
+  }
+  if (!(t0 <= t1)) {
+    i0 = 1;
+    i1 = 0;
+    return;
+  }
+  const double f0 = floor((t0 - M.t_near) / M.dt - 0.5) - 1.0, f1 = ceil((t1 - M.t_near) / M.dt - 0.5) + 1.0;
+  i0 = (int)fmax(f0, 0.0);
+  i1 = (int)fmin(f1, (double)(M.n_samples - 1));
+}
+
+// Static part of the forward warp of the occupied canonical cells (once per
+// sequence): exact canonical k-NN and Gaussian weights, i.e. the reference's
+// canonical_blend_info (edgraph.py:186-195). Compacted (order irrelevant).
+template <int K>
+__global__ void __launch_bounds__(128) occ_cache_kernel(const uint32_t* __restrict__ cbits, cf_occ_grid cg,
+                                                        const BucketParams* __restrict__ Pp,
+                                                        const int* __restrict__ cell_start,
+                                                        const double4* __restrict__ sorted, int k, double r2,
+                                                        int64_t capacity, int* __restrict__ cell_out,
+                                                        int* __restrict__ nbr_out, double* __restrict__ w_out,
+                                                        int* __restrict__ count) {
+  __shared__ BucketParams sP;
+  if (threadIdx.x == 0) sP = *Pp;
+  __syncthreads();
+  const int64_t total = (int64_t)cg.res * cg.res * cg.res;
+  for (int64_t cell = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; cell < total;
+       cell += (int64_t)gridDim.x * blockDim.x) {
+    if (!((cbits[cell >> 5] >> (cell & 31)) & 1u)) continue;
+    TopK<K> top;
+    top.init(k);
+    bucket_knn<K>(sP, cell_start, sorted, cell_center(cg, cell), top);
+    double w[K];
+    bool valid = false;
+#pragma unroll
+    for (int j = 0; j < K; ++j)
+      if (j < k) {
+        w[j] = exp(x_div(-top.d[j], r2));
+        valid |= w[j] > 1e-6;
+      }
+    if (!valid) continue;  // forward warp invalid: the cell is never splatted
+    const int slot = atomicAdd(count, 1);
+    if (slot >= capacity) continue;
+    cell_out[slot] = (int)cell;
+#pragma unroll
+    for (int j = 0; j < K; ++j)
+      if (j < k) {
+        nbr_out[(int64_t)slot * k + j] = top.i[j];
+        w_out[(int64_t)slot * k + j] = w[j];
+      }
+  }
+}
+
+// per frame: blend the cached neighbours' dqs, apply, set the centre live cell
+template <int K>
+__global__ void occ_splat_cached_kernel(const int* __restrict__ cells, const int* __restrict__ nbr,
+                                        const double* __restrict__ w, const int* __restrict__ count,
+                                        int64_t capacity, int k, const double* __restrict__ dqs, cf_occ_grid cg,
+                                        cf_occ_grid lg, uint32_t* __restrict__ centre_bits, int* __restrict__ bbox) {
+  const int64_t n = min((int64_t)*count, capacity);
+  int lo[3] = {0x7fffffff, 0x7fffffff, 0x7fffffff}, hi[3] = {-0x7fffffff, -0x7fffffff, -0x7fffffff};
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
+    DqbAcc acc;
+#pragma unroll
+    for (int j = 0; j < K; ++j)
+      if (j < k) acc.add(w[s * k + j], load_dq(dqs + 8 * (int64_t)nbr[s * k + j]));
+    const d3 x = dq_apply(acc.result(), cell_center(cg, cells[s]));
+    const double q[3] = {x.x, x.y, x.z};
+    int64_t c[3];
+    bool ok = true;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double f = floor(x_div(x_sub(q[a], lg.min[a]), lg.cell));
+      ok &= (f >= -1.0) && (f <= (double)lg.res);
+      c[a] = ok ? (int64_t)f : 0;
+    }
+    if (!ok) continue;
+    // centre cell may lie one cell outside the grid: record it clamped into a
+    // 1-cell-padded index space so the dilation still reaches the border cells
+    const int64_t P = lg.res + 2;
+    const int64_t f = ((c[0] + 1) * P + (c[1] + 1)) * P + (c[2] + 1);
+    atomicOr(centre_bits + (f >> 5), 1u << (f & 31));
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = min(lo[a], (int)c[a]);
+      hi[a] = max(hi[a], (int)c[a]);
+    }
+  }
+  if (!bbox) return;
+  // centre bbox (warp-reduced); the dilate kernel widens it to the live-cell bbox
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    for (int o = 16; o > 0; o >>= 1) {
+      lo[a] = min(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+      hi[a] = max(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+    }
+    if ((threadIdx.x & 31) == 0 && lo[a] <= hi[a]) {
+      atomicMin(bbox + a, lo[a]);
+      atomicMax(bbox + 3 + a, hi[a]);
+    }
+  }
+}
+
+__device__ __forceinline__ uint64_t window64(const uint32_t* __restrict__ bits, int64_t start) {
+  const int64_t w = start >> 5;
+  const int sh = (int)(start & 31);
+  const uint64_t lo = (uint64_t)bits[w] | ((uint64_t)bits[w + 1] << 32);
+  const uint64_t hi = bits[w + 2];
+  return (lo >> sh) | (sh ? (hi << (64 - sh)) : 0ull);
+}
+
+// live = 3x3x3 dilation of the padded centre set, cropped to the grid
+__global__ void occ_dilate_kernel(const uint32_t* __restrict__ centre_bits, int res, uint32_t* __restrict__ live,
+                                  int* __restrict__ bbox) {
+  const int64_t r = res, P = r + 2, total = r * r * r;
+  const int64_t words = (total + 31) / 32;
+  if (bbox && blockIdx.x == 0 && threadIdx.x == 0) {
+    // centre bbox -> live-cell bbox of the 3x3x3 dilation cropped to the grid
+    for (int a = 0; a < 3; ++a) {
+      const int lo = bbox[a], hi = bbox[3 + a];
+      if (lo > hi) continue;
+      bbox[a] = max(lo - 1, 0);
+      bbox[3 + a] = min(hi + 1, res - 1);
+    }
+  }
+  if ((res & 31) == 0) {  // rows are whole words: 9 row windows of 34 bits per output word
+    const int64_t wpr = r / 32;
+    for (int64_t wi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; wi < words;
+         wi += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t row = wi / wpr, kb = wi % wpr, i = row / r, j = row % r;
+      uint64_t acc = 0;
+#pragma unroll
+      for (int di = 0; di < 3; ++di)
+#pragma unroll
+        for (int dj = 0; dj < 3; ++dj) {
+          const uint64_t win = window64(centre_bits, ((i + di) * P + (j + dj)) * P + kb * 32);
+          acc |= win | (win >> 1) | (win >> 2);
+        }
+      live[wi] = (uint32_t)acc;
+    }
+    return;
+  }
+  for (int64_t wi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; wi < words; wi += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t out = 0;
+    for (int b = 0; b < 32; ++b) {
+      const int64_t f = wi * 32 + b;
+      if (f >= total) break;
+      const int64_t i = f / (r * r) + 1, j = (f / r) % r + 1, kk = f % r + 1;
+      bool on = false;
+      for (int di = -1; di <= 1 && !on; ++di)
+        for (int dj = -1; dj <= 1 && !on; ++dj) {
+          const int64_t g = ((i + di) * P + (j + dj)) * P + kk;
+          // three consecutive k bits g-1, g, g+1
+          for (int dk = -1; dk <= 1; ++dk) {
+            const int64_t h = g + dk;
+            if ((centre_bits[h >> 5] >> (h & 31)) & 1u) {
+              on = true;
+              break;
+            }
+          }
+        }
+      if (on) out |= 1u << b;
+    }
+    live[wi] = out;
+  }
+}
+
+// bbox of the set cells, one CTA (block-reduced, no host init needed)
+__global__ void __launch_bounds__(1024) occ_bbox_kernel(const uint32_t* __restrict__ bits, cf_occ_grid g,
+                                                        int* __restrict__ bbox) {
+  __shared__ int s[6];
+  if (threadIdx.x < 3) {
+    s[threadIdx.x] = 0x7fffffff;
+    s[3 + threadIdx.x] = -1;
+  }
+  __syncthreads();
+  const int64_t r = g.res, total = r * r * r, words = (total + 31) / 32;
+  int lo[3] = {0x7fffffff, 0x7fffffff, 0x7fffffff}, hi[3] = {-1, -1, -1};
+  for (int64_t w = threadIdx.x; w < words; w += blockDim.x) {
+    uint32_t b = bits[w];
+    while (b) {
+      const int j = __ffs(b) - 1;
+      b &= b - 1;
+      const int64_t f = w * 32 + j;
+      if (f >= total) break;
+      const int c[3] = {(int)(f / (r * r)), (int)((f / r) % r), (int)(f % r)};
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        lo[a] = min(lo[a], c[a]);
+        hi[a] = max(hi[a], c[a]);
+      }
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    for (int o = 16; o > 0; o >>= 1) {
+      lo[a] = min(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+      hi[a] = max(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicMin(&s[a], lo[a]);
+      atomicMax(&s[3 + a], hi[a]);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 6) bbox[threadIdx.x] = s[threadIdx.x];
+}
+
 __device__ __forceinline__ int warp_excl_scan(int v, int& total) {
   int x = v;
 #pragma unroll
@@ -167,24 +397,50 @@ __global__ void __launch_bounds__(128) march_kernel(cf_march_desc M, const doubl
                                                     const uint32_t* __restrict__ obits, cf_march_out H,
                                                     cf_march_out O) {
   const d3 o{M.origin[0], M.origin[1], M.origin[2]};
+  // boxes that contain every set cell: the live cell bbox, the object grid
+  double hlo[3], hhi[3], olo[3], ohi[3];
+  bool hempty = false;
+  for (int a = 0; a < 3; ++a) {
+    int lo = 0, hi = M.human_grid.res - 1;
+    if (M.human_cell_bbox) {
+      lo = M.human_cell_bbox[a];
+      hi = M.human_cell_bbox[3 + a];
+    }
+    hempty |= lo > hi;
+    hlo[a] = M.human_grid.min[a] + lo * M.human_grid.cell;
+    hhi[a] = M.human_grid.min[a] + (hi + 1) * M.human_grid.cell;
+    olo[a] = M.object_grid.min[a];
+    ohi[a] = M.object_grid.min[a] + M.object_grid.res * M.object_grid.cell;
+  }
+  const d3 oo = to_object(M.obj_R, M.obj_t, o);
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < M.n_rays; base += (int64_t)gridDim.x * blockDim.x) {
     const int64_t ray = base + threadIdx.x;
     const bool live = ray < M.n_rays;
     const d3 d = live ? load_d3(dirs + 3 * ray) : d3{0.0, 0.0, 1.0};
     uint32_t hm[4] = {0, 0, 0, 0}, om[4] = {0, 0, 0, 0};  // occupancy masks of up to 128 samples
     int hc = 0, oc = 0;
-    if (live)
-      for (int i = 0; i < M.n_samples; ++i) {
-        const d3 p = sample_p(o, d, sample_t(M, i));
-        if (hbits && occ_test(M.human_grid, hbits, p)) {
+    if (live && hbits && !hempty) {
+      int i0, i1;
+      sample_range(M, o, d, hlo, hhi, i0, i1);
+      for (int i = i0; i <= i1; ++i)
+        if (occ_test(M.human_grid, hbits, sample_p(o, d, sample_t(M, i)))) {
           hm[i >> 5] |= 1u << (i & 31);
           ++hc;
         }
-        if (obits && occ_test(M.object_grid, obits, to_object(M.obj_R, M.obj_t, p))) {
+    }
+    if (live && obits) {
+      // the object box is clipped in object space: ray (R^T (o - t), R^T d)
+      const d3 od{d.x * M.obj_R[0] + d.y * M.obj_R[3] + d.z * M.obj_R[6],
+                  d.x * M.obj_R[1] + d.y * M.obj_R[4] + d.z * M.obj_R[7],
+                  d.x * M.obj_R[2] + d.y * M.obj_R[5] + d.z * M.obj_R[8]};
+      int i0, i1;
+      sample_range(M, oo, od, olo, ohi, i0, i1);
+      for (int i = i0; i <= i1; ++i)
+        if (occ_test(M.object_grid, obits, to_object(M.obj_R, M.obj_t, sample_p(o, d, sample_t(M, i))))) {
           om[i >> 5] |= 1u << (i & 31);
           ++oc;
         }
-      }
+    }
     for (int f = 0; f < 2; ++f) {
       const cf_march_out& out = f == 0 ? H : O;
       if (!out.records) continue;
@@ -373,6 +629,55 @@ int cf_occ_splat(const uint32_t* canon_bits, const cf_occ_grid* cg, const cf_buc
     occ_splat_kernel<8><<<grid, 128, 0, st>>>(canon_bits, *cg, node_buckets->params, node_buckets->cell_start,
                                               node_buckets->sorted, dqs, k, r2, *lg, live_bits);
   return cf::check_launch("cf_occ_splat");
+}
+
+int cf_occ_cache(const uint32_t* canon_bits, const cf_occ_grid* cg, const cf_buckets_t* node_buckets, int k,
+                 double radius, int64_t capacity, int* cells, int* nbr, double* w, int* count, void* stream) {
+  if (!canon_bits || !cg || !node_buckets || node_buckets->grid_res == 0 || k < 1 || k > 8 || !count)
+    return cf::fail(CF_E_BAD_ARG, "cf_occ_cache: bad args");
+  cudaStream_t st = cf::as_stream(stream);
+  CF_CHECK_CUDA(cudaMemsetAsync(count, 0, sizeof(int), st));
+  const int64_t total = (int64_t)cg->res * cg->res * cg->res;
+  const unsigned grid = cf::grid_for(total, 128, 8);
+  if (k <= 4)
+    occ_cache_kernel<4><<<grid, 128, 0, st>>>(canon_bits, *cg, node_buckets->params, node_buckets->cell_start,
+                                              node_buckets->sorted, k, radius * radius, capacity, cells, nbr, w,
+                                              count);
+  else
+    occ_cache_kernel<8><<<grid, 128, 0, st>>>(canon_bits, *cg, node_buckets->params, node_buckets->cell_start,
+                                              node_buckets->sorted, k, radius * radius, capacity, cells, nbr, w,
+                                              count);
+  return cf::check_launch("cf_occ_cache");
+}
+
+int cf_occ_splat_cached(const int* cells, const int* nbr, const double* w, const int* count, int64_t capacity, int k,
+                        const double* dqs, const cf_occ_grid* cg, const cf_occ_grid* lg, uint32_t* scratch_bits,
+                        uint32_t* live_bits, int* live_bbox, void* stream) {
+  if (!cells || !nbr || !w || !count || !dqs || !cg || !lg || !scratch_bits || !live_bits || k < 1 || k > 8)
+    return cf::fail(CF_E_BAD_ARG, "cf_occ_splat_cached: bad args");
+  cudaStream_t st = cf::as_stream(stream);
+  const int64_t P = lg->res + 2;
+  CF_CHECK_CUDA(cudaMemsetAsync(scratch_bits, 0, sizeof(uint32_t) * ((P * P * P + 31) / 32 + 3), st));
+  if (live_bbox) {  // lo = 0x7f7f7f7f, hi = 0x80808080 (negative)
+    CF_CHECK_CUDA(cudaMemsetAsync(live_bbox, 0x7f, 3 * sizeof(int), st));
+    CF_CHECK_CUDA(cudaMemsetAsync(live_bbox + 3, 0x80, 3 * sizeof(int), st));
+  }
+  const unsigned grid = cf::grid_for(capacity, 256, 4);
+  if (k <= 4)
+    occ_splat_cached_kernel<4><<<grid, 256, 0, st>>>(cells, nbr, w, count, capacity, k, dqs, *cg, *lg, scratch_bits,
+                                                     live_bbox);
+  else
+    occ_splat_cached_kernel<8><<<grid, 256, 0, st>>>(cells, nbr, w, count, capacity, k, dqs, *cg, *lg, scratch_bits,
+                                                     live_bbox);
+  const int64_t words = ((int64_t)lg->res * lg->res * lg->res + 31) / 32;
+  occ_dilate_kernel<<<cf::grid_for(words, 256, 8), 256, 0, st>>>(scratch_bits, lg->res, live_bits, live_bbox);
+  return cf::check_launch("cf_occ_splat_cached");
+}
+
+int cf_occ_bbox(const uint32_t* bits, const cf_occ_grid* g, int* bbox, void* stream) {
+  if (!bits || !g || !bbox || g->res < 1) return cf::fail(CF_E_BAD_ARG, "cf_occ_bbox: bad args");
+  occ_bbox_kernel<<<1, 1024, 0, cf::as_stream(stream)>>>(bits, *g, bbox);
+  return cf::check_launch("cf_occ_bbox");
 }
 
 int cf_march(const cf_march_desc* M, const double* dirs, const uint32_t* human_bits, const uint32_t* object_bits,

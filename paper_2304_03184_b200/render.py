@@ -123,6 +123,23 @@ class HumanField:
         _lib.call("cf_occ_from_points", tb.handle, _lib.byref(self.canon_occ), cfg.canon_occ_radius,
                   self.canon_bits.data_ptr(), _lib.stream_ptr())
         self._tb = tb
+        self.build_occ_cache()
+
+    def build_occ_cache(self) -> None:
+        """Static canonical k-NN of the occupied cells (re-run when canon_bits change)."""
+        cfg = self.cfg
+        n_on = int(torch.bitwise_count(self.canon_bits).sum()) if hasattr(torch, "bitwise_count") else \
+            int(np.unpackbits(self.canon_bits.cpu().numpy().view(np.uint8)).sum())
+        cap = max(n_on, 1)
+        d = self.nodes.device
+        self.occ_cells = torch.empty(cap, dtype=torch.int32, device=d)
+        self.occ_nbr = torch.empty((cap, cfg.ed_k), dtype=torch.int32, device=d)
+        self.occ_w = torch.empty((cap, cfg.ed_k), dtype=torch.float64, device=d)
+        self.occ_count = torch.zeros(1, dtype=torch.int32, device=d)
+        self.occ_cap = cap
+        _lib.call("cf_occ_cache", self.canon_bits.data_ptr(), _lib.byref(self.canon_occ), self.node_buckets.handle,
+                  cfg.ed_k, cfg.ed_radius, cap, self.occ_cells.data_ptr(), self.occ_nbr.data_ptr(),
+                  self.occ_w.data_ptr(), self.occ_count.data_ptr(), _lib.stream_ptr())
 
     def desc(self, dbias: torch.Tensor) -> _lib.FieldDesc:
         d = _lib.FieldDesc()
@@ -208,6 +225,10 @@ class Renderer:
         self.M.t_near, self.M.t_far = cfg.t_near, cfg.t_far
         self.M.dt = (cfg.t_far - cfg.t_near) / cfg.n_samples
         self.M.human_grid = self.live_occ
+        self.live_bbox = torch.zeros(6, dtype=torch.int32, device=d)
+        P = cfg.live_occ_res + 2
+        self.live_scratch = torch.zeros((P ** 3 + 31) // 32 + 3, dtype=torch.int32, device=d)
+        self.M.human_cell_bbox = self.live_bbox.data_ptr()
         if obj:
             self.M.object_grid = obj.occ
             for a in range(3):
@@ -247,9 +268,11 @@ class Renderer:
         _lib.call("cf_deform_nodes", h.nodes.data_ptr(), self._dqs.data_ptr(), n, self._anchors.data_ptr(), s)
         self._anchor_buckets.build(self._anchors)
         h.lbs.set_pose(self._A)
-        _lib.call("cf_occ_splat", h.canon_bits.data_ptr(), _lib.byref(h.canon_occ), h.node_buckets.handle,
-                  self._dqs.data_ptr(), self.cfg.ed_k, self.cfg.ed_radius, _lib.byref(self.live_occ),
-                  self.live_bits.data_ptr(), s)
+        _lib.call("cf_occ_splat_cached", h.occ_cells.data_ptr(), h.occ_nbr.data_ptr(), h.occ_w.data_ptr(),
+                  h.occ_count.data_ptr(), h.occ_cap, self.cfg.ed_k, self._dqs.data_ptr(), _lib.byref(h.canon_occ),
+                  _lib.byref(self.live_occ), self.live_scratch.data_ptr(), self.live_bits.data_ptr(),
+                  self.live_bbox.data_ptr(), s)
+        self._mark("frame_setup")
         if getattr(self, "hw", None) is None:
             w = _lib.HumanWarp()
             w.dqs = self._dqs.data_ptr()

@@ -72,6 +72,9 @@ def test_occupancy_bits_bitexact(setup):
     live = orr.occ_splat(got, (list(g.min), g.cell, g.res), sc.nodes, sc.node_dqs(fid), cfg.ed_k, cfg.ed_radius,
                          (list(lg.min), lg.cell, lg.res))
     assert np.array_equal(orr.unpack_bits(words(r.live_bits), lg.res ** 3), live)
+    f = np.nonzero(live)[0]
+    ijk = np.stack([f // lg.res ** 2, (f // lg.res) % lg.res, f % lg.res], -1)
+    assert list(r.live_bbox.cpu().numpy()) == list(ijk.min(0)) + list(ijk.max(0))
 
 
 def test_march_sets_bitexact(setup):
