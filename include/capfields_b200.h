@@ -267,9 +267,12 @@ typedef struct cf_field_desc {
   float delta_scale;        /* |dv| bound, metres (0.05) */
   float inv_side;           /* metres -> unit cube */
 } cf_field_desc;
-/* out: float4 (sigma, r, g, b) per compacted sample of S (count read on device) */
+/* device scratch needed by cf_field_forward for `capacity` samples */
+int cf_field_scratch_bytes(const cf_field_desc* F, int64_t capacity, int64_t* bytes);
+/* out: float4 (sigma, r, g, b) per compacted sample of S (count read on device).
+ * Stages: hash (fp16 features) [-> DeformNet -> hash] -> E_g/E_c, see field.cu */
 int cf_field_forward(const cf_field_desc* F, const cf_march_out* S, const double* dirs, const float* xu, float* out,
-                     void* stream);
+                     void* scratch, void* stream);
 
 #ifdef __cplusplus
 }

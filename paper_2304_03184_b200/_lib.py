@@ -120,7 +120,8 @@ _SIGS = {
     "cf_object_canon": [_P(MarchDesc), _p, _P(MarchOut), _p, _p],
     "cf_composite": [_P(MarchDesc), _P(MarchOut), _p, ctypes.c_float, _p, _p, _p, _p],
     "cf_composite_layers": [_i64, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p],
-    "cf_field_forward": [_P(FieldDesc), _P(MarchOut), _p, _p, _p, _p],
+    "cf_field_forward": [_P(FieldDesc), _P(MarchOut), _p, _p, _p, _p, _p],
+    "cf_field_scratch_bytes": [_P(FieldDesc), _i64, _P(_i64)],
 }
 
 _lock = threading.Lock()

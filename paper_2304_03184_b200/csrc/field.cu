@@ -1,31 +1,126 @@
-// Fused radiance-field evaluation of compacted samples, one persistent CTA per
-// SM, two 128-sample slots (4 warps each). Per slot and tile, everything stays
-// on chip: hash-grid gathers (CUDA cores, L2-resident tables) write fp16
-// features straight into the UMMA A-operand buffer in shared memory, each MLP
-// layer is a chain of tcgen05.mma (M=128, N<=128, K=16 steps) accumulating in
-// TMEM, and the epilogue (TMEM -> registers -> bias/ReLU -> fp16 -> smem) feeds
-// the next layer. Weights of all networks (128 KB fp16) are loaded into smem
-// once per CTA.
+// Radiance-field evaluation of compacted samples, as a chain of
+// stage kernels sized for what bounds each stage on B200:
 //
-// Human field:
-//   x   = canonicalised sample (unit cube), from cf_human_canon
-//   dv  = 0.05 * tanh(DeformNet(hash_d(x)))          32 -> 128 x4 -> 3 (theta folded in layer-1 bias)
-//   xc  = x + dv / side
-//   g   = E_g(hash_c(xc))                             32 -> 64 -> 16 ; sigma = exp(g0), geo = g1..15
-//   rgb = sigmoid(E_c([geo, SH4(dir)]))               32 -> 64 -> 64 -> 3
-// Object field: the same without the deformation stage.
+//   hash_f16_kernel   CUDA cores, L2 gathers. Thread per sample at full
+//                     occupancy (latency hiding needs many warps; ncu showed
+//                     the fused variant stalled 55% on long-scoreboard gathers
+//                     with 8 warps/SM); 8*CH corner loads in flight per thread.
+//                     Writes 32 fp16 features (64 B) per sample.
+//   deform_mlp_kernel tcgen05: DeformNet 32->128x4->3 (theta folded into the
+//                     layer-1 bias), 3 slots x 128 samples per persistent CTA,
+//                     weights (108 KB fp16) resident in smem, accumulators in
+//                     TMEM. Epilogue: dv = 0.05 tanh(.), xc = x + dv / side.
+//   color_mlp_kernel  tcgen05: E_g 32->64->16 (sigma = exp, 15 geo) and
+//                     E_c [geo, SH4(dir)] 32->64->64->3 (sigmoid), 4 slots.
+//
+// Human:  hash_d(xu) -> deform_mlp -> hash_c(xc) -> color_mlp
+// Object: hash_c(xu) -> color_mlp
+// Between stages only 64 B/sample (features) or 16 B/sample (xc) touch HBM.
 #include "common.cuh"
 #include "tc.cuh"
 
 namespace {
 
 constexpr int kSlotThreads = 128;
-constexpr int kSlots = 2;
-constexpr int kABytes = 128 * 128 * 2;  // A buffer per slot (K <= 128)
+
+// ------------------------------------------------------------------ hash stage
+
+// Hash features of L levels, CH levels at a time: all 8*CH corner gathers of a
+// chunk are issued before any is consumed. Same arithmetic as hashgrid.cu.
+template <int F, int L, int CH>
+__device__ __forceinline__ void hash_features(const cf_hashgrid_desc& D, const float* __restrict__ table, float x,
+                                              float y, float z, float* feat) {
+  static_assert(L % CH == 0, "chunk must divide the level count");
+  x = fminf(fmaxf(x, 0.0f), 1.0f);
+  y = fminf(fmaxf(y, 0.0f), 1.0f);
+  z = fminf(fmaxf(z, 0.0f), 1.0f);
+  const uint32_t mask = (1u << D.log2_table) - 1u;
+#pragma unroll
+  for (int l0 = 0; l0 < L; l0 += CH) {
+    float t[CH][8][F];
+    float w[CH][8];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      const int l = l0 + c;
+      const int N = D.resolution[l];
+      const float s = (float)N;
+      const float pos[3] = {f_mul(x, s), f_mul(y, s), f_mul(z, s)};
+      uint32_t g[3];
+      float fr[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        int gi = (int)floorf(pos[a]);
+        gi = gi > N - 1 ? N - 1 : gi;
+        g[a] = (uint32_t)gi;
+        fr[a] = f_sub(pos[a], (float)gi);
+      }
+      const uint32_t stride = (uint32_t)N + 1u;
+      const bool dense = D.dense[l] != 0;
+      const float* base = table + D.offset[l] * F;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t cx = g[0] + (k & 1), cy = g[1] + ((k >> 1) & 1), cz = g[2] + ((k >> 2) & 1);
+        const uint32_t idx = dense ? (cx + cy * stride + cz * stride * stride)
+                                   : ((cx ^ (cy * 2654435761u) ^ (cz * 805459861u)) & mask);
+        if constexpr (F == 2) {
+          const float2 v = __ldg(reinterpret_cast<const float2*>(base) + idx);
+          t[c][k][0] = v.x;
+          t[c][k][1] = v.y;
+        } else {
+          const float4 v = __ldg(reinterpret_cast<const float4*>(base) + idx);
+          t[c][k][0] = v.x;
+          t[c][k][1] = v.y;
+          t[c][k][2] = v.z;
+          t[c][k][3] = v.w;
+        }
+        const float wx = (k & 1) ? fr[0] : f_sub(1.0f, fr[0]);
+        const float wy = (k & 2) ? fr[1] : f_sub(1.0f, fr[1]);
+        const float wz = (k & 4) ? fr[2] : f_sub(1.0f, fr[2]);
+        w[c][k] = f_mul(f_mul(wx, wy), wz);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+#pragma unroll
+      for (int f = 0; f < F; ++f) {
+        float acc = f_mul(w[c][0], t[c][0][f]);
+#pragma unroll
+        for (int k = 1; k < 8; ++k) acc = f_add(acc, f_mul(w[c][k], t[c][k][f]));
+        feat[(l0 + c) * F + f] = acc;
+      }
+  }
+}
+
+// 32 features of a valid sample (flag > 0) -> fp16 row; invalid -> zeros
+template <int F, int L, int CH>
+__global__ void __launch_bounds__(128) hash_f16_kernel(cf_hashgrid_desc D, const float* __restrict__ table,
+                                                       const float4* __restrict__ x, const int* __restrict__ count,
+                                                       int64_t capacity, uint4* __restrict__ out) {
+  const int64_t n = min((int64_t)*count, capacity);
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
+    const float4 p = x[s];
+    float feat[32];
+    if (p.w > 0.0f) {
+      hash_features<F, L, CH>(D, table, p.x, p.y, p.z, feat);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) feat[i] = 0.0f;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      __half2 h[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) h[i] = __floats2half2_rn(feat[8 * q + 2 * i], feat[8 * q + 2 * i + 1]);
+      out[s * 4 + q] = *reinterpret_cast<uint4*>(h);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ MLP slots
 
 struct Slot {
   uint8_t* abuf;
-  uint8_t* w_s;
+  const uint8_t* w_s;
   uint64_t* bar;
   uint32_t tmem;      // slot column base (lane 0)
   uint32_t tmem_row;  // + this warp's lane quarter
@@ -49,73 +144,110 @@ __device__ __forceinline__ void run_layer(Slot& S, int w_off, int K, int N) {
 }
 
 // hidden-layer epilogue: (+bias) ReLU -> fp16 -> A buffer with K = N
-__device__ __forceinline__ void relu_to_abuf(Slot& S, int N, const float* bias) {
-  for (int c0 = 0; c0 < N; c0 += 16) {
-    float v[16];
-    tc::tmem_ld16(S.tmem_row + (uint32_t)c0, v);
+template <int N>
+__device__ __forceinline__ void relu_to_abuf(Slot& S, const float* bias) {
 #pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = fmaxf(bias ? v[i] + bias[c0 + i] : v[i], 0.0f);
-    tc::st_row8(S.abuf, S.r, c0, N, v);
-    tc::st_row8(S.abuf, S.r, c0 + 8, N, v + 8);
+  for (int c0 = 0; c0 < N; c0 += 32) {
+    float v[32];
+    tc::tmem_ld32(S.tmem_row + (uint32_t)c0, v);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = fmaxf(bias ? v[i] + bias[c0 + i] : v[i], 0.0f);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) tc::st_row8(S.abuf, S.r, c0 + 8 * q, N, v + 8 * q);
   }
 }
 
-template <int F>
-__device__ __forceinline__ void hash_features(const cf_hashgrid_desc& D, const float* __restrict__ table, float x,
-                                              float y, float z, float* feat) {
-  x = fminf(fmaxf(x, 0.0f), 1.0f);
-  y = fminf(fmaxf(y, 0.0f), 1.0f);
-  z = fminf(fmaxf(z, 0.0f), 1.0f);
-  const uint32_t mask = (1u << D.log2_table) - 1u;
-#pragma unroll 1
-  for (int l = 0; l < D.n_levels; ++l) {
-    const int N = D.resolution[l];
-    const float s = (float)N;
-    const float pos[3] = {f_mul(x, s), f_mul(y, s), f_mul(z, s)};
-    uint32_t g[3];
-    float fr[3];
+// copy one 64-byte fp16 feature row into the A buffer (K = 32)
+__device__ __forceinline__ void row_to_abuf(Slot& S, const uint4* __restrict__ feat, int64_t s, bool live) {
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      int gi = (int)floorf(pos[a]);
-      gi = gi > N - 1 ? N - 1 : gi;
-      g[a] = (uint32_t)gi;
-      fr[a] = f_sub(pos[a], (float)gi);
-    }
-    const uint32_t stride = (uint32_t)N + 1u;
-    const bool dense = D.dense[l] != 0;
-    const float* base = table + D.offset[l] * F;
-    float t[8][F];
-    float w[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const uint32_t cx = g[0] + (k & 1), cy = g[1] + ((k >> 1) & 1), cz = g[2] + ((k >> 2) & 1);
-      const uint32_t idx =
-          dense ? (cx + cy * stride + cz * stride * stride) : ((cx ^ (cy * 2654435761u) ^ (cz * 805459861u)) & mask);
-      if constexpr (F == 2) {
-        const float2 v = __ldg(reinterpret_cast<const float2*>(base) + idx);
-        t[k][0] = v.x;
-        t[k][1] = v.y;
-      } else {
-        const float4 v = __ldg(reinterpret_cast<const float4*>(base) + idx);
-        t[k][0] = v.x;
-        t[k][1] = v.y;
-        t[k][2] = v.z;
-        t[k][3] = v.w;
-      }
-      const float wx = (k & 1) ? fr[0] : f_sub(1.0f, fr[0]);
-      const float wy = (k & 2) ? fr[1] : f_sub(1.0f, fr[1]);
-      const float wz = (k & 4) ? fr[2] : f_sub(1.0f, fr[2]);
-      w[k] = f_mul(f_mul(wx, wy), wz);
-    }
-#pragma unroll
-    for (int f = 0; f < F; ++f) {
-      float acc = f_mul(w[0], t[0][f]);
-#pragma unroll
-      for (int k = 1; k < 8; ++k) acc = f_add(acc, f_mul(w[k], t[k][f]));
-      feat[l * F + f] = acc;
-    }
+  for (int q = 0; q < 4; ++q) {
+    const uint4 v = live ? feat[s * 4 + q] : make_uint4(0, 0, 0, 0);
+    *reinterpret_cast<uint4*>(S.abuf + tc::core_offset(S.r, 8 * q, 32)) = v;
   }
 }
+
+template <int SLOTS, int TMEM_COLS>
+__device__ __forceinline__ void slots_setup(const uint8_t* __restrict__ wblob, int w_bytes, uint8_t* smem,
+                                            uint64_t* mbar, uint32_t* tmem_base) {
+  const int tid = threadIdx.x, warp = tid / 32;
+  for (int i = tid * 16; i < w_bytes; i += blockDim.x * 16)
+    *reinterpret_cast<uint4*>(smem + i) = *reinterpret_cast<const uint4*>(wblob + i);
+  if (tid == 0) {
+    for (int s = 0; s < SLOTS; ++s) tc::bar_init(&mbar[s], 1);
+    tc::bar_fence_init();
+  }
+  if (warp == 0) tc::tmem_alloc<TMEM_COLS>(tmem_base);
+  tc::fence_async_smem();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+}
+
+template <int SLOTS, int COLS, int ABYTES>
+__device__ __forceinline__ Slot make_slot(uint8_t* smem, int w_bytes, uint64_t* mbar, uint32_t tmem_base) {
+  Slot S;
+  const int tid = threadIdx.x;
+  S.slot = tid / kSlotThreads;
+  S.r = tid % kSlotThreads;
+  S.w_s = smem;
+  S.abuf = smem + ((w_bytes + 1023) / 1024) * 1024 + S.slot * ABYTES;
+  S.bar = &mbar[S.slot];
+  S.tmem = tmem_base + (uint32_t)(S.slot * COLS);
+  S.tmem_row = S.tmem + ((uint32_t)(((tid / 32) % 4) * 32) << 16);
+  S.phase = 0;
+  return S;
+}
+
+// ---------------------------------------------------------------- DeformNet
+
+constexpr int kDeformSlots = 3;
+constexpr int kDeformA = 128 * 128 * 2;
+constexpr int kDeformW = (128 * 32 + 3 * 128 * 128 + 16 * 128) * 2;  // 110,592 B
+
+__global__ void __launch_bounds__(kDeformSlots* kSlotThreads, 1)
+    deform_mlp_kernel(const uint8_t* __restrict__ wblob, const float* __restrict__ bias1, float delta_scale,
+                      float inv_side, const float4* __restrict__ xu, const uint4* __restrict__ dfeat,
+                      const int* __restrict__ count, int64_t capacity, float4* __restrict__ xc) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t mbar[kDeformSlots];
+  __shared__ uint32_t tmem_base;
+  slots_setup<kDeformSlots, 512>(wblob, kDeformW, smem, mbar, &tmem_base);
+  Slot S = make_slot<kDeformSlots, 128, kDeformA>(smem, kDeformW, mbar, tmem_base);
+  constexpr int o1 = 0, o2 = 128 * 32 * 2, o3 = o2 + 128 * 128 * 2, o4 = o3 + 128 * 128 * 2, o5 = o4 + 128 * 128 * 2;
+  const int64_t n = min((int64_t)*count, capacity);
+  const int64_t n_tiles = (n + 127) / 128;
+  for (int64_t tile = (int64_t)blockIdx.x * kDeformSlots + S.slot; tile < n_tiles;
+       tile += (int64_t)gridDim.x * kDeformSlots) {
+    const int64_t s = tile * 128 + S.r;
+    const bool live = s < n;
+    row_to_abuf(S, dfeat, s, live);
+    run_layer(S, o1, 32, 128);
+    relu_to_abuf<128>(S, bias1);
+    run_layer(S, o2, 128, 128);
+    relu_to_abuf<128>(S, nullptr);
+    run_layer(S, o3, 128, 128);
+    relu_to_abuf<128>(S, nullptr);
+    run_layer(S, o4, 128, 128);
+    relu_to_abuf<128>(S, nullptr);
+    run_layer(S, o5, 128, 16);
+    float v[16];
+    tc::tmem_ld16(S.tmem_row, v);
+    if (live) {
+      float4 p = xu[s];
+      if (p.w > 0.0f) {
+        p.x = f_add(p.x, f_mul(delta_scale * tanhf(v[0]), inv_side));
+        p.y = f_add(p.y, f_mul(delta_scale * tanhf(v[1]), inv_side));
+        p.z = f_add(p.z, f_mul(delta_scale * tanhf(v[2]), inv_side));
+      }
+      xc[s] = p;
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (threadIdx.x / 32 == 0) tc::tmem_free<512>(tmem_base);
+}
+
+// ---------------------------------------------------------------- E_g / E_c
 
 // real spherical harmonics up to degree 3 (16 coefficients), unit direction
 __device__ __forceinline__ void sh16(float x, float y, float z, float* o) {
@@ -138,79 +270,33 @@ __device__ __forceinline__ void sh16(float x, float y, float z, float* o) {
   o[15] = 0.59004358992664352f * x * (-xx + 3.0f * yy);
 }
 
-struct Offsets {
-  int d[5], g[2], c[3];
-};
+constexpr int kColorSlots = 4;
+constexpr int kColorA = 128 * 64 * 2;
+constexpr int kColorW = (64 * 32 + 16 * 64 + 64 * 32 + 64 * 64 + 16 * 64) * 2;  // 20,480 B
 
-__global__ void __launch_bounds__(kSlots* kSlotThreads, 1)
-    field_kernel(cf_field_desc FD, Offsets W, const double* __restrict__ dirs, const uint32_t* __restrict__ records,
-                 const int* __restrict__ count, int64_t capacity, const float4* __restrict__ xu,
-                 float4* __restrict__ out) {
+__global__ void __launch_bounds__(kColorSlots* kSlotThreads, 1)
+    color_mlp_kernel(const uint8_t* __restrict__ wblob, const float4* __restrict__ xu, const uint4* __restrict__ cfeat,
+                     const uint32_t* __restrict__ records, const double* __restrict__ dirs,
+                     const int* __restrict__ count, int64_t capacity, float4* __restrict__ out) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t mbar[kSlots];
+  __shared__ uint64_t mbar[kColorSlots];
   __shared__ uint32_t tmem_base;
-  const int tid = threadIdx.x, warp = tid / 32;
-  for (int i = tid * 16; i < FD.w_bytes; i += blockDim.x * 16)
-    *reinterpret_cast<uint4*>(smem + i) = *reinterpret_cast<const uint4*>(FD.wblob + i);
-  if (tid == 0) {
-    for (int s = 0; s < kSlots; ++s) tc::bar_init(&mbar[s], 1);
-    tc::bar_fence_init();
-  }
-  if (warp == 0) tc::tmem_alloc<kSlots * 128>(&tmem_base);
-  tc::fence_async_smem();
-  tc::fence_before();
-  __syncthreads();
-  tc::fence_after();
-
-  Slot S;
-  S.slot = tid / kSlotThreads;
-  S.r = tid % kSlotThreads;
-  S.w_s = smem;
-  S.abuf = smem + ((FD.w_bytes + 1023) / 1024) * 1024 + S.slot * kABytes;
-  S.bar = &mbar[S.slot];
-  S.tmem = tmem_base + (uint32_t)(S.slot * 128);
-  S.tmem_row = S.tmem + ((uint32_t)((warp % 4) * 32) << 16);
-  S.phase = 0;
-
+  slots_setup<kColorSlots, 256>(wblob, kColorW, smem, mbar, &tmem_base);
+  Slot S = make_slot<kColorSlots, 64, kColorA>(smem, kColorW, mbar, tmem_base);
+  constexpr int g1 = 0, g2 = 64 * 32 * 2, c1 = g2 + 16 * 64 * 2, c2 = c1 + 64 * 32 * 2, c3 = c2 + 64 * 64 * 2;
   const int64_t n = min((int64_t)*count, capacity);
   const int64_t n_tiles = (n + 127) / 128;
-  for (int64_t tile = (int64_t)blockIdx.x * kSlots + S.slot; tile < n_tiles; tile += (int64_t)gridDim.x * kSlots) {
+  for (int64_t tile = (int64_t)blockIdx.x * kColorSlots + S.slot; tile < n_tiles;
+       tile += (int64_t)gridDim.x * kColorSlots) {
     const int64_t s = tile * 128 + S.r;
     const bool live = s < n;
-    float4 x = live ? xu[s] : make_float4(0.f, 0.f, 0.f, 0.f);
-    const bool valid = live && x.w > 0.0f;
-    float feat[32];
-    if (FD.has_deform) {
-      if (valid) hash_features<4>(FD.dgrid, FD.dtable, x.x, x.y, x.z, feat);
-#pragma unroll
-      for (int i = 0; i < 32; ++i)
-        if (!valid) feat[i] = 0.0f;
-#pragma unroll
-      for (int k0 = 0; k0 < 32; k0 += 8) tc::st_row8(S.abuf, S.r, k0, 32, feat + k0);
-      run_layer(S, W.d[0], 32, 128);
-      relu_to_abuf(S, 128, FD.dbias);
-      for (int l = 1; l < 4; ++l) {
-        run_layer(S, W.d[l], 128, 128);
-        relu_to_abuf(S, 128, nullptr);
-      }
-      run_layer(S, W.d[4], 128, 16);
-      float v[16];
-      tc::tmem_ld16(S.tmem_row, v);
-      x.x = f_add(x.x, f_mul(FD.delta_scale * tanhf(v[0]), FD.inv_side));
-      x.y = f_add(x.y, f_mul(FD.delta_scale * tanhf(v[1]), FD.inv_side));
-      x.z = f_add(x.z, f_mul(FD.delta_scale * tanhf(v[2]), FD.inv_side));
-    }
-    if (valid) hash_features<2>(FD.cgrid, FD.ctable, x.x, x.y, x.z, feat);
-#pragma unroll
-    for (int i = 0; i < 32; ++i)
-      if (!valid) feat[i] = 0.0f;
-#pragma unroll
-    for (int k0 = 0; k0 < 32; k0 += 8) tc::st_row8(S.abuf, S.r, k0, 32, feat + k0);
-    run_layer(S, W.g[0], 32, 64);
-    relu_to_abuf(S, 64, nullptr);
-    run_layer(S, W.g[1], 64, 16);
+    row_to_abuf(S, cfeat, s, live);
+    run_layer(S, g1, 32, 64);
+    relu_to_abuf<64>(S, nullptr);
+    run_layer(S, g2, 64, 16);
     float gv[16];
     tc::tmem_ld16(S.tmem_row, gv);
+    const bool valid = live && xu[s].w > 0.0f;
     const float sigma = valid ? expf(gv[0]) : 0.0f;
     // colour input: [geo(15), SH4(dir)(16), 0]
     float cin[32];
@@ -227,11 +313,11 @@ __global__ void __launch_bounds__(kSlots* kSlotThreads, 1)
     cin[31] = 0.0f;
 #pragma unroll
     for (int k0 = 0; k0 < 32; k0 += 8) tc::st_row8(S.abuf, S.r, k0, 32, cin + k0);
-    run_layer(S, W.c[0], 32, 64);
-    relu_to_abuf(S, 64, nullptr);
-    run_layer(S, W.c[1], 64, 64);
-    relu_to_abuf(S, 64, nullptr);
-    run_layer(S, W.c[2], 64, 16);
+    run_layer(S, c1, 32, 64);
+    relu_to_abuf<64>(S, nullptr);
+    run_layer(S, c2, 64, 64);
+    relu_to_abuf<64>(S, nullptr);
+    run_layer(S, c3, 64, 16);
     float cv[16];
     tc::tmem_ld16(S.tmem_row, cv);
     if (live) {
@@ -242,47 +328,60 @@ __global__ void __launch_bounds__(kSlots* kSlotThreads, 1)
   }
   tc::fence_before();
   __syncthreads();
-  if (warp == 0) tc::tmem_free<kSlots * 128>(tmem_base);
+  if (threadIdx.x / 32 == 0) tc::tmem_free<256>(tmem_base);
+}
+
+unsigned persistent_grid(int64_t capacity, int slots) {
+  const int64_t tiles = (capacity + 127) / 128;
+  int64_t g = (tiles + slots - 1) / slots;
+  if (g > cf::sm_count()) g = cf::sm_count();
+  return (unsigned)(g < 1 ? 1 : g);
 }
 
 }  // namespace
 
 extern "C" {
 
-int cf_field_forward(const cf_field_desc* FD, const cf_march_out* S, const double* dirs, const float* xu,
-                     float* out, void* stream) {
-  if (!FD || !S || !FD->wblob || !FD->ctable || (FD->has_deform && (!FD->dtable || !FD->dbias)))
+int cf_field_scratch_bytes(const cf_field_desc* FD, int64_t capacity, int64_t* bytes) {
+  if (!FD || !bytes || capacity < 0) return cf::fail(CF_E_BAD_ARG, "cf_field_scratch_bytes: bad args");
+  // cfeat (64 B) [+ dfeat (64 B) + xc (16 B)] per sample
+  *bytes = capacity * (64 + (FD->has_deform ? 64 + 16 : 0));
+  return CF_OK;
+}
+
+int cf_field_forward(const cf_field_desc* FD, const cf_march_out* S, const double* dirs, const float* xu_f,
+                     float* out_f, void* scratch, void* stream) {
+  if (!FD || !S || !FD->wblob || !FD->ctable || !scratch || (FD->has_deform && (!FD->dtable || !FD->dbias)))
     return cf::fail(CF_E_BAD_ARG, "cf_field_forward: bad args");
-  if (FD->cgrid.n_levels * FD->cgrid.n_features != 32 || FD->cgrid.n_features != 2 ||
-      (FD->has_deform && (FD->dgrid.n_levels * FD->dgrid.n_features != 32 || FD->dgrid.n_features != 4)))
-    return cf::fail(CF_E_BAD_ARG, "cf_field_forward: grids must encode to 32 features (F=2 canonical, F=4 deform)");
-  Offsets W{};
-  int off = 0;
-  auto take = [&](int n, int k) {
-    const int o = off;
-    off += n * k * 2;
-    return o;
-  };
+  if (FD->cgrid.n_levels != 16 || FD->cgrid.n_features != 2 ||
+      (FD->has_deform && (FD->dgrid.n_levels != 8 || FD->dgrid.n_features != 4)))
+    return cf::fail(CF_E_BAD_ARG, "cf_field_forward: grids must be 16x F2 (canonical) and 8x F4 (deform)");
+  if (FD->w_bytes != (FD->has_deform ? kDeformW : 0) + kColorW)
+    return cf::fail(CF_E_BAD_ARG, "cf_field_forward: weight blob size mismatch");
+  cudaStream_t st = cf::as_stream(stream);
+  const int64_t cap = S->capacity;
+  if (cap == 0) return CF_OK;
+  const float4* xu = reinterpret_cast<const float4*>(xu_f);
+  float4* out = reinterpret_cast<float4*>(out_f);
+  uint4* cfeat = reinterpret_cast<uint4*>(scratch);
+  const float4* xcan = xu;
+  const unsigned hgrid = cf::grid_for(cap, 128, 16);
   if (FD->has_deform) {
-    W.d[0] = take(128, 32);
-    for (int l = 1; l < 4; ++l) W.d[l] = take(128, 128);
-    W.d[4] = take(16, 128);
+    uint4* dfeat = cfeat + cap * 4;
+    float4* xc = reinterpret_cast<float4*>(dfeat + cap * 4);
+    hash_f16_kernel<4, 8, 2><<<hgrid, 128, 0, st>>>(FD->dgrid, FD->dtable, xu, S->counters, cap, dfeat);
+    const int smem = ((kDeformW + 1023) / 1024) * 1024 + kDeformSlots * kDeformA;
+    CF_CHECK_CUDA(cudaFuncSetAttribute(deform_mlp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    deform_mlp_kernel<<<persistent_grid(cap, kDeformSlots), kDeformSlots * kSlotThreads, smem, st>>>(
+        FD->wblob, FD->dbias, FD->delta_scale, FD->inv_side, xu, dfeat, S->counters, cap, xc);
+    xcan = xc;
   }
-  W.g[0] = take(64, 32);
-  W.g[1] = take(16, 64);
-  W.c[0] = take(64, 32);
-  W.c[1] = take(64, 64);
-  W.c[2] = take(16, 64);
-  if (off != FD->w_bytes) return cf::fail(CF_E_BAD_ARG, "cf_field_forward: weight blob size mismatch");
-  const int smem = ((off + 1023) / 1024) * 1024 + kSlots * kABytes;
-  CF_CHECK_CUDA(cudaFuncSetAttribute(field_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  const int64_t max_tiles = (S->capacity + 127) / 128;
-  int64_t grid = (max_tiles + kSlots - 1) / kSlots;
-  if (grid > cf::sm_count()) grid = cf::sm_count();
-  if (grid < 1) return CF_OK;
-  field_kernel<<<(unsigned)grid, kSlots * kSlotThreads, smem, cf::as_stream(stream)>>>(
-      *FD, W, dirs, S->records, S->counters, S->capacity, reinterpret_cast<const float4*>(xu),
-      reinterpret_cast<float4*>(out));
+  hash_f16_kernel<2, 16, 4><<<hgrid, 128, 0, st>>>(FD->cgrid, FD->ctable, xcan, S->counters, cap, cfeat);
+  const int csmem = ((kColorW + 1023) / 1024) * 1024 + kColorSlots * kColorA;
+  CF_CHECK_CUDA(cudaFuncSetAttribute(color_mlp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, csmem));
+  const uint8_t* cw = FD->wblob + (FD->has_deform ? kDeformW : 0);
+  color_mlp_kernel<<<persistent_grid(cap, kColorSlots), kColorSlots * kSlotThreads, csmem, st>>>(
+      cw, xu, cfeat, S->records, dirs, S->counters, cap, out);
   return cf::check_launch("cf_field_forward");
 }
 

@@ -311,6 +311,14 @@ class Renderer:
             self.M.origin[a] = float(t[a])
         self.M.n_rays = self.n_rays
 
+    def _scratch(self, buf, desc) -> torch.Tensor:
+        """Per-field scratch of cf_field_forward (allocated once)."""
+        if getattr(buf, "scratch", None) is None:
+            nb = ctypes.c_int64()
+            _lib.call("cf_field_scratch_bytes", _lib.byref(desc), int(buf.mo.capacity), ctypes.byref(nb))
+            buf.scratch = torch.empty(max(int(nb.value), 16), dtype=torch.uint8, device=self.dirs.device)
+        return buf.scratch
+
     def _mark(self, name):
         if self.marks is not None:
             e = torch.cuda.Event(enable_timing=True)
@@ -334,7 +342,7 @@ class Renderer:
                       _lib.byref(self.hw), self._anchor_buckets.handle, h.lbs.buckets.handle, hb.xu.data_ptr(), s)
             self._mark("human_canon")
             _lib.call("cf_field_forward", _lib.byref(self.hdesc), _lib.byref(hb.mo), self.dirs.data_ptr(),
-                      hb.xu.data_ptr(), hb.out.data_ptr(), s)
+                      hb.xu.data_ptr(), hb.out.data_ptr(), self._scratch(hb, self.hdesc).data_ptr(), s)
             self._mark("human_field")
             _lib.call("cf_composite", _lib.byref(self.M), _lib.byref(hb.mo), hb.out.data_ptr(), self.cfg.t_term,
                       hb.rgb.data_ptr(), hb.depth.data_ptr(), hb.opacity.data_ptr(), s)
@@ -344,7 +352,7 @@ class Renderer:
                       ob.xu.data_ptr(), s)
             self._mark("object_canon")
             _lib.call("cf_field_forward", _lib.byref(self.odesc), _lib.byref(ob.mo), self.dirs.data_ptr(),
-                      ob.xu.data_ptr(), ob.out.data_ptr(), s)
+                      ob.xu.data_ptr(), ob.out.data_ptr(), self._scratch(ob, self.odesc).data_ptr(), s)
             self._mark("object_field")
             _lib.call("cf_composite", _lib.byref(self.M), _lib.byref(ob.mo), ob.out.data_ptr(), self.cfg.t_term,
                       ob.rgb.data_ptr(), ob.depth.data_ptr(), ob.opacity.data_ptr(), s)
