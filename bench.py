@@ -209,7 +209,7 @@ def run_ours(args, rank, world, pg):
         for k in range(args.steps):
             fi = (k + rank) % nF
             flush.zero_()
-            r.marks = [("start", starts[k])]
+            r.marks = [(0, "start", starts[k])]
             starts[k].record()
             step(fi, dframes)
             ends[k].record()
@@ -226,10 +226,17 @@ def run_ours(args, rank, world, pg):
     ms_per_step = ms_total / args.steps
 
     # per-stage times (CUDA events on the launching stream inside the timed region)
+    # each stage is timed from the mark it depends on (the two streams interleave)
+    pred = {"lbs_setup": "start", "ed_setup": "start", "rays": "ed_setup", "march": "rays",
+            "object_canon": "march", "object_field": "object_canon", "object_composite": "object_field",
+            "human_canon": "march", "human_field": "human_canon", "human_composite": "human_field",
+            "layers": "human_composite"}
     stages = {}
     for marks in stage_marks:
-        for (n0, e0), (n1, e1) in zip(marks[:-1], marks[1:]):
-            stages.setdefault(n1, []).append(e0.elapsed_time(e1))
+        ev = {name: e for _, name, e in marks}
+        for name, p in pred.items():
+            if name in ev and p in ev:
+                stages.setdefault(name, []).append(ev[p].elapsed_time(ev[name]))
     stage_ms = {k: float(np.mean(v)) for k, v in stages.items()}
 
     # ---- e2e: pinned host prior -> device, render through the public API, image -> pinned host

@@ -236,6 +236,10 @@ class Renderer:
             self.M.obj_inv_side = obj.inv_side
         self.frame = None
         self.marks = None
+        self.side = torch.cuda.Stream(device=d)
+        self._lbs_done = torch.cuda.Event()
+        self._obj_done = torch.cuda.Event()
+        self._lbs_done.record(torch.cuda.current_stream())
 
     # -- per-frame setup ------------------------------------------------------
 
@@ -265,14 +269,21 @@ class Renderer:
         self._A.copy_(bone_A, non_blocking=True)
         self.dbias.copy_(dbias, non_blocking=True)
         n = self._dqs.shape[0]
+        # the backward-LBS chain (vertex transforms, posed vertices, their buckets)
+        # is independent of the ED chain: run it on the side stream
+        main = torch.cuda.current_stream()
+        self._fork(main, self.side)
+        with torch.cuda.stream(self.side):
+            h.lbs.set_pose(self._A)
+            self._mark("lbs_setup")
+            self._lbs_done.record(self.side)
         _lib.call("cf_deform_nodes", h.nodes.data_ptr(), self._dqs.data_ptr(), n, self._anchors.data_ptr(), s)
         self._anchor_buckets.build(self._anchors)
-        h.lbs.set_pose(self._A)
         _lib.call("cf_occ_splat_cached", h.occ_cells.data_ptr(), h.occ_nbr.data_ptr(), h.occ_w.data_ptr(),
                   h.occ_count.data_ptr(), h.occ_cap, self.cfg.ed_k, self._dqs.data_ptr(), _lib.byref(h.canon_occ),
                   _lib.byref(self.live_occ), self.live_scratch.data_ptr(), self.live_bits.data_ptr(),
                   self.live_bbox.data_ptr(), s)
-        self._mark("frame_setup")
+        self._mark("ed_setup")
         if getattr(self, "hw", None) is None:
             w = _lib.HumanWarp()
             w.dqs = self._dqs.data_ptr()
@@ -320,10 +331,20 @@ class Renderer:
         return buf.scratch
 
     def _mark(self, name):
+        """Timing event after a stage, on the stream it ran on: marks hold
+        (stream id, name, event); a stage's time is the gap to the previous mark
+        of the same stream."""
         if self.marks is not None:
             e = torch.cuda.Event(enable_timing=True)
-            e.record()
-            self.marks.append((name, e))
+            st = torch.cuda.current_stream()
+            e.record(st)
+            self.marks.append((st.cuda_stream, name, e))
+
+    @staticmethod
+    def _fork(src: torch.cuda.Stream, dst: torch.cuda.Stream) -> None:
+        ev = torch.cuda.Event()
+        ev.record(src)
+        dst.wait_event(ev)
 
     def render(self, R, t, fx, fy, cx, cy):
         """All stages of one novel view; returns the composited image tensor (H*W, 3).
@@ -336,8 +357,25 @@ class Renderer:
                   self.live_bits.data_ptr() if hb else None, self.obj.bits.data_ptr() if ob else None,
                   _lib.byref(hb.mo) if hb else None, _lib.byref(ob.mo) if ob else None, s)
         self._mark("march")
+        main = torch.cuda.current_stream()
+        if ob:
+            # the object field is independent of the human one: side stream
+            self._fork(main, self.side)
+            with torch.cuda.stream(self.side):
+                so = _lib.stream_ptr()
+                _lib.call("cf_object_canon", _lib.byref(self.M), self.dirs.data_ptr(), _lib.byref(ob.mo),
+                          ob.xu.data_ptr(), so)
+                self._mark("object_canon")
+                _lib.call("cf_field_forward", _lib.byref(self.odesc), _lib.byref(ob.mo), self.dirs.data_ptr(),
+                          ob.xu.data_ptr(), ob.out.data_ptr(), self._scratch(ob, self.odesc).data_ptr(), so)
+                self._mark("object_field")
+                _lib.call("cf_composite", _lib.byref(self.M), _lib.byref(ob.mo), ob.out.data_ptr(),
+                          self.cfg.t_term, ob.rgb.data_ptr(), ob.depth.data_ptr(), ob.opacity.data_ptr(), so)
+                self._mark("object_composite")
+                self._obj_done.record(self.side)
         if hb:
             h = self.human
+            main.wait_event(self._lbs_done)
             _lib.call("cf_human_canon", _lib.byref(self.M), self.dirs.data_ptr(), _lib.byref(hb.mo),
                       _lib.byref(self.hw), self._anchor_buckets.handle, h.lbs.buckets.handle, hb.xu.data_ptr(), s)
             self._mark("human_canon")
@@ -348,15 +386,7 @@ class Renderer:
                       hb.rgb.data_ptr(), hb.depth.data_ptr(), hb.opacity.data_ptr(), s)
             self._mark("human_composite")
         if ob:
-            _lib.call("cf_object_canon", _lib.byref(self.M), self.dirs.data_ptr(), _lib.byref(ob.mo),
-                      ob.xu.data_ptr(), s)
-            self._mark("object_canon")
-            _lib.call("cf_field_forward", _lib.byref(self.odesc), _lib.byref(ob.mo), self.dirs.data_ptr(),
-                      ob.xu.data_ptr(), ob.out.data_ptr(), self._scratch(ob, self.odesc).data_ptr(), s)
-            self._mark("object_field")
-            _lib.call("cf_composite", _lib.byref(self.M), _lib.byref(ob.mo), ob.out.data_ptr(), self.cfg.t_term,
-                      ob.rgb.data_ptr(), ob.depth.data_ptr(), ob.opacity.data_ptr(), s)
-            self._mark("object_composite")
+            main.wait_event(self._obj_done)
         _lib.call("cf_composite_layers", self.n_rays, hb.rgb.data_ptr() if hb else None,
                   hb.depth.data_ptr() if hb else None, hb.opacity.data_ptr() if hb else None,
                   ob.rgb.data_ptr() if ob else None, ob.depth.data_ptr() if ob else None,
