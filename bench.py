@@ -229,7 +229,8 @@ def run_ours(args, rank, world, pg):
     # each stage is timed from the mark it depends on (the two streams interleave)
     pred = {"lbs_setup": "start", "ed_setup": "start", "rays": "ed_setup", "march": "rays",
             "object_canon": "march", "object_field": "object_canon", "object_composite": "object_field",
-            "human_canon": "march", "human_field": "human_canon", "human_composite": "human_field",
+            "human_canon": "march", "human_hash_d": "human_canon", "human_deform_mlp": "human_hash_d",
+            "human_hash_c": "human_deform_mlp", "human_color_mlp": "human_hash_c", "human_composite": "human_color_mlp",
             "layers": "human_composite"}
     stages = {}
     for marks in stage_marks:
@@ -263,29 +264,45 @@ def run_ours(args, rank, world, pg):
     # ---- roofline of the dominant kernel
     hs = float(np.mean([counts[(k + rank) % nF][0] for k in range(args.steps)]))
     os_ = float(np.mean([counts[(k + rank) % nF][1] for k in range(args.steps)]))
-    dom = max(stage_ms, key=stage_ms.get)
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        peak_src = "of measured (MEASURED_PEAKS.json)"
     except Exception:
-        pass
+        peak_src = "of fallback (B200_PROFILING.md)"
     tensor_peak = float(peaks.get("bf16_tflops", 1590.0))
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    if dom in ("human_field", "object_field"):
-        n = hs if dom == "human_field" else os_
-        flop = n * (FLOP_PER_SAMPLE_HUMAN if dom == "human_field" else FLOP_PER_SAMPLE_OBJECT)
-        ach = flop / (stage_ms[dom] / 1e3) / 1e12
+    # algorithmic cost per unit of each single-kernel stage
+    cost = {
+        "human_canon": ("hbm", hs, 4 + 16 + 2, "B/sample: record 4 + xu 16 + ray dir 24/~12 samples"),
+        "human_hash_d": ("hbm", hs, 16 + 64 * 16 + 64, "B/sample: xu 16 + 8 lv x 8 corners x 16 B + 64 out"),
+        "human_hash_c": ("hbm", hs, 16 + 128 * 8 + 64, "B/sample: xc 16 + 16 lv x 8 corners x 8 B + 64 out"),
+        "human_deform_mlp": ("tensor", hs, 110592, "FLOP/sample: 2(32x128 + 3x128x128 + 128x16)"),
+        "human_color_mlp": ("tensor", hs, 20480, "FLOP/sample: 2(32x64 + 64x16 + 32x64 + 64x64 + 64x16)"),
+        "march": ("hbm", r.n_rays, 24 + 8 + 4 * (hs + os_) / r.n_rays, "B/ray: dir 24 + offset/count 8 + 4/record"),
+    }
+    dom = max((k for k in stage_ms if k in cost), key=stage_ms.get)
+    bound, units, per_unit, per_text = cost[dom]
+    work = units * per_unit
+    traffic = None
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(dom)
+    except Exception:
+        pass
+    if bound == "tensor":
+        ach = work / (stage_ms[dom] / 1e3) / 1e12
         roof = {"kernel": dom, "bound": "tensor", "achieved": ach, "peak": tensor_peak, "unit": "TFLOP/s",
-                "frac": ach / tensor_peak, "traffic": None,
-                "per_unit": "131072 FLOP/sample (human) / 20480 (object)",
-                "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst; fp16 dense rate is the same)"}
+                "frac": ach / tensor_peak, "traffic": traffic, "per_unit": per_text,
+                "peak_source": peak_src + " bf16_tflops (burst; fp16 dense rate equal)"}
     else:
-        per = {"human_canon": 4 + 24 + 16, "march": 24 + 8 + 4 * 0, "human_composite": 24, "object_composite": 24}
-        n = hs if dom.startswith("human") else (os_ if dom.startswith("object") else r.n_rays)
-        byt = n * per.get(dom, 16)
-        ach = byt / (stage_ms[dom] / 1e3) / 1e9
+        ach = work / (stage_ms[dom] / 1e3) / 1e9
         roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
-                "frac": ach / hbm_peak, "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+                "frac": ach / hbm_peak, "traffic": traffic, "per_unit": per_text,
+                "peak_source": peak_src + " hbm_gbs"}
+    roof["all_stages"] = {k: {"ms": stage_ms[k], "bound": c[0],
+                              "achieved": (c[1] * c[2] / (stage_ms[k] / 1e3)) / (1e12 if c[0] == "tensor" else 1e9),
+                              "unit": "TFLOP/s" if c[0] == "tensor" else "GB/s"}
+                          for k, c in cost.items() if k in stage_ms}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,

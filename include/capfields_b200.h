@@ -208,6 +208,9 @@ typedef struct cf_human_warp {
   double lbs_max_d2;
   double canon_min[3];      /* canonical unit-cube normalisation */
   double inv_side;
+  const double* anchors;    /* (n,3) deformed nodes of the frame; with n_nodes <= 1024 the
+                               k-NN scans them from shared memory (anchor_buckets may be NULL) */
+  int n_nodes;
 } cf_human_warp;
 
 int cf_camera_rays(const cf_camera* cam, double* dirs, void* stream);
@@ -273,6 +276,10 @@ int cf_field_scratch_bytes(const cf_field_desc* F, int64_t capacity, int64_t* by
  * Stages: hash (fp16 features) [-> DeformNet -> hash] -> E_g/E_c, see field.cu */
 int cf_field_forward(const cf_field_desc* F, const cf_march_out* S, const double* dirs, const float* xu, float* out,
                      void* scratch, void* stream);
+/* one stage of cf_field_forward (so hosts can time / overlap them):
+ * 0 deform-grid hash, 1 DeformNet, 2 canonical-grid hash, 3 E_g/E_c (0-1 human only) */
+int cf_field_stage(const cf_field_desc* F, const cf_march_out* S, const double* dirs, const float* xu, float* out,
+                   void* scratch, int stage, void* stream);
 
 #ifdef __cplusplus
 }

@@ -74,7 +74,8 @@ class MarchOut(ctypes.Structure):
 class HumanWarp(ctypes.Structure):
     _fields_ = [("dqs", ctypes.c_void_p), ("k", ctypes.c_int), ("r2", ctypes.c_double),
                 ("vert_Tinv", ctypes.c_void_p), ("lbs_max_d2", ctypes.c_double),
-                ("canon_min", ctypes.c_double * 3), ("inv_side", ctypes.c_double)]
+                ("canon_min", ctypes.c_double * 3), ("inv_side", ctypes.c_double),
+                ("anchors", ctypes.c_void_p), ("n_nodes", ctypes.c_int)]
 
 
 class FieldDesc(ctypes.Structure):
@@ -122,6 +123,7 @@ _SIGS = {
     "cf_composite_layers": [_i64, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p],
     "cf_field_forward": [_P(FieldDesc), _P(MarchOut), _p, _p, _p, _p, _p],
     "cf_field_scratch_bytes": [_P(FieldDesc), _i64, _P(_i64)],
+    "cf_field_stage": [_P(FieldDesc), _P(MarchOut), _p, _p, _p, _p, _i32, _p],
 }
 
 _lock = threading.Lock()

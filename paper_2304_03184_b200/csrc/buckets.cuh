@@ -92,7 +92,7 @@ __device__ __forceinline__ void bucket_knn(const BucketParams& P, const int* __r
     }
     if (covered) break;
     bound -= P.margin;
-    if (bound > 0.0 && top.worst_d < bound * bound) break;
+    if (bound > 0.0 && top.worst_d() < bound * bound) break;
   }
 }
 

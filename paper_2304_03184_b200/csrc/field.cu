@@ -351,6 +351,12 @@ int cf_field_scratch_bytes(const cf_field_desc* FD, int64_t capacity, int64_t* b
 
 int cf_field_forward(const cf_field_desc* FD, const cf_march_out* S, const double* dirs, const float* xu_f,
                      float* out_f, void* scratch, void* stream) {
+  return cf_field_stage(FD, S, dirs, xu_f, out_f, scratch, -1, stream);
+}
+
+int cf_field_stage(const cf_field_desc* FD, const cf_march_out* S, const double* dirs, const float* xu_f,
+                   float* out_f, void* scratch, int stage, void* stream) {
+  auto run = [&](int s) { return stage < 0 || stage == s; };
   if (!FD || !S || !FD->wblob || !FD->ctable || !scratch || (FD->has_deform && (!FD->dtable || !FD->dbias)))
     return cf::fail(CF_E_BAD_ARG, "cf_field_forward: bad args");
   if (FD->cgrid.n_levels != 16 || FD->cgrid.n_features != 2 ||
@@ -369,19 +375,23 @@ int cf_field_forward(const cf_field_desc* FD, const cf_march_out* S, const doubl
   if (FD->has_deform) {
     uint4* dfeat = cfeat + cap * 4;
     float4* xc = reinterpret_cast<float4*>(dfeat + cap * 4);
-    hash_f16_kernel<4, 8, 2><<<hgrid, 128, 0, st>>>(FD->dgrid, FD->dtable, xu, S->counters, cap, dfeat);
-    const int smem = ((kDeformW + 1023) / 1024) * 1024 + kDeformSlots * kDeformA;
-    CF_CHECK_CUDA(cudaFuncSetAttribute(deform_mlp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    deform_mlp_kernel<<<persistent_grid(cap, kDeformSlots), kDeformSlots * kSlotThreads, smem, st>>>(
-        FD->wblob, FD->dbias, FD->delta_scale, FD->inv_side, xu, dfeat, S->counters, cap, xc);
+    if (run(0)) hash_f16_kernel<4, 8, 2><<<hgrid, 128, 0, st>>>(FD->dgrid, FD->dtable, xu, S->counters, cap, dfeat);
+    if (run(1)) {
+      const int smem = ((kDeformW + 1023) / 1024) * 1024 + kDeformSlots * kDeformA;
+      CF_CHECK_CUDA(cudaFuncSetAttribute(deform_mlp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      deform_mlp_kernel<<<persistent_grid(cap, kDeformSlots), kDeformSlots * kSlotThreads, smem, st>>>(
+          FD->wblob, FD->dbias, FD->delta_scale, FD->inv_side, xu, dfeat, S->counters, cap, xc);
+    }
     xcan = xc;
   }
-  hash_f16_kernel<2, 16, 4><<<hgrid, 128, 0, st>>>(FD->cgrid, FD->ctable, xcan, S->counters, cap, cfeat);
-  const int csmem = ((kColorW + 1023) / 1024) * 1024 + kColorSlots * kColorA;
-  CF_CHECK_CUDA(cudaFuncSetAttribute(color_mlp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, csmem));
-  const uint8_t* cw = FD->wblob + (FD->has_deform ? kDeformW : 0);
-  color_mlp_kernel<<<persistent_grid(cap, kColorSlots), kColorSlots * kSlotThreads, csmem, st>>>(
-      cw, xu, cfeat, S->records, dirs, S->counters, cap, out);
+  if (run(2)) hash_f16_kernel<2, 16, 4><<<hgrid, 128, 0, st>>>(FD->cgrid, FD->ctable, xcan, S->counters, cap, cfeat);
+  if (run(3)) {
+    const int csmem = ((kColorW + 1023) / 1024) * 1024 + kColorSlots * kColorA;
+    CF_CHECK_CUDA(cudaFuncSetAttribute(color_mlp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, csmem));
+    const uint8_t* cw = FD->wblob + (FD->has_deform ? kDeformW : 0);
+    color_mlp_kernel<<<persistent_grid(cap, kColorSlots), kColorSlots * kSlotThreads, csmem, st>>>(
+        cw, xu, cfeat, S->records, dirs, S->counters, cap, out);
+  }
   return cf::check_launch("cf_field_forward");
 }
 

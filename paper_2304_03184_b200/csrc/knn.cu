@@ -217,7 +217,7 @@ __device__ __forceinline__ void finish_query(const WarpArgs& A, int64_t q, d3 p,
 }
 
 template <int K>
-__global__ void __launch_bounds__(128) knn_brute_kernel(WarpArgs A) {
+__global__ void __launch_bounds__(128, 4) knn_brute_kernel(WarpArgs A) {
   constexpr int TILE = 512;
   __shared__ double4 tile[TILE];
   const int64_t nblk = (A.n_pts + blockDim.x - 1) / blockDim.x;
@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(128) knn_brute_kernel(WarpArgs A) {
 }
 
 template <int K>
-__global__ void __launch_bounds__(128) knn_bucket_kernel(WarpArgs A, const BucketParams* __restrict__ Pp,
+__global__ void __launch_bounds__(128, 4) knn_bucket_kernel(WarpArgs A, const BucketParams* __restrict__ Pp,
                                                          const int* __restrict__ cell_start,
                                                          const double4* __restrict__ sorted) {
   __shared__ BucketParams sP;
@@ -359,11 +359,9 @@ int cf_knn_warp(const cf_buckets_t* buckets, const double* anchors, const double
   if (n_pts == 0) return CF_OK;
   WarpArgs A{anchors, dqs, (int)n_nodes, k, radius * radius, mode, pts, n_pts, idx_out, w_out, pc_out, valid_out};
   cudaStream_t st = cf::as_stream(stream);
-  if (k <= 1) return launch_knn<1>(buckets, A, st);
-  if (k <= 2) return launch_knn<2>(buckets, A, st);
-  if (k <= 4) return launch_knn<4>(buckets, A, st);
-  if (k <= 8) return launch_knn<8>(buckets, A, st);
-  return launch_knn<16>(buckets, A, st);
+  const int rc = dispatch_k(k, [&]<int K>() { return launch_knn<K>(buckets, A, st); });
+  if (rc < 0) return cf::fail(CF_E_BAD_ARG, "cf_knn_warp: k must be 1..8 or 16");
+  return rc;
 }
 
 }  // extern "C"

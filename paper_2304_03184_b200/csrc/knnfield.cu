@@ -46,7 +46,7 @@ __device__ __forceinline__ int64_t flat_index(const Grid& g, d3 p, bool& inside,
 // sum(c*c) + |n|^2 - 2 * (c @ n), where the BLAS dot is an FMA chain
 // fma(c2, n2, fma(c1, n1, c0*n0)) (matches OpenBLAS dgemm on K=3).
 template <int K>
-__global__ void __launch_bounds__(128) field_build_kernel(const double* __restrict__ nodes, int n, int s, Grid g,
+__global__ void __launch_bounds__(128, 4) field_build_kernel(const double* __restrict__ nodes, int n, int s, Grid g,
                                                           double sup2, int32_t* __restrict__ out) {
   constexpr int TILE = 512;
   __shared__ double4 tile[TILE];  // (x, y, z, |n|^2)
@@ -164,7 +164,7 @@ __global__ void live_dilate_kernel(const uint32_t* __restrict__ winner, int res,
 }
 
 template <int K>
-__global__ void __launch_bounds__(128) query_kernel(const int32_t* __restrict__ live, const int32_t* __restrict__ nidx,
+__global__ void __launch_bounds__(128, 4) query_kernel(const int32_t* __restrict__ live, const int32_t* __restrict__ nidx,
                                                     const double* __restrict__ dqs,
                                                     const double* __restrict__ anchors, int s, Grid g, double r2,
                                                     const double* __restrict__ pts, int64_t n, int64_t* nbr_out,
@@ -232,11 +232,11 @@ int cf_knnfield_build(const double* nodes, int64_t n, int s, int res, const doub
   const int64_t total = (int64_t)res * res * res;
   cudaStream_t st = cf::as_stream(stream);
   const unsigned grid = cf::grid_for(total, 128, 8);
-  if (s <= 1) field_build_kernel<1><<<grid, 128, 0, st>>>(nodes, (int)n, s, g, sup2, neighbor_idx);
-  else if (s <= 2) field_build_kernel<2><<<grid, 128, 0, st>>>(nodes, (int)n, s, g, sup2, neighbor_idx);
-  else if (s <= 4) field_build_kernel<4><<<grid, 128, 0, st>>>(nodes, (int)n, s, g, sup2, neighbor_idx);
-  else if (s <= 8) field_build_kernel<8><<<grid, 128, 0, st>>>(nodes, (int)n, s, g, sup2, neighbor_idx);
-  else field_build_kernel<16><<<grid, 128, 0, st>>>(nodes, (int)n, s, g, sup2, neighbor_idx);
+  if (dispatch_k(s, [&]<int K>() {
+        field_build_kernel<K><<<grid, 128, 0, st>>>(nodes, (int)n, s, g, sup2, neighbor_idx);
+        return 0;
+      }) < 0)
+    return cf::fail(CF_E_BAD_ARG, "cf_knnfield_build: s must be 1..8 or 16");
   return cf::check_launch("cf_knnfield_build");
 }
 

@@ -62,7 +62,7 @@ __global__ void lbs_vertex_kernel(const double* __restrict__ A, int J, const dou
 }
 
 template <bool kBuckets>
-__global__ void __launch_bounds__(128) lbs_backward_kernel(const BucketParams* __restrict__ Pp,
+__global__ void __launch_bounds__(128, 4) lbs_backward_kernel(const BucketParams* __restrict__ Pp,
                                                            const int* __restrict__ cell_start,
                                                            const double4* __restrict__ sorted,
                                                            const double* __restrict__ verts, int64_t V,

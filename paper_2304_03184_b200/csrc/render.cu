@@ -13,6 +13,10 @@
 
 namespace {
 
+// graphs up to this many nodes are scanned exhaustively from shared memory
+// (cheaper than the bucket ring search's divergent loops at render sizes)
+constexpr int kSmemAnchors = 1024;
+
 __device__ __forceinline__ bool occ_test(const cf_occ_grid& g, const uint32_t* __restrict__ bits, d3 p) {
   const double q[3] = {p.x, p.y, p.z};
   int64_t c[3];
@@ -66,7 +70,7 @@ __global__ void rays_kernel(cf_camera cam, double* __restrict__ dirs) {
 }
 
 // cells whose centre lies within `radius` of any bucketed point
-__global__ void __launch_bounds__(128) occ_points_kernel(cf_occ_grid g, const BucketParams* __restrict__ Pp,
+__global__ void __launch_bounds__(128, 4) occ_points_kernel(cf_occ_grid g, const BucketParams* __restrict__ Pp,
                                                          const int* __restrict__ cell_start,
                                                          const double4* __restrict__ sorted, double r2,
                                                          uint32_t* __restrict__ bits) {
@@ -114,7 +118,7 @@ __global__ void occ_box_kernel(cf_occ_grid g, double hx, double hy, double hz, d
 // forward-warp every occupied canonical cell centre into live space and set
 // the 3x3x3 block of live cells around it
 template <int K>
-__global__ void __launch_bounds__(128) occ_splat_kernel(const uint32_t* __restrict__ cbits, cf_occ_grid cg,
+__global__ void __launch_bounds__(128, 4) occ_splat_kernel(const uint32_t* __restrict__ cbits, cf_occ_grid cg,
                                                         const BucketParams* __restrict__ Pp,
                                                         const int* __restrict__ cell_start,
                                                         const double4* __restrict__ sorted,
@@ -187,7 +191,7 @@ __device__ __forceinline__ void sample_range(const cf_march_desc& M, d3 o, d3 d,
 // sequence): exact canonical k-NN and Gaussian weights, i.e. the reference's
 // canonical_blend_info (edgraph.py:186-195). Compacted (order irrelevant).
 template <int K>
-__global__ void __launch_bounds__(128) occ_cache_kernel(const uint32_t* __restrict__ cbits, cf_occ_grid cg,
+__global__ void __launch_bounds__(128, 4) occ_cache_kernel(const uint32_t* __restrict__ cbits, cf_occ_grid cg,
                                                         const BucketParams* __restrict__ Pp,
                                                         const int* __restrict__ cell_start,
                                                         const double4* __restrict__ sorted, int k, double r2,
@@ -474,8 +478,8 @@ __global__ void __launch_bounds__(128) march_kernel(cf_march_desc M, const doubl
 
 // human samples: live point -> ED backward warp (exact bucketed k-NN + DQB^-1),
 // falling back to backward LBS outside the ED support; -> canonical unit cube
-template <int K>
-__global__ void __launch_bounds__(128) human_canon_kernel(cf_march_desc M, const double* __restrict__ dirs,
+template <int K, bool kSmem>
+__global__ void __launch_bounds__(128, 4) human_canon_kernel(cf_march_desc M, const double* __restrict__ dirs,
                                                           const uint32_t* __restrict__ records,
                                                           const int* __restrict__ count, int64_t capacity,
                                                           cf_human_warp W, const BucketParams* __restrict__ EPp,
@@ -484,10 +488,14 @@ __global__ void __launch_bounds__(128) human_canon_kernel(cf_march_desc M, const
                                                           const int* __restrict__ lcs, const double4* __restrict__ ls,
                                                           float4* __restrict__ xu) {
   __shared__ BucketParams sE, sL;
+  extern __shared__ double4 s_anchors[];  // kSmem: the frame's deformed nodes
   if (threadIdx.x == 0) {
-    sE = *EPp;
+    if (!kSmem) sE = *EPp;
     if (LPp) sL = *LPp;
   }
+  if (kSmem)
+    for (int i = threadIdx.x; i < W.n_nodes; i += blockDim.x)
+      s_anchors[i] = make_double4(W.anchors[3 * i], W.anchors[3 * i + 1], W.anchors[3 * i + 2], 0.0);
   __syncthreads();
   const int64_t n = min((int64_t)*count, capacity);
   const d3 o{M.origin[0], M.origin[1], M.origin[2]};
@@ -497,7 +505,9 @@ __global__ void __launch_bounds__(128) human_canon_kernel(cf_march_desc M, const
     const d3 p = sample_p(o, load_d3(dirs + 3 * ray), sample_t(M, (int)(rec & 255u)));
     d3 pt;
     float flag = 0.0f;
-    if (ed_warp_point<K>(sE, ecs, es, W.dqs, W.k, W.r2, true, p, pt)) {
+    const bool ed_ok = kSmem ? ed_warp_point_smem<K>(s_anchors, W.n_nodes, W.dqs, W.k, W.r2, true, p, pt)
+                             : ed_warp_point<K>(sE, ecs, es, W.dqs, W.k, W.r2, true, p, pt);
+    if (ed_ok) {
       flag = 1.0f;
     } else if (LPp) {
       TopK<1> top;
@@ -622,12 +632,11 @@ int cf_occ_splat(const uint32_t* canon_bits, const cf_occ_grid* cg, const cf_buc
   const int64_t total = (int64_t)cg->res * cg->res * cg->res;
   const unsigned grid = cf::grid_for(total, 128, 8);
   const double r2 = radius * radius;
-  if (k <= 4)
-    occ_splat_kernel<4><<<grid, 128, 0, st>>>(canon_bits, *cg, node_buckets->params, node_buckets->cell_start,
+  dispatch_k(k, [&]<int K>() {
+    occ_splat_kernel<K><<<grid, 128, 0, st>>>(canon_bits, *cg, node_buckets->params, node_buckets->cell_start,
                                               node_buckets->sorted, dqs, k, r2, *lg, live_bits);
-  else
-    occ_splat_kernel<8><<<grid, 128, 0, st>>>(canon_bits, *cg, node_buckets->params, node_buckets->cell_start,
-                                              node_buckets->sorted, dqs, k, r2, *lg, live_bits);
+    return 0;
+  });
   return cf::check_launch("cf_occ_splat");
 }
 
@@ -639,14 +648,12 @@ int cf_occ_cache(const uint32_t* canon_bits, const cf_occ_grid* cg, const cf_buc
   CF_CHECK_CUDA(cudaMemsetAsync(count, 0, sizeof(int), st));
   const int64_t total = (int64_t)cg->res * cg->res * cg->res;
   const unsigned grid = cf::grid_for(total, 128, 8);
-  if (k <= 4)
-    occ_cache_kernel<4><<<grid, 128, 0, st>>>(canon_bits, *cg, node_buckets->params, node_buckets->cell_start,
+  dispatch_k(k, [&]<int K>() {
+    occ_cache_kernel<K><<<grid, 128, 0, st>>>(canon_bits, *cg, node_buckets->params, node_buckets->cell_start,
                                               node_buckets->sorted, k, radius * radius, capacity, cells, nbr, w,
                                               count);
-  else
-    occ_cache_kernel<8><<<grid, 128, 0, st>>>(canon_bits, *cg, node_buckets->params, node_buckets->cell_start,
-                                              node_buckets->sorted, k, radius * radius, capacity, cells, nbr, w,
-                                              count);
+    return 0;
+  });
   return cf::check_launch("cf_occ_cache");
 }
 
@@ -699,19 +706,24 @@ int cf_march(const cf_march_desc* M, const double* dirs, const uint32_t* human_b
 int cf_human_canon(const cf_march_desc* M, const double* dirs, const cf_march_out* F, const cf_human_warp* W,
                    const cf_buckets_t* anchor_buckets, const cf_buckets_t* vert_buckets, float* xu_f, void* stream) {
   float4* xu = reinterpret_cast<float4*>(xu_f);
-  if (!M || !F || !W || !anchor_buckets || anchor_buckets->grid_res == 0 || W->k < 1 || W->k > 8)
+  const bool smem = W && W->anchors && W->n_nodes > 0 && W->n_nodes <= kSmemAnchors;
+  if (!M || !F || !W || W->k < 1 || W->k > 8 || (!smem && (!anchor_buckets || anchor_buckets->grid_res == 0)))
     return cf::fail(CF_E_BAD_ARG, "cf_human_canon: bad args");
   const bool lbs = vert_buckets && W->vert_Tinv;
   cudaStream_t st = cf::as_stream(stream);
   const unsigned grid = cf::grid_for(F->capacity, 128, 8);
-#define CF_HC(KK)                                                                                                \
-  human_canon_kernel<KK><<<grid, 128, 0, st>>>(*M, dirs, F->records, F->counters, F->capacity, *W,               \
-                                               anchor_buckets->params, anchor_buckets->cell_start,              \
-                                               anchor_buckets->sorted, lbs ? vert_buckets->params : nullptr,    \
-                                               lbs ? vert_buckets->cell_start : nullptr,                        \
-                                               lbs ? vert_buckets->sorted : nullptr, xu)
-  if (W->k <= 4) CF_HC(4);
-  else CF_HC(8);
+  const size_t dsm = smem ? sizeof(double4) * W->n_nodes : 0;
+#define CF_HC(KK, SM)                                                                                             \
+  human_canon_kernel<KK, SM><<<grid, 128, dsm, st>>>(                                                            \
+      *M, dirs, F->records, F->counters, F->capacity, *W, anchor_buckets ? anchor_buckets->params : nullptr,    \
+      anchor_buckets ? anchor_buckets->cell_start : nullptr, anchor_buckets ? anchor_buckets->sorted : nullptr, \
+      lbs ? vert_buckets->params : nullptr, lbs ? vert_buckets->cell_start : nullptr,                            \
+      lbs ? vert_buckets->sorted : nullptr, xu)
+  dispatch_k(W->k, [&]<int K>() {
+    if (smem) CF_HC(K, true);
+    else CF_HC(K, false);
+    return 0;
+  });
 #undef CF_HC
   return cf::check_launch("cf_human_canon");
 }

@@ -294,6 +294,8 @@ class Renderer:
             for a in range(3):
                 w.canon_min[a] = h.canon_min[a]
             w.inv_side = h.inv_side
+            w.anchors = self._anchors.data_ptr()
+            w.n_nodes = int(self._anchors.shape[0])
             self.hw = w
             self.hdesc = h.desc(self.dbias)
 
@@ -379,9 +381,11 @@ class Renderer:
             _lib.call("cf_human_canon", _lib.byref(self.M), self.dirs.data_ptr(), _lib.byref(hb.mo),
                       _lib.byref(self.hw), self._anchor_buckets.handle, h.lbs.buckets.handle, hb.xu.data_ptr(), s)
             self._mark("human_canon")
-            _lib.call("cf_field_forward", _lib.byref(self.hdesc), _lib.byref(hb.mo), self.dirs.data_ptr(),
-                      hb.xu.data_ptr(), hb.out.data_ptr(), self._scratch(hb, self.hdesc).data_ptr(), s)
-            self._mark("human_field")
+            scratch = self._scratch(hb, self.hdesc).data_ptr()
+            for stage, name in enumerate(("human_hash_d", "human_deform_mlp", "human_hash_c", "human_color_mlp")):
+                _lib.call("cf_field_stage", _lib.byref(self.hdesc), _lib.byref(hb.mo), self.dirs.data_ptr(),
+                          hb.xu.data_ptr(), hb.out.data_ptr(), scratch, stage, s)
+                self._mark(name)
             _lib.call("cf_composite", _lib.byref(self.M), _lib.byref(hb.mo), hb.out.data_ptr(), self.cfg.t_term,
                       hb.rgb.data_ptr(), hb.depth.data_ptr(), hb.opacity.data_ptr(), s)
             self._mark("human_composite")
