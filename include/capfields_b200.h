@@ -187,6 +187,8 @@ typedef struct cf_march_desc {
   double obj_R[9], obj_t[3]; /* object pose (object-to-world) */
   double obj_min[3], obj_inv_side; /* object unit-cube normalisation */
   const int* human_cell_bbox;      /* device int[6] (lo xyz, hi xyz) of set live cells, or NULL */
+  const double* sample_t;          /* training: explicit depth of compacted sample s (NULL = uniform t_i);
+                                      delta_s = t_{s+1} - t_s within a ray, dt for its last sample */
 } cf_march_desc;
 
 /* compacted samples of one field: records (capacity) = ray << 8 | i, grouped
@@ -280,6 +282,48 @@ int cf_field_forward(const cf_field_desc* F, const cf_march_out* S, const double
  * 0 deform-grid hash, 1 DeformNet, 2 canonical-grid hash, 3 E_g/E_c (0-1 human only) */
 int cf_field_stage(const cf_field_desc* F, const cf_march_out* S, const double* dirs, const float* xu, float* out,
                    void* scratch, int stage, void* stream);
+
+/* ------------------------------------------------------------------ training (SPEC train_step) */
+
+/* depth-guided samples of the masked rays: fills F (records, per-ray
+ * offset/count, counters) and t_out (float64 depth per compacted sample; pass it as
+ * M->sample_t to the canonicalisation / field / composite calls) */
+int cf_train_sample(const cf_march_desc* M, const float* gt_depth, const uint8_t* mask, int n_guided, int n_uniform,
+                    int n_empty, double sigma_d, uint64_t seed, const cf_march_out* F, double* t_out, void* stream);
+/* masked L2 colour + lambda * L1 depth (lambda_depth = 0.1) and the
+ * compositing backward: grad = float4 (dL/dsigma, dL/dr, dL/dg, dL/db) per sample;
+ * loss[0] += L_color, loss[1] += L_depth (unweighted), normalised by inv_n_* */
+int cf_loss_composite_bwd(const cf_march_desc* M, const cf_march_out* F, const float* field, float t_term,
+                          const float* gt_rgb, const float* gt_depth, const uint8_t* mask, float lambda_depth,
+                          float inv_n_color, float inv_n_depth, float* grad, float* loss, void* stream);
+
+/* saved activations (fp16 rows) and gradients of the E_g/E_c backward (S = capacity) */
+typedef struct cf_color_bwd_io {
+  void* h1;    /* (S,64) */
+  void* cin;   /* (S,32) */
+  void* c1;    /* (S,64) */
+  void* c2;    /* (S,64) */
+  void* d_o;   /* (S,16) */
+  void* dc2;   /* (S,64) */
+  void* dc1;   /* (S,64) */
+  void* dg;    /* (S,16) */
+  void* dh1;   /* (S,64) */
+  float* dfeat; /* (S,32) fp32 dL/d(canonical hash features) */
+} cf_color_bwd_io;
+/* E_g/E_c backward on tcgen05 (forward recomputed per tile from the features that
+ * cf_field_forward left in `scratch`): dX chain with the transposed weights
+ * wt_blob = [C3^T 64x16, C2^T 64x64, C1^T 32x64, G2^T 64x16, G1^T 32x64] */
+int cf_color_backward(const cf_field_desc* F, const uint8_t* wt_blob, const cf_march_out* S, const double* dirs,
+                      const float* xu, const float* grad_out, const void* scratch, const cf_color_bwd_io* io,
+                      void* stream);
+/* canonical hash-grid backward at the positions the forward used (xc / xu) */
+int cf_field_hash_backward(const cf_field_desc* F, const cf_march_out* S, const float* xu, const void* scratch,
+                           const float* dfeat, float* table_grad, void* stream);
+/* Adam: p -= lr * mhat / (sqrt(vhat) + eps), m/v in place; grads scaled by grad_scale */
+int cf_adam(float* p, const float* g, float* m, float* v, int64_t n, float lr, float beta1, float beta2, float eps,
+            int step, float grad_scale, void* stream);
+/* fp32 (n x k) row-major weight -> fp16 UMMA canonical K-major blob (n, k padded to 16) */
+int cf_pack_weight(const float* w, int n, int k, uint8_t* blob, void* stream);
 
 #ifdef __cplusplus
 }

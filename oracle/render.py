@@ -216,3 +216,40 @@ def layers(h, o, bg):
     if orr is not None:
         out[L == 2] = orr[L == 2]
     return out, L
+
+
+# ----------------------------------------------------------------- training sampler
+
+def u01(seed, ray, j):
+    """splitmix64(seed + golden * (ray*64 + j + 1)) -> [0,1) with 53 bits (render.cu:u01)."""
+    M64 = (1 << 64) - 1
+    z = (seed + 0x9E3779B97F4A7C15 * (ray * 64 + j + 1)) & M64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M64
+    z ^= z >> 31
+    return float(z >> 11) * 2.0 ** -53
+
+
+def train_samples(gt_depth, mask, t_near, t_far, n_guided, n_uniform, n_empty, sigma_d, seed):
+    """Depth-guided samples per ray -> list of sorted t arrays (None for unmasked)."""
+    out = []
+    for ray, (d, m) in enumerate(zip(gt_depth, mask)):
+        if not m:
+            out.append(None)
+            continue
+        strat = lambda lo, hi, n, j, slot: lo + ((j + u01(seed, ray, slot)) / n) * (hi - lo)  # noqa: E731
+        if not d > 0:
+            out.append(np.array([strat(t_near, t_far, n_empty, j, j) for j in range(n_empty)]))
+            continue
+        lo = max(t_near, float(d) - 6.0 * sigma_d)
+        hi = min(t_far, float(d) + 6.0 * sigma_d)
+        a = [strat(lo, hi, n_guided, j, j) for j in range(n_guided)]
+        b = [strat(t_near, t_far, n_uniform, j, 32 + j) for j in range(n_uniform)]
+        merged, i, k = [], 0, 0
+        while i < len(a) or k < len(b):
+            if k >= len(b) or (i < len(a) and a[i] <= b[k]):
+                merged.append(a[i]); i += 1
+            else:
+                merged.append(b[k]); k += 1
+        out.append(np.array(merged))
+    return out

@@ -63,7 +63,7 @@ class MarchDesc(ctypes.Structure):
                 ("t_near", ctypes.c_double), ("t_far", ctypes.c_double), ("dt", ctypes.c_double),
                 ("human_grid", OccGrid), ("object_grid", OccGrid), ("obj_R", ctypes.c_double * 9),
                 ("obj_t", ctypes.c_double * 3), ("obj_min", ctypes.c_double * 3), ("obj_inv_side", ctypes.c_double),
-                ("human_cell_bbox", ctypes.c_void_p)]
+                ("human_cell_bbox", ctypes.c_void_p), ("sample_t", ctypes.c_void_p)]
 
 
 class MarchOut(ctypes.Structure):
@@ -83,6 +83,10 @@ class FieldDesc(ctypes.Structure):
                 ("cgrid", HashGridDesc), ("ctable", ctypes.c_void_p), ("wblob", ctypes.c_void_p),
                 ("w_bytes", ctypes.c_int), ("dbias", ctypes.c_void_p), ("delta_scale", ctypes.c_float),
                 ("inv_side", ctypes.c_float)]
+
+
+class ColorBwdIO(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in ("h1", "cin", "c1", "c2", "d_o", "dc2", "dc1", "dg", "dh1", "dfeat")]
 
 
 def byref(x):
@@ -124,6 +128,14 @@ _SIGS = {
     "cf_field_forward": [_P(FieldDesc), _P(MarchOut), _p, _p, _p, _p, _p],
     "cf_field_scratch_bytes": [_P(FieldDesc), _i64, _P(_i64)],
     "cf_field_stage": [_P(FieldDesc), _P(MarchOut), _p, _p, _p, _p, _i32, _p],
+    "cf_train_sample": [_P(MarchDesc), _p, _p, _i32, _i32, _i32, _f64, ctypes.c_uint64, _P(MarchOut), _p, _p],
+    "cf_loss_composite_bwd": [_P(MarchDesc), _P(MarchOut), _p, ctypes.c_float, _p, _p, _p, ctypes.c_float,
+                              ctypes.c_float, ctypes.c_float, _p, _p, _p],
+    "cf_color_backward": [_P(FieldDesc), _p, _P(MarchOut), _p, _p, _p, _p, _P(ColorBwdIO), _p],
+    "cf_field_hash_backward": [_P(FieldDesc), _P(MarchOut), _p, _p, _p, _p, _p],
+    "cf_adam": [_p, _p, _p, _p, _i64, ctypes.c_float, ctypes.c_float, ctypes.c_float, ctypes.c_float, _i32,
+                ctypes.c_float, _p],
+    "cf_pack_weight": [_p, _i32, _i32, _p, _p],
 }
 
 _lock = threading.Lock()

@@ -331,6 +331,242 @@ __global__ void __launch_bounds__(kColorSlots* kSlotThreads, 1)
   if (threadIdx.x / 32 == 0) tc::tmem_free<256>(tmem_base);
 }
 
+// ---------------------------------------------------------------- E_g / E_c backward
+
+// Transposed weights for dX = dY . W, in the blob order C3t (64x16), C2t (64x64),
+// C1t (32x64), G2t (64x16), G1t (32x64): each W^T packed K-major (K = N_out).
+constexpr int kColorWT = (64 * 16 + 64 * 64 + 32 * 64 + 64 * 16 + 32 * 64) * 2;  // 20,480 B
+constexpr int kBwdSlots = 4;
+constexpr int kBwdA = 128 * 64 * 2;
+
+struct ColorBwdIO {
+  // saved activations / output grads (fp16 rows) for the weight-gradient GEMMs
+  __half* h1;    // (S,64) relu(G1 x)
+  __half* cin;   // (S,32) [geo, SH, 0]
+  __half* c1;    // (S,64)
+  __half* c2;    // (S,64)
+  __half* d_o;   // (S,16) dL/d(E_c output)
+  __half* dc2;   // (S,64) dL/d(C2 pre-activation)
+  __half* dc1;   // (S,64)
+  __half* dg;    // (S,16) dL/d(E_g output)
+  __half* dh1;   // (S,64)
+  float* dfeat;  // (S,32) dL/d(hash features)
+};
+
+__device__ __forceinline__ void store_row_f16(__half* dst, int64_t s, int width, const float* v) {
+  uint4* d = reinterpret_cast<uint4*>(dst + s * width);
+#pragma unroll 4
+  for (int q = 0; q < width / 8; ++q) {
+    __half2 h[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = __floats2half2_rn(v[8 * q + 2 * i], v[8 * q + 2 * i + 1]);
+    d[q] = *reinterpret_cast<uint4*>(h);
+  }
+}
+
+// forward hidden layer with ReLU: keep the activation mask, write fp16 to A buffer (+ HBM copy)
+template <int N>
+__device__ __forceinline__ uint64_t fwd_relu(Slot& S, __half* save, int64_t s, bool live) {
+  uint64_t mask = 0;
+#pragma unroll
+  for (int c0 = 0; c0 < N; c0 += 32) {
+    float v[32];
+    tc::tmem_ld32(S.tmem_row + (uint32_t)c0, v);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      if (v[i] > 0.f) mask |= 1ull << (c0 + i);
+      v[i] = fmaxf(v[i], 0.0f);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) tc::st_row8(S.abuf, S.r, c0 + 8 * q, N, v + 8 * q);
+    if (live) {
+      uint4* d = reinterpret_cast<uint4*>(save + s * N + c0);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        __half2 h[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) h[i] = __floats2half2_rn(v[8 * q + 2 * i], v[8 * q + 2 * i + 1]);
+        d[q] = *reinterpret_cast<uint4*>(h);
+      }
+    }
+  }
+  return mask;
+}
+
+// backward through a ReLU layer: dpre = dact (from TMEM) * relu'(mask) -> A buffer (+ HBM)
+template <int N>
+__device__ __forceinline__ void bwd_relu(Slot& S, uint64_t mask, __half* save, int64_t s, bool live) {
+#pragma unroll
+  for (int c0 = 0; c0 < N; c0 += 32) {
+    float v[32];
+    tc::tmem_ld32(S.tmem_row + (uint32_t)c0, v);
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (!((mask >> (c0 + i)) & 1ull)) v[i] = 0.0f;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) tc::st_row8(S.abuf, S.r, c0 + 8 * q, N, v + 8 * q);
+    if (live) {
+      uint4* d = reinterpret_cast<uint4*>(save + s * N + c0);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        __half2 h[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) h[i] = __floats2half2_rn(v[8 * q + 2 * i], v[8 * q + 2 * i + 1]);
+        d[q] = *reinterpret_cast<uint4*>(h);
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kBwdSlots* kSlotThreads, 1)
+    color_bwd_kernel(const uint8_t* __restrict__ wblob, const uint8_t* __restrict__ wtblob,
+                     const float4* __restrict__ xu, const uint4* __restrict__ cfeat,
+                     const uint32_t* __restrict__ records, const double* __restrict__ dirs,
+                     const float4* __restrict__ gout, const int* __restrict__ count, int64_t capacity,
+                     ColorBwdIO io) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t mbar[kBwdSlots];
+  __shared__ uint32_t tmem_base;
+  // stage both weight blobs contiguously: forward (20 KB) then transposed (20 KB)
+  for (int i = threadIdx.x * 16; i < kColorWT; i += blockDim.x * 16)
+    *reinterpret_cast<uint4*>(smem + kColorW + i) = *reinterpret_cast<const uint4*>(wtblob + i);
+  slots_setup<kBwdSlots, 256>(wblob, kColorW, smem, mbar, &tmem_base);
+  Slot S = make_slot<kBwdSlots, 64, kBwdA>(smem, kColorW + kColorWT, mbar, tmem_base);
+  constexpr int g1 = 0, g2 = 64 * 32 * 2, c1 = g2 + 16 * 64 * 2, c2 = c1 + 64 * 32 * 2, c3 = c2 + 64 * 64 * 2;
+  constexpr int t_c3 = kColorW, t_c2 = t_c3 + 64 * 16 * 2, t_c1 = t_c2 + 64 * 64 * 2, t_g2 = t_c1 + 32 * 64 * 2,
+                t_g1 = t_g2 + 64 * 16 * 2;
+  const int64_t n = min((int64_t)*count, capacity);
+  const int64_t n_tiles = (n + 127) / 128;
+  for (int64_t tile = (int64_t)blockIdx.x * kBwdSlots + S.slot; tile < n_tiles; tile += (int64_t)gridDim.x * kBwdSlots) {
+    const int64_t s = tile * 128 + S.r;
+    const bool live = s < n;
+    const bool valid = live && xu[s].w > 0.0f;
+    // ---- forward recompute, saving what the weight gradients need
+    row_to_abuf(S, cfeat, s, live);
+    run_layer(S, g1, 32, 64);
+    const uint64_t m_h1 = fwd_relu<64>(S, io.h1, s, live);
+    run_layer(S, g2, 64, 16);
+    float gv[16];
+    tc::tmem_ld16(S.tmem_row, gv);
+    const float sigma = expf(gv[0]);
+    float cin[32];
+#pragma unroll
+    for (int i = 0; i < 15; ++i) cin[i] = gv[1 + i];
+    float dx = 0.f, dy = 0.f, dz = 1.f;
+    if (live) {
+      const int64_t ray = records[s] >> 8;
+      dx = (float)dirs[3 * ray];
+      dy = (float)dirs[3 * ray + 1];
+      dz = (float)dirs[3 * ray + 2];
+    }
+    sh16(dx, dy, dz, cin + 15);
+    cin[31] = 0.0f;
+#pragma unroll
+    for (int k0 = 0; k0 < 32; k0 += 8) tc::st_row8(S.abuf, S.r, k0, 32, cin + k0);
+    if (live) store_row_f16(io.cin, s, 32, cin);
+    run_layer(S, c1, 32, 64);
+    const uint64_t m_c1 = fwd_relu<64>(S, io.c1, s, live);
+    run_layer(S, c2, 64, 64);
+    const uint64_t m_c2 = fwd_relu<64>(S, io.c2, s, live);
+    run_layer(S, c3, 64, 16);
+    float ov[16];
+    tc::tmem_ld16(S.tmem_row, ov);
+    // ---- backward: dO = dL/drgb * sigmoid'
+    const float4 g = valid ? gout[s] : make_float4(0.f, 0.f, 0.f, 0.f);
+    float d_o[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) d_o[i] = 0.f;
+    {
+      const float gr[3] = {g.y, g.z, g.w};
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const float sg = 1.0f / (1.0f + expf(-ov[c]));
+        d_o[c] = gr[c] * sg * (1.0f - sg);
+      }
+    }
+    tc::st_row8(S.abuf, S.r, 0, 16, d_o);
+    tc::st_row8(S.abuf, S.r, 8, 16, d_o + 8);
+    if (live) store_row_f16(io.d_o, s, 16, d_o);
+    run_layer(S, t_c3, 16, 64);  // dC2act = dO . C3
+    bwd_relu<64>(S, m_c2, io.dc2, s, live);
+    run_layer(S, t_c2, 64, 64);  // dC1act = dC2 . C2
+    bwd_relu<64>(S, m_c1, io.dc1, s, live);
+    run_layer(S, t_c1, 64, 32);  // dCin = dC1 . C1
+    float dcin[32];
+    tc::tmem_ld32(S.tmem_row, dcin);
+    float dg[16];
+    dg[0] = valid ? g.x * sigma : 0.f;  // sigma = exp(g0)
+#pragma unroll
+    for (int i = 1; i < 16; ++i) dg[i] = dcin[i - 1];
+    tc::st_row8(S.abuf, S.r, 0, 16, dg);
+    tc::st_row8(S.abuf, S.r, 8, 16, dg + 8);
+    if (live) store_row_f16(io.dg, s, 16, dg);
+    run_layer(S, t_g2, 16, 64);  // dH1act = dG . G2
+    bwd_relu<64>(S, m_h1, io.dh1, s, live);
+    run_layer(S, t_g1, 64, 32);  // dX0 = dH1 . G1
+    float dfx[32];
+    tc::tmem_ld32(S.tmem_row, dfx);
+    if (live) {
+      float4* d = reinterpret_cast<float4*>(io.dfeat + s * 32);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) d[q] = make_float4(dfx[4 * q], dfx[4 * q + 1], dfx[4 * q + 2], dfx[4 * q + 3]);
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (threadIdx.x / 32 == 0) tc::tmem_free<256>(tmem_base);
+}
+
+// hash backward on the compacted samples: grad[entry] += w_corner * dfeat (fp32 vector atomics)
+template <int F, int L>
+__global__ void __launch_bounds__(128) hash_bwd_kernel(cf_hashgrid_desc D, const float4* __restrict__ x,
+                                                       const float* __restrict__ dfeat, const int* __restrict__ count,
+                                                       int64_t capacity, float* __restrict__ grad) {
+  const int64_t n = min((int64_t)*count, capacity);
+  const uint32_t mask = (1u << D.log2_table) - 1u;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
+    const float4 p = x[s];
+    if (!(p.w > 0.0f)) continue;
+    const float px = fminf(fmaxf(p.x, 0.f), 1.f), py = fminf(fmaxf(p.y, 0.f), 1.f), pz = fminf(fmaxf(p.z, 0.f), 1.f);
+    const float* g = dfeat + s * (L * F);
+#pragma unroll 2
+    for (int l = 0; l < L; ++l) {
+      const int N = D.resolution[l];
+      const float sc = (float)N;
+      const float pos[3] = {f_mul(px, sc), f_mul(py, sc), f_mul(pz, sc)};
+      uint32_t gi[3];
+      float fr[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        int v = (int)floorf(pos[a]);
+        v = v > N - 1 ? N - 1 : v;
+        gi[a] = (uint32_t)v;
+        fr[a] = f_sub(pos[a], (float)v);
+      }
+      const uint32_t stride = (uint32_t)N + 1u;
+      const bool dense = D.dense[l] != 0;
+      float gl[F];
+#pragma unroll
+      for (int f = 0; f < F; ++f) gl[f] = g[l * F + f];
+      float* base = grad + D.offset[l] * F;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t cx = gi[0] + (k & 1), cy = gi[1] + ((k >> 1) & 1), cz = gi[2] + ((k >> 2) & 1);
+        const uint32_t idx = dense ? (cx + cy * stride + cz * stride * stride)
+                                   : ((cx ^ (cy * 2654435761u) ^ (cz * 805459861u)) & mask);
+        const float w = f_mul(f_mul((k & 1) ? fr[0] : f_sub(1.f, fr[0]), (k & 2) ? fr[1] : f_sub(1.f, fr[1])),
+                              (k & 4) ? fr[2] : f_sub(1.f, fr[2]));
+        float* dst = base + (int64_t)idx * F;
+        if constexpr (F == 2) {
+          atomicAdd(reinterpret_cast<float2*>(dst), make_float2(w * gl[0], w * gl[1]));
+        } else {
+          atomicAdd(reinterpret_cast<float4*>(dst), make_float4(w * gl[0], w * gl[1], w * gl[2], w * gl[3]));
+        }
+      }
+    }
+  }
+}
+
 unsigned persistent_grid(int64_t capacity, int slots) {
   const int64_t tiles = (capacity + 127) / 128;
   int64_t g = (tiles + slots - 1) / slots;
@@ -352,6 +588,42 @@ int cf_field_scratch_bytes(const cf_field_desc* FD, int64_t capacity, int64_t* b
 int cf_field_forward(const cf_field_desc* FD, const cf_march_out* S, const double* dirs, const float* xu_f,
                      float* out_f, void* scratch, void* stream) {
   return cf_field_stage(FD, S, dirs, xu_f, out_f, scratch, -1, stream);
+}
+
+int cf_color_backward(const cf_field_desc* FD, const uint8_t* wt_blob, const cf_march_out* S, const double* dirs,
+                      const float* xu, const float* grad_out, const void* scratch, const cf_color_bwd_io* io,
+                      void* stream) {
+  if (!FD || !wt_blob || !S || !dirs || !xu || !grad_out || !scratch || !io || !io->dfeat)
+    return cf::fail(CF_E_BAD_ARG, "cf_color_backward: bad args");
+  const int64_t cap = S->capacity;
+  if (cap == 0) return CF_OK;
+  ColorBwdIO o{reinterpret_cast<__half*>(io->h1),  reinterpret_cast<__half*>(io->cin),
+               reinterpret_cast<__half*>(io->c1),  reinterpret_cast<__half*>(io->c2),
+               reinterpret_cast<__half*>(io->d_o), reinterpret_cast<__half*>(io->dc2),
+               reinterpret_cast<__half*>(io->dc1), reinterpret_cast<__half*>(io->dg),
+               reinterpret_cast<__half*>(io->dh1), io->dfeat};
+  const int smem = kColorW + kColorWT + kBwdSlots * kBwdA;
+  CF_CHECK_CUDA(cudaFuncSetAttribute(color_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const uint8_t* cw = FD->wblob + (FD->has_deform ? kDeformW : 0);
+  color_bwd_kernel<<<persistent_grid(cap, kBwdSlots), kBwdSlots * kSlotThreads, smem, cf::as_stream(stream)>>>(
+      cw, wt_blob, reinterpret_cast<const float4*>(xu), reinterpret_cast<const uint4*>(scratch), S->records, dirs,
+      reinterpret_cast<const float4*>(grad_out), S->counters, cap, o);
+  return cf::check_launch("cf_color_backward");
+}
+
+int cf_field_hash_backward(const cf_field_desc* FD, const cf_march_out* S, const float* xu, const void* scratch,
+                           const float* dfeat, float* table_grad, void* stream) {
+  if (!FD || !S || !xu || !scratch || !dfeat || !table_grad)
+    return cf::fail(CF_E_BAD_ARG, "cf_field_hash_backward: bad args");
+  const int64_t cap = S->capacity;
+  if (cap == 0) return CF_OK;
+  // the canonical grid saw xc (human: after DeformNet, stored in scratch) or xu (object)
+  const float4* x = reinterpret_cast<const float4*>(xu);
+  if (FD->has_deform)
+    x = reinterpret_cast<const float4*>(reinterpret_cast<const uint4*>(scratch) + cap * 8);
+  hash_bwd_kernel<2, 16><<<cf::grid_for(cap, 128, 16), 128, 0, cf::as_stream(stream)>>>(
+      FD->cgrid, x, dfeat, S->counters, cap, table_grad);
+  return cf::check_launch("cf_field_hash_backward");
 }
 
 int cf_field_stage(const cf_field_desc* FD, const cf_march_out* S, const double* dirs, const float* xu_f,

@@ -41,6 +41,10 @@ __device__ __forceinline__ d3 cell_center(const cf_occ_grid& g, int64_t flat) {
 __device__ __forceinline__ double sample_t(const cf_march_desc& M, int i) {
   return x_add(M.t_near, x_mul((double)i + 0.5, M.dt));
 }
+// depth of compacted sample s: explicit (training sampler) or the uniform t_i
+__device__ __forceinline__ double rec_t(const cf_march_desc& M, int64_t s, uint32_t rec) {
+  return M.sample_t ? M.sample_t[s] : sample_t(M, (int)(rec & 255u));
+}
 __device__ __forceinline__ d3 sample_p(d3 o, d3 d, double t) {
   return d3{x_add(o.x, x_mul(t, d.x)), x_add(o.y, x_mul(t, d.y)), x_add(o.z, x_mul(t, d.z))};
 }
@@ -502,7 +506,7 @@ __global__ void __launch_bounds__(128, 4) human_canon_kernel(cf_march_desc M, co
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t rec = records[s];
     const int64_t ray = rec >> 8;
-    const d3 p = sample_p(o, load_d3(dirs + 3 * ray), sample_t(M, (int)(rec & 255u)));
+    const d3 p = sample_p(o, load_d3(dirs + 3 * ray), rec_t(M, s, rec));
     d3 pt;
     float flag = 0.0f;
     const bool ed_ok = kSmem ? ed_warp_point_smem<K>(s_anchors, W.n_nodes, W.dqs, W.k, W.r2, true, p, pt)
@@ -539,10 +543,24 @@ __global__ void object_canon_kernel(cf_march_desc M, const double* __restrict__ 
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t rec = records[s];
     const int64_t ray = rec >> 8;
-    const d3 p = to_object(M.obj_R, M.obj_t, sample_p(o, load_d3(dirs + 3 * ray), sample_t(M, (int)(rec & 255u))));
+    const d3 p = to_object(M.obj_R, M.obj_t, sample_p(o, load_d3(dirs + 3 * ray), rec_t(M, s, rec)));
     xu[s] = make_float4(__double2float_rn(x_mul(x_sub(p.x, M.obj_min[0]), M.obj_inv_side)),
                         __double2float_rn(x_mul(x_sub(p.y, M.obj_min[1]), M.obj_inv_side)),
                         __double2float_rn(x_mul(x_sub(p.z, M.obj_min[2]), M.obj_inv_side)), 1.0f);
+  }
+}
+
+// depth t and step delta of the j-th sample of a ray segment: uniform march
+// (t_i, dt), or explicit training depths (delta = t_{j+1} - t_j, dt for the last)
+__device__ __forceinline__ void seg_t_delta(const cf_march_desc& M, const cf_march_out& F, int off, int cnt, int j,
+                                            float& t, float& delta) {
+  if (M.sample_t) {
+    const double tj = M.sample_t[off + j];
+    t = (float)tj;
+    delta = (j + 1 < cnt) ? (float)(M.sample_t[off + j + 1] - tj) : (float)M.dt;
+  } else {
+    t = (float)sample_t(M, (int)(F.records[off + j] & 255u));
+    delta = (float)M.dt;
   }
 }
 
@@ -550,20 +568,20 @@ __global__ void object_canon_kernel(cf_march_desc M, const double* __restrict__ 
 // T_i = prod_{j<i} (1 - alpha_j); stops once T < t_term
 __global__ void composite_kernel(cf_march_desc M, cf_march_out F, const float4* __restrict__ field, float t_term,
                                  float* __restrict__ rgb, float* __restrict__ depth, float* __restrict__ opacity) {
-  const float dt = (float)M.dt;
   for (int64_t ray = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ray < M.n_rays;
        ray += (int64_t)gridDim.x * blockDim.x) {
     const int off = F.ray_offset[ray], cnt = F.ray_count[ray];
     float T = 1.0f, r = 0.f, g = 0.f, b = 0.f, dep = 0.f, op = 0.f;
     for (int j = 0; j < cnt; ++j) {
       const float4 f = field[off + j];
-      const int i = (int)(F.records[off + j] & 255u);
-      const float alpha = 1.0f - expf(-f.x * dt);
+      float t, delta;
+      seg_t_delta(M, F, off, cnt, j, t, delta);
+      const float alpha = 1.0f - expf(-f.x * delta);
       const float w = T * alpha;
       r += w * f.y;
       g += w * f.z;
       b += w * f.w;
-      dep += w * (float)sample_t(M, i);
+      dep += w * t;
       op += w;
       T *= 1.0f - alpha;
       if (T < t_term) break;
@@ -573,6 +591,159 @@ __global__ void composite_kernel(cf_march_desc M, cf_march_out F, const float4* 
     rgb[3 * ray + 2] = b;
     depth[ray] = dep / fmaxf(op, 1e-6f);
     opacity[ray] = op;
+  }
+}
+
+// Loss (lambda_depth config.py:55) and compositing backward.
+//   L = 1/Nm sum_masked |rgb - gt|^2 + lambda / Nd sum_masked,valid-depth |depth - gt_depth|
+// d rgb = sum w c, D = sum w t, O = sum w, depth = D / max(O, 1e-6):
+//   dL/dc_j     = w_j dL/drgb
+//   dL/dsigma_j = delta_j [ sum_v g_v (T_{j+1} v_j - (S_v - P_v,j)) ]   v in {r,g,b, t, 1}
+// (S_v: ray total, P_v,j: prefix through sample j). Samples after early
+// termination get zero gradient, exactly mirroring the forward.
+__global__ void composite_bwd_kernel(cf_march_desc M, cf_march_out F, const float4* __restrict__ field,
+                                     float t_term, const float* __restrict__ gt_rgb,
+                                     const float* __restrict__ gt_depth, const uint8_t* __restrict__ mask,
+                                     float lambda, float inv_nm, float inv_nd, float4* __restrict__ grad,
+                                     float* __restrict__ loss) {
+  float lc = 0.f, ld = 0.f;
+  for (int64_t ray = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ray < M.n_rays;
+       ray += (int64_t)gridDim.x * blockDim.x) {
+    const int off = F.ray_offset[ray], cnt = F.ray_count[ray];
+    // forward again: totals and the number of samples used
+    float T = 1.f, S[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+    int used = 0;
+    for (int j = 0; j < cnt; ++j) {
+      const float4 f = field[off + j];
+      float t, delta;
+      seg_t_delta(M, F, off, cnt, j, t, delta);
+      const float a = 1.0f - expf(-f.x * delta), w = T * a;
+      S[0] += w * f.y;
+      S[1] += w * f.z;
+      S[2] += w * f.w;
+      S[3] += w * t;
+      S[4] += w;
+      T *= 1.0f - a;
+      used = j + 1;
+      if (T < t_term) break;
+    }
+    float gv[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+    if (mask[ray]) {
+      for (int c = 0; c < 3; ++c) {
+        const float e = S[c] - gt_rgb[3 * ray + c];
+        lc += e * e * inv_nm;
+        gv[c] = 2.0f * e * inv_nm;
+      }
+      const float gd = gt_depth[ray];
+      if (gd > 0.f) {
+        const float O = fmaxf(S[4], 1e-6f), depth = S[3] / O, e = depth - gd;
+        ld += fabsf(e) * inv_nd;
+        const float gdep = lambda * inv_nd * (e > 0.f ? 1.f : (e < 0.f ? -1.f : 0.f));
+        gv[3] = gdep / O;
+        gv[4] = S[4] > 1e-6f ? -gdep * S[3] / (S[4] * S[4]) : 0.f;
+      }
+    }
+    T = 1.f;
+    float P[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int j = 0; j < cnt; ++j) {
+      if (j >= used) {
+        grad[off + j] = make_float4(0.f, 0.f, 0.f, 0.f);
+        continue;
+      }
+      const float4 f = field[off + j];
+      float t, delta;
+      seg_t_delta(M, F, off, cnt, j, t, delta);
+      const float a = 1.0f - expf(-f.x * delta), w = T * a;
+      const float v[5] = {f.y, f.z, f.w, t, 1.0f};
+      const float Tn = T * (1.0f - a);
+      float ds = 0.f;
+#pragma unroll
+      for (int q = 0; q < 5; ++q) {
+        P[q] += w * v[q];
+        ds += gv[q] * (Tn * v[q] - (S[q] - P[q]));
+      }
+      grad[off + j] = make_float4(delta * ds, w * gv[0], w * gv[1], w * gv[2]);
+      T = Tn;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lc += __shfl_xor_sync(0xffffffffu, lc, o);
+    ld += __shfl_xor_sync(0xffffffffu, ld, o);
+  }
+  if ((threadIdx.x & 31) == 0 && loss) {
+    atomicAdd(loss, lc);
+    atomicAdd(loss + 1, ld);
+  }
+}
+
+// counter-based uniform in [0,1): splitmix64 of (seed, ray, j) -> 53-bit mantissa
+__device__ __forceinline__ double u01(uint64_t seed, uint64_t ray, uint64_t j) {
+  uint64_t z = seed + 0x9E3779B97F4A7C15ull * (ray * 64ull + j + 1ull);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return (double)(z >> 11) * 0x1.0p-53;
+}
+
+// Depth-guided training samples: a masked ray with valid depth d
+// gets n_guided stratified samples in [d - 6 s, d + 6 s] (clamped to
+// [t_near, t_far]) merged with n_uniform stratified samples over [t_near, t_far];
+// without depth, n_empty stratified samples. Sorted per ray; t in float64:
+//   t = lo + ((j + u) / n) * (hi - lo)      (un-contracted, u = u01(seed, ray, slot))
+// Stratum j of the guided set uses slot j, of the uniform set slot 32 + j.
+__global__ void __launch_bounds__(128) train_sample_kernel(cf_march_desc M, const float* __restrict__ gt_depth,
+                                                           const uint8_t* __restrict__ mask, int n_guided,
+                                                           int n_uniform, int n_empty, double sigma_d,
+                                                           uint64_t seed, cf_march_out F, double* __restrict__ t_out) {
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < M.n_rays; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t ray = base + threadIdx.x;
+    const bool live = ray < M.n_rays && mask[ray] != 0;
+    const float d = live ? gt_depth[ray] : 0.f;
+    const bool guided = live && d > 0.f;
+    const int c = !live ? 0 : (guided ? n_guided + n_uniform : n_empty);
+    int wtot;
+    const int excl = warp_excl_scan(c, wtot);
+    int wbase = 0;
+    if ((threadIdx.x & 31) == 0 && wtot > 0) wbase = atomicAdd(F.counters, wtot);
+    wbase = __shfl_sync(0xffffffffu, wbase, 0);
+    if (ray >= M.n_rays) continue;
+    const int64_t pos = (int64_t)wbase + excl;
+    const bool fits = pos + c <= F.capacity;
+    F.ray_offset[ray] = (int)pos;
+    F.ray_count[ray] = fits ? c : 0;
+    if (!fits) {
+      if (c > 0) atomicExch(F.counters + 1, 1);
+      continue;
+    }
+    if (c == 0) continue;
+    auto strat = [&](double lo, double hi, int n, int j, int slot) {
+      return x_add(lo, x_mul(x_div((double)j + u01(seed, ray, slot), (double)n), x_sub(hi, lo)));
+    };
+    if (!guided) {
+      for (int j = 0; j < n_empty; ++j) {
+        t_out[pos + j] = strat(M.t_near, M.t_far, n_empty, j, j);
+        F.records[pos + j] = ((uint32_t)ray << 8) | (uint32_t)j;
+      }
+      continue;
+    }
+    const double lo = fmax(M.t_near, x_sub((double)d, x_mul(6.0, sigma_d)));
+    const double hi = fmin(M.t_far, x_add((double)d, x_mul(6.0, sigma_d)));
+    // merge two sorted stratified sets
+    int a = 0, b = 0;
+    double ta = strat(lo, hi, n_guided, 0, 0), tb = strat(M.t_near, M.t_far, n_uniform, 0, 32);
+    for (int j = 0; j < c; ++j) {
+      const bool takeA = b >= n_uniform || (a < n_guided && ta <= tb);
+      const double t = takeA ? ta : tb;
+      if (takeA) {
+        ++a;
+        if (a < n_guided) ta = strat(lo, hi, n_guided, a, a);
+      } else {
+        ++b;
+        if (b < n_uniform) tb = strat(M.t_near, M.t_far, n_uniform, b, 32 + b);
+      }
+      t_out[pos + j] = t;
+      F.records[pos + j] = ((uint32_t)ray << 8) | (uint32_t)j;
+    }
   }
 }
 
@@ -744,6 +915,31 @@ int cf_composite(const cf_march_desc* M, const cf_march_out* F, const float* fie
   composite_kernel<<<cf::grid_for(M->n_rays, 128, 8), 128, 0, cf::as_stream(stream)>>>(*M, *F, field, t_term, rgb,
                                                                                         depth, opacity);
   return cf::check_launch("cf_composite");
+}
+
+int cf_train_sample(const cf_march_desc* M, const float* gt_depth, const uint8_t* mask, int n_guided, int n_uniform,
+                    int n_empty, double sigma_d, uint64_t seed, const cf_march_out* F, double* t_out, void* stream) {
+  if (!M || !F || !gt_depth || !mask || !t_out || n_guided < 1 || n_uniform < 1 || n_empty < 1 ||
+      n_guided + n_uniform > 128 || n_empty > 128 || n_guided > 32)
+    return cf::fail(CF_E_BAD_ARG, "cf_train_sample: bad args");
+  cudaStream_t st = cf::as_stream(stream);
+  CF_CHECK_CUDA(cudaMemsetAsync(F->counters, 0, 2 * sizeof(int), st));
+  if (M->n_rays == 0) return CF_OK;
+  train_sample_kernel<<<cf::grid_for(M->n_rays, 128, 8), 128, 0, st>>>(*M, gt_depth, mask, n_guided, n_uniform,
+                                                                        n_empty, sigma_d, seed, *F, t_out);
+  return cf::check_launch("cf_train_sample");
+}
+
+int cf_loss_composite_bwd(const cf_march_desc* M, const cf_march_out* F, const float* field, float t_term,
+                          const float* gt_rgb, const float* gt_depth, const uint8_t* mask, float lambda_depth,
+                          float inv_n_color, float inv_n_depth, float* grad, float* loss, void* stream) {
+  if (!M || !F || !field || !gt_rgb || !gt_depth || !mask || !grad)
+    return cf::fail(CF_E_BAD_ARG, "cf_loss_composite_bwd: bad args");
+  if (M->n_rays == 0) return CF_OK;
+  composite_bwd_kernel<<<cf::grid_for(M->n_rays, 128, 8), 128, 0, cf::as_stream(stream)>>>(
+      *M, *F, reinterpret_cast<const float4*>(field), t_term, gt_rgb, gt_depth, mask, lambda_depth, inv_n_color,
+      inv_n_depth, reinterpret_cast<float4*>(grad), loss);
+  return cf::check_launch("cf_loss_composite_bwd");
 }
 
 int cf_composite_layers(int64_t n, const float* h_rgb, const float* h_depth, const float* h_opac, const float* o_rgb,

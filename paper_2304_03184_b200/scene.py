@@ -190,7 +190,7 @@ class Scene:
         self.cfg = cfg = cfg or SceneConfig()
         rng = np.random.default_rng(seed)
         # the reference draws palette / phases first; keep the stream aligned
-        rng.uniform(0.25, 0.9, size=(N_JOINTS, 3))
+        self.palette = rng.uniform(0.25, 0.9, size=(N_JOINTS, 3))
         rng.uniform(0, 2 * np.pi, size=N_JOINTS)
         rng.uniform(0, 2 * np.pi, size=N_JOINTS)
         rng.uniform(0, 2 * np.pi, size=3)
@@ -257,6 +257,67 @@ class Scene:
         """GT ED-node motion of frame fid (synthetic.py:122-131)."""
         A = self.bone_transforms(fid)
         return np.stack([dq_from_rt(A[b, :3, :3], A[b, :3, 3]) for b in self.node_bones])
+
+    def posed_segments(self, fid: int):
+        """World capsule segments (A, B), radii and driver joints of frame fid."""
+        G = forward_kinematics(self.theta(fid))
+        pos = G[:, :3, 3]
+        j = np.arange(1, N_JOINTS)
+        return pos[PARENTS[j]], pos[j], BONE_RADII[j], PARENTS[j]
+
+    def raycast(self, o: np.ndarray, d: np.ndarray, fid: int):
+        """Analytic ray cast of the posed capsules and the box (training targets):
+        -> t_human, t_object (inf = miss; distance along the unit ray), rgb, masks."""
+        A, B, R, drv = self.posed_segments(fid)
+        o = np.asarray(o, dtype=np.float64)
+        d = np.asarray(d, dtype=np.float64)
+        n = len(d)
+        t_h = np.full(n, np.inf)
+        hit_cap = np.zeros(n, dtype=np.int64)
+        for i in range(len(A)):
+            ba = B[i] - A[i]
+            oa = o - A[i]
+            baba = ba @ ba
+            bard = d @ ba
+            baoa = oa @ ba
+            rdoa = np.sum(oa * d, -1)
+            oaoa = np.sum(oa * oa, -1)
+            a = baba - bard * bard
+            b = baba * rdoa - baoa * bard
+            c = baba * oaoa - baoa * baoa - R[i] * R[i] * baba
+            h = b * b - a * c
+            with np.errstate(invalid="ignore", divide="ignore"):
+                t = (-b - np.sqrt(np.maximum(h, 0.0))) / a
+            y = baoa + t * bard
+            ok = (h >= 0) & (np.abs(a) > 1e-12) & (t > 1e-6) & (y > 0) & (y < baba)
+            tc = np.where(ok, t, np.inf)
+            for cen in (A[i], B[i]):  # end caps
+                oc = o - cen
+                bq = np.sum(oc * d, -1)
+                cq = np.sum(oc * oc, -1) - R[i] * R[i]
+                h2 = bq * bq - cq
+                ts = -bq - np.sqrt(np.maximum(h2, 0.0))
+                tc = np.where((h2 >= 0) & (ts > 1e-6) & (ts < tc), ts, tc)
+            better = tc < t_h
+            t_h = np.where(better, tc, t_h)
+            hit_cap = np.where(better, i, hit_cap)
+        Rb, tb = self.object_pose(fid)
+        ol = (o - tb) @ Rb
+        dl = d @ Rb
+        with np.errstate(divide="ignore", invalid="ignore"):
+            t1 = (-self.box_half - ol) / dl
+            t2 = (self.box_half - ol) / dl
+        te = np.minimum(t1, t2).max(-1)
+        tx = np.maximum(t1, t2).min(-1)
+        t_o = np.where((tx >= te) & (te > 1e-6), te, np.inf)
+        rgb = np.zeros((n, 3))
+        hum = np.isfinite(t_h) & (t_h <= t_o)
+        obj = np.isfinite(t_o) & (t_o < t_h)
+        rgb[hum] = self.palette[drv[hit_cap[hum]]]
+        if obj.any():
+            p = ol[obj] + te[obj, None] * dl[obj]
+            rgb[obj] = np.clip(0.52 + 0.42 * np.sin(18.0 * p), 0.0, 1.0)
+        return t_h, t_o, rgb, hum, obj
 
     def object_pose(self, fid: int):
         """World pose (R, t) of the box at frame fid (synthetic.py:37-45)."""
