@@ -26,8 +26,8 @@ def cell_centers(gmin, cell, res, flat):
 
 
 def cell_of(p, gmin, cell, res):
-    """flat index and inside flag: floor((p - min) / cell) in [0, res)."""
-    f = np.floor((p - np.asarray(gmin, dtype=np.float64)) / cell)
+    """flat index and inside flag: floor((p - min) * (1 / cell)) in [0, res) (render.cu:occ_test)."""
+    f = np.floor((p - np.asarray(gmin, dtype=np.float64)) * (1.0 / cell))
     inside = np.all((f >= 0) & (f < res), axis=-1)
     fi = np.where(inside[:, None], f, 0).astype(np.int64)
     return (fi[:, 0] * res + fi[:, 1]) * res + fi[:, 2], inside

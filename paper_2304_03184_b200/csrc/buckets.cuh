@@ -51,8 +51,12 @@ __device__ __forceinline__ void scan_range(int b, int e, const double4* __restri
 // points (distances are evaluated on them only through the sorted copy, which
 // holds identical values).
 template <int K>
+// `cutoff2`: callers that only use neighbours within sqrt(cutoff2) (occupancy,
+// LBS validity) stop once every unvisited cell is farther than that; the result
+// is then exact for every neighbour within the cutoff (others may be missing).
 __device__ __forceinline__ void bucket_knn(const BucketParams& P, const int* __restrict__ cell_start,
-                                           const double4* __restrict__ sorted, d3 p, TopK<K>& top) {
+                                           const double4* __restrict__ sorted, d3 p, TopK<K>& top,
+                                           double cutoff2 = 1.0e300) {
   int c0[3];
   bucket_cell(P, p, c0);
   const double q[3] = {p.x, p.y, p.z};
@@ -92,7 +96,7 @@ __device__ __forceinline__ void bucket_knn(const BucketParams& P, const int* __r
     }
     if (covered) break;
     bound -= P.margin;
-    if (bound > 0.0 && top.worst_d() < bound * bound) break;
+    if (bound > 0.0 && (top.worst_d() < bound * bound || bound * bound > cutoff2)) break;
   }
 }
 

@@ -211,18 +211,35 @@ __global__ void __launch_bounds__(kDeformSlots* kSlotThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t mbar[kDeformSlots];
   __shared__ uint32_t tmem_base;
+  __shared__ float s_bias[128];
+  if (threadIdx.x < 128) s_bias[threadIdx.x] = bias1[threadIdx.x];
   slots_setup<kDeformSlots, 512>(wblob, kDeformW, smem, mbar, &tmem_base);
   Slot S = make_slot<kDeformSlots, 128, kDeformA>(smem, kDeformW, mbar, tmem_base);
   constexpr int o1 = 0, o2 = 128 * 32 * 2, o3 = o2 + 128 * 128 * 2, o4 = o3 + 128 * 128 * 2, o5 = o4 + 128 * 128 * 2;
   const int64_t n = min((int64_t)*count, capacity);
   const int64_t n_tiles = (n + 127) / 128;
-  for (int64_t tile = (int64_t)blockIdx.x * kDeformSlots + S.slot; tile < n_tiles;
-       tile += (int64_t)gridDim.x * kDeformSlots) {
+  const int64_t tstride = (int64_t)gridDim.x * kDeformSlots;
+  // software pipelining: the next tile's feature row is loaded during this tile's MLP
+  int64_t tile = (int64_t)blockIdx.x * kDeformSlots + S.slot;
+  uint4 nxt[4];
+  {
+    const int64_t s0 = tile * 128 + S.r;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) nxt[q] = (s0 < n) ? dfeat[s0 * 4 + q] : make_uint4(0, 0, 0, 0);
+  }
+  for (; tile < n_tiles; tile += tstride) {
     const int64_t s = tile * 128 + S.r;
     const bool live = s < n;
-    row_to_abuf(S, dfeat, s, live);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) *reinterpret_cast<uint4*>(S.abuf + tc::core_offset(S.r, 8 * q, 32)) = nxt[q];
+    const float4 xs = live ? xu[s] : make_float4(0.f, 0.f, 0.f, 0.f);
     run_layer(S, o1, 32, 128);
-    relu_to_abuf<128>(S, bias1);
+    {
+      const int64_t sn = (tile + tstride) * 128 + S.r;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) nxt[q] = (sn < n) ? dfeat[sn * 4 + q] : make_uint4(0, 0, 0, 0);
+    }
+    relu_to_abuf<128>(S, s_bias);
     run_layer(S, o2, 128, 128);
     relu_to_abuf<128>(S, nullptr);
     run_layer(S, o3, 128, 128);
@@ -233,7 +250,7 @@ __global__ void __launch_bounds__(kDeformSlots* kSlotThreads, 1)
     float v[16];
     tc::tmem_ld16(S.tmem_row, v);
     if (live) {
-      float4 p = xu[s];
+      float4 p = xs;
       if (p.w > 0.0f) {
         p.x = f_add(p.x, f_mul(delta_scale * tanhf(v[0]), inv_side));
         p.y = f_add(p.y, f_mul(delta_scale * tanhf(v[1]), inv_side));
@@ -291,24 +308,26 @@ __global__ void __launch_bounds__(kColorSlots* kSlotThreads, 1)
     const int64_t s = tile * 128 + S.r;
     const bool live = s < n;
     row_to_abuf(S, cfeat, s, live);
+    // per-sample inputs of the later layers, loaded while the first MMAs run
+    const bool valid = live && xu[s].w > 0.0f;
+    double ddx = 0.0, ddy = 0.0, ddz = 1.0;
+    if (live) {
+      const int64_t ray = records[s] >> 8;
+      ddx = dirs[3 * ray];
+      ddy = dirs[3 * ray + 1];
+      ddz = dirs[3 * ray + 2];
+    }
     run_layer(S, g1, 32, 64);
     relu_to_abuf<64>(S, nullptr);
     run_layer(S, g2, 64, 16);
     float gv[16];
     tc::tmem_ld16(S.tmem_row, gv);
-    const bool valid = live && xu[s].w > 0.0f;
     const float sigma = valid ? expf(gv[0]) : 0.0f;
     // colour input: [geo(15), SH4(dir)(16), 0]
     float cin[32];
 #pragma unroll
     for (int i = 0; i < 15; ++i) cin[i] = gv[1 + i];
-    float dx = 0.f, dy = 0.f, dz = 1.f;
-    if (live) {
-      const int64_t ray = records[s] >> 8;
-      dx = (float)dirs[3 * ray];
-      dy = (float)dirs[3 * ray + 1];
-      dz = (float)dirs[3 * ray + 2];
-    }
+    const float dx = (float)ddx, dy = (float)ddy, dz = (float)ddz;
     sh16(dx, dy, dz, cin + 15);
     cin[31] = 0.0f;
 #pragma unroll

@@ -13,16 +13,22 @@
 
 namespace {
 
+#ifndef CF_CANON_MINB
+#define CF_CANON_MINB 6  // resident CTAs/SM the canonicalisation kernel is compiled for
+#endif
 // graphs up to this many nodes are scanned exhaustively from shared memory
 // (cheaper than the bucket ring search's divergent loops at render sizes)
 constexpr int kSmemAnchors = 1024;
 
 __device__ __forceinline__ bool occ_test(const cf_occ_grid& g, const uint32_t* __restrict__ bits, d3 p) {
+  // floor((p - min) * (1 / cell)): a multiply by the correctly rounded
+  // reciprocal instead of a float64 division (the oracle uses the same formula)
   const double q[3] = {p.x, p.y, p.z};
+  const double inv = 1.0 / g.cell;
   int64_t c[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    const double f = floor(x_div(x_sub(q[a], g.min[a]), g.cell));
+    const double f = floor(x_mul(x_sub(q[a], g.min[a]), inv));
     if (!(f >= 0.0) || f >= (double)g.res) return false;
     c[a] = (int64_t)f;
   }
@@ -90,7 +96,7 @@ __global__ void __launch_bounds__(128, 4) occ_points_kernel(cf_occ_grid g, const
     if (cell < total) {
       TopK<1> top;
       top.init(1);
-      bucket_knn<1>(sP, cell_start, sorted, cell_center(g, cell), top);
+      bucket_knn<1>(sP, cell_start, sorted, cell_center(g, cell), top, r2);
       on = top.d[0] <= r2;
     }
     const uint32_t word = __ballot_sync(0xffffffffu, on);
@@ -483,7 +489,7 @@ __global__ void __launch_bounds__(128) march_kernel(cf_march_desc M, const doubl
 // human samples: live point -> ED backward warp (exact bucketed k-NN + DQB^-1),
 // falling back to backward LBS outside the ED support; -> canonical unit cube
 template <int K, bool kSmem>
-__global__ void __launch_bounds__(128, 4) human_canon_kernel(cf_march_desc M, const double* __restrict__ dirs,
+__global__ void __launch_bounds__(128, CF_CANON_MINB) human_canon_kernel(cf_march_desc M, const double* __restrict__ dirs,
                                                           const uint32_t* __restrict__ records,
                                                           const int* __restrict__ count, int64_t capacity,
                                                           cf_human_warp W, const BucketParams* __restrict__ EPp,
@@ -492,31 +498,49 @@ __global__ void __launch_bounds__(128, 4) human_canon_kernel(cf_march_desc M, co
                                                           const int* __restrict__ lcs, const double4* __restrict__ ls,
                                                           float4* __restrict__ xu) {
   __shared__ BucketParams sE, sL;
-  extern __shared__ double4 s_anchors[];  // kSmem: the frame's deformed nodes
+  extern __shared__ double4 s_anchors[];  // kSmem: the frame's deformed nodes (+ fp32 copies)
+  float4* s_af = reinterpret_cast<float4*>(s_anchors + (kSmem ? W.n_nodes : 0));
+  __shared__ unsigned s_mag;
   if (threadIdx.x == 0) {
     if (!kSmem) sE = *EPp;
     if (LPp) sL = *LPp;
+    s_mag = 0u;
   }
-  if (kSmem)
-    for (int i = threadIdx.x; i < W.n_nodes; i += blockDim.x)
-      s_anchors[i] = make_double4(W.anchors[3 * i], W.anchors[3 * i + 1], W.anchors[3 * i + 2], 0.0);
+  __syncthreads();
+  if (kSmem) {
+    float mag = 0.f;
+    for (int i = threadIdx.x; i < W.n_nodes; i += blockDim.x) {
+      const double x = W.anchors[3 * i], y = W.anchors[3 * i + 1], z = W.anchors[3 * i + 2];
+      s_anchors[i] = make_double4(x, y, z, 0.0);
+      s_af[i] = make_float4((float)x, (float)y, (float)z, 0.f);
+      mag = fmaxf(mag, fmaxf(fabsf((float)x), fmaxf(fabsf((float)y), fabsf((float)z))));
+    }
+    atomicMax(&s_mag, __float_as_uint(mag));  // non-negative floats order as their bits
+    __syncthreads();
+    if (threadIdx.x == 0) s_af[0].w = __uint_as_float(s_mag);
+  }
   __syncthreads();
   const int64_t n = min((int64_t)*count, capacity);
   const d3 o{M.origin[0], M.origin[1], M.origin[2]};
-  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t rec = records[s];
+  // warp-uniform trip count (the culled scan is warp-cooperative)
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < n; base += stride) {
+    const int64_t s = base + (threadIdx.x & 31);
+    const bool live = s < n;
+    const uint32_t rec = live ? records[s] : 0u;
     const int64_t ray = rec >> 8;
-    const d3 p = sample_p(o, load_d3(dirs + 3 * ray), rec_t(M, s, rec));
+    const d3 p = live ? sample_p(o, load_d3(dirs + 3 * ray), rec_t(M, s, rec)) : d3{0.0, 0.0, 0.0};
     d3 pt;
     float flag = 0.0f;
-    const bool ed_ok = kSmem ? ed_warp_point_smem<K>(s_anchors, W.n_nodes, W.dqs, W.k, W.r2, true, p, pt)
-                             : ed_warp_point<K>(sE, ecs, es, W.dqs, W.k, W.r2, true, p, pt);
+    const bool ed_ok = kSmem ? ed_warp_point_cull<K>(s_anchors, s_af, W.n_nodes, W.dqs, W.k, W.r2, true, p, live, pt)
+                             : (live && ed_warp_point<K>(sE, ecs, es, W.dqs, W.k, W.r2, true, p, pt));
+    if (!live) continue;
     if (ed_ok) {
       flag = 1.0f;
     } else if (LPp) {
       TopK<1> top;
       top.init(1);
-      bucket_knn<1>(sL, lcs, ls, p, top);
+      bucket_knn<1>(sL, lcs, ls, p, top, W.lbs_max_d2);
       if (top.d[0] <= W.lbs_max_d2) {
         const double* T = W.vert_Tinv + 12 * (int64_t)top.i[0];
         pt = d3{T[0] * p.x + T[1] * p.y + T[2] * p.z + T[3], T[4] * p.x + T[5] * p.y + T[6] * p.z + T[7],
@@ -883,7 +907,7 @@ int cf_human_canon(const cf_march_desc* M, const double* dirs, const cf_march_ou
   const bool lbs = vert_buckets && W->vert_Tinv;
   cudaStream_t st = cf::as_stream(stream);
   const unsigned grid = cf::grid_for(F->capacity, 128, 8);
-  const size_t dsm = smem ? sizeof(double4) * W->n_nodes : 0;
+  const size_t dsm = smem ? (sizeof(double4) + sizeof(float4)) * W->n_nodes : 0;
 #define CF_HC(KK, SM)                                                                                             \
   human_canon_kernel<KK, SM><<<grid, 128, dsm, st>>>(                                                            \
       *M, dirs, F->records, F->counters, F->capacity, *W, anchor_buckets ? anchor_buckets->params : nullptr,    \

@@ -278,7 +278,8 @@ class Renderer:
             self._mark("lbs_setup")
             self._lbs_done.record(self.side)
         _lib.call("cf_deform_nodes", h.nodes.data_ptr(), self._dqs.data_ptr(), n, self._anchors.data_ptr(), s)
-        self._anchor_buckets.build(self._anchors)
+        if n > 1024:  # small graphs are scanned from shared memory (no buckets needed)
+            self._anchor_buckets.build(self._anchors)
         _lib.call("cf_occ_splat_cached", h.occ_cells.data_ptr(), h.occ_nbr.data_ptr(), h.occ_w.data_ptr(),
                   h.occ_count.data_ptr(), h.occ_cap, self.cfg.ed_k, self._dqs.data_ptr(), _lib.byref(h.canon_occ),
                   _lib.byref(self.live_occ), self.live_scratch.data_ptr(), self.live_bits.data_ptr(),

@@ -172,13 +172,16 @@ class Trainer:
         if n == 0:
             return
         x0 = scratch[: n * 64].view(torch.float16).view(n, 32)
-        f = lambda t: t[:n].float()  # noqa: E731
+        # fp16 operands on the tensor cores, fp32 accumulation (reduced-precision
+        # split-K reduction disabled), fp32 gradient accumulation across frames
+        torch.backends.cuda.matmul.allow_fp16_reduced_precision_reduction = False
+        f = lambda t: t[:n]  # noqa: E731
         G = P.G
-        G["C3"] += (f(bwd.d_o).t() @ f(bwd.c2))[:3]
-        G["C2"] += f(bwd.dc2).t() @ f(bwd.c1)
-        G["C1"] += (f(bwd.dc1).t() @ f(bwd.cin))[:, :31]
-        G["G2"] += f(bwd.dg).t() @ f(bwd.h1)
-        G["G1"] += f(bwd.dh1).t() @ x0.float()
+        G["C3"] += (f(bwd.d_o).t() @ f(bwd.c2)).float()[:3]
+        G["C2"] += (f(bwd.dc2).t() @ f(bwd.c1)).float()
+        G["C1"] += (f(bwd.dc1).t() @ f(bwd.cin)).float()[:, :31]
+        G["G2"] += (f(bwd.dg).t() @ f(bwd.h1)).float()
+        G["G1"] += (f(bwd.dh1).t() @ x0).float()
 
     def set_frame(self, b: FrameBatch):
         r = self.r
