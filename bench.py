@@ -45,8 +45,9 @@ def parse():
     ap.add_argument("--samples", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--workload", default="render", choices=["render", "train"],
-                    help="render = configs[1] (the headline); train = configs[2] key-frame training step")
+    ap.add_argument("--workload", default="render", choices=["render", "train", "knn"],
+                    help="render = configs[1] (the headline); train = configs[2] key-frame training step; "
+                         "knn = configs[3] dense-graph k-NN scaling")
     ap.add_argument("--train-rays", type=int, default=1 << 18)
     return ap.parse_args()
 
@@ -535,6 +536,63 @@ def run_train(args, rank, world, pg):
         print(json.dumps(line))
 
 
+def run_knn(args, rank, world, pg):
+    """configs[3]: dense ED graph scaling — exact k-NN + DQB^-1 backward warp of
+    2^20 queries over n = 1024..8192 deformed nodes, k = 4/8: hierarchical bucket
+    search vs the exhaustive GPU kernel (bit-identical results checked here)."""
+    import torch
+    from oracle import deform as od
+    from paper_2304_03184_b200 import _lib
+    from paper_2304_03184_b200.edgraph import Buckets, knn_warp
+    from paper_2304_03184_b200.scene import Scene, SceneConfig
+    sc = Scene(SceneConfig(), seed=0)
+    rng = np.random.default_rng(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    rows = []
+    for n in (1024, 2048, 4096, 8192):
+        nodes = sc.template_points[rng.choice(len(sc.template_points), n, replace=False)]
+        A = sc.bone_transforms(7)
+        bones = sc.template_bones[np.argmin(((nodes[:, None] - sc.template_points[None, :4000]) ** 2).sum(-1), 1)]
+        dqs = np.stack([od.dq_from_rt(A[b, :3, :3], A[b, :3, 3]) for b in bones])
+        anchors = od.deformed_nodes(nodes, dqs)
+        half = 1 << 19
+        q = np.concatenate([anchors[rng.integers(0, n, half)] + rng.normal(scale=0.02, size=(half, 3)),
+                            rng.uniform(anchors.min(0), anchors.max(0), size=(half, 3))])
+        a_t = torch.from_numpy(anchors).to(dev)
+        d_t = torch.from_numpy(dqs).to(dev)
+        q_t = torch.from_numpy(q).to(dev)
+        b = Buckets(n)
+        for k in (4, 8):
+            res = {}
+            for name, bk in (("hierarchical", b), ("brute", None)):
+                if bk is not None:
+                    bk.build(a_t, candidates_k=k)
+                for _ in range(2):
+                    out = knn_warp(a_t, d_t, k, 0.1, _lib.CF_WARP_BACKWARD, q_t, bk, want_idx=True)
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                reps = 5
+                e0.record()
+                for _ in range(reps):
+                    if bk is not None:
+                        bk.build(a_t, candidates_k=k)  # per-frame build (buckets + lists) included
+                    out = knn_warp(a_t, d_t, k, 0.1, _lib.CF_WARP_BACKWARD, q_t, bk, want_idx=True)
+                e1.record()
+                torch.cuda.synchronize()
+                res[name] = (len(q) * reps / (e0.elapsed_time(e1) / 1e3), out[0])
+            same = bool(torch.equal(res["hierarchical"][1], res["brute"][1]))
+            rows.append({"n_nodes": n, "k": k, "hierarchical_qps": res["hierarchical"][0],
+                         "brute_force_qps": res["brute"][0], "speedup": res["hierarchical"][0] / res["brute"][0],
+                         "indices_identical": same})
+    line = {"metric": "exact k-NN + DQB^-1 backward warps/s (dense ED graph, configs[3])",
+            "value": min(r["hierarchical_qps"] for r in rows), "unit": "queries/s", "n_gpus": 1,
+            "higher_is_better": True, "dtype": "f64", "data": "synthetic (template subsets, GT motion, 2^20 queries)",
+            "config": {"workload": "configs[3]: n = 1024..8192 nodes, k = 4/8, half near-surface / half uniform "
+                                   "queries; bucket build included per call"}, "rows": rows}
+    if rank == 0:
+        print(json.dumps(line))
+
+
 def main():
     args = parse()
     rank, world, local, pg = dist_setup(args.gpus)
@@ -542,6 +600,8 @@ def main():
         run_reference(args, rank, world, pg)
     elif args.workload == "train":
         run_train(args, rank, world, pg)
+    elif args.workload == "knn":
+        run_knn(args, rank, world, pg)
     else:
         run_ours(args, rank, world, pg)
     if pg is not None:

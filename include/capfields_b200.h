@@ -67,6 +67,11 @@ int cf_buckets_create(int64_t max_points, int max_grid_res, cf_buckets_t** out);
 int cf_buckets_destroy(cf_buckets_t* b);
 /* grid_res <= 0 picks a resolution from n (~4 points per occupied cell). */
 int cf_buckets_build(cf_buckets_t* b, const double* pts, int64_t n, int grid_res, void* stream);
+/* Optional second level, after cf_buckets_build: per cell, the exact candidate
+ * list of points that can be among the k nearest of any query in the cell
+ * (radius d_k(centre) + 2 half-diagonals). cf_knn_warp then scans one list per
+ * query (ring search only outside the grid box); results stay bit-identical. */
+int cf_buckets_build_candidates(cf_buckets_t* b, int k, void* stream);
 
 /* Exact k-NN (ties by index, squared distance evaluated as the reference's
  * sum((p - a)**2)) over `anchors` followed by the dual-quaternion blend.

@@ -25,6 +25,13 @@ struct cf_buckets {
   int* point_slot = nullptr;       // device, max_points
   double4* sorted = nullptr;       // device, max_points: (x, y, z, id as double)
   int grid_res = 0;                // last build
+  // cell candidate lists (cf_buckets_build_candidates): for every cell, the
+  // points that can be among the k nearest of ANY query inside that cell
+  int* ccl_count = nullptr;        // device, max_cells + 1 (count, then exclusive start)
+  int* ccl_len = nullptr;          // device, max_cells
+  int* ccl_ids = nullptr;          // device, ccl_cap
+  int64_t ccl_cap = 0;
+  int ccl_k = 0;                   // k the lists are valid for (0 = not built)
 };
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }

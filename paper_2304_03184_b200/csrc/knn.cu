@@ -164,6 +164,100 @@ __global__ void __launch_bounds__(1024) bucket_build_small_kernel(const double* 
   bucket_scatter_body(pts, n, cell_start, point_cell, point_slot, sorted);
 }
 
+// ------------------------------------------------------------------ cell candidate lists
+// For cell C with centre c and half-diagonal hd, any query p in C has
+// d_k(p) <= d_k(c) + hd, so every member x of p's k-NN satisfies
+// |c - x| <= |c - p| + |p - x| <= d_k(c) + 2 hd. The list of C is exactly the
+// points within that radius (float64, relative slack 1e-9): scanning it yields
+// the exact (d2, index)-ordered k-NN of any query inside C.
+
+__device__ __forceinline__ d3 bucket_center(const BucketParams& P, int cell) {
+  const int x = cell % P.g[0], y = (cell / P.g[0]) % P.g[1], z = cell / (P.g[0] * P.g[1]);
+  return d3{P.origin[0] + (x + 0.5) * P.h, P.origin[1] + (y + 0.5) * P.h, P.origin[2] + (z + 0.5) * P.h};
+}
+
+template <int K>
+__global__ void __launch_bounds__(128, 4) ccl_kernel(const BucketParams* __restrict__ Pp,
+                                                     const int* __restrict__ cell_start,
+                                                     const double4* __restrict__ sorted, int phase,
+                                                     int* __restrict__ count, int* __restrict__ len,
+                                                     int* __restrict__ ids, int64_t cap) {
+  __shared__ BucketParams sP;
+  if (threadIdx.x == 0) sP = *Pp;
+  __syncthreads();
+  const BucketParams P = sP;
+  const int ncells = P.g[0] * P.g[1] * P.g[2];
+  if (phase == 0 && blockIdx.x == 0 && threadIdx.x == 0) count[ncells] = 0;
+  const double hd = 0.5 * P.h * 1.7320508075688772 * 1.001;
+  for (int cell = blockIdx.x * blockDim.x + threadIdx.x; cell < ncells; cell += gridDim.x * blockDim.x) {
+    const d3 c = bucket_center(P, cell);
+    TopK<K> top;
+    top.init(K);
+    bucket_knn<K>(P, cell_start, sorted, c, top);
+    const double R = sqrt(top.worst_d()) + 2.0 * hd;
+    const double R2 = R * R * (1.0 + 1e-9) + 1e-300;
+    const double cq[3] = {c.x, c.y, c.z};
+    int lo[3], hi[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = clampi((int)floor((cq[a] - R - P.origin[a]) / P.h), 0, P.g[a] - 1);
+      hi[a] = clampi((int)floor((cq[a] + R - P.origin[a]) / P.h), 0, P.g[a] - 1);
+    }
+    int m = 0;
+    int64_t base = 0;
+    bool ok = true;
+    if (phase == 1) {
+      base = count[cell];
+      ok = len[cell] >= 0 && base + len[cell] <= cap;
+      if (!ok) {
+        len[cell] = -1;  // list does not fit: queries of this cell use the ring search
+        continue;
+      }
+    }
+    for (int z = lo[2]; z <= hi[2]; ++z)
+      for (int y = lo[1]; y <= hi[1]; ++y) {
+        const int row = (z * P.g[1] + y) * P.g[0];
+        const int b = cell_start[row + lo[0]], e = cell_start[row + hi[0] + 1];
+        for (int t = b; t < e; ++t) {
+          const double4 s = sorted[t];
+          if (sqdist(c, d3{s.x, s.y, s.z}) <= R2) {
+            if (phase == 1) ids[base + m] = (int)s.w;
+            ++m;
+          }
+        }
+      }
+    if (phase == 0) {
+      count[cell] = m;
+      len[cell] = m;
+    }
+  }
+}
+
+// exact k-NN of p from its cell's candidate list; false if p is outside the
+// grid box or the list was not materialised (caller falls back to the ring search)
+template <int K>
+__device__ __forceinline__ bool ccl_knn(const BucketParams& P, const int* __restrict__ start,
+                                        const int* __restrict__ len, const int* __restrict__ ids,
+                                        const double* __restrict__ pts, d3 p, TopK<K>& top) {
+  const double q[3] = {p.x, p.y, p.z};
+  int c[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double f = (q[a] - P.origin[a]) / P.h;
+    if (!(f >= 0.0) || f > (double)P.g[a]) return false;
+    c[a] = clampi((int)f, 0, P.g[a] - 1);
+  }
+  const int cell = (c[2] * P.g[1] + c[1]) * P.g[0] + c[0];
+  const int L = len[cell];
+  if (L < 0) return false;
+  const int b = start[cell];
+  for (int j = 0; j < L; ++j) {
+    const int id = ids[b + j];
+    top.insert(sqdist(p, load_d3(pts + 3 * (int64_t)id)), id);
+  }
+  return true;
+}
+
 // ------------------------------------------------------------------ k-NN + blend
 
 struct WarpArgs {
@@ -248,7 +342,10 @@ __global__ void __launch_bounds__(128, 4) knn_brute_kernel(WarpArgs A) {
 template <int K>
 __global__ void __launch_bounds__(128, 4) knn_bucket_kernel(WarpArgs A, const BucketParams* __restrict__ Pp,
                                                          const int* __restrict__ cell_start,
-                                                         const double4* __restrict__ sorted) {
+                                                         const double4* __restrict__ sorted,
+                                                         const int* __restrict__ ccl_start,
+                                                         const int* __restrict__ ccl_len,
+                                                         const int* __restrict__ ccl_ids) {
   __shared__ BucketParams sP;
   if (threadIdx.x == 0) sP = *Pp;
   __syncthreads();
@@ -257,7 +354,8 @@ __global__ void __launch_bounds__(128, 4) knn_bucket_kernel(WarpArgs A, const Bu
     const d3 p = load_d3(A.pts + 3 * q);
     TopK<K> top;
     top.init(A.k);
-    bucket_knn<K>(P, cell_start, sorted, p, top);
+    if (!ccl_ids || !ccl_knn<K>(P, ccl_start, ccl_len, ccl_ids, A.anchors, p, top))
+      bucket_knn<K>(P, cell_start, sorted, p, top);
     finish_query<K>(A, q, p, top);
   }
 }
@@ -266,7 +364,10 @@ template <int K>
 int launch_knn(const cf_buckets* b, const WarpArgs& A, cudaStream_t st) {
   const int block = 128;
   if (b) {
-    knn_bucket_kernel<K><<<cf::grid_for(A.n_pts, block, 8), block, 0, st>>>(A, b->params, b->cell_start, b->sorted);
+    const bool ccl = b->ccl_k >= K;
+    knn_bucket_kernel<K><<<cf::grid_for(A.n_pts, block, 8), block, 0, st>>>(
+        A, b->params, b->cell_start, b->sorted, ccl ? b->ccl_count : nullptr, ccl ? b->ccl_len : nullptr,
+        ccl ? b->ccl_ids : nullptr);
   } else {
     knn_brute_kernel<K><<<cf::grid_for(A.n_pts, block, 8), block, 0, st>>>(A);
   }
@@ -283,6 +384,7 @@ int buckets_build(cf_buckets* b, const double* pts, int64_t n, int grid_res, cud
   if (G <= 0) G = (int)std::ceil(std::cbrt((double)n / 2.0) * 2.0);
   G = std::max(1, std::min(G, b->max_grid_res));
   b->grid_res = G;
+  b->ccl_k = 0;  // candidate lists describe the previous point set
   const int64_t cells = (int64_t)G * G * G;
   if (n <= 65536 && cells <= (1 << 18)) {
     bucket_build_small_kernel<<<1, 1024, 0, st>>>(pts, (int)n, G, b->params, b->cell_start, b->point_cell,
@@ -322,6 +424,10 @@ int cf_buckets_create(int64_t max_points, int max_grid_res, cf_buckets_t** out) 
   if (e == cudaSuccess) e = cudaMalloc(&b->point_cell, sizeof(int) * max_points);
   if (e == cudaSuccess) e = cudaMalloc(&b->point_slot, sizeof(int) * max_points);
   if (e == cudaSuccess) e = cudaMalloc(&b->sorted, sizeof(double4) * max_points);
+  b->ccl_cap = std::max<int64_t>(max_points * 64, 1 << 20);
+  if (e == cudaSuccess) e = cudaMalloc(&b->ccl_count, sizeof(int) * (cells + 1));
+  if (e == cudaSuccess) e = cudaMalloc(&b->ccl_len, sizeof(int) * cells);
+  if (e == cudaSuccess) e = cudaMalloc(&b->ccl_ids, sizeof(int) * b->ccl_cap);
   if (e != cudaSuccess) {
     cf_buckets_destroy(b);
     return cf::fail(CF_E_CUDA, std::string("cf_buckets_create: ") + cudaGetErrorString(e));
@@ -337,8 +443,30 @@ int cf_buckets_destroy(cf_buckets_t* b) {
   cudaFree(b->point_cell);
   cudaFree(b->point_slot);
   cudaFree(b->sorted);
+  cudaFree(b->ccl_count);
+  cudaFree(b->ccl_len);
+  cudaFree(b->ccl_ids);
   delete b;
   return CF_OK;
+}
+
+int cf_buckets_build_candidates(cf_buckets_t* b, int k, void* stream) {
+  if (!b || b->grid_res == 0 || k < 1) return cf::fail(CF_E_BAD_ARG, "cf_buckets_build_candidates: bad args");
+  cudaStream_t st = cf::as_stream(stream);
+  const int64_t cells = (int64_t)b->grid_res * b->grid_res * b->grid_res;
+  const unsigned grid = cf::grid_for(cells, 128, 8);
+  b->ccl_k = 0;
+  const int rc = dispatch_k(k, [&]<int K>() {
+    ccl_kernel<K><<<grid, 128, 0, st>>>(b->params, b->cell_start, b->sorted, 0, b->ccl_count, b->ccl_len, nullptr,
+                                        b->ccl_cap);
+    bucket_scan_kernel<<<1, 1024, 0, st>>>(b->ccl_count, b->params);
+    ccl_kernel<K><<<grid, 128, 0, st>>>(b->params, b->cell_start, b->sorted, 1, b->ccl_count, b->ccl_len,
+                                        b->ccl_ids, b->ccl_cap);
+    return 0;
+  });
+  if (rc < 0) return cf::fail(CF_E_BAD_ARG, "cf_buckets_build_candidates: k must be 1..8 or 16");
+  b->ccl_k = k;
+  return cf::check_launch("cf_buckets_build_candidates");
 }
 
 int cf_buckets_build(cf_buckets_t* b, const double* pts, int64_t n, int grid_res, void* stream) {

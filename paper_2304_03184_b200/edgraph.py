@@ -81,12 +81,12 @@ class FrameMotion:
         self.live_buckets = None
         if buckets is not False and buckets is not None:
             self.live_buckets = buckets if isinstance(buckets, Buckets) else Buckets(self.n)
-            self.live_buckets.build(self.anchors)
+            self.live_buckets.build(self.anchors, candidates_k=self.k)
 
     def canonical_buckets(self) -> "Buckets":
         if self.canon_buckets is None:
             self.canon_buckets = Buckets(self.n)
-            self.canon_buckets.build(self.nodes)
+            self.canon_buckets.build(self.nodes, candidates_k=self.k)
         return self.canon_buckets
 
 
@@ -99,9 +99,14 @@ class Buckets:
         self.handle = h.value
         self.max_points = int(max_points)
 
-    def build(self, pts: torch.Tensor, grid_res: int = 0) -> None:
+    def build(self, pts: torch.Tensor, grid_res: int = 0, candidates_k: int = 0) -> None:
+        """Counting-sort `pts` into the grid; with candidates_k > 0 also build the
+        per-cell candidate lists for k-NN queries with k <= candidates_k."""
         self._pts = pts  # keep alive for stream-ordered use
         _lib.call("cf_buckets_build", self.handle, pts.data_ptr(), int(pts.shape[0]), int(grid_res), _lib.stream_ptr())
+        if candidates_k > 0:
+            _lib.call("cf_buckets_build_candidates", self.handle, int(min(candidates_k, pts.shape[0])),
+                      _lib.stream_ptr())
 
     def __del__(self):
         h = getattr(self, "handle", None)
