@@ -197,7 +197,9 @@ typedef struct cf_march_desc {
 } cf_march_desc;
 
 /* compacted samples of one field: records (capacity) = ray << 8 | i, grouped
- * per ray in ascending i; counters[0] = total emitted, counters[1] = overflow flag */
+ * per ray in ascending i; counters: int[4] — [0] = total emitted, [1] = overflow
+ * flag, [2..3] = work ticket of the per-sample kernels (zeroed by the producer,
+ * re-armed by each consumer launch) */
 typedef struct cf_march_out {
   uint32_t* records;
   int* ray_offset;

@@ -52,6 +52,20 @@ __device__ __forceinline__ bool ed_warp_point_smem(const double4* __restrict__ s
   return blend_apply<K>(top, dqs, k, r2, inverse, p, out);
 }
 
+// ballot of the nodes (w*32 + lane) whose nearest distance^2 to the box [lo, hi] is <= cut
+__device__ __forceinline__ unsigned cull_ballot(const float4* __restrict__ s_af, int n, int i, const float* lo,
+                                                const float* hi, float cut) {
+  bool cand = false;
+  if (i < n) {
+    const float4 a = s_af[i];
+    const float dx = fmaxf(fmaxf(lo[0] - a.x, a.x - hi[0]), 0.f);
+    const float dy = fmaxf(fmaxf(lo[1] - a.y, a.y - hi[1]), 0.f);
+    const float dz = fmaxf(fmaxf(lo[2] - a.z, a.z - hi[2]), 0.f);
+    cand = dx * dx + dy * dy + dz * dz <= cut;
+  }
+  return __ballot_sync(0xffffffffu, cand);
+}
+
 // Warp-cooperative culling for the exhaustive scan (all 32 lanes must call it,
 // `live` marks lanes holding a sample). The warp's samples are spatially
 // coherent (consecutive compacted samples of neighbouring rays), so:
@@ -60,8 +74,10 @@ __device__ __forceinline__ bool ed_warp_point_smem(const double4* __restrict__ s
 //     every sample in B has its k-th neighbour within U;
 //  3. only nodes whose nearest distance^2 to B is <= U (+ fp32 slack) can be
 //     in any lane's top-k; the warp walks that candidate set uniformly
-//     (ballot masks, smem broadcast reads), each lane ranking its own sample
+//     (ballot masks, smem broadcast reads): pass 1 ranks the candidates per
+//     lane in fp32, pass 2 re-ranks the few that can still be in the top-k
 //     exactly in float64. Identical result to scanning every node.
+// n <= 1024 (pass 1 packs the node index into 10 key bits).
 template <int K>
 __device__ __forceinline__ bool ed_warp_point_cull(const double4* __restrict__ s_anchors,
                                                    const float4* __restrict__ s_af, int n,
@@ -116,30 +132,66 @@ __device__ __forceinline__ bool ed_warp_point_cull(const double4* __restrict__ s
     }
   }
   const float cut = U + 2.0f * slack;
-  TopK<K> top;
-  top.init(k);
-  float bound = INF;
-  for (int c0 = 0; c0 < n; c0 += 32) {
-    const int i = c0 + lane;
-    bool cand = false;
-    if (i < n) {
-      const float4 a = s_af[i];
-      const float dx = fmaxf(fmaxf(lo[0] - a.x, a.x - hi[0]), 0.f);
-      const float dy = fmaxf(fmaxf(lo[1] - a.y, a.y - hi[1]), 0.f);
-      const float dz = fmaxf(fmaxf(lo[2] - a.z, a.z - hi[2]), 0.f);
-      cand = dx * dx + dy * dy + dz * dz <= cut;
-    }
-    unsigned mask = __ballot_sync(FULL, cand);
+  // Pass 1 (fp32 only): each lane keeps the L = K+2 smallest keys over the
+  // warp's candidate set, key = (fp32 d^2 bits with the low 10 mantissa bits
+  // replaced by the node index) — non-negative floats order as their bits, so
+  // one unsigned min/max pair per slot keeps the list sorted.
+  constexpr int L = K + 2;
+  unsigned key[L];
+#pragma unroll
+  for (int j = 0; j < L; ++j) key[j] = 0xffffffffu;
+  const int nw = (n + 31) >> 5;
+  for (int w = 0; w < nw; ++w) {
+    unsigned mask = cull_ballot(s_af, n, (w << 5) + lane, lo, hi, cut);
     while (mask) {
-      const int b = __ffs(mask) - 1;
+      const int node = (w << 5) + __ffs(mask) - 1;
       mask &= mask - 1;
-      const int node = c0 + b;
       const float4 af = s_af[node];
       const float ddx = px - af.x, ddy = py - af.y, ddz = pz - af.z;
-      if (ddx * ddx + ddy * ddy + ddz * ddz > bound) continue;
-      const double4 a = s_anchors[node];
-      top.insert(sqdist(p, d3{a.x, a.y, a.z}), node);
-      bound = (float)top.worst_d() * (1.0f + 4.0f * 1.1920929e-7f) + slack;
+      unsigned v = (__float_as_uint(ddx * ddx + ddy * ddy + ddz * ddz) & ~1023u) | (unsigned)node;
+#pragma unroll
+      for (int j = 0; j < L; ++j) {
+        const unsigned lo_v = min(v, key[j]);
+        v = max(v, key[j]);
+        key[j] = lo_v;
+      }
+    }
+  }
+  // Every node of the exact top-k has fp32 d^2 <= fcut: the k-th exact d^2 is
+  // <= (k-th smallest fp32 d^2) + slack <= trunc(key[K-1]) (1 + 2^-13) + slack,
+  // and each fp32 d^2 is within slack of its exact value. Truncation only lowers
+  // keys, so key <= fcut_key <=> trunc(fp32 d^2) <= fcut. The list is complete
+  // when its last slot is beyond fcut (or empty): every node outside it has a
+  // key >= key[L-1].
+  const float fcut = __uint_as_float(key[K - 1] & ~1023u) * (1.0f + 2.4414062e-4f) + 2.0f * slack;
+  const unsigned fcut_key = __float_as_uint(fcut) | 1023u;
+  const bool complete = key[L - 1] > fcut_key;
+  TopK<K> top;
+  top.init(k);
+  if (__all_sync(FULL, complete || !live)) {
+    // Pass 2: exact float64 ranking of the (typically k) survivors per lane
+#pragma unroll
+    for (int j = 0; j < L; ++j)
+      if (key[j] <= fcut_key) {
+        const int node = (int)(key[j] & 1023u);
+        const double4 a = s_anchors[node];
+        top.insert(sqdist(p, d3{a.x, a.y, a.z}), node);
+      }
+  } else {
+    // rare near-tie band wider than the list: exact scan of the candidate set
+    float bound = INF;
+    for (int w = 0; w < nw; ++w) {
+      unsigned mask = cull_ballot(s_af, n, (w << 5) + lane, lo, hi, cut);
+      while (mask) {
+        const int node = (w << 5) + __ffs(mask) - 1;
+        mask &= mask - 1;
+        const float4 af = s_af[node];
+        const float ddx = px - af.x, ddy = py - af.y, ddz = pz - af.z;
+        if (ddx * ddx + ddy * ddy + ddz * ddz > bound) continue;
+        const double4 a = s_anchors[node];
+        top.insert(sqdist(p, d3{a.x, a.y, a.z}), node);
+        bound = (float)top.worst_d() * (1.0f + 4.0f * 1.1920929e-7f) + slack;
+      }
     }
   }
   if (!live) return false;

@@ -14,7 +14,7 @@
 namespace {
 
 #ifndef CF_CANON_MINB
-#define CF_CANON_MINB 6  // resident CTAs/SM the canonicalisation kernel is compiled for
+#define CF_CANON_MINB 4  // resident CTAs/SM the canonicalisation kernel is compiled for
 #endif
 // graphs up to this many nodes are scanned exhaustively from shared memory
 // (cheaper than the bucket ring search's divergent loops at render sizes)
@@ -491,7 +491,7 @@ __global__ void __launch_bounds__(128) march_kernel(cf_march_desc M, const doubl
 template <int K, bool kSmem>
 __global__ void __launch_bounds__(128, CF_CANON_MINB) human_canon_kernel(cf_march_desc M, const double* __restrict__ dirs,
                                                           const uint32_t* __restrict__ records,
-                                                          const int* __restrict__ count, int64_t capacity,
+                                                          int* count, int64_t capacity,
                                                           cf_human_warp W, const BucketParams* __restrict__ EPp,
                                                           const int* __restrict__ ecs, const double4* __restrict__ es,
                                                           const BucketParams* __restrict__ LPp,
@@ -520,11 +520,17 @@ __global__ void __launch_bounds__(128, CF_CANON_MINB) human_canon_kernel(cf_marc
     if (threadIdx.x == 0) s_af[0].w = __uint_as_float(s_mag);
   }
   __syncthreads();
-  const int64_t n = min((int64_t)*count, capacity);
+  const int64_t n = min((int64_t)count[0], capacity);
   const d3 o{M.origin[0], M.origin[1], M.origin[2]};
-  // warp-uniform trip count (the culled scan is warp-cooperative)
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < n; base += stride) {
+  // warps pull 32-sample chunks from a ticket (count[2]): per-chunk cost varies
+  // (LBS fallback, candidate-set size), so static striding leaves a long tail.
+  // Warp-uniform trip count: the culled scan is warp-cooperative.
+  int* ticket = count + 2;
+  for (;;) {
+    int64_t base = 0;
+    if ((threadIdx.x & 31) == 0) base = atomicAdd(ticket, 32);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (base >= n) break;
     const int64_t s = base + (threadIdx.x & 31);
     const bool live = s < n;
     const uint32_t rec = live ? records[s] : 0u;
@@ -554,6 +560,15 @@ __global__ void __launch_bounds__(128, CF_CANON_MINB) human_canon_kernel(cf_marc
                       __double2float_rn(x_mul(x_sub(pt.y, W.canon_min[1]), W.inv_side)),
                       __double2float_rn(x_mul(x_sub(pt.z, W.canon_min[2]), W.inv_side)), flag);
     xu[s] = r;
+  }
+  // the last CTA out re-arms the ticket for the next launch on these counters
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(ticket + 1, 1) == (int)gridDim.x - 1) {
+      ticket[0] = 0;
+      ticket[1] = 0;
+    }
   }
 }
 
@@ -890,8 +905,8 @@ int cf_march(const cf_march_desc* M, const double* dirs, const uint32_t* human_b
   if (human && human_bits) H = *human;
   if (object && object_bits) O = *object;
   cudaStream_t st = cf::as_stream(stream);
-  if (H.records) CF_CHECK_CUDA(cudaMemsetAsync(H.counters, 0, 2 * sizeof(int), st));
-  if (O.records) CF_CHECK_CUDA(cudaMemsetAsync(O.counters, 0, 2 * sizeof(int), st));
+  if (H.records) CF_CHECK_CUDA(cudaMemsetAsync(H.counters, 0, 4 * sizeof(int), st));
+  if (O.records) CF_CHECK_CUDA(cudaMemsetAsync(O.counters, 0, 4 * sizeof(int), st));
   if (M->n_rays == 0) return CF_OK;
   march_kernel<<<cf::grid_for(M->n_rays, 128, 8), 128, 0, st>>>(*M, dirs, H.records ? human_bits : nullptr,
                                                                   O.records ? object_bits : nullptr, H, O);
@@ -906,17 +921,23 @@ int cf_human_canon(const cf_march_desc* M, const double* dirs, const cf_march_ou
     return cf::fail(CF_E_BAD_ARG, "cf_human_canon: bad args");
   const bool lbs = vert_buckets && W->vert_Tinv;
   cudaStream_t st = cf::as_stream(stream);
-  const unsigned grid = cf::grid_for(F->capacity, 128, 8);
   const size_t dsm = smem ? (sizeof(double4) + sizeof(float4)) * W->n_nodes : 0;
+  // persistent: exactly the resident CTAs (the ticket balances the work)
 #define CF_HC(KK, SM)                                                                                             \
+  int per_sm = 0;                                                                                                \
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, human_canon_kernel<KK, SM>, 128, dsm);                  \
+  const unsigned grid = cf::grid_for(F->capacity, 128, per_sm > 0 ? per_sm : 1);                                 \
   human_canon_kernel<KK, SM><<<grid, 128, dsm, st>>>(                                                            \
       *M, dirs, F->records, F->counters, F->capacity, *W, anchor_buckets ? anchor_buckets->params : nullptr,    \
       anchor_buckets ? anchor_buckets->cell_start : nullptr, anchor_buckets ? anchor_buckets->sorted : nullptr, \
       lbs ? vert_buckets->params : nullptr, lbs ? vert_buckets->cell_start : nullptr,                            \
       lbs ? vert_buckets->sorted : nullptr, xu)
   dispatch_k(W->k, [&]<int K>() {
-    if (smem) CF_HC(K, true);
-    else CF_HC(K, false);
+    if (smem) {
+      CF_HC(K, true);
+    } else {
+      CF_HC(K, false);
+    }
     return 0;
   });
 #undef CF_HC
@@ -947,7 +968,7 @@ int cf_train_sample(const cf_march_desc* M, const float* gt_depth, const uint8_t
       n_guided + n_uniform > 128 || n_empty > 128 || n_guided > 32)
     return cf::fail(CF_E_BAD_ARG, "cf_train_sample: bad args");
   cudaStream_t st = cf::as_stream(stream);
-  CF_CHECK_CUDA(cudaMemsetAsync(F->counters, 0, 2 * sizeof(int), st));
+  CF_CHECK_CUDA(cudaMemsetAsync(F->counters, 0, 4 * sizeof(int), st));
   if (M->n_rays == 0) return CF_OK;
   train_sample_kernel<<<cf::grid_for(M->n_rays, 128, 8), 128, 0, st>>>(*M, gt_depth, mask, n_guided, n_uniform,
                                                                         n_empty, sigma_d, seed, *F, t_out);

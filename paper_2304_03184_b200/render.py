@@ -191,7 +191,7 @@ class _FieldBuffers:
         self.records = torch.empty(capacity, dtype=torch.int32, device=device)
         self.ray_offset = torch.empty(n_rays, dtype=torch.int32, device=device)
         self.ray_count = torch.empty(n_rays, dtype=torch.int32, device=device)
-        self.counters = torch.zeros(2, dtype=torch.int32, device=device)
+        self.counters = torch.zeros(4, dtype=torch.int32, device=device)  # emitted, overflow, work ticket
         self.xu = torch.empty((capacity, 4), dtype=torch.float32, device=device)
         self.out = torch.empty((capacity, 4), dtype=torch.float32, device=device)
         self.rgb = torch.empty((n_rays, 3), dtype=torch.float32, device=device)
