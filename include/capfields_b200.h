@@ -52,6 +52,11 @@ int cf_version(void);
 const char* cf_last_error(void);
 /* number of SMs of the current device (grid sizing helper for hosts) */
 int cf_device_sm_count(void);
+/* self-test of the shared-denominator division used by the warp kernels:
+ * n random (a, b) pairs (seeded; log-uniform magnitudes incl. adversarial
+ * significands) divided both ways on the device; *mismatches = number of
+ * results not bit-equal to IEEE a / b. Synchronous. */
+int cf_selftest_exact_div(int64_t n, uint64_t seed, int64_t* mismatches);
 
 /* ---------------------------------------------------------------- deformation */
 

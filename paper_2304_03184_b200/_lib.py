@@ -97,6 +97,7 @@ _P = ctypes.POINTER
 # name -> argtypes (all return int status)
 _SIGS = {
     "cf_device_sm_count": [],
+    "cf_selftest_exact_div": [_i64, ctypes.c_uint64, ctypes.POINTER(_i64)],
     "cf_deform_nodes": [_p, _p, _i64, _p, _p],
     "cf_buckets_create": [_i64, _i32, ctypes.POINTER(_p)],
     "cf_buckets_destroy": [_p],

@@ -41,6 +41,29 @@ __device__ __forceinline__ double x_add(double a, double b) { return __dadd_rn(a
 __device__ __forceinline__ double x_sub(double a, double b) { return __dadd_rn(a, -b); }
 __device__ __forceinline__ double x_div(double a, double b) { return __ddiv_rn(a, b); }
 
+// Correctly rounded a / b for many numerators over one denominator: with
+// y = RN(1/b) and the faithful q = RN(a*y), the exact residual r = a - b*q
+// (one FMA) gives RN(a/b) = RN(q + r*y) (Markstein's theorem; __ddiv_rn ends
+// with the same correction step after refining y). Bit-equal to x_div; the
+// residual is exact only away from the subnormal range, so tiny or huge
+// operands take __ddiv_rn.
+struct ExactDiv {
+  double b, y;
+  bool fast;
+  __device__ __forceinline__ explicit ExactDiv(double b_) : b(b_) {
+    y = __drcp_rn(b_);
+    const double ab = fabs(b_);
+    fast = ab > 0x1p-500 && ab < 0x1p500;
+  }
+  __device__ __forceinline__ double operator()(double a) const {
+    const double aa = fabs(a);
+    if (!fast || !(aa < 0x1p500) || (aa < 0x1p-500 && a != 0.0)) return __ddiv_rn(a, b);
+    const double q = __dmul_rn(a, y);
+    const double r = __fma_rn(-q, b, a);
+    return r == 0.0 ? q : __fma_rn(r, y, q);  // r == 0: q exact (keeps the sign of a zero quotient)
+  }
+};
+
 __device__ __forceinline__ float f_mul(float a, float b) { return __fmul_rn(a, b); }
 __device__ __forceinline__ float f_add(float a, float b) { return __fadd_rn(a, b); }
 __device__ __forceinline__ float f_sub(float a, float b) { return __fadd_rn(a, -b); }

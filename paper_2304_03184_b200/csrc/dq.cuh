@@ -81,10 +81,11 @@ __device__ __forceinline__ dq8 dq_normalize(const dq8& q) {
   double n = sqrt(x_add(x_add(x_add(x_mul(q.r[0], q.r[0]), x_mul(q.r[1], q.r[1])), x_mul(q.r[2], q.r[2])),
                        x_mul(q.r[3], q.r[3])));
   dq8 o;
+  const ExactDiv by_n(n);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    o.r[i] = x_div(q.r[i], n);
-    o.d[i] = x_div(q.d[i], n);
+    o.r[i] = by_n(q.r[i]);
+    o.d[i] = by_n(q.d[i]);
   }
   double s = x_add(x_add(x_add(x_mul(o.r[0], o.d[0]), x_mul(o.r[1], o.d[1])), x_mul(o.r[2], o.d[2])),
                   x_mul(o.r[3], o.d[3]));

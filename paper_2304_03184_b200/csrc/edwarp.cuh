@@ -203,10 +203,11 @@ __device__ __forceinline__ bool blend_apply(const TopK<K>& top, const double* __
                                             bool inverse, d3 p, d3& out) {
   double w[K];
   bool valid = false;
+  const ExactDiv by_r2(r2);
 #pragma unroll
   for (int j = 0; j < K; ++j)
     if (j < k) {
-      w[j] = exp(x_div(-top.d[j], r2));
+      w[j] = exp(by_r2(-top.d[j]));
       valid |= w[j] > 1e-6;
     }
   DqbAcc acc;

@@ -244,3 +244,13 @@ def test_lbs_backward_vs_oracle():
     lb.set_pose(np.tile(np.eye(4), (24, 1, 1)))
     _, pc0, _ = lb(q)
     assert np.allclose(pc0, q, atol=1e-12)
+
+
+def test_shared_denominator_division_is_ieee_exact():
+    """ExactDiv (rcp + one Markstein correction), used for the DQB weights and
+    normalisation in every warp kernel, equals IEEE a / b bit for bit."""
+    from paper_2304_03184_b200 import _lib
+
+    bad = _lib.ctypes.c_int64(-1)
+    _lib.call("cf_selftest_exact_div", 1 << 24, 20240607, _lib.ctypes.byref(bad))
+    assert bad.value == 0
