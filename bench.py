@@ -153,6 +153,14 @@ class ClockSampler:
 
 # ----------------------------------------------------------------- workload
 
+# stage -> the mark it is timed from (render.py Renderer._launch_view order)
+STAGE_PRED = {"lbs_setup": "start", "ed_setup": "start", "rays": "ed_setup", "march": "rays",
+              "object_canon": "march", "object_field": "object_canon", "object_composite": "object_field",
+              "human_canon": "march", "human_hash_d": "human_canon", "human_deform_mlp": "human_hash_d",
+              "human_hash_c": "human_deform_mlp", "human_color_mlp": "human_hash_c",
+              "human_composite": "human_color_mlp", "layers": "human_composite"}
+
+
 def build_workload(args, rank):
     from paper_2304_03184_b200.render import HumanField, ObjectField, RenderConfig, Renderer
     from paper_2304_03184_b200.scene import Scene, SceneConfig
@@ -207,19 +215,17 @@ def run_ours(args, rank, world, pg):
     torch.cuda.synchronize()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    stage_marks = []
     processed = 0
     with ClockSampler(torch.cuda.current_device()) as clk:
+        t_issue = time.perf_counter()
         for k in range(args.steps):
             fi = (k + rank) % nF
             flush.zero_()
-            r.marks = [(0, "start", starts[k])]
             starts[k].record()
             step(fi, dframes)
             ends[k].record()
-            stage_marks.append(r.marks)
-            r.marks = None
             processed += counts[fi][0] + counts[fi][1]
+        t_issue = time.perf_counter() - t_issue  # host time to enqueue K steps (GPU starves if > device time)
         torch.cuda.synchronize()
     barrier(pg)
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
@@ -229,20 +235,22 @@ def run_ours(args, rank, world, pg):
     value = processed_all / (ms_total / 1e3)
     ms_per_step = ms_total / args.steps
 
-    # per-stage times (CUDA events on the launching stream inside the timed region)
+    # per-stage times: the same steps replayed from a graph variant that records an
+    # event after every stage on the stream it ran on (read after each step);
     # each stage is timed from the mark it depends on (the two streams interleave)
-    pred = {"lbs_setup": "start", "ed_setup": "start", "rays": "ed_setup", "march": "rays",
-            "object_canon": "march", "object_field": "object_canon", "object_composite": "object_field",
-            "human_canon": "march", "human_hash_d": "human_canon", "human_deform_mlp": "human_hash_d",
-            "human_hash_c": "human_deform_mlp", "human_color_mlp": "human_hash_c", "human_composite": "human_color_mlp",
-            "layers": "human_composite"}
-    stages = {}
-    for marks in stage_marks:
-        ev = {name: e for _, name, e in marks}
-        for name, p in pred.items():
-            if name in ev and p in ev:
-                stages.setdefault(name, []).append(ev[p].elapsed_time(ev[name]))
-    stage_ms = {k: float(np.mean(v)) for k, v in stages.items()}
+    stage_marks = []
+    for k in range(min(args.steps, 50)):
+        flush.zero_()
+        r.marks = []
+        step((k + rank) % nF, dframes)
+        torch.cuda.synchronize()
+        stage_marks.append([(name, e) for _, name, e in r.marks])
+        r.marks = None
+        ev = dict(stage_marks[-1])
+        stage_marks[-1] = {name: ev[p].elapsed_time(ev[name]) for name, p in STAGE_PRED.items()
+                           if name in ev and p in ev}
+    stage_ms = {name: float(np.mean([m[name] for m in stage_marks if name in m]))
+                for name in STAGE_PRED if any(name in m for m in stage_marks)}
 
     # ---- e2e: pinned host prior -> device, render through the public API, image -> pinned host
     e2e = None
@@ -323,6 +331,7 @@ def run_ours(args, rank, world, pg):
         "ms_per_frame": ms_per_step,
         "nominal_samples_per_s": (r.n_rays * args.samples * args.steps * world) / (ms_total / 1e3),
         "stage_ms": stage_ms,
+        "host_issue_ms_per_step": t_issue * 1e3 / args.steps,
         "roofline": roof,
         "gpu_launches": KERNELS_PER_STEP * args.steps,
         "e2e": e2e,
@@ -390,6 +399,7 @@ def _live_on_host(r, hf, cfg, frames, fid):
     if dev is not None:
         r.load_prior(torch.from_numpy(f["dqs"]).to(dev), torch.from_numpy(f["A"]).to(dev),
                      torch.from_numpy(f["dbias"]).to(dev))
+        r.prepare_frame()
         torch.cuda.synchronize()
         return orr.unpack_bits(r.live_bits.cpu().numpy().view(np.uint32), cfg.live_occ_res ** 3)
     raise RuntimeError("live occupancy needs the device setup")

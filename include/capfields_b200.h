@@ -176,6 +176,9 @@ typedef struct cf_camera {
   double R[9];
   double fx, fy, cx, cy;
   int width, height;
+  const double* params; /* optional device double[13] = R[9], fx, fy, cx, cy read by the kernel
+                           instead of the fields above (a captured CUDA graph replays with new
+                           cameras by rewriting this block); NULL = use the fields */
 } cf_camera;
 
 /* cubic occupancy bit grid: res^3 cells of edge `cell` from `min`, x-major
@@ -199,6 +202,9 @@ typedef struct cf_march_desc {
   const int* human_cell_bbox;      /* device int[6] (lo xyz, hi xyz) of set live cells, or NULL */
   const double* sample_t;          /* training: explicit depth of compacted sample s (NULL = uniform t_i);
                                       delta_s = t_{s+1} - t_s within a ray, dt for its last sample */
+  const double* frame;             /* optional device double[15] = origin[3], obj_R[9], obj_t[3] read by
+                                      the kernels instead of the fields (graph-replayable frames);
+                                      NULL = use the fields */
 } cf_march_desc;
 
 /* compacted samples of one field: records (capacity) = ray << 8 | i, grouped

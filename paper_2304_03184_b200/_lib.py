@@ -51,7 +51,8 @@ class HashGridDesc(ctypes.Structure):
 
 class Camera(ctypes.Structure):
     _fields_ = [("R", ctypes.c_double * 9), ("fx", ctypes.c_double), ("fy", ctypes.c_double),
-                ("cx", ctypes.c_double), ("cy", ctypes.c_double), ("width", ctypes.c_int), ("height", ctypes.c_int)]
+                ("cx", ctypes.c_double), ("cy", ctypes.c_double), ("width", ctypes.c_int), ("height", ctypes.c_int),
+                ("params", ctypes.c_void_p)]
 
 
 class OccGrid(ctypes.Structure):
@@ -63,7 +64,7 @@ class MarchDesc(ctypes.Structure):
                 ("t_near", ctypes.c_double), ("t_far", ctypes.c_double), ("dt", ctypes.c_double),
                 ("human_grid", OccGrid), ("object_grid", OccGrid), ("obj_R", ctypes.c_double * 9),
                 ("obj_t", ctypes.c_double * 3), ("obj_min", ctypes.c_double * 3), ("obj_inv_side", ctypes.c_double),
-                ("human_cell_bbox", ctypes.c_void_p), ("sample_t", ctypes.c_void_p)]
+                ("human_cell_bbox", ctypes.c_void_p), ("sample_t", ctypes.c_void_p), ("frame", ctypes.c_void_p)]
 
 
 class MarchOut(ctypes.Structure):

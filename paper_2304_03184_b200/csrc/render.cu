@@ -51,6 +51,21 @@ __device__ __forceinline__ double sample_t(const cf_march_desc& M, int i) {
 __device__ __forceinline__ double rec_t(const cf_march_desc& M, int64_t s, uint32_t rec) {
   return M.sample_t ? M.sample_t[s] : sample_t(M, (int)(rec & 255u));
 }
+// per-frame values into shared memory: origin s[0..2], object pose R s[3..11],
+// t s[12..14] — from the device frame block when set (a captured graph replays
+// frames by rewriting it), else from the by-value descriptor. Block-wide.
+__device__ __forceinline__ void load_frame(const cf_march_desc& M, double* s) {
+  if (threadIdx.x == 0) {  // constant indices only: no local copy of the by-value descriptor
+#pragma unroll
+    for (int i = 0; i < 3; ++i) s[i] = M.frame ? M.frame[i] : M.origin[i];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) s[3 + i] = M.frame ? M.frame[3 + i] : M.obj_R[i];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) s[12 + i] = M.frame ? M.frame[12 + i] : M.obj_t[i];
+  }
+  __syncthreads();
+}
+
 __device__ __forceinline__ d3 sample_p(d3 o, d3 d, double t) {
   return d3{x_add(o.x, x_mul(t, d.x)), x_add(o.y, x_mul(t, d.y)), x_add(o.z, x_mul(t, d.z))};
 }
@@ -64,18 +79,32 @@ __device__ __forceinline__ d3 to_object(const double* R, const double* t, d3 p) 
 }
 
 __global__ void rays_kernel(cf_camera cam, double* __restrict__ dirs) {
-  const int64_t n = (int64_t)cam.width * cam.height;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const double u = (double)(i % cam.width), v = (double)(i / cam.width);
-    const double dc[3] = {x_div(x_sub(u, cam.cx), cam.fx), x_div(x_sub(v, cam.cy), cam.fy), 1.0};
+  __shared__ double s_cam[13];  // R[9], fx, fy, cx, cy
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < 9; ++i) s_cam[i] = cam.params ? cam.params[i] : cam.R[i];
+    s_cam[9] = cam.params ? cam.params[9] : cam.fx;
+    s_cam[10] = cam.params ? cam.params[10] : cam.fy;
+    s_cam[11] = cam.params ? cam.params[11] : cam.cx;
+    s_cam[12] = cam.params ? cam.params[12] : cam.cy;
+  }
+  __syncthreads();
+  const double* R = s_cam;
+  const double cx = s_cam[11], cy = s_cam[12];
+  const int n = cam.width * cam.height;
+  const ExactDiv by_fx(s_cam[9]), by_fy(s_cam[10]);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int v_i = i / cam.width;
+    const double u = (double)(i - v_i * cam.width), v = (double)v_i;
+    const double dc[3] = {by_fx(x_sub(u, cx)), by_fy(x_sub(v, cy)), 1.0};
     double d[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a)
-      d[a] = __fma_rn(dc[2], cam.R[3 * a + 2], __fma_rn(dc[1], cam.R[3 * a + 1], x_mul(dc[0], cam.R[3 * a])));
-    const double nrm = sqrt(x_add(x_add(x_mul(d[0], d[0]), x_mul(d[1], d[1])), x_mul(d[2], d[2])));
-    dirs[3 * i] = x_div(d[0], nrm);
-    dirs[3 * i + 1] = x_div(d[1], nrm);
-    dirs[3 * i + 2] = x_div(d[2], nrm);
+      d[a] = __fma_rn(dc[2], R[3 * a + 2], __fma_rn(dc[1], R[3 * a + 1], x_mul(dc[0], R[3 * a])));
+    const ExactDiv by_nrm(sqrt(x_add(x_add(x_mul(d[0], d[0]), x_mul(d[1], d[1])), x_mul(d[2], d[2]))));
+    dirs[3 * (int64_t)i] = by_nrm(d[0]);
+    dirs[3 * (int64_t)i + 1] = by_nrm(d[1]);
+    dirs[3 * (int64_t)i + 2] = by_nrm(d[2]);
   }
 }
 
@@ -410,7 +439,11 @@ __global__ void __launch_bounds__(128) march_kernel(cf_march_desc M, const doubl
                                                     const uint32_t* __restrict__ hbits,
                                                     const uint32_t* __restrict__ obits, cf_march_out H,
                                                     cf_march_out O) {
-  const d3 o{M.origin[0], M.origin[1], M.origin[2]};
+  __shared__ double s_fr[15];
+  load_frame(M, s_fr);
+  const double* obj_R = s_fr + 3;
+  const double* obj_t = s_fr + 12;
+  const d3 o{s_fr[0], s_fr[1], s_fr[2]};
   // boxes that contain every set cell: the live cell bbox, the object grid
   double hlo[3], hhi[3], olo[3], ohi[3];
   bool hempty = false;
@@ -426,7 +459,7 @@ __global__ void __launch_bounds__(128) march_kernel(cf_march_desc M, const doubl
     olo[a] = M.object_grid.min[a];
     ohi[a] = M.object_grid.min[a] + M.object_grid.res * M.object_grid.cell;
   }
-  const d3 oo = to_object(M.obj_R, M.obj_t, o);
+  const d3 oo = to_object(obj_R, obj_t, o);
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < M.n_rays; base += (int64_t)gridDim.x * blockDim.x) {
     const int64_t ray = base + threadIdx.x;
     const bool live = ray < M.n_rays;
@@ -444,13 +477,13 @@ __global__ void __launch_bounds__(128) march_kernel(cf_march_desc M, const doubl
     }
     if (live && obits) {
       // the object box is clipped in object space: ray (R^T (o - t), R^T d)
-      const d3 od{d.x * M.obj_R[0] + d.y * M.obj_R[3] + d.z * M.obj_R[6],
-                  d.x * M.obj_R[1] + d.y * M.obj_R[4] + d.z * M.obj_R[7],
-                  d.x * M.obj_R[2] + d.y * M.obj_R[5] + d.z * M.obj_R[8]};
+      const d3 od{d.x * obj_R[0] + d.y * obj_R[3] + d.z * obj_R[6],
+                  d.x * obj_R[1] + d.y * obj_R[4] + d.z * obj_R[7],
+                  d.x * obj_R[2] + d.y * obj_R[5] + d.z * obj_R[8]};
       int i0, i1;
       sample_range(M, oo, od, olo, ohi, i0, i1);
       for (int i = i0; i <= i1; ++i)
-        if (occ_test(M.object_grid, obits, to_object(M.obj_R, M.obj_t, sample_p(o, d, sample_t(M, i))))) {
+        if (occ_test(M.object_grid, obits, to_object(obj_R, obj_t, sample_p(o, d, sample_t(M, i))))) {
           om[i >> 5] |= 1u << (i & 31);
           ++oc;
         }
@@ -520,8 +553,10 @@ __global__ void __launch_bounds__(128, CF_CANON_MINB) human_canon_kernel(cf_marc
     if (threadIdx.x == 0) s_af[0].w = __uint_as_float(s_mag);
   }
   __syncthreads();
+  __shared__ double s_fr[15];
+  load_frame(M, s_fr);
   const int64_t n = min((int64_t)count[0], capacity);
-  const d3 o{M.origin[0], M.origin[1], M.origin[2]};
+  const d3 o{s_fr[0], s_fr[1], s_fr[2]};
   // warps pull 32-sample chunks from a ticket (count[2]): per-chunk cost varies
   // (LBS fallback, candidate-set size), so static striding leaves a long tail.
   // Warp-uniform trip count: the culled scan is warp-cooperative.
@@ -577,12 +612,14 @@ __global__ void object_canon_kernel(cf_march_desc M, const double* __restrict__ 
                                     const uint32_t* __restrict__ records, const int* __restrict__ count,
                                     int64_t capacity, const double* obj_min, double inv_side,
                                     float4* __restrict__ xu) {
+  __shared__ double s_fr[15];
+  load_frame(M, s_fr);
   const int64_t n = min((int64_t)*count, capacity);
-  const d3 o{M.origin[0], M.origin[1], M.origin[2]};
+  const d3 o{s_fr[0], s_fr[1], s_fr[2]};
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t rec = records[s];
     const int64_t ray = rec >> 8;
-    const d3 p = to_object(M.obj_R, M.obj_t, sample_p(o, load_d3(dirs + 3 * ray), rec_t(M, s, rec)));
+    const d3 p = to_object(s_fr + 3, s_fr + 12, sample_p(o, load_d3(dirs + 3 * ray), rec_t(M, s, rec)));
     xu[s] = make_float4(__double2float_rn(x_mul(x_sub(p.x, M.obj_min[0]), M.obj_inv_side)),
                         __double2float_rn(x_mul(x_sub(p.y, M.obj_min[1]), M.obj_inv_side)),
                         __double2float_rn(x_mul(x_sub(p.z, M.obj_min[2]), M.obj_inv_side)), 1.0f);
@@ -810,9 +847,10 @@ __global__ void layers_kernel(int64_t n, const float* __restrict__ hr, const flo
 extern "C" {
 
 int cf_camera_rays(const cf_camera* cam, double* dirs, void* stream) {
-  if (!cam || cam->width < 1 || cam->height < 1 || !dirs) return cf::fail(CF_E_BAD_ARG, "cf_camera_rays: bad args");
+  if (!cam || cam->width < 1 || cam->height < 1 || !dirs || (int64_t)cam->width * cam->height > INT32_MAX)
+    return cf::fail(CF_E_BAD_ARG, "cf_camera_rays: bad args");
   const int64_t n = (int64_t)cam->width * cam->height;
-  rays_kernel<<<cf::grid_for(n, 256, 4), 256, 0, cf::as_stream(stream)>>>(*cam, dirs);
+  rays_kernel<<<cf::grid_for(n, 256, 8), 256, 0, cf::as_stream(stream)>>>(*cam, dirs);
   return cf::check_launch("cf_camera_rays");
 }
 

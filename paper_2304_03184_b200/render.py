@@ -2,11 +2,16 @@
 render path (canonicalize_human SPEC.md:372-380, volume_render :381-389,
 render_view :399-407, composite :555-563) with occupancy skipping.
 
-Per frame (host orchestrates, every step a CUDA kernel, stream-ordered, no host
-sync):  deformed nodes + live buckets -> backward-LBS vertex transforms ->
-live occupancy splat ; per view: rays -> march (occupancy-skipped compaction) ->
-canonicalise (ED DQB^-1 / LBS fallback | rigid) -> fused field (hash + tcgen05
-MLPs) -> front-to-back composite -> depth-occlusion layer composite.
+Per frame (every step a CUDA kernel, stream-ordered, no host sync): deformed
+nodes + live buckets -> backward-LBS vertex transforms -> live occupancy splat ;
+per view: rays -> march (occupancy-skipped compaction) -> canonicalise (ED
+DQB^-1 / LBS fallback | rigid) -> fused field (hash + tcgen05 MLPs) ->
+front-to-back composite -> depth-occlusion layer composite.
+
+The launch sequence is static: per-frame inputs live in fixed device buffers
+(prior tensors, a 28-double frame block holding the camera and object pose), so
+it is captured once into a CUDA graph and replayed per view — the host cost of a
+frame is a few small copies and one graph launch instead of ~25 launches.
 """
 from __future__ import annotations
 
@@ -43,6 +48,7 @@ class RenderConfig:
     obj_occ_res: int = 64
     obj_shell: float = 0.02
     background: tuple = (24 / 255.0, 28 / 255.0, 34 / 255.0)   # config.py bg_r/g/b
+    cuda_graphs: bool = True      # replay the captured frame (False: launch every kernel each view)
 
 
 def _kaiming(rng, n_out, n_in):
@@ -186,6 +192,9 @@ class ObjectField:
         return d
 
 
+_FRAME_DOUBLES = 28
+
+
 class _FieldBuffers:
     def __init__(self, n_rays, capacity, device):
         self.records = torch.empty(capacity, dtype=torch.int32, device=device)
@@ -240,6 +249,18 @@ class Renderer:
         self._lbs_done = torch.cuda.Event()
         self._obj_done = torch.cuda.Event()
         self._lbs_done.record(torch.cuda.current_stream())
+        # frame block: origin[3], obj_R[9], obj_t[3] | camera R[9], fx, fy, cx, cy
+        self.frame_dev = torch.zeros(_FRAME_DOUBLES, dtype=torch.float64, device=d)
+        self._frame_host = np.zeros(_FRAME_DOUBLES)
+        self._staging = [torch.zeros(_FRAME_DOUBLES, dtype=torch.float64).pin_memory() for _ in range(4)]
+        self._staging_ev = [None] * len(self._staging)
+        self._slot = 0
+        self.M.frame = self.frame_dev.data_ptr()
+        self.cam = _lib.Camera()
+        self.cam.width, self.cam.height = self.W, self.H
+        self.cam.params = self.frame_dev.data_ptr() + 15 * 8
+        self._setup_pending = False   # per-frame human setup still to run (load_prior since the last view)
+        self._graphs = {}             # (with_setup,) -> torch.cuda.CUDAGraph
 
     # -- per-frame setup ------------------------------------------------------
 
@@ -254,9 +275,10 @@ class Renderer:
             self.set_object_pose(obj_R, obj_t)
 
     def load_prior(self, dqs: torch.Tensor, bone_A: torch.Tensor, dbias: torch.Tensor) -> None:
-        """Per-frame human setup from device-resident prior tensors (no host sync):
-        node dqs (n,8) f64, bone transforms (J,4,4) f64, DeformNet pose bias (128,) f32."""
-        s = _lib.stream_ptr()
+        """Per-frame human prior from device-resident tensors (no host sync): node
+        dqs (n,8) f64, bone transforms (J,4,4) f64, DeformNet pose bias (128,) f32.
+        Staged into the renderer's fixed buffers; the setup kernels run with the
+        next view (inside its graph)."""
         h = self.human
         if getattr(self, "_dqs", None) is None:
             n = len(h.graph.nodes)
@@ -268,6 +290,27 @@ class Renderer:
         self._dqs.copy_(dqs, non_blocking=True)
         self._A.copy_(bone_A, non_blocking=True)
         self.dbias.copy_(dbias, non_blocking=True)
+        if getattr(self, "hw", None) is None:
+            w = _lib.HumanWarp()
+            w.dqs = self._dqs.data_ptr()
+            w.k = self.cfg.ed_k
+            w.r2 = self.cfg.ed_radius ** 2
+            w.vert_Tinv = h.lbs.Tinv.data_ptr()
+            w.lbs_max_d2 = self.cfg.lbs_max_dist ** 2
+            for a in range(3):
+                w.canon_min[a] = h.canon_min[a]
+            w.inv_side = h.inv_side
+            w.anchors = self._anchors.data_ptr()
+            w.n_nodes = int(self._anchors.shape[0])
+            self.hw = w
+            self.hdesc = h.desc(self.dbias)
+        self._setup_pending = True
+
+    def _human_setup(self) -> None:
+        """The frame's human setup kernels: backward-LBS chain on the side stream,
+        deformed nodes + live occupancy splat on the current stream."""
+        s = _lib.stream_ptr()
+        h = self.human
         n = self._dqs.shape[0]
         # the backward-LBS chain (vertex transforms, posed vertices, their buckets)
         # is independent of the ED chain: run it on the side stream
@@ -285,44 +328,43 @@ class Renderer:
                   _lib.byref(self.live_occ), self.live_scratch.data_ptr(), self.live_bits.data_ptr(),
                   self.live_bbox.data_ptr(), s)
         self._mark("ed_setup")
-        if getattr(self, "hw", None) is None:
-            w = _lib.HumanWarp()
-            w.dqs = self._dqs.data_ptr()
-            w.k = self.cfg.ed_k
-            w.r2 = self.cfg.ed_radius ** 2
-            w.vert_Tinv = h.lbs.Tinv.data_ptr()
-            w.lbs_max_d2 = self.cfg.lbs_max_dist ** 2
-            for a in range(3):
-                w.canon_min[a] = h.canon_min[a]
-            w.inv_side = h.inv_side
-            w.anchors = self._anchors.data_ptr()
-            w.n_nodes = int(self._anchors.shape[0])
-            self.hw = w
-            self.hdesc = h.desc(self.dbias)
 
     def set_object_pose(self, obj_R, obj_t) -> None:
-        """Object-to-world pose of the frame (kernel parameters, no device copy)."""
-        R = np.asarray(obj_R, dtype=np.float64).reshape(9)
-        t = np.asarray(obj_t, dtype=np.float64).reshape(3)
-        for i in range(9):
-            self.M.obj_R[i] = R[i]
-        for i in range(3):
-            self.M.obj_t[i] = t[i]
+        """Object-to-world pose of the frame (frame block, uploaded with the next view)."""
+        self._frame_host[3:12] = np.asarray(obj_R, dtype=np.float64).reshape(9)
+        self._frame_host[12:15] = np.asarray(obj_t, dtype=np.float64).reshape(3)
         if getattr(self, "odesc", None) is None:
             self.odesc = self.obj.desc()
 
     # -- per-view --------------------------------------------------------------
 
     def rays(self, R, t, fx, fy, cx, cy):
-        cam = _lib.Camera()
-        Rf = np.asarray(R, dtype=np.float64).reshape(9)
-        for i in range(9):
-            cam.R[i] = Rf[i]
-        cam.fx, cam.fy, cam.cx, cam.cy = float(fx), float(fy), float(cx), float(cy)
-        cam.width, cam.height = self.W, self.H
-        _lib.call("cf_camera_rays", _lib.byref(cam), self.dirs.data_ptr(), _lib.stream_ptr())
-        for a in range(3):
-            self.M.origin[a] = float(t[a])
+        """Camera of the view (frame block) and its ray directions."""
+        self._set_camera(R, t, fx, fy, cx, cy)
+        self._upload_frame()
+        self._rays()
+
+    def _set_camera(self, R, t, fx, fy, cx, cy):
+        self._frame_host[0:3] = np.asarray(t, dtype=np.float64).reshape(3)
+        self._frame_host[15:24] = np.asarray(R, dtype=np.float64).reshape(9)
+        self._frame_host[24:28] = (float(fx), float(fy), float(cx), float(cy))
+
+    def _upload_frame(self):
+        """Frame block -> device through a ring of pinned staging slots (a slot is
+        reused only after its previous copy completed)."""
+        i = self._slot
+        self._slot = (i + 1) % len(self._staging)
+        if self._staging_ev[i] is not None:
+            self._staging_ev[i].synchronize()
+        buf = self._staging[i]
+        buf.numpy()[:] = self._frame_host
+        self.frame_dev.copy_(buf, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._staging_ev[i] = ev
+
+    def _rays(self):
+        _lib.call("cf_camera_rays", _lib.byref(self.cam), self.dirs.data_ptr(), _lib.stream_ptr())
         self.M.n_rays = self.n_rays
 
     def _scratch(self, buf, desc) -> torch.Tensor:
@@ -338,7 +380,8 @@ class Renderer:
         (stream id, name, event); a stage's time is the gap to the previous mark
         of the same stream."""
         if self.marks is not None:
-            e = torch.cuda.Event(enable_timing=True)
+            # inside a graph capture: an external event, recorded by every replay
+            e = torch.cuda.Event(enable_timing=True, external=getattr(self, "_capturing", False))
             st = torch.cuda.current_stream()
             e.record(st)
             self.marks.append((st.cuda_stream, name, e))
@@ -349,11 +392,59 @@ class Renderer:
         ev.record(src)
         dst.wait_event(ev)
 
+    def prepare_frame(self) -> None:
+        """Run the pending per-frame human setup now (eager launches) — for callers
+        that use the frame's warp state without rendering a view (training)."""
+        if self._setup_pending and self.human is not None:
+            self._human_setup()
+        self._setup_pending = False
+
     def render(self, R, t, fx, fy, cx, cy):
         """All stages of one novel view; returns the composited image tensor (H*W, 3).
-        If `self.marks` is a list, a CUDA event is appended after each stage."""
+        Replays the captured graph of the view (cfg.cuda_graphs). If `self.marks` is
+        a list, it is replaced by [(stream, name, event)] for "start" and each stage
+        (read them after synchronizing, before the next view)."""
+        self._set_camera(R, t, fx, fy, cx, cy)
+        self._upload_frame()
+        setup = self._setup_pending and self.human is not None
+        self._setup_pending = False
+        timed = self.marks is not None
+        key = (setup, timed)
+        if not self.cfg.cuda_graphs or (key not in self._graphs and not getattr(self, "_eager_done", False)):
+            # eager launches (also the first view: lazily allocated state must exist before capture)
+            if timed:
+                self.marks = []
+                self._mark("start")
+            self._launch_view(setup)
+            self._eager_done = True
+            return self.image
+        if key not in self._graphs:
+            g = torch.cuda.CUDAGraph()
+            main = torch.cuda.current_stream()
+            cap = torch.cuda.Stream(device=self.dirs.device)
+            self._fork(main, cap)
+            self._capturing = True
+            try:
+                with torch.cuda.graph(g, stream=cap, capture_error_mode="thread_local"):
+                    if timed:
+                        self.marks = []
+                        self._mark("start")
+                    self._launch_view(setup)
+            finally:
+                self._capturing = False
+            main.wait_stream(cap)
+            self._graphs[key] = (g, self.marks if timed else None)
+        g, marks = self._graphs[key]
+        g.replay()
+        if timed:
+            self.marks = marks
+        return self.image
+
+    def _launch_view(self, setup: bool):
         s = _lib.stream_ptr()
-        self.rays(R, t, fx, fy, cx, cy)
+        if setup:
+            self._human_setup()
+        self._rays()
         hb, ob = self.hb, self.ob
         self._mark("rays")
         _lib.call("cf_march", _lib.byref(self.M), self.dirs.data_ptr(),
@@ -378,7 +469,8 @@ class Renderer:
                 self._obj_done.record(self.side)
         if hb:
             h = self.human
-            main.wait_event(self._lbs_done)
+            if setup:
+                main.wait_event(self._lbs_done)
             _lib.call("cf_human_canon", _lib.byref(self.M), self.dirs.data_ptr(), _lib.byref(hb.mo),
                       _lib.byref(self.hw), self._anchor_buckets.handle, h.lbs.buckets.handle, hb.xu.data_ptr(), s)
             self._mark("human_canon")
@@ -397,7 +489,6 @@ class Renderer:
                   ob.rgb.data_ptr() if ob else None, ob.depth.data_ptr() if ob else None,
                   ob.opacity.data_ptr() if ob else None, self.bg, self.image.data_ptr(), self.layer.data_ptr(), s)
         self._mark("layers")
-        return self.image
 
     def sample_counts(self):
         """(human, object) processed-sample counts of the last view (syncs)."""

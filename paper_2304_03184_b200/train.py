@@ -125,6 +125,7 @@ class Trainer:
         self.dirs = torch.empty((self.max_rays, 3), dtype=torch.float64, device=d)
         self.M = _lib.MarchDesc()
         ctypes.memmove(ctypes.byref(self.M), ctypes.byref(renderer.M), ctypes.sizeof(self.M))
+        self.M.frame = None  # the trainer passes its frame (origin, object pose) by value
         self.loss = torch.zeros(2, dtype=torch.float32, device=d)
         self.step_count = 0
         self.seed = 1234
@@ -187,14 +188,17 @@ class Trainer:
         r = self.r
         r.load_prior(b.dqs, b.bone_A, b.dbias)
         r.set_object_pose(b.obj_R, b.obj_t)
+        r.prepare_frame()
         n = b.dirs.shape[0]
         if n > self.max_rays:
             raise ValueError("frame batch larger than max_rays")
         self.dirs[:n].copy_(b.dirs)
+        fr = r._frame_host  # origin[3], obj_R[9], obj_t[3] of the renderer's frame block
         for a in range(3):
-            self.M.origin[a] = r.M.origin[a]
-        self.M.obj_R[:] = r.M.obj_R[:]
-        self.M.obj_t[:] = r.M.obj_t[:]
+            self.M.origin[a] = fr[a]
+            self.M.obj_t[a] = fr[12 + a]
+        for a in range(9):
+            self.M.obj_R[a] = fr[3 + a]
         torch.cuda.current_stream().wait_event(r._lbs_done)
 
     def step(self, batches, allreduce=None):
