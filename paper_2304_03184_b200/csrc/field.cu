@@ -200,11 +200,78 @@ __device__ __forceinline__ Slot make_slot(uint8_t* smem, int w_bytes, uint64_t* 
 
 // ---------------------------------------------------------------- DeformNet
 
+// Each layer is MMA -> epilogue -> MMA per 128-sample slot, so the tensor pipe
+// is busy only while some slot is in its MMA phase: the kernel runs as many
+// slots as TMEM allows. Two slots keep their activations in TMEM and use the
+// "TS" MMA form (A from TMEM, weights B from smem): D (128 fp32 columns) +
+// A (64 packed fp16x2 columns) each. The third slot's D takes the remaining 128
+// columns and its A lives in shared memory (SS form) — 512 columns in all.
+// 8 warps per slot: warps w and w+4 share a TMEM lane quarter and split the
+// columns; the epilogue is tcgen05.ld -> (+bias) -> cvt.relu.f16x2 ->
+// tcgen05.st (TS) or st.shared in the canonical layout (SS).
 constexpr int kDeformSlots = 3;
-constexpr int kDeformA = 128 * 128 * 2;
+constexpr int kDeformSlotThreads = 256;
 constexpr int kDeformW = (128 * 32 + 3 * 128 * 128 + 16 * 128) * 2;  // 110,592 B
+constexpr int kDeformA = 128 * 128 * 2;                              // SS slot's A buffer
 
-__global__ void __launch_bounds__(kDeformSlots* kSlotThreads, 1)
+struct TsSlot {
+  uint64_t* bar;
+  uint8_t* abuf;   // SS slot: A in smem (nullptr for TS slots)
+  uint32_t d;      // D columns (+ lane quarter)
+  uint32_t a;      // TS: A columns (+ lane quarter)
+  uint32_t d0, a0; // slot base columns (MMA operands)
+  uint32_t phase;
+  int slot, r, half;
+};
+
+// one layer: the slot's A writes are complete and visible -> one thread issues
+// the MMAs -> all wait for the commit
+__device__ __forceinline__ void ts_layer(TsSlot& S, const uint8_t* w, int K, int N) {
+  if (S.abuf) tc::fence_async_smem();
+  else tc::tmem_wait_st();
+  tc::fence_before();
+  tc::named_sync(1 + S.slot, kDeformSlotThreads);
+  if (threadIdx.x % kDeformSlotThreads == 0) {
+    tc::fence_after();
+    if (S.abuf) tc::issue_layer(S.d0, S.abuf, w, K, N);
+    else tc::issue_layer_ts(S.d0, S.a0, w, K, N);
+    tc::mma_commit(S.bar);
+  }
+  tc::bar_wait(S.bar, S.phase);
+  S.phase ^= 1u;
+  tc::fence_after();
+}
+
+// hidden epilogue of a 128-wide layer: this warp's 64 columns -> (+bias) ReLU -> fp16 -> A
+__device__ __forceinline__ void ts_relu128(const TsSlot& S, const float* bias) {
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const int col = 64 * S.half + 32 * c;
+    uint32_t r[32];
+    tc::tmem_ld32_nowait(S.d + (uint32_t)col, r);
+    tc::tmem_wait_ld();
+    uint32_t h[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      float x0 = __uint_as_float(r[2 * i]), x1 = __uint_as_float(r[2 * i + 1]);
+      if (bias) {
+        x0 += bias[col + 2 * i];
+        x1 += bias[col + 2 * i + 1];
+      }
+      h[i] = tc::relu_f16x2(x0, x1);
+    }
+    if (S.abuf) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        *reinterpret_cast<uint4*>(S.abuf + tc::core_offset(S.r, col + 8 * q, 128)) =
+            make_uint4(h[4 * q], h[4 * q + 1], h[4 * q + 2], h[4 * q + 3]);
+    } else {
+      tc::tmem_st16(S.a + (uint32_t)(col / 2), h);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kDeformSlots* kDeformSlotThreads, 1)
     deform_mlp_kernel(const uint8_t* __restrict__ wblob, const float* __restrict__ bias1, float delta_scale,
                       float inv_side, const float4* __restrict__ xu, const uint4* __restrict__ dfeat,
                       const int* __restrict__ count, int64_t capacity, float4* __restrict__ xc) {
@@ -212,56 +279,91 @@ __global__ void __launch_bounds__(kDeformSlots* kSlotThreads, 1)
   __shared__ uint64_t mbar[kDeformSlots];
   __shared__ uint32_t tmem_base;
   __shared__ float s_bias[128];
-  if (threadIdx.x < 128) s_bias[threadIdx.x] = bias1[threadIdx.x];
-  slots_setup<kDeformSlots, 512>(wblob, kDeformW, smem, mbar, &tmem_base);
-  Slot S = make_slot<kDeformSlots, 128, kDeformA>(smem, kDeformW, mbar, tmem_base);
+  const int tid = threadIdx.x, warp = tid / 32;
+  if (tid < 128) s_bias[tid] = bias1[tid];
+  for (int i = tid * 16; i < kDeformW; i += blockDim.x * 16)
+    *reinterpret_cast<uint4*>(smem + i) = *reinterpret_cast<const uint4*>(wblob + i);
+  if (tid == 0) {
+    for (int q = 0; q < kDeformSlots; ++q) tc::bar_init(&mbar[q], 1);
+    tc::bar_fence_init();
+  }
+  if (warp == 0) tc::tmem_alloc<512>(&tmem_base);
+  tc::fence_async_smem();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  TsSlot S;
+  S.slot = tid / kDeformSlotThreads;
+  const int ws = warp % (kDeformSlotThreads / 32);  // warp within the slot
+  S.half = ws / 4;                                 // column half
+  S.r = (ws % 4) * 32 + (tid & 31);                // sample row = TMEM lane
+  S.bar = &mbar[S.slot];
+  S.phase = 0;
+  const uint32_t lane_q = (uint32_t)((ws % 4) * 32) << 16;
+  // TMEM columns: slot 0 D [0,128) A [128,192); slot 1 D [192,320) A [320,384); slot 2 (SS) D [384,512)
+  S.d0 = tmem_base + (uint32_t)(S.slot * 192);
+  S.a0 = S.d0 + 128u;
+  S.abuf = S.slot == 2 ? smem + kDeformW : nullptr;
+  S.d = S.d0 + lane_q;
+  S.a = S.a0 + lane_q;
   constexpr int o1 = 0, o2 = 128 * 32 * 2, o3 = o2 + 128 * 128 * 2, o4 = o3 + 128 * 128 * 2, o5 = o4 + 128 * 128 * 2;
   const int64_t n = min((int64_t)*count, capacity);
   const int64_t n_tiles = (n + 127) / 128;
   const int64_t tstride = (int64_t)gridDim.x * kDeformSlots;
-  // software pipelining: the next tile's feature row is loaded during this tile's MLP
+  // this thread's half of its row's 32 input features (2 x 16 B), prefetched one tile ahead
   int64_t tile = (int64_t)blockIdx.x * kDeformSlots + S.slot;
-  uint4 nxt[4];
+  uint4 nxt[2];
   {
     const int64_t s0 = tile * 128 + S.r;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) nxt[q] = (s0 < n) ? dfeat[s0 * 4 + q] : make_uint4(0, 0, 0, 0);
+    for (int q = 0; q < 2; ++q) nxt[q] = (s0 < n) ? dfeat[s0 * 4 + 2 * S.half + q] : make_uint4(0, 0, 0, 0);
   }
   for (; tile < n_tiles; tile += tstride) {
     const int64_t s = tile * 128 + S.r;
     const bool live = s < n;
+    if (S.abuf) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) *reinterpret_cast<uint4*>(S.abuf + tc::core_offset(S.r, 8 * q, 32)) = nxt[q];
-    const float4 xs = live ? xu[s] : make_float4(0.f, 0.f, 0.f, 0.f);
-    run_layer(S, o1, 32, 128);
+      for (int q = 0; q < 2; ++q)
+        *reinterpret_cast<uint4*>(S.abuf + tc::core_offset(S.r, 16 * S.half + 8 * q, 32)) = nxt[q];
+    } else {
+      const uint32_t w8[8] = {nxt[0].x, nxt[0].y, nxt[0].z, nxt[0].w, nxt[1].x, nxt[1].y, nxt[1].z, nxt[1].w};
+      tc::tmem_st8(S.a + (uint32_t)(8 * S.half), w8);
+    }
+    const float4 xs = (live && S.half == 0) ? xu[s] : make_float4(0.f, 0.f, 0.f, 0.f);
+    ts_layer(S, smem + o1, 32, 128);
     {
       const int64_t sn = (tile + tstride) * 128 + S.r;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) nxt[q] = (sn < n) ? dfeat[sn * 4 + q] : make_uint4(0, 0, 0, 0);
+      for (int q = 0; q < 2; ++q) nxt[q] = (sn < n) ? dfeat[sn * 4 + 2 * S.half + q] : make_uint4(0, 0, 0, 0);
     }
-    relu_to_abuf<128>(S, s_bias);
-    run_layer(S, o2, 128, 128);
-    relu_to_abuf<128>(S, nullptr);
-    run_layer(S, o3, 128, 128);
-    relu_to_abuf<128>(S, nullptr);
-    run_layer(S, o4, 128, 128);
-    relu_to_abuf<128>(S, nullptr);
-    run_layer(S, o5, 128, 16);
-    float v[16];
-    tc::tmem_ld16(S.tmem_row, v);
-    if (live) {
-      float4 p = xs;
-      if (p.w > 0.0f) {
-        p.x = f_add(p.x, f_mul(delta_scale * tanhf(v[0]), inv_side));
-        p.y = f_add(p.y, f_mul(delta_scale * tanhf(v[1]), inv_side));
-        p.z = f_add(p.z, f_mul(delta_scale * tanhf(v[2]), inv_side));
+    ts_relu128(S, s_bias);
+    ts_layer(S, smem + o2, 128, 128);
+    ts_relu128(S, nullptr);
+    ts_layer(S, smem + o3, 128, 128);
+    ts_relu128(S, nullptr);
+    ts_layer(S, smem + o4, 128, 128);
+    ts_relu128(S, nullptr);
+    ts_layer(S, smem + o5, 128, 16);
+    if (S.half == 0) {
+      float v[16];
+      tc::tmem_ld16(S.d, v);
+      if (live) {
+        float4 p = xs;
+        if (p.w > 0.0f) {
+          p.x = f_add(p.x, f_mul(delta_scale * tanhf(v[0]), inv_side));
+          p.y = f_add(p.y, f_mul(delta_scale * tanhf(v[1]), inv_side));
+          p.z = f_add(p.z, f_mul(delta_scale * tanhf(v[2]), inv_side));
+        }
+        xc[s] = p;
       }
-      xc[s] = p;
     }
+    // the next tile's first A write happens after this tile's last MMA completed
+    // (ts_layer waited on its commit); its first MMA is issued only after every
+    // thread of the slot passed the next barrier, i.e. finished reading this D
   }
   tc::fence_before();
   __syncthreads();
-  if (threadIdx.x / 32 == 0) tc::tmem_free<512>(tmem_base);
+  if (warp == 0) tc::tmem_free<512>(tmem_base);
 }
 
 // ---------------------------------------------------------------- E_g / E_c
@@ -668,9 +770,9 @@ int cf_field_stage(const cf_field_desc* FD, const cf_march_out* S, const double*
     float4* xc = reinterpret_cast<float4*>(dfeat + cap * 4);
     if (run(0)) hash_f16_kernel<4, 8, 2><<<hgrid, 128, 0, st>>>(FD->dgrid, FD->dtable, xu, S->counters, cap, dfeat);
     if (run(1)) {
-      const int smem = ((kDeformW + 1023) / 1024) * 1024 + kDeformSlots * kDeformA;
+      const int smem = kDeformW + kDeformA;
       CF_CHECK_CUDA(cudaFuncSetAttribute(deform_mlp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      deform_mlp_kernel<<<persistent_grid(cap, kDeformSlots), kDeformSlots * kSlotThreads, smem, st>>>(
+      deform_mlp_kernel<<<persistent_grid(cap, kDeformSlots), kDeformSlots * kDeformSlotThreads, smem, st>>>(
           FD->wblob, FD->dbias, FD->delta_scale, FD->inv_side, xu, dfeat, S->counters, cap, xc);
     }
     xcan = xc;
