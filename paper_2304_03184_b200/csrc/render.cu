@@ -206,7 +206,9 @@ __device__ __forceinline__ void sample_range(const cf_march_desc& M, d3 o, d3 d,
       if (oq[a] < lo[a] || oq[a] > hi[a]) t0 = INFINITY;
       continue;
     }
-    const double inv = 1.0 / dq[a];
+    // any reciprocal within ~1e-7 relative will do: the index range below keeps a
+    // one-sample margin (dt ~ cm) on both ends, far beyond the rounding of t0/t1
+    const double inv = (double)__frcp_rn((float)dq[a]);
     double ta = (lo[a] - oq[a]) * inv, tb = (hi[a] - oq[a]) * inv;
     if (ta > tb) {
       const double s = ta;
@@ -221,7 +223,8 @@ __device__ __forceinline__ void sample_range(const cf_march_desc& M, d3 o, d3 d,
     i1 = 0;
     return;
   }
-  const double f0 = floor((t0 - M.t_near) / M.dt - 0.5) - 1.0, f1 = ceil((t1 - M.t_near) / M.dt - 0.5) + 1.0;
+  const double inv_dt = (double)__frcp_rn((float)M.dt);
+  const double f0 = floor((t0 - M.t_near) * inv_dt - 0.5) - 1.0, f1 = ceil((t1 - M.t_near) * inv_dt - 0.5) + 1.0;
   i0 = (int)fmax(f0, 0.0);
   i1 = (int)fmin(f1, (double)(M.n_samples - 1));
 }
@@ -435,6 +438,19 @@ __device__ __forceinline__ int warp_excl_scan(int v, int& total) {
 }
 
 // occupancy-skipped sample compaction, one thread per ray, up to two fields
+// occupancy masks of samples i0..i1 (< 128), word loop unrolled so the masks
+// stay in registers (a runtime word index would put them in local memory)
+template <class Test>
+__device__ __forceinline__ void scan_samples(int i0, int i1, Test test, uint32_t (&m)[4]) {
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    uint32_t mw = 0;
+    const int lo = max(i0, 32 * w), hi = min(i1, 32 * w + 31);
+    for (int i = lo; i <= hi; ++i) mw |= (uint32_t)test(i) << (i & 31);
+    m[w] = mw;
+  }
+}
+
 __global__ void __launch_bounds__(128) march_kernel(cf_march_desc M, const double* __restrict__ dirs,
                                                     const uint32_t* __restrict__ hbits,
                                                     const uint32_t* __restrict__ obits, cf_march_out H,
@@ -469,11 +485,8 @@ __global__ void __launch_bounds__(128) march_kernel(cf_march_desc M, const doubl
     if (live && hbits && !hempty) {
       int i0, i1;
       sample_range(M, o, d, hlo, hhi, i0, i1);
-      for (int i = i0; i <= i1; ++i)
-        if (occ_test(M.human_grid, hbits, sample_p(o, d, sample_t(M, i)))) {
-          hm[i >> 5] |= 1u << (i & 31);
-          ++hc;
-        }
+      scan_samples(i0, i1, [&](int i) { return occ_test(M.human_grid, hbits, sample_p(o, d, sample_t(M, i))); }, hm);
+      hc = __popc(hm[0]) + __popc(hm[1]) + __popc(hm[2]) + __popc(hm[3]);
     }
     if (live && obits) {
       // the object box is clipped in object space: ray (R^T (o - t), R^T d)
@@ -482,17 +495,21 @@ __global__ void __launch_bounds__(128) march_kernel(cf_march_desc M, const doubl
                   d.x * obj_R[2] + d.y * obj_R[5] + d.z * obj_R[8]};
       int i0, i1;
       sample_range(M, oo, od, olo, ohi, i0, i1);
-      for (int i = i0; i <= i1; ++i)
-        if (occ_test(M.object_grid, obits, to_object(obj_R, obj_t, sample_p(o, d, sample_t(M, i))))) {
-          om[i >> 5] |= 1u << (i & 31);
-          ++oc;
-        }
+      scan_samples(
+          i0, i1,
+          [&](int i) {
+            return occ_test(M.object_grid, obits, to_object(obj_R, obj_t, sample_p(o, d, sample_t(M, i))));
+          },
+          om);
+      oc = __popc(om[0]) + __popc(om[1]) + __popc(om[2]) + __popc(om[3]);
     }
+#pragma unroll
     for (int f = 0; f < 2; ++f) {
       const cf_march_out& out = f == 0 ? H : O;
       if (!out.records) continue;
       const int c = f == 0 ? hc : oc;
-      const uint32_t* m = f == 0 ? hm : om;
+      const uint32_t m[4] = {f == 0 ? hm[0] : om[0], f == 0 ? hm[1] : om[1], f == 0 ? hm[2] : om[2],
+                             f == 0 ? hm[3] : om[3]};
       int wtot;
       const int excl = warp_excl_scan(c, wtot);
       int wbase = 0;
@@ -507,6 +524,7 @@ __global__ void __launch_bounds__(128) march_kernel(cf_march_desc M, const doubl
         if (c > 0) atomicExch(out.counters + 1, 1);
         continue;
       }
+#pragma unroll
       for (int w = 0; w < 4; ++w) {
         uint32_t bitsw = m[w];
         while (bitsw) {
