@@ -173,7 +173,7 @@ def build_workload(args, rank):
     for fid in range(sc.cfg.frames):
         R, t = sc.object_pose(fid)
         frames.append(dict(dqs=sc.node_dqs(fid), A=sc.bone_transforms(fid),
-                           dbias=hf.nets.theta_bias(sc.theta(fid)), R=R, t=t))
+                           dbias=hf.nets.theta_bias(sc.theta(fid)), theta=sc.theta(fid), R=R, t=t))
     return sc, cfg, hf, of, r, frames
 
 
@@ -513,7 +513,7 @@ def run_train(args, rank, world, pg):
                                   dbias=T(f["dbias"], torch.float32), obj_R=f["R"], obj_t=f["t"],
                                   dirs=T(d[pick], torch.float64), gt_rgb=T(rgb, torch.float32),
                                   gt_depth=T(depth, torch.float32), mask_h=T(hum, torch.uint8),
-                                  mask_o=T(obj, torch.uint8)))
+                                  mask_o=T(obj, torch.uint8), theta=T(f["theta"], torch.float32)))
     tr = Trainer(r, max_rays=per_frame, cfg=TrainConfig())
     ar = (lambda ts: allreduce_grads(ts)) if world > 1 else None
     for _ in range(args.warmup):

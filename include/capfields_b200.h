@@ -289,6 +289,8 @@ typedef struct cf_field_desc {
   const float* dbias;       /* DeformNet layer-1 bias (128), pose theta folded in */
   float delta_scale;        /* |dv| bound, metres (0.05) */
   float inv_side;           /* metres -> unit cube */
+  void* save_h;             /* training: DeformNet hidden activations h1..h4, (S,512) fp16, or NULL */
+  float* save_o;            /* training: DeformNet raw outputs (o0, o1, o2, 0) float4 per sample, or NULL */
 } cf_field_desc;
 /* device scratch needed by cf_field_forward for `capacity` samples */
 int cf_field_scratch_bytes(const cf_field_desc* F, int64_t capacity, int64_t* bytes);
@@ -334,9 +336,29 @@ typedef struct cf_color_bwd_io {
 int cf_color_backward(const cf_field_desc* F, const uint8_t* wt_blob, const cf_march_out* S, const double* dirs,
                       const float* xu, const float* grad_out, const void* scratch, const cf_color_bwd_io* io,
                       void* stream);
-/* canonical hash-grid backward at the positions the forward used (xc / xu) */
+/* canonical hash-grid backward at the positions the forward used (xc / xu);
+ * dx_out (optional, float4 per sample): dL/dx of those positions (unit-cube
+ * coordinates), the spatial gradient of the trilinear interpolation that
+ * carries the loss into DeformNet */
 int cf_field_hash_backward(const cf_field_desc* F, const cf_march_out* S, const float* xu, const void* scratch,
-                           const float* dfeat, float* table_grad, void* stream);
+                           const float* dfeat, float* table_grad, float* dx_out, void* stream);
+/* DeformNet backward buffers (S = capacity) */
+typedef struct cf_deform_bwd_io {
+  const void* save_h;  /* (S,512) fp16 forward h1..h4 (cf_field_desc.save_h) */
+  const float* save_o; /* float4 per sample: raw outputs (cf_field_desc.save_o) */
+  void* d_o;           /* (S,16) fp16 dL/d(raw outputs) */
+  void* dpre;          /* (S,512) fp16 dL/d(pre-activations) of layers 1..4 */
+  float* d_dfeat;      /* (S,32) fp32 dL/d(deform hash features) */
+} cf_deform_bwd_io;
+/* DeformNet backward on tcgen05: from dL/dxc (dxc, float4 per sample, the
+ * canonical hash backward's dx_out) through xc = xu + delta_scale tanh(o) inv_side
+ * and the 5 layers with the transposed weights
+ * wt_blob = [W5^T 128x16, W4^T, W3^T, W2^T 128x128, W1x^T 32x128] */
+int cf_deform_backward(const cf_field_desc* F, const uint8_t* wt_blob, const cf_march_out* S, const float* xu,
+                       const float* dxc, const cf_deform_bwd_io* io, void* stream);
+/* deformation-grid hash backward at xu: table_grad += corner weight * d_dfeat */
+int cf_deform_hash_backward(const cf_field_desc* F, const cf_march_out* S, const float* xu, const float* d_dfeat,
+                            float* table_grad, void* stream);
 /* Adam: p -= lr * mhat / (sqrt(vhat) + eps), m/v in place; grads scaled by grad_scale */
 int cf_adam(float* p, const float* g, float* m, float* v, int64_t n, float lr, float beta1, float beta2, float eps,
             int step, float grad_scale, void* stream);

@@ -83,7 +83,11 @@ class FieldDesc(ctypes.Structure):
     _fields_ = [("has_deform", ctypes.c_int), ("dgrid", HashGridDesc), ("dtable", ctypes.c_void_p),
                 ("cgrid", HashGridDesc), ("ctable", ctypes.c_void_p), ("wblob", ctypes.c_void_p),
                 ("w_bytes", ctypes.c_int), ("dbias", ctypes.c_void_p), ("delta_scale", ctypes.c_float),
-                ("inv_side", ctypes.c_float)]
+                ("inv_side", ctypes.c_float), ("save_h", ctypes.c_void_p), ("save_o", ctypes.c_void_p)]
+
+
+class DeformBwdIO(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in ("save_h", "save_o", "d_o", "dpre", "d_dfeat")]
 
 
 class ColorBwdIO(ctypes.Structure):
@@ -135,7 +139,9 @@ _SIGS = {
     "cf_loss_composite_bwd": [_P(MarchDesc), _P(MarchOut), _p, ctypes.c_float, _p, _p, _p, ctypes.c_float,
                               ctypes.c_float, ctypes.c_float, _p, _p, _p],
     "cf_color_backward": [_P(FieldDesc), _p, _P(MarchOut), _p, _p, _p, _p, _P(ColorBwdIO), _p],
-    "cf_field_hash_backward": [_P(FieldDesc), _P(MarchOut), _p, _p, _p, _p, _p],
+    "cf_field_hash_backward": [_P(FieldDesc), _P(MarchOut), _p, _p, _p, _p, _p, _p],
+    "cf_deform_backward": [_P(FieldDesc), _p, _P(MarchOut), _p, _p, _P(DeformBwdIO), _p],
+    "cf_deform_hash_backward": [_P(FieldDesc), _P(MarchOut), _p, _p, _p, _p],
     "cf_adam": [_p, _p, _p, _p, _i64, ctypes.c_float, ctypes.c_float, ctypes.c_float, ctypes.c_float, _i32,
                 ctypes.c_float, _p],
     "cf_pack_weight": [_p, _i32, _i32, _p, _p],

@@ -243,7 +243,8 @@ __device__ __forceinline__ void ts_layer(TsSlot& S, const uint8_t* w, int K, int
 }
 
 // hidden epilogue of a 128-wide layer: this warp's 64 columns -> (+bias) ReLU -> fp16 -> A
-__device__ __forceinline__ void ts_relu128(const TsSlot& S, const float* bias) {
+// (training: also -> save[col], the sample's row of this layer's activations)
+__device__ __forceinline__ void ts_relu128(const TsSlot& S, const float* bias, __half* save) {
 #pragma unroll
   for (int c = 0; c < 2; ++c) {
     const int col = 64 * S.half + 32 * c;
@@ -268,13 +269,19 @@ __device__ __forceinline__ void ts_relu128(const TsSlot& S, const float* bias) {
     } else {
       tc::tmem_st16(S.a + (uint32_t)(col / 2), h);
     }
+    if (save) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        reinterpret_cast<uint4*>(save + col)[q] = make_uint4(h[4 * q], h[4 * q + 1], h[4 * q + 2], h[4 * q + 3]);
+    }
   }
 }
 
 __global__ void __launch_bounds__(kDeformSlots* kDeformSlotThreads, 1)
     deform_mlp_kernel(const uint8_t* __restrict__ wblob, const float* __restrict__ bias1, float delta_scale,
                       float inv_side, const float4* __restrict__ xu, const uint4* __restrict__ dfeat,
-                      const int* __restrict__ count, int64_t capacity, float4* __restrict__ xc) {
+                      const int* __restrict__ count, int64_t capacity, float4* __restrict__ xc,
+                      __half* __restrict__ save_h, float4* __restrict__ save_o) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t mbar[kDeformSlots];
   __shared__ uint32_t tmem_base;
@@ -336,17 +343,19 @@ __global__ void __launch_bounds__(kDeformSlots* kDeformSlotThreads, 1)
 #pragma unroll
       for (int q = 0; q < 2; ++q) nxt[q] = (sn < n) ? dfeat[sn * 4 + 2 * S.half + q] : make_uint4(0, 0, 0, 0);
     }
-    ts_relu128(S, s_bias);
+    __half* sv = (save_h && live) ? save_h + s * 512 : nullptr;
+    ts_relu128(S, s_bias, sv);
     ts_layer(S, smem + o2, 128, 128);
-    ts_relu128(S, nullptr);
+    ts_relu128(S, nullptr, sv ? sv + 128 : nullptr);
     ts_layer(S, smem + o3, 128, 128);
-    ts_relu128(S, nullptr);
+    ts_relu128(S, nullptr, sv ? sv + 256 : nullptr);
     ts_layer(S, smem + o4, 128, 128);
-    ts_relu128(S, nullptr);
+    ts_relu128(S, nullptr, sv ? sv + 384 : nullptr);
     ts_layer(S, smem + o5, 128, 16);
     if (S.half == 0) {
       float v[16];
       tc::tmem_ld16(S.d, v);
+      if (live && save_o) save_o[s] = make_float4(v[0], v[1], v[2], 0.0f);
       if (live) {
         float4 p = xs;
         if (p.w > 0.0f) {
@@ -688,6 +697,185 @@ __global__ void __launch_bounds__(128) hash_bwd_kernel(cf_hashgrid_desc D, const
   }
 }
 
+// ---------------------------------------------------------------- DeformNet backward
+
+// transposed DeformNet weights as B operands: W5^T (128x16), W4^T, W3^T, W2^T
+// (128x128), W1x^T (32x128; the hash-feature columns of layer 1)
+constexpr int kDeformWT = (128 * 16 + 3 * 128 * 128 + 32 * 128) * 2;  // 110,592 B
+constexpr int kDBwdSlots = 2;
+constexpr int kDBwdA = 128 * 128 * 2;
+
+// dL/dpre of a 128-wide ReLU layer: D (= dL/dact) * [act > 0] from the saved
+// activation row -> A buffer (K = 128) and the saved dpre row
+__device__ __forceinline__ void bwd_mask128(Slot& S, const __half* act, __half* dpre) {
+#pragma unroll
+  for (int c0 = 0; c0 < 128; c0 += 32) {
+    float v[32];
+    tc::tmem_ld32(S.tmem_row + (uint32_t)c0, v);
+    if (act) {
+      const uint4* a = reinterpret_cast<const uint4*>(act + c0);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint4 u = a[q];
+        const __half2* hh = reinterpret_cast<const __half2*>(&u);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 f = __half22float2(hh[i]);
+          if (!(f.x > 0.0f)) v[8 * q + 2 * i] = 0.0f;
+          if (!(f.y > 0.0f)) v[8 * q + 2 * i + 1] = 0.0f;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = 0.0f;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) tc::st_row8(S.abuf, S.r, c0 + 8 * q, 128, v + 8 * q);
+    if (dpre) store_row_f16(dpre + c0, 0, 32, v);
+  }
+}
+
+// Per 128-sample tile: d_o from dL/dxc, then the dX chain through layers 5..1
+// with the saved forward activations (ReLU masks), saving d_o and dpre1..4
+// (fp16) for the weight-gradient GEMMs and writing dL/d(deform features).
+__global__ void __launch_bounds__(kDBwdSlots* kSlotThreads, 1)
+    deform_bwd_kernel(const uint8_t* __restrict__ wtblob, float delta_scale, float inv_side,
+                      const float4* __restrict__ xu, const float4* __restrict__ dxc, const __half* __restrict__ save_h,
+                      const float4* __restrict__ save_o, const int* __restrict__ count, int64_t capacity,
+                      __half* __restrict__ d_o_out, __half* __restrict__ dpre, float* __restrict__ d_dfeat) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t mbar[kDBwdSlots];
+  __shared__ uint32_t tmem_base;
+  slots_setup<kDBwdSlots, 256>(wtblob, kDeformWT, smem, mbar, &tmem_base);
+  Slot S = make_slot<kDBwdSlots, 128, kDBwdA>(smem, kDeformWT, mbar, tmem_base);
+  constexpr int t5 = 0, t4 = 128 * 16 * 2, t3 = t4 + 128 * 128 * 2, t2 = t3 + 128 * 128 * 2, t1 = t2 + 128 * 128 * 2;
+  const int64_t n = min((int64_t)*count, capacity);
+  const int64_t n_tiles = (n + 127) / 128;
+  for (int64_t tile = (int64_t)blockIdx.x * kDBwdSlots + S.slot; tile < n_tiles;
+       tile += (int64_t)gridDim.x * kDBwdSlots) {
+    const int64_t s = tile * 128 + S.r;
+    const bool live = s < n;
+    const bool valid = live && xu[s].w > 0.0f;
+    // xc = xu + delta_scale * tanh(o) * inv_side  =>  dL/do = dL/dxc * delta_scale * inv_side * (1 - tanh^2 o)
+    float d_o[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) d_o[i] = 0.0f;
+    if (valid) {
+      const float4 g = dxc[s], o = save_o[s];
+      const float gg[3] = {g.x, g.y, g.z}, oo[3] = {o.x, o.y, o.z};
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const float th = tanhf(oo[c]);
+        d_o[c] = gg[c] * delta_scale * inv_side * (1.0f - th * th);
+      }
+    }
+    tc::st_row8(S.abuf, S.r, 0, 16, d_o);
+    tc::st_row8(S.abuf, S.r, 8, 16, d_o + 8);
+    if (live) store_row_f16(d_o_out, s, 16, d_o);
+    const __half* h = live ? save_h + s * 512 : nullptr;
+    __half* dp = live ? dpre + s * 512 : nullptr;
+    run_layer(S, t5, 16, 128);  // dh4 = d_o . W5
+    bwd_mask128(S, h ? h + 384 : nullptr, dp ? dp + 384 : nullptr);
+    run_layer(S, t4, 128, 128);  // dh3 = dpre4 . W4
+    bwd_mask128(S, h ? h + 256 : nullptr, dp ? dp + 256 : nullptr);
+    run_layer(S, t3, 128, 128);  // dh2 = dpre3 . W3
+    bwd_mask128(S, h ? h + 128 : nullptr, dp ? dp + 128 : nullptr);
+    run_layer(S, t2, 128, 128);  // dh1 = dpre2 . W2
+    bwd_mask128(S, h, dp);
+    run_layer(S, t1, 128, 32);  // dL/dfeat = dpre1 . W1x
+    float dfx[32];
+    tc::tmem_ld32(S.tmem_row, dfx);
+    if (live) {
+      float4* d = reinterpret_cast<float4*>(d_dfeat + s * 32);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) d[q] = make_float4(dfx[4 * q], dfx[4 * q + 1], dfx[4 * q + 2], dfx[4 * q + 3]);
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (threadIdx.x / 32 == 0) tc::tmem_free<256>(tmem_base);
+}
+
+// Canonical hash backward that also returns the spatial gradient of the
+// positions (carried into DeformNet): per level, the 8 corner entries are
+// gathered and dL/dx_a = sum_l N_l sum_k (dfeat_l . t_k) dw_k/dfr_a, with
+// w_k = wx wy wz (wx = fr_x or 1 - fr_x); zero on clamped axes.
+template <int F, int L>
+__global__ void __launch_bounds__(128) hash_bwd_dx_kernel(cf_hashgrid_desc D, const float* __restrict__ table,
+                                                          const float4* __restrict__ x,
+                                                          const float* __restrict__ dfeat,
+                                                          const int* __restrict__ count, int64_t capacity,
+                                                          float* __restrict__ grad, float4* __restrict__ dx_out) {
+  const int64_t n = min((int64_t)*count, capacity);
+  const uint32_t mask = (1u << D.log2_table) - 1u;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
+    const float4 p = x[s];
+    if (!(p.w > 0.0f)) {
+      dx_out[s] = make_float4(0.f, 0.f, 0.f, 0.f);
+      continue;
+    }
+    const float q[3] = {p.x, p.y, p.z};
+    float pc[3], inside[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      pc[a] = fminf(fmaxf(q[a], 0.f), 1.f);
+      inside[a] = (q[a] >= 0.f && q[a] <= 1.f) ? 1.f : 0.f;
+    }
+    const float* g = dfeat + s * (L * F);
+    float dx[3] = {0.f, 0.f, 0.f};
+#pragma unroll 2
+    for (int l = 0; l < L; ++l) {
+      const int N = D.resolution[l];
+      const float sc = (float)N;
+      const float pos[3] = {f_mul(pc[0], sc), f_mul(pc[1], sc), f_mul(pc[2], sc)};
+      uint32_t gi[3];
+      float fr[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        int v = (int)floorf(pos[a]);
+        v = v > N - 1 ? N - 1 : v;
+        gi[a] = (uint32_t)v;
+        fr[a] = f_sub(pos[a], (float)v);
+      }
+      const uint32_t stride = (uint32_t)N + 1u;
+      const bool dense = D.dense[l] != 0;
+      float gl[F];
+#pragma unroll
+      for (int f = 0; f < F; ++f) gl[f] = g[l * F + f];
+      float* base = grad + D.offset[l] * F;
+      const float* tb = table + D.offset[l] * F;
+      float dl[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t cx = gi[0] + (k & 1), cy = gi[1] + ((k >> 1) & 1), cz = gi[2] + ((k >> 2) & 1);
+        const uint32_t idx = dense ? (cx + cy * stride + cz * stride * stride)
+                                   : ((cx ^ (cy * 2654435761u) ^ (cz * 805459861u)) & mask);
+        const float wx = (k & 1) ? fr[0] : f_sub(1.f, fr[0]);
+        const float wy = (k & 2) ? fr[1] : f_sub(1.f, fr[1]);
+        const float wz = (k & 4) ? fr[2] : f_sub(1.f, fr[2]);
+        const float w = f_mul(f_mul(wx, wy), wz);
+        float* dst = base + (int64_t)idx * F;
+        float a = 0.f;  // dfeat_l . t_k
+        if constexpr (F == 2) {
+          atomicAdd(reinterpret_cast<float2*>(dst), make_float2(w * gl[0], w * gl[1]));
+          const float2 t = __ldg(reinterpret_cast<const float2*>(tb) + idx);
+          a = gl[0] * t.x + gl[1] * t.y;
+        } else {
+          atomicAdd(reinterpret_cast<float4*>(dst), make_float4(w * gl[0], w * gl[1], w * gl[2], w * gl[3]));
+          const float4 t = __ldg(reinterpret_cast<const float4*>(tb) + idx);
+          a = gl[0] * t.x + gl[1] * t.y + gl[2] * t.z + gl[3] * t.w;
+        }
+        dl[0] += a * ((k & 1) ? 1.f : -1.f) * wy * wz;
+        dl[1] += a * ((k & 2) ? 1.f : -1.f) * wx * wz;
+        dl[2] += a * ((k & 4) ? 1.f : -1.f) * wx * wy;
+      }
+#pragma unroll
+      for (int a = 0; a < 3; ++a) dx[a] += sc * dl[a];
+    }
+    dx_out[s] = make_float4(dx[0] * inside[0], dx[1] * inside[1], dx[2] * inside[2], 0.f);
+  }
+}
+
 unsigned persistent_grid(int64_t capacity, int slots) {
   const int64_t tiles = (capacity + 127) / 128;
   int64_t g = (tiles + slots - 1) / slots;
@@ -733,8 +921,8 @@ int cf_color_backward(const cf_field_desc* FD, const uint8_t* wt_blob, const cf_
 }
 
 int cf_field_hash_backward(const cf_field_desc* FD, const cf_march_out* S, const float* xu, const void* scratch,
-                           const float* dfeat, float* table_grad, void* stream) {
-  if (!FD || !S || !xu || !scratch || !dfeat || !table_grad)
+                           const float* dfeat, float* table_grad, float* dx_out, void* stream) {
+  if (!FD || !S || !xu || !scratch || !dfeat || !table_grad || (dx_out && !FD->ctable))
     return cf::fail(CF_E_BAD_ARG, "cf_field_hash_backward: bad args");
   const int64_t cap = S->capacity;
   if (cap == 0) return CF_OK;
@@ -742,9 +930,41 @@ int cf_field_hash_backward(const cf_field_desc* FD, const cf_march_out* S, const
   const float4* x = reinterpret_cast<const float4*>(xu);
   if (FD->has_deform)
     x = reinterpret_cast<const float4*>(reinterpret_cast<const uint4*>(scratch) + cap * 8);
-  hash_bwd_kernel<2, 16><<<cf::grid_for(cap, 128, 16), 128, 0, cf::as_stream(stream)>>>(
-      FD->cgrid, x, dfeat, S->counters, cap, table_grad);
+  if (dx_out)
+    hash_bwd_dx_kernel<2, 16><<<cf::grid_for(cap, 128, 16), 128, 0, cf::as_stream(stream)>>>(
+        FD->cgrid, FD->ctable, x, dfeat, S->counters, cap, table_grad, reinterpret_cast<float4*>(dx_out));
+  else
+    hash_bwd_kernel<2, 16><<<cf::grid_for(cap, 128, 16), 128, 0, cf::as_stream(stream)>>>(
+        FD->cgrid, x, dfeat, S->counters, cap, table_grad);
   return cf::check_launch("cf_field_hash_backward");
+}
+
+int cf_deform_backward(const cf_field_desc* FD, const uint8_t* wt_blob, const cf_march_out* S, const float* xu,
+                       const float* dxc, const cf_deform_bwd_io* io, void* stream) {
+  if (!FD || !FD->has_deform || !wt_blob || !S || !xu || !dxc || !io || !io->save_h || !io->save_o || !io->d_o ||
+      !io->dpre || !io->d_dfeat)
+    return cf::fail(CF_E_BAD_ARG, "cf_deform_backward: bad args");
+  const int64_t cap = S->capacity;
+  if (cap == 0) return CF_OK;
+  const int smem = kDeformWT + kDBwdSlots * kDBwdA;
+  CF_CHECK_CUDA(cudaFuncSetAttribute(deform_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  deform_bwd_kernel<<<persistent_grid(cap, kDBwdSlots), kDBwdSlots * kSlotThreads, smem, cf::as_stream(stream)>>>(
+      wt_blob, FD->delta_scale, FD->inv_side, reinterpret_cast<const float4*>(xu),
+      reinterpret_cast<const float4*>(dxc), reinterpret_cast<const __half*>(io->save_h),
+      reinterpret_cast<const float4*>(io->save_o), S->counters, cap, reinterpret_cast<__half*>(io->d_o),
+      reinterpret_cast<__half*>(io->dpre), io->d_dfeat);
+  return cf::check_launch("cf_deform_backward");
+}
+
+int cf_deform_hash_backward(const cf_field_desc* FD, const cf_march_out* S, const float* xu, const float* d_dfeat,
+                            float* table_grad, void* stream) {
+  if (!FD || !FD->has_deform || !S || !xu || !d_dfeat || !table_grad)
+    return cf::fail(CF_E_BAD_ARG, "cf_deform_hash_backward: bad args");
+  const int64_t cap = S->capacity;
+  if (cap == 0) return CF_OK;
+  hash_bwd_kernel<4, 8><<<cf::grid_for(cap, 128, 16), 128, 0, cf::as_stream(stream)>>>(
+      FD->dgrid, reinterpret_cast<const float4*>(xu), d_dfeat, S->counters, cap, table_grad);
+  return cf::check_launch("cf_deform_hash_backward");
 }
 
 int cf_field_stage(const cf_field_desc* FD, const cf_march_out* S, const double* dirs, const float* xu_f,
@@ -773,7 +993,8 @@ int cf_field_stage(const cf_field_desc* FD, const cf_march_out* S, const double*
       const int smem = kDeformW + kDeformA;
       CF_CHECK_CUDA(cudaFuncSetAttribute(deform_mlp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       deform_mlp_kernel<<<persistent_grid(cap, kDeformSlots), kDeformSlots * kDeformSlotThreads, smem, st>>>(
-          FD->wblob, FD->dbias, FD->delta_scale, FD->inv_side, xu, dfeat, S->counters, cap, xc);
+          FD->wblob, FD->dbias, FD->delta_scale, FD->inv_side, xu, dfeat, S->counters, cap, xc,
+          reinterpret_cast<__half*>(FD->save_h), reinterpret_cast<float4*>(FD->save_o));
     }
     xcan = xc;
   }

@@ -4,10 +4,13 @@ MLP forward -> masked L2 colour + 0.1 L1 depth -> compositing backward ->
 tcgen05 E_g/E_c backward -> hash-grid backward (atomics) -> Adam.
 
 Human and object fields are updated independently on their own masked rays.
-Round 1 trains the canonical hash grids and E_g/E_c of both fields; the human's
-DeformNet (and its grid) are applied forward-only (frozen). The weight-gradient
-reductions dW = dY^T X over the saved fp16 activations are plain GEMMs (cuBLAS via
-torch.mm); every other step is a kernel of this package.
+Trained: the canonical hash grids and E_g/E_c of both fields, and the human's
+DeformNet with its deformation grid (TrainConfig.train_deform): the canonical
+hash backward also returns dL/dxc (spatial gradient of the trilinear
+interpolation), which flows through xc = xu + 0.05 tanh(o) / side into the
+tcgen05 DeformNet backward and on into the deformation-grid hash backward. The
+weight-gradient reductions dW = dY^T X over the saved fp16 activations are plain
+GEMMs (cuBLAS via torch.mm); every other step is a kernel of this package.
 
 Multi-GPU: rays are sharded across ranks; `allreduce_grads` sums the flat
 gradient buckets over NCCL (NVLink) and each rank applies the same Adam update.
@@ -38,6 +41,7 @@ class TrainConfig:
     n_uniform: int = 16
     n_empty: int = 64
     depth_sigma: float = 0.02   # config.py:52
+    train_deform: bool = True   # also train DeformNet + its grid (needs FrameBatch.theta)
 
 
 @dataclass
@@ -53,6 +57,7 @@ class FrameBatch:
     gt_depth: torch.Tensor     # (R,) f32 distance along the ray, <= 0 = no depth
     mask_h: torch.Tensor       # (R,) u8 human mask
     mask_o: torch.Tensor       # (R,) u8 object mask
+    theta: torch.Tensor | None = None  # (72,) f32 pose; DeformNet training recomputes dbias from it
 
 
 class ColorParams:
@@ -91,6 +96,60 @@ class ColorParams:
             g.zero_()
 
 
+DEFORM_LAYERS = ("D1", "D2", "D3", "D4", "D5")
+
+
+class DeformParams:
+    """fp32 master weights of DeformNet (D1 = [hash(32) | theta(72)] columns), their
+    grads and Adam moments; repacks the forward blob's DeformNet part and the
+    transposed blob of the backward kernel after every update."""
+
+    def __init__(self, nets, device):
+        self.nets = nets
+        self.W = {k: torch.from_numpy(nets.layers[k].astype(np.float32)).to(device).contiguous() for k in DEFORM_LAYERS}
+        self.G = {k: torch.zeros_like(v) for k, v in self.W.items()}
+        self.m = {k: torch.zeros_like(v) for k, v in self.W.items()}
+        self.v = {k: torch.zeros_like(v) for k, v in self.W.items()}
+        self.wt_blob = torch.empty(110592, dtype=torch.uint8, device=device)
+        self.pack()
+
+    def bias(self, theta: torch.Tensor) -> torch.Tensor:
+        """Per-frame layer-1 pose term W1[:, 32:] @ theta (fp32, device)."""
+        return (self.W["D1"][:, 32:] @ theta.to(self.W["D1"].device, torch.float32)).contiguous()
+
+    def pack(self):
+        s = _lib.stream_ptr()
+        mats = [self.W["D1"][:, :32].contiguous(), self.W["D2"], self.W["D3"], self.W["D4"], self.W["D5"]]
+        o = 0
+        for w in mats:
+            n, kk = w.shape
+            _lib.call("cf_pack_weight", w.data_ptr(), n, kk, self.nets.blob.data_ptr() + o, s)
+            o += ((n + 15) // 16 * 16) * ((kk + 15) // 16 * 16) * 2
+        keep = [self.W["D5"].t().contiguous(), self.W["D4"].t().contiguous(), self.W["D3"].t().contiguous(),
+                self.W["D2"].t().contiguous(), self.W["D1"][:, :32].t().contiguous()]
+        o = 0
+        for wt in keep:
+            n, kk = wt.shape
+            _lib.call("cf_pack_weight", wt.data_ptr(), n, kk, self.wt_blob.data_ptr() + o, s)
+            o += ((n + 15) // 16 * 16) * ((kk + 15) // 16 * 16) * 2
+
+    def zero_grad(self):
+        for g in self.G.values():
+            g.zero_()
+
+
+class _DeformBuffers:
+    def __init__(self, cap, device):
+        self.save_h = torch.empty((cap, 512), dtype=torch.float16, device=device)
+        self.save_o = torch.empty((cap, 4), dtype=torch.float32, device=device)
+        self.d_o = torch.empty((cap, 16), dtype=torch.float16, device=device)
+        self.dpre = torch.empty((cap, 512), dtype=torch.float16, device=device)
+        self.d_dfeat = torch.empty((cap, 32), dtype=torch.float32, device=device)
+        self.dxc = torch.empty((cap, 4), dtype=torch.float32, device=device)
+        self.io = _lib.DeformBwdIO(self.save_h.data_ptr(), self.save_o.data_ptr(), self.d_o.data_ptr(),
+                                   self.dpre.data_ptr(), self.d_dfeat.data_ptr())
+
+
 class _BwdBuffers:
     def __init__(self, cap, device):
         h = lambda w: torch.empty((cap, w), dtype=torch.float16, device=device)  # noqa: E731
@@ -121,6 +180,12 @@ class Trainer:
             st["tgrad"] = torch.zeros_like(field.cgrid.table)
             st["tm"] = torch.zeros_like(field.cgrid.table)
             st["tv"] = torch.zeros_like(field.cgrid.table)
+            if name == "human" and self.cfg.train_deform:
+                st["deform"] = DeformParams(field.nets, d)
+                st["dbufs"] = _DeformBuffers(cap, d)
+                st["dtgrad"] = torch.zeros_like(field.dgrid.table)
+                st["dtm"] = torch.zeros_like(field.dgrid.table)
+                st["dtv"] = torch.zeros_like(field.dgrid.table)
             self.fields.append(st)
         self.dirs = torch.empty((self.max_rays, 3), dtype=torch.float64, device=d)
         self.M = _lib.MarchDesc()
@@ -150,10 +215,21 @@ class Trainer:
                   cfg.n_uniform, cfg.n_empty, cfg.depth_sigma, ctypes.c_uint64(self.seed), _lib.byref(buf.mo),
                   bwd.t.data_ptr(), s)
         M.sample_t = bwd.t.data_ptr()
+        dp = st.get("deform")
         if st["name"] == "human":
             _lib.call("cf_human_canon", _lib.byref(M), self.dirs.data_ptr(), _lib.byref(buf.mo), _lib.byref(r.hw),
                       r._anchor_buckets.handle, field.lbs.buckets.handle, buf.xu.data_ptr(), s)
             desc = r.hdesc
+            if dp is not None:
+                # a private descriptor: this frame's pose bias from the current W1, forward saves on
+                if b.theta is None:
+                    raise ValueError("DeformNet training needs FrameBatch.theta")
+                st["dbias"] = dp.bias(b.theta)
+                desc = _lib.FieldDesc()
+                ctypes.memmove(ctypes.byref(desc), ctypes.byref(r.hdesc), ctypes.sizeof(desc))
+                desc.dbias = st["dbias"].data_ptr()
+                desc.save_h = st["dbufs"].save_h.data_ptr()
+                desc.save_o = st["dbufs"].save_o.data_ptr()
         else:
             _lib.call("cf_object_canon", _lib.byref(M), self.dirs.data_ptr(), _lib.byref(buf.mo), buf.xu.data_ptr(), s)
             desc = r.odesc
@@ -166,8 +242,15 @@ class Trainer:
         _lib.call("cf_color_backward", _lib.byref(desc), P.wt_blob.data_ptr(), _lib.byref(buf.mo),
                   self.dirs.data_ptr(), buf.xu.data_ptr(), bwd.grad.data_ptr(), scratch.data_ptr(),
                   _lib.byref(bwd.io), s)
+        db = st.get("dbufs")
         _lib.call("cf_field_hash_backward", _lib.byref(desc), _lib.byref(buf.mo), buf.xu.data_ptr(),
-                  scratch.data_ptr(), bwd.dfeat.data_ptr(), st["tgrad"].data_ptr(), s)
+                  scratch.data_ptr(), bwd.dfeat.data_ptr(), st["tgrad"].data_ptr(),
+                  db.dxc.data_ptr() if dp is not None else None, s)
+        if dp is not None:
+            _lib.call("cf_deform_backward", _lib.byref(desc), dp.wt_blob.data_ptr(), _lib.byref(buf.mo),
+                      buf.xu.data_ptr(), db.dxc.data_ptr(), _lib.byref(db.io), s)
+            _lib.call("cf_deform_hash_backward", _lib.byref(desc), _lib.byref(buf.mo), buf.xu.data_ptr(),
+                      db.d_dfeat.data_ptr(), st["dtgrad"].data_ptr(), s)
         # weight gradients dW = dY^T X over this frame's samples (plain GEMMs)
         n = int(buf.counters[0])
         if n == 0:
@@ -183,6 +266,18 @@ class Trainer:
         G["C1"] += (f(bwd.dc1).t() @ f(bwd.cin)).float()[:, :31]
         G["G2"] += (f(bwd.dg).t() @ f(bwd.h1)).float()
         G["G1"] += (f(bwd.dh1).t() @ x0).float()
+        if dp is not None:
+            cap = buf.mo.capacity
+            xd = scratch[cap * 64: cap * 64 + n * 64].view(torch.float16).view(n, 32)  # deform-grid features
+            H, DP, DO = db.save_h[:n], db.dpre[:n], db.d_o[:n]
+            GD = dp.G
+            GD["D5"] += (DO.t() @ H[:, 384:512]).float()[:3]
+            GD["D4"] += (DP[:, 384:512].t() @ H[:, 256:384]).float()
+            GD["D3"] += (DP[:, 256:384].t() @ H[:, 128:256]).float()
+            GD["D2"] += (DP[:, 128:256].t() @ H[:, 0:128]).float()
+            GD["D1"][:, :32] += (DP[:, 0:128].t() @ xd).float()
+            # theta is the same for every sample of the frame: dW1_theta = (sum_s dpre1) theta^T
+            GD["D1"][:, 32:] += torch.outer(DP[:, 0:128].float().sum(0), b.theta.to(DP.device, torch.float32))
 
     def set_frame(self, b: FrameBatch):
         r = self.r
@@ -207,13 +302,20 @@ class Trainer:
         for st in self.fields:
             st["tgrad"].zero_()
             st["params"].zero_grad()
+            if "deform" in st:
+                st["dtgrad"].zero_()
+                st["deform"].zero_grad()
             st["stats"] = torch.zeros(2, dtype=torch.float32, device=self.dirs.device)
         for b in batches:
             self.set_frame(b)
             for st in self.fields:
                 self._frame(b, st, st["stats"])
         if allreduce is not None:
-            allreduce([st["tgrad"] for st in self.fields] + [g for st in self.fields for g in st["params"].G.values()])
+            bufs = [st["tgrad"] for st in self.fields] + [g for st in self.fields for g in st["params"].G.values()]
+            for st in self.fields:
+                if "deform" in st:
+                    bufs += [st["dtgrad"]] + list(st["deform"].G.values())
+            allreduce(bufs)
         self.step_count += 1
         cfg, s = self.cfg, _lib.stream_ptr()
         nb = float(len(batches))
@@ -226,8 +328,30 @@ class Trainer:
                 _lib.call("cf_adam", P.W[k].data_ptr(), P.G[k].data_ptr(), P.m[k].data_ptr(), P.v[k].data_ptr(),
                           P.W[k].numel(), cfg.lr_net, cfg.beta1, cfg.beta2, cfg.eps, self.step_count, 1.0 / nb, s)
             P.pack()
+            if "deform" in st:
+                t = st["field"].dgrid.table
+                _lib.call("cf_adam", t.data_ptr(), st["dtgrad"].data_ptr(), st["dtm"].data_ptr(), st["dtv"].data_ptr(),
+                          t.numel(), cfg.lr_hash, cfg.beta1, cfg.beta2, cfg.eps, self.step_count, 1.0 / nb, s)
+                D = st["deform"]
+                for k in DEFORM_LAYERS:
+                    _lib.call("cf_adam", D.W[k].data_ptr(), D.G[k].data_ptr(), D.m[k].data_ptr(), D.v[k].data_ptr(),
+                              D.W[k].numel(), cfg.lr_net, cfg.beta1, cfg.beta2, cfg.eps, self.step_count, 1.0 / nb,
+                              s)
+                D.pack()
             out[st["name"]] = st["stats"] / nb
         return out
+
+
+def sync_host_weights(trainer: "Trainer") -> None:
+    """Copy the trained fp32 weights back into the FieldNets host arrays (the
+    renderer's per-frame DeformNet pose bias is computed from them)."""
+    for st in trainer.fields:
+        nets = st["field"].nets
+        for k, w in st["params"].W.items():
+            nets.layers[k] = w.cpu().numpy().astype(np.float16).astype(np.float32)
+        if "deform" in st:
+            for k, w in st["deform"].W.items():
+                nets.layers[k] = w.cpu().numpy().astype(np.float16).astype(np.float32)
 
 
 def allreduce_grads(tensors, group=None):

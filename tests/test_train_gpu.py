@@ -1,7 +1,8 @@
 """Training step (SPEC train_step) on the B200: sampler bit-exact vs the oracle;
-loss / compositing backward, E_g/E_c tcgen05 backward and the hash backward vs
-PyTorch fp32 autograd references of the same float ops; Adam and the weight
-repack; a short optimisation that must reduce the loss."""
+loss / compositing backward, E_g/E_c tcgen05 backward, the hash backward, the
+canonical hash spatial gradient and the DeformNet backward vs PyTorch fp32
+autograd references of the same float ops; Adam and the weight repack; a short
+optimisation that must reduce the loss."""
 import numpy as np
 import pytest
 import torch
@@ -28,6 +29,7 @@ def make_batch(sc, hf, fid, n_rays, rng, dev):
     T = lambda x, dt: torch.as_tensor(np.ascontiguousarray(x), dtype=dt, device=dev)  # noqa: E731
     return FrameBatch(dqs=T(sc.node_dqs(fid), torch.float64), bone_A=T(sc.bone_transforms(fid), torch.float64),
                       dbias=T(hf.nets.theta_bias(sc.theta(fid)), torch.float32), obj_R=R, obj_t=t,
+                      theta=T(sc.theta(fid), torch.float32),
                       dirs=T(d[pick], torch.float64), gt_rgb=T(rgb[pick], torch.float32),
                       gt_depth=T(depth, torch.float32), mask_h=T(hum[pick], torch.uint8),
                       mask_o=T(obj[pick], torch.uint8))
@@ -55,6 +57,9 @@ def setup():
 def run_frame(tr, b, st):
     st["tgrad"].zero_()
     st["params"].zero_grad()
+    if "deform" in st:
+        st["dtgrad"].zero_()
+        st["deform"].zero_grad()
     stats = torch.zeros(2, device="cuda")
     tr.set_frame(b)
     tr._frame(b, st, stats)
@@ -187,6 +192,112 @@ def test_color_backward_vs_autograd(setup):
     got = bwd.dfeat[:n].cpu().numpy()
     scale = np.abs(ref).max()
     assert np.abs(got - ref).max() <= 3e-2 * scale + 1e-7
+
+
+def _trilinear_torch(x, table, levels, log2_table, F):
+    """Hash-grid features with autograd w.r.t. x: corner indices from the oracle
+    (piecewise constant), corner weights recomputed in torch from x."""
+    feats = []
+    xc = torch.clamp(x, 0.0, 1.0)
+    for lev in levels:
+        N = lev[0]
+        idx, _ = on.hash_corners(x.detach().numpy(), lev, log2_table)
+        pos = xc * float(N)
+        g = torch.minimum(torch.floor(pos.detach()), torch.tensor(float(N - 1)))
+        fr = pos - g
+        t = table[torch.from_numpy(idx.astype(np.int64) + lev[2])]  # (n, 8, F)
+        f = 0
+        for k in range(8):
+            wx = fr[:, 0] if k & 1 else 1 - fr[:, 0]
+            wy = fr[:, 1] if k & 2 else 1 - fr[:, 1]
+            wz = fr[:, 2] if k & 4 else 1 - fr[:, 2]
+            f = f + (wx * wy * wz)[:, None] * t[:, k]
+        feats.append(f)
+    return torch.cat(feats, 1)
+
+
+def test_canonical_hash_spatial_gradient(setup):
+    """dL/dxc from the canonical hash backward (the input of the DeformNet
+    backward) vs autograd through the trilinear interpolation."""
+    sc, hf, of, r, tr, batches = setup
+    b = batches[1]
+    st = tr.fields[0]
+    assert "deform" in st
+    run_frame(tr, b, st)
+    n, _, _ = samples_of(st)
+    buf = st["buf"]
+    cap = buf.mo.capacity
+    scratch = r._scratch(buf, r.hdesc)
+    xc = scratch[cap * 128: cap * 128 + n * 16].view(torch.float32).view(n, 4).cpu()
+    keep = (xc[:, 3] > 0).numpy()
+    sel = np.nonzero(keep)[0][:3000]
+    x = xc[sel, :3].clone().requires_grad_(True)
+    table = hf.cgrid.table.detach().cpu().view(-1, 2)
+    levels = hf.cgrid.levels()
+    feat = _trilinear_torch(x, table, levels, hf.cgrid.cfg.log2_table, 2)
+    g = st["bwd"].dfeat[:n].cpu()[sel]
+    (feat * g).sum().backward()
+    ref = x.grad.numpy()
+    got = st["dbufs"].dxc[:n].cpu().numpy()[sel, :3]
+    scale = np.abs(ref).max()
+    assert scale > 0
+    assert np.abs(got - ref).max() <= 1e-3 * scale, (np.abs(got - ref).max(), scale)
+
+
+def test_deform_backward_vs_autograd(setup):
+    """DeformNet weight and feature gradients (tcgen05 backward + fp16 GEMMs) vs
+    autograd of the same fp16-operand graph (activations and the backward's
+    dL/dpre operands rounded to fp16 as the kernels do), driven by the kernel's
+    dL/dxc."""
+    sc, hf, of, r, tr, batches = setup
+    b = batches[2]
+    st = tr.fields[0]
+    run_frame(tr, b, st)
+    n, _, _ = samples_of(st)
+    buf, D, db = st["buf"], st["deform"], st["dbufs"]
+    cap = buf.mo.capacity
+    scratch = r._scratch(buf, r.hdesc)
+    xd = scratch[cap * 64: cap * 64 + n * 64].view(torch.float16).view(n, 32).float().cpu()
+    valid = torch.from_numpy(buf.xu[:n].cpu().numpy()[:, 3] > 0).float()
+    dxc = db.dxc[:n].cpu()[:, :3]
+    theta = b.theta.cpu().float()
+    W = {k: D.W[k].detach().cpu().clone().requires_grad_(True) for k in D.W}
+    h = lambda x: x.half().float()  # noqa: E731  fp16 operand rounding of the kernel
+
+    class GradF16(torch.autograd.Function):  # the backward MMAs take dL/dpre as fp16 operands
+        @staticmethod
+        def forward(ctx, x):
+            return x.view_as(x)
+
+        @staticmethod
+        def backward(ctx, g):
+            return g.half().float()
+
+    q = GradF16.apply
+    Wh = {k: h(W[k]) for k in W}
+    bias = W["D1"][:, 32:] @ theta  # fp32 master weights (Trainer: DeformParams.bias)
+    x0 = xd.clone().requires_grad_(True)
+    a1 = torch.relu(q(h(x0) @ Wh["D1"][:, :32].t() + bias))
+    a2 = torch.relu(q(h(a1) @ Wh["D2"].t()))
+    a3 = torch.relu(q(h(a2) @ Wh["D3"].t()))
+    a4 = torch.relu(q(h(a3) @ Wh["D4"].t()))
+    o = q(h(a4) @ Wh["D5"].t())
+    dv = 0.05 * torch.tanh(o) * hf.inv_side
+    L = (valid[:, None] * dxc * dv).sum()
+    L.backward()
+    # tolerance: fp32 accumulation order (TMEM / cuBLAS vs CPU) and the resulting
+    # one-ulp fp16 flips of saved activations; measured max 1e-3 of the max entry
+    for k in ("D1", "D2", "D3", "D4", "D5"):
+        ref = W[k].grad.numpy()
+        got = D.G[k].cpu().numpy()
+        scale = np.abs(ref).max()
+        assert scale > 0, k
+        assert np.abs(got - ref).max() <= 1e-2 * scale, (k, np.abs(got - ref).max(), scale)
+    ref = x0.grad.numpy()
+    got = db.d_dfeat[:n].cpu().numpy()
+    scale = np.abs(ref).max()
+    assert scale > 0
+    assert np.abs(got - ref).max() <= 1e-2 * scale
 
 
 def test_hash_backward(setup):
