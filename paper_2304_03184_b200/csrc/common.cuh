@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string>
+#include <utility>
 
 #include "../../include/capfields_b200.h"
 
@@ -23,7 +24,32 @@ inline unsigned grid_for(int64_t n, int block, int per_sm = 8) {
   return (unsigned)(need < cap ? need : cap);
 }
 
+// Programmatic dependent launch (PDL): the kernel is launched while its stream
+// predecessor drains, so its launch latency and prologue overlap the
+// predecessor's tail. Kernels launched this way call pdl_wait() before touching
+// any memory the predecessor reads or writes, and pdl_trigger() once their CTA's
+// work is done (launch-completion of the next kernel); both are no-ops for a
+// normal launch. In a captured graph these become programmatic edges.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 }  // namespace cf
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 #define CF_CHECK_CUDA(call)                                                                 \
   do {                                                                                      \

@@ -96,6 +96,7 @@ template <int F, int L, int CH>
 __global__ void __launch_bounds__(128) hash_f16_kernel(cf_hashgrid_desc D, const float* __restrict__ table,
                                                        const float4* __restrict__ x, const int* __restrict__ count,
                                                        int64_t capacity, uint4* __restrict__ out) {
+  pdl_wait();
   const int64_t n = min((int64_t)*count, capacity);
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
     const float4 p = x[s];
@@ -114,6 +115,7 @@ __global__ void __launch_bounds__(128) hash_f16_kernel(cf_hashgrid_desc D, const
       out[s * 4 + q] = *reinterpret_cast<uint4*>(h);
     }
   }
+  pdl_trigger();
 }
 
 // ------------------------------------------------------------------ MLP slots
@@ -299,6 +301,7 @@ __global__ void __launch_bounds__(kDeformSlots* kDeformSlotThreads, 1)
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
+  pdl_wait();  // weights staged and TMEM allocated while the previous kernel drained
   TsSlot S;
   S.slot = tid / kDeformSlotThreads;
   const int ws = warp % (kDeformSlotThreads / 32);  // warp within the slot
@@ -370,6 +373,7 @@ __global__ void __launch_bounds__(kDeformSlots* kDeformSlotThreads, 1)
     // (ts_layer waited on its commit); its first MMA is issued only after every
     // thread of the slot passed the next barrier, i.e. finished reading this D
   }
+  pdl_trigger();
   tc::fence_before();
   __syncthreads();
   if (warp == 0) tc::tmem_free<512>(tmem_base);
@@ -410,6 +414,7 @@ __global__ void __launch_bounds__(kColorSlots* kSlotThreads, 1)
   __shared__ uint64_t mbar[kColorSlots];
   __shared__ uint32_t tmem_base;
   slots_setup<kColorSlots, 256>(wblob, kColorW, smem, mbar, &tmem_base);
+  pdl_wait();  // weights staged and TMEM allocated while the previous kernel drained
   Slot S = make_slot<kColorSlots, 64, kColorA>(smem, kColorW, mbar, tmem_base);
   constexpr int g1 = 0, g2 = 64 * 32 * 2, c1 = g2 + 16 * 64 * 2, c2 = c1 + 64 * 32 * 2, c3 = c2 + 64 * 64 * 2;
   const int64_t n = min((int64_t)*count, capacity);
@@ -459,6 +464,7 @@ __global__ void __launch_bounds__(kColorSlots* kSlotThreads, 1)
   tc::fence_before();
   __syncthreads();
   if (threadIdx.x / 32 == 0) tc::tmem_free<256>(tmem_base);
+  pdl_trigger();
 }
 
 // ---------------------------------------------------------------- E_g / E_c backward
@@ -988,23 +994,21 @@ int cf_field_stage(const cf_field_desc* FD, const cf_march_out* S, const double*
   if (FD->has_deform) {
     uint4* dfeat = cfeat + cap * 4;
     float4* xc = reinterpret_cast<float4*>(dfeat + cap * 4);
-    if (run(0)) hash_f16_kernel<4, 8, 2><<<hgrid, 128, 0, st>>>(FD->dgrid, FD->dtable, xu, S->counters, cap, dfeat);
+    if (run(0)) cf::launch_pdl(hash_f16_kernel<4, 8, 2>, hgrid, 128, 0, st, FD->dgrid, FD->dtable, xu, S->counters, cap, dfeat);
     if (run(1)) {
       const int smem = kDeformW + kDeformA;
       CF_CHECK_CUDA(cudaFuncSetAttribute(deform_mlp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      deform_mlp_kernel<<<persistent_grid(cap, kDeformSlots), kDeformSlots * kDeformSlotThreads, smem, st>>>(
-          FD->wblob, FD->dbias, FD->delta_scale, FD->inv_side, xu, dfeat, S->counters, cap, xc,
+      cf::launch_pdl(deform_mlp_kernel, persistent_grid(cap, kDeformSlots), kDeformSlots * kDeformSlotThreads, smem, st, FD->wblob, FD->dbias, FD->delta_scale, FD->inv_side, xu, dfeat, S->counters, cap, xc,
           reinterpret_cast<__half*>(FD->save_h), reinterpret_cast<float4*>(FD->save_o));
     }
     xcan = xc;
   }
-  if (run(2)) hash_f16_kernel<2, 16, 4><<<hgrid, 128, 0, st>>>(FD->cgrid, FD->ctable, xcan, S->counters, cap, cfeat);
+  if (run(2)) cf::launch_pdl(hash_f16_kernel<2, 16, 4>, hgrid, 128, 0, st, FD->cgrid, FD->ctable, xcan, S->counters, cap, cfeat);
   if (run(3)) {
     const int csmem = ((kColorW + 1023) / 1024) * 1024 + kColorSlots * kColorA;
     CF_CHECK_CUDA(cudaFuncSetAttribute(color_mlp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, csmem));
     const uint8_t* cw = FD->wblob + (FD->has_deform ? kDeformW : 0);
-    color_mlp_kernel<<<persistent_grid(cap, kColorSlots), kColorSlots * kSlotThreads, csmem, st>>>(
-        cw, xu, cfeat, S->records, dirs, S->counters, cap, out);
+    cf::launch_pdl(color_mlp_kernel, persistent_grid(cap, kColorSlots), kColorSlots * kSlotThreads, csmem, st, cw, xu, cfeat, S->records, dirs, S->counters, cap, out);
   }
   return cf::check_launch("cf_field_forward");
 }

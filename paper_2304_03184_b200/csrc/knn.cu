@@ -16,10 +16,12 @@ constexpr double kWeightFloor = 1e-6;  // edgraph.py:24
 
 __global__ void deform_nodes_kernel(const double* __restrict__ nodes, const double* __restrict__ dqs, int64_t n,
                                     double* __restrict__ anchors) {
+  pdl_wait();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     dq8 q = load_dq(dqs + 8 * i);
     store_d3(anchors + 3 * i, dq_apply(q, load_d3(nodes + 3 * i)));
   }
+  pdl_trigger();
 }
 
 // ------------------------------------------------------------------ buckets
@@ -153,6 +155,7 @@ __global__ void __launch_bounds__(1024) bucket_build_small_kernel(const double* 
                                                                   int* __restrict__ point_cell,
                                                                   int* __restrict__ point_slot,
                                                                   double4* __restrict__ sorted) {
+  pdl_wait();
   const int cells = G * G * G;
   for (int i = threadIdx.x; i <= cells; i += blockDim.x) cell_start[i] = 0;
   bucket_params_body(pts, n, G, P);
@@ -162,6 +165,7 @@ __global__ void __launch_bounds__(1024) bucket_build_small_kernel(const double* 
   bucket_scan_body(cell_start, P);
   __syncthreads();
   bucket_scatter_body(pts, n, cell_start, point_cell, point_slot, sorted);
+  pdl_trigger();
 }
 
 // ------------------------------------------------------------------ cell candidate lists
@@ -387,7 +391,7 @@ int buckets_build(cf_buckets* b, const double* pts, int64_t n, int grid_res, cud
   b->ccl_k = 0;  // candidate lists describe the previous point set
   const int64_t cells = (int64_t)G * G * G;
   if (n <= 65536 && cells <= (1 << 18)) {
-    bucket_build_small_kernel<<<1, 1024, 0, st>>>(pts, (int)n, G, b->params, b->cell_start, b->point_cell,
+    cf::launch_pdl(bucket_build_small_kernel, 1, 1024, 0, st, pts, (int)n, G, b->params, b->cell_start, b->point_cell,
                                                   b->point_slot, b->sorted);
     return check_launch("buckets_build");
   }
@@ -408,7 +412,7 @@ extern "C" {
 int cf_deform_nodes(const double* nodes, const double* dqs, int64_t n, double* anchors, void* stream) {
   if (n < 0 || (n > 0 && (!nodes || !dqs || !anchors))) return cf::fail(CF_E_BAD_ARG, "cf_deform_nodes: bad args");
   if (n == 0) return CF_OK;
-  deform_nodes_kernel<<<cf::grid_for(n, 128, 4), 128, 0, cf::as_stream(stream)>>>(nodes, dqs, n, anchors);
+  cf::launch_pdl(deform_nodes_kernel, cf::grid_for(n, 128, 4), 128, 0, cf::as_stream(stream), nodes, dqs, n, anchors);
   return cf::check_launch("cf_deform_nodes");
 }
 

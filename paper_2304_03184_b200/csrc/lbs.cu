@@ -10,6 +10,7 @@ namespace {
 
 __global__ void lbs_forward_kernel(const double* __restrict__ A, int J, const double* __restrict__ pts,
                                    const double* __restrict__ W, int64_t n, double* __restrict__ out) {
+  pdl_wait();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const double p[4] = {pts[3 * i], pts[3 * i + 1], pts[3 * i + 2], 1.0};
     double o[3] = {0.0, 0.0, 0.0};
@@ -25,11 +26,13 @@ __global__ void lbs_forward_kernel(const double* __restrict__ A, int J, const do
     out[3 * i + 1] = o[1];
     out[3 * i + 2] = o[2];
   }
+  pdl_trigger();
 }
 
 // T_v = sum_j W[v,j] A_j[:3,:]; Tinv_v = [R^-1 | -R^-1 t]
 __global__ void lbs_vertex_kernel(const double* __restrict__ A, int J, const double* __restrict__ W, int64_t V,
                                   double* __restrict__ T, double* __restrict__ Tinv) {
+  pdl_wait();
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x) {
     double m[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     for (int j = 0; j < J; ++j) {
@@ -59,6 +62,7 @@ __global__ void lbs_vertex_kernel(const double* __restrict__ A, int J, const dou
 #pragma unroll
       for (int e2 = 0; e2 < 12; ++e2) T[12 * v + e2] = m[e2];
   }
+  pdl_trigger();
 }
 
 template <bool kBuckets>
@@ -105,14 +109,14 @@ int cf_lbs_forward(const double* A, int J, const double* pts, const double* weig
                    void* stream) {
   if (J < 1 || n_pts < 0) return cf::fail(CF_E_BAD_ARG, "cf_lbs_forward: bad args");
   if (n_pts == 0) return CF_OK;
-  lbs_forward_kernel<<<cf::grid_for(n_pts, 128, 8), 128, 0, cf::as_stream(stream)>>>(A, J, pts, weights, n_pts, out);
+  cf::launch_pdl(lbs_forward_kernel, cf::grid_for(n_pts, 128, 8), 128, 0, cf::as_stream(stream), A, J, pts, weights, n_pts, out);
   return cf::check_launch("cf_lbs_forward");
 }
 
 int cf_lbs_vertex_transforms(const double* A, int J, const double* vert_weights, int64_t n_verts, double* T_out,
                              double* Tinv_out, void* stream) {
   if (J < 1 || n_verts < 1 || !Tinv_out) return cf::fail(CF_E_BAD_ARG, "cf_lbs_vertex_transforms: bad args");
-  lbs_vertex_kernel<<<cf::grid_for(n_verts, 128, 4), 128, 0, cf::as_stream(stream)>>>(A, J, vert_weights, n_verts,
+  cf::launch_pdl(lbs_vertex_kernel, cf::grid_for(n_verts, 128, 4), 128, 0, cf::as_stream(stream), A, J, vert_weights, n_verts,
                                                                                        T_out, Tinv_out);
   return cf::check_launch("cf_lbs_vertex_transforms");
 }

@@ -79,6 +79,7 @@ __device__ __forceinline__ d3 to_object(const double* R, const double* t, d3 p) 
 }
 
 __global__ void rays_kernel(cf_camera cam, double* __restrict__ dirs) {
+  pdl_wait();
   __shared__ double s_cam[13];  // R[9], fx, fy, cx, cy
   if (threadIdx.x == 0) {
 #pragma unroll
@@ -106,6 +107,7 @@ __global__ void rays_kernel(cf_camera cam, double* __restrict__ dirs) {
     dirs[3 * (int64_t)i + 1] = by_nrm(d[1]);
     dirs[3 * (int64_t)i + 2] = by_nrm(d[2]);
   }
+  pdl_trigger();
 }
 
 // cells whose centre lies within `radius` of any bucketed point
@@ -277,6 +279,7 @@ __global__ void occ_splat_cached_kernel(const int* __restrict__ cells, const int
                                         const double* __restrict__ w, const int* __restrict__ count,
                                         int64_t capacity, int k, const double* __restrict__ dqs, cf_occ_grid cg,
                                         cf_occ_grid lg, uint32_t* __restrict__ centre_bits, int* __restrict__ bbox) {
+  pdl_wait();
   const int64_t n = min((int64_t)*count, capacity);
   int lo[3] = {0x7fffffff, 0x7fffffff, 0x7fffffff}, hi[3] = {-0x7fffffff, -0x7fffffff, -0x7fffffff};
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
@@ -319,6 +322,7 @@ __global__ void occ_splat_cached_kernel(const int* __restrict__ cells, const int
       atomicMax(bbox + 3 + a, hi[a]);
     }
   }
+  pdl_trigger();
 }
 
 __device__ __forceinline__ uint64_t window64(const uint32_t* __restrict__ bits, int64_t start) {
@@ -332,6 +336,7 @@ __device__ __forceinline__ uint64_t window64(const uint32_t* __restrict__ bits, 
 // live = 3x3x3 dilation of the padded centre set, cropped to the grid
 __global__ void occ_dilate_kernel(const uint32_t* __restrict__ centre_bits, int res, uint32_t* __restrict__ live,
                                   int* __restrict__ bbox) {
+  pdl_wait();
   const int64_t r = res, P = r + 2, total = r * r * r;
   const int64_t words = (total + 31) / 32;
   if (bbox && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -383,6 +388,7 @@ __global__ void occ_dilate_kernel(const uint32_t* __restrict__ centre_bits, int 
     }
     live[wi] = out;
   }
+  pdl_trigger();
 }
 
 // bbox of the set cells, one CTA (block-reduced, no host init needed)
@@ -455,6 +461,7 @@ __global__ void __launch_bounds__(128) march_kernel(cf_march_desc M, const doubl
                                                     const uint32_t* __restrict__ hbits,
                                                     const uint32_t* __restrict__ obits, cf_march_out H,
                                                     cf_march_out O) {
+  pdl_wait();
   __shared__ double s_fr[15];
   load_frame(M, s_fr);
   const double* obj_R = s_fr + 3;
@@ -535,6 +542,7 @@ __global__ void __launch_bounds__(128) march_kernel(cf_march_desc M, const doubl
       }
     }
   }
+  pdl_trigger();
 }
 
 // human samples: live point -> ED backward warp (exact bucketed k-NN + DQB^-1),
@@ -548,6 +556,7 @@ __global__ void __launch_bounds__(128, CF_CANON_MINB) human_canon_kernel(cf_marc
                                                           const BucketParams* __restrict__ LPp,
                                                           const int* __restrict__ lcs, const double4* __restrict__ ls,
                                                           float4* __restrict__ xu) {
+  pdl_wait();
   __shared__ BucketParams sE, sL;
   extern __shared__ double4 s_anchors[];  // kSmem: the frame's deformed nodes (+ fp32 copies)
   float4* s_af = reinterpret_cast<float4*>(s_anchors + (kSmem ? W.n_nodes : 0));
@@ -623,6 +632,7 @@ __global__ void __launch_bounds__(128, CF_CANON_MINB) human_canon_kernel(cf_marc
       ticket[1] = 0;
     }
   }
+  pdl_trigger();
 }
 
 // rigid object samples: live point -> object-local frame -> unit cube
@@ -630,6 +640,7 @@ __global__ void object_canon_kernel(cf_march_desc M, const double* __restrict__ 
                                     const uint32_t* __restrict__ records, const int* __restrict__ count,
                                     int64_t capacity, const double* obj_min, double inv_side,
                                     float4* __restrict__ xu) {
+  pdl_wait();
   __shared__ double s_fr[15];
   load_frame(M, s_fr);
   const int64_t n = min((int64_t)*count, capacity);
@@ -642,6 +653,7 @@ __global__ void object_canon_kernel(cf_march_desc M, const double* __restrict__ 
                         __double2float_rn(x_mul(x_sub(p.y, M.obj_min[1]), M.obj_inv_side)),
                         __double2float_rn(x_mul(x_sub(p.z, M.obj_min[2]), M.obj_inv_side)), 1.0f);
   }
+  pdl_trigger();
 }
 
 // depth t and step delta of the j-th sample of a ray segment: uniform march
@@ -662,6 +674,7 @@ __device__ __forceinline__ void seg_t_delta(const cf_march_desc& M, const cf_mar
 // T_i = prod_{j<i} (1 - alpha_j); stops once T < t_term
 __global__ void composite_kernel(cf_march_desc M, cf_march_out F, const float4* __restrict__ field, float t_term,
                                  float* __restrict__ rgb, float* __restrict__ depth, float* __restrict__ opacity) {
+  pdl_wait();
   for (int64_t ray = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ray < M.n_rays;
        ray += (int64_t)gridDim.x * blockDim.x) {
     const int off = F.ray_offset[ray], cnt = F.ray_count[ray];
@@ -686,6 +699,7 @@ __global__ void composite_kernel(cf_march_desc M, cf_march_out F, const float4* 
     depth[ray] = dep / fmaxf(op, 1e-6f);
     opacity[ray] = op;
   }
+  pdl_trigger();
 }
 
 // Loss (lambda_depth config.py:55) and compositing backward.
@@ -846,6 +860,7 @@ __global__ void layers_kernel(int64_t n, const float* __restrict__ hr, const flo
                               const float* __restrict__ ho, const float* __restrict__ orgb,
                               const float* __restrict__ od, const float* __restrict__ oo, float bg0, float bg1,
                               float bg2, float* __restrict__ out, uint8_t* __restrict__ layer) {
+  pdl_wait();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const bool h = hr && ho[i] > 0.5f, o = orgb && oo[i] > 0.5f;
     int L = 0;
@@ -858,6 +873,7 @@ __global__ void layers_kernel(int64_t n, const float* __restrict__ hr, const flo
     out[3 * i + 2] = src ? src[2] : bg2;
     if (layer) layer[i] = (uint8_t)L;
   }
+  pdl_trigger();
 }
 
 }  // namespace
@@ -868,7 +884,7 @@ int cf_camera_rays(const cf_camera* cam, double* dirs, void* stream) {
   if (!cam || cam->width < 1 || cam->height < 1 || !dirs || (int64_t)cam->width * cam->height > INT32_MAX)
     return cf::fail(CF_E_BAD_ARG, "cf_camera_rays: bad args");
   const int64_t n = (int64_t)cam->width * cam->height;
-  rays_kernel<<<cf::grid_for(n, 256, 8), 256, 0, cf::as_stream(stream)>>>(*cam, dirs);
+  cf::launch_pdl(rays_kernel, cf::grid_for(n, 256, 8), 256, 0, cf::as_stream(stream), *cam, dirs);
   return cf::check_launch("cf_camera_rays");
 }
 
@@ -937,13 +953,13 @@ int cf_occ_splat_cached(const int* cells, const int* nbr, const double* w, const
   }
   const unsigned grid = cf::grid_for(capacity, 256, 4);
   if (k <= 4)
-    occ_splat_cached_kernel<4><<<grid, 256, 0, st>>>(cells, nbr, w, count, capacity, k, dqs, *cg, *lg, scratch_bits,
+    cf::launch_pdl(occ_splat_cached_kernel<4>, grid, 256, 0, st, cells, nbr, w, count, capacity, k, dqs, *cg, *lg, scratch_bits,
                                                      live_bbox);
   else
-    occ_splat_cached_kernel<8><<<grid, 256, 0, st>>>(cells, nbr, w, count, capacity, k, dqs, *cg, *lg, scratch_bits,
+    cf::launch_pdl(occ_splat_cached_kernel<8>, grid, 256, 0, st, cells, nbr, w, count, capacity, k, dqs, *cg, *lg, scratch_bits,
                                                      live_bbox);
   const int64_t words = ((int64_t)lg->res * lg->res * lg->res + 31) / 32;
-  occ_dilate_kernel<<<cf::grid_for(words, 256, 8), 256, 0, st>>>(scratch_bits, lg->res, live_bits, live_bbox);
+  cf::launch_pdl(occ_dilate_kernel, cf::grid_for(words, 256, 8), 256, 0, st, scratch_bits, lg->res, live_bits, live_bbox);
   return cf::check_launch("cf_occ_splat_cached");
 }
 
@@ -964,7 +980,7 @@ int cf_march(const cf_march_desc* M, const double* dirs, const uint32_t* human_b
   if (H.records) CF_CHECK_CUDA(cudaMemsetAsync(H.counters, 0, 4 * sizeof(int), st));
   if (O.records) CF_CHECK_CUDA(cudaMemsetAsync(O.counters, 0, 4 * sizeof(int), st));
   if (M->n_rays == 0) return CF_OK;
-  march_kernel<<<cf::grid_for(M->n_rays, 128, 8), 128, 0, st>>>(*M, dirs, H.records ? human_bits : nullptr,
+  cf::launch_pdl(march_kernel, cf::grid_for(M->n_rays, 128, 8), 128, 0, st, *M, dirs, H.records ? human_bits : nullptr,
                                                                   O.records ? object_bits : nullptr, H, O);
   return cf::check_launch("cf_march");
 }
@@ -983,7 +999,7 @@ int cf_human_canon(const cf_march_desc* M, const double* dirs, const cf_march_ou
   int per_sm = 0;                                                                                                \
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, human_canon_kernel<KK, SM>, 128, dsm);                  \
   const unsigned grid = cf::grid_for(F->capacity, 128, per_sm > 0 ? per_sm : 1);                                 \
-  human_canon_kernel<KK, SM><<<grid, 128, dsm, st>>>(                                                            \
+  cf::launch_pdl(human_canon_kernel<KK, SM>, grid, 128, dsm, st, \
       *M, dirs, F->records, F->counters, F->capacity, *W, anchor_buckets ? anchor_buckets->params : nullptr,    \
       anchor_buckets ? anchor_buckets->cell_start : nullptr, anchor_buckets ? anchor_buckets->sorted : nullptr, \
       lbs ? vert_buckets->params : nullptr, lbs ? vert_buckets->cell_start : nullptr,                            \
@@ -1003,8 +1019,7 @@ int cf_human_canon(const cf_march_desc* M, const double* dirs, const cf_march_ou
 int cf_object_canon(const cf_march_desc* M, const double* dirs, const cf_march_out* F, float* xu_f, void* stream) {
   float4* xu = reinterpret_cast<float4*>(xu_f);
   if (!M || !F) return cf::fail(CF_E_BAD_ARG, "cf_object_canon: bad args");
-  object_canon_kernel<<<cf::grid_for(F->capacity, 256, 4), 256, 0, cf::as_stream(stream)>>>(
-      *M, dirs, F->records, F->counters, F->capacity, M->obj_min, M->obj_inv_side, xu);
+  cf::launch_pdl(object_canon_kernel, cf::grid_for(F->capacity, 256, 4), 256, 0, cf::as_stream(stream), *M, dirs, F->records, F->counters, F->capacity, M->obj_min, M->obj_inv_side, xu);
   return cf::check_launch("cf_object_canon");
 }
 
@@ -1013,7 +1028,7 @@ int cf_composite(const cf_march_desc* M, const cf_march_out* F, const float* fie
   if (!M || !F || !rgb || !depth || !opacity) return cf::fail(CF_E_BAD_ARG, "cf_composite: bad args");
   const float4* field = reinterpret_cast<const float4*>(field_f);
   if (M->n_rays == 0) return CF_OK;
-  composite_kernel<<<cf::grid_for(M->n_rays, 128, 8), 128, 0, cf::as_stream(stream)>>>(*M, *F, field, t_term, rgb,
+  cf::launch_pdl(composite_kernel, cf::grid_for(M->n_rays, 128, 8), 128, 0, cf::as_stream(stream), *M, *F, field, t_term, rgb,
                                                                                         depth, opacity);
   return cf::check_launch("cf_composite");
 }
@@ -1048,7 +1063,7 @@ int cf_composite_layers(int64_t n, const float* h_rgb, const float* h_depth, con
                         void* stream) {
   if (n < 0 || !bg || !out) return cf::fail(CF_E_BAD_ARG, "cf_composite_layers: bad args");
   if (n == 0) return CF_OK;
-  layers_kernel<<<cf::grid_for(n, 256, 4), 256, 0, cf::as_stream(stream)>>>(n, h_rgb, h_depth, h_opac, o_rgb, o_depth,
+  cf::launch_pdl(layers_kernel, cf::grid_for(n, 256, 4), 256, 0, cf::as_stream(stream), n, h_rgb, h_depth, h_opac, o_rgb, o_depth,
                                                                              o_opac, bg[0], bg[1], bg[2], out, layer);
   return cf::check_launch("cf_composite_layers");
 }
