@@ -154,11 +154,11 @@ class ClockSampler:
 # ----------------------------------------------------------------- workload
 
 # stage -> the mark it is timed from (render.py Renderer._launch_view order)
-STAGE_PRED = {"lbs_setup": "start", "ed_setup": "start", "rays": "ed_setup", "march": "rays",
+STAGE_PRED = {"lbs_setup": "start", "ed_setup": "start", "march": "ed_setup",
               "object_canon": "march", "object_field": "object_canon", "object_composite": "object_field",
               "human_canon": "march", "human_hash_d": "human_canon", "human_deform_mlp": "human_hash_d",
               "human_hash_c": "human_deform_mlp", "human_color_mlp": "human_hash_c",
-              "human_composite": "human_color_mlp", "layers": "human_composite"}
+              "human_composite": "human_color_mlp"}
 
 
 def build_workload(args, rank):

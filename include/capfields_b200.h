@@ -263,6 +263,10 @@ int cf_occ_bbox(const uint32_t* bits, const cf_occ_grid* g, int* bbox, void* str
  * margin, so decisions equal a test of every sample */
 int cf_march(const cf_march_desc* M, const double* dirs, const uint32_t* human_bits, const uint32_t* object_bits,
              const cf_march_out* human, const cf_march_out* object, void* stream);
+/* cf_camera_rays + cf_march in one kernel: each ray's direction is generated
+ * (and written to dirs) by the thread that marches it; n_rays = width * height */
+int cf_rays_march(const cf_camera* cam, const cf_march_desc* M, double* dirs, const uint32_t* human_bits,
+                  const uint32_t* object_bits, const cf_march_out* human, const cf_march_out* object, void* stream);
 /* human samples -> canonical unit cube (xu: float4 x,y,z,flag; flag 1 = ED, 2 = LBS, 0 = invalid) */
 int cf_human_canon(const cf_march_desc* M, const double* dirs, const cf_march_out* F, const cf_human_warp* W,
                    const cf_buckets_t* anchor_buckets, const cf_buckets_t* vert_buckets, float* xu, void* stream);
@@ -274,6 +278,11 @@ int cf_composite(const cf_march_desc* M, const cf_march_out* F, const float* fie
 int cf_composite_layers(int64_t n, const float* h_rgb, const float* h_depth, const float* h_opac, const float* o_rgb,
                         const float* o_depth, const float* o_opac, const float* bg, float* out, uint8_t* layer,
                         void* stream);
+/* cf_composite of the human field fused with cf_composite_layers against an
+ * already composited object layer (o_* may be NULL: no object) */
+int cf_composite_final(const cf_march_desc* M, const cf_march_out* F, const float* field, float t_term, float* rgb,
+                       float* depth, float* opacity, const float* o_rgb, const float* o_depth, const float* o_opac,
+                       const float* bg, float* out, uint8_t* layer, void* stream);
 
 /* fused radiance field of one field: hash grids + MLPs on tcgen05.
  * wblob = fp16 canonical-layout weights, in order

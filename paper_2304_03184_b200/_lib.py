@@ -125,6 +125,8 @@ _SIGS = {
     "cf_occ_box_shell": [_P(OccGrid), _p, _f64, _p, _p],
     "cf_occ_splat": [_p, _P(OccGrid), _p, _p, _i32, _f64, _P(OccGrid), _p, _p],
     "cf_march": [_P(MarchDesc), _p, _p, _p, _P(MarchOut), _P(MarchOut), _p],
+    "cf_rays_march": [_P(Camera), _P(MarchDesc), _p, _p, _p, _P(MarchOut), _P(MarchOut), _p],
+    "cf_composite_final": [_P(MarchDesc), _P(MarchOut), _p, ctypes.c_float, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p],
     "cf_occ_bbox": [_p, _P(OccGrid), _p, _p],
     "cf_occ_cache": [_p, _P(OccGrid), _p, _i32, _f64, _i64, _p, _p, _p, _p, _p],
     "cf_occ_splat_cached": [_p, _p, _p, _p, _i64, _i32, _p, _P(OccGrid), _P(OccGrid), _p, _p, _p, _p],

@@ -7,6 +7,8 @@
 #include <algorithm>
 #include <cmath>
 
+#include <cooperative_groups.h>
+
 #include "buckets.cuh"
 #include "dq.cuh"
 
@@ -25,6 +27,26 @@ __global__ void deform_nodes_kernel(const double* __restrict__ nodes, const doub
 }
 
 // ------------------------------------------------------------------ buckets
+
+// grid of G cells along the longest extent of the bbox [mn, mx]
+__device__ __forceinline__ void bucket_params_finish(const double* mn, const double* mx, int n, int G,
+                                                     BucketParams* P) {
+  double ext = 0.0, scale = 0.0;
+  for (int a = 0; a < 3; ++a) {
+    ext = fmax(ext, mx[a] - mn[a]);
+    scale = fmax(scale, fmax(fabs(mn[a]), fabs(mx[a])));
+  }
+  if (!(ext > 0.0)) ext = fmax(scale, 1.0) * 1e-3;
+  const double h = ext * (1.0 + 1e-9) / G;
+  for (int a = 0; a < 3; ++a) {
+    P->origin[a] = mn[a] - 1e-12 * (fabs(mn[a]) + ext);
+    int g = (int)ceil((mx[a] - P->origin[a]) / h);
+    P->g[a] = g < 1 ? 1 : (g > G ? G : g);
+  }
+  P->h = h;
+  P->margin = 1e-10 * (scale + ext) + 1e-300;
+  P->n = n;
+}
 
 __device__ __forceinline__ void bucket_params_body(const double* __restrict__ pts, int n, int G, BucketParams* P) {
   __shared__ double smin[3][32], smax[3][32];
@@ -49,7 +71,7 @@ __device__ __forceinline__ void bucket_params_body(const double* __restrict__ pt
   __syncthreads();
   if (threadIdx.x == 0) {
     const int nw = blockDim.x >> 5;
-    double mn[3], mx[3], ext = 0.0, scale = 0.0;
+    double mn[3], mx[3];
     for (int a = 0; a < 3; ++a) {
       mn[a] = smin[a][0];
       mx[a] = smax[a][0];
@@ -57,19 +79,8 @@ __device__ __forceinline__ void bucket_params_body(const double* __restrict__ pt
         mn[a] = fmin(mn[a], smin[a][j]);
         mx[a] = fmax(mx[a], smax[a][j]);
       }
-      ext = fmax(ext, mx[a] - mn[a]);
-      scale = fmax(scale, fmax(fabs(mn[a]), fabs(mx[a])));
     }
-    if (!(ext > 0.0)) ext = fmax(scale, 1.0) * 1e-3;
-    const double h = ext * (1.0 + 1e-9) / G;
-    for (int a = 0; a < 3; ++a) {
-      P->origin[a] = mn[a] - 1e-12 * (fabs(mn[a]) + ext);
-      int g = (int)ceil((mx[a] - P->origin[a]) / h);
-      P->g[a] = g < 1 ? 1 : (g > G ? G : g);
-    }
-    P->h = h;
-    P->margin = 1e-10 * (scale + ext) + 1e-300;
-    P->n = n;
+    bucket_params_finish(mn, mx, n, G, P);
   }
 }
 
@@ -146,6 +157,170 @@ __global__ void bucket_scatter_kernel(const double* __restrict__ pts, int n, con
                                       const int* __restrict__ point_cell, const int* __restrict__ point_slot,
                                       double4* __restrict__ sorted) {
   bucket_scatter_body(pts, n, cell_start, point_cell, point_slot, sorted);
+}
+
+// single-CTA exclusive scan of an int array in shared memory (n = ncells + 1 entries)
+__device__ __forceinline__ void smem_scan(int* __restrict__ a, int n) {
+  __shared__ int warp_tot[32];
+  const int chunk = (n + blockDim.x - 1) / blockDim.x;
+  const int b = min(n, (int)threadIdx.x * chunk), e = min(n, b + chunk);
+  int v = 0;
+  for (int i = b; i < e; ++i) v += a[i];
+  int x = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if ((threadIdx.x & 31) >= o) x += y;
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 31) warp_tot[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int t = (threadIdx.x < (blockDim.x >> 5)) ? warp_tot[threadIdx.x] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, t, o);
+      if (threadIdx.x >= o) t += y;
+    }
+    if (threadIdx.x < (blockDim.x >> 5)) warp_tot[threadIdx.x] = t;
+  }
+  __syncthreads();
+  int run = (w > 0 ? warp_tot[w - 1] : 0) + x - v;
+  for (int i = b; i < e; ++i) {
+    const int c = a[i];
+    a[i] = run;
+    run += c;
+  }
+}
+
+// The whole build in one CTA with the cell counts in shared memory (per-frame
+// skin vertices: 6 890 points, 31^3 cells): shared-memory atomics and scan,
+// one coalesced write of cell_start — no global atomics or round trips.
+constexpr int kSmemBucketCells = 48 * 1024;
+__global__ void __launch_bounds__(1024) bucket_build_smem_kernel(const double* __restrict__ pts, int n, int G,
+                                                                 BucketParams* P, int* __restrict__ cell_start,
+                                                                 int* __restrict__ point_cell,
+                                                                 int* __restrict__ point_slot,
+                                                                 double4* __restrict__ sorted) {
+  extern __shared__ int s_cnt[];
+  pdl_wait();
+  const int cells_max = G * G * G;
+  for (int i = threadIdx.x; i <= cells_max; i += blockDim.x) s_cnt[i] = 0;
+  bucket_params_body(pts, n, G, P);
+  __syncthreads();
+  const BucketParams Pl = *P;
+  const int ncells = Pl.g[0] * Pl.g[1] * Pl.g[2];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    int c[3];
+    bucket_cell(Pl, load_d3(pts + 3 * i), c);
+    const int cell = (c[2] * Pl.g[1] + c[1]) * Pl.g[0] + c[0];
+    point_cell[i] = cell;
+    point_slot[i] = atomicAdd(s_cnt + cell, 1);
+  }
+  __syncthreads();
+  smem_scan(s_cnt, ncells + 1);
+  __syncthreads();
+  for (int i = threadIdx.x; i <= ncells; i += blockDim.x) cell_start[i] = s_cnt[i];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int dst = s_cnt[point_cell[i]] + point_slot[i];
+    sorted[dst] = make_double4(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2], (double)i);
+  }
+  pdl_trigger();
+}
+
+// The build spread over a thread-block cluster of kBucketCluster CTAs (one per
+// SM), with the cell counts in CTA 0's shared memory and every CTA counting /
+// scattering its slice of the points through distributed shared memory: the
+// per-point phases run on 8 SMs instead of one, and the phase boundaries are
+// cluster barriers instead of kernel launches (per-frame skin vertices: 6 890
+// points, 31^3 cells).
+constexpr int kBucketCluster = 8;
+__global__ void __cluster_dims__(kBucketCluster, 1, 1) __launch_bounds__(1024)
+    bucket_build_cluster_kernel(const double* __restrict__ pts, int n, int G, BucketParams* P,
+                                int* __restrict__ cell_start, int* __restrict__ point_cell,
+                                int* __restrict__ point_slot, double4* __restrict__ sorted) {
+  extern __shared__ int s_cnt[];  // cell counts, used in CTA 0
+  __shared__ double s_box[6];     // this CTA's partial bbox (lo xyz, hi xyz)
+  __shared__ double s_w[6][32];
+  __shared__ BucketParams s_P;    // CTA 0: the grid parameters
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const int tid = threadIdx.x, stride = kBucketCluster * blockDim.x;
+  const int first = rank * blockDim.x + tid;
+  pdl_wait();
+  if (rank == 0)
+    for (int i = tid; i <= G * G * G; i += blockDim.x) s_cnt[i] = 0;
+  // 1. partial bounding boxes
+  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int i = first; i < n; i += stride)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double v = pts[3 * i + a];
+      lo[a] = fmin(lo[a], v);
+      hi[a] = fmax(hi[a], v);
+    }
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+    for (int o = 16; o > 0; o >>= 1) {
+      lo[a] = fmin(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+      hi[a] = fmax(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+    }
+  if ((tid & 31) == 0)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      s_w[a][tid >> 5] = lo[a];
+      s_w[3 + a][tid >> 5] = hi[a];
+    }
+  __syncthreads();
+  if (tid < 6) {
+    double v = s_w[tid][0];
+    for (int j = 1; j < (int)(blockDim.x >> 5); ++j) v = tid < 3 ? fmin(v, s_w[tid][j]) : fmax(v, s_w[tid][j]);
+    s_box[tid] = v;
+  }
+  cl.sync();
+  // 2. CTA 0: grid parameters from the cluster's bbox
+  if (rank == 0 && tid == 0) {
+    double mn[3], mx[3];
+    for (int a = 0; a < 3; ++a) {
+      mn[a] = INFINITY;
+      mx[a] = -INFINITY;
+    }
+    for (int r = 0; r < kBucketCluster; ++r) {
+      const double* b = cl.map_shared_rank(s_box, r);
+      for (int a = 0; a < 3; ++a) {
+        mn[a] = fmin(mn[a], b[a]);
+        mx[a] = fmax(mx[a], b[3 + a]);
+      }
+    }
+    bucket_params_finish(mn, mx, n, G, &s_P);
+    *P = s_P;
+  }
+  cl.sync();
+  const BucketParams Pl = *cl.map_shared_rank(&s_P, 0);
+  int* cnt0 = cl.map_shared_rank(s_cnt, 0);
+  const int ncells = Pl.g[0] * Pl.g[1] * Pl.g[2];
+  // 3. counts (DSMEM atomics into CTA 0)
+  for (int i = first; i < n; i += stride) {
+    int c[3];
+    bucket_cell(Pl, load_d3(pts + 3 * i), c);
+    const int cell = (c[2] * Pl.g[1] + c[1]) * Pl.g[0] + c[0];
+    point_cell[i] = cell;
+    point_slot[i] = atomicAdd(cnt0 + cell, 1);
+  }
+  cl.sync();
+  // 4. CTA 0: exclusive scan -> cell starts
+  if (rank == 0) {
+    smem_scan(s_cnt, ncells + 1);
+    __syncthreads();
+    for (int i = tid; i <= ncells; i += blockDim.x) cell_start[i] = s_cnt[i];
+  }
+  cl.sync();
+  // 5. scatter (starts read from CTA 0 through DSMEM)
+  for (int i = first; i < n; i += stride) {
+    const int dst = cnt0[point_cell[i]] + point_slot[i];
+    sorted[dst] = make_double4(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2], (double)i);
+  }
+  cl.sync();  // CTA 0's shared memory stays alive until every CTA is done with it
+  pdl_trigger();
 }
 
 // the whole build in one CTA for small point sets (per-frame ED nodes / skin
@@ -390,6 +565,22 @@ int buckets_build(cf_buckets* b, const double* pts, int64_t n, int grid_res, cud
   b->grid_res = G;
   b->ccl_k = 0;  // candidate lists describe the previous point set
   const int64_t cells = (int64_t)G * G * G;
+  if (n >= 2048 && n <= 65536 && cells + 1 <= kSmemBucketCells) {
+    const size_t smem = sizeof(int) * (size_t)(cells + 1);
+    CF_CHECK_CUDA(cudaFuncSetAttribute(bucket_build_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(sizeof(int) * kSmemBucketCells)));
+    cf::launch_pdl(bucket_build_cluster_kernel, kBucketCluster, 1024, smem, st, pts, (int)n, G, b->params,
+                   b->cell_start, b->point_cell, b->point_slot, b->sorted);
+    return check_launch("buckets_build");
+  }
+  if (n <= 65536 && cells + 1 <= kSmemBucketCells) {
+    const size_t smem = sizeof(int) * (size_t)(cells + 1);
+    CF_CHECK_CUDA(cudaFuncSetAttribute(bucket_build_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(sizeof(int) * kSmemBucketCells)));
+    cf::launch_pdl(bucket_build_smem_kernel, 1, 1024, smem, st, pts, (int)n, G, b->params, b->cell_start,
+                   b->point_cell, b->point_slot, b->sorted);
+    return check_launch("buckets_build");
+  }
   if (n <= 65536 && cells <= (1 << 18)) {
     cf::launch_pdl(bucket_build_small_kernel, 1, 1024, 0, st, pts, (int)n, G, b->params, b->cell_start, b->point_cell,
                                                   b->point_slot, b->sorted);

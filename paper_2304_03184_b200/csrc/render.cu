@@ -78,9 +78,9 @@ __device__ __forceinline__ d3 to_object(const double* R, const double* t, d3 p) 
   return d3{o[0], o[1], o[2]};
 }
 
-__global__ void rays_kernel(cf_camera cam, double* __restrict__ dirs) {
-  pdl_wait();
-  __shared__ double s_cam[13];  // R[9], fx, fy, cx, cy
+// camera parameters into shared memory: R[9], fx, fy, cx, cy — from the device
+// block cam.params when set (graph replay), else the by-value fields. Block-wide.
+__device__ __forceinline__ void load_camera(const cf_camera& cam, double* s_cam) {
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int i = 0; i < 9; ++i) s_cam[i] = cam.params ? cam.params[i] : cam.R[i];
@@ -90,23 +90,30 @@ __global__ void rays_kernel(cf_camera cam, double* __restrict__ dirs) {
     s_cam[12] = cam.params ? cam.params[12] : cam.cy;
   }
   __syncthreads();
-  const double* R = s_cam;
-  const double cx = s_cam[11], cy = s_cam[12];
+}
+
+// unit direction of pixel i (camera.py:94-108: R (u-cx)/fx, (v-cy)/fy, 1), normalised
+__device__ __forceinline__ d3 pixel_dir(const double* s_cam, const ExactDiv& by_fx, const ExactDiv& by_fy, int width,
+                                        int i) {
+  const int v_i = i / width;
+  const double u = (double)(i - v_i * width), v = (double)v_i;
+  const double dc[3] = {by_fx(x_sub(u, s_cam[11])), by_fy(x_sub(v, s_cam[12])), 1.0};
+  double d[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+    d[a] = __fma_rn(dc[2], s_cam[3 * a + 2], __fma_rn(dc[1], s_cam[3 * a + 1], x_mul(dc[0], s_cam[3 * a])));
+  const ExactDiv by_nrm(sqrt(x_add(x_add(x_mul(d[0], d[0]), x_mul(d[1], d[1])), x_mul(d[2], d[2]))));
+  return d3{by_nrm(d[0]), by_nrm(d[1]), by_nrm(d[2])};
+}
+
+__global__ void rays_kernel(cf_camera cam, double* __restrict__ dirs) {
+  pdl_wait();
+  __shared__ double s_cam[13];
+  load_camera(cam, s_cam);
   const int n = cam.width * cam.height;
   const ExactDiv by_fx(s_cam[9]), by_fy(s_cam[10]);
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int v_i = i / cam.width;
-    const double u = (double)(i - v_i * cam.width), v = (double)v_i;
-    const double dc[3] = {by_fx(x_sub(u, cx)), by_fy(x_sub(v, cy)), 1.0};
-    double d[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-      d[a] = __fma_rn(dc[2], R[3 * a + 2], __fma_rn(dc[1], R[3 * a + 1], x_mul(dc[0], R[3 * a])));
-    const ExactDiv by_nrm(sqrt(x_add(x_add(x_mul(d[0], d[0]), x_mul(d[1], d[1])), x_mul(d[2], d[2]))));
-    dirs[3 * (int64_t)i] = by_nrm(d[0]);
-    dirs[3 * (int64_t)i + 1] = by_nrm(d[1]);
-    dirs[3 * (int64_t)i + 2] = by_nrm(d[2]);
-  }
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    store_d3(dirs + 3 * (int64_t)i, pixel_dir(s_cam, by_fx, by_fy, cam.width, i));
   pdl_trigger();
 }
 
@@ -457,13 +464,19 @@ __device__ __forceinline__ void scan_samples(int i0, int i1, Test test, uint32_t
   }
 }
 
-__global__ void __launch_bounds__(128) march_kernel(cf_march_desc M, const double* __restrict__ dirs,
+// kRays: the march also generates the ray directions (one thread per pixel) and
+// writes them to dirs for the later stages, instead of reading them
+template <bool kRays>
+__global__ void __launch_bounds__(128) march_kernel(cf_march_desc M, cf_camera cam, double* __restrict__ dirs,
                                                     const uint32_t* __restrict__ hbits,
                                                     const uint32_t* __restrict__ obits, cf_march_out H,
                                                     cf_march_out O) {
   pdl_wait();
   __shared__ double s_fr[15];
+  __shared__ double s_cam[13];
+  if (kRays) load_camera(cam, s_cam);
   load_frame(M, s_fr);
+  const ExactDiv by_fx(kRays ? s_cam[9] : 1.0), by_fy(kRays ? s_cam[10] : 1.0);
   const double* obj_R = s_fr + 3;
   const double* obj_t = s_fr + 12;
   const d3 o{s_fr[0], s_fr[1], s_fr[2]};
@@ -486,7 +499,15 @@ __global__ void __launch_bounds__(128) march_kernel(cf_march_desc M, const doubl
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < M.n_rays; base += (int64_t)gridDim.x * blockDim.x) {
     const int64_t ray = base + threadIdx.x;
     const bool live = ray < M.n_rays;
-    const d3 d = live ? load_d3(dirs + 3 * ray) : d3{0.0, 0.0, 1.0};
+    d3 d{0.0, 0.0, 1.0};
+    if (live) {
+      if (kRays) {
+        d = pixel_dir(s_cam, by_fx, by_fy, cam.width, (int)ray);
+        store_d3(dirs + 3 * ray, d);
+      } else {
+        d = load_d3(dirs + 3 * ray);
+      }
+    }
     uint32_t hm[4] = {0, 0, 0, 0}, om[4] = {0, 0, 0, 0};  // occupancy masks of up to 128 samples
     int hc = 0, oc = 0;
     if (live && hbits && !hempty) {
@@ -698,6 +719,52 @@ __global__ void composite_kernel(cf_march_desc M, cf_march_out F, const float4* 
     rgb[3 * ray + 2] = b;
     depth[ray] = dep / fmaxf(op, 1e-6f);
     opacity[ray] = op;
+  }
+  pdl_trigger();
+}
+
+// human-field composite of a ray fused with the layer choice:
+// the object layer was composited before (side stream); writes the human layer's
+// rgb/depth/opacity too (same values as composite_kernel)
+__global__ void composite_final_kernel(cf_march_desc M, cf_march_out F, const float4* __restrict__ field,
+                                       float t_term, float* __restrict__ rgb, float* __restrict__ depth,
+                                       float* __restrict__ opacity, const float* __restrict__ orgb,
+                                       const float* __restrict__ od, const float* __restrict__ oo, float bg0,
+                                       float bg1, float bg2, float* __restrict__ out, uint8_t* __restrict__ layer) {
+  pdl_wait();
+  for (int64_t ray = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ray < M.n_rays;
+       ray += (int64_t)gridDim.x * blockDim.x) {
+    const int off = F.ray_offset[ray], cnt = F.ray_count[ray];
+    float T = 1.0f, r = 0.f, g = 0.f, b = 0.f, dep = 0.f, op = 0.f;
+    for (int j = 0; j < cnt; ++j) {
+      const float4 f = field[off + j];
+      float t, delta;
+      seg_t_delta(M, F, off, cnt, j, t, delta);
+      const float alpha = 1.0f - expf(-f.x * delta);
+      const float w = T * alpha;
+      r += w * f.y;
+      g += w * f.z;
+      b += w * f.w;
+      dep += w * t;
+      op += w;
+      T *= 1.0f - alpha;
+      if (T < t_term) break;
+    }
+    const float hd = dep / fmaxf(op, 1e-6f);
+    rgb[3 * ray] = r;
+    rgb[3 * ray + 1] = g;
+    rgb[3 * ray + 2] = b;
+    depth[ray] = hd;
+    opacity[ray] = op;
+    const bool h = op > 0.5f, o = orgb && oo[ray] > 0.5f;
+    int L = 0;
+    if (h && o) L = hd <= od[ray] ? 1 : 2;
+    else if (h) L = 1;
+    else if (o) L = 2;
+    out[3 * ray] = L == 1 ? r : (L == 2 ? orgb[3 * ray] : bg0);
+    out[3 * ray + 1] = L == 1 ? g : (L == 2 ? orgb[3 * ray + 1] : bg1);
+    out[3 * ray + 2] = L == 1 ? b : (L == 2 ? orgb[3 * ray + 2] : bg2);
+    if (layer) layer[ray] = (uint8_t)L;
   }
   pdl_trigger();
 }
@@ -980,9 +1047,25 @@ int cf_march(const cf_march_desc* M, const double* dirs, const uint32_t* human_b
   if (H.records) CF_CHECK_CUDA(cudaMemsetAsync(H.counters, 0, 4 * sizeof(int), st));
   if (O.records) CF_CHECK_CUDA(cudaMemsetAsync(O.counters, 0, 4 * sizeof(int), st));
   if (M->n_rays == 0) return CF_OK;
-  cf::launch_pdl(march_kernel, cf::grid_for(M->n_rays, 128, 8), 128, 0, st, *M, dirs, H.records ? human_bits : nullptr,
-                                                                  O.records ? object_bits : nullptr, H, O);
+  cf::launch_pdl(march_kernel<false>, cf::grid_for(M->n_rays, 128, 8), 128, 0, st, *M, cf_camera{},
+                 const_cast<double*>(dirs), H.records ? human_bits : nullptr, O.records ? object_bits : nullptr, H, O);
   return cf::check_launch("cf_march");
+}
+
+int cf_rays_march(const cf_camera* cam, const cf_march_desc* M, double* dirs, const uint32_t* human_bits,
+                  const uint32_t* object_bits, const cf_march_out* human, const cf_march_out* object, void* stream) {
+  if (!cam || !M || !dirs || M->n_samples < 1 || M->n_samples > 128 || cam->width < 1 || cam->height < 1 ||
+      (int64_t)cam->width * cam->height != M->n_rays || M->n_rays >= (1LL << 24))
+    return cf::fail(CF_E_BAD_ARG, "cf_rays_march: bad args (n_rays = width*height < 2^24, <= 128 samples)");
+  cf_march_out H{}, O{};
+  if (human && human_bits) H = *human;
+  if (object && object_bits) O = *object;
+  cudaStream_t st = cf::as_stream(stream);
+  if (H.records) CF_CHECK_CUDA(cudaMemsetAsync(H.counters, 0, 4 * sizeof(int), st));
+  if (O.records) CF_CHECK_CUDA(cudaMemsetAsync(O.counters, 0, 4 * sizeof(int), st));
+  cf::launch_pdl(march_kernel<true>, cf::grid_for(M->n_rays, 128, 8), 128, 0, st, *M, *cam, dirs,
+                 H.records ? human_bits : nullptr, O.records ? object_bits : nullptr, H, O);
+  return cf::check_launch("cf_rays_march");
 }
 
 int cf_human_canon(const cf_march_desc* M, const double* dirs, const cf_march_out* F, const cf_human_warp* W,
@@ -1066,6 +1149,18 @@ int cf_composite_layers(int64_t n, const float* h_rgb, const float* h_depth, con
   cf::launch_pdl(layers_kernel, cf::grid_for(n, 256, 4), 256, 0, cf::as_stream(stream), n, h_rgb, h_depth, h_opac, o_rgb, o_depth,
                                                                              o_opac, bg[0], bg[1], bg[2], out, layer);
   return cf::check_launch("cf_composite_layers");
+}
+
+int cf_composite_final(const cf_march_desc* M, const cf_march_out* F, const float* field, float t_term, float* rgb,
+                       float* depth, float* opacity, const float* o_rgb, const float* o_depth, const float* o_opac,
+                       const float* bg, float* out, uint8_t* layer, void* stream) {
+  if (!M || !F || !field || !rgb || !depth || !opacity || !bg || !out || (o_rgb && (!o_depth || !o_opac)))
+    return cf::fail(CF_E_BAD_ARG, "cf_composite_final: bad args");
+  if (M->n_rays == 0) return CF_OK;
+  cf::launch_pdl(composite_final_kernel, cf::grid_for(M->n_rays, 128, 8), 128, 0, cf::as_stream(stream), *M, *F,
+                 reinterpret_cast<const float4*>(field), t_term, rgb, depth, opacity, o_rgb, o_depth, o_opac, bg[0],
+                 bg[1], bg[2], out, layer);
+  return cf::check_launch("cf_composite_final");
 }
 
 }  // extern "C"

@@ -245,6 +245,8 @@ class Renderer:
             self.M.obj_inv_side = obj.inv_side
         self.frame = None
         self.marks = None
+        # side stream: the per-frame LBS chain and the object field run next to the
+        # human chain (stream priorities and a later object fork were measured: no gain)
         self.side = torch.cuda.Stream(device=d)
         self._lbs_done = torch.cuda.Event()
         self._obj_done = torch.cuda.Event()
@@ -314,15 +316,18 @@ class Renderer:
         n = self._dqs.shape[0]
         # the backward-LBS chain (vertex transforms, posed vertices, their buckets)
         # is independent of the ED chain: run it on the side stream
+        # (and the deformed nodes + their buckets, which only the canonicalisation reads,
+        # after the same event)
         main = torch.cuda.current_stream()
         self._fork(main, self.side)
         with torch.cuda.stream(self.side):
+            ss = _lib.stream_ptr()
+            _lib.call("cf_deform_nodes", h.nodes.data_ptr(), self._dqs.data_ptr(), n, self._anchors.data_ptr(), ss)
+            if n > 1024:  # small graphs are scanned from shared memory (no buckets needed)
+                self._anchor_buckets.build(self._anchors)
             h.lbs.set_pose(self._A)
             self._mark("lbs_setup")
             self._lbs_done.record(self.side)
-        _lib.call("cf_deform_nodes", h.nodes.data_ptr(), self._dqs.data_ptr(), n, self._anchors.data_ptr(), s)
-        if n > 1024:  # small graphs are scanned from shared memory (no buckets needed)
-            self._anchor_buckets.build(self._anchors)
         _lib.call("cf_occ_splat_cached", h.occ_cells.data_ptr(), h.occ_nbr.data_ptr(), h.occ_w.data_ptr(),
                   h.occ_count.data_ptr(), h.occ_cap, self.cfg.ed_k, self._dqs.data_ptr(), _lib.byref(h.canon_occ),
                   _lib.byref(self.live_occ), self.live_scratch.data_ptr(), self.live_bits.data_ptr(),
@@ -444,15 +449,16 @@ class Renderer:
         s = _lib.stream_ptr()
         if setup:
             self._human_setup()
-        self._rays()
         hb, ob = self.hb, self.ob
-        self._mark("rays")
-        _lib.call("cf_march", _lib.byref(self.M), self.dirs.data_ptr(),
+        # ray generation fused into the march (directions written for the later stages)
+        self.M.n_rays = self.n_rays
+        _lib.call("cf_rays_march", _lib.byref(self.cam), _lib.byref(self.M), self.dirs.data_ptr(),
                   self.live_bits.data_ptr() if hb else None, self.obj.bits.data_ptr() if ob else None,
                   _lib.byref(hb.mo) if hb else None, _lib.byref(ob.mo) if ob else None, s)
         self._mark("march")
         main = torch.cuda.current_stream()
-        if ob:
+
+        def object_field():
             # the object field is independent of the human one: side stream
             self._fork(main, self.side)
             with torch.cuda.stream(self.side):
@@ -467,6 +473,9 @@ class Renderer:
                           self.cfg.t_term, ob.rgb.data_ptr(), ob.depth.data_ptr(), ob.opacity.data_ptr(), so)
                 self._mark("object_composite")
                 self._obj_done.record(self.side)
+
+        if ob:
+            object_field()
         if hb:
             h = self.human
             if setup:
@@ -479,16 +488,21 @@ class Renderer:
                 _lib.call("cf_field_stage", _lib.byref(self.hdesc), _lib.byref(hb.mo), self.dirs.data_ptr(),
                           hb.xu.data_ptr(), hb.out.data_ptr(), scratch, stage, s)
                 self._mark(name)
-            _lib.call("cf_composite", _lib.byref(self.M), _lib.byref(hb.mo), hb.out.data_ptr(), self.cfg.t_term,
-                      hb.rgb.data_ptr(), hb.depth.data_ptr(), hb.opacity.data_ptr(), s)
+            if ob:
+                main.wait_event(self._obj_done)
+            # human composite fused with the layer choice against the object layer
+            _lib.call("cf_composite_final", _lib.byref(self.M), _lib.byref(hb.mo), hb.out.data_ptr(),
+                      self.cfg.t_term, hb.rgb.data_ptr(), hb.depth.data_ptr(), hb.opacity.data_ptr(),
+                      ob.rgb.data_ptr() if ob else None, ob.depth.data_ptr() if ob else None,
+                      ob.opacity.data_ptr() if ob else None, self.bg, self.image.data_ptr(), self.layer.data_ptr(), s)
             self._mark("human_composite")
-        if ob:
-            main.wait_event(self._obj_done)
-        _lib.call("cf_composite_layers", self.n_rays, hb.rgb.data_ptr() if hb else None,
-                  hb.depth.data_ptr() if hb else None, hb.opacity.data_ptr() if hb else None,
-                  ob.rgb.data_ptr() if ob else None, ob.depth.data_ptr() if ob else None,
-                  ob.opacity.data_ptr() if ob else None, self.bg, self.image.data_ptr(), self.layer.data_ptr(), s)
-        self._mark("layers")
+        else:
+            if ob:
+                main.wait_event(self._obj_done)
+            _lib.call("cf_composite_layers", self.n_rays, None, None, None, ob.rgb.data_ptr() if ob else None,
+                      ob.depth.data_ptr() if ob else None, ob.opacity.data_ptr() if ob else None, self.bg,
+                      self.image.data_ptr(), self.layer.data_ptr(), s)
+            self._mark("layers")
 
     def sample_counts(self):
         """(human, object) processed-sample counts of the last view (syncs)."""
