@@ -121,6 +121,10 @@ int cf_lbs_forward(const double* A, int J, const double* pts, const double* weig
  * Tinv_v its inverse, both (V,3,4) row-major; T_out may be NULL. */
 int cf_lbs_vertex_transforms(const double* A, int J, const double* vert_weights, int64_t n_verts, double* T_out,
                              double* Tinv_out, void* stream);
+/* per-frame skin setup in one kernel: cf_lbs_vertex_transforms (T, Tinv) plus
+ * the posed vertices of cf_lbs_forward with the same weights (J <= 64) */
+int cf_lbs_setup(const double* A, int J, const double* verts, const double* vert_weights, int64_t n_verts,
+                 double* T_out, double* Tinv_out, double* posed_out, void* stream);
 /* backward LBS (builder-defined): nearest posed skin vertex
  * v* (exact 1-NN, ties by index; vert_buckets built over verts_posed, or NULL
  * for an exhaustive scan) -> p_c = Tinv_{v*} [p, 1];

@@ -114,6 +114,7 @@ _SIGS = {
     "cf_knnfield_query": [_p, _p, _p, _p, _i32, _i32, _p, _f64, _f64, _p, _i64, _p, _p, _p, _p, _p],
     "cf_lbs_forward": [_p, _i32, _p, _p, _i64, _p, _p],
     "cf_lbs_vertex_transforms": [_p, _i32, _p, _i64, _p, _p, _p],
+    "cf_lbs_setup": [_p, _i32, _p, _p, _i64, _p, _p, _p, _p],
     "cf_lbs_backward": [_p, _p, _p, _i64, _f64, _p, _i64, _p, _p, _p, _p],
     "cf_hashgrid_init": [ctypes.POINTER(HashGridDesc), _i32, _i32, _i32, _i32, _i32],
     "cf_hashgrid_encode": [ctypes.POINTER(HashGridDesc), _p, _p, _i64, _p, _p],

@@ -65,6 +65,68 @@ __global__ void lbs_vertex_kernel(const double* __restrict__ A, int J, const dou
   pdl_trigger();
 }
 
+// Per-frame setup of every skin vertex in one pass: blended transform T_v, its
+// inverse, and the posed position (the lbs_forward arithmetic). The bone
+// transforms are staged in shared memory and the vertex's weight row is read
+// with independent vector loads up front (the separate kernels were latency
+// bound: 24 dependent weight loads per thread).
+constexpr int kMaxBones = 64;
+__global__ void __launch_bounds__(128) lbs_setup_kernel(const double* __restrict__ A, int J,
+                                                        const double* __restrict__ verts,
+                                                        const double* __restrict__ W, int64_t V,
+                                                        double* __restrict__ T, double* __restrict__ Tinv,
+                                                        double* __restrict__ posed) {
+  __shared__ double sA[kMaxBones * 16];
+  pdl_wait();
+  for (int i = threadIdx.x; i < J * 16; i += blockDim.x) sA[i] = A[i];
+  __syncthreads();
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < V; v += (int64_t)gridDim.x * blockDim.x) {
+    const double p[4] = {verts[3 * v], verts[3 * v + 1], verts[3 * v + 2], 1.0};
+    double m[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    double o[3] = {0.0, 0.0, 0.0};
+    const double* wr = W + v * J;
+    for (int j0 = 0; j0 < J; j0 += 8) {
+      double w8[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) w8[q] = j0 + q < J ? wr[j0 + q] : 0.0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const double w = w8[q];
+        if (w == 0.0) continue;
+        const double* M = sA + 16 * (j0 + q);
+#pragma unroll
+        for (int e = 0; e < 12; ++e) m[e] += w * M[e];
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+          o[a] += w * (M[4 * a] * p[0] + M[4 * a + 1] * p[1] + M[4 * a + 2] * p[2] + M[4 * a + 3] * p[3]);
+      }
+    }
+    posed[3 * v] = o[0];
+    posed[3 * v + 1] = o[1];
+    posed[3 * v + 2] = o[2];
+    const double a = m[0], b = m[1], c = m[2], d = m[4], e = m[5], f = m[6], g = m[8], h = m[9], k = m[10];
+    const double A00 = e * k - f * h, A01 = c * h - b * k, A02 = b * f - c * e;
+    const double A10 = f * g - d * k, A11 = a * k - c * g, A12 = c * d - a * f;
+    const double A20 = d * h - e * g, A21 = b * g - a * h, A22 = a * e - b * d;
+    const double det = a * A00 + b * A10 + c * A20;
+    const double id = 1.0 / det;
+    const double R[9] = {A00 * id, A01 * id, A02 * id, A10 * id, A11 * id, A12 * id, A20 * id, A21 * id, A22 * id};
+    const double t[3] = {m[3], m[7], m[11]};
+    double* oi = Tinv + 12 * v;
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      oi[4 * r] = R[3 * r];
+      oi[4 * r + 1] = R[3 * r + 1];
+      oi[4 * r + 2] = R[3 * r + 2];
+      oi[4 * r + 3] = -(R[3 * r] * t[0] + R[3 * r + 1] * t[1] + R[3 * r + 2] * t[2]);
+    }
+    if (T)
+#pragma unroll
+      for (int e2 = 0; e2 < 12; ++e2) T[12 * v + e2] = m[e2];
+  }
+  pdl_trigger();
+}
+
 template <bool kBuckets>
 __global__ void __launch_bounds__(128, 4) lbs_backward_kernel(const BucketParams* __restrict__ Pp,
                                                            const int* __restrict__ cell_start,
@@ -119,6 +181,16 @@ int cf_lbs_vertex_transforms(const double* A, int J, const double* vert_weights,
   cf::launch_pdl(lbs_vertex_kernel, cf::grid_for(n_verts, 128, 4), 128, 0, cf::as_stream(stream), A, J, vert_weights, n_verts,
                                                                                        T_out, Tinv_out);
   return cf::check_launch("cf_lbs_vertex_transforms");
+}
+
+int cf_lbs_setup(const double* A, int J, const double* verts, const double* vert_weights, int64_t n_verts,
+                 double* T_out, double* Tinv_out, double* posed_out, void* stream) {
+  if (J < 1 || J > kMaxBones || n_verts < 1 || !A || !verts || !vert_weights || !Tinv_out || !posed_out)
+    return cf::fail(CF_E_BAD_ARG, "cf_lbs_setup: bad args");
+  // 64 threads per CTA: a few thousand vertices still spread over ~all SMs
+  cf::launch_pdl(lbs_setup_kernel, cf::grid_for(n_verts, 64, 4), 64, 0, cf::as_stream(stream), A, J, verts,
+                 vert_weights, n_verts, T_out, Tinv_out, posed_out);
+  return cf::check_launch("cf_lbs_setup");
 }
 
 int cf_lbs_backward(const cf_buckets_t* vert_buckets, const double* verts_posed, const double* vert_Tinv,

@@ -55,10 +55,9 @@ class BackwardLBS:
         """Per-frame setup from bone transforms A (J,4,4): numpy, or a CUDA tensor used in place."""
         self.A = A.contiguous() if is_device(A) else dev(np.asarray(A, dtype=np.float64))
         s = _lib.stream_ptr()
-        _lib.call("cf_lbs_vertex_transforms", self.A.data_ptr(), self.J, self.W.data_ptr(), self.V, self.T.data_ptr(),
-                  self.Tinv.data_ptr(), s)
-        _lib.call("cf_lbs_forward", self.A.data_ptr(), self.J, self.verts.data_ptr(), self.W.data_ptr(), self.V,
-                  self.posed.data_ptr(), s)
+        # blended vertex transforms + inverses + posed vertices in one kernel
+        _lib.call("cf_lbs_setup", self.A.data_ptr(), self.J, self.verts.data_ptr(), self.W.data_ptr(), self.V,
+                  self.T.data_ptr(), self.Tinv.data_ptr(), self.posed.data_ptr(), s)
         self.buckets.build(self.posed)
 
     def warp(self, pts: torch.Tensor):
