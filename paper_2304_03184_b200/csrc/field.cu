@@ -29,7 +29,7 @@ constexpr int kSlotThreads = 128;
 // chunk are issued before any is consumed. Same arithmetic as hashgrid.cu.
 template <int F, int L, int CH>
 __device__ __forceinline__ void hash_features(const cf_hashgrid_desc& D, const float* __restrict__ table, float x,
-                                              float y, float z, float* feat) {
+                                              float y, float z, float* feat, int l_base = 0) {
   static_assert(L % CH == 0, "chunk must divide the level count");
   x = fminf(fmaxf(x, 0.0f), 1.0f);
   y = fminf(fmaxf(y, 0.0f), 1.0f);
@@ -41,7 +41,7 @@ __device__ __forceinline__ void hash_features(const cf_hashgrid_desc& D, const f
     float w[CH][8];
 #pragma unroll
     for (int c = 0; c < CH; ++c) {
-      const int l = l0 + c;
+      const int l = l_base + l0 + c;
       const int N = D.resolution[l];
       const float s = (float)N;
       const float pos[3] = {f_mul(x, s), f_mul(y, s), f_mul(z, s)};
@@ -92,27 +92,38 @@ __device__ __forceinline__ void hash_features(const cf_hashgrid_desc& D, const f
 }
 
 // 32 features of a valid sample (flag > 0) -> fp16 row; invalid -> zeros
-template <int F, int L, int CH>
+// SPLIT threads per sample, each doing L / SPLIT consecutive levels and writing
+// its 32 / SPLIT features of the row: SPLIT > 1 multiplies the warps in flight
+// for small sample counts (the object field), where one thread per sample left
+// the SMs mostly idle.
+template <int F, int L, int CH, int SPLIT>
 __global__ void __launch_bounds__(128) hash_f16_kernel(cf_hashgrid_desc D, const float* __restrict__ table,
                                                        const float4* __restrict__ x, const int* __restrict__ count,
                                                        int64_t capacity, uint4* __restrict__ out) {
+  constexpr int LS = L / SPLIT, NF = LS * F;  // levels and features per thread
+  static_assert(L % SPLIT == 0 && NF % 8 == 0, "whole 16-byte chunks per thread");
   pdl_wait();
-  const int64_t n = min((int64_t)*count, capacity);
-  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t n = min((int64_t)*count, capacity) * SPLIT;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = SPLIT == 1 ? t : t / SPLIT;
+    const int part = SPLIT == 1 ? 0 : (int)(t % SPLIT);
     const float4 p = x[s];
-    float feat[32];
+    float feat[NF];
     if (p.w > 0.0f) {
-      hash_features<F, L, CH>(D, table, p.x, p.y, p.z, feat);
+      if constexpr (SPLIT == 1)
+        hash_features<F, LS, CH>(D, table, p.x, p.y, p.z, feat);
+      else
+        hash_features<F, LS, (CH < LS ? CH : LS)>(D, table, p.x, p.y, p.z, feat, part * LS);
     } else {
 #pragma unroll
-      for (int i = 0; i < 32; ++i) feat[i] = 0.0f;
+      for (int i = 0; i < NF; ++i) feat[i] = 0.0f;
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < NF / 8; ++q) {
       __half2 h[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) h[i] = __floats2half2_rn(feat[8 * q + 2 * i], feat[8 * q + 2 * i + 1]);
-      out[s * 4 + q] = *reinterpret_cast<uint4*>(h);
+      out[s * 4 + part * (NF / 8) + q] = *reinterpret_cast<uint4*>(h);
     }
   }
   pdl_trigger();
@@ -994,7 +1005,8 @@ int cf_field_stage(const cf_field_desc* FD, const cf_march_out* S, const double*
   if (FD->has_deform) {
     uint4* dfeat = cfeat + cap * 4;
     float4* xc = reinterpret_cast<float4*>(dfeat + cap * 4);
-    if (run(0)) cf::launch_pdl(hash_f16_kernel<4, 8, 2>, hgrid, 128, 0, st, FD->dgrid, FD->dtable, xu, S->counters, cap, dfeat);
+    if (run(0))
+      cf::launch_pdl(hash_f16_kernel<4, 8, 2, 1>, hgrid, 128, 0, st, FD->dgrid, FD->dtable, xu, S->counters, cap, dfeat);
     if (run(1)) {
       const int smem = kDeformW + kDeformA;
       CF_CHECK_CUDA(cudaFuncSetAttribute(deform_mlp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -1003,7 +1015,14 @@ int cf_field_stage(const cf_field_desc* FD, const cf_march_out* S, const double*
     }
     xcan = xc;
   }
-  if (run(2)) cf::launch_pdl(hash_f16_kernel<2, 16, 4>, hgrid, 128, 0, st, FD->cgrid, FD->ctable, xcan, S->counters, cap, cfeat);
+  if (run(2)) {
+    if (FD->has_deform)
+      cf::launch_pdl(hash_f16_kernel<2, 16, 4, 1>, hgrid, 128, 0, st, FD->cgrid, FD->ctable, xcan, S->counters, cap,
+                     cfeat);
+    else  // object field: few samples
+      cf::launch_pdl(hash_f16_kernel<2, 16, 4, 4>, cf::grid_for(cap * 4, 128, 16), 128, 0, st, FD->cgrid, FD->ctable,
+                     xcan, S->counters, cap, cfeat);
+  }
   if (run(3)) {
     const int csmem = ((kColorW + 1023) / 1024) * 1024 + kColorSlots * kColorA;
     CF_CHECK_CUDA(cudaFuncSetAttribute(color_mlp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, csmem));
