@@ -296,9 +296,12 @@ def run_ours(args, rank, world, pg):
     dom = max((k for k in stage_ms if k in cost), key=stage_ms.get)
     bound, units, per_unit, per_text = cost[dom]
     work = units * per_unit
+    # dram__bytes_read.sum + dram__bytes_write.sum of one launch of that kernel from
+    # the committed `ncu --set full` capture (profiles/ncu_traffic.json), or null
     traffic = None
     try:
-        traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(dom)
+        t = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(dom)
+        traffic = float(t["dram_bytes_per_launch"]) if isinstance(t, dict) else t
     except Exception:
         pass
     if bound == "tensor":
