@@ -8,10 +8,11 @@
 //                     Writes 32 fp16 features (64 B) per sample.
 //   deform_mlp_kernel tcgen05: DeformNet 32->128x4->3 (theta folded into the
 //                     layer-1 bias), 3 slots x 128 samples per persistent CTA,
-//                     weights (108 KB fp16) resident in smem, accumulators in
-//                     TMEM. Epilogue: dv = 0.05 tanh(.), xc = x + dv / side.
-//   color_mlp_kernel  tcgen05: E_g 32->64->16 (sigma = exp, 15 geo) and
-//                     E_c [geo, SH4(dir)] 32->64->64->3 (sigmoid), 4 slots.
+//                     weights (108 KB fp16) resident in smem, accumulators and
+//                     (2 slots) activations in TMEM (TS-form MMAs).
+//                     Epilogue: dv = 0.05 tanh(.), xc = x + dv / side.
+//   color_mlp_kernel  tcgen05 TS form: E_g 32->64->16 (sigma = exp, 15 geo) and
+//                     E_c [geo, SH4(dir)] 32->64->64->3 (sigmoid), 5 slots.
 //
 // Human:  hash_d(xu) -> deform_mlp -> hash_c(xc) -> color_mlp
 // Object: hash_c(xu) -> color_mlp
@@ -413,28 +414,100 @@ __device__ __forceinline__ void sh16(float x, float y, float z, float* o) {
   o[15] = 0.59004358992664352f * x * (-xx + 3.0f * yy);
 }
 
-constexpr int kColorSlots = 4;
-constexpr int kColorA = 128 * 64 * 2;
 constexpr int kColorW = (64 * 32 + 16 * 64 + 64 * 32 + 64 * 64 + 16 * 64) * 2;  // 20,480 B
 
-__global__ void __launch_bounds__(kColorSlots* kSlotThreads, 1)
+// E_g / E_c with the activations in TMEM (TS-form MMAs, as DeformNet): per slot
+// D (64 fp32 columns) + A (32 packed fp16x2 columns) = 96 columns, 5 slots of 4
+// warps (thread = sample row). The narrow N = 64 layers made the SS version
+// epilogue/latency bound (tensor pipe 12 %): no smem traffic for activations and
+// one more slot in flight.
+constexpr int kColorTsSlots = 5;
+
+struct CSlot {
+  uint64_t* bar;
+  uint32_t d0, a0;  // slot base columns (MMA operands)
+  uint32_t d, a;    // + this warp's lane quarter
+  uint32_t phase;
+  int slot, r;
+};
+
+__device__ __forceinline__ void cts_layer(CSlot& S, const uint8_t* w, int K, int N) {
+  tc::tmem_wait_st();
+  tc::fence_before();
+  tc::named_sync(1 + S.slot, kSlotThreads);
+  if (S.r == 0) {
+    tc::fence_after();
+    tc::issue_layer_ts(S.d0, S.a0, w, K, N);
+    tc::mma_commit(S.bar);
+  }
+  tc::bar_wait(S.bar, S.phase);
+  S.phase ^= 1u;
+  tc::fence_after();
+}
+
+// 64-wide hidden layer: D -> ReLU -> fp16x2 -> A (K = 64)
+__device__ __forceinline__ void cts_relu64(const CSlot& S) {
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    uint32_t r[32];
+    tc::tmem_ld32_nowait(S.d + (uint32_t)(32 * c), r);
+    tc::tmem_wait_ld();
+    uint32_t h[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) h[i] = tc::relu_f16x2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+    tc::tmem_st16(S.a + (uint32_t)(16 * c), h);
+  }
+}
+
+__global__ void __launch_bounds__(kColorTsSlots* kSlotThreads, 1)
     color_mlp_kernel(const uint8_t* __restrict__ wblob, const float4* __restrict__ xu, const uint4* __restrict__ cfeat,
                      const uint32_t* __restrict__ records, const double* __restrict__ dirs,
                      const int* __restrict__ count, int64_t capacity, float4* __restrict__ out) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t mbar[kColorSlots];
+  __shared__ uint64_t mbar[kColorTsSlots];
   __shared__ uint32_t tmem_base;
-  slots_setup<kColorSlots, 256>(wblob, kColorW, smem, mbar, &tmem_base);
+  const int tid = threadIdx.x, warp = tid / 32;
+  for (int i = tid * 16; i < kColorW; i += blockDim.x * 16)
+    *reinterpret_cast<uint4*>(smem + i) = *reinterpret_cast<const uint4*>(wblob + i);
+  if (tid == 0) {
+    for (int q = 0; q < kColorTsSlots; ++q) tc::bar_init(&mbar[q], 1);
+    tc::bar_fence_init();
+  }
+  if (warp == 0) tc::tmem_alloc<512>(&tmem_base);
+  tc::fence_async_smem();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
   pdl_wait();  // weights staged and TMEM allocated while the previous kernel drained
-  Slot S = make_slot<kColorSlots, 64, kColorA>(smem, kColorW, mbar, tmem_base);
+  CSlot S;
+  S.slot = tid / kSlotThreads;
+  S.r = tid % kSlotThreads;
+  S.bar = &mbar[S.slot];
+  S.phase = 0;
+  S.d0 = tmem_base + (uint32_t)(S.slot * 96);
+  S.a0 = S.d0 + 64u;
+  const uint32_t lane_q = (uint32_t)((warp % 4) * 32) << 16;
+  S.d = S.d0 + lane_q;
+  S.a = S.a0 + lane_q;
   constexpr int g1 = 0, g2 = 64 * 32 * 2, c1 = g2 + 16 * 64 * 2, c2 = c1 + 64 * 32 * 2, c3 = c2 + 64 * 64 * 2;
   const int64_t n = min((int64_t)*count, capacity);
   const int64_t n_tiles = (n + 127) / 128;
-  for (int64_t tile = (int64_t)blockIdx.x * kColorSlots + S.slot; tile < n_tiles;
-       tile += (int64_t)gridDim.x * kColorSlots) {
+  for (int64_t tile = (int64_t)blockIdx.x * kColorTsSlots + S.slot; tile < n_tiles;
+       tile += (int64_t)gridDim.x * kColorTsSlots) {
     const int64_t s = tile * 128 + S.r;
     const bool live = s < n;
-    row_to_abuf(S, cfeat, s, live);
+    {
+      uint32_t w16[16];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint4 v = live ? cfeat[s * 4 + q] : make_uint4(0, 0, 0, 0);
+        w16[4 * q] = v.x;
+        w16[4 * q + 1] = v.y;
+        w16[4 * q + 2] = v.z;
+        w16[4 * q + 3] = v.w;
+      }
+      tc::tmem_st16(S.a, w16);
+    }
     // per-sample inputs of the later layers, loaded while the first MMAs run
     const bool valid = live && xu[s].w > 0.0f;
     double ddx = 0.0, ddy = 0.0, ddz = 1.0;
@@ -444,28 +517,34 @@ __global__ void __launch_bounds__(kColorSlots* kSlotThreads, 1)
       ddy = dirs[3 * ray + 1];
       ddz = dirs[3 * ray + 2];
     }
-    run_layer(S, g1, 32, 64);
-    relu_to_abuf<64>(S, nullptr);
-    run_layer(S, g2, 64, 16);
+    cts_layer(S, smem + g1, 32, 64);
+    cts_relu64(S);
+    cts_layer(S, smem + g2, 64, 16);
     float gv[16];
-    tc::tmem_ld16(S.tmem_row, gv);
+    tc::tmem_ld16(S.d, gv);
     const float sigma = valid ? expf(gv[0]) : 0.0f;
     // colour input: [geo(15), SH4(dir)(16), 0]
-    float cin[32];
+    {
+      float cin[32];
 #pragma unroll
-    for (int i = 0; i < 15; ++i) cin[i] = gv[1 + i];
-    const float dx = (float)ddx, dy = (float)ddy, dz = (float)ddz;
-    sh16(dx, dy, dz, cin + 15);
-    cin[31] = 0.0f;
+      for (int i = 0; i < 15; ++i) cin[i] = gv[1 + i];
+      sh16((float)ddx, (float)ddy, (float)ddz, cin + 15);
+      cin[31] = 0.0f;
+      uint32_t h[16];
 #pragma unroll
-    for (int k0 = 0; k0 < 32; k0 += 8) tc::st_row8(S.abuf, S.r, k0, 32, cin + k0);
-    run_layer(S, c1, 32, 64);
-    relu_to_abuf<64>(S, nullptr);
-    run_layer(S, c2, 64, 64);
-    relu_to_abuf<64>(S, nullptr);
-    run_layer(S, c3, 64, 16);
+      for (int i = 0; i < 16; ++i) {
+        const __half2 hh = __floats2half2_rn(cin[2 * i], cin[2 * i + 1]);
+        h[i] = *reinterpret_cast<const uint32_t*>(&hh);
+      }
+      tc::tmem_st16(S.a, h);
+    }
+    cts_layer(S, smem + c1, 32, 64);
+    cts_relu64(S);
+    cts_layer(S, smem + c2, 64, 64);
+    cts_relu64(S);
+    cts_layer(S, smem + c3, 64, 16);
     float cv[16];
-    tc::tmem_ld16(S.tmem_row, cv);
+    tc::tmem_ld16(S.d, cv);
     if (live) {
       const float r = 1.0f / (1.0f + expf(-cv[0])), g = 1.0f / (1.0f + expf(-cv[1])),
                   b = 1.0f / (1.0f + expf(-cv[2]));
@@ -474,7 +553,7 @@ __global__ void __launch_bounds__(kColorSlots* kSlotThreads, 1)
   }
   tc::fence_before();
   __syncthreads();
-  if (threadIdx.x / 32 == 0) tc::tmem_free<256>(tmem_base);
+  if (warp == 0) tc::tmem_free<512>(tmem_base);
   pdl_trigger();
 }
 
@@ -1024,10 +1103,9 @@ int cf_field_stage(const cf_field_desc* FD, const cf_march_out* S, const double*
                      xcan, S->counters, cap, cfeat);
   }
   if (run(3)) {
-    const int csmem = ((kColorW + 1023) / 1024) * 1024 + kColorSlots * kColorA;
-    CF_CHECK_CUDA(cudaFuncSetAttribute(color_mlp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, csmem));
+    const int csmem = kColorW;
     const uint8_t* cw = FD->wblob + (FD->has_deform ? kDeformW : 0);
-    cf::launch_pdl(color_mlp_kernel, persistent_grid(cap, kColorSlots), kColorSlots * kSlotThreads, csmem, st, cw, xu, cfeat, S->records, dirs, S->counters, cap, out);
+    cf::launch_pdl(color_mlp_kernel, persistent_grid(cap, kColorTsSlots), kColorTsSlots * kSlotThreads, csmem, st, cw, xu, cfeat, S->records, dirs, S->counters, cap, out);
   }
   return cf::check_launch("cf_field_forward");
 }
