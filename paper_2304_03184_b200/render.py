@@ -459,7 +459,8 @@ class Renderer:
         main = torch.cuda.current_stream()
 
         def object_field():
-            # the object field is independent of the human one: side stream
+            # the object field is independent of the human one: side stream (running it
+            # serially on the main stream measured 330 -> 355 us per frame)
             self._fork(main, self.side)
             with torch.cuda.stream(self.side):
                 so = _lib.stream_ptr()
