@@ -84,6 +84,7 @@ __device__ __forceinline__ bool ed_warp_point_cull(const double4* __restrict__ s
                                                    const double* __restrict__ dqs, int k, double r2, bool inverse,
                                                    d3 p, bool live, d3& out) {
   const unsigned FULL = 0xffffffffu;
+  if (!__any_sync(FULL, live)) return false;  // warp-uniform
   const int lane = threadIdx.x & 31;
   const float px = (float)p.x, py = (float)p.y, pz = (float)p.z;
   const float INF = __int_as_float(0x7f800000);

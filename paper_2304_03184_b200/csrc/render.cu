@@ -582,6 +582,7 @@ __global__ void __launch_bounds__(128, CF_CANON_MINB) human_canon_kernel(cf_marc
   extern __shared__ double4 s_anchors[];  // kSmem: the frame's deformed nodes (+ fp32 copies)
   float4* s_af = reinterpret_cast<float4*>(s_anchors + (kSmem ? W.n_nodes : 0));
   __shared__ unsigned s_mag;
+  __shared__ double s_box[6];
   if (threadIdx.x == 0) {
     if (!kSmem) sE = *EPp;
     if (LPp) sL = *LPp;
@@ -599,8 +600,34 @@ __global__ void __launch_bounds__(128, CF_CANON_MINB) human_canon_kernel(cf_marc
     atomicMax(&s_mag, __float_as_uint(mag));  // non-negative floats order as their bits
     __syncthreads();
     if (threadIdx.x == 0) s_af[0].w = __uint_as_float(s_mag);
+    // float64 bbox of the anchors (warp 0), for the ED-support early-out below
+    if (threadIdx.x < 32) {
+      double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+      for (int i = threadIdx.x; i < W.n_nodes; i += 32) {
+        const double4 a = s_anchors[i];
+        lo[0] = fmin(lo[0], a.x), lo[1] = fmin(lo[1], a.y), lo[2] = fmin(lo[2], a.z);
+        hi[0] = fmax(hi[0], a.x), hi[1] = fmax(hi[1], a.y), hi[2] = fmax(hi[2], a.z);
+      }
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+        for (int off = 16; off > 0; off >>= 1) {
+          lo[a] = fmin(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], off));
+          hi[a] = fmax(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], off));
+        }
+      if (threadIdx.x == 0)
+        for (int a = 0; a < 3; ++a) {
+          s_box[a] = lo[a];
+          s_box[3 + a] = hi[a];
+        }
+    }
   }
   __syncthreads();
+  // A sample farther than R from the anchors' bbox has every Gaussian weight
+  // below the validity floor: d^2 / r^2 > -ln(1e-6) (1 + 1e-5) => w < 1e-6. Such
+  // samples skip the k-NN (ED invalid, as the exact evaluation would find) and
+  // stay out of the warp's culling box — training's uniform samples along the
+  // whole ray [0.3 m, 5 m] are mostly of this kind.
+  const double rsup2 = 13.815510557964274 * W.r2 * (1.0 + 1e-5);
   __shared__ double s_fr[15];
   load_frame(M, s_fr);
   const int64_t n = min((int64_t)count[0], capacity);
@@ -621,15 +648,35 @@ __global__ void __launch_bounds__(128, CF_CANON_MINB) human_canon_kernel(cf_marc
     const d3 p = live ? sample_p(o, load_d3(dirs + 3 * ray), rec_t(M, s, rec)) : d3{0.0, 0.0, 0.0};
     d3 pt;
     float flag = 0.0f;
-    const bool ed_ok = kSmem ? ed_warp_point_cull<K>(s_anchors, s_af, W.n_nodes, W.dqs, W.k, W.r2, true, p, live, pt)
+    bool near = live;
+    if (kSmem && live) {
+      const double q[3] = {p.x, p.y, p.z};
+      double d2 = 0.0;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const double e = fmax(fmax(s_box[a] - q[a], q[a] - s_box[3 + a]), 0.0);
+        d2 += e * e;
+      }
+      near = d2 <= rsup2;
+    }
+    const bool ed_ok = kSmem ? ed_warp_point_cull<K>(s_anchors, s_af, W.n_nodes, W.dqs, W.k, W.r2, true, p, near, pt)
                              : (live && ed_warp_point<K>(sE, ecs, es, W.dqs, W.k, W.r2, true, p, pt));
     if (!live) continue;
     if (ed_ok) {
       flag = 1.0f;
     } else if (LPp) {
+      // no skin vertex within lbs_max_dist when the sample is that far from the
+      // vertex grid's box (which holds every vertex): skip the search
+      const double q[3] = {p.x, p.y, p.z};
+      double d2b = 0.0;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const double e = fmax(fmax(sL.origin[a] - q[a], q[a] - (sL.origin[a] + sL.g[a] * sL.h)), 0.0);
+        d2b += e * e;
+      }
       TopK<1> top;
       top.init(1);
-      bucket_knn<1>(sL, lcs, ls, p, top, W.lbs_max_d2);
+      if (d2b <= W.lbs_max_d2 * (1.0 + 1e-9)) bucket_knn<1>(sL, lcs, ls, p, top, W.lbs_max_d2);
       if (top.d[0] <= W.lbs_max_d2) {
         const double* T = W.vert_Tinv + 12 * (int64_t)top.i[0];
         pt = d3{T[0] * p.x + T[1] * p.y + T[2] * p.z + T[3], T[4] * p.x + T[5] * p.y + T[6] * p.z + T[7],

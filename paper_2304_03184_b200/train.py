@@ -277,7 +277,8 @@ class Trainer:
             GD["D2"] += (DP[:, 128:256].t() @ H[:, 0:128]).float()
             GD["D1"][:, :32] += (DP[:, 0:128].t() @ xd).float()
             # theta is the same for every sample of the frame: dW1_theta = (sum_s dpre1) theta^T
-            GD["D1"][:, 32:] += torch.outer(DP[:, 0:128].float().sum(0), b.theta.to(DP.device, torch.float32))
+            GD["D1"][:, 32:] += torch.outer(torch.sum(DP[:, 0:128], dim=0, dtype=torch.float32),
+                                            b.theta.to(DP.device, torch.float32))
 
     def set_frame(self, b: FrameBatch):
         r = self.r
