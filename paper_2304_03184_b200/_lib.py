@@ -148,6 +148,7 @@ _SIGS = {
     "cf_adam": [_p, _p, _p, _p, _i64, ctypes.c_float, ctypes.c_float, ctypes.c_float, ctypes.c_float, _i32,
                 ctypes.c_float, _p],
     "cf_pack_weight": [_p, _i32, _i32, _p, _p],
+    "cf_colsum128_f16": [_p, _i64, _i32, _p, _p],
 }
 
 _lock = threading.Lock()

@@ -31,9 +31,30 @@ __global__ void pack_kernel(const float* __restrict__ w, int n, int k, int np, i
   }
 }
 
+// out[c] += sum_{r < n} x[r * ld + c], c < 128: fp16 rows, fp32 accumulation
+// (DeformNet's theta gradient needs the column sums of dL/dpre1 over a frame)
+__global__ void colsum128_kernel(const __half* __restrict__ x, int64_t n, int ld, float* __restrict__ out) {
+  __shared__ float part[256];
+  const int c = threadIdx.x & 127, rg = threadIdx.x >> 7;
+  float acc = 0.0f;
+  for (int64_t r = (int64_t)blockIdx.x * 2 + rg; r < n; r += (int64_t)gridDim.x * 2)
+    acc += __half2float(x[r * ld + c]);
+  part[threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.x < 128) atomicAdd(out + c, part[threadIdx.x] + part[threadIdx.x + 128]);
+}
+
 }  // namespace
 
 extern "C" {
+
+int cf_colsum128_f16(const void* x, int64_t n, int ld, float* out, void* stream) {
+  if (!x || !out || n < 0 || ld < 128) return cf::fail(CF_E_BAD_ARG, "cf_colsum128_f16: bad args");
+  if (n == 0) return CF_OK;
+  colsum128_kernel<<<cf::grid_for((n + 1) / 2, 1, 4), 256, 0, cf::as_stream(stream)>>>(
+      reinterpret_cast<const __half*>(x), n, ld, out);
+  return cf::check_launch("cf_colsum128_f16");
+}
 
 int cf_adam(float* p, const float* g, float* m, float* v, int64_t n, float lr, float beta1, float beta2, float eps,
             int step, float grad_scale, void* stream) {

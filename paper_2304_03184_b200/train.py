@@ -146,6 +146,7 @@ class _DeformBuffers:
         self.dpre = torch.empty((cap, 512), dtype=torch.float16, device=device)
         self.d_dfeat = torch.empty((cap, 32), dtype=torch.float32, device=device)
         self.dxc = torch.empty((cap, 4), dtype=torch.float32, device=device)
+        self.colsum = torch.empty(128, dtype=torch.float32, device=device)
         self.io = _lib.DeformBwdIO(self.save_h.data_ptr(), self.save_o.data_ptr(), self.d_o.data_ptr(),
                                    self.dpre.data_ptr(), self.d_dfeat.data_ptr())
 
@@ -277,8 +278,10 @@ class Trainer:
             GD["D2"] += (DP[:, 128:256].t() @ H[:, 0:128]).float()
             GD["D1"][:, :32] += (DP[:, 0:128].t() @ xd).float()
             # theta is the same for every sample of the frame: dW1_theta = (sum_s dpre1) theta^T
-            GD["D1"][:, 32:] += torch.outer(torch.sum(DP[:, 0:128], dim=0, dtype=torch.float32),
-                                            b.theta.to(DP.device, torch.float32))
+            csum = db.colsum
+            csum.zero_()
+            _lib.call("cf_colsum128_f16", DP.data_ptr(), n, 512, csum.data_ptr(), s)
+            GD["D1"][:, 32:] += torch.outer(csum, b.theta.to(DP.device, torch.float32))
 
     def set_frame(self, b: FrameBatch):
         r = self.r
