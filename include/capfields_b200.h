@@ -183,6 +183,9 @@ typedef struct cf_camera {
   const double* params; /* optional device double[13] = R[9], fx, fy, cx, cy read by the kernel
                            instead of the fields above (a captured CUDA graph replays with new
                            cameras by rewriting this block); NULL = use the fields */
+  int row0, row_stride; /* row shard: local row j is image row row0 + j * row_stride (height =
+                           local rows; row_stride <= 0 means 1). Multi-GPU renders deal the rows
+                           of one frame round-robin; the directions equal the full frame's. */
 } cf_camera;
 
 /* cubic occupancy bit grid: res^3 cells of edge `cell` from `min`, x-major

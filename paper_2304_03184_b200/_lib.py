@@ -52,7 +52,7 @@ class HashGridDesc(ctypes.Structure):
 class Camera(ctypes.Structure):
     _fields_ = [("R", ctypes.c_double * 9), ("fx", ctypes.c_double), ("fy", ctypes.c_double),
                 ("cx", ctypes.c_double), ("cy", ctypes.c_double), ("width", ctypes.c_int), ("height", ctypes.c_int),
-                ("params", ctypes.c_void_p)]
+                ("params", ctypes.c_void_p), ("row0", ctypes.c_int), ("row_stride", ctypes.c_int)]
 
 
 class OccGrid(ctypes.Structure):

@@ -93,10 +93,11 @@ __device__ __forceinline__ void load_camera(const cf_camera& cam, double* s_cam)
 }
 
 // unit direction of pixel i (camera.py:94-108: R (u-cx)/fx, (v-cy)/fy, 1), normalised
+// local pixel i of a row shard: image row row0 + (i / width) * row_stride
 __device__ __forceinline__ d3 pixel_dir(const double* s_cam, const ExactDiv& by_fx, const ExactDiv& by_fy, int width,
-                                        int i) {
+                                        int i, int row0 = 0, int row_stride = 1) {
   const int v_i = i / width;
-  const double u = (double)(i - v_i * width), v = (double)v_i;
+  const double u = (double)(i - v_i * width), v = (double)(row0 + v_i * row_stride);
   const double dc[3] = {by_fx(x_sub(u, s_cam[11])), by_fy(x_sub(v, s_cam[12])), 1.0};
   double d[3];
 #pragma unroll
@@ -113,7 +114,8 @@ __global__ void rays_kernel(cf_camera cam, double* __restrict__ dirs) {
   const int n = cam.width * cam.height;
   const ExactDiv by_fx(s_cam[9]), by_fy(s_cam[10]);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    store_d3(dirs + 3 * (int64_t)i, pixel_dir(s_cam, by_fx, by_fy, cam.width, i));
+    store_d3(dirs + 3 * (int64_t)i,
+             pixel_dir(s_cam, by_fx, by_fy, cam.width, i, cam.row0, cam.row_stride > 0 ? cam.row_stride : 1));
   pdl_trigger();
 }
 
@@ -502,7 +504,7 @@ __global__ void __launch_bounds__(128) march_kernel(cf_march_desc M, cf_camera c
     d3 d{0.0, 0.0, 1.0};
     if (live) {
       if (kRays) {
-        d = pixel_dir(s_cam, by_fx, by_fy, cam.width, (int)ray);
+        d = pixel_dir(s_cam, by_fx, by_fy, cam.width, (int)ray, cam.row0, cam.row_stride > 0 ? cam.row_stride : 1);
         store_d3(dirs + 3 * ray, d);
       } else {
         d = load_d3(dirs + 3 * ray);

@@ -210,15 +210,54 @@ class _FieldBuffers:
                                 self.counters.data_ptr(), int(capacity))
 
 
+def row_shard_rows(height: int, rank: int, world: int) -> range:
+    """Image rows of rank `rank` when the rows of a frame are dealt round-robin."""
+    return range(rank, height, world)
+
+
+def assemble_row_shards(parts, width: int, height: int):
+    """Interleave the ranks' row-shard images (rank r: rows r, r + world, ...) into
+    the (height * width, C) frame."""
+    world = len(parts)
+    c = parts[0].shape[-1]
+    full = parts[0].new_empty((height, width, c))
+    for r, part in enumerate(parts):
+        full[r::world] = part.reshape(-1, width, c)
+    return full.reshape(height * width, c)
+
+
+def gather_row_shards(part, width: int, height: int, group=None):
+    """All-gather the ranks' row-shard images (NCCL on GPUs, gloo on CPU) and
+    interleave them into the full (height * width, C) frame on every rank."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    c = part.shape[-1]
+    rows_max = -(-height // world)
+    buf = part.new_zeros((rows_max * width, c))
+    buf[: part.shape[0]] = part
+    got = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(got, buf, group=group)
+    parts = [g[: len(row_shard_rows(height, r, world)) * width] for r, g in enumerate(got)]
+    return assemble_row_shards(parts, width, height)
+
+
 class Renderer:
     """render_view for one human + one rigid object."""
 
     def __init__(self, human: HumanField | None, obj: ObjectField | None, width: int, height: int,
-                 cfg: RenderConfig | None = None, capacity_per_ray: int | None = None):
+                 cfg: RenderConfig | None = None, capacity_per_ray: int | None = None,
+                 row_shard: tuple[int, int] | None = None):
+        """row_shard = (rank, world): render only image rows rank, rank + world, ...
+        (multi-GPU frames); `image` then holds those rows in order and
+        assemble_row_shards() interleaves the ranks' parts back into the frame."""
         self.cfg = cfg = cfg or RenderConfig()
         self.human, self.obj = human, obj
         self.W, self.H = int(width), int(height)
-        self.n_rays = self.W * self.H
+        self.row0, self.row_stride = (0, 1) if row_shard is None else (int(row_shard[0]), int(row_shard[1]))
+        if not (0 <= self.row0 < self.row_stride):
+            raise ValueError("row_shard must be (rank, world) with 0 <= rank < world")
+        self.rows = len(range(self.row0, self.H, self.row_stride))
+        self.n_rays = self.W * self.rows
         d = _lib.require_cuda()
         cap = self.n_rays * int(capacity_per_ray or cfg.n_samples)
         self.dirs = torch.empty((self.n_rays, 3), dtype=torch.float64, device=d)
@@ -259,7 +298,8 @@ class Renderer:
         self._slot = 0
         self.M.frame = self.frame_dev.data_ptr()
         self.cam = _lib.Camera()
-        self.cam.width, self.cam.height = self.W, self.H
+        self.cam.width, self.cam.height = self.W, self.rows
+        self.cam.row0, self.cam.row_stride = self.row0, self.row_stride
         self.cam.params = self.frame_dev.data_ptr() + 15 * 8
         self._setup_pending = False   # per-frame human setup still to run (load_prior since the last view)
         self._graphs = {}             # (with_setup,) -> torch.cuda.CUDAGraph

@@ -1,6 +1,7 @@
-"""Multi-rank host logic of the training step on CPU (gloo, world size 2): ray
-sharding covers the global batch exactly once, and the gradient-bucket
-all-reduce averages every bucket across ranks."""
+"""Multi-rank host logic on CPU (gloo, world size 2): training-ray sharding
+covers the global batch exactly once, the gradient-bucket all-reduce averages
+every bucket across ranks, and the row-sharded multi-GPU render reassembles the
+frame from the ranks' round-robin rows."""
 import os
 import socket
 
@@ -9,6 +10,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
+from paper_2304_03184_b200.render import assemble_row_shards, gather_row_shards, row_shard_rows
 from paper_2304_03184_b200.train import allreduce_grads, shard_rays
 
 
@@ -30,7 +32,13 @@ def _worker(rank, world, port, q):
         g_w = torch.arange(12, dtype=torch.float32).view(3, 4) * (rank + 1)
         allreduce_grads([g_table, g_w])
         sl = shard_rays(10001, rank, world)
-        q.put((rank, float(g_table[0, 0]), g_w.tolist(), sl.start, sl.stop))
+        # row-sharded frame (H = 7 rows of W = 3 pixels): pixel value = its image row
+        W, H = 3, 7
+        rows = row_shard_rows(H, rank, world)
+        part = torch.tensor([[float(v)] * 3 for v in rows for _ in range(W)])
+        frame = gather_row_shards(part, W, H)
+        ok = torch.equal(frame, torch.arange(H, dtype=torch.float32).repeat_interleave(W)[:, None].repeat(1, 3))
+        q.put((rank, float(g_table[0, 0]), g_w.tolist(), sl.start, sl.stop, ok))
     finally:
         dist.destroy_process_group()
 
@@ -47,10 +55,11 @@ def test_allreduce_and_sharding_world2():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    for rank, g0, gw, a, b in res:
+    for rank, g0, gw, a, b, ok in res:
         assert g0 == pytest.approx(1.5)  # mean of 1 and 2
         assert gw == (torch.arange(12, dtype=torch.float32).view(3, 4) * 1.5).tolist()
-    spans = [(a, b) for _, _, _, a, b in res]
+        assert ok, f"rank {rank}: row-sharded frame not reassembled"
+    spans = [(a, b) for _, _, _, a, b, _ in res]
     assert spans[0][0] == 0 and spans[-1][1] == 10001 and spans[0][1] == spans[1][0]
 
 
@@ -62,3 +71,14 @@ def test_shard_rays_balanced():
             assert all(a.stop == b.start for a, b in zip(sl, sl[1:]))
             sizes = [s.stop - s.start for s in sl]
             assert max(sizes) - min(sizes) <= 1
+
+
+def test_row_shards_cover_and_assemble():
+    for H in (1, 7, 1080):
+        for w in (1, 2, 3, 8):
+            rows = [list(row_shard_rows(H, r, w)) for r in range(w)]
+            assert sorted(sum(rows, [])) == list(range(H))
+    W, H, w = 4, 9, 4
+    full = torch.arange(H * W * 3, dtype=torch.float32).view(H * W, 3)
+    parts = [full.view(H, W, 3)[r::w].reshape(-1, 3) for r in range(w)]
+    assert torch.equal(assemble_row_shards(parts, W, H), full)

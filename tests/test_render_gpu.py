@@ -211,3 +211,22 @@ def test_march_full_frame_bitexact():
         exp = np.concatenate(want[name])
         assert n == len(exp) and n > 10000
         assert np.array_equal(np.sort(ray * 256 + i), np.sort(exp))
+
+
+def test_row_sharded_render_equals_full_frame(setup):
+    """Multi-GPU frames deal image rows round-robin; each shard's rays
+    are generated from the full frame's pixel rows, so the reassembled image is
+    bit-identical to the single-GPU render (two shards emulated on one GPU)."""
+    from paper_2304_03184_b200.render import assemble_row_shards
+    sc, cfg, hf, of, r, fid, img = setup
+    R, t = sc.object_pose(fid)
+    cam = sc.camera
+    full = r.render(cam.R, cam.t, cam.fx, cam.fy, cam.cx, cam.cy).clone()
+    parts = []
+    for rank in range(2):
+        rs = Renderer(hf, of, 64, 64, cfg, row_shard=(rank, 2))
+        rs.set_frame(sc.node_dqs(fid), sc.theta(fid), sc.bone_transforms(fid), R, t)
+        parts.append(rs.render(cam.R, cam.t, cam.fx, cam.fy, cam.cx, cam.cy).clone())
+        assert torch.equal(rs.dirs, r.dirs.view(64, 64, 3)[rank::2].reshape(-1, 3))
+    torch.cuda.synchronize()
+    assert torch.equal(assemble_row_shards(parts, 64, 64), full)
