@@ -94,6 +94,14 @@ int cf_buckets_build_candidates(cf_buckets_t* b, int k, void* stream);
 int cf_knn_warp(const cf_buckets_t* buckets, const double* anchors, const double* dqs, int64_t n_nodes,
                 int k, double radius, int mode, const double* pts, int64_t n_pts,
                 int64_t* idx_out, double* w_out, double* pc_out, uint8_t* valid_out, void* stream);
+/* Hierarchical exact k-NN warp for graphs of up to 8192 nodes (k <= 8): queries
+ * are visited in `order` (optional permutation, e.g. by Morton code of the query
+ * position, so that each warp's 32 queries are neighbours); each warp culls the
+ * nodes against its queries' box and ranks survivors fp32-first, float64-exact.
+ * Same outputs and modes as cf_knn_warp, bit-identical indices. */
+int cf_knn_warp_cull(const double* anchors, const double* dqs, int64_t n_nodes, int k, double radius, int mode,
+                     const double* pts, const int* order, int64_t n_pts, int64_t* idx_out, double* w_out,
+                     double* pc_out, uint8_t* valid_out, void* stream);
 
 /* ------------------------------------------------------------------ KnnField */
 

@@ -109,6 +109,7 @@ _SIGS = {
     "cf_buckets_build": [_p, _p, _i64, _i32, _p],
     "cf_buckets_build_candidates": [_p, _i32, _p],
     "cf_knn_warp": [_p, _p, _p, _i64, _i32, _f64, _i32, _p, _i64, _p, _p, _p, _p, _p],
+    "cf_knn_warp_cull": [_p, _p, _i64, _i32, _f64, _i32, _p, _p, _i64, _p, _p, _p, _p, _p],
     "cf_knnfield_build": [_p, _i64, _i32, _i32, _p, _f64, _f64, _p, _p],
     "cf_knnfield_update": [_p, _p, _i64, _p, _i32, _i32, _p, _f64, _f64, _p, _p, _p, _p],
     "cf_knnfield_query": [_p, _p, _p, _p, _i32, _i32, _p, _f64, _f64, _p, _i64, _p, _p, _p, _p, _p],

@@ -77,14 +77,18 @@ __device__ __forceinline__ unsigned cull_ballot(const float4* __restrict__ s_af,
 //     (ballot masks, smem broadcast reads): pass 1 ranks the candidates per
 //     lane in fp32, pass 2 re-ranks the few that can still be in the top-k
 //     exactly in float64. Identical result to scanning every node.
-// n <= 1024 (pass 1 packs the node index into 10 key bits).
-template <int K>
-__device__ __forceinline__ bool ed_warp_point_cull(const double4* __restrict__ s_anchors,
-                                                   const float4* __restrict__ s_af, int n,
-                                                   const double* __restrict__ dqs, int k, double r2, bool inverse,
-                                                   d3 p, bool live, d3& out) {
+// n <= 2^IDXB (pass 1 packs the node index into IDXB key bits). `a64(i)` returns
+// node i in float64 (shared or global memory); s_af holds the fp32 copies with
+// s_af[0].w = max |coordinate|. Lanes with live = false only cooperate.
+template <int K, int IDXB, class A64>
+__device__ __forceinline__ void cull_topk(const A64& a64, const float4* __restrict__ s_af, int n, int k, d3 p,
+                                          bool live, TopK<K>& top) {
+  static_assert(IDXB >= 1 && IDXB <= 16, "node index bits");
+  constexpr unsigned IMASK = (1u << IDXB) - 1u;
+  // 2x the relative truncation of the fp32 d^2 by IDXB low bits: 2^(IDXB - 22)
+  constexpr float TRUNC = 1.0f / (float)(1u << (22 - IDXB));
   const unsigned FULL = 0xffffffffu;
-  if (!__any_sync(FULL, live)) return false;  // warp-uniform
+  top.init(k);
   const int lane = threadIdx.x & 31;
   const float px = (float)p.x, py = (float)p.y, pz = (float)p.z;
   const float INF = __int_as_float(0x7f800000);
@@ -134,7 +138,7 @@ __device__ __forceinline__ bool ed_warp_point_cull(const double4* __restrict__ s
   }
   const float cut = U + 2.0f * slack;
   // Pass 1 (fp32 only): each lane keeps the L = K+2 smallest keys over the
-  // warp's candidate set, key = (fp32 d^2 bits with the low 10 mantissa bits
+  // warp's candidate set, key = (fp32 d^2 bits with the low IDXB mantissa bits
   // replaced by the node index) — non-negative floats order as their bits, so
   // one unsigned min/max pair per slot keeps the list sorted.
   constexpr int L = K + 2;
@@ -149,7 +153,7 @@ __device__ __forceinline__ bool ed_warp_point_cull(const double4* __restrict__ s
       mask &= mask - 1;
       const float4 af = s_af[node];
       const float ddx = px - af.x, ddy = py - af.y, ddz = pz - af.z;
-      unsigned v = (__float_as_uint(ddx * ddx + ddy * ddy + ddz * ddz) & ~1023u) | (unsigned)node;
+      unsigned v = (__float_as_uint(ddx * ddx + ddy * ddy + ddz * ddz) & ~IMASK) | (unsigned)node;
 #pragma unroll
       for (int j = 0; j < L; ++j) {
         const unsigned lo_v = min(v, key[j]);
@@ -159,24 +163,21 @@ __device__ __forceinline__ bool ed_warp_point_cull(const double4* __restrict__ s
     }
   }
   // Every node of the exact top-k has fp32 d^2 <= fcut: the k-th exact d^2 is
-  // <= (k-th smallest fp32 d^2) + slack <= trunc(key[K-1]) (1 + 2^-13) + slack,
+  // <= (k-th smallest fp32 d^2) + slack <= trunc(key[K-1]) (1 + TRUNC) + slack,
   // and each fp32 d^2 is within slack of its exact value. Truncation only lowers
   // keys, so key <= fcut_key <=> trunc(fp32 d^2) <= fcut. The list is complete
   // when its last slot is beyond fcut (or empty): every node outside it has a
   // key >= key[L-1].
-  const float fcut = __uint_as_float(key[K - 1] & ~1023u) * (1.0f + 2.4414062e-4f) + 2.0f * slack;
-  const unsigned fcut_key = __float_as_uint(fcut) | 1023u;
+  const float fcut = __uint_as_float(key[K - 1] & ~IMASK) * (1.0f + TRUNC) + 2.0f * slack;
+  const unsigned fcut_key = __float_as_uint(fcut) | IMASK;
   const bool complete = key[L - 1] > fcut_key;
-  TopK<K> top;
-  top.init(k);
   if (__all_sync(FULL, complete || !live)) {
     // Pass 2: exact float64 ranking of the (typically k) survivors per lane
 #pragma unroll
     for (int j = 0; j < L; ++j)
       if (key[j] <= fcut_key) {
-        const int node = (int)(key[j] & 1023u);
-        const double4 a = s_anchors[node];
-        top.insert(sqdist(p, d3{a.x, a.y, a.z}), node);
+        const int node = (int)(key[j] & IMASK);
+        top.insert(sqdist(p, a64(node)), node);
       }
   } else {
     // rare near-tie band wider than the list: exact scan of the candidate set
@@ -189,12 +190,23 @@ __device__ __forceinline__ bool ed_warp_point_cull(const double4* __restrict__ s
         const float4 af = s_af[node];
         const float ddx = px - af.x, ddy = py - af.y, ddz = pz - af.z;
         if (ddx * ddx + ddy * ddy + ddz * ddz > bound) continue;
-        const double4 a = s_anchors[node];
-        top.insert(sqdist(p, d3{a.x, a.y, a.z}), node);
+        top.insert(sqdist(p, a64(node)), node);
         bound = (float)top.worst_d() * (1.0f + 4.0f * 1.1920929e-7f) + slack;
       }
     }
   }
+}
+
+// render path: anchors staged in shared memory, n <= 1024
+template <int K>
+__device__ __forceinline__ bool ed_warp_point_cull(const double4* __restrict__ s_anchors,
+                                                   const float4* __restrict__ s_af, int n,
+                                                   const double* __restrict__ dqs, int k, double r2, bool inverse,
+                                                   d3 p, bool live, d3& out) {
+  if (!__any_sync(0xffffffffu, live)) return false;  // warp-uniform
+  TopK<K> top;
+  cull_topk<K, 10>([&](int i) { const double4 a = s_anchors[i]; return d3{a.x, a.y, a.z}; }, s_af, n, k, p, live,
+                   top);
   if (!live) return false;
   return blend_apply<K>(top, dqs, k, r2, inverse, p, out);
 }

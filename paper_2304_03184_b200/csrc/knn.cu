@@ -11,6 +11,7 @@
 
 #include "buckets.cuh"
 #include "dq.cuh"
+#include "edwarp.cuh"
 
 namespace {
 
@@ -462,7 +463,7 @@ __device__ __forceinline__ void finish_query(const WarpArgs& A, int64_t q, d3 p,
   for (int j = 0; j < K; ++j)
     if (j < A.k) {
       // np.exp(-d2 / (r * r))
-      w[j] = exp(x_div(-top.d[j], A.r2));
+      w[j] = exp(ExactDiv(A.r2)(-top.d[j]));
       valid |= w[j] > kWeightFloor;
     }
 #pragma unroll
@@ -536,6 +537,47 @@ __global__ void __launch_bounds__(128, 4) knn_bucket_kernel(WarpArgs A, const Bu
     if (!ccl_ids || !ccl_knn<K>(P, ccl_start, ccl_len, ccl_ids, A.anchors, p, top))
       bucket_knn<K>(P, cell_start, sorted, p, top);
     finish_query<K>(A, q, p, top);
+  }
+}
+
+// Hierarchical exact k-NN for graphs of up to 8192 nodes: the queries are
+// visited in a spatial order (`order`, e.g. Morton codes of the query cells) so
+// a warp's 32 queries are neighbours; the warp culls the nodes against its
+// queries' bounding box and ranks the survivors per lane, fp32 first and
+// float64 for the final top-k (edwarp.cuh cull_topk). The fp32 copies of the
+// nodes live in shared memory (16 B / node); the float64 coordinates are read
+// from global memory for the few survivors. Results are written at the
+// original query index: identical to the exhaustive kernel.
+constexpr int kCullMaxNodes = 8192;
+template <int K>
+__global__ void __launch_bounds__(256) knn_cull_kernel(WarpArgs A, const int* __restrict__ order) {
+  extern __shared__ float4 s_af[];
+  __shared__ unsigned s_mag;
+  if (threadIdx.x == 0) s_mag = 0u;
+  __syncthreads();
+  float mag = 0.f;
+  for (int i = threadIdx.x; i < A.n_nodes; i += blockDim.x) {
+    const double* a = A.anchors + 3 * (int64_t)i;
+    const float x = (float)a[0], y = (float)a[1], z = (float)a[2];
+    s_af[i] = make_float4(x, y, z, 0.f);
+    mag = fmaxf(mag, fmaxf(fabsf(x), fmaxf(fabsf(y), fabsf(z))));
+  }
+  atomicMax(&s_mag, __float_as_uint(mag));
+  __syncthreads();
+  if (threadIdx.x == 0) s_af[0].w = __uint_as_float(s_mag);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t n_warps = (A.n_pts + 31) / 32;
+  const int64_t wstride = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; w < n_warps; w += wstride) {
+    const int64_t slot = w * 32 + lane;
+    const bool live = slot < A.n_pts;
+    const int64_t q = live ? (order ? (int64_t)order[slot] : slot) : 0;
+    const d3 p = live ? load_d3(A.pts + 3 * q) : d3{0.0, 0.0, 0.0};
+    TopK<K> top;
+    cull_topk<K, 13>([&](int i) { return load_d3(A.anchors + 3 * (int64_t)i); }, s_af, A.n_nodes, A.k, p, live,
+                     top);
+    if (live) finish_query<K>(A, q, p, top);
   }
 }
 
@@ -666,6 +708,35 @@ int cf_buckets_build_candidates(cf_buckets_t* b, int k, void* stream) {
 
 int cf_buckets_build(cf_buckets_t* b, const double* pts, int64_t n, int grid_res, void* stream) {
   return cf::buckets_build(b, pts, n, grid_res, cf::as_stream(stream));
+}
+
+int cf_knn_warp_cull(const double* anchors, const double* dqs, int64_t n_nodes, int k, double radius, int mode,
+                     const double* pts, const int* order, int64_t n_pts, int64_t* idx_out, double* w_out,
+                     double* pc_out, uint8_t* valid_out, void* stream) {
+  if (n_nodes < 1 || n_nodes > kCullMaxNodes)
+    return cf::fail(CF_E_BAD_ARG, "cf_knn_warp_cull: 1 <= n_nodes <= 8192 (use the bucketed cf_knn_warp above)");
+  if (mode < CF_WARP_BACKWARD || mode > CF_NEIGHBORS_ONLY) return cf::fail(CF_E_BAD_ARG, "cf_knn_warp_cull: bad mode");
+  if (!(radius > 0.0)) return cf::fail(CF_E_BAD_ARG, "influence radius must be positive");
+  if (k < 1) return cf::fail(CF_E_BAD_ARG, "cf_knn_warp_cull: k must be >= 1");
+  if (k > n_nodes) k = (int)n_nodes;
+  if (mode != CF_NEIGHBORS_ONLY && !dqs) return cf::fail(CF_E_BAD_ARG, "cf_knn_warp_cull: dqs required");
+  if (n_pts == 0) return CF_OK;
+  WarpArgs A{anchors, dqs, (int)n_nodes, k, radius * radius, mode, pts, n_pts, idx_out, w_out, pc_out, valid_out};
+  cudaStream_t st = cf::as_stream(stream);
+  const size_t smem = sizeof(float4) * (size_t)n_nodes;
+  const int rc = dispatch_k(k, [&]<int K>() {
+    if (K > 8) return -1;  // the K+2 key list lives in registers
+    CF_CHECK_CUDA(cudaFuncSetAttribute(knn_cull_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(sizeof(float4) * kCullMaxNodes)));
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, knn_cull_kernel<K>, 256, smem);
+    const int64_t warps = (n_pts + 31) / 32;
+    int64_t grid = std::min<int64_t>((warps + 7) / 8, (int64_t)cf::sm_count() * std::max(per_sm, 1));
+    knn_cull_kernel<K><<<(unsigned)std::max<int64_t>(grid, 1), 256, smem, st>>>(A, order);
+    return cf::check_launch("cf_knn_warp_cull");
+  });
+  if (rc < 0) return cf::fail(CF_E_BAD_ARG, "cf_knn_warp_cull: k must be 1..8");
+  return rc;
 }
 
 int cf_knn_warp(const cf_buckets_t* buckets, const double* anchors, const double* dqs, int64_t n_nodes, int k,

@@ -132,6 +132,45 @@ def knn_warp(anchors: torch.Tensor, dqs: torch.Tensor | None, k: int, radius: fl
     return idx, w, pc, valid
 
 
+def morton_order(pts: torch.Tensor) -> torch.Tensor:
+    """int32 permutation visiting `pts` (N,3) in Morton (Z-curve) order of a 1024^3
+    grid over their bounding box: consecutive queries are spatial neighbours, which
+    is what the warp-level culling of cf_knn_warp_cull needs."""
+    lo = pts.min(0).values
+    ext = (pts.max(0).values - lo).clamp_min(1e-12)
+    c = ((pts - lo) / ext * 1023.0).clamp(0, 1023).to(torch.int64)
+
+    def spread(x):  # 10 bits -> every third bit
+        x = (x | (x << 16)) & 0x030000FF
+        x = (x | (x << 8)) & 0x0300F00F
+        x = (x | (x << 4)) & 0x030C30C3
+        return (x | (x << 2)) & 0x09249249
+
+    code = spread(c[:, 0]) | (spread(c[:, 1]) << 1) | (spread(c[:, 2]) << 2)
+    return torch.argsort(code).to(torch.int32)
+
+
+def knn_warp_cull(anchors: torch.Tensor, dqs: torch.Tensor | None, k: int, radius: float, mode: int,
+                  pts: torch.Tensor, order: torch.Tensor | None = None, want_idx=False, want_w=False, want_pc=True,
+                  want_valid=True):
+    """Hierarchical exact k-NN warp (n <= 8192 nodes, k <= 8) of cf_knn_warp_cull:
+    queries in Morton order, warp-level culling, fp32 ranking, float64 top-k.
+    Same outputs as knn_warp, bit-identical indices."""
+    n = pts.shape[0]
+    k = int(min(k, anchors.shape[0]))
+    d = pts.device
+    if order is None and n > 0:
+        order = morton_order(pts)
+    idx = torch.empty((n, k), dtype=torch.int64, device=d) if want_idx else None
+    w = torch.empty((n, k), dtype=torch.float64, device=d) if want_w else None
+    pc = torch.empty((n, 3), dtype=torch.float64, device=d) if want_pc else None
+    valid = torch.empty((n,), dtype=torch.uint8, device=d) if want_valid else None
+    _lib.call("cf_knn_warp_cull", anchors.data_ptr(), dqs.data_ptr() if dqs is not None else None,
+              int(anchors.shape[0]), k, float(radius), int(mode), pts.data_ptr(), _lib.ptr(order), int(n),
+              _lib.ptr(idx), _lib.ptr(w), _lib.ptr(pc), _lib.ptr(valid), _lib.stream_ptr())
+    return idx, w, pc, valid
+
+
 def _as_pts(pts):
     if is_device(pts):
         return dev(pts, shape_last=3), True
@@ -149,11 +188,16 @@ def deformed_nodes(graph, motion) -> np.ndarray:
 
 def warp_backward_batch(graph, motion, pts_live, strict: bool = False, search: str = "bucket",
                         frame: FrameMotion | None = None):
-    """Live -> canonical warp (edgraph.py:174-183); returns (pts_c, valid)."""
+    """Live -> canonical warp (edgraph.py:174-183); returns (pts_c, valid).
+    search: "bucket" (voxel buckets + ring search), "cull" (Morton-ordered warp
+    culling, n <= 8192, k <= 8) or "brute" — identical results."""
     pts, on_dev = _as_pts(pts_live)
     fm = frame or FrameMotion(graph, motion, buckets=(search == "bucket"))
-    _, _, pc, valid = knn_warp(fm.anchors, fm.dqs, fm.k, fm.radius, _lib.CF_WARP_BACKWARD, pts,
-                               fm.live_buckets if search == "bucket" else None)
+    if search == "cull":
+        _, _, pc, valid = knn_warp_cull(fm.anchors, fm.dqs, fm.k, fm.radius, _lib.CF_WARP_BACKWARD, pts)
+    else:
+        _, _, pc, valid = knn_warp(fm.anchors, fm.dqs, fm.k, fm.radius, _lib.CF_WARP_BACKWARD, pts,
+                                   fm.live_buckets if search == "bucket" else None)
     valid = valid.bool()
     if strict and not bool(valid.all()):
         raise OutOfSupportError("point outside deformed node influence")

@@ -15,7 +15,7 @@ import torch
 
 from . import _lib
 from ._tensors import dev, host, is_device
-from .edgraph import EDGraph, GraphMotion, FrameMotion, knn_warp, Buckets
+from .edgraph import EDGraph, GraphMotion, FrameMotion, knn_warp, knn_warp_cull, Buckets
 from .errors import OutOfSupportError
 
 
@@ -35,13 +35,18 @@ def brute_force_neighbors(graph, p, s: int) -> np.ndarray:
 def brute_force_query(graph, motion, pts_live, s: int, search: str = "brute"):
     """Exact (indices, weights, canonical pts) over deformed nodes (knnfield.py:32-42).
 
-    search="brute" is the exhaustive kernel; "bucket" the hierarchical search
-    (bit-identical indices)."""
+    search="brute" is the exhaustive kernel; "bucket" the voxel-bucket ring search;
+    "cull" the Morton-ordered warp-culled search (n <= 8192, s <= 8); all
+    bit-identical."""
     on_dev = is_device(pts_live)
     p = dev(pts_live if on_dev else np.atleast_2d(np.asarray(pts_live, dtype=np.float64)), shape_last=3)
     fm = FrameMotion(graph, motion, buckets=(search == "bucket"))
-    idx, w, pc, _ = knn_warp(fm.anchors, fm.dqs, s, fm.radius, _lib.CF_BRUTE_QUERY, p, fm.live_buckets,
-                             want_idx=True, want_w=True, want_valid=False)
+    if search == "cull":
+        idx, w, pc, _ = knn_warp_cull(fm.anchors, fm.dqs, s, fm.radius, _lib.CF_BRUTE_QUERY, p,
+                                      want_idx=True, want_w=True, want_valid=False)
+    else:
+        idx, w, pc, _ = knn_warp(fm.anchors, fm.dqs, s, fm.radius, _lib.CF_BRUTE_QUERY, p, fm.live_buckets,
+                                 want_idx=True, want_w=True, want_valid=False)
     if on_dev:
         return idx, w, pc
     return host(idx), host(w), host(pc)

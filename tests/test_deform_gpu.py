@@ -66,8 +66,8 @@ def test_scene_samples_vs_golden(stage1):
 
 @pytest.mark.parametrize("n,k", [(1024, 4), (2048, 8), (8192, 4), (8192, 8)])
 def test_dense_graph_bucket_equals_bruteforce(n, k):
-    """C4: hierarchical search == exhaustive kernel bit-for-bit on 2^16 queries,
-    and == the oracle on a subset."""
+    """C4: both hierarchical searches (voxel buckets; Morton-ordered warp culling)
+    == exhaustive kernel bit-for-bit on 2^16 queries, and == the oracle on a subset."""
     rng = np.random.default_rng(n + k)
     from paper_2304_03184_b200.scene import Scene, SceneConfig
     sc = Scene(SceneConfig(), seed=0)
@@ -81,9 +81,13 @@ def test_dense_graph_bucket_equals_bruteforce(n, k):
     motion = eg.GraphMotion(0, dqs)
     ib, wb, pb = kf.brute_force_query(graph, motion, q, k, search="bucket")
     ie, we, pe = kf.brute_force_query(graph, motion, q, k, search="brute")
+    ic, wc, pcc = kf.brute_force_query(graph, motion, q, k, search="cull")
     assert np.array_equal(ib, ie)
     assert np.array_equal(wb.view(np.int64), we.view(np.int64))
     assert np.array_equal(np.nan_to_num(pb), np.nan_to_num(pe))
+    assert np.array_equal(ic, ie)  # Morton-ordered warp-culled search
+    assert np.array_equal(wc.view(np.int64), we.view(np.int64))
+    assert np.array_equal(np.nan_to_num(pcc), np.nan_to_num(pe))
     sub = rng.choice(len(q), 2048, replace=False)
     io, wo, po = od.brute_force_query(nodes, 0.1, dqs, q[sub], k)
     assert np.array_equal(ib[sub], io)
