@@ -568,6 +568,37 @@ __global__ void __launch_bounds__(128) march_kernel(cf_march_desc M, cf_camera c
   pdl_trigger();
 }
 
+// backward-LBS fallback of a sample outside the ED support: its nearest posed
+// skin vertex (exact 1-NN on the vertex buckets) within lbs_max_dist -> that
+// vertex's inverse blended transform. No vertex can be that close when the
+// sample is that far from the vertex grid's box (which holds every vertex).
+__device__ __forceinline__ bool lbs_fallback(const BucketParams& sL, const int* __restrict__ lcs,
+                                             const double4* __restrict__ ls, const cf_human_warp& W, d3 p, d3& pt) {
+  const double q[3] = {p.x, p.y, p.z};
+  double d2b = 0.0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double e = fmax(fmax(sL.origin[a] - q[a], q[a] - (sL.origin[a] + sL.g[a] * sL.h)), 0.0);
+    d2b += e * e;
+  }
+  TopK<1> top;
+  top.init(1);
+  if (d2b <= W.lbs_max_d2 * (1.0 + 1e-9)) bucket_knn<1>(sL, lcs, ls, p, top, W.lbs_max_d2);
+  if (!(top.d[0] <= W.lbs_max_d2)) return false;
+  const double* T = W.vert_Tinv + 12 * (int64_t)top.i[0];
+  pt = d3{T[0] * p.x + T[1] * p.y + T[2] * p.z + T[3], T[4] * p.x + T[5] * p.y + T[6] * p.z + T[7],
+          T[8] * p.x + T[9] * p.y + T[10] * p.z + T[11]};
+  return true;
+}
+
+// canonical unit-cube coordinates + flag (1 = ED, 2 = LBS, 0 = empty)
+__device__ __forceinline__ float4 canon_out(const cf_human_warp& W, d3 pt, float flag) {
+  if (!(flag > 0.0f)) return make_float4(0.f, 0.f, 0.f, 0.f);
+  return make_float4(__double2float_rn(x_mul(x_sub(pt.x, W.canon_min[0]), W.inv_side)),
+                     __double2float_rn(x_mul(x_sub(pt.y, W.canon_min[1]), W.inv_side)),
+                     __double2float_rn(x_mul(x_sub(pt.z, W.canon_min[2]), W.inv_side)), flag);
+}
+
 // human samples: live point -> ED backward warp (exact bucketed k-NN + DQB^-1),
 // falling back to backward LBS outside the ED support; -> canonical unit cube
 template <int K, bool kSmem>
@@ -664,34 +695,9 @@ __global__ void __launch_bounds__(128, CF_CANON_MINB) human_canon_kernel(cf_marc
     const bool ed_ok = kSmem ? ed_warp_point_cull<K>(s_anchors, s_af, W.n_nodes, W.dqs, W.k, W.r2, true, p, near, pt)
                              : (live && ed_warp_point<K>(sE, ecs, es, W.dqs, W.k, W.r2, true, p, pt));
     if (!live) continue;
-    if (ed_ok) {
-      flag = 1.0f;
-    } else if (LPp) {
-      // no skin vertex within lbs_max_dist when the sample is that far from the
-      // vertex grid's box (which holds every vertex): skip the search
-      const double q[3] = {p.x, p.y, p.z};
-      double d2b = 0.0;
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        const double e = fmax(fmax(sL.origin[a] - q[a], q[a] - (sL.origin[a] + sL.g[a] * sL.h)), 0.0);
-        d2b += e * e;
-      }
-      TopK<1> top;
-      top.init(1);
-      if (d2b <= W.lbs_max_d2 * (1.0 + 1e-9)) bucket_knn<1>(sL, lcs, ls, p, top, W.lbs_max_d2);
-      if (top.d[0] <= W.lbs_max_d2) {
-        const double* T = W.vert_Tinv + 12 * (int64_t)top.i[0];
-        pt = d3{T[0] * p.x + T[1] * p.y + T[2] * p.z + T[3], T[4] * p.x + T[5] * p.y + T[6] * p.z + T[7],
-                T[8] * p.x + T[9] * p.y + T[10] * p.z + T[11]};
-        flag = 2.0f;
-      }
-    }
-    float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (flag > 0.0f)
-      r = make_float4(__double2float_rn(x_mul(x_sub(pt.x, W.canon_min[0]), W.inv_side)),
-                      __double2float_rn(x_mul(x_sub(pt.y, W.canon_min[1]), W.inv_side)),
-                      __double2float_rn(x_mul(x_sub(pt.z, W.canon_min[2]), W.inv_side)), flag);
-    xu[s] = r;
+    if (ed_ok) flag = 1.0f;
+    else if (LPp && lbs_fallback(sL, lcs, ls, W, p, pt)) flag = 2.0f;
+    xu[s] = canon_out(W, pt, flag);
   }
   // the last CTA out re-arms the ticket for the next launch on these counters
   __syncthreads();
