@@ -263,7 +263,14 @@ class Renderer:
         self.dirs = torch.empty((self.n_rays, 3), dtype=torch.float64, device=d)
         self.hb = _FieldBuffers(self.n_rays, cap, d) if human else None
         self.ob = _FieldBuffers(self.n_rays, cap, d) if obj else None
-        self.image = torch.empty((self.n_rays, 3), dtype=torch.float32, device=d)
+        # two image buffers, alternated per view: a view's image can be read back
+        # (render_to_host) while the next view renders into the other one
+        self._images = [torch.empty((self.n_rays, 3), dtype=torch.float32, device=d) for _ in range(2)]
+        self._img_slot = 0
+        self.image = self._images[0]
+        self._copy_stream = None
+        self._host_images = [None, None]
+        self._copy_done = [None, None]
         self.layer = torch.empty(self.n_rays, dtype=torch.uint8, device=d)
         self.live_occ = occ_grid(cfg.world_min, cfg.world_size, cfg.live_occ_res)
         self.live_bits = torch.zeros((cfg.live_occ_res ** 3 + 31) // 32, dtype=torch.int32, device=d)
@@ -437,6 +444,25 @@ class Renderer:
         ev.record(src)
         dst.wait_event(ev)
 
+    def render_to_host(self, R, t, fx, fy, cx, cy):
+        """render() and read the image back into pinned host memory without
+        blocking: returns (event, host image); the image is valid once the event
+        completed. The device-to-host copy runs on a copy stream, overlapping the
+        next view (which renders into the other image buffer)."""
+        img = self.render(R, t, fx, fy, cx, cy)
+        slot = self._img_slot ^ 1  # the buffer render() just used
+        if self._copy_stream is None:
+            self._copy_stream = torch.cuda.Stream(device=self.dirs.device)
+        if self._host_images[slot] is None:
+            self._host_images[slot] = torch.empty(img.shape, dtype=img.dtype).pin_memory()
+        self._copy_stream.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(self._copy_stream):
+            self._host_images[slot].copy_(img, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(self._copy_stream)
+        self._copy_done[slot] = ev
+        return ev, self._host_images[slot]  # reused two views later
+
     def prepare_frame(self) -> None:
         """Run the pending per-frame human setup now (eager launches) — for callers
         that use the frame's warp state without rendering a view (training)."""
@@ -454,7 +480,12 @@ class Renderer:
         setup = self._setup_pending and self.human is not None
         self._setup_pending = False
         timed = self.marks is not None
-        key = (setup, timed)
+        slot = self._img_slot
+        self._img_slot ^= 1
+        self.image = self._images[slot]
+        if self._copy_done[slot] is not None:  # this buffer's previous read-back must be done
+            torch.cuda.current_stream().wait_event(self._copy_done[slot])
+        key = (setup, timed, slot)
         if not self.cfg.cuda_graphs or (key not in self._graphs and not getattr(self, "_eager_done", False)):
             # eager launches (also the first view: lazily allocated state must exist before capture)
             if timed:

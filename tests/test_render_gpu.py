@@ -179,9 +179,9 @@ def test_render_deterministic(setup):
 
 
 def test_march_full_frame_bitexact():
-    """configs[1] (512x512, 128 samples/ray, frame 7): the march's fp32 fast path
-    (exact float64 only near cell boundaries) must give exactly the oracle's
-    float64 decisions for all 33.5 M nominal samples (oracle in ray chunks)."""
+    """configs[1] (512x512, 128 samples/ray, frame 7): the march (float64 tests
+    inside each ray's clipped interval of the occupied box) must give exactly the
+    oracle's decisions for all 33.5 M nominal samples (oracle in ray chunks)."""
     sc = Scene(SceneConfig(width=512, height=512), seed=0)
     cfg = RenderConfig(n_samples=128)
     hf = HumanField(sc.nodes, sc.template_points, sc.skin_verts, sc.skin_weights, cfg, seed=0)
