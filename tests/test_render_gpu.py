@@ -230,3 +230,43 @@ def test_row_sharded_render_equals_full_frame(setup):
         assert torch.equal(rs.dirs, r.dirs.view(64, 64, 3)[rank::2].reshape(-1, 3))
     torch.cuda.synchronize()
     assert torch.equal(assemble_row_shards(parts, 64, 64), full)
+
+
+def test_human_canon_dense_graph_and_eager_equals_graph():
+    """A 2048-node ED graph takes the bucketed ring-search path of the
+    canonicalisation (graphs > 1024 nodes), against the oracle; and the eager
+    launch sequence (cuda_graphs=False) renders the same image as the replayed
+    frame graph."""
+    sc = Scene(SceneConfig(width=64, height=64), seed=0)
+    rng = np.random.default_rng(5)
+    nodes = sc.template_points[rng.choice(len(sc.template_points), 2048, replace=False)]
+    fid = 7
+    A = sc.bone_transforms(fid)
+    near = np.argmin(((nodes[:, None] - sc.template_points[None, ::4]) ** 2).sum(-1), 1)
+    bones = sc.template_bones[::4][near]
+    dqs = np.stack([od.dq_from_rt(A[b, :3, :3], A[b, :3, 3]) for b in bones])
+    R, t = sc.object_pose(fid)
+    cam = sc.camera
+    imgs = []
+    for graphs in (False, True):
+        cfg = RenderConfig(n_samples=64, cuda_graphs=graphs)
+        hf = HumanField(nodes, sc.template_points, sc.skin_verts, sc.skin_weights, cfg, seed=0,
+                        zero_deform_out=False, table_scale=0.5)
+        of = ObjectField(sc.box_half, cfg, seed=1, table_scale=0.5)
+        r = Renderer(hf, of, 64, 64, cfg)
+        for _ in range(3):  # eager, capture, replay
+            r.set_frame(dqs, sc.theta(fid), A, R, t)
+            img = r.render(cam.R, cam.t, cam.fx, cam.fy, cam.cx, cam.cy)
+        torch.cuda.synchronize()
+        r.check_overflow()
+        imgs.append(img.clone())
+    assert torch.equal(imgs[0], imgs[1])
+    n, ray, i = field_samples(r.hb)
+    p = orr.sample_points(sc.camera.t, r.dirs.cpu().numpy(), ray, i, cfg.t_near, r.M.dt)
+    ref = orr.human_canon(p, nodes, dqs, cfg.ed_k, cfg.ed_radius, A, sc.skin_verts, sc.skin_weights,
+                          cfg.lbs_max_dist, hf.canon_min, hf.inv_side)
+    got = r.hb.xu[:n].cpu().numpy()
+    assert n > 1000 and np.array_equal(got[:, 3], ref[:, 3])
+    ed = ref[:, 3] == 1
+    ulp = np.abs(got[ed, :3].view(np.int32) - ref[ed, :3].view(np.int32))
+    assert ulp.max() <= 1 and (ulp == 0).mean() > 0.999
