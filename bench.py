@@ -426,9 +426,9 @@ def _prepare_cpu(sc, cfg, hf, of, frames, fid, live_on):
     _W.update(origin=sc.camera.t, dirs=d, S=cfg.n_samples, t_near=cfg.t_near,
               dt=(cfg.t_far - cfg.t_near) / cfg.n_samples, live_on=live_on, lg=lg, obj_on=obj_on, og=og,
               R=f["R"], t=f["t"], nodes=sc.nodes, dqs=f["dqs"], A=f["A"], verts=sc.skin_verts, vw=sc.skin_weights,
-              cmin=hf.canon_min, cinv=hf.inv_side, hl=hf.nets.layers, htab=hf.cgrid.table.cpu().numpy(),
-              dtab=hf.dgrid.table.cpu().numpy(), dbias=f["dbias"], ol=of.nets.layers,
-              otab=of.cgrid.table.cpu().numpy(), omin=of.obj_min, oinv=of.inv_side)
+              cmin=hf.canon_min, cinv=hf.inv_side, hl=hf.nets.layers, htab=hf.cgrid.table_as_read().cpu().numpy(),
+              dtab=hf.dgrid.table_as_read().cpu().numpy(), dbias=f["dbias"], ol=of.nets.layers,
+              otab=of.cgrid.table_as_read().cpu().numpy(), omin=of.obj_min, oinv=of.inv_side)
 
 
 def _live_on_host(r, hf, cfg, frames, fid):

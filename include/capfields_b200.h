@@ -305,9 +305,9 @@ int cf_composite_final(const cf_march_desc* M, const cf_march_out* F, const floa
 typedef struct cf_field_desc {
   int has_deform;
   cf_hashgrid_desc dgrid;   /* deformation grid (L*F = 32, F = 4) */
-  const float* dtable;
+  const void* dtable;       /* fp16 (entries, F): the fp16 copy of the fp32 parameters */
   cf_hashgrid_desc cgrid;   /* canonical grid (L*F = 32, F = 2) */
-  const float* ctable;
+  const void* ctable;       /* fp32 (entries, F) */
   const uint8_t* wblob;
   int w_bytes;
   const float* dbias;       /* DeformNet layer-1 bias (128), pose theta folded in */

@@ -28,8 +28,44 @@ constexpr int kSlotThreads = 128;
 
 // Hash features of L levels, CH levels at a time: all 8*CH corner gathers of a
 // chunk are issued before any is consumed. Same arithmetic as hashgrid.cu.
-template <int F, int L, int CH>
-__device__ __forceinline__ void hash_features(const cf_hashgrid_desc& D, const float* __restrict__ table, float x,
+// load one table entry (F values, fp32 or fp16) as fp32
+template <int F>
+__device__ __forceinline__ void ld_entry(const float* __restrict__ base, uint32_t idx, float* v) {
+  if constexpr (F == 2) {
+    const float2 f = __ldg(reinterpret_cast<const float2*>(base) + idx);
+    v[0] = f.x;
+    v[1] = f.y;
+  } else {
+    const float4 f = __ldg(reinterpret_cast<const float4*>(base) + idx);
+    v[0] = f.x;
+    v[1] = f.y;
+    v[2] = f.z;
+    v[3] = f.w;
+  }
+}
+template <int F>
+__device__ __forceinline__ void ld_entry(const __half* __restrict__ base, uint32_t idx, float* v) {
+  if constexpr (F == 2) {
+    const float2 f = __half22float2(__ldg(reinterpret_cast<const __half2*>(base) + idx));
+    v[0] = f.x;
+    v[1] = f.y;
+  } else {
+    const uint2 u = __ldg(reinterpret_cast<const uint2*>(base) + idx);
+    const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+    const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+    v[0] = a.x;
+    v[1] = a.y;
+    v[2] = b.x;
+    v[3] = b.y;
+  }
+}
+
+// table: (entries, F) row-major, fp32 or fp16 (TT); interpolation in fp32.
+// Measured: the deformation grid (F = 4) reads its fp16 copy (16 -> 8 B gathers:
+// 39 -> 28 us); the canonical grid (F = 2) stays fp32, where the two extra
+// conversions per corner outweighed the halved bytes (45 -> 59 us).
+template <int F, int L, int CH, class TT>
+__device__ __forceinline__ void hash_features(const cf_hashgrid_desc& D, const TT* __restrict__ table, float x,
                                               float y, float z, float* feat, int l_base = 0) {
   static_assert(L % CH == 0, "chunk must divide the level count");
   x = fminf(fmaxf(x, 0.0f), 1.0f);
@@ -57,23 +93,13 @@ __device__ __forceinline__ void hash_features(const cf_hashgrid_desc& D, const f
       }
       const uint32_t stride = (uint32_t)N + 1u;
       const bool dense = D.dense[l] != 0;
-      const float* base = table + D.offset[l] * F;
+      const TT* base = table + D.offset[l] * F;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const uint32_t cx = g[0] + (k & 1), cy = g[1] + ((k >> 1) & 1), cz = g[2] + ((k >> 2) & 1);
         const uint32_t idx = dense ? (cx + cy * stride + cz * stride * stride)
                                    : ((cx ^ (cy * 2654435761u) ^ (cz * 805459861u)) & mask);
-        if constexpr (F == 2) {
-          const float2 v = __ldg(reinterpret_cast<const float2*>(base) + idx);
-          t[c][k][0] = v.x;
-          t[c][k][1] = v.y;
-        } else {
-          const float4 v = __ldg(reinterpret_cast<const float4*>(base) + idx);
-          t[c][k][0] = v.x;
-          t[c][k][1] = v.y;
-          t[c][k][2] = v.z;
-          t[c][k][3] = v.w;
-        }
+        ld_entry<F>(base, idx, t[c][k]);
         const float wx = (k & 1) ? fr[0] : f_sub(1.0f, fr[0]);
         const float wy = (k & 2) ? fr[1] : f_sub(1.0f, fr[1]);
         const float wz = (k & 4) ? fr[2] : f_sub(1.0f, fr[2]);
@@ -97,8 +123,8 @@ __device__ __forceinline__ void hash_features(const cf_hashgrid_desc& D, const f
 // its 32 / SPLIT features of the row: SPLIT > 1 multiplies the warps in flight
 // for small sample counts (the object field), where one thread per sample left
 // the SMs mostly idle.
-template <int F, int L, int CH, int SPLIT>
-__global__ void __launch_bounds__(128) hash_f16_kernel(cf_hashgrid_desc D, const float* __restrict__ table,
+template <int F, int L, int CH, int SPLIT, class TT>
+__global__ void __launch_bounds__(128) hash_f16_kernel(cf_hashgrid_desc D, const TT* __restrict__ table,
                                                        const float4* __restrict__ x, const int* __restrict__ count,
                                                        int64_t capacity, uint4* __restrict__ out) {
   constexpr int LS = L / SPLIT, NF = LS * F;  // levels and features per thread
@@ -112,9 +138,9 @@ __global__ void __launch_bounds__(128) hash_f16_kernel(cf_hashgrid_desc D, const
     float feat[NF];
     if (p.w > 0.0f) {
       if constexpr (SPLIT == 1)
-        hash_features<F, LS, CH>(D, table, p.x, p.y, p.z, feat);
+        hash_features<F, LS, CH, TT>(D, table, p.x, p.y, p.z, feat);
       else
-        hash_features<F, LS, (CH < LS ? CH : LS)>(D, table, p.x, p.y, p.z, feat, part * LS);
+        hash_features<F, LS, (CH < LS ? CH : LS), TT>(D, table, p.x, p.y, p.z, feat, part * LS);
     } else {
 #pragma unroll
       for (int i = 0; i < NF; ++i) feat[i] = 0.0f;
@@ -989,7 +1015,7 @@ __global__ void __launch_bounds__(128) hash_bwd_dx_kernel(cf_hashgrid_desc D, co
 #pragma unroll
       for (int f = 0; f < F; ++f) gl[f] = g[l * F + f];
       float* base = grad + D.offset[l] * F;
-      const float* tb = table + D.offset[l] * F;
+      const float* tb = table + D.offset[l] * F;  // the values the forward interpolated
       float dl[3] = {0.f, 0.f, 0.f};
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
@@ -1010,14 +1036,11 @@ __global__ void __launch_bounds__(128) hash_bwd_dx_kernel(cf_hashgrid_desc D, co
           if constexpr (F == 2) atomicAdd(reinterpret_cast<float2*>(dst), make_float2(wv[0], wv[1]));
           else atomicAdd(reinterpret_cast<float4*>(dst), make_float4(wv[0], wv[1], wv[2], wv[3]));
         }
+        float tv[F];
+        ld_entry<F>(tb, idx, tv);
         float a = 0.f;  // dfeat_l . t_k
-        if constexpr (F == 2) {
-          const float2 t = __ldg(reinterpret_cast<const float2*>(tb) + idx);
-          a = gl[0] * t.x + gl[1] * t.y;
-        } else {
-          const float4 t = __ldg(reinterpret_cast<const float4*>(tb) + idx);
-          a = gl[0] * t.x + gl[1] * t.y + gl[2] * t.z + gl[3] * t.w;
-        }
+#pragma unroll
+        for (int f = 0; f < F; ++f) a += gl[f] * tv[f];
         dl[0] += a * ((k & 1) ? 1.f : -1.f) * wy * wz;
         dl[1] += a * ((k & 2) ? 1.f : -1.f) * wx * wz;
         dl[2] += a * ((k & 4) ? 1.f : -1.f) * wx * wy;
@@ -1085,7 +1108,8 @@ int cf_field_hash_backward(const cf_field_desc* FD, const cf_march_out* S, const
     x = reinterpret_cast<const float4*>(reinterpret_cast<const uint4*>(scratch) + cap * 8);
   if (dx_out)
     hash_bwd_dx_kernel<2, 16><<<cf::grid_for(cap, 128, 16), 128, 0, cf::as_stream(stream)>>>(
-        FD->cgrid, FD->ctable, x, dfeat, S->counters, cap, table_grad, reinterpret_cast<float4*>(dx_out));
+        FD->cgrid, reinterpret_cast<const float*>(FD->ctable), x, dfeat, S->counters, cap, table_grad,
+        reinterpret_cast<float4*>(dx_out));
   else
     hash_bwd_kernel<2, 16><<<cf::grid_for(cap, 128, 16), 128, 0, cf::as_stream(stream)>>>(
         FD->cgrid, x, dfeat, S->counters, cap, table_grad);
@@ -1142,7 +1166,7 @@ int cf_field_stage(const cf_field_desc* FD, const cf_march_out* S, const double*
     uint4* dfeat = cfeat + cap * 4;
     float4* xc = reinterpret_cast<float4*>(dfeat + cap * 4);
     if (run(0))
-      cf::launch_pdl(hash_f16_kernel<4, 8, 2, 1>, hgrid, 128, 0, st, FD->dgrid, FD->dtable, xu, S->counters, cap, dfeat);
+      cf::launch_pdl(hash_f16_kernel<4, 8, 2, 1, __half>, hgrid, 128, 0, st, FD->dgrid, reinterpret_cast<const __half*>(FD->dtable), xu, S->counters, cap, dfeat);
     if (run(1)) {
       const int smem = kDeformW + kDeformA;
       CF_CHECK_CUDA(cudaFuncSetAttribute(deform_mlp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -1153,10 +1177,10 @@ int cf_field_stage(const cf_field_desc* FD, const cf_march_out* S, const double*
   }
   if (run(2)) {
     if (FD->has_deform)
-      cf::launch_pdl(hash_f16_kernel<2, 16, 4, 1>, hgrid, 128, 0, st, FD->cgrid, FD->ctable, xcan, S->counters, cap,
+      cf::launch_pdl(hash_f16_kernel<2, 16, 4, 1, float>, hgrid, 128, 0, st, FD->cgrid, reinterpret_cast<const float*>(FD->ctable), xcan, S->counters, cap,
                      cfeat);
     else  // object field: few samples
-      cf::launch_pdl(hash_f16_kernel<2, 16, 4, 4>, cf::grid_for(cap * 4, 128, 16), 128, 0, st, FD->cgrid, FD->ctable,
+      cf::launch_pdl(hash_f16_kernel<2, 16, 4, 4, float>, cf::grid_for(cap * 4, 128, 16), 128, 0, st, FD->cgrid, reinterpret_cast<const float*>(FD->ctable),
                      xcan, S->counters, cap, cfeat);
   }
   if (run(3)) {

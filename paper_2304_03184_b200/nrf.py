@@ -30,10 +30,14 @@ class HashGridConfig:
 
 
 class HashGrid:
-    """Learnable multi-resolution hash tables (fp32, HBM/L2 resident)."""
+    """Learnable multi-resolution hash tables: fp32 parameters (`table`, what
+    training updates). With read_half=True the radiance-field kernels read an fp16
+    copy (`table_f16`, refreshed by refresh_f16(); half the gather bytes — used for
+    the F = 4 deformation grid). The standalone encode API reads the
+    fp32 table."""
 
     def __init__(self, cfg: HashGridConfig | None = None, init_scale: float = 1e-4, seed: int = 0,
-                 table: np.ndarray | torch.Tensor | None = None):
+                 table: np.ndarray | torch.Tensor | None = None, read_half: bool = False):
         self.cfg = cfg = cfg or HashGridConfig()
         self.desc = _lib.HashGridDesc()
         _lib.call("cf_hashgrid_init", ctypes.byref(self.desc), cfg.n_levels, cfg.n_features, cfg.log2_table,
@@ -45,6 +49,21 @@ class HashGrid:
         self.table = dev(table, dtype=torch.float32, shape_last=cfg.n_features)
         if self.table.shape[0] != self.n_entries:
             raise ValueError(f"table must have {self.n_entries} entries")
+        self.read_half = bool(read_half)
+        self.table_f16 = self.table.to(torch.float16) if self.read_half else None
+
+    def refresh_f16(self) -> None:
+        """Re-round the fp16 copy after the fp32 table changed (stream-ordered)."""
+        if self.read_half:
+            self.table_f16.copy_(self.table)
+
+    def table_for_kernels(self) -> torch.Tensor:
+        """The tensor the field kernels read (fp16 copy or the fp32 table)."""
+        return self.table_f16 if self.read_half else self.table
+
+    def table_as_read(self) -> torch.Tensor:
+        """The values the field kernels interpolate, as fp32."""
+        return self.table_f16.float() if self.read_half else self.table
 
     @property
     def out_dim(self) -> int:

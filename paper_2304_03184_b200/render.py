@@ -112,7 +112,7 @@ class HumanField:
         self.inv_side = 1.0 / self.side
         rng = np.random.default_rng(seed)
         self.cgrid = HashGrid(CANON_GRID, init_scale=table_scale, seed=seed + 1)
-        self.dgrid = HashGrid(DEFORM_GRID, init_scale=table_scale, seed=seed + 2)
+        self.dgrid = HashGrid(DEFORM_GRID, init_scale=table_scale, seed=seed + 2, read_half=True)
         self.nets = FieldNets(rng, deform=True, zero_deform_out=zero_deform_out)
         self.graph = EDGraph(nodes, radius=cfg.ed_radius, knn_k=cfg.ed_k)
         self.nodes = dev(nodes, shape_last=3)
@@ -151,9 +151,9 @@ class HumanField:
         d = _lib.FieldDesc()
         d.has_deform = 1
         d.dgrid = self.dgrid.desc
-        d.dtable = self.dgrid.table.data_ptr()
+        d.dtable = self.dgrid.table_for_kernels().data_ptr()
         d.cgrid = self.cgrid.desc
-        d.ctable = self.cgrid.table.data_ptr()
+        d.ctable = self.cgrid.table_for_kernels().data_ptr()
         d.wblob = self.nets.blob.data_ptr()
         d.w_bytes = self.nets.w_bytes
         d.dbias = dbias.data_ptr()
@@ -184,7 +184,7 @@ class ObjectField:
         d = _lib.FieldDesc()
         d.has_deform = 0
         d.cgrid = self.cgrid.desc
-        d.ctable = self.cgrid.table.data_ptr()
+        d.ctable = self.cgrid.table_for_kernels().data_ptr()
         d.wblob = self.nets.blob.data_ptr()
         d.w_bytes = self.nets.w_bytes
         d.delta_scale = 0.05

@@ -327,6 +327,7 @@ class Trainer:
             t = st["field"].cgrid.table
             _lib.call("cf_adam", t.data_ptr(), st["tgrad"].data_ptr(), st["tm"].data_ptr(), st["tv"].data_ptr(),
                       t.numel(), cfg.lr_hash, cfg.beta1, cfg.beta2, cfg.eps, self.step_count, 1.0 / nb, s)
+            st["field"].cgrid.refresh_f16()
             P = st["params"]
             for k in COLOR_LAYERS:
                 _lib.call("cf_adam", P.W[k].data_ptr(), P.G[k].data_ptr(), P.m[k].data_ptr(), P.v[k].data_ptr(),
@@ -336,6 +337,7 @@ class Trainer:
                 t = st["field"].dgrid.table
                 _lib.call("cf_adam", t.data_ptr(), st["dtgrad"].data_ptr(), st["dtm"].data_ptr(), st["dtv"].data_ptr(),
                           t.numel(), cfg.lr_hash, cfg.beta1, cfg.beta2, cfg.eps, self.step_count, 1.0 / nb, s)
+                st["field"].dgrid.refresh_f16()
                 D = st["deform"]
                 for k in DEFORM_LAYERS:
                     _lib.call("cf_adam", D.W[k].data_ptr(), D.G[k].data_ptr(), D.m[k].data_ptr(), D.v[k].data_ptr(),

@@ -232,7 +232,7 @@ def test_canonical_hash_spatial_gradient(setup):
     keep = (xc[:, 3] > 0).numpy()
     sel = np.nonzero(keep)[0][:3000]
     x = xc[sel, :3].clone().requires_grad_(True)
-    table = hf.cgrid.table.detach().cpu().view(-1, 2)
+    table = hf.cgrid.table_as_read().cpu().view(-1, 2)  # the values the forward interpolated
     levels = hf.cgrid.levels()
     feat = _trilinear_torch(x, table, levels, hf.cgrid.cfg.log2_table, 2)
     g = st["bwd"].dfeat[:n].cpu()[sel]
