@@ -529,45 +529,46 @@ def run_reference(args, rank, world, pg):
 
 def run_train(args, rank, world, pg):
     """configs[2]: key-frame training step, 2^18 rays (global; sharded over ranks)
-    drawn from the 10 key frames, forward + backward + Adam, gradients all-reduced."""
+    drawn from the 10 key frames, forward + backward + Adam, gradients all-reduced.
+    The key frames' images live in HBM; every step draws fresh rays from their
+    foreground pixels on the device (KeyFrame.sample, inside the timed step)."""
     import torch
-    from paper_2304_03184_b200.train import FrameBatch, Trainer, TrainConfig, allreduce_grads, shard_rays
+    from paper_2304_03184_b200.train import KeyFrame, Trainer, TrainConfig, allreduce_grads, shard_rays
     sc, cfg, hf, of, r, frames = build_workload(args, rank)
     cam = sc.camera
     r.rays(cam.R, cam.t, cam.fx, cam.fy, cam.cx, cam.cy)
     dev = torch.device("cuda", torch.cuda.current_device())
-    rng = np.random.default_rng(rank)
     mine = shard_rays(args.train_rays, rank, world)
     n_local = mine.stop - mine.start
     per_frame = int(np.ceil(n_local / len(frames)))
     o, d = cam.all_rays()
-    batches = []
+    T = lambda x, dt: torch.as_tensor(np.ascontiguousarray(x), dtype=dt, device=dev)  # noqa: E731
+    keyframes = []
     for fid, f in enumerate(frames):
-        # rays from the foreground (human / object mask) pixels of the frame (SURVEY §8d C3)
-        _, _, _, hum_all, obj_all = sc.raycast(o, d, fid)
-        fg = np.nonzero(hum_all | obj_all)[0]
-        pick = rng.choice(fg, per_frame, replace=per_frame > len(fg))
-        th, to, rgb, hum, obj = sc.raycast(o[pick], d[pick], fid)
+        # the key frame's images (SURVEY 8d C3: targets of the human / object pixels), once, untimed
+        th, to, rgb, hum, obj = sc.raycast(o, d, fid)
         depth = np.where(hum, th, np.where(obj, to, 0.0))
-        T = lambda x, dt: torch.as_tensor(np.ascontiguousarray(x), dtype=dt, device=dev)  # noqa: E731
-        batches.append(FrameBatch(dqs=T(f["dqs"], torch.float64), bone_A=T(f["A"], torch.float64),
-                                  dbias=T(f["dbias"], torch.float32), obj_R=f["R"], obj_t=f["t"],
-                                  dirs=T(d[pick], torch.float64), gt_rgb=T(rgb, torch.float32),
-                                  gt_depth=T(depth, torch.float32), mask_h=T(hum, torch.uint8),
-                                  mask_o=T(obj, torch.uint8), theta=T(f["theta"], torch.float32)))
+        keyframes.append(KeyFrame(cam, T(rgb, torch.float32), T(depth, torch.float32), T(hum, torch.uint8),
+                                  T(obj, torch.uint8), T(f["dqs"], torch.float64), T(f["A"], torch.float64),
+                                  T(f["dbias"], torch.float32), T(f["theta"], torch.float32), f["R"], f["t"]))
+    step_no = [0]
+
+    def draw():
+        step_no[0] += 1
+        return [kf.sample(per_frame, seed=(step_no[0] * 1000 + fid) * 64 + rank)
+                for fid, kf in enumerate(keyframes)]
+
+    batches = draw()
     tr = Trainer(r, max_rays=per_frame, cfg=TrainConfig())
     ar = (lambda ts: allreduce_grads(ts)) if world > 1 else None
     for _ in range(args.warmup):
-        tr.step(batches, allreduce=ar)
+        tr.step(draw(), allreduce=ar)
     torch.cuda.synchronize()
     barrier(pg)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    n_samples = 0
     a.record()
     for _ in range(args.steps):
-        tr.step(batches, allreduce=ar)
-        for st in tr.fields:
-            n_samples += int(st["buf"].counters[0]) * 0  # counts per frame summed below
+        tr.step(draw(), allreduce=ar)
     b.record()
     torch.cuda.synchronize()
     barrier(pg)
@@ -585,7 +586,8 @@ def run_train(args, rank, world, pg):
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64 deform / f32 hash+grads / fp16-in fp32-acc MLP",
             "data": "synthetic (analytic ray-cast targets of the scripted scene)",
-            "config": {"workload": f"key-frame training step (configs[2]): {args.train_rays} rays over 10 frames, "
+            "config": {"workload": f"key-frame training step (configs[2]): {args.train_rays} rays over 10 frames "
+                                   f"drawn on the device every step from the HBM-resident key-frame images, "
                                    f"32 guided + 16 uniform / 64 empty samples per ray",
                        "samples_per_step": per_step, "parallelism": f"dp{world} (rays sharded, grads all-reduced)"}}
     if rank == 0:

@@ -329,6 +329,15 @@ int cf_field_stage(const cf_field_desc* F, const cf_march_out* S, const double* 
 
 /* ------------------------------------------------------------------ training (SPEC train_step) */
 
+/* training rays of one key frame (device ray-batch sampler): n_rays pixels drawn
+ * uniformly with replacement from fg_pixels (the frame's foreground pixel ids) by a
+ * counter-based hash of (seed, i); gathers rgb (H*W,3), depth, masks at those pixels
+ * and writes each pixel's exact camera ray (same directions as cf_camera_rays);
+ * pix_out (optional) = the drawn pixel ids */
+int cf_keyframe_rays(const cf_camera* cam, const int* fg_pixels, int64_t n_fg, int64_t n_rays, uint64_t seed,
+                     const float* rgb, const float* depth, const uint8_t* mask_h, const uint8_t* mask_o, int* pix_out,
+                     double* dirs, float* rgb_out, float* depth_out, uint8_t* mask_h_out, uint8_t* mask_o_out,
+                     void* stream);
 /* depth-guided samples of the masked rays: fills F (records, per-ray
  * offset/count, counters) and t_out (float64 depth per compacted sample; pass it as
  * M->sample_t to the canonicalisation / field / composite calls) */

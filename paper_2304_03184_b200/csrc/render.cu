@@ -915,6 +915,33 @@ __device__ __forceinline__ double u01(uint64_t seed, uint64_t ray, uint64_t j) {
   return (double)(z >> 11) * 0x1.0p-53;
 }
 
+// Training rays of one key frame (the ray-batch sampler on the
+// device): n pixels drawn uniformly with replacement from the frame's foreground
+// pixel list (u01 of (seed, i)); their targets are gathered from the frame's
+// HBM-resident images and their exact camera rays generated (pixel_dir).
+__global__ void keyframe_rays_kernel(cf_camera cam, const int* __restrict__ fg, int64_t n_fg, int64_t n,
+                                     uint64_t seed, const float* __restrict__ rgb, const float* __restrict__ depth,
+                                     const uint8_t* __restrict__ mask_h, const uint8_t* __restrict__ mask_o,
+                                     int* __restrict__ pix_out, double* __restrict__ dirs, float* __restrict__ rgb_o,
+                                     float* __restrict__ depth_o, uint8_t* __restrict__ mh_o,
+                                     uint8_t* __restrict__ mo_o) {
+  __shared__ double s_cam[13];
+  load_camera(cam, s_cam);
+  const ExactDiv by_fx(s_cam[9]), by_fy(s_cam[10]);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = min((int64_t)(u01(seed, (uint64_t)i, 0) * (double)n_fg), n_fg - 1);
+    const int px = fg[k];
+    if (pix_out) pix_out[i] = px;
+    store_d3(dirs + 3 * i, pixel_dir(s_cam, by_fx, by_fy, cam.width, px));
+    rgb_o[3 * i] = rgb[3 * (int64_t)px];
+    rgb_o[3 * i + 1] = rgb[3 * (int64_t)px + 1];
+    rgb_o[3 * i + 2] = rgb[3 * (int64_t)px + 2];
+    depth_o[i] = depth[px];
+    mh_o[i] = mask_h[px];
+    mo_o[i] = mask_o[px];
+  }
+}
+
 // Depth-guided training samples: a masked ray with valid depth d
 // gets n_guided stratified samples in [d - 6 s, d + 6 s] (clamped to
 // [t_near, t_far]) merged with n_uniform stratified samples over [t_near, t_far];
@@ -1169,6 +1196,20 @@ int cf_composite(const cf_march_desc* M, const cf_march_out* F, const float* fie
   cf::launch_pdl(composite_kernel, cf::grid_for(M->n_rays, 128, 8), 128, 0, cf::as_stream(stream), *M, *F, field, t_term, rgb,
                                                                                         depth, opacity);
   return cf::check_launch("cf_composite");
+}
+
+int cf_keyframe_rays(const cf_camera* cam, const int* fg_pixels, int64_t n_fg, int64_t n_rays, uint64_t seed,
+                     const float* rgb, const float* depth, const uint8_t* mask_h, const uint8_t* mask_o, int* pix_out,
+                     double* dirs, float* rgb_out, float* depth_out, uint8_t* mask_h_out, uint8_t* mask_o_out,
+                     void* stream) {
+  if (!cam || !fg_pixels || n_fg < 1 || n_rays < 0 || !rgb || !depth || !mask_h || !mask_o || !dirs || !rgb_out ||
+      !depth_out || !mask_h_out || !mask_o_out)
+    return cf::fail(CF_E_BAD_ARG, "cf_keyframe_rays: bad args");
+  if (n_rays == 0) return CF_OK;
+  keyframe_rays_kernel<<<cf::grid_for(n_rays, 256, 4), 256, 0, cf::as_stream(stream)>>>(
+      *cam, fg_pixels, n_fg, n_rays, seed, rgb, depth, mask_h, mask_o, pix_out, dirs, rgb_out, depth_out, mask_h_out,
+      mask_o_out);
+  return cf::check_launch("cf_keyframe_rays");
 }
 
 int cf_train_sample(const cf_march_desc* M, const float* gt_depth, const uint8_t* mask, int n_guided, int n_uniform,

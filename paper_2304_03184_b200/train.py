@@ -60,6 +60,43 @@ class FrameBatch:
     theta: torch.Tensor | None = None  # (72,) f32 pose; DeformNet training recomputes dbias from it
 
 
+class KeyFrame:
+    """A key frame resident in HBM: its images at full resolution
+    (rgb (H*W,3) f32, depth (H*W,) f32 with <= 0 = none, human/object masks u8),
+    its camera and its motion prior / object pose. sample() draws a FrameBatch of
+    training rays on the device (cf_keyframe_rays)."""
+
+    def __init__(self, camera, rgb, depth, mask_h, mask_o, dqs, bone_A, dbias, theta, obj_R, obj_t):
+        self.cam = _lib.Camera()
+        Rf = np.asarray(camera.R, dtype=np.float64).reshape(9)
+        for i in range(9):
+            self.cam.R[i] = Rf[i]
+        self.cam.fx, self.cam.fy = float(camera.fx), float(camera.fy)
+        self.cam.cx, self.cam.cy = float(camera.cx), float(camera.cy)
+        self.cam.width, self.cam.height = int(camera.width), int(camera.height)
+        self.rgb = rgb.contiguous()
+        self.depth = depth.contiguous()
+        self.mask_h = mask_h.contiguous()
+        self.mask_o = mask_o.contiguous()
+        self.fg = torch.nonzero((self.mask_h | self.mask_o).view(-1)).view(-1).to(torch.int32)
+        self.dqs, self.bone_A, self.theta, self.dbias = dqs, bone_A, theta, dbias
+        self.obj_R, self.obj_t = obj_R, obj_t
+
+    def sample(self, n_rays: int, seed: int) -> FrameBatch:
+        d = self.rgb.device
+        dirs = torch.empty((n_rays, 3), dtype=torch.float64, device=d)
+        rgb = torch.empty((n_rays, 3), dtype=torch.float32, device=d)
+        depth = torch.empty(n_rays, dtype=torch.float32, device=d)
+        mh = torch.empty(n_rays, dtype=torch.uint8, device=d)
+        mo = torch.empty(n_rays, dtype=torch.uint8, device=d)
+        _lib.call("cf_keyframe_rays", _lib.byref(self.cam), self.fg.data_ptr(), int(self.fg.numel()), int(n_rays),
+                  ctypes.c_uint64(seed), self.rgb.data_ptr(), self.depth.data_ptr(), self.mask_h.data_ptr(),
+                  self.mask_o.data_ptr(), None, dirs.data_ptr(), rgb.data_ptr(), depth.data_ptr(), mh.data_ptr(),
+                  mo.data_ptr(), _lib.stream_ptr())
+        return FrameBatch(dqs=self.dqs, bone_A=self.bone_A, dbias=self.dbias, obj_R=self.obj_R, obj_t=self.obj_t,
+                          dirs=dirs, gt_rgb=rgb, gt_depth=depth, mask_h=mh, mask_o=mo, theta=self.theta)
+
+
 class ColorParams:
     """fp32 master weights of E_g/E_c on the device, their grads and Adam moments;
     repacks the fp16 forward and transposed blobs after every update."""
@@ -256,6 +293,16 @@ class Trainer:
         n = int(buf.counters[0])
         if n == 0:
             return
+        # The GEMM row count is rounded up to one of 8 sizes per power of two (within
+        # the buffers) so that frames with different sample counts reuse cuBLASLt's
+        # cached plans (a new shape costs ~4 ms of host-side heuristics); the padding
+        # rows of the dY operands are zeroed, so they add nothing.
+        q = 1 << max(n.bit_length() - 4, 10)
+        n_pad = min(-(-n // q) * q, buf.mo.capacity)
+        dys = [bwd.d_o, bwd.dc2, bwd.dc1, bwd.dg, bwd.dh1] + ([db.d_o, db.dpre] if dp is not None else [])
+        for t in dys:
+            t[n:n_pad].zero_()
+        n, n_true = n_pad, n
         x0 = scratch[: n * 64].view(torch.float16).view(n, 32)
         # fp16 operands on the tensor cores, fp32 accumulation (reduced-precision
         # split-K reduction disabled), fp32 gradient accumulation across frames
@@ -280,7 +327,7 @@ class Trainer:
             # theta is the same for every sample of the frame: dW1_theta = (sum_s dpre1) theta^T
             csum = db.colsum
             csum.zero_()
-            _lib.call("cf_colsum128_f16", DP.data_ptr(), n, 512, csum.data_ptr(), s)
+            _lib.call("cf_colsum128_f16", DP.data_ptr(), n_true, 512, csum.data_ptr(), s)
             GD["D1"][:, 32:] += torch.outer(csum, b.theta.to(DP.device, torch.float32))
 
     def set_frame(self, b: FrameBatch):

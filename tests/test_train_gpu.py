@@ -345,3 +345,41 @@ def test_training_reduces_loss(setup):
     o0, o1 = first["object"].cpu().numpy(), last["object"].cpu().numpy()
     assert f1[0] < 0.5 * f0[0], (f0, f1)
     assert o1[0] < 0.5 * o0[0], (o0, o1)
+
+
+def test_keyframe_ray_sampler(setup):
+    """Device ray-batch sampler: drawn pixels are foreground pixels of the key
+    frame, their targets are gathered from its images, and their rays equal the
+    camera's rays of those pixels (cf_keyframe_rays)."""
+    from paper_2304_03184_b200.train import KeyFrame
+    sc, hf, of, r, tr, batches = setup
+    cam = sc.camera
+    o, d = cam.all_rays()
+    th, to, rgb, hum, obj = sc.raycast(o, d, 3)
+    depth = np.where(hum, th, np.where(obj, to, 0.0))
+    T = lambda x, dt: torch.as_tensor(np.ascontiguousarray(x), dtype=dt, device="cuda")  # noqa: E731
+    kf = KeyFrame(cam, T(rgb, torch.float32), T(depth, torch.float32), T(hum, torch.uint8), T(obj, torch.uint8),
+                  T(sc.node_dqs(3), torch.float64), T(sc.bone_transforms(3), torch.float64),
+                  T(hf.nets.theta_bias(sc.theta(3)), torch.float32), T(sc.theta(3), torch.float32),
+                  *sc.object_pose(3))
+    n = 20000
+    pix = torch.empty(n, dtype=torch.int32, device="cuda")
+    dirs = torch.empty((n, 3), dtype=torch.float64, device="cuda")
+    g_rgb = torch.empty((n, 3), dtype=torch.float32, device="cuda")
+    g_d = torch.empty(n, dtype=torch.float32, device="cuda")
+    mh = torch.empty(n, dtype=torch.uint8, device="cuda")
+    mo = torch.empty(n, dtype=torch.uint8, device="cuda")
+    _lib.call("cf_keyframe_rays", _lib.byref(kf.cam), kf.fg.data_ptr(), int(kf.fg.numel()), n,
+              _lib.ctypes.c_uint64(7), kf.rgb.data_ptr(), kf.depth.data_ptr(), kf.mask_h.data_ptr(),
+              kf.mask_o.data_ptr(), pix.data_ptr(), dirs.data_ptr(), g_rgb.data_ptr(), g_d.data_ptr(),
+              mh.data_ptr(), mo.data_ptr(), _lib.stream_ptr())
+    p = pix.cpu().numpy()
+    fg = np.nonzero(hum | obj)[0]
+    assert np.isin(p, fg).all() and len(np.unique(p)) > 0.5 * min(len(fg), n)
+    assert np.array_equal(g_rgb.cpu().numpy(), rgb[p].astype(np.float32))
+    assert np.array_equal(g_d.cpu().numpy(), depth[p].astype(np.float32))
+    assert np.array_equal(mh.cpu().numpy(), hum[p].astype(np.uint8))
+    assert np.array_equal(mo.cpu().numpy(), obj[p].astype(np.uint8))
+    assert np.allclose(dirs.cpu().numpy(), d[p], rtol=0, atol=1e-15)
+    b = kf.sample(4096, seed=11)
+    assert b.dirs.shape == (4096, 3) and int(b.mask_h.sum() + b.mask_o.sum()) >= 4096
