@@ -349,6 +349,10 @@ def run_ours(args, rank, world, pg):
         roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
                 "frac": ach / hbm_peak, "traffic": traffic, "per_unit": per_text,
                 "peak_source": peak_src + " hbm_gbs"}
+    if dom == "human_canon":
+        roof["note"] = ("float64 k-NN + DQB^-1 blend in the reference's exact op order: FP64-issue / latency bound "
+                        "(ncu: fp64 pipe ~17 %, IPC 1.5, 24 % warps active, profiles/r01_kernels_ncu_full.csv); "
+                        "its HBM fraction is small by construction (inputs L2-resident)")
     roof["all_stages"] = {k: {"ms": stage_ms[k], "bound": c[0],
                               "achieved": (c[1] * c[2] / (stage_ms[k] / 1e3)) / (1e12 if c[0] == "tensor" else 1e9),
                               "unit": "TFLOP/s" if c[0] == "tensor" else "GB/s"}
