@@ -315,6 +315,7 @@ typedef struct cf_field_desc {
   float inv_side;           /* metres -> unit cube */
   void* save_h;             /* training: DeformNet hidden activations h1..h4, (S,512) fp16, or NULL */
   float* save_o;            /* training: DeformNet raw outputs (o0, o1, o2, 0) float4 per sample, or NULL */
+  uint32_t* save_mask;      /* training: ReLU bits of layers 1..4, (S,16) uint32 = [layer][half][2], or NULL */
 } cf_field_desc;
 /* device scratch needed by cf_field_forward for `capacity` samples */
 int cf_field_scratch_bytes(const cf_field_desc* F, int64_t capacity, int64_t* bytes);
@@ -377,8 +378,9 @@ int cf_field_hash_backward(const cf_field_desc* F, const cf_march_out* S, const 
                            const float* dfeat, float* table_grad, float* dx_out, void* stream);
 /* DeformNet backward buffers (S = capacity) */
 typedef struct cf_deform_bwd_io {
-  const void* save_h;  /* (S,512) fp16 forward h1..h4 (cf_field_desc.save_h) */
+  const void* save_h;  /* (S,512) fp16 forward h1..h4 (cf_field_desc.save_h; read by the dW GEMMs, not here) */
   const float* save_o; /* float4 per sample: raw outputs (cf_field_desc.save_o) */
+  const uint32_t* save_mask; /* (S,16) ReLU bits of layers 1..4 (cf_field_desc.save_mask) */
   void* d_o;           /* (S,16) fp16 dL/d(raw outputs) */
   void* dpre;          /* (S,512) fp16 dL/d(pre-activations) of layers 1..4 */
   float* d_dfeat;      /* (S,32) fp32 dL/d(deform hash features) */

@@ -83,11 +83,12 @@ class FieldDesc(ctypes.Structure):
     _fields_ = [("has_deform", ctypes.c_int), ("dgrid", HashGridDesc), ("dtable", ctypes.c_void_p),
                 ("cgrid", HashGridDesc), ("ctable", ctypes.c_void_p), ("wblob", ctypes.c_void_p),
                 ("w_bytes", ctypes.c_int), ("dbias", ctypes.c_void_p), ("delta_scale", ctypes.c_float),
-                ("inv_side", ctypes.c_float), ("save_h", ctypes.c_void_p), ("save_o", ctypes.c_void_p)]
+                ("inv_side", ctypes.c_float), ("save_h", ctypes.c_void_p), ("save_o", ctypes.c_void_p),
+                ("save_mask", ctypes.c_void_p)]
 
 
 class DeformBwdIO(ctypes.Structure):
-    _fields_ = [(n, ctypes.c_void_p) for n in ("save_h", "save_o", "d_o", "dpre", "d_dfeat")]
+    _fields_ = [(n, ctypes.c_void_p) for n in ("save_h", "save_o", "save_mask", "d_o", "dpre", "d_dfeat")]
 
 
 class ColorBwdIO(ctypes.Structure):

@@ -284,7 +284,10 @@ __device__ __forceinline__ void ts_layer(TsSlot& S, const uint8_t* w, int K, int
 
 // hidden epilogue of a 128-wide layer: this warp's 64 columns -> (+bias) ReLU -> fp16 -> A
 // (training: also -> save[col], the sample's row of this layer's activations)
-__device__ __forceinline__ void ts_relu128(const TsSlot& S, const float* bias, __half* save) {
+// (training: mask = the ReLU derivative bits of these 64 columns, 2 x uint32)
+__device__ __forceinline__ void ts_relu128(const TsSlot& S, const float* bias, __half* save,
+                                           uint32_t* mask = nullptr) {
+  uint32_t mw[2];
 #pragma unroll
   for (int c = 0; c < 2; ++c) {
     const int col = 64 * S.half + 32 * c;
@@ -292,6 +295,7 @@ __device__ __forceinline__ void ts_relu128(const TsSlot& S, const float* bias, _
     tc::tmem_ld32_nowait(S.d + (uint32_t)col, r);
     tc::tmem_wait_ld();
     uint32_t h[16];
+    uint32_t bits = 0;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       float x0 = __uint_as_float(r[2 * i]), x1 = __uint_as_float(r[2 * i + 1]);
@@ -299,8 +303,10 @@ __device__ __forceinline__ void ts_relu128(const TsSlot& S, const float* bias, _
         x0 += bias[col + 2 * i];
         x1 += bias[col + 2 * i + 1];
       }
+      bits |= (x0 > 0.0f ? 1u : 0u) << (2 * i) | (x1 > 0.0f ? 1u : 0u) << (2 * i + 1);
       h[i] = tc::relu_f16x2(x0, x1);
     }
+    mw[c] = bits;
     if (S.abuf) {
 #pragma unroll
       for (int q = 0; q < 4; ++q)
@@ -315,13 +321,17 @@ __device__ __forceinline__ void ts_relu128(const TsSlot& S, const float* bias, _
         reinterpret_cast<uint4*>(save + col)[q] = make_uint4(h[4 * q], h[4 * q + 1], h[4 * q + 2], h[4 * q + 3]);
     }
   }
+  if (mask) *reinterpret_cast<uint2*>(mask) = make_uint2(mw[0], mw[1]);
 }
 
+// kSave: the training forward (saves h, o and the ReLU bits); the render path
+// compiles without them
+template <bool kSave>
 __global__ void __launch_bounds__(kDeformSlots* kDeformSlotThreads, 1)
     deform_mlp_kernel(const uint8_t* __restrict__ wblob, const float* __restrict__ bias1, float delta_scale,
                       float inv_side, const float4* __restrict__ xu, const uint4* __restrict__ dfeat,
                       const int* __restrict__ count, int64_t capacity, float4* __restrict__ xc,
-                      __half* __restrict__ save_h, float4* __restrict__ save_o) {
+                      __half* __restrict__ save_h, float4* __restrict__ save_o, uint32_t* __restrict__ save_mask) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t mbar[kDeformSlots];
   __shared__ uint32_t tmem_base;
@@ -384,19 +394,21 @@ __global__ void __launch_bounds__(kDeformSlots* kDeformSlotThreads, 1)
 #pragma unroll
       for (int q = 0; q < 2; ++q) nxt[q] = (sn < n) ? dfeat[sn * 4 + 2 * S.half + q] : make_uint4(0, 0, 0, 0);
     }
-    __half* sv = (save_h && live) ? save_h + s * 512 : nullptr;
-    ts_relu128(S, s_bias, sv);
+    __half* sv = (kSave && live) ? save_h + s * 512 : nullptr;
+    // ReLU masks: per sample 4 layers x 2 halves x 64 bits
+    uint32_t* mk = (kSave && live) ? save_mask + s * 16 + 2 * S.half : nullptr;  // [layer][half][2]
+    ts_relu128(S, s_bias, sv, mk);
     ts_layer(S, smem + o2, 128, 128);
-    ts_relu128(S, nullptr, sv ? sv + 128 : nullptr);
+    ts_relu128(S, nullptr, sv ? sv + 128 : nullptr, mk ? mk + 4 : nullptr);
     ts_layer(S, smem + o3, 128, 128);
-    ts_relu128(S, nullptr, sv ? sv + 256 : nullptr);
+    ts_relu128(S, nullptr, sv ? sv + 256 : nullptr, mk ? mk + 8 : nullptr);
     ts_layer(S, smem + o4, 128, 128);
-    ts_relu128(S, nullptr, sv ? sv + 384 : nullptr);
+    ts_relu128(S, nullptr, sv ? sv + 384 : nullptr, mk ? mk + 12 : nullptr);
     ts_layer(S, smem + o5, 128, 16);
     if (S.half == 0) {
       float v[16];
       tc::tmem_ld16(S.d, v);
-      if (live && save_o) save_o[s] = make_float4(v[0], v[1], v[2], 0.0f);
+      if (kSave && live) save_o[s] = make_float4(v[0], v[1], v[2], 0.0f);
       if (live) {
         float4 p = xs;
         if (p.w > 0.0f) {
@@ -872,52 +884,80 @@ __global__ void __launch_bounds__(128) hash_bwd_kernel(cf_hashgrid_desc D, const
 // transposed DeformNet weights as B operands: W5^T (128x16), W4^T, W3^T, W2^T
 // (128x128), W1x^T (32x128; the hash-feature columns of layer 1)
 constexpr int kDeformWT = (128 * 16 + 3 * 128 * 128 + 32 * 128) * 2;  // 110,592 B
-constexpr int kDBwdSlots = 2;
-constexpr int kDBwdA = 128 * 128 * 2;
+// The backward uses the forward kernel's slot machinery (TsSlot / ts_layer):
+// 3 slots of 8 warps, two with dL/dpre in TMEM (TS-form MMAs) and one in smem.
+constexpr int kDBwdSlots = kDeformSlots;
 
-// dL/dpre of a 128-wide ReLU layer: D (= dL/dact) * [act > 0] from the saved
-// activation row -> A buffer (K = 128) and the saved dpre row
-__device__ __forceinline__ void bwd_mask128(Slot& S, const __half* act, __half* dpre) {
+// dL/dpre of a 128-wide ReLU layer for this warp's 64 columns: D (= dL/dact) *
+// [pre > 0] (the forward's saved ReLU bits, bit j = column 64*half + j) -> fp16
+// A operand (TMEM or smem) and the sample's dpre row (or null)
+__device__ __forceinline__ void ts_bwd_mask128(const TsSlot& S, uint64_t mask, __half* dpre) {
 #pragma unroll
-  for (int c0 = 0; c0 < 128; c0 += 32) {
-    float v[32];
-    tc::tmem_ld32(S.tmem_row + (uint32_t)c0, v);
-    if (act) {
-      const uint4* a = reinterpret_cast<const uint4*>(act + c0);
+  for (int c = 0; c < 2; ++c) {
+    const int col = 64 * S.half + 32 * c;
+    const uint32_t m = (uint32_t)(mask >> (32 * c));
+    float r[32];
+    tc::tmem_ld32(S.d + (uint32_t)col, r);
+    uint32_t h[16];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint4 u = a[q];
-        const __half2* hh = reinterpret_cast<const __half2*>(&u);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float2 f = __half22float2(hh[i]);
-          if (!(f.x > 0.0f)) v[8 * q + 2 * i] = 0.0f;
-          if (!(f.y > 0.0f)) v[8 * q + 2 * i + 1] = 0.0f;
-        }
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = 0.0f;
+    for (int i = 0; i < 16; ++i) {
+      const float x0 = (m >> (2 * i)) & 1u ? r[2 * i] : 0.0f;
+      const float x1 = (m >> (2 * i + 1)) & 1u ? r[2 * i + 1] : 0.0f;
+      const __half2 o = __floats2half2_rn(x0, x1);
+      h[i] = *reinterpret_cast<const uint32_t*>(&o);
     }
+    if (S.abuf) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) tc::st_row8(S.abuf, S.r, c0 + 8 * q, 128, v + 8 * q);
-    if (dpre) store_row_f16(dpre + c0, 0, 32, v);
+      for (int q = 0; q < 4; ++q)
+        *reinterpret_cast<uint4*>(S.abuf + tc::core_offset(S.r, col + 8 * q, 128)) =
+            make_uint4(h[4 * q], h[4 * q + 1], h[4 * q + 2], h[4 * q + 3]);
+    } else {
+      tc::tmem_st16(S.a + (uint32_t)(col / 2), h);
+    }
+    if (dpre) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        reinterpret_cast<uint4*>(dpre + col)[q] = make_uint4(h[4 * q], h[4 * q + 1], h[4 * q + 2], h[4 * q + 3]);
+    }
   }
 }
 
 // Per 128-sample tile: d_o from dL/dxc, then the dX chain through layers 5..1
 // with the saved forward activations (ReLU masks), saving d_o and dpre1..4
 // (fp16) for the weight-gradient GEMMs and writing dL/d(deform features).
-__global__ void __launch_bounds__(kDBwdSlots* kSlotThreads, 1)
+__global__ void __launch_bounds__(kDBwdSlots* kDeformSlotThreads, 1)
     deform_bwd_kernel(const uint8_t* __restrict__ wtblob, float delta_scale, float inv_side,
-                      const float4* __restrict__ xu, const float4* __restrict__ dxc, const __half* __restrict__ save_h,
-                      const float4* __restrict__ save_o, const int* __restrict__ count, int64_t capacity,
+                      const float4* __restrict__ xu, const float4* __restrict__ dxc,
+                      const uint2* __restrict__ save_mask, const float4* __restrict__ save_o, const int* __restrict__ count, int64_t capacity,
                       __half* __restrict__ d_o_out, __half* __restrict__ dpre, float* __restrict__ d_dfeat) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t mbar[kDBwdSlots];
   __shared__ uint32_t tmem_base;
-  slots_setup<kDBwdSlots, 256>(wtblob, kDeformWT, smem, mbar, &tmem_base);
-  Slot S = make_slot<kDBwdSlots, 128, kDBwdA>(smem, kDeformWT, mbar, tmem_base);
+  const int tid = threadIdx.x, warp = tid / 32;
+  for (int i = tid * 16; i < kDeformWT; i += blockDim.x * 16)
+    *reinterpret_cast<uint4*>(smem + i) = *reinterpret_cast<const uint4*>(wtblob + i);
+  if (tid == 0) {
+    for (int q = 0; q < kDBwdSlots; ++q) tc::bar_init(&mbar[q], 1);
+    tc::bar_fence_init();
+  }
+  if (warp == 0) tc::tmem_alloc<512>(&tmem_base);
+  tc::fence_async_smem();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  TsSlot S;
+  S.slot = tid / kDeformSlotThreads;
+  const int ws = warp % (kDeformSlotThreads / 32);
+  S.half = ws / 4;
+  S.r = (ws % 4) * 32 + (tid & 31);
+  S.bar = &mbar[S.slot];
+  S.phase = 0;
+  const uint32_t lane_q = (uint32_t)((ws % 4) * 32) << 16;
+  S.d0 = tmem_base + (uint32_t)(S.slot * 192);
+  S.a0 = S.d0 + 128u;
+  S.abuf = S.slot == 2 ? smem + kDeformWT : nullptr;
+  S.d = S.d0 + lane_q;
+  S.a = S.a0 + lane_q;
   constexpr int t5 = 0, t4 = 128 * 16 * 2, t3 = t4 + 128 * 128 * 2, t2 = t3 + 128 * 128 * 2, t1 = t2 + 128 * 128 * 2;
   const int64_t n = min((int64_t)*count, capacity);
   const int64_t n_tiles = (n + 127) / 128;
@@ -925,45 +965,69 @@ __global__ void __launch_bounds__(kDBwdSlots* kSlotThreads, 1)
        tile += (int64_t)gridDim.x * kDBwdSlots) {
     const int64_t s = tile * 128 + S.r;
     const bool live = s < n;
-    const bool valid = live && xu[s].w > 0.0f;
-    // xc = xu + delta_scale * tanh(o) * inv_side  =>  dL/do = dL/dxc * delta_scale * inv_side * (1 - tanh^2 o)
-    float d_o[16];
+    if (S.half == 0) {
+      // xc = xu + delta_scale * tanh(o) * inv_side => dL/do = dL/dxc delta_scale inv_side (1 - tanh^2 o)
+      float d_o[16];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) d_o[i] = 0.0f;
-    if (valid) {
-      const float4 g = dxc[s], o = save_o[s];
-      const float gg[3] = {g.x, g.y, g.z}, oo[3] = {o.x, o.y, o.z};
+      for (int i = 0; i < 16; ++i) d_o[i] = 0.0f;
+      if (live && xu[s].w > 0.0f) {
+        const float4 g = dxc[s], o = save_o[s];
+        const float gg[3] = {g.x, g.y, g.z}, oo[3] = {o.x, o.y, o.z};
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const float th = tanhf(oo[c]);
-        d_o[c] = gg[c] * delta_scale * inv_side * (1.0f - th * th);
+        for (int c = 0; c < 3; ++c) {
+          const float th = tanhf(oo[c]);
+          d_o[c] = gg[c] * delta_scale * inv_side * (1.0f - th * th);
+        }
+      }
+      uint32_t h[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const __half2 o = __floats2half2_rn(d_o[2 * i], d_o[2 * i + 1]);
+        h[i] = *reinterpret_cast<const uint32_t*>(&o);
+      }
+      if (S.abuf) {
+        *reinterpret_cast<uint4*>(S.abuf + tc::core_offset(S.r, 0, 16)) = make_uint4(h[0], h[1], h[2], h[3]);
+        *reinterpret_cast<uint4*>(S.abuf + tc::core_offset(S.r, 8, 16)) = make_uint4(h[4], h[5], h[6], h[7]);
+      } else {
+        tc::tmem_st8(S.a, h);
+      }
+      if (live) {
+        reinterpret_cast<uint4*>(d_o_out + s * 16)[0] = make_uint4(h[0], h[1], h[2], h[3]);
+        reinterpret_cast<uint4*>(d_o_out + s * 16)[1] = make_uint4(h[4], h[5], h[6], h[7]);
       }
     }
-    tc::st_row8(S.abuf, S.r, 0, 16, d_o);
-    tc::st_row8(S.abuf, S.r, 8, 16, d_o + 8);
-    if (live) store_row_f16(d_o_out, s, 16, d_o);
-    const __half* h = live ? save_h + s * 512 : nullptr;
-    __half* dp = live ? dpre + s * 512 : nullptr;
-    run_layer(S, t5, 16, 128);  // dh4 = d_o . W5
-    bwd_mask128(S, h ? h + 384 : nullptr, dp ? dp + 384 : nullptr);
-    run_layer(S, t4, 128, 128);  // dh3 = dpre4 . W4
-    bwd_mask128(S, h ? h + 256 : nullptr, dp ? dp + 256 : nullptr);
-    run_layer(S, t3, 128, 128);  // dh2 = dpre3 . W3
-    bwd_mask128(S, h ? h + 128 : nullptr, dp ? dp + 128 : nullptr);
-    run_layer(S, t2, 128, 128);  // dh1 = dpre2 . W2
-    bwd_mask128(S, h, dp);
-    run_layer(S, t1, 128, 32);  // dL/dfeat = dpre1 . W1x
-    float dfx[32];
-    tc::tmem_ld32(S.tmem_row, dfx);
+    // the 4 layers' ReLU bits for this half, fetched once per tile
+    uint64_t mk[4] = {0, 0, 0, 0};
     if (live) {
-      float4* d = reinterpret_cast<float4*>(d_dfeat + s * 32);
 #pragma unroll
-      for (int q = 0; q < 8; ++q) d[q] = make_float4(dfx[4 * q], dfx[4 * q + 1], dfx[4 * q + 2], dfx[4 * q + 3]);
+      for (int l = 0; l < 4; ++l) {
+        const uint2 v = save_mask[s * 8 + 2 * l + S.half];
+        mk[l] = (uint64_t)v.x | (uint64_t)v.y << 32;
+      }
+    }
+    __half* dp = live ? dpre + s * 512 : nullptr;
+    ts_layer(S, smem + t5, 16, 128);  // dh4 = d_o . W5
+    ts_bwd_mask128(S, mk[3], dp ? dp + 384 : nullptr);
+    ts_layer(S, smem + t4, 128, 128);  // dh3 = dpre4 . W4
+    ts_bwd_mask128(S, mk[2], dp ? dp + 256 : nullptr);
+    ts_layer(S, smem + t3, 128, 128);  // dh2 = dpre3 . W3
+    ts_bwd_mask128(S, mk[1], dp ? dp + 128 : nullptr);
+    ts_layer(S, smem + t2, 128, 128);  // dh1 = dpre2 . W2
+    ts_bwd_mask128(S, mk[0], dp);
+    ts_layer(S, smem + t1, 128, 32);  // dL/dfeat = dpre1 . W1x
+    if (S.half == 0) {
+      float dfx[32];
+      tc::tmem_ld32(S.d, dfx);
+      if (live) {
+        float4* d = reinterpret_cast<float4*>(d_dfeat + s * 32);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) d[q] = make_float4(dfx[4 * q], dfx[4 * q + 1], dfx[4 * q + 2], dfx[4 * q + 3]);
+      }
     }
   }
   tc::fence_before();
   __syncthreads();
-  if (threadIdx.x / 32 == 0) tc::tmem_free<256>(tmem_base);
+  if (warp == 0) tc::tmem_free<512>(tmem_base);
 }
 
 // Canonical hash backward that also returns the spatial gradient of the
@@ -1118,16 +1182,17 @@ int cf_field_hash_backward(const cf_field_desc* FD, const cf_march_out* S, const
 
 int cf_deform_backward(const cf_field_desc* FD, const uint8_t* wt_blob, const cf_march_out* S, const float* xu,
                        const float* dxc, const cf_deform_bwd_io* io, void* stream) {
-  if (!FD || !FD->has_deform || !wt_blob || !S || !xu || !dxc || !io || !io->save_h || !io->save_o || !io->d_o ||
+  if (!FD || !FD->has_deform || !wt_blob || !S || !xu || !dxc || !io || !io->save_mask || !io->save_o || !io->d_o ||
       !io->dpre || !io->d_dfeat)
     return cf::fail(CF_E_BAD_ARG, "cf_deform_backward: bad args");
   const int64_t cap = S->capacity;
   if (cap == 0) return CF_OK;
-  const int smem = kDeformWT + kDBwdSlots * kDBwdA;
+  const int smem = kDeformWT + kDeformA;  // weights + the SS slot's A buffer
   CF_CHECK_CUDA(cudaFuncSetAttribute(deform_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  deform_bwd_kernel<<<persistent_grid(cap, kDBwdSlots), kDBwdSlots * kSlotThreads, smem, cf::as_stream(stream)>>>(
+  deform_bwd_kernel<<<persistent_grid(cap, kDBwdSlots), kDBwdSlots * kDeformSlotThreads, smem,
+                      cf::as_stream(stream)>>>(
       wt_blob, FD->delta_scale, FD->inv_side, reinterpret_cast<const float4*>(xu),
-      reinterpret_cast<const float4*>(dxc), reinterpret_cast<const __half*>(io->save_h),
+      reinterpret_cast<const float4*>(dxc), reinterpret_cast<const uint2*>(io->save_mask),
       reinterpret_cast<const float4*>(io->save_o), S->counters, cap, reinterpret_cast<__half*>(io->d_o),
       reinterpret_cast<__half*>(io->dpre), io->d_dfeat);
   return cf::check_launch("cf_deform_backward");
@@ -1169,9 +1234,13 @@ int cf_field_stage(const cf_field_desc* FD, const cf_march_out* S, const double*
       cf::launch_pdl(hash_f16_kernel<4, 8, 2, 1, __half>, hgrid, 128, 0, st, FD->dgrid, reinterpret_cast<const __half*>(FD->dtable), xu, S->counters, cap, dfeat);
     if (run(1)) {
       const int smem = kDeformW + kDeformA;
-      CF_CHECK_CUDA(cudaFuncSetAttribute(deform_mlp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      cf::launch_pdl(deform_mlp_kernel, persistent_grid(cap, kDeformSlots), kDeformSlots * kDeformSlotThreads, smem, st, FD->wblob, FD->dbias, FD->delta_scale, FD->inv_side, xu, dfeat, S->counters, cap, xc,
-          reinterpret_cast<__half*>(FD->save_h), reinterpret_cast<float4*>(FD->save_o));
+      const bool save = FD->save_h != nullptr;
+      if (save && (!FD->save_o || !FD->save_mask))
+        return cf::fail(CF_E_BAD_ARG, "cf_field_forward: save_h needs save_o and save_mask");
+      auto kern = save ? deform_mlp_kernel<true> : deform_mlp_kernel<false>;
+      CF_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      cf::launch_pdl(kern, persistent_grid(cap, kDeformSlots), kDeformSlots * kDeformSlotThreads, smem, st, FD->wblob, FD->dbias, FD->delta_scale, FD->inv_side, xu, dfeat, S->counters, cap, xc,
+          reinterpret_cast<__half*>(FD->save_h), reinterpret_cast<float4*>(FD->save_o), FD->save_mask);
     }
     xcan = xc;
   }

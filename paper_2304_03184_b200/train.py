@@ -179,12 +179,14 @@ class _DeformBuffers:
     def __init__(self, cap, device):
         self.save_h = torch.empty((cap, 512), dtype=torch.float16, device=device)
         self.save_o = torch.empty((cap, 4), dtype=torch.float32, device=device)
+        self.save_mask = torch.empty((cap, 16), dtype=torch.int32, device=device)
         self.d_o = torch.empty((cap, 16), dtype=torch.float16, device=device)
         self.dpre = torch.empty((cap, 512), dtype=torch.float16, device=device)
         self.d_dfeat = torch.empty((cap, 32), dtype=torch.float32, device=device)
         self.dxc = torch.empty((cap, 4), dtype=torch.float32, device=device)
         self.colsum = torch.empty(128, dtype=torch.float32, device=device)
-        self.io = _lib.DeformBwdIO(self.save_h.data_ptr(), self.save_o.data_ptr(), self.d_o.data_ptr(),
+        self.io = _lib.DeformBwdIO(self.save_h.data_ptr(), self.save_o.data_ptr(), self.save_mask.data_ptr(),
+                                   self.d_o.data_ptr(),
                                    self.dpre.data_ptr(), self.d_dfeat.data_ptr())
 
 
@@ -268,6 +270,7 @@ class Trainer:
                 desc.dbias = st["dbias"].data_ptr()
                 desc.save_h = st["dbufs"].save_h.data_ptr()
                 desc.save_o = st["dbufs"].save_o.data_ptr()
+                desc.save_mask = st["dbufs"].save_mask.data_ptr()
         else:
             _lib.call("cf_object_canon", _lib.byref(M), self.dirs.data_ptr(), _lib.byref(buf.mo), buf.xu.data_ptr(), s)
             desc = r.odesc
@@ -296,12 +299,17 @@ class Trainer:
         # The GEMM row count is rounded up to one of 8 sizes per power of two (within
         # the buffers) so that frames with different sample counts reuse cuBLASLt's
         # cached plans (a new shape costs ~4 ms of host-side heuristics); the padding
-        # rows of the dY operands are zeroed, so they add nothing.
+        # rows of both operands are zeroed, so they add nothing (zero dY alone is not
+        # enough: stale X rows may hold inf/NaN bit patterns, and 0 * NaN = NaN).
         q = 1 << max(n.bit_length() - 4, 10)
-        n_pad = min(-(-n // q) * q, buf.mo.capacity)
-        dys = [bwd.d_o, bwd.dc2, bwd.dc1, bwd.dg, bwd.dh1] + ([db.d_o, db.dpre] if dp is not None else [])
-        for t in dys:
-            t[n:n_pad].zero_()
+        cap = buf.mo.capacity
+        n_pad = min(-(-n // q) * q, cap)
+        pads = [bwd.d_o, bwd.dc2, bwd.dc1, bwd.dg, bwd.dh1, bwd.c2, bwd.c1, bwd.cin, bwd.h1]
+        pads += [scratch[n * 64: n_pad * 64]]  # colour-MLP input rows (x0 below)
+        if dp is not None:
+            pads += [db.d_o, db.dpre, db.save_h, scratch[cap * 64 + n * 64: cap * 64 + n_pad * 64]]
+        for t in pads:
+            (t[n:n_pad] if t.dim() == 2 else t).zero_()
         n, n_true = n_pad, n
         x0 = scratch[: n * 64].view(torch.float16).view(n, 32)
         # fp16 operands on the tensor cores, fp32 accumulation (reduced-precision
@@ -315,7 +323,6 @@ class Trainer:
         G["G2"] += (f(bwd.dg).t() @ f(bwd.h1)).float()
         G["G1"] += (f(bwd.dh1).t() @ x0).float()
         if dp is not None:
-            cap = buf.mo.capacity
             xd = scratch[cap * 64: cap * 64 + n * 64].view(torch.float16).view(n, 32)  # deform-grid features
             H, DP, DO = db.save_h[:n], db.dpre[:n], db.d_o[:n]
             GD = dp.G
