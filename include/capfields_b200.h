@@ -13,6 +13,7 @@
  *   CF_E_BAD_ARG         -> ValueError                             (knnfield.py:56-57,134-135)
  *   CF_E_DEGENERATE      -> capfields.transforms.DegenerateWeightsError (transforms.py:15)
  *   CF_E_CUDA            -> RuntimeError (device fault / launch failure)
+ *   CF_E_FORMAT          -> capfields.records.RecordFormatError      (records.py:24)
  * cf_last_error() returns a thread-local message for the last non-zero status.
  *
  * Reference interfaces replaced (the reference has no FFI; these are the Python
@@ -47,6 +48,7 @@ extern "C" {
 #define CF_E_DUPLICATE_FRAME 3
 #define CF_E_DEGENERATE 4
 #define CF_E_CUDA 5
+#define CF_E_FORMAT 6
 
 int cf_version(void);
 const char* cf_last_error(void);
@@ -401,6 +403,37 @@ int cf_adam(float* p, const float* g, float* m, float* v, int64_t n, float lr, f
 int cf_colsum128_f16(const void* x, int64_t n, int ld, float* out, void* stream);
 /* fp32 (n x k) row-major weight -> fp16 UMMA canonical K-major blob (n, k padded to 16) */
 int cf_pack_weight(const float* w, int n, int k, uint8_t* blob, void* stream);
+
+/* ------------------------------------------------- motion-prior ingestion */
+/* CFMP v1 motion-prior stream (records.py:98-147): "CFMP", u32 version, u32
+ * n_nodes, u32 n_theta, then per frame i64 frame_id and four length-prefixed
+ * float64 arrays (dqs n_nodes*8, theta n_theta, rotation 9, translation 3).
+ * The codec is host code (no GPU needed); the arrays it fills are caller-owned
+ * (pin them for one upload into the device LUT). */
+typedef struct cf_mp_info {
+  int64_t n_frames;
+  int32_t n_nodes;
+  int32_t n_theta;
+  int64_t bytes;
+} cf_mp_info;
+/* validate a stream and count its frames (load_motion_priors, records.py:128-147);
+ * CF_E_FORMAT on a bad magic / version / array length or a truncated frame */
+int cf_mp_scan(const char* path, cf_mp_info* info);
+/* decode frames [first, first + count) into host arrays: frame_ids (count) int64,
+ * dqs (count, n_nodes, 8), theta (count, n_theta), rot (count, 3, 3), trans (count, 3) float64 */
+int cf_mp_read(const char* path, int64_t first, int64_t count, int64_t* frame_ids, double* dqs, double* theta,
+               double* rot, double* trans);
+/* encode (MotionPriorWriter, records.py:98-120): create (header + frames) or append
+ * `count` frames; appending checks the stream's n_nodes / n_theta */
+int cf_mp_write(const char* path, int create, int32_t n_nodes, int32_t n_theta, int64_t count,
+                const int64_t* frame_ids, const double* dqs, const double* theta, const double* rot,
+                const double* trans);
+/* per-frame skeleton FK on the device (skinning_transforms, skeleton.py:121-139):
+ * theta (n_frames, 3J) device float64 -> A (n_frames, J, 4, 4) device float64,
+ * A_j = G_j(theta) G_j(0)^-1. parents (J) int32 and offsets (J, 3) float64 are HOST
+ * arrays (parents[j] < j, -1 = root), J <= 64. */
+int cf_skinning_transforms(const double* theta, int64_t n_frames, const int32_t* parents, const double* offsets,
+                           int32_t n_joints, double* A, void* stream);
 
 #ifdef __cplusplus
 }

@@ -11,7 +11,7 @@ import threading
 
 import torch
 
-from .errors import DegenerateWeightsError, OutOfSupportError
+from .errors import DegenerateWeightsError, OutOfSupportError, RecordFormatError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", "libcapfields_b200.so")
@@ -22,6 +22,7 @@ CF_E_OUT_OF_SUPPORT = 2
 CF_E_DUPLICATE_FRAME = 3
 CF_E_DEGENERATE = 4
 CF_E_CUDA = 5
+CF_E_FORMAT = 6
 
 CF_WARP_BACKWARD = 0
 CF_WARP_FORWARD = 1
@@ -85,6 +86,11 @@ class FieldDesc(ctypes.Structure):
                 ("w_bytes", ctypes.c_int), ("dbias", ctypes.c_void_p), ("delta_scale", ctypes.c_float),
                 ("inv_side", ctypes.c_float), ("save_h", ctypes.c_void_p), ("save_o", ctypes.c_void_p),
                 ("save_mask", ctypes.c_void_p)]
+
+
+class MpInfo(ctypes.Structure):
+    _fields_ = [("n_frames", ctypes.c_int64), ("n_nodes", ctypes.c_int32), ("n_theta", ctypes.c_int32),
+                ("bytes", ctypes.c_int64)]
 
 
 class DeformBwdIO(ctypes.Structure):
@@ -152,6 +158,10 @@ _SIGS = {
                 ctypes.c_float, _p],
     "cf_pack_weight": [_p, _i32, _i32, _p, _p],
     "cf_colsum128_f16": [_p, _i64, _i32, _p, _p],
+    "cf_mp_scan": [ctypes.c_char_p, _P(MpInfo)],
+    "cf_mp_read": [ctypes.c_char_p, _i64, _i64, _p, _p, _p, _p, _p],
+    "cf_mp_write": [ctypes.c_char_p, _i32, _i32, _i32, _i64, _p, _p, _p, _p, _p],
+    "cf_skinning_transforms": [_p, _i64, _p, _p, _i32, _p, _p],
 }
 
 _lock = threading.Lock()
@@ -206,6 +216,8 @@ def check(rc: int, what: str = "") -> None:
         raise OutOfSupportError(text)
     if rc == CF_E_DEGENERATE:
         raise DegenerateWeightsError(text)
+    if rc == CF_E_FORMAT:
+        raise RecordFormatError(msg)
     if rc in (CF_E_BAD_ARG, CF_E_DUPLICATE_FRAME):
         raise ValueError(msg)
     raise RuntimeError(text)

@@ -2,6 +2,7 @@
 
 OutOfSupportError      capfields/edgraph.py:27
 DegenerateWeightsError capfields/transforms.py:15
+RecordFormatError      capfields/records.py:24
 """
 from __future__ import annotations
 
@@ -16,5 +17,12 @@ except Exception:  # the reference is not installed on the GPU box
     class DegenerateWeightsError(ValueError):
         """A blend received no positive weight."""
 
+try:
+    from capfields.records import RecordFormatError  # type: ignore
+except Exception:
 
-__all__ = ["OutOfSupportError", "DegenerateWeightsError"]
+    class RecordFormatError(ValueError):
+        """A record file with a bad magic, version or payload."""
+
+
+__all__ = ["OutOfSupportError", "DegenerateWeightsError", "RecordFormatError"]
