@@ -781,45 +781,45 @@ __global__ void __launch_bounds__(kBwdSlots* kSlotThreads, 1)
   if (threadIdx.x / 32 == 0) tc::tmem_free<256>(tmem_base);
 }
 
-// grad[idx] += v for the valid lanes of a warp, pre-summing lanes that hit the
-// same entry: on the coarse levels nearly every sample of a warp (samples of one
-// or two rays, cells of several cm) lands in the same few cells, and the plain
-// atomics serialised on a few hot L2 slices (lts throughput max 89 % vs avg 38 %).
-// Up to 3 rounds take the group of the lowest pending lane (warp butterfly sum,
-// one atomic by the leader); whatever is left issues its own atomic.
+// Scatter-add of one level's 8 corner contributions v[k][0..F) at idx[k] (lanes
+// with !valid add nothing). Consecutive lanes are consecutive samples, mostly of one
+// ray, so at the coarse levels runs of lanes share a cell: each run is summed in
+// registers first (segmented suffix sums over shuffles, log2(longest run) steps) and
+// its head issues the 8 vector atomics. A level whose lanes all sit in distinct
+// cells (the fine levels) costs one key compare and goes straight to the atomics.
 template <int F>
-__device__ __forceinline__ void warp_scatter_add(bool valid, uint32_t idx, float* __restrict__ base, const float* v) {
+__device__ __forceinline__ void level_scatter(bool valid, const uint32_t* gi, const uint32_t* idx, float (*v)[F],
+                                              float* __restrict__ base) {
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
-  unsigned todo = __ballot_sync(FULL, valid);
-  for (int round = 0; round < 3 && todo; ++round) {
-    const int leader = __ffs(todo) - 1;
-    const uint32_t lidx = __shfl_sync(FULL, idx, leader);
-    const bool mine = ((todo >> lane) & 1u) && idx == lidx;
-    const unsigned grp = __ballot_sync(FULL, mine);
-    float sum[F];
+  const uint32_t klo = gi[0] | (gi[1] << 16), khi = gi[2];
+  const uint32_t plo = __shfl_up_sync(FULL, klo, 1), phi = __shfl_up_sync(FULL, khi, 1);
+  const int pvalid = __shfl_up_sync(FULL, (int)valid, 1);
+  const bool head = lane == 0 || !valid || !pvalid || plo != klo || phi != khi;
+  const unsigned heads = __ballot_sync(FULL, head);
+  if (heads != FULL) {
+    for (int o = 1; o < 32; o <<= 1) {
+      // lane + o lies in this lane's run iff no run starts in (lane, lane + o]
+      const bool ok = lane + o < 32 && ((heads >> (lane + 1)) & ((1u << o) - 1u)) == 0u;
+      if (!__any_sync(FULL, ok)) break;
 #pragma unroll
-    for (int f = 0; f < F; ++f) {
-      sum[f] = mine ? v[f] : 0.0f;
+      for (int k = 0; k < 8; ++k)
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) sum[f] += __shfl_xor_sync(FULL, sum[f], o);
+        for (int f = 0; f < F; ++f) {
+          const float t = __shfl_down_sync(FULL, v[k][f], o);
+          if (ok) v[k][f] += t;
+        }
     }
-    if (lane == leader) {
-      float* dst = base + (int64_t)lidx * F;
-      if constexpr (F == 2) atomicAdd(reinterpret_cast<float2*>(dst), make_float2(sum[0], sum[1]));
-      else atomicAdd(reinterpret_cast<float4*>(dst), make_float4(sum[0], sum[1], sum[2], sum[3]));
-    }
-    todo &= ~grp;
   }
-  if ((todo >> lane) & 1u) {
-    float* dst = base + (int64_t)idx * F;
-    if constexpr (F == 2) atomicAdd(reinterpret_cast<float2*>(dst), make_float2(v[0], v[1]));
-    else atomicAdd(reinterpret_cast<float4*>(dst), make_float4(v[0], v[1], v[2], v[3]));
+  if (valid && head) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      float* dst = base + (int64_t)idx[k] * F;
+      if constexpr (F == 2) atomicAdd(reinterpret_cast<float2*>(dst), make_float2(v[k][0], v[k][1]));
+      else atomicAdd(reinterpret_cast<float4*>(dst), make_float4(v[k][0], v[k][1], v[k][2], v[k][3]));
+    }
   }
 }
-
-// coarse levels (cells of >= 1/32 of the cube) get the warp-aggregated scatter
-constexpr int kAggMaxRes = 32;
 
 // hash backward on the compacted samples: grad[entry] += w_corner * dfeat (fp32 vector atomics)
 template <int F, int L>
@@ -856,25 +856,19 @@ __global__ void __launch_bounds__(128) hash_bwd_kernel(cf_hashgrid_desc D, const
       float gl[F];
 #pragma unroll
       for (int f = 0; f < F; ++f) gl[f] = g[l * F + f];
-      float* base = grad + D.offset[l] * F;
+      uint32_t idx[8];
+      float v[8][F];
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const uint32_t cx = gi[0] + (k & 1), cy = gi[1] + ((k >> 1) & 1), cz = gi[2] + ((k >> 2) & 1);
-        const uint32_t idx = dense ? (cx + cy * stride + cz * stride * stride)
-                                   : ((cx ^ (cy * 2654435761u) ^ (cz * 805459861u)) & mask);
+        idx[k] = dense ? (cx + cy * stride + cz * stride * stride)
+                       : ((cx ^ (cy * 2654435761u) ^ (cz * 805459861u)) & mask);
         const float w = f_mul(f_mul((k & 1) ? fr[0] : f_sub(1.f, fr[0]), (k & 2) ? fr[1] : f_sub(1.f, fr[1])),
                               (k & 4) ? fr[2] : f_sub(1.f, fr[2]));
-        float wv[F];
 #pragma unroll
-        for (int f = 0; f < F; ++f) wv[f] = w * gl[f];
-        if (dense && N <= kAggMaxRes) {
-          warp_scatter_add<F>(valid, idx, base, wv);
-        } else if (valid) {
-          float* dst = base + (int64_t)idx * F;
-          if constexpr (F == 2) atomicAdd(reinterpret_cast<float2*>(dst), make_float2(wv[0], wv[1]));
-          else atomicAdd(reinterpret_cast<float4*>(dst), make_float4(wv[0], wv[1], wv[2], wv[3]));
-        }
+        for (int f = 0; f < F; ++f) v[k][f] = w * gl[f];
       }
+      level_scatter<F>(valid, gi, idx, v, grad + D.offset[l] * F);
     }
   }
 }
@@ -1078,30 +1072,23 @@ __global__ void __launch_bounds__(128) hash_bwd_dx_kernel(cf_hashgrid_desc D, co
       float gl[F];
 #pragma unroll
       for (int f = 0; f < F; ++f) gl[f] = g[l * F + f];
-      float* base = grad + D.offset[l] * F;
       const float* tb = table + D.offset[l] * F;  // the values the forward interpolated
       float dl[3] = {0.f, 0.f, 0.f};
+      uint32_t idx[8];
+      float v[8][F];
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const uint32_t cx = gi[0] + (k & 1), cy = gi[1] + ((k >> 1) & 1), cz = gi[2] + ((k >> 2) & 1);
-        const uint32_t idx = dense ? (cx + cy * stride + cz * stride * stride)
-                                   : ((cx ^ (cy * 2654435761u) ^ (cz * 805459861u)) & mask);
+        idx[k] = dense ? (cx + cy * stride + cz * stride * stride)
+                       : ((cx ^ (cy * 2654435761u) ^ (cz * 805459861u)) & mask);
         const float wx = (k & 1) ? fr[0] : f_sub(1.f, fr[0]);
         const float wy = (k & 2) ? fr[1] : f_sub(1.f, fr[1]);
         const float wz = (k & 4) ? fr[2] : f_sub(1.f, fr[2]);
         const float w = f_mul(f_mul(wx, wy), wz);
-        float wv[F];
 #pragma unroll
-        for (int f = 0; f < F; ++f) wv[f] = w * gl[f];
-        if (dense && N <= kAggMaxRes) {
-          warp_scatter_add<F>(valid, idx, base, wv);
-        } else if (valid) {
-          float* dst = base + (int64_t)idx * F;
-          if constexpr (F == 2) atomicAdd(reinterpret_cast<float2*>(dst), make_float2(wv[0], wv[1]));
-          else atomicAdd(reinterpret_cast<float4*>(dst), make_float4(wv[0], wv[1], wv[2], wv[3]));
-        }
+        for (int f = 0; f < F; ++f) v[k][f] = w * gl[f];
         float tv[F];
-        ld_entry<F>(tb, idx, tv);
+        ld_entry<F>(tb, idx[k], tv);
         float a = 0.f;  // dfeat_l . t_k
 #pragma unroll
         for (int f = 0; f < F; ++f) a += gl[f] * tv[f];
@@ -1109,6 +1096,7 @@ __global__ void __launch_bounds__(128) hash_bwd_dx_kernel(cf_hashgrid_desc D, co
         dl[1] += a * ((k & 2) ? 1.f : -1.f) * wx * wz;
         dl[2] += a * ((k & 4) ? 1.f : -1.f) * wx * wy;
       }
+      level_scatter<F>(valid, gi, idx, v, grad + D.offset[l] * F);
 #pragma unroll
       for (int a = 0; a < 3; ++a) dx[a] += sc * dl[a];
     }
