@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--samples", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--workload", default="render", choices=["render", "train", "knn"],
+    ap.add_argument("--workload", default="render", choices=["render", "train", "knn", "frontend"],
                     help="render = configs[1] (the headline); train = configs[2] key-frame training step; "
                          "knn = configs[3] dense-graph k-NN scaling")
     ap.add_argument("--train-rays", type=int, default=1 << 18)
@@ -666,6 +666,98 @@ def run_knn(args, rank, world, pg):
         print(json.dumps(line))
 
 
+def run_frontend(args, rank, world, pg):
+    """SURVEY §8(f) 2-3, the stages either side of the path: motion-prior ingestion
+    (CFMP decode + one upload + device FK of every frame) and key-frame selection
+    per tracked frame (blur gate on the 512^2 RGB, Eq. 5 visibility of the deformed
+    nodes, Eq. 6 scan + update of a 100-entry pool incl. the decision readback)."""
+    import tempfile
+    import time
+    import torch
+    from oracle import keyframes as okf
+    from paper_2304_03184_b200 import keyframes as kf, records
+    from paper_2304_03184_b200.scene import Scene, SceneConfig
+    sc = Scene(SceneConfig(), seed=0)
+    rng = np.random.default_rng(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    n_nodes, n_frames = 8192, 1000
+    # -- ingestion: a 1000-frame stream of an 8192-node graph (~540 MB)
+    path = os.path.join(tempfile.mkdtemp(), "motions.bin")
+    wr = records.MotionPriorWriter(path, n_nodes, 72)
+    dq = np.zeros((n_nodes, 8))
+    dq[:, 0] = 1.0
+    batch = [records.MotionPrior(f, records.GraphMotion(f, dq), records.SkeletonPose(None, sc.theta(f % 10)),
+                                 records.Se3()) for f in range(100)]
+    for rep in range(n_frames // 100):
+        for i, b in enumerate(batch):
+            b.frame_id = b.graph_motion.frame_id = rep * 100 + i
+        wr.append_batch(batch)
+    records.MotionPriorStream(path)  # warm (page cache, pinned pool)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    st = records.MotionPriorStream(path)
+    torch.cuda.synchronize()
+    ingest_s = time.perf_counter() - t0
+    th = st.theta
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    records.skinning_transforms(th)
+    e0.record()
+    for _ in range(10):
+        records.skinning_transforms(th)
+    e1.record()
+    torch.cuda.synchronize()
+    fk_us = e0.elapsed_time(e1) * 100.0  # per call of 1000 frames, us
+    os.remove(path)
+    # -- key-frame selection per tracked frame
+    W = H = 512
+    rgbs = [torch.from_numpy(rng.integers(0, 256, size=(H, W, 3), dtype=np.uint8)).to(dev) for _ in range(4)]
+    depth = torch.from_numpy(rng.uniform(0.5, 4.0, size=(H, W))).to(dev)
+    nodes = torch.from_numpy(sc.template_points[rng.choice(len(sc.template_points), n_nodes, replace=False)]).to(dev)
+    cam = sc.camera
+    pool = kf.KeyFramePool("human", n_nodes=n_nodes, capacity=100, gamma=0.0)  # every frame inserted / evicts
+    thetas = torch.from_numpy(rng.normal(size=(64, 72)) * 0.3)
+
+    def frame(f):
+        b = kf.blur_score(rgbs[f % 4])
+        vis = kf.visibility_bits(nodes, depth, cam)
+        pool.update(kf.FrameSummary(f, thetas[f % 64].numpy(), vis))
+        return b
+
+    for f in range(args.warmup + 100):
+        frame(f)
+    torch.cuda.synchronize()
+    K = max(args.steps, 200)
+    t0 = time.perf_counter()
+    for f in range(K):
+        frame(1000 + f)
+    torch.cuda.synchronize()
+    sel_ms = (time.perf_counter() - t0) * 1e3 / K
+    # CPU oracle of the same per-frame selection work (blur + visibility + 100-entry scan), 1 core
+    rgb_h, depth_h, nodes_h = rgbs[0].cpu().numpy(), depth.cpu().numpy(), nodes.cpu().numpy()
+    Rwc, twc = kf.world_to_cam(cam)
+    ent = [(i, rng.normal(size=72), okf.pack_bits(rng.random(n_nodes) < 0.5)) for i in range(100)]
+    t0 = time.perf_counter()
+    reps = 3
+    for _ in range(reps):
+        okf.blur_score(rgb_h)
+        vb = okf.pack_bits(okf.visibility_map(nodes_h, depth_h, Rwc, twc, cam.fx, cam.fy, cam.cx, cam.cy))
+        ds = [okf.dissim_human(thetas[0].numpy(), vb, 5000, e[1], e[2], e[0]) for e in ent]
+        okf.pool_decision(ds, [e[0] for e in ent])
+    cpu_ms = (time.perf_counter() - t0) * 1e3 / reps
+    line = {"metric": "front-end stages: key-frame selection per tracked frame; motion-prior ingestion",
+            "value": 1e3 / sel_ms, "unit": "tracked frames/s (selection)", "n_gpus": 1, "higher_is_better": True,
+            "ms_per_frame_selection": sel_ms, "dtype": "u8 / f64 / int",
+            "data": "synthetic (random 512^2 RGB and depth, 8192 template nodes, 1000-frame CFMP stream)",
+            "ingest": {"frames": n_frames, "n_nodes": n_nodes, "stream_bytes": int(st.dqs.numel() * 8 + n_frames * 700),
+                       "decode_upload_fk_s": ingest_s, "fk_us_per_1000_frames": fk_us},
+            "cpu_baseline": {"value": 1e3 / cpu_ms, "unit": "tracked frames/s", "cores": 1, "kind": "port",
+                             "sample": "oracle blur + visibility + 100-entry Eq. 6 scan, 3 frames"},
+            "config": {"workload": "SURVEY 8(f) 2-3 front-end stages; selection = blur(512^2) + visibility(8192 "
+                                   "nodes) + pool scan/update (100 entries, decision readback each frame)"}}
+    if rank == 0:
+        print(json.dumps(line))
+
+
 def main():
     args = parse()
     rank, world, local, pg = dist_setup(args.gpus)
@@ -675,6 +767,8 @@ def main():
         run_train(args, rank, world, pg)
     elif args.workload == "knn":
         run_knn(args, rank, world, pg)
+    elif args.workload == "frontend":
+        run_frontend(args, rank, world, pg)
     else:
         run_ours(args, rank, world, pg)
     if pg is not None:

@@ -435,6 +435,54 @@ int cf_mp_write(const char* path, int create, int32_t n_nodes, int32_t n_theta, 
 int cf_skinning_transforms(const double* theta, int64_t n_frames, const int32_t* parents, const double* offsets,
                            int32_t n_joints, double* A, void* stream);
 
+/* ------------------------------------------------------ key-frame selection */
+/* SPEC.md:434-519 (module keyframes), Eq. 5-7.
+ * No reference code exists; the exact evaluation order is frozen in
+ * oracle/keyframes.py and DESIGN.md §3.6. All pointers are device pointers. */
+/* Crete-Roffet blur score of an 8-bit RGB image (H, W, 3), 0 = sharp, 1 = blurred;
+ * sums = 4 x u64 device scratch (s_F / s_V per axis, exact); score = 1 double */
+int cf_blur_score(const uint8_t* rgb, int height, int width, unsigned long long* sums, double* score, void* stream);
+typedef struct cf_vis_camera {
+  double R[9]; /* world -> camera rotation (row-major) */
+  double t[3]; /* world -> camera translation */
+  double fx, fy, cx, cy;
+} cf_vis_camera;
+/* Eq. 5 visibility map of n nodes (n,3) against a depth map (H, W) float64 metres
+ * (0 = invalid): bits (ceil(n/32) words), bit i = node i visible */
+int cf_visibility_map(const double* nodes, int n, const double* depth, int height, int width,
+                      const cf_vis_camera* cam, double eps, uint32_t* bits, void* stream);
+#define CF_POOL_HUMAN 0
+#define CF_POOL_OBJECT 1
+typedef struct cf_pool_desc {
+  int kind;             /* CF_POOL_HUMAN (Eq. 6) or CF_POOL_OBJECT (Eq. 7) */
+  int count, capacity;  /* entries in use, capacity (100) */
+  int n_theta;          /* pose components (72) */
+  int vis_words;        /* visibility words per entry */
+  const double* theta;  /* (capacity, n_theta) */
+  const uint32_t* vis;  /* (capacity, vis_words) */
+  const int64_t* t;     /* (capacity) frame index / insertion time */
+  const double* d;      /* (capacity, 3) object translations */
+  const double* beta_pose; /* (n_theta) Eq. 6 pose weights */
+  double beta_vis, beta_t, beta_d, gamma;
+} cf_pool_desc;
+typedef struct cf_pool_entry {
+  const double* theta;
+  const uint32_t* vis;
+  int64_t t;
+  const double* d;
+} cf_pool_entry;
+typedef struct cf_pool_decision {
+  int insert;        /* 1: push the candidate */
+  int evict;         /* entry to evict first, or -1 */
+  int nearest;       /* least dissimilar entry (ties -> oldest), -1 if empty */
+  int pad;
+  double min_dissim;
+} cf_pool_decision;
+/* dissimilarity of a candidate to every pool entry (dissim: count doubles) and
+ * the pool-update decision, one launch */
+int cf_pool_scan(const cf_pool_desc* pool, const cf_pool_entry* cand, double* dissim, cf_pool_decision* decision,
+                 void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -23,6 +23,8 @@ CF_E_DUPLICATE_FRAME = 3
 CF_E_DEGENERATE = 4
 CF_E_CUDA = 5
 CF_E_FORMAT = 6
+CF_POOL_HUMAN = 0
+CF_POOL_OBJECT = 1
 
 CF_WARP_BACKWARD = 0
 CF_WARP_FORWARD = 1
@@ -91,6 +93,28 @@ class FieldDesc(ctypes.Structure):
 class MpInfo(ctypes.Structure):
     _fields_ = [("n_frames", ctypes.c_int64), ("n_nodes", ctypes.c_int32), ("n_theta", ctypes.c_int32),
                 ("bytes", ctypes.c_int64)]
+
+
+class VisCamera(ctypes.Structure):
+    _fields_ = [("R", ctypes.c_double * 9), ("t", ctypes.c_double * 3), ("fx", ctypes.c_double),
+                ("fy", ctypes.c_double), ("cx", ctypes.c_double), ("cy", ctypes.c_double)]
+
+
+class PoolDesc(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int), ("count", ctypes.c_int), ("capacity", ctypes.c_int),
+                ("n_theta", ctypes.c_int), ("vis_words", ctypes.c_int), ("theta", ctypes.c_void_p),
+                ("vis", ctypes.c_void_p), ("t", ctypes.c_void_p), ("d", ctypes.c_void_p),
+                ("beta_pose", ctypes.c_void_p), ("beta_vis", ctypes.c_double), ("beta_t", ctypes.c_double),
+                ("beta_d", ctypes.c_double), ("gamma", ctypes.c_double)]
+
+
+class PoolEntry(ctypes.Structure):
+    _fields_ = [("theta", ctypes.c_void_p), ("vis", ctypes.c_void_p), ("t", ctypes.c_int64), ("d", ctypes.c_void_p)]
+
+
+class PoolDecision(ctypes.Structure):
+    _fields_ = [("insert", ctypes.c_int), ("evict", ctypes.c_int), ("nearest", ctypes.c_int), ("pad", ctypes.c_int),
+                ("min_dissim", ctypes.c_double)]
 
 
 class DeformBwdIO(ctypes.Structure):
@@ -162,6 +186,9 @@ _SIGS = {
     "cf_mp_read": [ctypes.c_char_p, _i64, _i64, _p, _p, _p, _p, _p],
     "cf_mp_write": [ctypes.c_char_p, _i32, _i32, _i32, _i64, _p, _p, _p, _p, _p],
     "cf_skinning_transforms": [_p, _i64, _p, _p, _i32, _p, _p],
+    "cf_blur_score": [_p, _i32, _i32, _p, _p, _p],
+    "cf_visibility_map": [_p, _i32, _p, _i32, _i32, _P(VisCamera), ctypes.c_double, _p, _p],
+    "cf_pool_scan": [_P(PoolDesc), _P(PoolEntry), _p, _p, _p],
 }
 
 _lock = threading.Lock()
