@@ -744,12 +744,46 @@ def run_frontend(args, rank, world, pg):
         ds = [okf.dissim_human(thetas[0].numpy(), vb, 5000, e[1], e[2], e[0]) for e in ent]
         okf.pool_decision(ds, [e[0] for e in ent])
     cpu_ms = (time.perf_counter() - t0) * 1e3 / reps
+    # -- rigid-object TSDF (tracking front-end): 256^3 volume, 512^2 depth of a sphere
+    from paper_2304_03184_b200.tsdf import TsdfVolume
+
+    class _P:
+        rotation, translation = np.eye(3), np.zeros(3)
+    tcam = type("C", (), dict(fx=560.0, fy=560.0, cx=255.5, cy=255.5, width=512, height=512, pose=_P()))()
+    us, vs = np.meshgrid(np.arange(512.0), np.arange(512.0))
+    dx, dy = (us - 255.5) / 560.0, (vs - 255.5) / 560.0
+    dn = np.sqrt(dx * dx + dy * dy + 1.0)
+    b = 1.3 / dn
+    disc = b * b - (1.3 * 1.3 - 0.3 * 0.3)
+    tdepth = np.where(disc > 0, (b - np.sqrt(np.maximum(disc, 0))) / dn, 0.0)  # camera z of the sphere hit
+    tv = TsdfVolume(256, 0.7 / 256, np.array([-0.35, -0.35, 0.95]))
+    tdev = torch.from_numpy(tdepth).to(dev)
+    for _ in range(3):
+        tv.integrate(tdev, tcam, _P())
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(10):
+        tv.integrate(tdev, tcam, _P())
+    e1.record()
+    torch.cuda.synchronize()
+    integ_ms = e0.elapsed_time(e1) / 10
+    tv.raycast(tcam, _P(), stride=1)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(5):
+        rp, _ = tv.raycast(tcam, _P(), stride=1)
+    e1.record()
+    torch.cuda.synchronize()
+    ray_ms = e0.elapsed_time(e1) / 5
     line = {"metric": "front-end stages: key-frame selection per tracked frame; motion-prior ingestion",
             "value": 1e3 / sel_ms, "unit": "tracked frames/s (selection)", "n_gpus": 1, "higher_is_better": True,
             "ms_per_frame_selection": sel_ms, "dtype": "u8 / f64 / int",
             "data": "synthetic (random 512^2 RGB and depth, 8192 template nodes, 1000-frame CFMP stream)",
             "ingest": {"frames": n_frames, "n_nodes": n_nodes, "stream_bytes": int(st.dqs.numel() * 8 + n_frames * 700),
                        "decode_upload_fk_s": ingest_s, "fk_us_per_1000_frames": fk_us},
+            "tsdf": {"resolution": 256, "integrate_ms": integ_ms, "voxels_per_s": 256 ** 3 / (integ_ms * 1e-3),
+                     "raycast_512x512_ms": ray_ms, "raycast_hits": int(len(rp))},
             "cpu_baseline": {"value": 1e3 / cpu_ms, "unit": "tracked frames/s", "cores": 1, "kind": "port",
                              "sample": "oracle blur + visibility + 100-entry Eq. 6 scan, 3 frames"},
             "config": {"workload": "SURVEY 8(f) 2-3 front-end stages; selection = blur(512^2) + visibility(8192 "

@@ -483,6 +483,45 @@ typedef struct cf_pool_decision {
 int cf_pool_scan(const cf_pool_desc* pool, const cf_pool_entry* cand, double* dissim, cf_pool_decision* decision,
                  void* stream);
 
+/* --------------------------------------------- rigid-object TSDF (tsdf.py) */
+/* SURVEY §8(f) 4 (tracking front-end): TsdfVolume (tsdf.py:17-171) on the device.
+ * tsdf / weight: (r, r, r) float64 device arrays (x-major, as the reference's
+ * meshgrid(indexing="ij")); truncation band `trunc`; weights saturate at 64. */
+typedef struct cf_tsdf_desc {
+  double* tsdf;
+  double* weight;
+  int resolution;
+  int pad;
+  double voxel;
+  double origin[3];
+  double trunc;
+} cf_tsdf_desc;
+typedef struct cf_rigid { /* p' = R p + t, R row-major */
+  double R[9];
+  double t[3];
+} cf_rigid;
+typedef struct cf_pinhole {
+  double fx, fy, cx, cy;
+  int width, height;
+} cf_pinhole;
+/* integrate (tsdf.py:33-61): vol_to_world = the object pose, world_to_cam = the
+ * camera's inverse pose; depth (H, W) float64 metres; mask (H, W) u8 or NULL */
+int cf_tsdf_integrate(const cf_tsdf_desc* V, const double* depth, int height, int width, const uint8_t* mask,
+                      const cf_rigid* vol_to_world, const cf_rigid* world_to_cam, const cf_pinhole* cam, void* stream);
+/* sample (tsdf.py:63-88) and/or gradient (tsdf.py:90-100) at n points (n,3):
+ * val (n) + valid (n) u8 and/or grad (n,3); any output may be NULL (not both) */
+int cf_tsdf_sample(const cf_tsdf_desc* V, const double* pts, int64_t n, double* val, uint8_t* valid, double* grad,
+                   void* stream);
+/* ray cast (tsdf.py:134-171) of every `stride`-th pixel: cam_rot = camera-to-world
+ * rotation (t ignored), vol_rot = world-to-volume rotation, origin = the camera centre
+ * in volume coordinates (device double[3]); per ray: pts / nrm (3) and hit (u8) */
+int cf_tsdf_raycast(const cf_tsdf_desc* V, const cf_pinhole* cam, const cf_rigid* cam_rot, const cf_rigid* vol_rot,
+                    const double* origin, int stride, double t0, double step, double max_t, double* pts, double* nrm,
+                    uint8_t* hit, void* stream);
+/* zero crossings along `axis` (tsdf.py:102-132): per voxel pair of the slice
+ * ((r-1) along axis, row-major) a flag and the interpolated point (pts (n,3)) */
+int cf_tsdf_crossings(const cf_tsdf_desc* V, int axis, double* pts, uint8_t* flag, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

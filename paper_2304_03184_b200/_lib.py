@@ -117,6 +117,21 @@ class PoolDecision(ctypes.Structure):
                 ("min_dissim", ctypes.c_double)]
 
 
+class TsdfDesc(ctypes.Structure):
+    _fields_ = [("tsdf", ctypes.c_void_p), ("weight", ctypes.c_void_p), ("resolution", ctypes.c_int),
+                ("pad", ctypes.c_int), ("voxel", ctypes.c_double), ("origin", ctypes.c_double * 3),
+                ("trunc", ctypes.c_double)]
+
+
+class Rigid(ctypes.Structure):
+    _fields_ = [("R", ctypes.c_double * 9), ("t", ctypes.c_double * 3)]
+
+
+class Pinhole(ctypes.Structure):
+    _fields_ = [("fx", ctypes.c_double), ("fy", ctypes.c_double), ("cx", ctypes.c_double), ("cy", ctypes.c_double),
+                ("width", ctypes.c_int), ("height", ctypes.c_int)]
+
+
 class DeformBwdIO(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in ("save_h", "save_o", "save_mask", "d_o", "dpre", "d_dfeat")]
 
@@ -189,6 +204,11 @@ _SIGS = {
     "cf_blur_score": [_p, _i32, _i32, _p, _p, _p],
     "cf_visibility_map": [_p, _i32, _p, _i32, _i32, _P(VisCamera), ctypes.c_double, _p, _p],
     "cf_pool_scan": [_P(PoolDesc), _P(PoolEntry), _p, _p, _p],
+    "cf_tsdf_integrate": [_P(TsdfDesc), _p, _i32, _i32, _p, _P(Rigid), _P(Rigid), _P(Pinhole), _p],
+    "cf_tsdf_sample": [_P(TsdfDesc), _p, _i64, _p, _p, _p, _p],
+    "cf_tsdf_raycast": [_P(TsdfDesc), _P(Pinhole), _P(Rigid), _P(Rigid), _p, _i32, ctypes.c_double, ctypes.c_double,
+                        ctypes.c_double, _p, _p, _p, _p],
+    "cf_tsdf_crossings": [_P(TsdfDesc), _i32, _p, _p, _p],
 }
 
 _lock = threading.Lock()
