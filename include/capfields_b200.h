@@ -315,7 +315,8 @@ typedef struct cf_field_desc {
   const float* dbias;       /* DeformNet layer-1 bias (128), pose theta folded in */
   float delta_scale;        /* |dv| bound, metres (0.05) */
   float inv_side;           /* metres -> unit cube */
-  void* save_h;             /* training: DeformNet hidden activations h1..h4, (S,512) fp16, or NULL */
+  void* save_h;             /* training: DeformNet hidden activations h1..h4, feature-major (512, S) fp16
+                               (row = layer * 128 + unit, S = capacity), or NULL */
   float* save_o;            /* training: DeformNet raw outputs (o0, o1, o2, 0) float4 per sample, or NULL */
   uint32_t* save_mask;      /* training: ReLU bits of layers 1..4, (S,16) uint32 = [layer][half][2], or NULL */
 } cf_field_desc;
@@ -380,11 +381,11 @@ int cf_field_hash_backward(const cf_field_desc* F, const cf_march_out* S, const 
                            const float* dfeat, float* table_grad, float* dx_out, void* stream);
 /* DeformNet backward buffers (S = capacity) */
 typedef struct cf_deform_bwd_io {
-  const void* save_h;  /* (S,512) fp16 forward h1..h4 (cf_field_desc.save_h; read by the dW GEMMs, not here) */
+  const void* save_h;  /* (512,S) fp16 forward h1..h4 (cf_field_desc.save_h; read by the dW GEMMs, not here) */
   const float* save_o; /* float4 per sample: raw outputs (cf_field_desc.save_o) */
   const uint32_t* save_mask; /* (S,16) ReLU bits of layers 1..4 (cf_field_desc.save_mask) */
   void* d_o;           /* (S,16) fp16 dL/d(raw outputs) */
-  void* dpre;          /* (S,512) fp16 dL/d(pre-activations) of layers 1..4 */
+  void* dpre;          /* (512,S) fp16 dL/d(pre-activations) of layers 1..4, feature-major as save_h */
   float* d_dfeat;      /* (S,32) fp32 dL/d(deform hash features) */
 } cf_deform_bwd_io;
 /* DeformNet backward on tcgen05: from dL/dxc (dxc, float4 per sample, the
@@ -401,6 +402,11 @@ int cf_adam(float* p, const float* g, float* m, float* v, int64_t n, float lr, f
             int step, float grad_scale, void* stream);
 /* out[c] += sum over the n rows of x (fp16, row stride ld elements) of column c < 128, fp32 */
 int cf_colsum128_f16(const void* x, int64_t n, int ld, float* out, void* stream);
+/* split-K weight-gradient GEMM on tcgen05: C[128 x n_cols] += A[128 x K] B[n_cols x K]^T,
+ * A / B fp16 K-major (row strides lda / ldb elements), C fp32 row-major (ldc);
+ * n_cols in {32, 64, 128} */
+int cf_gemm_kmajor_f16(const void* A, int64_t lda, const void* B, int64_t ldb, int n_cols, int64_t K, float* C,
+                       int ldc, void* stream);
 /* fp32 (n x k) row-major weight -> fp16 UMMA canonical K-major blob (n, k padded to 16) */
 int cf_pack_weight(const float* w, int n, int k, uint8_t* blob, void* stream);
 

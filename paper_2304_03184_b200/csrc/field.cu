@@ -282,11 +282,23 @@ __device__ __forceinline__ void ts_layer(TsSlot& S, const uint8_t* w, int K, int
   tc::fence_after();
 }
 
+// Store this thread's 32 fp16 values (16 packed pairs, columns col .. col+31) into a
+// column-major (feature-major) matrix: column c of the sample at dst[c * ld]. Lanes
+// are consecutive samples, so every store is a coalesced 64-byte warp segment.
+__device__ __forceinline__ void store_cols_f16(uint16_t* dst, int64_t ld, int col, const uint32_t* h) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    dst[(int64_t)(col + 2 * i) * ld] = (uint16_t)(h[i] & 0xffffu);
+    dst[(int64_t)(col + 2 * i + 1) * ld] = (uint16_t)(h[i] >> 16);
+  }
+}
+
 // hidden epilogue of a 128-wide layer: this warp's 64 columns -> (+bias) ReLU -> fp16 -> A
-// (training: also -> save[col], the sample's row of this layer's activations)
-// (training: mask = the ReLU derivative bits of these 64 columns, 2 x uint32)
+// (training: also -> save, this layer's activations of the sample in the feature-major
+// (128, ld) block at save (column c at save[c * ld]), and mask = the ReLU derivative
+// bits of these 64 columns, 2 x uint32)
 __device__ __forceinline__ void ts_relu128(const TsSlot& S, const float* bias, __half* save,
-                                           uint32_t* mask = nullptr) {
+                                           uint32_t* mask = nullptr, int64_t ld = 0) {
   uint32_t mw[2];
 #pragma unroll
   for (int c = 0; c < 2; ++c) {
@@ -315,11 +327,7 @@ __device__ __forceinline__ void ts_relu128(const TsSlot& S, const float* bias, _
     } else {
       tc::tmem_st16(S.a + (uint32_t)(col / 2), h);
     }
-    if (save) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        reinterpret_cast<uint4*>(save + col)[q] = make_uint4(h[4 * q], h[4 * q + 1], h[4 * q + 2], h[4 * q + 3]);
-    }
+    if (save) store_cols_f16(reinterpret_cast<uint16_t*>(save), ld, col, h);
   }
   if (mask) *reinterpret_cast<uint2*>(mask) = make_uint2(mw[0], mw[1]);
 }
@@ -394,16 +402,18 @@ __global__ void __launch_bounds__(kDeformSlots* kDeformSlotThreads, 1)
 #pragma unroll
       for (int q = 0; q < 2; ++q) nxt[q] = (sn < n) ? dfeat[sn * 4 + 2 * S.half + q] : make_uint4(0, 0, 0, 0);
     }
-    __half* sv = (kSave && live) ? save_h + s * 512 : nullptr;
+    // activations h1..h4 feature-major: save_h (512, capacity), row = layer * 128 + column
+    __half* sv = (kSave && live) ? save_h + s : nullptr;
+    const int64_t L = 128 * capacity;
     // ReLU masks: per sample 4 layers x 2 halves x 64 bits
     uint32_t* mk = (kSave && live) ? save_mask + s * 16 + 2 * S.half : nullptr;  // [layer][half][2]
-    ts_relu128(S, s_bias, sv, mk);
+    ts_relu128(S, s_bias, sv, mk, capacity);
     ts_layer(S, smem + o2, 128, 128);
-    ts_relu128(S, nullptr, sv ? sv + 128 : nullptr, mk ? mk + 4 : nullptr);
+    ts_relu128(S, nullptr, sv ? sv + L : nullptr, mk ? mk + 4 : nullptr, capacity);
     ts_layer(S, smem + o3, 128, 128);
-    ts_relu128(S, nullptr, sv ? sv + 256 : nullptr, mk ? mk + 8 : nullptr);
+    ts_relu128(S, nullptr, sv ? sv + 2 * L : nullptr, mk ? mk + 8 : nullptr, capacity);
     ts_layer(S, smem + o4, 128, 128);
-    ts_relu128(S, nullptr, sv ? sv + 384 : nullptr, mk ? mk + 12 : nullptr);
+    ts_relu128(S, nullptr, sv ? sv + 3 * L : nullptr, mk ? mk + 12 : nullptr, capacity);
     ts_layer(S, smem + o5, 128, 16);
     if (S.half == 0) {
       float v[16];
@@ -884,8 +894,9 @@ constexpr int kDBwdSlots = kDeformSlots;
 
 // dL/dpre of a 128-wide ReLU layer for this warp's 64 columns: D (= dL/dact) *
 // [pre > 0] (the forward's saved ReLU bits, bit j = column 64*half + j) -> fp16
-// A operand (TMEM or smem) and the sample's dpre row (or null)
-__device__ __forceinline__ void ts_bwd_mask128(const TsSlot& S, uint64_t mask, __half* dpre) {
+// A operand (TMEM or smem) and the sample's dpre column in the feature-major
+// (128, ld) block at dpre (or null)
+__device__ __forceinline__ void ts_bwd_mask128(const TsSlot& S, uint64_t mask, __half* dpre, int64_t ld) {
 #pragma unroll
   for (int c = 0; c < 2; ++c) {
     const int col = 64 * S.half + 32 * c;
@@ -908,11 +919,7 @@ __device__ __forceinline__ void ts_bwd_mask128(const TsSlot& S, uint64_t mask, _
     } else {
       tc::tmem_st16(S.a + (uint32_t)(col / 2), h);
     }
-    if (dpre) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        reinterpret_cast<uint4*>(dpre + col)[q] = make_uint4(h[4 * q], h[4 * q + 1], h[4 * q + 2], h[4 * q + 3]);
-    }
+    if (dpre) store_cols_f16(reinterpret_cast<uint16_t*>(dpre), ld, col, h);
   }
 }
 
@@ -999,15 +1006,17 @@ __global__ void __launch_bounds__(kDBwdSlots* kDeformSlotThreads, 1)
         mk[l] = (uint64_t)v.x | (uint64_t)v.y << 32;
       }
     }
-    __half* dp = live ? dpre + s * 512 : nullptr;
+    // dpre1..4 feature-major: (512, capacity), row = layer * 128 + column
+    __half* dp = live ? dpre + s : nullptr;
+    const int64_t L = 128 * capacity;
     ts_layer(S, smem + t5, 16, 128);  // dh4 = d_o . W5
-    ts_bwd_mask128(S, mk[3], dp ? dp + 384 : nullptr);
+    ts_bwd_mask128(S, mk[3], dp ? dp + 3 * L : nullptr, capacity);
     ts_layer(S, smem + t4, 128, 128);  // dh3 = dpre4 . W4
-    ts_bwd_mask128(S, mk[2], dp ? dp + 256 : nullptr);
+    ts_bwd_mask128(S, mk[2], dp ? dp + 2 * L : nullptr, capacity);
     ts_layer(S, smem + t3, 128, 128);  // dh2 = dpre3 . W3
-    ts_bwd_mask128(S, mk[1], dp ? dp + 128 : nullptr);
+    ts_bwd_mask128(S, mk[1], dp ? dp + L : nullptr, capacity);
     ts_layer(S, smem + t2, 128, 128);  // dh1 = dpre2 . W2
-    ts_bwd_mask128(S, mk[0], dp);
+    ts_bwd_mask128(S, mk[0], dp, capacity);
     ts_layer(S, smem + t1, 128, 32);  // dL/dfeat = dpre1 . W1x
     if (S.half == 0) {
       float dfx[32];

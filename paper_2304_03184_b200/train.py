@@ -177,14 +177,14 @@ class DeformParams:
 
 class _DeformBuffers:
     def __init__(self, cap, device):
-        self.save_h = torch.empty((cap, 512), dtype=torch.float16, device=device)
+        # feature-major (512, capacity): the kernels' stores coalesce across samples
+        self.save_h = torch.empty((512, cap), dtype=torch.float16, device=device)
         self.save_o = torch.empty((cap, 4), dtype=torch.float32, device=device)
         self.save_mask = torch.empty((cap, 16), dtype=torch.int32, device=device)
         self.d_o = torch.empty((cap, 16), dtype=torch.float16, device=device)
-        self.dpre = torch.empty((cap, 512), dtype=torch.float16, device=device)
+        self.dpre = torch.empty((512, cap), dtype=torch.float16, device=device)
         self.d_dfeat = torch.empty((cap, 32), dtype=torch.float32, device=device)
         self.dxc = torch.empty((cap, 4), dtype=torch.float32, device=device)
-        self.colsum = torch.empty(128, dtype=torch.float32, device=device)
         self.io = _lib.DeformBwdIO(self.save_h.data_ptr(), self.save_o.data_ptr(), self.save_mask.data_ptr(),
                                    self.d_o.data_ptr(),
                                    self.dpre.data_ptr(), self.d_dfeat.data_ptr())
@@ -307,7 +307,9 @@ class Trainer:
         pads = [bwd.d_o, bwd.dc2, bwd.dc1, bwd.dg, bwd.dh1, bwd.c2, bwd.c1, bwd.cin, bwd.h1]
         pads += [scratch[n * 64: n_pad * 64]]  # colour-MLP input rows (x0 below)
         if dp is not None:
-            pads += [db.d_o, db.dpre, db.save_h, scratch[cap * 64 + n * 64: cap * 64 + n_pad * 64]]
+            pads += [db.d_o, scratch[cap * 64 + n * 64: cap * 64 + n_pad * 64]]
+            db.dpre[:, n:n_pad].zero_()
+            db.save_h[:, n:n_pad].zero_()
         for t in pads:
             (t[n:n_pad] if t.dim() == 2 else t).zero_()
         n, n_true = n_pad, n
@@ -324,17 +326,18 @@ class Trainer:
         G["G1"] += (f(bwd.dh1).t() @ x0).float()
         if dp is not None:
             xd = scratch[cap * 64: cap * 64 + n * 64].view(torch.float16).view(n, 32)  # deform-grid features
-            H, DP, DO = db.save_h[:n], db.dpre[:n], db.d_o[:n]
+            H, DP, DO = db.save_h[:, :n], db.dpre[:, :n], db.d_o[:n]  # H, DP feature-major
             GD = dp.G
-            GD["D5"] += (DO.t() @ H[:, 384:512]).float()[:3]
-            GD["D4"] += (DP[:, 384:512].t() @ H[:, 256:384]).float()
-            GD["D3"] += (DP[:, 256:384].t() @ H[:, 128:256]).float()
-            GD["D2"] += (DP[:, 128:256].t() @ H[:, 0:128]).float()
-            GD["D1"][:, :32] += (DP[:, 0:128].t() @ xd).float()
+            GD["D5"] += (DO.t() @ H[384:512].t()).float()[:3]
+            # dW_l = dpre_l h_{l-1}^T over the frame's samples: both operands feature-major
+            # (K = samples contiguous), split-K on tcgen05 accumulating into the fp32 grads
+            ld = db.save_h.stride(0)
+            for l, key in ((3, "D4"), (2, "D3"), (1, "D2")):
+                _lib.call("cf_gemm_kmajor_f16", db.dpre[128 * l].data_ptr(), ld, db.save_h[128 * (l - 1)].data_ptr(),
+                          ld, 128, n, GD[key].data_ptr(), 128, s)
+            GD["D1"][:, :32] += (DP[0:128] @ xd).float()
             # theta is the same for every sample of the frame: dW1_theta = (sum_s dpre1) theta^T
-            csum = db.colsum
-            csum.zero_()
-            _lib.call("cf_colsum128_f16", DP.data_ptr(), n_true, 512, csum.data_ptr(), s)
+            csum = DP[0:128, :n_true].sum(1, dtype=torch.float32)
             GD["D1"][:, 32:] += torch.outer(csum, b.theta.to(DP.device, torch.float32))
 
     def set_frame(self, b: FrameBatch):

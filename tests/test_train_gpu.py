@@ -383,3 +383,24 @@ def test_keyframe_ray_sampler(setup):
     assert np.allclose(dirs.cpu().numpy(), d[p], rtol=0, atol=1e-15)
     b = kf.sample(4096, seed=11)
     assert b.dirs.shape == (4096, 3) and int(b.mask_h.sum() + b.mask_o.sum()) >= 4096
+
+
+@pytest.mark.parametrize("n_cols,K", [(128, 1_000_000), (128, 4097), (64, 64), (32, 12345), (128, 1)])
+def test_gemm_kmajor_vs_torch(n_cols, K):
+    """tcgen05 split-K dW GEMM (C += A B^T, K-major fp16 operands with row strides)
+    vs an fp32 torch reference on the same fp16 values."""
+    from paper_2304_03184_b200 import _lib
+    g = torch.Generator(device="cuda").manual_seed(K)
+    ld = (K + 7) // 8 * 8 + 8  # rows 16-byte aligned, with a gap past K
+    A = torch.randn((128, ld), generator=g, device="cuda").half()
+    B = torch.randn((n_cols, ld), generator=g, device="cuda").half()
+    C = torch.randn((128, n_cols + 5), generator=g, device="cuda")
+    ref = C[:, :n_cols] + A[:, :K].float() @ B[:, :K].float().t()
+    _lib.call("cf_gemm_kmajor_f16", A.data_ptr(), ld, B.data_ptr(), ld, n_cols, K, C.data_ptr(), n_cols + 5,
+              _lib.stream_ptr())
+    torch.cuda.synchronize()
+    err = (C[:, :n_cols] - ref).abs().max().item()
+    assert err <= 1e-5 * max(1.0, K ** 0.5) * 4, err  # fp32 accumulation-order differences only
+    with pytest.raises(ValueError):  # unaligned rows are refused, not faulted on
+        _lib.call("cf_gemm_kmajor_f16", A.data_ptr(), ld + 1, B.data_ptr(), ld, n_cols, K, C.data_ptr(), n_cols + 5,
+                  _lib.stream_ptr())
