@@ -4,6 +4,9 @@
 // tcgen05 kernels after every update.
 #include <cuda_fp16.h>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 
 #include "common.cuh"
@@ -50,34 +53,46 @@ __global__ void colsum128_kernel(const __half* __restrict__ x, int64_t n, int ld
 // Split-K weight-gradient GEMM on tcgen05: C[128 x N] += A[128 x K] B[N x K]^T with
 // both operands K-major (row stride lda / ldb elements) — the feature-major saved
 // activations and dL/dpre of DeformNet, where K = the frame's samples. Each CTA
-// (one per SM) owns a contiguous range of 64-wide K tiles: cp.async (16 B, zero-
-// filled past K) into a 4-stage ring of canonical K-major smem tiles, one elected
-// thread issues 4 MMAs (K = 16) per tile into a 128 x N fp32 TMEM accumulator and
-// commits to the stage's mbarrier, which gates the stage's refill. The partial
-// product is added into C with fp32 atomics (one per element per CTA).
-constexpr int kGKT = 64;     // K per stage
-constexpr int kGStages = 4;
+// (one per SM) owns a contiguous range of 64-wide K tiles. Warp-specialised: one
+// thread streams the tiles with TMA (2-D boxes of 8 halves x rows, zero fill past
+// K) into a 6-stage ring, one thread issues 4 MMAs (K = 16) per tile into a
+// 128 x N fp32 TMEM accumulator and commits each stage back to the producer; the
+// four warps then add the partial product into C with fp32 atomics.
+//
+// A TMA box of 64 halves x R rows with the 128-byte swizzle lands as the canonical
+// K-major SWIZZLE_128B layout: 128-byte rows, 8-row atoms of 1024 B (SBO), the 16 B
+// chunks of row r XOR-permuted by r % 8; a K = 16 step advances the start by 32 B.
+constexpr int kGKT = 64;  // K per stage
+constexpr int kGStages = 6;
 
-// 16-byte async copy of the 8 halves at k .. k+7 of a row; the part past K is zero-filled
-__device__ __forceinline__ void cp_async_k8(uint32_t dst, const __half* row, int64_t k, int64_t K) {
-  const int64_t left = K - k;
-  const int bytes = left >= 8 ? 16 : (left > 0 ? (int)left * 2 : 0);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(row + (left > 0 ? k : 0)),
-               "r"(bytes)
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(tc::smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(bar)), "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+
+__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;           // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;  // SBO: next 8-row atom
+  d |= (uint64_t)1 << 46;           // version
+  d |= (uint64_t)2 << 61;           // layout: SWIZZLE_128B
+  return d;
 }
 
 template <int N>
-__global__ void __launch_bounds__(128, 1) gemm_kmajor_kernel(const __half* __restrict__ A, int64_t lda,
-                                                             const __half* __restrict__ B, int64_t ldb, int64_t K,
+__global__ void __launch_bounds__(128, 1) gemm_kmajor_kernel(const __grid_constant__ CUtensorMap map_a,
+                                                             const __grid_constant__ CUtensorMap map_b, int64_t K,
                                                              float* __restrict__ C, int ldc) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t mbar[kGStages];
+  __shared__ uint64_t full[kGStages], empty[kGStages], done;
   __shared__ uint32_t tmem_base;
   constexpr int kStageA = 128 * kGKT * 2, kStageB = N * kGKT * 2, kStage = kStageA + kStageB;
   const int tid = threadIdx.x, warp = tid / 32;
@@ -86,72 +101,95 @@ __global__ void __launch_bounds__(128, 1) gemm_kmajor_kernel(const __half* __res
   const int64_t t0 = (int64_t)blockIdx.x * per, nt = max((int64_t)0, min(per, T - t0));
   if (nt == 0) return;
   if (tid == 0) {
-    for (int q = 0; q < kGStages; ++q) tc::bar_init(&mbar[q], 1);
+    for (int q = 0; q < kGStages; ++q) {
+      tc::bar_init(&full[q], 1);
+      tc::bar_init(&empty[q], 1);
+    }
+    tc::bar_init(&done, 1);
     tc::bar_fence_init();
   }
-  if (warp == 0) tc::tmem_alloc<N < 32 ? 32 : N>(&tmem_base);
+  if (warp == 2) tc::tmem_alloc<N < 32 ? 32 : N>(&tmem_base);
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t sbase = tc::smem_u32(smem);
-  auto load = [&](int stage, int64_t tile) {
-    const int64_t k0 = (t0 + tile) * kGKT;
-    const uint32_t sa = sbase + stage * kStage, sb = sa + kStageA;
-    // 16-byte chunks: (row, c) with c = 8-half group along K; 8 consecutive lanes read a row's 128 B
-#pragma unroll
-    for (int i = 0; i < (128 * 8) / 128; ++i) {
-      const int q = tid + 128 * i, r = q >> 3, c = q & 7;
-      cp_async_k8(sa + tc::core_offset(r, 8 * c, kGKT), A + r * lda, k0 + 8 * c, K);
+  if (tid == 0) {
+    // TMA producer
+    for (int64_t i = 0; i < nt; ++i) {
+      const int st = (int)(i % kGStages);
+      if (i >= kGStages) tc::bar_wait(&empty[st], (uint32_t)(((i / kGStages) - 1) & 1));
+      bar_expect_tx(&full[st], kStage);
+      const int k0 = (int)((t0 + i) * kGKT);
+      const uint32_t sa = sbase + st * kStage, sb = sa + kStageA;
+      tma_load_2d(sa, &map_a, k0, 0, &full[st]);
+      tma_load_2d(sb, &map_b, k0, 0, &full[st]);
     }
-#pragma unroll
-    for (int i = 0; i < (N * 8 + 127) / 128; ++i) {
-      const int q = tid + 128 * i, r = q >> 3, c = q & 7;
-      if (r < N) cp_async_k8(sb + tc::core_offset(r, 8 * c, kGKT), B + r * ldb, k0 + 8 * c, K);
-    }
-  };
-#pragma unroll
-  for (int s = 0; s < kGStages - 1; ++s) {
-    if (s < nt) load(s, s);
-    cp_async_commit();
-  }
-  constexpr uint32_t idesc = tc::idesc_f16(128, N);
-  for (int64_t i = 0; i < nt; ++i) {
-    const int stage = (int)(i % kGStages);
-    cp_async_wait<kGStages - 2>();
-    tc::fence_async_smem();  // cp.async (generic proxy) -> tcgen05.mma (async proxy)
-    __syncthreads();
-    if (tid == 0) {
+  } else if (tid == 32) {
+    // MMA issuer
+    constexpr uint32_t idesc = tc::idesc_f16(128, N);
+    for (int64_t i = 0; i < nt; ++i) {
+      const int st = (int)(i % kGStages);
+      tc::bar_wait(&full[st], (uint32_t)((i / kGStages) & 1));
       tc::fence_after();
-      const uint32_t sa = sbase + stage * kStage, sb = sa + kStageA;
+      const uint32_t sa = sbase + st * kStage, sb = sa + kStageA;
 #pragma unroll
       for (int ks = 0; ks < kGKT / 16; ++ks) {
-        const uint64_t ad = tc::sdesc(sa + ks * 256, 128, kGKT * 16);
-        const uint64_t bd = tc::sdesc(sb + ks * 256, 128, kGKT * 16);
+        const uint64_t ad = sdesc_sw128(sa + ks * 32);
+        const uint64_t bd = sdesc_sw128(sb + ks * 32);
         tc::mma_f16(tmem_base, ad, bd, idesc, (i > 0 || ks > 0) ? 1u : 0u);
       }
-      tc::mma_commit(&mbar[stage]);
+      tc::mma_commit(&empty[st]);
     }
-    const int64_t j = i + kGStages - 1;  // refill the stage the previous tile's MMAs read
-    if (j < nt) {
-      if (i >= 1) tc::bar_wait(&mbar[(i - 1) % kGStages], (uint32_t)(((i - 1) / kGStages) & 1));
-      load((int)(j % kGStages), j);
-    }
-    cp_async_commit();
+    tc::mma_commit(&done);
   }
-  tc::bar_wait(&mbar[(nt - 1) % kGStages], (uint32_t)(((nt - 1) / kGStages) & 1));
+  tc::bar_wait(&done, 0);
+  __syncwarp();  // producer / issuer lanes rejoin their warps before the aligned TMEM loads
   tc::fence_after();
   const int row = warp * 32 + (tid & 31);
+  const bool vec4 = (ldc % 4) == 0 && (reinterpret_cast<uintptr_t>(C) % 16) == 0;
 #pragma unroll 1
   for (int c0 = 0; c0 < N; c0 += 32) {
     float v[32];
     tc::tmem_ld32(tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
     float* dst = C + (int64_t)row * ldc + c0;
+    if (vec4) {
 #pragma unroll
-    for (int c = 0; c < 32; ++c) atomicAdd(dst + c, v[c]);
+      for (int c = 0; c < 32; c += 4)
+        atomicAdd(reinterpret_cast<float4*>(dst + c), make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]));
+    } else {
+#pragma unroll
+      for (int c = 0; c < 32; ++c) atomicAdd(dst + c, v[c]);
+    }
   }
   tc::fence_before();
   __syncthreads();
-  if (warp == 0) tc::tmem_free<N < 32 ? 32 : N>(tmem_base);
+  if (warp == 2) tc::tmem_free<N < 32 ? 32 : N>(tmem_base);
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// rows x K fp16, row stride ld elements; boxes of 64 halves (128 B) x rows, 128B swizzle
+bool make_map(CUtensorMap* map, const void* base, int rows, int64_t K, int64_t ld) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  const cuuint32_t box[2] = {64, (cuuint32_t)rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 }  // namespace
@@ -166,28 +204,23 @@ int cf_gemm_kmajor_f16(const void* A, int64_t lda, const void* B, int64_t ldb, i
   if ((lda | ldb) % 8 != 0 || (reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) % 16 != 0)
     return cf::fail(CF_E_BAD_ARG, "cf_gemm_kmajor_f16: operands need 16-byte aligned rows (lda, ldb % 8 == 0)");
   if (K == 0) return CF_OK;
+  if (K >= (int64_t)1 << 31) return cf::fail(CF_E_BAD_ARG, "cf_gemm_kmajor_f16: K must be < 2^31");
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, A, 128, K, lda) || !make_map(&mb, B, n_cols, K, ldb))
+    return cf::fail(CF_E_CUDA, "cf_gemm_kmajor_f16: cuTensorMapEncodeTiled failed");
   const int64_t T = (K + kGKT - 1) / kGKT;
   const unsigned grid = (unsigned)std::min<int64_t>(T, cf::sm_count());
   cudaStream_t st = cf::as_stream(stream);
   auto run = [&](auto kern, int N) -> int {
     const int smem = kGStages * (128 + N) * kGKT * 2;
     CF_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    kern<<<grid, 128, smem, st>>>(reinterpret_cast<const __half*>(A), lda, reinterpret_cast<const __half*>(B), ldb,
-                                  K, C, ldc);
+    kern<<<grid, 128, smem, st>>>(ma, mb, K, C, ldc);
     return CF_OK;
   };
   int rc = n_cols == 128 ? run(gemm_kmajor_kernel<128>, 128)
                          : (n_cols == 64 ? run(gemm_kmajor_kernel<64>, 64) : run(gemm_kmajor_kernel<32>, 32));
   if (rc) return rc;
   return cf::check_launch("cf_gemm_kmajor_f16");
-}
-
-int cf_colsum128_f16(const void* x, int64_t n, int ld, float* out, void* stream) {
-  if (!x || !out || n < 0 || ld < 128) return cf::fail(CF_E_BAD_ARG, "cf_colsum128_f16: bad args");
-  if (n == 0) return CF_OK;
-  colsum128_kernel<<<cf::grid_for((n + 1) / 2, 1, 4), 256, 0, cf::as_stream(stream)>>>(
-      reinterpret_cast<const __half*>(x), n, ld, out);
-  return cf::check_launch("cf_colsum128_f16");
 }
 
 int cf_adam(float* p, const float* g, float* m, float* v, int64_t n, float lr, float beta1, float beta2, float eps,
