@@ -776,6 +776,27 @@ def run_frontend(args, rank, world, pg):
     e1.record()
     torch.cuda.synchronize()
     ray_ms = e0.elapsed_time(e1) / 5
+    # -- non-rigid tracking solve: the reference tracker's own Gauss-Newton system
+    import scipy.sparse as sps
+    from oracle import tracking as otr
+    from paper_2304_03184_b200.tracking import GaussNewtonSystem
+    with np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "tests", "golden", "pcg_ref.npz")) as z:
+        pj = {k: z[k] for k in z.files}
+    gn = GaussNewtonSystem((pj["val"], pj["col"], pj["rowptr"], pj["shape"]), pj["r"])
+    for _ in range(3):
+        gn.solve(1e-4)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(20):
+        gn.solve(1e-4)
+    e1.record()
+    torch.cuda.synchronize()
+    pcg_us = e0.elapsed_time(e1) * 1e3 / 20
+    Js = sps.csr_matrix((pj["val"], pj["col"], pj["rowptr"]), shape=tuple(pj["shape"]))
+    t0 = time.perf_counter()
+    for _ in range(5):
+        otr.pcg_solve_sparse(Js, pj["r"], 1e-4)
+    pcg_cpu_us = (time.perf_counter() - t0) * 1e6 / 5
     line = {"metric": "front-end stages: key-frame selection per tracked frame; motion-prior ingestion",
             "value": 1e3 / sel_ms, "unit": "tracked frames/s (selection)", "n_gpus": 1, "higher_is_better": True,
             "ms_per_frame_selection": sel_ms, "dtype": "u8 / f64 / int",
@@ -784,6 +805,8 @@ def run_frontend(args, rank, world, pg):
                        "decode_upload_fk_s": ingest_s, "fk_us_per_1000_frames": fk_us},
             "tsdf": {"resolution": 256, "integrate_ms": integ_ms, "voxels_per_s": 256 ** 3 / (integ_ms * 1e-3),
                      "raycast_512x512_ms": ray_ms, "raycast_hits": int(len(rp))},
+            "pcg": {"system": f"{int(pj['shape'][0])}x{int(pj['shape'][1])}, nnz {len(pj['val'])} (reference tracker)",
+                    "iterations": 32, "gpu_us_per_solve": pcg_us, "cpu_scipy_us_per_solve": pcg_cpu_us},
             "cpu_baseline": {"value": 1e3 / cpu_ms, "unit": "tracked frames/s", "cores": 1, "kind": "port",
                              "sample": "oracle blur + visibility + 100-entry Eq. 6 scan, 3 frames"},
             "config": {"workload": "SURVEY 8(f) 2-3 front-end stages; selection = blur(512^2) + visibility(8192 "

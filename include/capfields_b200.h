@@ -528,6 +528,23 @@ int cf_tsdf_raycast(const cf_tsdf_desc* V, const cf_pinhole* cam, const cf_rigid
  * ((r-1) along axis, row-major) a flag and the interpolated point (pts (n,3)) */
 int cf_tsdf_crossings(const cf_tsdf_desc* V, int axis, double* pts, uint8_t* flag, void* stream);
 
+/* ------------------------------------- non-rigid tracking solve (tracking.py) */
+/* CSR matrix on the device (int32 indices) */
+typedef struct cf_csr {
+  const double* val;
+  const int* col;
+  const int* rowptr; /* rows + 1 */
+  int rows, cols;
+  int64_t nnz;
+} cf_csr;
+/* workspace (doubles) cf_pcg_solve needs for a rows x cols Jacobian */
+int cf_pcg_workspace_doubles(int rows, int cols, int64_t* n_doubles);
+/* pcg_solve (tracking.py:158-193): Jacobi-PCG on (J^T J + lambda diag(J^T J)) x = -J^T r,
+ * at most max_iters iterations, stop when |res| <= tol |b|; one cooperative launch.
+ * JT = J transposed (CSR); x (cols) out; iters (device int) = iterations run, or NULL */
+int cf_pcg_solve(const cf_csr* J, const cf_csr* JT, const double* r, double lm_lambda, int max_iters, double tol,
+                 double* x, double* work, int* iters, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -132,6 +132,11 @@ class Pinhole(ctypes.Structure):
                 ("width", ctypes.c_int), ("height", ctypes.c_int)]
 
 
+class Csr(ctypes.Structure):
+    _fields_ = [("val", ctypes.c_void_p), ("col", ctypes.c_void_p), ("rowptr", ctypes.c_void_p),
+                ("rows", ctypes.c_int), ("cols", ctypes.c_int), ("nnz", ctypes.c_int64)]
+
+
 class DeformBwdIO(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in ("save_h", "save_o", "save_mask", "d_o", "dpre", "d_dfeat")]
 
@@ -210,6 +215,8 @@ _SIGS = {
     "cf_tsdf_raycast": [_P(TsdfDesc), _P(Pinhole), _P(Rigid), _P(Rigid), _p, _i32, ctypes.c_double, ctypes.c_double,
                         ctypes.c_double, _p, _p, _p, _p],
     "cf_tsdf_crossings": [_P(TsdfDesc), _i32, _p, _p, _p],
+    "cf_pcg_workspace_doubles": [_i32, _i32, _P(ctypes.c_int64)],
+    "cf_pcg_solve": [_P(Csr), _P(Csr), _p, ctypes.c_double, _i32, ctypes.c_double, _p, _p, _p, _p],
 }
 
 _lock = threading.Lock()

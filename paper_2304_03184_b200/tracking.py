@@ -1,0 +1,85 @@
+"""Non-rigid tracking solve on the GPU — drop-in for capfields.tracking.pcg_solve
+(tracking.py:158-193), the inner solver of the tracker's Levenberg-Marquardt loop.
+
+SURVEY §8(f) 4. The Jacobi-preconditioned CG on (J^T J + lambda diag(J^T J)) x =
+-J^T r runs as one cooperative kernel (csrc/pcg.cu, `cf_pcg_solve`): both sparse
+products, the dot products and the stopping tests happen on the device between
+grid-wide barriers. `GaussNewtonSystem` uploads J once and builds J^T on the device,
+so the LM loop's retries at growing damping (tracking.py:523-536) reuse it.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+
+PCG_ITERS = 32    # tracking.py:28-29
+PCG_TOL = 1e-6
+
+
+def _csr_parts(J):
+    """(val, col, rowptr, rows, cols) from a scipy.sparse matrix or a tuple."""
+    if hasattr(J, "tocsr"):
+        J = J.tocsr()
+        return J.data, J.indices, J.indptr, J.shape[0], J.shape[1]
+    val, col, rowptr, shape = J
+    return val, col, rowptr, int(shape[0]), int(shape[1])
+
+
+class GaussNewtonSystem:
+    """A Jacobian J (rows x cols, CSR) and residual r resident in HBM, with J^T."""
+
+    def __init__(self, J, r):
+        d = _lib.require_cuda()
+        val, col, rowptr, rows, cols = _csr_parts(J)
+        self.rows, self.cols = int(rows), int(cols)
+        as_t = lambda a, dt: torch.as_tensor(np.asarray(a), dtype=dt).to(d)  # noqa: E731
+        self.val = as_t(val, torch.float64).contiguous()
+        self.col = as_t(col, torch.int32).contiguous()
+        self.rowptr = as_t(rowptr, torch.int32).contiguous()
+        r = torch.as_tensor(np.asarray(r, dtype=np.float64) if not isinstance(r, torch.Tensor) else r)
+        self.r = r.to(d, torch.float64).contiguous()
+        if self.r.numel() != self.rows or self.rowptr.numel() != self.rows + 1:
+            raise ValueError("residual / row pointer length does not match the Jacobian")
+        # J^T on the device: stable sort of the entries by (column, row)
+        nnz = self.val.numel()
+        row = torch.repeat_interleave(torch.arange(self.rows, device=d, dtype=torch.int64),
+                                      (self.rowptr[1:] - self.rowptr[:-1]).to(torch.int64))
+        order = torch.argsort(self.col.to(torch.int64) * max(self.rows, 1) + row, stable=True)
+        self.tval = self.val[order].contiguous()
+        self.tcol = row[order].to(torch.int32).contiguous()
+        counts = torch.bincount(self.col.to(torch.int64), minlength=self.cols)
+        self.trowptr = torch.cat([torch.zeros(1, dtype=torch.int64, device=d), torch.cumsum(counts, 0)]).to(
+            torch.int32).contiguous()
+        self.J = self._desc(self.val, self.col, self.rowptr, self.rows, self.cols, nnz)
+        self.JT = self._desc(self.tval, self.tcol, self.trowptr, self.cols, self.rows, nnz)
+        nd = ctypes.c_int64()
+        _lib.call("cf_pcg_workspace_doubles", self.rows, self.cols, ctypes.byref(nd))
+        self.work = torch.empty(int(nd.value), dtype=torch.float64, device=d)
+        self.iters = torch.zeros(1, dtype=torch.int32, device=d)
+
+    @staticmethod
+    def _desc(val, col, rowptr, rows, cols, nnz) -> _lib.Csr:
+        c = _lib.Csr()
+        c.val, c.col, c.rowptr = val.data_ptr(), col.data_ptr(), rowptr.data_ptr()
+        c.rows, c.cols, c.nnz = rows, cols, nnz
+        return c
+
+    def solve(self, lm_lambda: float, max_iters: int = PCG_ITERS, tol: float = PCG_TOL) -> torch.Tensor:
+        """x (cols,) on the device; `last_iters` holds the iteration count (device)."""
+        x = torch.empty(self.cols, dtype=torch.float64, device=self.val.device)
+        _lib.call("cf_pcg_solve", _lib.byref(self.J), _lib.byref(self.JT), self.r.data_ptr(), float(lm_lambda),
+                  int(max_iters), float(tol), x.data_ptr(), self.work.data_ptr(), self.iters.data_ptr(),
+                  _lib.stream_ptr())
+        return x
+
+
+def pcg_solve(J, r, lm_lambda: float, max_iters: int = PCG_ITERS, tol: float = PCG_TOL) -> np.ndarray:
+    """Solve (J^T J + lm_lambda diag(J^T J)) x = -J^T r by Jacobi-PCG (tracking.py:158-193)."""
+    return GaussNewtonSystem(J, r).solve(lm_lambda, max_iters, tol).cpu().numpy()
+
+
+__all__ = ["PCG_ITERS", "PCG_TOL", "GaussNewtonSystem", "pcg_solve"]
