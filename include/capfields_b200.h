@@ -400,8 +400,6 @@ int cf_deform_hash_backward(const cf_field_desc* F, const cf_march_out* S, const
 /* Adam: p -= lr * mhat / (sqrt(vhat) + eps), m/v in place; grads scaled by grad_scale */
 int cf_adam(float* p, const float* g, float* m, float* v, int64_t n, float lr, float beta1, float beta2, float eps,
             int step, float grad_scale, void* stream);
-/* out[c] += sum over the n rows of x (fp16, row stride ld elements) of column c < 128, fp32 */
-int cf_colsum128_f16(const void* x, int64_t n, int ld, float* out, void* stream);
 /* split-K weight-gradient GEMM on tcgen05: C[128 x n_cols] += A[128 x K] B[n_cols x K]^T,
  * A / B fp16 K-major (row strides lda / ldb elements), C fp32 row-major (ldc);
  * n_cols in {32, 64, 128} */

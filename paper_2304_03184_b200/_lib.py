@@ -201,7 +201,6 @@ _SIGS = {
     "cf_adam": [_p, _p, _p, _p, _i64, ctypes.c_float, ctypes.c_float, ctypes.c_float, ctypes.c_float, _i32,
                 ctypes.c_float, _p],
     "cf_pack_weight": [_p, _i32, _i32, _p, _p],
-    "cf_colsum128_f16": [_p, _i64, _i32, _p, _p],
     "cf_gemm_kmajor_f16": [_p, _i64, _p, _i64, _i32, _i64, _p, _i32, _p],
     "cf_mp_scan": [ctypes.c_char_p, _P(MpInfo)],
     "cf_mp_read": [ctypes.c_char_p, _i64, _i64, _p, _p, _p, _p, _p],

@@ -36,19 +36,6 @@ __global__ void pack_kernel(const float* __restrict__ w, int n, int k, int np, i
   }
 }
 
-// out[c] += sum_{r < n} x[r * ld + c], c < 128: fp16 rows, fp32 accumulation
-// (DeformNet's theta gradient needs the column sums of dL/dpre1 over a frame)
-__global__ void colsum128_kernel(const __half* __restrict__ x, int64_t n, int ld, float* __restrict__ out) {
-  __shared__ float part[256];
-  const int c = threadIdx.x & 127, rg = threadIdx.x >> 7;
-  float acc = 0.0f;
-  for (int64_t r = (int64_t)blockIdx.x * 2 + rg; r < n; r += (int64_t)gridDim.x * 2)
-    acc += __half2float(x[r * ld + c]);
-  part[threadIdx.x] = acc;
-  __syncthreads();
-  if (threadIdx.x < 128) atomicAdd(out + c, part[threadIdx.x] + part[threadIdx.x + 128]);
-}
-
 // ---------------------------------------------------------------- dW = dY X^T
 // Split-K weight-gradient GEMM on tcgen05: C[128 x N] += A[128 x K] B[N x K]^T with
 // both operands K-major (row stride lda / ldb elements) — the feature-major saved
