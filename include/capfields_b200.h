@@ -527,6 +527,19 @@ int cf_tsdf_raycast(const cf_tsdf_desc* V, const cf_pinhole* cam, const cf_rigid
 int cf_tsdf_crossings(const cf_tsdf_desc* V, int axis, double* pts, uint8_t* flag, void* stream);
 
 /* ------------------------------------- non-rigid tracking solve (tracking.py) */
+/* depth_normals (tracking.py:60-80): camera-facing world normals (H, W, 3) of a depth
+ * map (H, W) float64 by central differences of the backprojected points (0 = invalid);
+ * cam_pose = camera-to-world */
+int cf_depth_normals(const double* depth, int height, int width, const cf_pinhole* cam, const cf_rigid* cam_pose,
+                     double* normals, void* stream);
+/* find_correspondences (tracking.py:83-150) per model point (n,3) with normals (n,3):
+ * keep (n) u8, and for kept points the (subpixel) target (n,3) and depth normal n_u
+ * (n,3); mask (H, W) u8 or NULL; world_to_cam = the camera pose's inverse;
+ * cos_max = cos(normal gate) */
+int cf_find_correspondences(const double* pts, const double* pt_normals, int64_t n, const double* depth, int height,
+                            int width, const uint8_t* mask, const double* normals_map, const cf_pinhole* cam,
+                            const cf_rigid* cam_pose, const cf_rigid* world_to_cam, double tau, double cos_max,
+                            double* target, double* n_u, uint8_t* keep, void* stream);
 /* CSR matrix on the device (int32 indices) */
 typedef struct cf_csr {
   const double* val;

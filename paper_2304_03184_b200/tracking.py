@@ -1,5 +1,6 @@
-"""Non-rigid tracking solve on the GPU — drop-in for capfields.tracking.pcg_solve
-(tracking.py:158-193), the inner solver of the tracker's Levenberg-Marquardt loop.
+"""Non-rigid tracking on the GPU — drop-ins for capfields.tracking's data association
+(depth_normals, find_correspondences; tracking.py:60-150) and the inner solver of its
+Levenberg-Marquardt loop (pcg_solve, tracking.py:158-193).
 
 SURVEY §8(f) 4. The Jacobi-preconditioned CG on (J^T J + lambda diag(J^T J)) x =
 -J^T r runs as one cooperative kernel (csrc/pcg.cu, `cf_pcg_solve`): both sparse
@@ -16,8 +17,61 @@ import torch
 
 from . import _lib
 
-PCG_ITERS = 32    # tracking.py:28-29
+PCG_ITERS = 32    # tracking.py:24-29
 PCG_TOL = 1e-6
+CORR_DIST = 0.03
+CORR_NORMAL_DEG = 60.0
+
+
+def _cam_parts(cam):
+    from .tsdf import _cam_pose, _inverse, _pinhole, _rigid
+    Rc, tc = _cam_pose(cam)
+    Rwc, twc = _inverse(Rc, tc)
+    return _pinhole(cam), _rigid(Rc, tc), _rigid(Rwc, twc)
+
+
+def _dev(a, dtype=torch.float64):
+    d = _lib.require_cuda()
+    t = a if isinstance(a, torch.Tensor) else torch.as_tensor(np.ascontiguousarray(np.asarray(a)))
+    return t.to(d, dtype).contiguous()
+
+
+def depth_normals(depth, cam, as_tensor: bool = False):
+    """World-space, camera-facing normals of a depth map (tracking.py:60-80); zero
+    vectors mark invalid pixels."""
+    D = _dev(depth)
+    H, W = int(D.shape[0]), int(D.shape[1])
+    pin, pose, _ = _cam_parts(cam)
+    out = torch.empty((H, W, 3), dtype=torch.float64, device=D.device)
+    _lib.call("cf_depth_normals", D.data_ptr(), H, W, _lib.byref(pin), _lib.byref(pose), out.data_ptr(),
+              _lib.stream_ptr())
+    return out if as_tensor else out.cpu().numpy()
+
+
+def find_correspondences(model_points, model_normals, depth, cam, mask=None, tau: float = CORR_DIST,
+                         normal_deg: float = CORR_NORMAL_DEG, normals_map=None):
+    """Projective association -> (model indices, targets, depth normals) (tracking.py:83-150)."""
+    on_dev = isinstance(model_points, torch.Tensor) and model_points.is_cuda
+    P = _dev(np.atleast_2d(model_points) if not on_dev else model_points)
+    N = _dev(model_normals)
+    D = _dev(depth)
+    H, W = int(D.shape[0]), int(D.shape[1])
+    M = None if mask is None else _dev(np.asarray(mask.cpu() if isinstance(mask, torch.Tensor) else mask) > 0,
+                                       torch.uint8)
+    nm = depth_normals(D, cam, as_tensor=True) if normals_map is None else _dev(normals_map)
+    pin, pose, w2c = _cam_parts(cam)
+    n = int(P.shape[0])
+    tgt = torch.empty((n, 3), dtype=torch.float64, device=D.device)
+    nu = torch.empty((n, 3), dtype=torch.float64, device=D.device)
+    keep = torch.empty(n, dtype=torch.uint8, device=D.device)
+    _lib.call("cf_find_correspondences", P.data_ptr(), N.data_ptr(), n, D.data_ptr(), H, W,
+              None if M is None else M.data_ptr(), nm.data_ptr(), _lib.byref(pin), _lib.byref(pose),
+              _lib.byref(w2c), float(tau), float(np.cos(np.deg2rad(normal_deg))), tgt.data_ptr(), nu.data_ptr(),
+              keep.data_ptr(), _lib.stream_ptr())
+    k = keep.bool()
+    idx = torch.nonzero(k).reshape(-1)
+    out = (idx, tgt[k], nu[k])
+    return out if on_dev else tuple(t.cpu().numpy() for t in out)
 
 
 def _csr_parts(J):
@@ -82,4 +136,5 @@ def pcg_solve(J, r, lm_lambda: float, max_iters: int = PCG_ITERS, tol: float = P
     return GaussNewtonSystem(J, r).solve(lm_lambda, max_iters, tol).cpu().numpy()
 
 
-__all__ = ["PCG_ITERS", "PCG_TOL", "GaussNewtonSystem", "pcg_solve"]
+__all__ = ["PCG_ITERS", "PCG_TOL", "CORR_DIST", "CORR_NORMAL_DEG", "GaussNewtonSystem", "pcg_solve",
+           "depth_normals", "find_correspondences"]
