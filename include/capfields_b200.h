@@ -408,6 +408,12 @@ int cf_gemm_kmajor_f16(const void* A, int64_t lda, const void* B, int64_t ldb, i
 /* fp32 (n x k) row-major weight -> fp16 UMMA canonical K-major blob (n, k padded to 16) */
 int cf_pack_weight(const float* w, int n, int k, uint8_t* blob, void* stream);
 
+/* device -> pinned host (cudaHostAlloc'd, UVA-mapped) copy by `ctas` CTAs of stores
+ * instead of a copy-engine memcpy (overlaps the next view's uploads); 16-byte aligned */
+int cf_store_to_host(const void* src, void* dst_host, int64_t bytes, int ctas, void* stream);
+/* small pinned host -> device upload by one CTA (not queued behind copy-engine transfers) */
+int cf_load_from_host(void* dst, const void* src_host, int64_t bytes, void* stream);
+
 /* ------------------------------------------------- motion-prior ingestion */
 /* CFMP v1 motion-prior stream (records.py:98-147): "CFMP", u32 version, u32
  * n_nodes, u32 n_theta, then per frame i64 frame_id and four length-prefixed

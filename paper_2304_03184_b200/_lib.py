@@ -202,6 +202,8 @@ _SIGS = {
                 ctypes.c_float, _p],
     "cf_pack_weight": [_p, _i32, _i32, _p, _p],
     "cf_gemm_kmajor_f16": [_p, _i64, _p, _i64, _i32, _i64, _p, _i32, _p],
+    "cf_store_to_host": [_p, _p, _i64, _i32, _p],
+    "cf_load_from_host": [_p, _p, _i64, _p],
     "cf_mp_scan": [ctypes.c_char_p, _P(MpInfo)],
     "cf_mp_read": [ctypes.c_char_p, _i64, _i64, _p, _p, _p, _p, _p],
     "cf_mp_write": [ctypes.c_char_p, _i32, _i32, _i32, _i64, _p, _p, _p, _p, _p],

@@ -97,3 +97,4 @@ int cf_version(void) { return 1; }
 const char* cf_last_error(void) { return g_last_error.c_str(); }
 int cf_device_sm_count(void) { return cf::sm_count(); }
 }
+

@@ -46,6 +46,21 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
+// Fill n 32-bit words with `value` by a kernel. The frame's buffer resets use this
+// instead of cudaMemsetAsync: memset nodes in the frame's graph went through the
+// copy engine and queued behind the previous frame's image read-back.
+static __global__ void fill_u32_kernel(uint32_t* __restrict__ p, uint32_t value, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = value;
+}
+inline void fill_u32(void* p, uint32_t value, int64_t n, cudaStream_t st) {
+  if (n <= 0) return;
+  const int block = 256;
+  int64_t grid = (n + block - 1) / block;
+  if (grid > 1024) grid = 1024;
+  fill_u32_kernel<<<(unsigned)grid, block, 0, st>>>(reinterpret_cast<uint32_t*>(p), value, n);
+}
+
 }  // namespace cf
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }

@@ -1025,6 +1025,12 @@ __global__ void layers_kernel(int64_t n, const float* __restrict__ hr, const flo
   pdl_trigger();
 }
 
+__global__ void __launch_bounds__(256) store_to_host_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                                            int64_t n16) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
 }  // namespace
 
 extern "C" {
@@ -1059,7 +1065,7 @@ int cf_occ_splat(const uint32_t* canon_bits, const cf_occ_grid* cg, const cf_buc
     return cf::fail(CF_E_BAD_ARG, "cf_occ_splat: bad args");
   cudaStream_t st = cf::as_stream(stream);
   const int64_t lwords = ((int64_t)lg->res * lg->res * lg->res + 31) / 32;
-  CF_CHECK_CUDA(cudaMemsetAsync(live_bits, 0, sizeof(uint32_t) * lwords, st));
+  cf::fill_u32(live_bits, 0u, lwords, st);
   const int64_t total = (int64_t)cg->res * cg->res * cg->res;
   const unsigned grid = cf::grid_for(total, 128, 8);
   const double r2 = radius * radius;
@@ -1076,7 +1082,7 @@ int cf_occ_cache(const uint32_t* canon_bits, const cf_occ_grid* cg, const cf_buc
   if (!canon_bits || !cg || !node_buckets || node_buckets->grid_res == 0 || k < 1 || k > 8 || !count)
     return cf::fail(CF_E_BAD_ARG, "cf_occ_cache: bad args");
   cudaStream_t st = cf::as_stream(stream);
-  CF_CHECK_CUDA(cudaMemsetAsync(count, 0, sizeof(int), st));
+  cf::fill_u32(count, 0u, 1, st);
   const int64_t total = (int64_t)cg->res * cg->res * cg->res;
   const unsigned grid = cf::grid_for(total, 128, 8);
   dispatch_k(k, [&]<int K>() {
@@ -1095,10 +1101,10 @@ int cf_occ_splat_cached(const int* cells, const int* nbr, const double* w, const
     return cf::fail(CF_E_BAD_ARG, "cf_occ_splat_cached: bad args");
   cudaStream_t st = cf::as_stream(stream);
   const int64_t P = lg->res + 2;
-  CF_CHECK_CUDA(cudaMemsetAsync(scratch_bits, 0, sizeof(uint32_t) * ((P * P * P + 31) / 32 + 3), st));
+  cf::fill_u32(scratch_bits, 0u, (P * P * P + 31) / 32 + 3, st);
   if (live_bbox) {  // lo = 0x7f7f7f7f, hi = 0x80808080 (negative)
-    CF_CHECK_CUDA(cudaMemsetAsync(live_bbox, 0x7f, 3 * sizeof(int), st));
-    CF_CHECK_CUDA(cudaMemsetAsync(live_bbox + 3, 0x80, 3 * sizeof(int), st));
+    cf::fill_u32(live_bbox, 0x7f7f7f7fu, 3, st);
+    cf::fill_u32(live_bbox + 3, 0x80808080u, 3, st);
   }
   const unsigned grid = cf::grid_for(capacity, 256, 4);
   if (k <= 4)
@@ -1126,8 +1132,8 @@ int cf_march(const cf_march_desc* M, const double* dirs, const uint32_t* human_b
   if (human && human_bits) H = *human;
   if (object && object_bits) O = *object;
   cudaStream_t st = cf::as_stream(stream);
-  if (H.records) CF_CHECK_CUDA(cudaMemsetAsync(H.counters, 0, 4 * sizeof(int), st));
-  if (O.records) CF_CHECK_CUDA(cudaMemsetAsync(O.counters, 0, 4 * sizeof(int), st));
+  if (H.records) cf::fill_u32(H.counters, 0u, 4, st);
+  if (O.records) cf::fill_u32(O.counters, 0u, 4, st);
   if (M->n_rays == 0) return CF_OK;
   cf::launch_pdl(march_kernel<false>, cf::grid_for(M->n_rays, 128, 8), 128, 0, st, *M, cf_camera{},
                  const_cast<double*>(dirs), H.records ? human_bits : nullptr, O.records ? object_bits : nullptr, H, O);
@@ -1143,8 +1149,8 @@ int cf_rays_march(const cf_camera* cam, const cf_march_desc* M, double* dirs, co
   if (human && human_bits) H = *human;
   if (object && object_bits) O = *object;
   cudaStream_t st = cf::as_stream(stream);
-  if (H.records) CF_CHECK_CUDA(cudaMemsetAsync(H.counters, 0, 4 * sizeof(int), st));
-  if (O.records) CF_CHECK_CUDA(cudaMemsetAsync(O.counters, 0, 4 * sizeof(int), st));
+  if (H.records) cf::fill_u32(H.counters, 0u, 4, st);
+  if (O.records) cf::fill_u32(O.counters, 0u, 4, st);
   cf::launch_pdl(march_kernel<true>, cf::grid_for(M->n_rays, 128, 8), 128, 0, st, *M, *cam, dirs,
                  H.records ? human_bits : nullptr, O.records ? object_bits : nullptr, H, O);
   return cf::check_launch("cf_rays_march");
@@ -1218,7 +1224,7 @@ int cf_train_sample(const cf_march_desc* M, const float* gt_depth, const uint8_t
       n_guided + n_uniform > 128 || n_empty > 128 || n_guided > 32)
     return cf::fail(CF_E_BAD_ARG, "cf_train_sample: bad args");
   cudaStream_t st = cf::as_stream(stream);
-  CF_CHECK_CUDA(cudaMemsetAsync(F->counters, 0, 4 * sizeof(int), st));
+  cf::fill_u32(F->counters, 0u, 4, st);
   if (M->n_rays == 0) return CF_OK;
   train_sample_kernel<<<cf::grid_for(M->n_rays, 128, 8), 128, 0, st>>>(*M, gt_depth, mask, n_guided, n_uniform,
                                                                         n_empty, sigma_d, seed, *F, t_out);
@@ -1257,6 +1263,33 @@ int cf_composite_final(const cf_march_desc* M, const cf_march_out* F, const floa
                  reinterpret_cast<const float4*>(field), t_term, rgb, depth, opacity, o_rgb, o_depth, o_opac, bg[0],
                  bg[1], bg[2], out, layer);
   return cf::check_launch("cf_composite_final");
+}
+
+// Device -> pinned-host copy by a few SMs storing straight into the (UVA-mapped)
+// pinned buffer: unlike a copy-engine memcpy it never queues in front of the next
+// frame's small host -> device uploads, so the read-back overlaps the next view.
+// Small host -> device upload by one CTA reading the pinned (UVA-mapped) source: it
+// never waits behind a copy-engine read-back of the previous view.
+int cf_load_from_host(void* dst, const void* src_host, int64_t bytes, void* stream) {
+  if (!dst || !src_host || bytes < 0 || (bytes % 16) != 0 || ((uintptr_t)dst | (uintptr_t)src_host) % 16 != 0)
+    return cf::fail(CF_E_BAD_ARG, "cf_load_from_host: 16-byte aligned buffers and sizes required");
+  if (bytes == 0) return CF_OK;
+  void* src = nullptr;
+  CF_CHECK_CUDA(cudaHostGetDevicePointer(&src, const_cast<void*>(src_host), 0));
+  store_to_host_kernel<<<1, 256, 0, cf::as_stream(stream)>>>(reinterpret_cast<const uint4*>(src),
+                                                             reinterpret_cast<uint4*>(dst), bytes / 16);
+  return cf::check_launch("cf_load_from_host");
+}
+
+int cf_store_to_host(const void* src, void* dst_host, int64_t bytes, int ctas, void* stream) {
+  if (!src || !dst_host || bytes < 0 || (bytes % 16) != 0 || ((uintptr_t)src | (uintptr_t)dst_host) % 16 != 0)
+    return cf::fail(CF_E_BAD_ARG, "cf_store_to_host: 16-byte aligned buffers and sizes required");
+  if (bytes == 0) return CF_OK;
+  void* dst = nullptr;
+  CF_CHECK_CUDA(cudaHostGetDevicePointer(&dst, dst_host, 0));
+  store_to_host_kernel<<<ctas < 1 ? 8 : ctas, 256, 0, cf::as_stream(stream)>>>(
+      reinterpret_cast<const uint4*>(src), reinterpret_cast<uint4*>(dst), bytes / 16);
+  return cf::check_launch("cf_store_to_host");
 }
 
 }  // extern "C"

@@ -31,6 +31,19 @@ CANON_GRID = HashGridConfig(16, 2, 19, 16, 2048)   # config.py:56-60
 DEFORM_GRID = HashGridConfig(8, 4, 17, 16, 256)    # SPEC.md:419 (L=8, F=4); T, N_max frozen in DESIGN.md §4
 
 
+def _stage(dst: torch.Tensor, src: torch.Tensor) -> None:
+    """Stream-ordered copy into a device buffer. Pinned host sources go through a
+    one-CTA load kernel instead of the copy engine: copy-engine uploads queue behind
+    the previous view's image read-back and would delay the next frame by its length."""
+    if (not src.is_cuda and src.is_pinned() and src.dtype == dst.dtype and src.is_contiguous()
+            and dst.is_contiguous() and src.numel() == dst.numel()
+            and (src.numel() * src.element_size()) % 16 == 0 and src.data_ptr() % 16 == 0):
+        _lib.call("cf_load_from_host", dst.data_ptr(), src.data_ptr(), src.numel() * src.element_size(),
+                  _lib.stream_ptr())
+    else:
+        dst.copy_(src, non_blocking=True)
+
+
 @dataclass
 class RenderConfig:
     n_samples: int = 128          # C2: 128 samples / ray
@@ -336,9 +349,8 @@ class Renderer:
             self._A = torch.empty((h.lbs.J, 4, 4), dtype=torch.float64, device=self.dirs.device)
             self.dbias = torch.empty(128, dtype=torch.float32, device=self.dirs.device)
             self._anchor_buckets = Buckets(n)
-        self._dqs.copy_(dqs, non_blocking=True)
-        self._A.copy_(bone_A, non_blocking=True)
-        self.dbias.copy_(dbias, non_blocking=True)
+        for dst, src in ((self._dqs, dqs), (self._A, bone_A), (self.dbias, dbias)):
+            _stage(dst, src)
         if getattr(self, "hw", None) is None:
             w = _lib.HumanWarp()
             w.dqs = self._dqs.data_ptr()
@@ -410,7 +422,7 @@ class Renderer:
             self._staging_ev[i].synchronize()
         buf = self._staging[i]
         buf.numpy()[:] = self._frame_host
-        self.frame_dev.copy_(buf, non_blocking=True)
+        _stage(self.frame_dev, buf)
         ev = torch.cuda.Event()
         ev.record()
         self._staging_ev[i] = ev
