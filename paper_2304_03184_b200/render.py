@@ -44,6 +44,25 @@ def _stage(dst: torch.Tensor, src: torch.Tensor) -> None:
         dst.copy_(src, non_blocking=True)
 
 
+
+class _ReadBack:
+    """Handle of one view's image read-back (Renderer.render_to_host)."""
+
+    def __init__(self, renderer, slot, img, ready):
+        self.r, self.slot, self.img, self.ready, self.event = renderer, slot, img, ready, None
+
+    def _ensure(self):
+        if self.event is None:  # no later view issued it: issue it now
+            self.r._issue_readback(self)
+
+    def synchronize(self) -> None:
+        self._ensure()
+        self.event.synchronize()
+
+    def query(self) -> bool:
+        self._ensure()
+        return self.event.query()
+
 @dataclass
 class RenderConfig:
     n_samples: int = 128          # C2: 128 samples / ray
@@ -284,6 +303,7 @@ class Renderer:
         self._copy_stream = None
         self._host_images = [None, None]
         self._copy_done = [None, None]
+        self._pending_rb = None
         self.layer = torch.empty(self.n_rays, dtype=torch.uint8, device=d)
         self.live_occ = occ_grid(cfg.world_min, cfg.world_size, cfg.live_occ_res)
         self.live_bits = torch.zeros((cfg.live_occ_res ** 3 + 31) // 32, dtype=torch.int32, device=d)
@@ -458,22 +478,37 @@ class Renderer:
 
     def render_to_host(self, R, t, fx, fy, cx, cy):
         """render() and read the image back into pinned host memory without
-        blocking: returns (event, host image); the image is valid once the event
-        completed. The device-to-host copy runs on a copy stream, overlapping the
-        next view (which renders into the other image buffer)."""
+        blocking: returns (handle, host image); the image is valid once
+        handle.synchronize() returned (or handle.query() is True).
+
+        The device-to-host copy runs on a copy stream. It is issued when the NEXT
+        view has enqueued its uploads (or when the handle is waited on), so the
+        read-back overlaps that view's kernels but never the host link traffic of
+        its inputs (uploads queued behind a 3 MB read-back delayed every frame)."""
         img = self.render(R, t, fx, fy, cx, cy)
         slot = self._img_slot ^ 1  # the buffer render() just used
         if self._copy_stream is None:
             self._copy_stream = torch.cuda.Stream(device=self.dirs.device)
         if self._host_images[slot] is None:
             self._host_images[slot] = torch.empty(img.shape, dtype=img.dtype).pin_memory()
-        self._copy_stream.wait_stream(torch.cuda.current_stream())
+        ready = torch.cuda.Event()
+        ready.record()
+        rb = _ReadBack(self, slot, img, ready)
+        self._pending_rb = rb
+        return rb, self._host_images[slot]  # reused two views later
+
+    def _issue_readback(self, rb, after=None) -> None:
+        """Enqueue rb's copy on the copy stream after `after` (an event on the
+        current stream), or after the view's own completion event."""
+        self._copy_stream.wait_event(after if after is not None else rb.ready)
         with torch.cuda.stream(self._copy_stream):
-            self._host_images[slot].copy_(img, non_blocking=True)
+            self._host_images[rb.slot].copy_(rb.img, non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(self._copy_stream)
-        self._copy_done[slot] = ev
-        return ev, self._host_images[slot]  # reused two views later
+        rb.event = ev
+        self._copy_done[rb.slot] = ev
+        if self._pending_rb is rb:
+            self._pending_rb = None
 
     def prepare_frame(self) -> None:
         """Run the pending per-frame human setup now (eager launches) — for callers
@@ -489,6 +524,11 @@ class Renderer:
         (read them after synchronizing, before the next view)."""
         self._set_camera(R, t, fx, fy, cx, cy)
         self._upload_frame()
+        if getattr(self, "_pending_rb", None) is not None:
+            # the previous view's read-back starts once this view's uploads are done
+            after = torch.cuda.Event()
+            after.record()
+            self._issue_readback(self._pending_rb, after)
         setup = self._setup_pending and self.human is not None
         self._setup_pending = False
         timed = self.marks is not None

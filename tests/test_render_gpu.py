@@ -271,3 +271,17 @@ def test_human_canon_dense_graph_and_eager_equals_graph():
     ed = ref[:, 3] == 1
     ulp = np.abs(got[ed, :3].view(np.int32) - ref[ed, :3].view(np.int32))
     assert ulp.max() <= 1 and (ulp == 0).mean() > 0.999
+
+
+def test_render_to_host_readback(setup):
+    """render_to_host: the read-back of view k is issued by view k+1 (after its
+    uploads) or by waiting on the handle; both deliver the view's exact image."""
+    sc, cfg, hf, of, r, fid, img = setup
+    cam = sc.camera
+    ref = r.render(cam.R, cam.t, cam.fx, cam.fy, cam.cx, cam.cy).clone()
+    h1, host1 = r.render_to_host(cam.R, cam.t, cam.fx, cam.fy, cam.cx, cam.cy)
+    h2, host2 = r.render_to_host(cam.R, cam.t, cam.fx, cam.fy, cam.cx, cam.cy)  # issues h1's copy
+    h1.synchronize()
+    assert torch.equal(host1, ref.cpu())
+    h2.synchronize()  # nothing issued it: the handle does
+    assert torch.equal(host2, ref.cpu())
