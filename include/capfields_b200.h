@@ -546,6 +546,16 @@ int cf_find_correspondences(const double* pts, const double* pt_normals, int64_t
                             int width, const uint8_t* mask, const double* normals_map, const cf_pinhole* cam,
                             const cf_rigid* cam_pose, const cf_rigid* world_to_cam, double tau, double cos_max,
                             double* target, double* n_u, uint8_t* keep, void* stream);
+/* rigid_icp (tracking.py:560-620) building blocks: transform model points / normals by
+ * T; point-to-plane residuals of the kept correspondences (0 elsewhere); the Huber-
+ * weighted 6x6 normal equations sums[0..21) = upper triangle of Jr^T Jr (row-major),
+ * sums[21..27) = Jr^T (w r) (zeroed here, accumulated with fp64 atomics) */
+int cf_rigid_transform(const double* pts, const double* normals, int64_t n, const cf_rigid* T, double* out_pts,
+                       double* out_normals, void* stream);
+int cf_icp_residuals(const double* live, const uint8_t* keep, const double* target, const double* n_u, int64_t n,
+                     double* r, void* stream);
+int cf_icp_normal_equations(const double* live, const uint8_t* keep, const double* n_u, const double* r, int64_t n,
+                            double knee, double* sums, void* stream);
 /* CSR matrix on the device (int32 indices) */
 typedef struct cf_csr {
   const double* val;

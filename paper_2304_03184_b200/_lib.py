@@ -218,6 +218,9 @@ _SIGS = {
     "cf_tsdf_crossings": [_P(TsdfDesc), _i32, _p, _p, _p],
     "cf_pcg_workspace_doubles": [_i32, _i32, _P(ctypes.c_int64)],
     "cf_depth_normals": [_p, _i32, _i32, _P(Pinhole), _P(Rigid), _p, _p],
+    "cf_rigid_transform": [_p, _p, _i64, _P(Rigid), _p, _p, _p],
+    "cf_icp_residuals": [_p, _p, _p, _p, _i64, _p, _p],
+    "cf_icp_normal_equations": [_p, _p, _p, _p, _i64, ctypes.c_double, _p, _p],
     "cf_find_correspondences": [_p, _p, _i64, _p, _i32, _i32, _p, _p, _P(Pinhole), _P(Rigid), _P(Rigid),
                                 ctypes.c_double, ctypes.c_double, _p, _p, _p, _p],
     "cf_pcg_solve": [_P(Csr), _P(Csr), _p, ctypes.c_double, _i32, ctypes.c_double, _p, _p, _p, _p],

@@ -136,6 +136,83 @@ __global__ void __launch_bounds__(256) corr_kernel(const double* __restrict__ pt
   }
 }
 
+// rigid_icp (tracking.py:560-620): live = pose(model), rotated normals
+__global__ void __launch_bounds__(256) rigid_xform_kernel(const double* __restrict__ pts, const double* __restrict__ nrm,
+                                                          int64_t n, cf_rigid T, double* __restrict__ out_p,
+                                                          double* __restrict__ out_n) {
+  cf_rigid Rt = T;
+  Rt.t[0] = Rt.t[1] = Rt.t[2] = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double o[3];
+    pose_apply(T, pts + 3 * i, o);
+    out_p[3 * i] = o[0], out_p[3 * i + 1] = o[1], out_p[3 * i + 2] = o[2];
+    pose_apply(Rt, nrm + 3 * i, o);  // normals @ R^T (+ 0)
+    out_n[3 * i] = o[0], out_n[3 * i + 1] = o[1], out_n[3 * i + 2] = o[2];
+  }
+}
+
+// point-to-plane residual r = n_u . (p - u) of the kept pairs (0 elsewhere)
+__global__ void __launch_bounds__(256) icp_residual_kernel(const double* __restrict__ live,
+                                                           const uint8_t* __restrict__ keep,
+                                                           const double* __restrict__ tgt,
+                                                           const double* __restrict__ nu, int64_t n,
+                                                           double* __restrict__ r) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double v = 0.0;
+    if (keep[i]) {
+      const double* p = live + 3 * i;
+      v = __dadd_rn(__dadd_rn(__dmul_rn(nu[3 * i], __dsub_rn(p[0], tgt[3 * i])),
+                              __dmul_rn(nu[3 * i + 1], __dsub_rn(p[1], tgt[3 * i + 1]))),
+                    __dmul_rn(nu[3 * i + 2], __dsub_rn(p[2], tgt[3 * i + 2])));
+    }
+    r[i] = v;
+  }
+}
+
+// Huber-weighted normal equations: sums[0..21) = upper triangle of Jr^T Jr (row-major),
+// sums[21..27) = Jr^T (w r); Jr = w [p x n_u, n_u], w = sqrt(min(1, knee / |r|))
+__global__ void __launch_bounds__(256) icp_normal_eq_kernel(const double* __restrict__ live,
+                                                            const uint8_t* __restrict__ keep,
+                                                            const double* __restrict__ nu,
+                                                            const double* __restrict__ r, int64_t n, double knee,
+                                                            double* __restrict__ sums) {
+  double acc[27];
+#pragma unroll
+  for (int k = 0; k < 27; ++k) acc[k] = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (!keep[i]) continue;
+    const double* p = live + 3 * i;
+    const double* m = nu + 3 * i;
+    const double ri = r[i];
+    const double w = sqrt(fmin(1.0, knee / fmax(fabs(ri), 1e-300)));
+    const double j[6] = {w * (p[1] * m[2] - p[2] * m[1]), w * (p[2] * m[0] - p[0] * m[2]),
+                         w * (p[0] * m[1] - p[1] * m[0]), w * m[0], w * m[1], w * m[2]};
+    const double rw = w * ri;
+    int q = 0;
+#pragma unroll
+    for (int a = 0; a < 6; ++a)
+#pragma unroll
+      for (int b = a; b < 6; ++b) acc[q++] += j[a] * j[b];
+#pragma unroll
+    for (int a = 0; a < 6; ++a) acc[21 + a] += j[a] * rw;
+  }
+  __shared__ double red[27][8];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x / 32;
+#pragma unroll
+  for (int k = 0; k < 27; ++k) {
+    double v = acc[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[k][wp] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 27) {
+    double v = 0.0;
+    for (int k = 0; k < (int)(blockDim.x / 32); ++k) v += red[threadIdx.x][k];
+    atomicAdd(&sums[threadIdx.x], v);
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -162,6 +239,36 @@ int cf_find_correspondences(const double* pts, const double* pt_normals, int64_t
       pts, pt_normals, n, depth, height, width, mask, normals_map, *cam, *cam_pose, *world_to_cam, tau, cos_max,
       target, n_u, keep);
   return cf::check_launch("cf_find_correspondences");
+}
+
+int cf_rigid_transform(const double* pts, const double* normals, int64_t n, const cf_rigid* T, double* out_pts,
+                       double* out_normals, void* stream) {
+  if (n < 0 || !T || (n > 0 && (!pts || !normals || !out_pts || !out_normals)))
+    return cf::fail(CF_E_BAD_ARG, "cf_rigid_transform: bad args");
+  if (n == 0) return CF_OK;
+  rigid_xform_kernel<<<cf::grid_for(n, 256, 8), 256, 0, cf::as_stream(stream)>>>(pts, normals, n, *T, out_pts,
+                                                                                 out_normals);
+  return cf::check_launch("cf_rigid_transform");
+}
+
+int cf_icp_residuals(const double* live, const uint8_t* keep, const double* target, const double* n_u, int64_t n,
+                     double* r, void* stream) {
+  if (n < 0 || (n > 0 && (!live || !keep || !target || !n_u || !r)))
+    return cf::fail(CF_E_BAD_ARG, "cf_icp_residuals: bad args");
+  if (n == 0) return CF_OK;
+  icp_residual_kernel<<<cf::grid_for(n, 256, 8), 256, 0, cf::as_stream(stream)>>>(live, keep, target, n_u, n, r);
+  return cf::check_launch("cf_icp_residuals");
+}
+
+int cf_icp_normal_equations(const double* live, const uint8_t* keep, const double* n_u, const double* r, int64_t n,
+                            double knee, double* sums, void* stream) {
+  if (n < 0 || !sums || (n > 0 && (!live || !keep || !n_u || !r)))
+    return cf::fail(CF_E_BAD_ARG, "cf_icp_normal_equations: bad args");
+  cudaStream_t st = cf::as_stream(stream);
+  cf::fill_u32(sums, 0u, 27 * 2, st);
+  if (n == 0) return CF_OK;
+  icp_normal_eq_kernel<<<cf::grid_for(n, 256, 2), 256, 0, st>>>(live, keep, n_u, r, n, knee, sums);
+  return cf::check_launch("cf_icp_normal_equations");
 }
 
 }  // extern "C"

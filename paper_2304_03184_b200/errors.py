@@ -3,6 +3,7 @@
 OutOfSupportError      capfields/edgraph.py:27
 DegenerateWeightsError capfields/transforms.py:15
 RecordFormatError      capfields/records.py:24
+InsufficientOverlapError capfields/tracking.py:33
 """
 from __future__ import annotations
 
@@ -18,6 +19,13 @@ except Exception:  # the reference is not installed on the GPU box
         """A blend received no positive weight."""
 
 try:
+    from capfields.tracking import InsufficientOverlapError  # type: ignore
+except Exception:
+
+    class InsufficientOverlapError(ValueError):
+        """Too few valid depth pixels to constrain a pose."""
+
+try:
     from capfields.records import RecordFormatError  # type: ignore
 except Exception:
 
@@ -25,4 +33,4 @@ except Exception:
         """A record file with a bad magic, version or payload."""
 
 
-__all__ = ["OutOfSupportError", "DegenerateWeightsError", "RecordFormatError"]
+__all__ = ["OutOfSupportError", "DegenerateWeightsError", "RecordFormatError", "InsufficientOverlapError"]

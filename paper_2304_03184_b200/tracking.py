@@ -16,6 +16,7 @@ import numpy as np
 import torch
 
 from . import _lib
+from .errors import InsufficientOverlapError
 
 PCG_ITERS = 32    # tracking.py:24-29
 PCG_TOL = 1e-6
@@ -72,6 +73,100 @@ def find_correspondences(model_points, model_normals, depth, cam, mask=None, tau
     idx = torch.nonzero(k).reshape(-1)
     out = (idx, tgt[k], nu[k])
     return out if on_dev else tuple(t.cpu().numpy() for t in out)
+
+
+def _rotmat(rv) -> np.ndarray:
+    """rotmat_from_rotvec (transforms.py:66-111), numpy's operation order."""
+    rv = np.asarray(rv, dtype=np.float64)
+    ang = np.linalg.norm(rv, axis=-1, keepdims=True)
+    half = 0.5 * ang
+    small = ang < 1e-12
+    with np.errstate(invalid="ignore", divide="ignore"):
+        k = np.where(small, 0.5 - ang * ang / 48.0, np.sin(half) / np.where(small, 1.0, ang))
+    w, (x, y, z) = np.cos(half)[0], k * rv
+    return np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)],
+                     [2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)],
+                     [2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)]])
+
+
+class _Pose:
+    """Rigid transform with the reference Se3's rotation / translation attributes."""
+
+    def __init__(self, R, t):
+        self.rotation = np.asarray(R, dtype=np.float64).reshape(3, 3)
+        self.translation = np.asarray(t, dtype=np.float64).reshape(3)
+
+
+def rigid_icp(volume_or_model, depth, cam, mask, init, max_iters: int = 15, tau: float = 0.05,
+              min_pixels: int = 30, normal_deg: float = 30.0):
+    """Projective point-to-plane ICP refining init (canonical -> world), tracking.py:560-620.
+
+    Per iteration on the device: model transform, association, residuals and the
+    Huber-weighted 6x6 normal equations; the host solves the 6x6 system (with the
+    reference's Tikhonov damping and trust region) and composes the pose."""
+    from .tsdf import TsdfVolume, _rigid
+    D = _dev(depth)
+    M = None if mask is None else _dev(np.asarray(mask.cpu() if isinstance(mask, torch.Tensor) else mask) > 0,
+                                       torch.uint8)
+    valid = (D > 0) if M is None else ((D > 0) & (M > 0))
+    n_valid = int(valid.sum())
+    if n_valid < min_pixels:
+        raise InsufficientOverlapError(f"only {n_valid} valid depth pixels")
+    if isinstance(volume_or_model, TsdfVolume):
+        mp, mn = volume_or_model.extract_surface()
+        if len(mp) < min_pixels:
+            raise InsufficientOverlapError("TSDF surface is empty")
+    else:
+        mp, mn = volume_or_model
+    P, N = _dev(mp), _dev(mn)
+    n = int(P.shape[0])
+    H, W = int(D.shape[0]), int(D.shape[1])
+    nmap = depth_normals(D, cam, as_tensor=True)
+    pin, cpose, w2c = _cam_parts(cam)
+    live = torch.empty_like(P)
+    ln = torch.empty_like(N)
+    tgt = torch.empty_like(P)
+    nu = torch.empty_like(P)
+    keep = torch.empty(n, dtype=torch.uint8, device=D.device)
+    r = torch.empty(n, dtype=torch.float64, device=D.device)
+    sums = torch.empty(27, dtype=torch.float64, device=D.device)
+    cos_max = float(np.cos(np.deg2rad(normal_deg)))
+    R = np.asarray(init.rotation, dtype=np.float64).copy()
+    t = np.asarray(init.translation, dtype=np.float64).copy()
+    s = _lib.stream_ptr()
+    iu = np.triu_indices(6)
+    for _ in range(max_iters):
+        _lib.call("cf_rigid_transform", P.data_ptr(), N.data_ptr(), n, _lib.byref(_rigid(R, t)), live.data_ptr(),
+                  ln.data_ptr(), s)
+        _lib.call("cf_find_correspondences", live.data_ptr(), ln.data_ptr(), n, D.data_ptr(), H, W,
+                  None if M is None else M.data_ptr(), nmap.data_ptr(), _lib.byref(pin), _lib.byref(cpose),
+                  _lib.byref(w2c), float(tau), cos_max, tgt.data_ptr(), nu.data_ptr(), keep.data_ptr(), s)
+        _lib.call("cf_icp_residuals", live.data_ptr(), keep.data_ptr(), tgt.data_ptr(), nu.data_ptr(), n,
+                  r.data_ptr(), s)
+        k = keep.bool()
+        ar = r[k].abs()
+        C = int(ar.numel())
+        if C < min_pixels:
+            raise InsufficientOverlapError(f"only {C} ICP correspondences")
+        sa = torch.sort(ar).values  # np.median: the middle value, or the mean of the two middle ones
+        med = float(sa[C // 2]) if C % 2 else float((sa[C // 2 - 1] + sa[C // 2]) / 2.0)
+        knee = max(3.0 * med, 1e-5)
+        _lib.call("cf_icp_normal_equations", live.data_ptr(), keep.data_ptr(), nu.data_ptr(), r.data_ptr(), n,
+                  knee, sums.data_ptr(), s)
+        h = sums.cpu().numpy()
+        A = np.zeros((6, 6))
+        A[iu] = h[:21]
+        A = A + np.triu(A, 1).T
+        A += (1e-6 * np.trace(A) / 6.0 + 1e-12) * np.eye(6)
+        delta = np.linalg.solve(A, -h[21:])
+        rot_n = np.linalg.norm(delta[:3])
+        tr_n = np.linalg.norm(delta[3:])
+        delta *= min(1.0, 0.2 / max(rot_n, 1e-12), 0.05 / max(tr_n, 1e-12))
+        Ru = _rotmat(delta[:3])
+        R, t = Ru @ R, Ru @ t + delta[3:]  # Se3.compose (transforms.py:289-290)
+        if np.max(np.abs(delta)) < 1e-12:
+            break
+    return _Pose(R, t)
 
 
 def _csr_parts(J):
@@ -137,4 +232,4 @@ def pcg_solve(J, r, lm_lambda: float, max_iters: int = PCG_ITERS, tol: float = P
 
 
 __all__ = ["PCG_ITERS", "PCG_TOL", "CORR_DIST", "CORR_NORMAL_DEG", "GaussNewtonSystem", "pcg_solve",
-           "depth_normals", "find_correspondences"]
+           "depth_normals", "find_correspondences", "rigid_icp", "InsufficientOverlapError"]
