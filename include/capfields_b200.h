@@ -411,6 +411,16 @@ int cf_pack_weight(const float* w, int n, int k, uint8_t* blob, void* stream);
 /* device -> pinned host (cudaHostAlloc'd, UVA-mapped) copy by `ctas` CTAs of stores
  * instead of a copy-engine memcpy (overlaps the next view's uploads); 16-byte aligned */
 int cf_store_to_host(const void* src, void* dst_host, int64_t bytes, int ctas, void* stream);
+/* up to CF_COPY_BATCH_MAX small copies in one kernel launch (sources: device memory or
+ * pinned host memory, read through its mapping); one CTA per entry */
+#define CF_COPY_BATCH_MAX 8
+typedef struct cf_copy_list {
+  int n;
+  const void* src[CF_COPY_BATCH_MAX];
+  void* dst[CF_COPY_BATCH_MAX];
+  int64_t bytes[CF_COPY_BATCH_MAX];
+} cf_copy_list;
+int cf_copy_batch(const cf_copy_list* list, void* stream);
 /* small pinned host -> device upload by one CTA (not queued behind copy-engine transfers) */
 int cf_load_from_host(void* dst, const void* src_host, int64_t bytes, void* stream);
 

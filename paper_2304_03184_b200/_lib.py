@@ -137,6 +137,11 @@ class Csr(ctypes.Structure):
                 ("rows", ctypes.c_int), ("cols", ctypes.c_int), ("nnz", ctypes.c_int64)]
 
 
+class CopyList(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int), ("src", ctypes.c_void_p * 8), ("dst", ctypes.c_void_p * 8),
+                ("bytes", ctypes.c_int64 * 8)]
+
+
 class DeformBwdIO(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in ("save_h", "save_o", "save_mask", "d_o", "dpre", "d_dfeat")]
 
@@ -204,6 +209,7 @@ _SIGS = {
     "cf_gemm_kmajor_f16": [_p, _i64, _p, _i64, _i32, _i64, _p, _i32, _p],
     "cf_store_to_host": [_p, _p, _i64, _i32, _p],
     "cf_load_from_host": [_p, _p, _i64, _p],
+    "cf_copy_batch": [_P(CopyList), _p],
     "cf_mp_scan": [ctypes.c_char_p, _P(MpInfo)],
     "cf_mp_read": [ctypes.c_char_p, _i64, _i64, _p, _p, _p, _p, _p],
     "cf_mp_write": [ctypes.c_char_p, _i32, _i32, _i32, _i64, _p, _p, _p, _p, _p],

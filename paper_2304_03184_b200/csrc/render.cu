@@ -1031,6 +1031,22 @@ __global__ void __launch_bounds__(256) store_to_host_kernel(const uint4* __restr
     dst[i] = src[i];
 }
 
+// several small copies (device or UVA-mapped pinned host sources) in ONE launch:
+// one CTA per entry, 16-byte moves where both ends allow it
+__global__ void __launch_bounds__(256) copy_batch_kernel(cf_copy_list L) {
+  const int e = blockIdx.x;
+  if (e >= L.n) return;
+  const uint8_t* src = reinterpret_cast<const uint8_t*>(L.src[e]);
+  uint8_t* dst = reinterpret_cast<uint8_t*>(L.dst[e]);
+  const int64_t bytes = L.bytes[e];
+  if ((((uintptr_t)src | (uintptr_t)dst | (uintptr_t)bytes) & 15) == 0) {
+    for (int64_t i = threadIdx.x; i < bytes / 16; i += blockDim.x)
+      reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+  } else {
+    for (int64_t i = threadIdx.x; i < bytes; i += blockDim.x) dst[i] = src[i];
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -1290,6 +1306,25 @@ int cf_store_to_host(const void* src, void* dst_host, int64_t bytes, int ctas, v
   store_to_host_kernel<<<ctas < 1 ? 8 : ctas, 256, 0, cf::as_stream(stream)>>>(
       reinterpret_cast<const uint4*>(src), reinterpret_cast<uint4*>(dst), bytes / 16);
   return cf::check_launch("cf_store_to_host");
+}
+
+int cf_copy_batch(const cf_copy_list* list, void* stream) {
+  if (!list || list->n < 0 || list->n > CF_COPY_BATCH_MAX) return cf::fail(CF_E_BAD_ARG, "cf_copy_batch: bad list");
+  if (list->n == 0) return CF_OK;
+  cf_copy_list L = *list;
+  for (int e = 0; e < L.n; ++e) {
+    if (!L.src[e] || !L.dst[e] || L.bytes[e] < 0) return cf::fail(CF_E_BAD_ARG, "cf_copy_batch: bad entry");
+    cudaPointerAttributes a;
+    CF_CHECK_CUDA(cudaPointerGetAttributes(&a, L.src[e]));
+    if (a.type == cudaMemoryTypeHost) {
+      if (!a.devicePointer) return cf::fail(CF_E_BAD_ARG, "cf_copy_batch: host source is not mapped (pin it)");
+      L.src[e] = a.devicePointer;
+    } else if (a.type == cudaMemoryTypeUnregistered) {
+      return cf::fail(CF_E_BAD_ARG, "cf_copy_batch: pageable host source (pin it)");
+    }
+  }
+  copy_batch_kernel<<<L.n, 256, 0, cf::as_stream(stream)>>>(L);
+  return cf::check_launch("cf_copy_batch");
 }
 
 }  // extern "C"

@@ -31,20 +31,6 @@ CANON_GRID = HashGridConfig(16, 2, 19, 16, 2048)   # config.py:56-60
 DEFORM_GRID = HashGridConfig(8, 4, 17, 16, 256)    # SPEC.md:419 (L=8, F=4); T, N_max frozen in DESIGN.md §4
 
 
-def _stage(dst: torch.Tensor, src: torch.Tensor) -> None:
-    """Stream-ordered copy into a device buffer. Pinned host sources go through a
-    one-CTA load kernel instead of the copy engine: copy-engine uploads queue behind
-    the previous view's image read-back and would delay the next frame by its length."""
-    if (not src.is_cuda and src.is_pinned() and src.dtype == dst.dtype and src.is_contiguous()
-            and dst.is_contiguous() and src.numel() == dst.numel()
-            and (src.numel() * src.element_size()) % 16 == 0 and src.data_ptr() % 16 == 0):
-        _lib.call("cf_load_from_host", dst.data_ptr(), src.data_ptr(), src.numel() * src.element_size(),
-                  _lib.stream_ptr())
-    else:
-        dst.copy_(src, non_blocking=True)
-
-
-
 class _ReadBack:
     """Handle of one view's image read-back (Renderer.render_to_host)."""
 
@@ -62,6 +48,7 @@ class _ReadBack:
     def query(self) -> bool:
         self._ensure()
         return self.event.query()
+
 
 @dataclass
 class RenderConfig:
@@ -369,8 +356,10 @@ class Renderer:
             self._A = torch.empty((h.lbs.J, 4, 4), dtype=torch.float64, device=self.dirs.device)
             self.dbias = torch.empty(128, dtype=torch.float32, device=self.dirs.device)
             self._anchor_buckets = Buckets(n)
+        # enqueued with the next view's frame block as one batched copy (sources must
+        # stay valid until that view, or prepare_frame, is issued)
         for dst, src in ((self._dqs, dqs), (self._A, bone_A), (self.dbias, dbias)):
-            _stage(dst, src)
+            self._defer_copy(dst, src)
         if getattr(self, "hw", None) is None:
             w = _lib.HumanWarp()
             w.dqs = self._dqs.data_ptr()
@@ -390,6 +379,7 @@ class Renderer:
     def _human_setup(self) -> None:
         """The frame's human setup kernels: backward-LBS chain on the side stream,
         deformed nodes + live occupancy splat on the current stream."""
+        self._flush_copies()
         s = _lib.stream_ptr()
         h = self.human
         n = self._dqs.shape[0]
@@ -426,6 +416,7 @@ class Renderer:
         """Camera of the view (frame block) and its ray directions."""
         self._set_camera(R, t, fx, fy, cx, cy)
         self._upload_frame()
+        self._flush_copies()
         self._rays()
 
     def _set_camera(self, R, t, fx, fy, cx, cy):
@@ -442,10 +433,43 @@ class Renderer:
             self._staging_ev[i].synchronize()
         buf = self._staging[i]
         buf.numpy()[:] = self._frame_host
-        _stage(self.frame_dev, buf)
-        ev = torch.cuda.Event()
-        ev.record()
-        self._staging_ev[i] = ev
+        self._defer_copy(self.frame_dev, buf, staging_slot=i)
+
+    def _defer_copy(self, dst: torch.Tensor, src: torch.Tensor, staging_slot: int | None = None) -> None:
+        if not hasattr(self, "_pending_copies"):
+            self._pending_copies = {}
+        self._pending_copies[dst.data_ptr()] = (dst, src, staging_slot)
+
+    def _flush_copies(self) -> None:
+        """Issue the deferred small copies (prior + frame block) as ONE kernel launch
+        on the current stream; sources that cannot be read by the device (pageable
+        host memory, dtype / size mismatch) fall back to a stream-ordered copy_."""
+        pend = getattr(self, "_pending_copies", None)
+        if not pend:
+            return
+        L = _lib.CopyList()
+        rest = []
+        slots = []
+        for dst, src, slot in pend.values():
+            ok = (src.dtype == dst.dtype and src.numel() == dst.numel() and src.is_contiguous()
+                  and dst.is_contiguous() and (src.is_cuda or src.is_pinned()) and L.n < 8)
+            if ok:
+                L.src[L.n], L.dst[L.n] = src.data_ptr(), dst.data_ptr()
+                L.bytes[L.n] = src.numel() * src.element_size()
+                L.n += 1
+            else:
+                rest.append((dst, src))
+            if slot is not None:
+                slots.append(slot)
+        _lib.call("cf_copy_batch", _lib.byref(L), _lib.stream_ptr())
+        for dst, src in rest:
+            dst.copy_(src, non_blocking=True)
+        if slots:
+            ev = torch.cuda.Event()
+            ev.record()
+            for i in slots:
+                self._staging_ev[i] = ev
+        pend.clear()
 
     def _rays(self):
         _lib.call("cf_camera_rays", _lib.byref(self.cam), self.dirs.data_ptr(), _lib.stream_ptr())
@@ -524,6 +548,7 @@ class Renderer:
         (read them after synchronizing, before the next view)."""
         self._set_camera(R, t, fx, fy, cx, cy)
         self._upload_frame()
+        self._flush_copies()
         if getattr(self, "_pending_rb", None) is not None:
             # the previous view's read-back starts once this view's uploads are done
             after = torch.cuda.Event()
