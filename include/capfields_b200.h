@@ -127,6 +127,11 @@ int cf_knnfield_query(const int32_t* live, const int32_t* neighbor_idx, const do
 /* forward LBS (skeleton.py:142-149): A (J,4,4) float64, weights (N,J). */
 int cf_lbs_forward(const double* A, int J, const double* pts, const double* weights, int64_t n_pts, double* out,
                    void* stream);
+/* pose Jacobian of forward LBS by central differences (tracking.py:244-256): A_pm
+ * (2T, J, 4, 4) = bone transforms at theta +/- fd_step e_k (k-major, + first);
+ * out (n, 3, T) = (LBS(A+) - LBS(A-)) / (2 fd_step) */
+int cf_lbs_theta_jacobian(const double* A_pm, int n_theta, int J, const double* pts, const double* weights,
+                          int64_t n_pts, double fd_step, double* out, void* stream);
 /* per-frame vertex transforms for the backward warp: T_v = sum_j W[v,j] A_j[:3,:],
  * Tinv_v its inverse, both (V,3,4) row-major; T_out may be NULL. */
 int cf_lbs_vertex_transforms(const double* A, int J, const double* vert_weights, int64_t n_verts, double* T_out,

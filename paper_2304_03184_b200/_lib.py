@@ -225,6 +225,7 @@ _SIGS = {
     "cf_pcg_workspace_doubles": [_i32, _i32, _P(ctypes.c_int64)],
     "cf_depth_normals": [_p, _i32, _i32, _P(Pinhole), _P(Rigid), _p, _p],
     "cf_rigid_transform": [_p, _p, _i64, _P(Rigid), _p, _p, _p],
+    "cf_lbs_theta_jacobian": [_p, _i32, _i32, _p, _p, _i64, ctypes.c_double, _p, _p],
     "cf_icp_residuals": [_p, _p, _p, _p, _i64, _p, _p],
     "cf_icp_normal_equations": [_p, _p, _p, _p, _i64, ctypes.c_double, _p, _p],
     "cf_find_correspondences": [_p, _p, _i64, _p, _i32, _i32, _p, _p, _P(Pinhole), _P(Rigid), _P(Rigid),

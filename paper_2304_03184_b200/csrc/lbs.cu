@@ -163,6 +163,38 @@ __global__ void __launch_bounds__(128, 4) lbs_backward_kernel(const BucketParams
   }
 }
 
+// Central finite differences of forward LBS w.r.t. the pose (tracking.py:244-256,
+// _lbs_theta_jacobian): A_pm = (2T, J, 4, 4) with A_pm[2k] = A(theta + h e_k),
+// A_pm[2k+1] = A(theta - h e_k); one thread per (point, k).
+__device__ __forceinline__ void lbs_point(const double* __restrict__ A, int J, const double* __restrict__ w,
+                                          const double* p, double* o) {
+  o[0] = o[1] = o[2] = 0.0;
+  for (int j = 0; j < J; ++j) {
+    const double wj = w[j];
+    if (wj == 0.0) continue;
+    const double* M = A + 16 * j;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) o[a] += wj * (M[4 * a] * p[0] + M[4 * a + 1] * p[1] + M[4 * a + 2] * p[2] + M[4 * a + 3]);
+  }
+}
+
+__global__ void __launch_bounds__(128) lbs_theta_jac_kernel(const double* __restrict__ Apm, int T, int J,
+                                                            const double* __restrict__ pts,
+                                                            const double* __restrict__ W, int64_t n, double inv2h,
+                                                            double* __restrict__ out) {
+  const int64_t total = n * T;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = q / T;
+    const int k = (int)(q % T);
+    const double p[3] = {pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]};
+    double hi[3], lo[3];
+    lbs_point(Apm + (int64_t)(2 * k) * 16 * J, J, W + i * J, p, hi);
+    lbs_point(Apm + (int64_t)(2 * k + 1) * 16 * J, J, W + i * J, p, lo);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) out[(i * 3 + a) * T + k] = (hi[a] - lo[a]) * inv2h;
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -211,6 +243,16 @@ int cf_lbs_backward(const cf_buckets_t* vert_buckets, const double* verts_posed,
     lbs_backward_kernel<false><<<grid, 128, 0, st>>>(nullptr, nullptr, nullptr, verts_posed, n_verts, vert_Tinv, md2,
                                                       pts, n_pts, vert_out, pc_out, valid_out);
   return cf::check_launch("cf_lbs_backward");
+}
+
+int cf_lbs_theta_jacobian(const double* A_pm, int n_theta, int J, const double* pts, const double* weights,
+                          int64_t n_pts, double fd_step, double* out, void* stream) {
+  if (!A_pm || n_theta < 1 || J < 1 || n_pts < 0 || !(fd_step > 0.0) || (n_pts > 0 && (!pts || !weights || !out)))
+    return cf::fail(CF_E_BAD_ARG, "cf_lbs_theta_jacobian: bad args");
+  if (n_pts == 0) return CF_OK;
+  lbs_theta_jac_kernel<<<cf::grid_for(n_pts * n_theta, 128, 8), 128, 0, cf::as_stream(stream)>>>(
+      A_pm, n_theta, J, pts, weights, n_pts, 1.0 / (2.0 * fd_step), out);
+  return cf::check_launch("cf_lbs_theta_jacobian");
 }
 
 }  // extern "C"

@@ -20,6 +20,7 @@ from .errors import InsufficientOverlapError
 
 PCG_ITERS = 32    # tracking.py:24-29
 PCG_TOL = 1e-6
+FD_STEP = 1e-6
 CORR_DIST = 0.03
 CORR_NORMAL_DEG = 60.0
 
@@ -169,6 +170,32 @@ def rigid_icp(volume_or_model, depth, cam, mask, init, max_iters: int = 15, tau:
     return _Pose(R, t)
 
 
+def lbs_theta_jacobian(skel, theta, pts, weights, as_tensor: bool = False):
+    """Central finite differences of lbs_batch w.r.t. theta -> (P, 3, T)
+    (_lbs_theta_jacobian, tracking.py:244-256): the 2T perturbed poses' forward
+    kinematics in one device launch (records.skinning_transforms), then one thread
+    per (point, pose component)."""
+    from .records import skinning_transforms
+    theta = np.asarray(theta, dtype=np.float64).reshape(-1)
+    T = len(theta)
+    th = np.repeat(theta[None], 2 * T, axis=0)
+    for k in range(T):  # the reference's theta + e and theta - e (tracking.py:250-254)
+        e = np.zeros(T)
+        e[k] = FD_STEP
+        th[2 * k] = theta + e
+        th[2 * k + 1] = theta - e
+    d = _lib.require_cuda()
+    A = skinning_transforms(torch.from_numpy(th).to(d), skel)
+    P = _dev(np.atleast_2d(pts))
+    Wt = _dev(weights)
+    n = int(P.shape[0])
+    J = int(A.shape[1])
+    out = torch.empty((n, 3, T), dtype=torch.float64, device=d)
+    _lib.call("cf_lbs_theta_jacobian", A.data_ptr(), T, J, P.data_ptr(), Wt.data_ptr(), n, FD_STEP, out.data_ptr(),
+              _lib.stream_ptr())
+    return out if as_tensor else out.cpu().numpy()
+
+
 def _csr_parts(J):
     """(val, col, rowptr, rows, cols) from a scipy.sparse matrix or a tuple."""
     if hasattr(J, "tocsr"):
@@ -232,4 +259,4 @@ def pcg_solve(J, r, lm_lambda: float, max_iters: int = PCG_ITERS, tol: float = P
 
 
 __all__ = ["PCG_ITERS", "PCG_TOL", "CORR_DIST", "CORR_NORMAL_DEG", "GaussNewtonSystem", "pcg_solve",
-           "depth_normals", "find_correspondences", "rigid_icp", "InsufficientOverlapError"]
+           "depth_normals", "find_correspondences", "rigid_icp", "InsufficientOverlapError", "lbs_theta_jacobian"]

@@ -53,3 +53,17 @@ def test_find_correspondences(ref):
         assert np.array_equal(idx, ri), key
         assert len(idx) > 100
         assert np.abs(tgt - rt).max() <= 1e-12 and np.abs(nu - rn).max() <= 1e-12, key
+
+
+def test_lbs_theta_jacobian():
+    """Central-difference pose Jacobian of forward LBS (tracking.py:244-256) vs the
+    reference's on its tracked bend pose (tests/golden/make_lbsjac.py). The FD step is
+    1e-6, so ulp-level differences in the bone transforms (device FK vs numpy/BLAS)
+    become ~1e-10 in the quotient: compared at 1e-8."""
+    from paper_2304_03184_b200.tracking import lbs_theta_jacobian
+    with np.load(os.path.join(GOLDEN, "lbsjac_ref.npz")) as z:
+        g = {k: z[k] for k in z.files}
+    for pts, w, key in ((g["nodes"], g["nw"], "jn"), (g["pts"], g["pw"], "jp")):
+        j = lbs_theta_jacobian(None, g["theta"], pts, w)
+        assert j.shape == g[key].shape
+        assert np.abs(j - g[key]).max() <= 1e-8, (key, np.abs(j - g[key]).max())
