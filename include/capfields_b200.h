@@ -571,6 +571,51 @@ int cf_icp_residuals(const double* live, const uint8_t* keep, const double* targ
                      double* r, void* stream);
 int cf_icp_normal_equations(const double* live, const uint8_t* keep, const double* n_u, const double* r, int64_t n,
                             double knee, double* sums, void* stream);
+/* Non-rigid tracker (tracking.py:270-508) on the device. cf_nr_warp: apply_blended
+ * (edgraph.py:198-205) of n samples with fixed neighbours idx (n,k) int32 and weights
+ * w (n,k). cf_nr_terms: the data / bind / reg / pose terms of energy_terms
+ * (unweighted sums -> energy[0..4)) and, when val != NULL, their Jacobian rows in CSR
+ * (val / col at each term's entry offset, residuals at its row offset; rows: data 6k
+ * entries, bind 6+T, reg 12, pose T). cf_nr_step: _apply_step's node update. */
+typedef struct cf_nr_system {
+  const double* dqs;
+  const double* nodes;
+  int n_nodes, n_theta;
+  const double* warped;
+  const int64_t* data_idx;
+  const double* data_u;
+  const double* data_n;
+  int64_t n_data;
+  const int* blend_idx;
+  const double* blend_wn;
+  int k;
+  double w_data;
+  int64_t data_row0, data_entry0;
+  int do_bind;
+  const double* node_lbs;
+  const double* node_jth;
+  double s_bind;
+  int64_t bind_row0, bind_entry0;
+  const int64_t* edges;
+  int64_t n_edges;
+  double s_reg;
+  int64_t reg_row0, reg_entry0;
+  const double* pose_lbs;
+  const double* pose_u;
+  const double* pose_n;
+  const double* pose_jth;
+  int64_t n_pose;
+  double w_pose;
+  int64_t pose_row0, pose_entry0;
+  double* val;
+  int* col;
+  double* res;
+  double* energy;
+} cf_nr_system;
+int cf_nr_warp(const double* dqs, const int* idx, const double* w, int k, const double* pts, const double* normals,
+               int64_t n, double* out_pts, double* out_normals, void* stream);
+int cf_nr_terms(const cf_nr_system* S, void* stream);
+int cf_nr_step(const double* dqs, const double* delta, int n, double* out, void* stream);
 /* CSR matrix on the device (int32 indices) */
 typedef struct cf_csr {
   const double* val;

@@ -142,6 +142,21 @@ class CopyList(ctypes.Structure):
                 ("bytes", ctypes.c_int64 * 8)]
 
 
+class NrSystem(ctypes.Structure):
+    _p = ctypes.c_void_p
+    _fields_ = [("dqs", _p), ("nodes", _p), ("n_nodes", ctypes.c_int), ("n_theta", ctypes.c_int),
+                ("warped", _p), ("data_idx", _p), ("data_u", _p), ("data_n", _p), ("n_data", ctypes.c_int64),
+                ("blend_idx", _p), ("blend_wn", _p), ("k", ctypes.c_int), ("w_data", ctypes.c_double),
+                ("data_row0", ctypes.c_int64), ("data_entry0", ctypes.c_int64),
+                ("do_bind", ctypes.c_int), ("node_lbs", _p), ("node_jth", _p), ("s_bind", ctypes.c_double),
+                ("bind_row0", ctypes.c_int64), ("bind_entry0", ctypes.c_int64),
+                ("edges", _p), ("n_edges", ctypes.c_int64), ("s_reg", ctypes.c_double),
+                ("reg_row0", ctypes.c_int64), ("reg_entry0", ctypes.c_int64),
+                ("pose_lbs", _p), ("pose_u", _p), ("pose_n", _p), ("pose_jth", _p), ("n_pose", ctypes.c_int64),
+                ("w_pose", ctypes.c_double), ("pose_row0", ctypes.c_int64), ("pose_entry0", ctypes.c_int64),
+                ("val", _p), ("col", _p), ("res", _p), ("energy", _p)]
+
+
 class DeformBwdIO(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in ("save_h", "save_o", "save_mask", "d_o", "dpre", "d_dfeat")]
 
@@ -226,6 +241,9 @@ _SIGS = {
     "cf_depth_normals": [_p, _i32, _i32, _P(Pinhole), _P(Rigid), _p, _p],
     "cf_rigid_transform": [_p, _p, _i64, _P(Rigid), _p, _p, _p],
     "cf_lbs_theta_jacobian": [_p, _i32, _i32, _p, _p, _i64, ctypes.c_double, _p, _p],
+    "cf_nr_warp": [_p, _p, _p, _i32, _p, _p, _i64, _p, _p, _p],
+    "cf_nr_terms": [_P(NrSystem), _p],
+    "cf_nr_step": [_p, _p, _i32, _p, _p],
     "cf_icp_residuals": [_p, _p, _p, _p, _i64, _p, _p],
     "cf_icp_normal_equations": [_p, _p, _p, _p, _i64, ctypes.c_double, _p, _p],
     "cf_find_correspondences": [_p, _p, _i64, _p, _i32, _i32, _p, _p, _P(Pinhole), _P(Rigid), _P(Rigid),

@@ -186,7 +186,7 @@ def lbs_theta_jacobian(skel, theta, pts, weights, as_tensor: bool = False):
         th[2 * k + 1] = theta - e
     d = _lib.require_cuda()
     A = skinning_transforms(torch.from_numpy(th).to(d), skel)
-    P = _dev(np.atleast_2d(pts))
+    P = pts.to(d, torch.float64).contiguous() if isinstance(pts, torch.Tensor) else _dev(np.atleast_2d(pts))
     Wt = _dev(weights)
     n = int(P.shape[0])
     J = int(A.shape[1])
@@ -212,7 +212,7 @@ class GaussNewtonSystem:
         d = _lib.require_cuda()
         val, col, rowptr, rows, cols = _csr_parts(J)
         self.rows, self.cols = int(rows), int(cols)
-        as_t = lambda a, dt: torch.as_tensor(np.asarray(a), dtype=dt).to(d)  # noqa: E731
+        as_t = lambda a, dt: (a if isinstance(a, torch.Tensor) else torch.as_tensor(np.asarray(a))).to(d, dt)  # noqa: E731
         self.val = as_t(val, torch.float64).contiguous()
         self.col = as_t(col, torch.int32).contiguous()
         self.rowptr = as_t(rowptr, torch.int32).contiguous()
@@ -259,4 +259,258 @@ def pcg_solve(J, r, lm_lambda: float, max_iters: int = PCG_ITERS, tol: float = P
 
 
 __all__ = ["PCG_ITERS", "PCG_TOL", "CORR_DIST", "CORR_NORMAL_DEG", "GaussNewtonSystem", "pcg_solve",
-           "depth_normals", "find_correspondences", "rigid_icp", "InsufficientOverlapError", "lbs_theta_jacobian"]
+           "depth_normals", "find_correspondences", "rigid_icp", "InsufficientOverlapError", "lbs_theta_jacobian",
+           "NonrigidTracker", "SolveState", "EnergyWeights"]
+
+
+# ---------------------------------------------------------------------------
+# non-rigid tracker (tracking.py:196-556) with every per-iteration stage on the device
+# ---------------------------------------------------------------------------
+
+LM_LAMBDA_INIT = 1e-3   # tracking.py:26-27
+LM_LAMBDA_CAP = 1e6
+EDGE_K = 8
+
+
+class EnergyWeights:
+    """tracking.py:37-49."""
+
+    def __init__(self, data=1.0, bind=1.0, reg=4.0, prior=0.01, pose=0.02, inter=1.0):
+        self.data, self.bind, self.reg, self.prior, self.pose, self.inter = data, bind, reg, prior, pose, inter
+        for name in ("data", "bind", "reg", "prior", "pose", "inter"):
+            if getattr(self, name) < 0:
+                raise ValueError(f"energy weight {name} must be nonnegative")
+
+
+class SolveState:
+    """Node dual quaternions (n, 8) on the device and the pose theta (T,) on the host."""
+
+    def __init__(self, dqs, theta):
+        self.dqs_dev = _dev(dqs)
+        self.theta = np.asarray(theta, dtype=np.float64).copy()
+
+    @property
+    def dqs(self) -> np.ndarray:
+        return self.dqs_dev.cpu().numpy()
+
+    def copy(self) -> "SolveState":
+        return SolveState(self.dqs_dev.clone(), self.theta.copy())
+
+
+class NonrigidTracker:
+    """GPU drop-in for capfields.tracking.NonrigidTracker (tracking.py:259-556): the same
+    constructor and solve(); `model` is duck-typed (graph.nodes / radius / knn_k,
+    skeleton.parents / offsets / joint_limits, points, normals, lbs_weights,
+    node_lbs_weights, edges). The object-interpenetration term is not supported."""
+
+    def __init__(self, model, cam, weights=None, surface_samples: int = 4096, max_iters: int = 8,
+                 object_volume=None, seed: int = 0):
+        if object_volume is not None:
+            raise NotImplementedError("the interpenetration term is not built on the device")
+        from .knnfield import brute_force_neighbors_batch
+        self.model, self.cam = model, cam
+        self.weights = weights or EnergyWeights()
+        self.max_iters = max_iters
+        rng = np.random.default_rng(seed)
+        pts, nrm = np.asarray(model.points, dtype=np.float64), np.asarray(model.normals, dtype=np.float64)
+        take = min(surface_samples, len(pts))
+        sel = rng.choice(len(pts), size=take, replace=False)  # tracking.py:286-291
+        self.sub_pts, self.sub_normals = pts[sel], nrm[sel]
+        self.sub_lbs = np.asarray(model.lbs_weights, dtype=np.float64)[sel]
+        g = model.graph
+        self.nodes = np.asarray(g.nodes, dtype=np.float64)
+        k = int(min(g.knn_k, len(self.nodes)))
+        idx = brute_force_neighbors_batch(g, self.sub_pts, k)  # exact, ties by index (edgraph.py:121-131)
+        d2 = np.sum((self.sub_pts[:, None, :] - self.nodes[idx]) ** 2, axis=-1)
+        w = np.exp(-d2 / (g.radius * g.radius))  # canonical_blend_info (edgraph.py:186-195)
+        wn = w / np.maximum(w.sum(axis=1, keepdims=True), 1e-300)
+        self.k = k
+        self.d_idx, self.d_w, self.d_wn = _dev(idx, torch.int32), _dev(w), _dev(wn)
+        self.d_pts, self.d_nrm = _dev(self.sub_pts), _dev(self.sub_normals)
+        self.d_lbs = _dev(self.sub_lbs)
+        self.d_nodes = _dev(self.nodes)
+        self.node_w = np.asarray(model.node_lbs_weights, dtype=np.float64)
+        self.d_node_w = _dev(self.node_w)
+        e = model.edges if getattr(model, "edges", None) is not None else g.edges(EDGE_K)
+        self.edges = np.asarray(e, dtype=np.int64).reshape(-1, 2)
+        self.d_edges = _dev(self.edges, torch.int64)
+        self.skel = model.skeleton
+        self.lim = np.repeat(np.asarray(model.skeleton.joint_limits, dtype=np.float64), 3)
+        self.dom = _dev(np.argmax(self.sub_lbs, axis=1), torch.int64)
+        n = len(self.nodes)
+        dq = np.zeros((n, 8))
+        dq[:, 0] = 1.0
+        self.state = SolveState(dq, np.zeros(3 * len(np.asarray(model.skeleton.parents))))
+        self._e = torch.zeros(4, dtype=torch.float64, device=self.d_nodes.device)
+
+    # -- per-state quantities ----------------------------------------------------
+
+    def _bones(self, theta):
+        from .records import skinning_transforms
+        return skinning_transforms(torch.from_numpy(np.asarray(theta, dtype=np.float64)[None]).to(
+            self.d_nodes.device), self.skel)[0].contiguous()
+
+    def _lbs(self, A, pts, w):
+        out = torch.empty_like(pts)
+        _lib.call("cf_lbs_forward", A.data_ptr(), int(A.shape[0]), pts.data_ptr(), w.data_ptr(), int(pts.shape[0]),
+                  out.data_ptr(), _lib.stream_ptr())
+        return out
+
+    def warp_subset(self, state):
+        out_p, out_n = torch.empty_like(self.d_pts), torch.empty_like(self.d_nrm)
+        _lib.call("cf_nr_warp", state.dqs_dev.data_ptr(), self.d_idx.data_ptr(), self.d_w.data_ptr(), self.k,
+                  self.d_pts.data_ptr(), self.d_nrm.data_ptr(), int(self.d_pts.shape[0]), out_p.data_ptr(),
+                  out_n.data_ptr(), _lib.stream_ptr())
+        return out_p, out_n
+
+    def _associate(self, state, D, mask, nmap):
+        warped, wn = self.warp_subset(state)
+        data_corr = find_correspondences(warped, wn, D, self.cam, mask=mask, normals_map=nmap)
+        A = self._bones(state.theta)
+        lp = self._lbs(A, self.d_pts, self.d_lbs)
+        ln = torch.einsum("nab,nb->na", A[self.dom][:, :3, :3], self.d_nrm).contiguous()
+        pose_corr = find_correspondences(lp, ln, D, self.cam, mask=mask, normals_map=nmap)
+        return data_corr, pose_corr
+
+    def _system(self, state, data_corr, pose_corr, with_jacobian: bool):
+        """energy_terms (tracking.py:288-336) and, with_jacobian, _assemble (358-508)."""
+        w = self.weights
+        n, T = len(self.nodes), len(state.theta)
+        A = self._bones(state.theta)
+        warped, _ = self.warp_subset(state)
+        ci, cu, cn = data_corr
+        pi, pu, pn = pose_corr
+        node_lbs = self._lbs(A, self.d_nodes, self.d_node_w)
+        P = int(pi.numel())
+        pose_lbs = self._lbs(A, self.d_pts[pi].contiguous(), self.d_lbs[pi].contiguous()) if P else None
+        lim_r = np.maximum(0.0, np.abs(state.theta) - self.lim)
+        act = np.nonzero(lim_r > 0)[0]
+        C, E = int(ci.numel()), len(self.edges)
+        use = dict(data=C > 0 and w.data > 0, bind=w.bind > 0, reg=E > 0 and w.reg > 0, prior=w.prior > 0 and len(act),
+                   pose=P > 0 and w.pose > 0)
+        S = _lib.NrSystem()
+        S.dqs, S.nodes, S.n_nodes, S.n_theta = state.dqs_dev.data_ptr(), self.d_nodes.data_ptr(), n, T
+        S.warped, S.n_data = warped.data_ptr(), C
+        if C:
+            S.data_idx, S.data_u, S.data_n = ci.data_ptr(), cu.data_ptr(), cn.data_ptr()
+        S.blend_idx, S.blend_wn, S.k, S.w_data = self.d_idx.data_ptr(), self.d_wn.data_ptr(), self.k, w.data
+        S.do_bind, S.node_lbs, S.s_bind = 1, node_lbs.data_ptr(), float(np.sqrt(w.bind))
+        S.edges, S.n_edges, S.s_reg = self.d_edges.data_ptr(), E, float(np.sqrt(w.reg))
+        S.n_pose, S.w_pose = P, w.pose
+        if P:
+            S.pose_lbs, S.pose_u, S.pose_n = pose_lbs.data_ptr(), pu.data_ptr(), pn.data_ptr()
+        S.energy = self._e.data_ptr()
+        J = r = None
+        if with_jacobian:
+            sizes = [("data", C if use["data"] else 0, 6 * self.k), ("bind", 3 * n if use["bind"] else 0, 6 + T),
+                     ("reg", 3 * E if use["reg"] else 0, 12), ("prior", len(act) if use["prior"] else 0, 1),
+                     ("pose", P if use["pose"] else 0, T)]
+            rows = sum(s[1] for s in sizes)
+            if rows == 0:
+                return self._energy(state), None, None
+            nnz = sum(s[1] * s[2] for s in sizes)
+            d = self.d_nodes.device
+            val = torch.zeros(nnz, dtype=torch.float64, device=d)
+            col = torch.zeros(nnz, dtype=torch.int32, device=d)
+            res = torch.zeros(rows, dtype=torch.float64, device=d)
+            row0, ent0, off = 0, 0, {}
+            for name, nr, per in sizes:
+                off[name] = (row0, ent0)
+                row0 += nr
+                ent0 += nr * per
+            S.val, S.col, S.res = val.data_ptr(), col.data_ptr(), res.data_ptr()
+            S.data_row0, S.data_entry0 = off["data"]
+            S.bind_row0, S.bind_entry0 = off["bind"]
+            S.reg_row0, S.reg_entry0 = off["reg"]
+            S.pose_row0, S.pose_entry0 = off["pose"]
+            if not use["data"]:
+                S.n_data = 0
+            if not use["bind"]:
+                S.do_bind = 0
+            if not use["reg"]:
+                S.n_edges = 0
+            if use["bind"]:
+                jn = lbs_theta_jacobian(self.skel, state.theta, self.d_nodes, self.d_node_w, as_tensor=True)
+                S.node_jth = jn.data_ptr()
+            if use["pose"]:
+                jp = lbs_theta_jacobian(self.skel, state.theta, self.d_pts[pi].contiguous(),
+                                        self.d_lbs[pi].contiguous(), as_tensor=True)
+                S.pose_jth = jp.data_ptr()
+            else:
+                S.n_pose = 0
+            _lib.call("cf_nr_terms", _lib.byref(S), _lib.stream_ptr())
+            if use["prior"]:  # quadratic joint-limit rows (tracking.py:445-456)
+                s = np.sqrt(w.prior)
+                r0, e0 = off["prior"]
+                val[e0:e0 + len(act)] = torch.from_numpy(s * np.sign(state.theta[act])).to(d)
+                col[e0:e0 + len(act)] = torch.from_numpy((6 * n + act).astype(np.int32)).to(d)
+                res[r0:r0 + len(act)] = torch.from_numpy(s * lim_r[act]).to(d)
+            counts = torch.cat([torch.full((nr,), per, dtype=torch.int64, device=d) for _, nr, per in sizes if nr])
+            rowptr = torch.cat([torch.zeros(1, dtype=torch.int64, device=d), torch.cumsum(counts, 0)]).to(torch.int32)
+            J = (val, col, rowptr, (rows, 6 * n + T))
+            r = res
+        else:
+            _lib.call("cf_nr_terms", _lib.byref(S), _lib.stream_ptr())
+        return self._energy(state, lim_r), J, r
+
+    def _energy(self, state, lim_r=None):
+        w = self.weights
+        e = self._e.cpu().numpy()
+        if lim_r is None:
+            lim_r = np.maximum(0.0, np.abs(state.theta) - self.lim)
+        out = {"data": float(e[0]), "bind": float(e[1]), "reg": float(e[2]), "prior": float(np.sum(lim_r ** 2)),
+               "pose": float(e[3]), "inter": 0.0}
+        out["total"] = (w.data * out["data"] + w.bind * out["bind"] + w.reg * out["reg"] + w.prior * out["prior"]
+                        + w.pose * out["pose"] + w.inter * out["inter"])
+        return out
+
+    def energy_terms(self, state, data_corr, pose_corr) -> dict:
+        return self._system(state, data_corr, pose_corr, False)[0]
+
+    def _apply_step(self, state, delta):
+        n = len(self.nodes)
+        out = torch.empty_like(state.dqs_dev)
+        _lib.call("cf_nr_step", state.dqs_dev.data_ptr(), delta.data_ptr(), n, out.data_ptr(), _lib.stream_ptr())
+        return SolveState(out, state.theta + delta[6 * n:].cpu().numpy())
+
+    def solve(self, depth, mask, frame_id: int, init=None):
+        """LM outer loop with correspondences refreshed every iteration (tracking.py:510-544)."""
+        state = (init or self.state).copy()
+        if not isinstance(state, SolveState):
+            state = SolveState(state.dqs, state.theta)
+        lm = LM_LAMBDA_INIT
+        D = _dev(depth)
+        M = None if mask is None else _dev(np.asarray(mask.cpu() if isinstance(mask, torch.Tensor) else mask) > 0,
+                                           torch.uint8)
+        nmap = depth_normals(D, self.cam, as_tensor=True)
+        info = {"accepted": [], "warning": False, "iterations": 0, "energies": []}
+        best = state
+        delta = None
+        for it in range(self.max_iters):
+            data_corr, pose_corr = self._associate(state, D, M, nmap)
+            e0, J, r = self._system(state, data_corr, pose_corr, True)
+            info["energies"].append(e0)
+            if J is None:
+                break
+            sysm = GaussNewtonSystem(J, r)
+            stepped = False
+            while lm <= LM_LAMBDA_CAP:
+                delta = sysm.solve(lm)
+                cand = self._apply_step(state, delta)
+                e1 = self.energy_terms(cand, data_corr, pose_corr)
+                if e1["total"] <= e0["total"] + 1e-15:
+                    info["accepted"].append((e0["total"], e1["total"]))
+                    state = cand
+                    best = cand
+                    lm = max(lm * 0.5, 1e-9)
+                    stepped = True
+                    break
+                lm *= 10.0
+            info["iterations"] = it + 1
+            if not stepped:
+                info["warning"] = True
+                break
+            if float(delta.abs().max()) < 1e-10:
+                break
+        self.state = best
+        return best, info
