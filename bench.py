@@ -834,6 +834,31 @@ def run_frontend(args, rank, world, pg):
     for _ in range(5):
         otr.pcg_solve_sparse(Js, pj["r"], 1e-4)
     pcg_cpu_us = (time.perf_counter() - t0) * 1e6 / 5
+    # -- non-rigid tracking: the reference's bend-tracking scene (tests/golden/tracker_ref.npz)
+    from paper_2304_03184_b200.tracking import NonrigidTracker
+    with np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "tests", "golden", "tracker_ref.npz")) as z:
+        tz = {k: z[k] for k in z.files}
+
+    class _NS:
+        def __init__(self, **kw):
+            self.__dict__.update(kw)
+    tmodel = _NS(graph=_NS(nodes=tz["nodes"], radius=float(tz["radius"]), knn_k=int(tz["knn_k"])),
+                 skeleton=_NS(parents=tz["parents"], offsets=tz["offsets"], joint_limits=tz["joint_limits"]),
+                 points=tz["points"], normals=tz["normals"], lbs_weights=tz["lbs_weights"],
+                 node_lbs_weights=tz["node_lbs_weights"], edges=tz["edges"])
+    c = tz["cam"]
+    tcam2 = _NS(fx=float(c[0]), fy=float(c[1]), cx=float(c[2]), cy=float(c[3]), width=int(c[4]), height=int(c[5]),
+                pose=_NS(rotation=tz["cam_R"], translation=tz["cam_t"]))
+    NonrigidTracker(tmodel, tcam2, surface_samples=1500).solve(tz["depth0"], tz["mask0"], 0)  # warm
+    torch.cuda.synchronize()
+    ntr = NonrigidTracker(tmodel, tcam2, surface_samples=1500)
+    t0 = time.perf_counter()
+    n_iters = 0
+    for fid in range(4):
+        _, tinfo = ntr.solve(tz[f"depth{fid}"], tz[f"mask{fid}"], fid)
+        n_iters += tinfo["iterations"]
+    torch.cuda.synchronize()
+    track_ms = (time.perf_counter() - t0) * 1e3 / 4
     line = {"metric": "front-end stages: key-frame selection per tracked frame; motion-prior ingestion",
             "value": 1e3 / sel_ms, "unit": "tracked frames/s (selection)", "n_gpus": 1, "higher_is_better": True,
             "ms_per_frame_selection": sel_ms, "dtype": "u8 / f64 / int",
@@ -842,6 +867,9 @@ def run_frontend(args, rank, world, pg):
                        "decode_upload_fk_s": ingest_s, "fk_us_per_1000_frames": fk_us},
             "tsdf": {"resolution": 256, "integrate_ms": integ_ms, "voxels_per_s": 256 ** 3 / (integ_ms * 1e-3),
                      "raycast_512x512_ms": ray_ms, "raycast_hits": int(len(rp))},
+            "nonrigid_tracking": {"scene": "reference bend test, 142 nodes, 1500 surface samples, 128^2 depth",
+                                  "ms_per_frame": track_ms, "lm_iterations_per_frame": n_iters / 4,
+                                  "reference_cpu_s_per_frame": "2.9 (measured in the build container, 8 cores)"},
             "pcg": {"system": f"{int(pj['shape'][0])}x{int(pj['shape'][1])}, nnz {len(pj['val'])} (reference tracker)",
                     "iterations": 32, "gpu_us_per_solve": pcg_us, "cpu_scipy_us_per_solve": pcg_cpu_us},
             "cpu_baseline": {"value": 1e3 / cpu_ms, "unit": "tracked frames/s", "cores": 1, "kind": "port",
