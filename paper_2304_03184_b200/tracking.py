@@ -378,8 +378,12 @@ class NonrigidTracker:
         n, T = len(self.nodes), len(state.theta)
         A = self._bones(state.theta)
         warped, _ = self.warp_subset(state)
-        ci, cu, cn = data_corr
-        pi, pu, pn = pose_corr
+        conv = lambda c: (_dev(np.asarray(c[0]).reshape(-1), torch.int64) if not isinstance(c[0], torch.Tensor)  # noqa: E731
+                          else c[0], _dev(np.asarray(c[1]).reshape(-1, 3)) if not isinstance(c[1], torch.Tensor)
+                          else c[1], _dev(np.asarray(c[2]).reshape(-1, 3)) if not isinstance(c[2], torch.Tensor)
+                          else c[2])
+        ci, cu, cn = conv(data_corr)
+        pi, pu, pn = conv(pose_corr)
         node_lbs = self._lbs(A, self.d_nodes, self.d_node_w)
         P = int(pi.numel())
         pose_lbs = self._lbs(A, self.d_pts[pi].contiguous(), self.d_lbs[pi].contiguous()) if P else None

@@ -65,3 +65,30 @@ def test_tracker_matches_reference(ref):
         print(fid, info["iterations"], "gap to reference", gap.mean(), gap.max(), "err vs gt", err_gt,
               "theta gap", np.abs(state.theta - ref[f"theta{fid}"]).max())
         assert gap.max() <= 1e-3, (fid, gap.max())
+
+
+def test_energy_terms_reference_properties(ref):
+    """The reference's energy-term oracles (tests/test_tracking.py:113-137) on the
+    device tracker: ARAP energy of one displaced node, point-to-plane invariance to a
+    tangential slide of the target, and zero energy terms at the rest state."""
+    from paper_2304_03184_b200.tracking import NonrigidTracker, SolveState
+    model, cam = _model(ref)
+    tr = NonrigidTracker(model, cam, surface_samples=800)
+    n = len(ref["nodes"])
+    dq = np.zeros((n, 8))
+    dq[:, 0] = 1.0
+    rest = SolveState(dq, np.zeros(72))
+    empty = (np.zeros(0, dtype=np.int64), np.zeros((0, 3)), np.zeros((0, 3)))
+    e = tr.energy_terms(rest, empty, empty)
+    assert e["reg"] == 0.0 and e["data"] == 0.0 and e["pose"] == 0.0 and e["bind"] < 1e-20
+    moved = dq.copy()
+    moved[0, 5] = 0.5 * 0.05  # pure translation (0.05, 0, 0): dual = 0.5 * t * real
+    e = tr.energy_terms(SolveState(moved, np.zeros(72)), empty, empty)
+    edges = ref["edges"]
+    touched = (edges[:, 0] == 0) | (edges[:, 1] == 0)
+    assert abs(e["reg"] - touched.sum() * 0.05 ** 2) < 1e-12
+    nrm = np.array([[0.0, 0.0, 1.0]])
+    u0 = tr.sub_pts[:1] + np.array([[0.0, 0.0, 0.004]])
+    e0 = tr.energy_terms(rest, (np.array([0]), u0, nrm), empty)
+    e1 = tr.energy_terms(rest, (np.array([0]), u0 + np.array([[0.013, -0.007, 0.0]]), nrm), empty)
+    assert e0["data"] > 0 and abs(e0["data"] - e1["data"]) < 1e-14
