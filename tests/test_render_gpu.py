@@ -285,3 +285,34 @@ def test_render_to_host_readback(setup):
     assert torch.equal(host1, ref.cpu())
     h2.synchronize()  # nothing issued it: the handle does
     assert torch.equal(host2, ref.cpu())
+
+
+def test_small_copy_entry_points():
+    """cf_copy_batch (device and pinned-host sources), cf_load_from_host and
+    cf_store_to_host move the bytes exactly."""
+    from paper_2304_03184_b200 import _lib
+    g = torch.Generator().manual_seed(0)
+    srcs = [torch.randn(1024, generator=g, dtype=torch.float64).pin_memory(), torch.randn(13, dtype=torch.float64).cuda(),
+            torch.randint(0, 255, (37,), dtype=torch.uint8).pin_memory()]
+    dsts = [torch.empty(1024, dtype=torch.float64, device="cuda"), torch.empty(13, dtype=torch.float64, device="cuda"),
+            torch.empty(37, dtype=torch.uint8, device="cuda")]
+    L = _lib.CopyList()
+    for i, (s_, d_) in enumerate(zip(srcs, dsts)):
+        L.src[i], L.dst[i], L.bytes[i] = s_.data_ptr(), d_.data_ptr(), s_.numel() * s_.element_size()
+    L.n = 3
+    _lib.call("cf_copy_batch", _lib.byref(L), _lib.stream_ptr())
+    torch.cuda.synchronize()
+    for s_, d_ in zip(srcs, dsts):
+        assert torch.equal(d_.cpu(), s_.cpu())
+    with pytest.raises(ValueError):  # pageable host memory is refused
+        L2 = _lib.CopyList()
+        pageable = torch.zeros(16, dtype=torch.float64)
+        L2.n, L2.src[0], L2.dst[0], L2.bytes[0] = 1, pageable.data_ptr(), dsts[0].data_ptr(), 128
+        _lib.call("cf_copy_batch", _lib.byref(L2), _lib.stream_ptr())
+    h = torch.randn(4096, dtype=torch.float32).pin_memory()
+    dv = torch.empty(4096, dtype=torch.float32, device="cuda")
+    _lib.call("cf_load_from_host", dv.data_ptr(), h.data_ptr(), 4096 * 4, _lib.stream_ptr())
+    back = torch.empty(4096, dtype=torch.float32).pin_memory()
+    _lib.call("cf_store_to_host", dv.data_ptr(), back.data_ptr(), 4096 * 4, 8, _lib.stream_ptr())
+    torch.cuda.synchronize()
+    assert torch.equal(back, h)
