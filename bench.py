@@ -31,7 +31,7 @@ UNIT = "samples/s"
 FLOP_PER_SAMPLE_HUMAN = 2 * (32 * 128 + 3 * 128 * 128 + 128 * 16) + 2 * (32 * 64 + 64 * 16) + 2 * (
     32 * 64 + 64 * 64 + 64 * 16)  # 131,072 (DeformNet + E_g + E_c, padded widths as issued)
 FLOP_PER_SAMPLE_OBJECT = 2 * (32 * 64 + 64 * 16) + 2 * (32 * 64 + 64 * 64 + 64 * 16)  # 20,480
-KERNELS_PER_STEP = 16  # 5 per-frame setup + 11 render launches, checked against the ncu launch list
+KERNELS_PER_STEP = 19  # 1 input copy + 4 setup + 2 resets + 12 render launches, checked against the ncu launch list
 
 
 def parse():

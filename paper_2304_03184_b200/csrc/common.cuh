@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string>
+#include <initializer_list>
 #include <utility>
 
 #include "../../include/capfields_b200.h"
@@ -125,3 +126,40 @@ __device__ __forceinline__ double sqdist(d3 a, d3 b) {
   double dx = x_sub(a.x, b.x), dy = x_sub(a.y, b.y), dz = x_sub(a.z, b.z);
   return x_add(x_add(x_mul(dx, dx), x_mul(dy, dy)), x_mul(dz, dz));
 }
+
+namespace cf {
+// Several fills in ONE launch, launched with PDL (waits for the stream predecessor
+// before writing): the frame's counter / bit-grid resets between its kernels.
+struct FillSpan {
+  void* p;
+  uint32_t v;
+  int64_t n;  // 32-bit words
+};
+struct FillList {
+  FillSpan s[4];
+  int count;
+};
+static __global__ void fill_list_kernel(FillList L) {
+  pdl_wait();
+  for (int k = 0; k < L.count; ++k) {
+    uint32_t* p = reinterpret_cast<uint32_t*>(L.s[k].p);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < L.s[k].n;
+         i += (int64_t)gridDim.x * blockDim.x)
+      p[i] = L.s[k].v;
+  }
+  pdl_trigger();
+}
+inline void fill_list(cudaStream_t st, std::initializer_list<FillSpan> spans) {
+  FillList L{};
+  int64_t most = 1;
+  for (const FillSpan& f : spans) {
+    if (f.n <= 0 || L.count == 4) continue;
+    L.s[L.count++] = f;
+    most = f.n > most ? f.n : most;
+  }
+  if (L.count == 0) return;
+  int64_t grid = (most + 255) / 256;
+  if (grid > 1024) grid = 1024;
+  cf::launch_pdl(fill_list_kernel, dim3((unsigned)grid), dim3(256), 0, st, L);
+}
+}  // namespace cf

@@ -628,7 +628,7 @@ int buckets_build(cf_buckets* b, const double* pts, int64_t n, int grid_res, cud
                                                   b->point_slot, b->sorted);
     return check_launch("buckets_build");
   }
-  cf::fill_u32(b->cell_start, 0u, cells + 1, st);
+  cf::fill_list(st, {{b->cell_start, 0u, cells + 1}});
   bucket_params_kernel<<<1, 1024, 0, st>>>(pts, (int)n, G, b->params);
   bucket_count_kernel<<<grid_for(n, 256, 4), 256, 0, st>>>(pts, (int)n, b->params, b->cell_start, b->point_cell,
                                                              b->point_slot);

@@ -1081,7 +1081,7 @@ int cf_occ_splat(const uint32_t* canon_bits, const cf_occ_grid* cg, const cf_buc
     return cf::fail(CF_E_BAD_ARG, "cf_occ_splat: bad args");
   cudaStream_t st = cf::as_stream(stream);
   const int64_t lwords = ((int64_t)lg->res * lg->res * lg->res + 31) / 32;
-  cf::fill_u32(live_bits, 0u, lwords, st);
+  cf::fill_list(st, {{live_bits, 0u, lwords}});
   const int64_t total = (int64_t)cg->res * cg->res * cg->res;
   const unsigned grid = cf::grid_for(total, 128, 8);
   const double r2 = radius * radius;
@@ -1098,7 +1098,7 @@ int cf_occ_cache(const uint32_t* canon_bits, const cf_occ_grid* cg, const cf_buc
   if (!canon_bits || !cg || !node_buckets || node_buckets->grid_res == 0 || k < 1 || k > 8 || !count)
     return cf::fail(CF_E_BAD_ARG, "cf_occ_cache: bad args");
   cudaStream_t st = cf::as_stream(stream);
-  cf::fill_u32(count, 0u, 1, st);
+  cf::fill_list(st, {{count, 0u, 1}});
   const int64_t total = (int64_t)cg->res * cg->res * cg->res;
   const unsigned grid = cf::grid_for(total, 128, 8);
   dispatch_k(k, [&]<int K>() {
@@ -1117,11 +1117,9 @@ int cf_occ_splat_cached(const int* cells, const int* nbr, const double* w, const
     return cf::fail(CF_E_BAD_ARG, "cf_occ_splat_cached: bad args");
   cudaStream_t st = cf::as_stream(stream);
   const int64_t P = lg->res + 2;
-  cf::fill_u32(scratch_bits, 0u, (P * P * P + 31) / 32 + 3, st);
-  if (live_bbox) {  // lo = 0x7f7f7f7f, hi = 0x80808080 (negative)
-    cf::fill_u32(live_bbox, 0x7f7f7f7fu, 3, st);
-    cf::fill_u32(live_bbox + 3, 0x80808080u, 3, st);
-  }
+  // lo = 0x7f7f7f7f, hi = 0x80808080 (negative)
+  cf::fill_list(st, {{scratch_bits, 0u, (P * P * P + 31) / 32 + 3}, {live_bbox, 0x7f7f7f7fu, live_bbox ? 3 : 0},
+                     {live_bbox ? live_bbox + 3 : nullptr, 0x80808080u, live_bbox ? 3 : 0}});
   const unsigned grid = cf::grid_for(capacity, 256, 4);
   if (k <= 4)
     cf::launch_pdl(occ_splat_cached_kernel<4>, grid, 256, 0, st, cells, nbr, w, count, capacity, k, dqs, *cg, *lg, scratch_bits,
@@ -1148,8 +1146,7 @@ int cf_march(const cf_march_desc* M, const double* dirs, const uint32_t* human_b
   if (human && human_bits) H = *human;
   if (object && object_bits) O = *object;
   cudaStream_t st = cf::as_stream(stream);
-  if (H.records) cf::fill_u32(H.counters, 0u, 4, st);
-  if (O.records) cf::fill_u32(O.counters, 0u, 4, st);
+  cf::fill_list(st, {{H.counters, 0u, H.records ? 4 : 0}, {O.counters, 0u, O.records ? 4 : 0}});
   if (M->n_rays == 0) return CF_OK;
   cf::launch_pdl(march_kernel<false>, cf::grid_for(M->n_rays, 128, 8), 128, 0, st, *M, cf_camera{},
                  const_cast<double*>(dirs), H.records ? human_bits : nullptr, O.records ? object_bits : nullptr, H, O);
@@ -1165,8 +1162,7 @@ int cf_rays_march(const cf_camera* cam, const cf_march_desc* M, double* dirs, co
   if (human && human_bits) H = *human;
   if (object && object_bits) O = *object;
   cudaStream_t st = cf::as_stream(stream);
-  if (H.records) cf::fill_u32(H.counters, 0u, 4, st);
-  if (O.records) cf::fill_u32(O.counters, 0u, 4, st);
+  cf::fill_list(st, {{H.counters, 0u, H.records ? 4 : 0}, {O.counters, 0u, O.records ? 4 : 0}});
   cf::launch_pdl(march_kernel<true>, cf::grid_for(M->n_rays, 128, 8), 128, 0, st, *M, *cam, dirs,
                  H.records ? human_bits : nullptr, O.records ? object_bits : nullptr, H, O);
   return cf::check_launch("cf_rays_march");
@@ -1240,7 +1236,7 @@ int cf_train_sample(const cf_march_desc* M, const float* gt_depth, const uint8_t
       n_guided + n_uniform > 128 || n_empty > 128 || n_guided > 32)
     return cf::fail(CF_E_BAD_ARG, "cf_train_sample: bad args");
   cudaStream_t st = cf::as_stream(stream);
-  cf::fill_u32(F->counters, 0u, 4, st);
+  cf::fill_list(st, {{F->counters, 0u, 4}});
   if (M->n_rays == 0) return CF_OK;
   train_sample_kernel<<<cf::grid_for(M->n_rays, 128, 8), 128, 0, st>>>(*M, gt_depth, mask, n_guided, n_uniform,
                                                                         n_empty, sigma_d, seed, *F, t_out);
