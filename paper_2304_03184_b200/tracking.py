@@ -301,12 +301,12 @@ class NonrigidTracker:
     """GPU drop-in for capfields.tracking.NonrigidTracker (tracking.py:259-556): the same
     constructor and solve(); `model` is duck-typed (graph.nodes / radius / knn_k,
     skeleton.parents / offsets / joint_limits, points, normals, lbs_weights,
-    node_lbs_weights, edges). The object-interpenetration term is not supported."""
+    node_lbs_weights, edges); object_volume is this package's TsdfVolume."""
 
     def __init__(self, model, cam, weights=None, surface_samples: int = 4096, max_iters: int = 8,
                  object_volume=None, seed: int = 0):
-        if object_volume is not None:
-            raise NotImplementedError("the interpenetration term is not built on the device")
+        self.object_volume = object_volume  # a tsdf.TsdfVolume (device) or None
+        self.object_pose = _Pose(np.eye(3), np.zeros(3))  # canonical -> world, set by the object tracker
         from .knnfield import brute_force_neighbors_batch
         self.model, self.cam = model, cam
         self.weights = weights or EnergyWeights()
@@ -372,6 +372,21 @@ class NonrigidTracker:
         pose_corr = find_correspondences(lp, ln, D, self.cam, mask=mask, normals_map=nmap)
         return data_corr, pose_corr
 
+    def _inter(self, state):
+        """Interpenetration term (tracking.py:326-331, 481-496): penetration depth of the
+        live nodes inside the object volume -> (pen (n,), active ids, live nodes, m)."""
+        from .tsdf import _inverse
+        n = len(self.nodes)
+        live = torch.empty_like(self.d_nodes)
+        _lib.call("cf_deform_nodes", self.d_nodes.data_ptr(), state.dqs_dev.data_ptr(), n, live.data_ptr(),
+                  _lib.stream_ptr())
+        R, t = _inverse(np.asarray(self.object_pose.rotation), np.asarray(self.object_pose.translation))
+        Rt = torch.from_numpy(np.ascontiguousarray(R)).to(live.device)
+        q = (live @ Rt.t() + torch.from_numpy(t).to(live.device)).contiguous()  # inv.apply (Se3.apply)
+        phi, ok = self.object_volume.sample(q)
+        pen = torch.where(ok, torch.clamp(-phi, min=0.0), torch.zeros_like(phi))
+        return pen, q, live, Rt
+
     def _system(self, state, data_corr, pose_corr, with_jacobian: bool):
         """energy_terms (tracking.py:288-336) and, with_jacobian, _assemble (358-508)."""
         w = self.weights
@@ -392,6 +407,16 @@ class NonrigidTracker:
         C, E = int(ci.numel()), len(self.edges)
         use = dict(data=C > 0 and w.data > 0, bind=w.bind > 0, reg=E > 0 and w.reg > 0, prior=w.prior > 0 and len(act),
                    pose=P > 0 and w.pose > 0)
+        inter = None
+        if self.object_volume is not None:
+            pen, q, live, Rt = self._inter(state)
+            self._inter_e = float((pen * pen).sum())
+            iact = torch.nonzero(pen > 0).reshape(-1)
+            use["inter"] = w.inter > 0 and int(iact.numel()) > 0
+            inter = (pen, q, live, Rt, iact)
+        else:
+            self._inter_e = 0.0
+            use["inter"] = False
         S = _lib.NrSystem()
         S.dqs, S.nodes, S.n_nodes, S.n_theta = state.dqs_dev.data_ptr(), self.d_nodes.data_ptr(), n, T
         S.warped, S.n_data = warped.data_ptr(), C
@@ -408,7 +433,8 @@ class NonrigidTracker:
         if with_jacobian:
             sizes = [("data", C if use["data"] else 0, 6 * self.k), ("bind", 3 * n if use["bind"] else 0, 6 + T),
                      ("reg", 3 * E if use["reg"] else 0, 12), ("prior", len(act) if use["prior"] else 0, 1),
-                     ("pose", P if use["pose"] else 0, T)]
+                     ("pose", P if use["pose"] else 0, T),
+                     ("inter", int(inter[4].numel()) if use["inter"] else 0, 6)]
             rows = sum(s[1] for s in sizes)
             if rows == 0:
                 return self._energy(state), None, None
@@ -449,6 +475,17 @@ class NonrigidTracker:
                 val[e0:e0 + len(act)] = torch.from_numpy(s * np.sign(state.theta[act])).to(d)
                 col[e0:e0 + len(act)] = torch.from_numpy((6 * n + act).astype(np.int32)).to(d)
                 res[r0:r0 + len(act)] = torch.from_numpy(s * lim_r[act]).to(d)
+            if use["inter"]:  # rows s [v x m, m], m = -(grad_q R_inv) (tracking.py:481-496)
+                pen, q, live, Rt, iact = inter
+                si = float(np.sqrt(w.inter))
+                g = self.object_volume.gradient(q[iact].contiguous())
+                m = -(g @ Rt)
+                gom = torch.linalg.cross(live[iact], m)
+                r0, e0 = off["inter"]
+                ni = int(iact.numel())
+                val[e0:e0 + 6 * ni] = (si * torch.cat([gom, m], 1)).reshape(-1)
+                col[e0:e0 + 6 * ni] = (6 * iact[:, None] + torch.arange(6, device=d)[None]).reshape(-1).to(torch.int32)
+                res[r0:r0 + ni] = si * pen[iact]
             counts = torch.cat([torch.full((nr,), per, dtype=torch.int64, device=d) for _, nr, per in sizes if nr])
             rowptr = torch.cat([torch.zeros(1, dtype=torch.int64, device=d), torch.cumsum(counts, 0)]).to(torch.int32)
             J = (val, col, rowptr, (rows, 6 * n + T))
@@ -463,7 +500,7 @@ class NonrigidTracker:
         if lim_r is None:
             lim_r = np.maximum(0.0, np.abs(state.theta) - self.lim)
         out = {"data": float(e[0]), "bind": float(e[1]), "reg": float(e[2]), "prior": float(np.sum(lim_r ** 2)),
-               "pose": float(e[3]), "inter": 0.0}
+               "pose": float(e[3]), "inter": float(getattr(self, "_inter_e", 0.0))}
         out["total"] = (w.data * out["data"] + w.bind * out["bind"] + w.reg * out["reg"] + w.prior * out["prior"]
                         + w.pose * out["pose"] + w.inter * out["inter"])
         return out

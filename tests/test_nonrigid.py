@@ -92,3 +92,37 @@ def test_energy_terms_reference_properties(ref):
     e0 = tr.energy_terms(rest, (np.array([0]), u0, nrm), empty)
     e1 = tr.energy_terms(rest, (np.array([0]), u0 + np.array([[0.013, -0.007, 0.0]]), nrm), empty)
     assert e0["data"] > 0 and abs(e0["data"] - e1["data"]) < 1e-14
+
+
+def test_interpenetration_term(ref):
+    """Object interpenetration (tracking.py:326-331, 481-496) with a device TSDF: the
+    energy equals a numpy restatement on the same volume, and a solve with the term
+    keeps its accepted energies non-increasing."""
+    from paper_2304_03184_b200.tracking import NonrigidTracker, SolveState
+    from paper_2304_03184_b200.tsdf import TsdfVolume
+    model, cam = _model(ref)
+    nodes = ref["nodes"]
+    lo, hi = nodes.min(0) - 0.1, nodes.max(0) + 0.1
+    vol = TsdfVolume(48, float((hi - lo).max()) / 48, lo)
+
+    class _P:
+        rotation, translation = np.eye(3), np.zeros(3)
+    # a wall in front of the body's centre plane: nodes behind it read negative TSDF
+    zc = float(np.median((nodes - cam.pose.translation) @ cam.pose.rotation[:, 2]))
+    depth = np.full((cam.height, cam.width), zc - 0.02)
+    vol.integrate(depth, cam, _P())
+    tr = NonrigidTracker(model, cam, surface_samples=800, object_volume=vol)
+    n = len(nodes)
+    dq = np.zeros((n, 8))
+    dq[:, 0] = 1.0
+    rest = SolveState(dq, np.zeros(72))
+    empty = (np.zeros(0, dtype=np.int64), np.zeros((0, 3)), np.zeros((0, 3)))
+    e = tr.energy_terms(rest, empty, empty)
+    phi, ok = vol.sample(nodes)
+    pen = np.where(ok, np.maximum(0.0, -phi), 0.0)
+    assert pen.sum() > 0
+    assert abs(e["inter"] - np.sum(pen ** 2)) <= 1e-12 * max(1.0, np.sum(pen ** 2))
+    state, info = tr.solve(ref["depth0"], ref["mask0"], 0)
+    assert info["iterations"] >= 1
+    for before, after in info["accepted"]:
+        assert after <= before + 1e-12
