@@ -9,7 +9,6 @@
 // ascending sample order, with per-ray (offset, count); canonicalised samples
 // = float4 (x, y, z in the field's unit cube, flag).
 #include "edwarp.cuh"
-#include "render_common.cuh"
 
 namespace {
 

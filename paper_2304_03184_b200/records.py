@@ -221,72 +221,4 @@ class MotionPriorStream:
 
 __all__ = ["MOTION_MAGIC", "VERSION", "RecordFormatError", "MotionPrior", "MotionPriorWriter", "MotionPriorStream",
            "SkeletonPose", "Se3", "load_motion_priors", "read_motion_arrays", "scan_motion_priors",
-           "skinning_transforms", "GRAPH_MAGIC", "save_graph", "load_graph", "graph_debug_dump"]
-
-
-# -- graph dumps (CFGR v1, records.py:39-86): host-side file I/O -------------------
-
-GRAPH_MAGIC = b"CFGR"
-
-
-def save_graph(path: str, graph, motions=None) -> None:
-    """records.py:39-49: header, node array, then (frame id, dqs) per motion."""
-    import struct
-    nodes = np.ascontiguousarray(np.asarray(graph.nodes, dtype=np.float64))
-    with open(path, "wb") as f:
-        f.write(GRAPH_MAGIC)
-        f.write(struct.pack("<I", VERSION))
-        f.write(struct.pack("<IdI", len(nodes), float(graph.radius), int(graph.knn_k)))
-        f.write(struct.pack("<I", nodes.size))
-        f.write(nodes.tobytes())
-        motions = motions or []
-        f.write(struct.pack("<I", len(motions)))
-        for m in motions:
-            d = np.ascontiguousarray(np.asarray(m.dqs, dtype=np.float64))
-            f.write(struct.pack("<q", int(m.frame_id)))
-            f.write(struct.pack("<I", d.size))
-            f.write(d.tobytes())
-
-
-def load_graph(path: str):
-    """records.py:52-71 -> (EDGraph, [GraphMotion]); RecordFormatError on a bad file."""
-    import struct
-    from .edgraph import EDGraph
-
-    def arr(f, shape):
-        (n,) = struct.unpack("<I", f.read(4))
-        raw = f.read(8 * n)
-        if len(raw) != 8 * n or n != int(np.prod(shape)):
-            raise RecordFormatError(f"{path}: truncated or mis-sized array")
-        return np.frombuffer(raw, dtype="<f8").copy().reshape(shape)
-
-    with open(path, "rb") as f:
-        if f.read(4) != GRAPH_MAGIC:
-            raise RecordFormatError(f"{path}: not a graph record")
-        (version,) = struct.unpack("<I", f.read(4))
-        if version != VERSION:
-            raise RecordFormatError(f"{path}: unsupported version {version}")
-        n, radius, knn_k = struct.unpack("<IdI", f.read(16))
-        graph = EDGraph(arr(f, (n, 3)), radius=radius, knn_k=knn_k)
-        (n_motions,) = struct.unpack("<I", f.read(4))
-        motions = []
-        for _ in range(n_motions):
-            (fid,) = struct.unpack("<q", f.read(8))
-            motions.append(GraphMotion(fid, arr(f, (n, 8))))
-        return graph, motions
-
-
-def graph_debug_dump(graph, motions=None) -> str:
-    """records.py:74-86."""
-    import io
-    out = io.StringIO()
-    nodes = np.asarray(graph.nodes)
-    out.write(f"ed-graph: {len(nodes)} nodes, radius {graph.radius}, knn_k {graph.knn_k}\n")
-    for i, p in enumerate(nodes):
-        out.write(f"  node {i:4d}: ({p[0]:+.4f}, {p[1]:+.4f}, {p[2]:+.4f})\n")
-    for m in motions or []:
-        out.write(f"frame {m.frame_id}:\n")
-        for i, dq in enumerate(np.asarray(m.dqs)):
-            out.write(f"  dq {i:4d}: real({dq[0]:+.4f} {dq[1]:+.4f} {dq[2]:+.4f} {dq[3]:+.4f})"
-                      f" dual({dq[4]:+.4f} {dq[5]:+.4f} {dq[6]:+.4f} {dq[7]:+.4f})\n")
-    return out.getvalue()
+           "skinning_transforms"]

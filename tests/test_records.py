@@ -189,21 +189,3 @@ def test_stream_drives_the_renderer(tmp_path):
     d = (a - b).abs()
     assert a.abs().sum() > 0
     assert float(d.max()) <= 1e-2 and float(d.mean()) <= 1e-5, (float(d.max()), float(d.mean()))
-
-
-def test_graph_dump_roundtrip_against_reference(tmp_path):
-    """CFGR graph dumps (records.py:39-86): a file the reference wrote loads, re-saves
-    byte-identically and dumps the same debug text; bad magic is a RecordFormatError."""
-    gb = os.path.join(GOLDEN, "graph_ref.bin")
-    g, motions = records.load_graph(gb)
-    assert g.nodes.shape == (17, 3) and g.radius == 0.123 and g.knn_k == 5
-    assert [m.frame_id for m in motions] == [0, 7, 14]
-    p = str(tmp_path / "g.bin")
-    records.save_graph(p, g, motions)
-    assert open(p, "rb").read() == open(gb, "rb").read()
-    assert records.graph_debug_dump(g, motions) == open(os.path.join(GOLDEN, "graph_ref.txt")).read()
-    bad = str(tmp_path / "junk.bin")
-    with open(bad, "wb") as f:
-        f.write(b"NOPE" + b"\x00" * 64)
-    with pytest.raises(RecordFormatError):
-        records.load_graph(bad)
