@@ -49,6 +49,9 @@ def parse():
                     help="render = configs[1] (the headline); train = configs[2] key-frame training step; "
                          "knn = configs[3] dense-graph k-NN scaling")
     ap.add_argument("--train-rays", type=int, default=1 << 18)
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp16"],
+                    help="field arithmetic: fp32 = SPEC 32-bit semantics (split-fp16 tensor-core operands, fp32 "
+                         "tables / features); fp16 = fp16 operands and features")
     ap.add_argument("--shard", default="frames", choices=["frames", "rows"],
                     help="render at N GPUs: frames = each rank renders whole frames (weak scaling, the "
                          "headline); rows = the ranks split every frame's rows round-robin and all-gather the "
@@ -169,7 +172,7 @@ def build_workload(args, rank):
     from paper_2304_03184_b200.render import HumanField, ObjectField, RenderConfig, Renderer
     from paper_2304_03184_b200.scene import Scene, SceneConfig
     sc = Scene(SceneConfig(width=args.width, height=args.height), seed=0)
-    cfg = RenderConfig(n_samples=args.samples)
+    cfg = RenderConfig(n_samples=args.samples, precision=getattr(args, "precision", "fp32"))
     hf = HumanField(sc.nodes, sc.template_points, sc.skin_verts, sc.skin_weights, cfg, seed=0, zero_deform_out=False)
     of = ObjectField(sc.box_half, cfg, seed=1)
     world = int(os.environ.get("WORLD_SIZE", "1"))

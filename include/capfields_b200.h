@@ -324,9 +324,14 @@ typedef struct cf_field_desc {
                                (row = layer * 128 + unit, S = capacity), or NULL */
   float* save_o;            /* training: DeformNet raw outputs (o0, o1, o2, 0) float4 per sample, or NULL */
   uint32_t* save_mask;      /* training: ReLU bits of layers 1..4, (S,16) uint32 = [layer][half][2], or NULL */
+  int precise;              /* 1 = "fp32" mode: fp32 tables and features, split-fp16 (hi + lo) MLP operands
+                               (3 MMA chains per layer); 0 = "fp16" mode (fp16 operands, fp16 deform-table copy) */
+  const uint8_t* wblob_lo;  /* precise: the residual blob fp16(W - fp16(W)), same layout as wblob */
 } cf_field_desc;
 /* device scratch needed by cf_field_forward for `capacity` samples */
 int cf_field_scratch_bytes(const cf_field_desc* F, int64_t capacity, int64_t* bytes);
+/* scratch layout (S = capacity): fp16 mode: cfeat (S,32) fp16 | dfeat (S,32) fp16 | xc (S) float4;
+ * precise mode: cfeat (S,32) fp32 | dfeat (S,32) fp32 | xc (S) float4 (dfeat / xc human only) */
 /* out: float4 (sigma, r, g, b) per compacted sample of S (count read on device).
  * Stages: hash (fp16 features) [-> DeformNet -> hash] -> E_g/E_c, see field.cu */
 int cf_field_forward(const cf_field_desc* F, const cf_march_out* S, const double* dirs, const float* xu, float* out,
@@ -412,6 +417,9 @@ int cf_gemm_kmajor_f16(const void* A, int64_t lda, const void* B, int64_t ldb, i
                        int ldc, void* stream);
 /* fp32 (n x k) row-major weight -> fp16 UMMA canonical K-major blob (n, k padded to 16) */
 int cf_pack_weight(const float* w, int n, int k, uint8_t* blob, void* stream);
+/* as cf_pack_weight, plus the residual fp16(W - fp16(W)) into blob_lo (same layout):
+ * the B operand halves of the "fp32" precision mode */
+int cf_pack_weight_split(const float* w, int n, int k, uint8_t* blob, uint8_t* blob_lo, void* stream);
 
 /* device -> pinned host (cudaHostAlloc'd, UVA-mapped) copy by `ctas` CTAs of stores
  * instead of a copy-engine memcpy (overlaps the next view's uploads); 16-byte aligned */

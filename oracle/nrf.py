@@ -6,8 +6,11 @@ SPEC's worked examples (tests/test_oracle_nrf.py). The hyper-parameter choices
 the SPEC leaves open are frozen in DESIGN.md §4-§6 and restated here.
 
 Precision modes: hash encoding is evaluated in float32 with the kernel's exact
-operation order (indices bit-exact, features bit-equal); MLPs in
-"kernel precision" (fp16-rounded operands per layer, float64 accumulation).
+operation order (indices bit-exact, features bit-equal). MLPs either in the
+SPEC's 32-bit semantics (`mlp_forward_f32`: fp32 weights and inputs, float64
+arithmetic — the reference the "fp32" device mode is held to), or in "kernel
+precision" of the "fp16" device mode (`mlp_forward`: fp16-rounded operands per
+layer, float64 accumulation).
 """
 from __future__ import annotations
 
@@ -100,5 +103,20 @@ def mlp_forward(weights, x, biases=None):
             y = y + np.asarray(biases[l], dtype=np.float32).astype(np.float64)
         if l < n - 1:
             h = f16(np.maximum(y.astype(np.float32), 0.0))
+        else:
+            return y
+
+
+def mlp_forward_f32(weights, x, biases=None):
+    """SPEC 32-bit semantics: the fp32 weights and layer inputs
+    exactly, float64 accumulation, ReLU between layers, no output activation."""
+    h = np.asarray(x, dtype=np.float32).astype(np.float64)
+    n = len(weights)
+    for l, W in enumerate(weights):
+        y = h @ np.asarray(W, dtype=np.float32).astype(np.float64).T
+        if biases is not None and biases[l] is not None:
+            y = y + np.asarray(biases[l], dtype=np.float32).astype(np.float64)
+        if l < n - 1:
+            h = np.maximum(y, 0.0)
         else:
             return y

@@ -151,25 +151,46 @@ def sh16(d):
         0.59004358992664352 * x * (-xx + 3.0 * yy)], -1).astype(np.float32)
 
 
+def deform_forward(layers, fd, dbias, precision="fp32"):
+    """DeformNet raw outputs (N,3) float64 from the deformation-grid features fd."""
+    mlp = on.mlp_forward_f32 if precision == "fp32" else on.mlp_forward
+    Ws = [layers["D1"][:, :32], layers["D2"], layers["D3"], layers["D4"], layers["D5"]]
+    return mlp(Ws, fd, [dbias, None, None, None, None])[:, :3]
+
+
+def deformed_coords(xu, v, inv_side):
+    """xc = xu + 0.05 tanh(v) / side in float32 (field.cu deform_mlp epilogue)."""
+    x = xu[:, :3].astype(np.float32).copy()
+    delta = np.float32(0.05) * np.tanh(v.astype(np.float32))
+    return x + delta * np.float32(inv_side)
+
+
+def color_forward(layers, fc, dirs, precision="fp32"):
+    """E_g / E_c from the canonical features fc -> (N,4) float32 (sigma, r, g, b)."""
+    mlp = on.mlp_forward_f32 if precision == "fp32" else on.mlp_forward
+    g = mlp([layers["G1"], layers["G2"]], fc).astype(np.float32)
+    sigma = np.exp(g[:, 0])
+    cin = np.concatenate([g[:, 1:16], sh16(dirs)], axis=1)
+    c = mlp([layers["C1"], layers["C2"], layers["C3"]], cin).astype(np.float32)
+    rgb = 1.0 / (1.0 + np.exp(-c[:, :3]))
+    return np.concatenate([sigma[:, None], rgb], axis=1).astype(np.float32)
+
+
 def field_forward(layers, has_deform, xu, dirs, ctable, dtable=None, dbias=None, inv_side=1.0,
-                  cgrid=(16, 2, 19, 16, 2048), dgrid=(8, 4, 17, 16, 256)):
-    """Kernel-precision field: -> (N,4) float32 (sigma, r, g, b); zeros where flag == 0."""
+                  cgrid=(16, 2, 19, 16, 2048), dgrid=(8, 4, 17, 16, 256), precision="fp16"):
+    """Field -> (N,4) float32 (sigma, r, g, b); zeros where flag == 0.
+    precision "fp32": SPEC 32-bit semantics (fp32 tables, features and weights);
+    "fp16": kernel precision of the fp16 device mode (fp16 MLP operands; pass the
+    fp16-rounded deformation table the kernels read)."""
     x = xu[:, :3].astype(np.float32).copy()
     valid = xu[:, 3] > 0
     if has_deform:
         fd = on.hash_encode(dtable, x, *dgrid)
-        Ws = [layers["D1"][:, :32], layers["D2"], layers["D3"], layers["D4"], layers["D5"]]
-        bs = [dbias, None, None, None, None]
-        v = on.mlp_forward(Ws, fd, bs).astype(np.float32)
-        delta = np.float32(0.05) * np.tanh(v[:, :3])
-        x = x + delta * np.float32(inv_side)
+        x = deformed_coords(xu, deform_forward(layers, fd, dbias, precision), inv_side)
     fc = on.hash_encode(ctable, x, *cgrid)
-    g = on.mlp_forward([layers["G1"], layers["G2"]], fc).astype(np.float32)
-    sigma = np.exp(g[:, 0])
-    cin = np.concatenate([g[:, 1:16], sh16(dirs)], axis=1)
-    c = on.mlp_forward([layers["C1"], layers["C2"], layers["C3"]], cin).astype(np.float32)
-    rgb = 1.0 / (1.0 + np.exp(-c[:, :3]))
-    out = np.concatenate([sigma[:, None], rgb], axis=1).astype(np.float32)
+    if precision == "fp16":
+        fc = fc.astype(np.float16).astype(np.float32)  # the kernels hand fp16 features to the MLP
+    out = color_forward(layers, fc, dirs, precision)
     out[~valid] = 0.0
     return out
 

@@ -87,7 +87,7 @@ class FieldDesc(ctypes.Structure):
                 ("cgrid", HashGridDesc), ("ctable", ctypes.c_void_p), ("wblob", ctypes.c_void_p),
                 ("w_bytes", ctypes.c_int), ("dbias", ctypes.c_void_p), ("delta_scale", ctypes.c_float),
                 ("inv_side", ctypes.c_float), ("save_h", ctypes.c_void_p), ("save_o", ctypes.c_void_p),
-                ("save_mask", ctypes.c_void_p)]
+                ("save_mask", ctypes.c_void_p), ("precise", ctypes.c_int), ("wblob_lo", ctypes.c_void_p)]
 
 
 class MpInfo(ctypes.Structure):
@@ -221,6 +221,7 @@ _SIGS = {
     "cf_adam": [_p, _p, _p, _p, _i64, ctypes.c_float, ctypes.c_float, ctypes.c_float, ctypes.c_float, _i32,
                 ctypes.c_float, _p],
     "cf_pack_weight": [_p, _i32, _i32, _p, _p],
+    "cf_pack_weight_split": [_p, _i32, _i32, _p, _p, _p],
     "cf_gemm_kmajor_f16": [_p, _i64, _p, _i64, _i32, _i64, _p, _i32, _p],
     "cf_store_to_host": [_p, _p, _i64, _i32, _p],
     "cf_load_from_host": [_p, _p, _i64, _p],

@@ -123,7 +123,9 @@ __device__ __forceinline__ void hash_features(const cf_hashgrid_desc& D, const T
 // its 32 / SPLIT features of the row: SPLIT > 1 multiplies the warps in flight
 // for small sample counts (the object field), where one thread per sample left
 // the SMs mostly idle.
-template <int F, int L, int CH, int SPLIT, class TT>
+// F32 ("fp32" precision mode): the 32 features are written as fp32 (128 B / sample)
+// instead of fp16.
+template <int F, int L, int CH, int SPLIT, class TT, bool F32 = false>
 __global__ void __launch_bounds__(128) hash_f16_kernel(cf_hashgrid_desc D, const TT* __restrict__ table,
                                                        const float4* __restrict__ x, const int* __restrict__ count,
                                                        int64_t capacity, uint4* __restrict__ out) {
@@ -145,12 +147,19 @@ __global__ void __launch_bounds__(128) hash_f16_kernel(cf_hashgrid_desc D, const
 #pragma unroll
       for (int i = 0; i < NF; ++i) feat[i] = 0.0f;
     }
+    if constexpr (F32) {
+      float4* o = reinterpret_cast<float4*>(out) + s * 8 + part * (NF / 4);
 #pragma unroll
-    for (int q = 0; q < NF / 8; ++q) {
-      __half2 h[4];
+      for (int q = 0; q < NF / 4; ++q)
+        o[q] = make_float4(feat[4 * q], feat[4 * q + 1], feat[4 * q + 2], feat[4 * q + 3]);
+    } else {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) h[i] = __floats2half2_rn(feat[8 * q + 2 * i], feat[8 * q + 2 * i + 1]);
-      out[s * 4 + part * (NF / 8) + q] = *reinterpret_cast<uint4*>(h);
+      for (int q = 0; q < NF / 8; ++q) {
+        __half2 h[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) h[i] = __floats2half2_rn(feat[8 * q + 2 * i], feat[8 * q + 2 * i + 1]);
+        out[s * 4 + part * (NF / 8) + q] = *reinterpret_cast<uint4*>(h);
+      }
     }
   }
   pdl_trigger();
@@ -591,6 +600,264 @@ __global__ void __launch_bounds__(kColorTsSlots* kSlotThreads, 1)
     cts_layer(S, smem + c2, 64, 64);
     cts_relu64(S);
     cts_layer(S, smem + c3, 64, 16);
+    float cv[16];
+    tc::tmem_ld16(S.d, cv);
+    if (live) {
+      const float r = 1.0f / (1.0f + expf(-cv[0])), g = 1.0f / (1.0f + expf(-cv[1])),
+                  b = 1.0f / (1.0f + expf(-cv[2]));
+      out[s] = valid ? make_float4(sigma, r, g, b) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_free<512>(tmem_base);
+  pdl_trigger();
+}
+
+// ---------------------------------------------------------------- "fp32" precision mode
+// The same networks with every operand split into fp16 hi + lo halves and three
+// MMA chains per layer (tc::issue_layer_ts_split): ~22-bit operands, fp32 TMEM
+// accumulation, fp32 hash features in. This is the mode that meets the SPEC's
+// 32-bit semantics within 1e-4 (tests/test_precision_gpu.py);
+// the fp16-operand kernels above are the "fp16" mode.
+
+// DeformNet: both weight halves resident in smem (2 x 108 KB), 2 TS slots of 8
+// warps, per slot D (128) + A_hi (64) + A_lo (64) TMEM columns = 512 in all.
+constexpr int kPrecDeformSlots = 2;
+
+struct SplitSlot {
+  uint64_t* bar;
+  uint32_t d0, ahi0, alo0;  // slot base columns (MMA operands)
+  uint32_t d, ahi, alo;     // + this warp's lane quarter
+  uint32_t phase;
+  int slot, r, half, nthreads;
+};
+
+__device__ __forceinline__ void split_layer(SplitSlot& S, const uint8_t* w_hi, const uint8_t* w_lo, int K, int N) {
+  tc::tmem_wait_st();
+  tc::fence_before();
+  tc::named_sync(1 + S.slot, S.nthreads);
+  if (threadIdx.x % S.nthreads == 0) {
+    tc::fence_after();
+    tc::issue_layer_ts_split(S.d0, S.ahi0, S.alo0, w_hi, w_lo, K, N);
+    tc::mma_commit(S.bar);
+  }
+  tc::bar_wait(S.bar, S.phase);
+  S.phase ^= 1u;
+  tc::fence_after();
+}
+
+// 32 D columns from col -> (+bias) ReLU -> hi / lo fp16x2 -> A columns col/2
+__device__ __forceinline__ void split_relu32(const SplitSlot& S, int col, const float* bias) {
+  uint32_t r[32];
+  tc::tmem_ld32_nowait(S.d + (uint32_t)col, r);
+  tc::tmem_wait_ld();
+  uint32_t h[16], l[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    float x0 = __uint_as_float(r[2 * i]), x1 = __uint_as_float(r[2 * i + 1]);
+    if (bias) {
+      x0 += bias[col + 2 * i];
+      x1 += bias[col + 2 * i + 1];
+    }
+    tc::split_f16x2(fmaxf(x0, 0.0f), fmaxf(x1, 0.0f), h[i], l[i]);
+  }
+  tc::tmem_st16(S.ahi + (uint32_t)(col / 2), h);
+  tc::tmem_st16(S.alo + (uint32_t)(col / 2), l);
+}
+
+// n4 float4 of fp32 values -> hi / lo halves at A column c0 (2 values per column)
+template <int N4>
+__device__ __forceinline__ void split_store(const SplitSlot& S, const float4* v, int c0) {
+  uint32_t h[2 * N4], l[2 * N4];
+#pragma unroll
+  for (int q = 0; q < N4; ++q) {
+    tc::split_f16x2(v[q].x, v[q].y, h[2 * q], l[2 * q]);
+    tc::split_f16x2(v[q].z, v[q].w, h[2 * q + 1], l[2 * q + 1]);
+  }
+  if constexpr (N4 == 4) {
+    tc::tmem_st8(S.ahi + (uint32_t)c0, h);
+    tc::tmem_st8(S.alo + (uint32_t)c0, l);
+  } else {
+    static_assert(N4 == 8, "8 or 16 columns");
+    tc::tmem_st16(S.ahi + (uint32_t)c0, h);
+    tc::tmem_st16(S.alo + (uint32_t)c0, l);
+  }
+}
+
+__global__ void __launch_bounds__(kPrecDeformSlots* kDeformSlotThreads, 1)
+    deform_mlp_prec_kernel(const uint8_t* __restrict__ wblob, const uint8_t* __restrict__ wblob_lo,
+                           const float* __restrict__ bias1, float delta_scale, float inv_side,
+                           const float4* __restrict__ xu, const float4* __restrict__ dfeat,
+                           const int* __restrict__ count, int64_t capacity, float4* __restrict__ xc) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t mbar[kPrecDeformSlots];
+  __shared__ uint32_t tmem_base;
+  __shared__ float s_bias[128];
+  const int tid = threadIdx.x, warp = tid / 32;
+  if (tid < 128) s_bias[tid] = bias1[tid];
+  for (int i = tid * 16; i < kDeformW; i += blockDim.x * 16) {
+    *reinterpret_cast<uint4*>(smem + i) = *reinterpret_cast<const uint4*>(wblob + i);
+    *reinterpret_cast<uint4*>(smem + kDeformW + i) = *reinterpret_cast<const uint4*>(wblob_lo + i);
+  }
+  if (tid == 0) {
+    for (int q = 0; q < kPrecDeformSlots; ++q) tc::bar_init(&mbar[q], 1);
+    tc::bar_fence_init();
+  }
+  if (warp == 0) tc::tmem_alloc<512>(&tmem_base);
+  tc::fence_async_smem();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  pdl_wait();
+  SplitSlot S;
+  S.nthreads = kDeformSlotThreads;
+  S.slot = tid / kDeformSlotThreads;
+  const int ws = warp % (kDeformSlotThreads / 32);
+  S.half = ws / 4;
+  S.r = (ws % 4) * 32 + (tid & 31);
+  S.bar = &mbar[S.slot];
+  S.phase = 0;
+  const uint32_t lane_q = (uint32_t)((ws % 4) * 32) << 16;
+  S.d0 = tmem_base + (uint32_t)(S.slot * 256);
+  S.ahi0 = S.d0 + 128u;
+  S.alo0 = S.d0 + 192u;
+  S.d = S.d0 + lane_q;
+  S.ahi = S.ahi0 + lane_q;
+  S.alo = S.alo0 + lane_q;
+  const uint8_t* lo = smem + kDeformW;
+  constexpr int o1 = 0, o2 = 128 * 32 * 2, o3 = o2 + 128 * 128 * 2, o4 = o3 + 128 * 128 * 2, o5 = o4 + 128 * 128 * 2;
+  const int64_t n = min((int64_t)*count, capacity);
+  const int64_t n_tiles = (n + 127) / 128;
+  for (int64_t tile = (int64_t)blockIdx.x * kPrecDeformSlots + S.slot; tile < n_tiles;
+       tile += (int64_t)gridDim.x * kPrecDeformSlots) {
+    const int64_t s = tile * 128 + S.r;
+    const bool live = s < n;
+    {
+      float4 f[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) f[q] = live ? dfeat[s * 8 + 4 * S.half + q] : make_float4(0.f, 0.f, 0.f, 0.f);
+      split_store<4>(S, f, 8 * S.half);  // this half's 16 features
+    }
+    const float4 xs = (live && S.half == 0) ? xu[s] : make_float4(0.f, 0.f, 0.f, 0.f);
+    split_layer(S, smem + o1, lo + o1, 32, 128);
+    split_relu32(S, 64 * S.half, s_bias);
+    split_relu32(S, 64 * S.half + 32, s_bias);
+    split_layer(S, smem + o2, lo + o2, 128, 128);
+    split_relu32(S, 64 * S.half, nullptr);
+    split_relu32(S, 64 * S.half + 32, nullptr);
+    split_layer(S, smem + o3, lo + o3, 128, 128);
+    split_relu32(S, 64 * S.half, nullptr);
+    split_relu32(S, 64 * S.half + 32, nullptr);
+    split_layer(S, smem + o4, lo + o4, 128, 128);
+    split_relu32(S, 64 * S.half, nullptr);
+    split_relu32(S, 64 * S.half + 32, nullptr);
+    split_layer(S, smem + o5, lo + o5, 128, 16);
+    if (S.half == 0) {  // warp-uniform: tcgen05.ld is warp-collective
+      float v[16];
+      tc::tmem_ld16(S.d, v);
+      if (live) {
+        float4 p = xs;
+        if (p.w > 0.0f) {
+          p.x = f_add(p.x, f_mul(delta_scale * tanhf(v[0]), inv_side));
+          p.y = f_add(p.y, f_mul(delta_scale * tanhf(v[1]), inv_side));
+          p.z = f_add(p.z, f_mul(delta_scale * tanhf(v[2]), inv_side));
+        }
+        xc[s] = p;
+      }
+    }
+  }
+  pdl_trigger();
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_free<512>(tmem_base);
+}
+
+// E_g / E_c: weight halves 2 x 20 KB, 4 slots of 4 warps (thread = sample row),
+// per slot D (64) + A_hi (32) + A_lo (32) TMEM columns.
+constexpr int kColorPrecSlots = 4;
+
+__global__ void __launch_bounds__(kColorPrecSlots* kSlotThreads, 1)
+    color_mlp_prec_kernel(const uint8_t* __restrict__ wblob, const uint8_t* __restrict__ wblob_lo,
+                          const float4* __restrict__ xu, const float4* __restrict__ cfeat,
+                          const uint32_t* __restrict__ records, const double* __restrict__ dirs,
+                          const int* __restrict__ count, int64_t capacity, float4* __restrict__ out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t mbar[kColorPrecSlots];
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid / 32;
+  for (int i = tid * 16; i < kColorW; i += blockDim.x * 16) {
+    *reinterpret_cast<uint4*>(smem + i) = *reinterpret_cast<const uint4*>(wblob + i);
+    *reinterpret_cast<uint4*>(smem + kColorW + i) = *reinterpret_cast<const uint4*>(wblob_lo + i);
+  }
+  if (tid == 0) {
+    for (int q = 0; q < kColorPrecSlots; ++q) tc::bar_init(&mbar[q], 1);
+    tc::bar_fence_init();
+  }
+  if (warp == 0) tc::tmem_alloc<512>(&tmem_base);
+  tc::fence_async_smem();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  pdl_wait();
+  SplitSlot S;
+  S.nthreads = kSlotThreads;
+  S.slot = tid / kSlotThreads;
+  S.r = tid % kSlotThreads;
+  S.half = 0;
+  S.bar = &mbar[S.slot];
+  S.phase = 0;
+  const uint32_t lane_q = (uint32_t)((warp % 4) * 32) << 16;
+  S.d0 = tmem_base + (uint32_t)(S.slot * 128);
+  S.ahi0 = S.d0 + 64u;
+  S.alo0 = S.d0 + 96u;
+  S.d = S.d0 + lane_q;
+  S.ahi = S.ahi0 + lane_q;
+  S.alo = S.alo0 + lane_q;
+  const uint8_t* lo = smem + kColorW;
+  constexpr int g1 = 0, g2 = 64 * 32 * 2, c1 = g2 + 16 * 64 * 2, c2 = c1 + 64 * 32 * 2, c3 = c2 + 64 * 64 * 2;
+  const int64_t n = min((int64_t)*count, capacity);
+  const int64_t n_tiles = (n + 127) / 128;
+  for (int64_t tile = (int64_t)blockIdx.x * kColorPrecSlots + S.slot; tile < n_tiles;
+       tile += (int64_t)gridDim.x * kColorPrecSlots) {
+    const int64_t s = tile * 128 + S.r;
+    const bool live = s < n;
+    {
+      float4 f[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) f[q] = live ? cfeat[s * 8 + q] : make_float4(0.f, 0.f, 0.f, 0.f);
+      split_store<8>(S, f, 0);
+    }
+    const bool valid = live && xu[s].w > 0.0f;
+    double ddx = 0.0, ddy = 0.0, ddz = 1.0;
+    if (live) {
+      const int64_t ray = records[s] >> 8;
+      ddx = dirs[3 * ray];
+      ddy = dirs[3 * ray + 1];
+      ddz = dirs[3 * ray + 2];
+    }
+    split_layer(S, smem + g1, lo + g1, 32, 64);
+    split_relu32(S, 0, nullptr);
+    split_relu32(S, 32, nullptr);
+    split_layer(S, smem + g2, lo + g2, 64, 16);
+    float gv[16];
+    tc::tmem_ld16(S.d, gv);
+    const float sigma = valid ? expf(gv[0]) : 0.0f;
+    {
+      float cin[32];
+#pragma unroll
+      for (int i = 0; i < 15; ++i) cin[i] = gv[1 + i];
+      sh16((float)ddx, (float)ddy, (float)ddz, cin + 15);
+      cin[31] = 0.0f;
+      split_store<8>(S, reinterpret_cast<const float4*>(cin), 0);
+    }
+    split_layer(S, smem + c1, lo + c1, 32, 64);
+    split_relu32(S, 0, nullptr);
+    split_relu32(S, 32, nullptr);
+    split_layer(S, smem + c2, lo + c2, 64, 64);
+    split_relu32(S, 0, nullptr);
+    split_relu32(S, 32, nullptr);
+    split_layer(S, smem + c3, lo + c3, 64, 16);
     float cv[16];
     tc::tmem_ld16(S.d, cv);
     if (live) {
@@ -1120,14 +1387,62 @@ unsigned persistent_grid(int64_t capacity, int slots) {
   return (unsigned)(g < 1 ? 1 : g);
 }
 
+// "fp32" precision mode of cf_field_stage: fp32 tables (the deformation grid's fp32
+// parameters, not its fp16 copy), fp32 features, split-fp16 MLPs
+int field_stage_precise(const cf_field_desc* FD, const cf_march_out* S, const double* dirs, const float* xu_f,
+                        float* out_f, void* scratch, int stage, cudaStream_t st) {
+  auto run = [&](int s) { return stage < 0 || stage == s; };
+  if (FD->save_h) return cf::fail(CF_E_BAD_ARG, "cf_field_forward: training saves need the fp16 mode");
+  const int64_t cap = S->capacity;
+  const float4* xu = reinterpret_cast<const float4*>(xu_f);
+  float4* out = reinterpret_cast<float4*>(out_f);
+  float4* cfeat = reinterpret_cast<float4*>(scratch);  // (cap, 32) fp32
+  const float4* xcan = xu;
+  const unsigned hgrid = cf::grid_for(cap, 128, 16);
+  if (FD->has_deform) {
+    float4* dfeat = cfeat + cap * 8;
+    float4* xc = dfeat + cap * 8;
+    if (run(0))
+      cf::launch_pdl(hash_f16_kernel<4, 8, 2, 1, float, true>, hgrid, 128, 0, st, FD->dgrid,
+                     reinterpret_cast<const float*>(FD->dtable), xu, S->counters, cap, reinterpret_cast<uint4*>(dfeat));
+    if (run(1)) {
+      const int smem = 2 * kDeformW;
+      CF_CHECK_CUDA(cudaFuncSetAttribute(deform_mlp_prec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      cf::launch_pdl(deform_mlp_prec_kernel, persistent_grid(cap, kPrecDeformSlots),
+                     kPrecDeformSlots * kDeformSlotThreads, smem, st, FD->wblob, FD->wblob_lo, FD->dbias,
+                     FD->delta_scale, FD->inv_side, xu, static_cast<const float4*>(dfeat), S->counters, cap, xc);
+    }
+    xcan = xc;
+  }
+  if (run(2)) {
+    if (FD->has_deform)
+      cf::launch_pdl(hash_f16_kernel<2, 16, 4, 1, float, true>, hgrid, 128, 0, st, FD->cgrid,
+                     reinterpret_cast<const float*>(FD->ctable), xcan, S->counters, cap, reinterpret_cast<uint4*>(cfeat));
+    else
+      cf::launch_pdl(hash_f16_kernel<2, 16, 4, 4, float, true>, cf::grid_for(cap * 4, 128, 16), 128, 0, st, FD->cgrid,
+                     reinterpret_cast<const float*>(FD->ctable), xcan, S->counters, cap,
+                     reinterpret_cast<uint4*>(cfeat));
+  }
+  if (run(3)) {
+    const int off = FD->has_deform ? kDeformW : 0;
+    const int csmem = 2 * kColorW;
+    CF_CHECK_CUDA(cudaFuncSetAttribute(color_mlp_prec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, csmem));
+    cf::launch_pdl(color_mlp_prec_kernel, persistent_grid(cap, kColorPrecSlots), kColorPrecSlots * kSlotThreads, csmem,
+                   st, FD->wblob + off, FD->wblob_lo + off, xu, static_cast<const float4*>(cfeat), S->records, dirs,
+                   S->counters, cap, out);
+  }
+  return cf::check_launch("cf_field_forward (precise)");
+}
+
 }  // namespace
 
 extern "C" {
 
 int cf_field_scratch_bytes(const cf_field_desc* FD, int64_t capacity, int64_t* bytes) {
   if (!FD || !bytes || capacity < 0) return cf::fail(CF_E_BAD_ARG, "cf_field_scratch_bytes: bad args");
-  // cfeat (64 B) [+ dfeat (64 B) + xc (16 B)] per sample
-  *bytes = capacity * (64 + (FD->has_deform ? 64 + 16 : 0));
+  // cfeat (64 B fp16 / 128 B fp32) [+ dfeat (same) + xc (16 B)] per sample
+  const int64_t feat = FD->precise ? 128 : 64;
+  *bytes = capacity * (feat + (FD->has_deform ? feat + 16 : 0));
   return CF_OK;
 }
 
@@ -1216,9 +1531,11 @@ int cf_field_stage(const cf_field_desc* FD, const cf_march_out* S, const double*
     return cf::fail(CF_E_BAD_ARG, "cf_field_forward: grids must be 16x F2 (canonical) and 8x F4 (deform)");
   if (FD->w_bytes != (FD->has_deform ? kDeformW : 0) + kColorW)
     return cf::fail(CF_E_BAD_ARG, "cf_field_forward: weight blob size mismatch");
+  if (FD->precise && !FD->wblob_lo) return cf::fail(CF_E_BAD_ARG, "cf_field_forward: precise mode needs wblob_lo");
   cudaStream_t st = cf::as_stream(stream);
   const int64_t cap = S->capacity;
   if (cap == 0) return CF_OK;
+  if (FD->precise) return field_stage_precise(FD, S, dirs, xu_f, out_f, scratch, stage, st);
   const float4* xu = reinterpret_cast<const float4*>(xu_f);
   float4* out = reinterpret_cast<float4*>(out_f);
   uint4* cfeat = reinterpret_cast<uint4*>(scratch);

@@ -764,10 +764,10 @@ __global__ void composite_kernel(cf_march_desc M, cf_march_out F, const float4* 
       g += w * f.z;
       b += w * f.w;
       dep += w * t;
-      op += w;
       T *= 1.0f - alpha;
       if (T < t_term) break;
     }
+    op = 1.0f - T;  // = sum T_i alpha_i (telescoping), without its rounding drift
     rgb[3 * ray] = r;
     rgb[3 * ray + 1] = g;
     rgb[3 * ray + 2] = b;
@@ -800,10 +800,10 @@ __global__ void composite_final_kernel(cf_march_desc M, cf_march_out F, const fl
       g += w * f.z;
       b += w * f.w;
       dep += w * t;
-      op += w;
       T *= 1.0f - alpha;
       if (T < t_term) break;
     }
+    op = 1.0f - T;  // = sum T_i alpha_i (telescoping), without its rounding drift
     const float hd = dep / fmaxf(op, 1e-6f);
     rgb[3 * ray] = r;
     rgb[3 * ray + 1] = g;
@@ -851,11 +851,11 @@ __global__ void composite_bwd_kernel(cf_march_desc M, cf_march_out F, const floa
       S[1] += w * f.z;
       S[2] += w * f.w;
       S[3] += w * t;
-      S[4] += w;
       T *= 1.0f - a;
       used = j + 1;
       if (T < t_term) break;
     }
+    S[4] = 1.0f - T;  // opacity as the forward computes it
     float gv[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
     if (mask[ray]) {
       for (int c = 0; c < 3; ++c) {
@@ -887,10 +887,12 @@ __global__ void composite_bwd_kernel(cf_march_desc M, cf_march_out F, const floa
       const float Tn = T * (1.0f - a);
       float ds = 0.f;
 #pragma unroll
-      for (int q = 0; q < 5; ++q) {
+      for (int q = 0; q < 4; ++q) {
         P[q] += w * v[q];
         ds += gv[q] * (Tn * v[q] - (S[q] - P[q]));
       }
+      P[4] = 1.0f - Tn;  // opacity prefix, matching S[4] = 1 - T_end
+      ds += gv[4] * (Tn - (S[4] - P[4]));
       grad[off + j] = make_float4(delta * ds, w * gv[0], w * gv[1], w * gv[2]);
       T = Tn;
     }

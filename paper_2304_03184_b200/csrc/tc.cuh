@@ -132,12 +132,33 @@ __device__ __forceinline__ void mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uin
       "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
-__device__ __forceinline__ void issue_layer_ts(uint32_t tmem_d, uint32_t tmem_a, const uint8_t* b_buf, int K, int N) {
+__device__ __forceinline__ void issue_layer_ts(uint32_t tmem_d, uint32_t tmem_a, const uint8_t* b_buf, int K, int N,
+                                               bool accumulate = false) {
   const uint32_t b0 = smem_u32(b_buf);
   const uint32_t idesc = idesc_f16(128, N);
   for (int ks = 0; ks < K / 16; ++ks)
     mma_f16_ts(tmem_d, tmem_a + (uint32_t)(ks * 8), sdesc(b0 + ks * 256, 128, (uint32_t)K * 16), idesc,
-               ks > 0 ? 1u : 0u);
+               (accumulate || ks > 0) ? 1u : 0u);
+}
+
+// Split-fp16 layer ("fp32" precision mode): with A = Ah + Al and B = Bh + Bl
+// (hi = fp16(x), lo = fp16(x - hi)), D = Ah.Bh + Ah.Bl + Al.Bh accumulated in fp32
+// TMEM — three kind::f16 MMA chains, ~22 significant bits per operand (the
+// dropped Al.Bl term is 2^-22 relative). A halves in TMEM (TS form), B halves in smem.
+__device__ __forceinline__ void issue_layer_ts_split(uint32_t tmem_d, uint32_t a_hi, uint32_t a_lo,
+                                                     const uint8_t* b_hi, const uint8_t* b_lo, int K, int N) {
+  issue_layer_ts(tmem_d, a_hi, b_hi, K, N, false);
+  issue_layer_ts(tmem_d, a_hi, b_lo, K, N, true);
+  issue_layer_ts(tmem_d, a_lo, b_hi, K, N, true);
+}
+
+// (a, b) -> packed fp16x2 hi = fp16(x) and lo = fp16(x - hi) (low halves = a)
+__device__ __forceinline__ void split_f16x2(float a, float b, uint32_t& hi, uint32_t& lo) {
+  const __half2 h = __floats2half2_rn(a, b);
+  const float2 hf = __half22float2(h);
+  const __half2 l = __floats2half2_rn(a - hf.x, b - hf.y);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
 }
 
 // 32 fp32 columns without the wait (issue several, then tmem_wait_ld once)

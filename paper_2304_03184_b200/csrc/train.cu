@@ -27,12 +27,15 @@ __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g, 
   }
 }
 
-__global__ void pack_kernel(const float* __restrict__ w, int n, int k, int np, int kp, uint8_t* __restrict__ blob) {
+__global__ void pack_kernel(const float* __restrict__ w, int n, int k, int np, int kp, uint8_t* __restrict__ blob,
+                            uint8_t* __restrict__ blob_lo) {
   const int total = np * kp;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
     const int r = e / kp, c = e % kp;
     const float x = (r < n && c < k) ? w[r * k + c] : 0.0f;
-    *reinterpret_cast<__half*>(blob + tc::core_offset(r, c, kp)) = __float2half_rn(x);
+    const __half h = __float2half_rn(x);
+    *reinterpret_cast<__half*>(blob + tc::core_offset(r, c, kp)) = h;
+    if (blob_lo) *reinterpret_cast<__half*>(blob_lo + tc::core_offset(r, c, kp)) = __float2half_rn(x - __half2float(h));
   }
 }
 
@@ -223,8 +226,17 @@ int cf_adam(float* p, const float* g, float* m, float* v, int64_t n, float lr, f
 int cf_pack_weight(const float* w, int n, int k, uint8_t* blob, void* stream) {
   if (!w || !blob || n < 1 || k < 1) return cf::fail(CF_E_BAD_ARG, "cf_pack_weight: bad args");
   const int np = (n + 15) / 16 * 16, kp = (k + 15) / 16 * 16;
-  pack_kernel<<<cf::grid_for((int64_t)np * kp, 256, 2), 256, 0, cf::as_stream(stream)>>>(w, n, k, np, kp, blob);
+  pack_kernel<<<cf::grid_for((int64_t)np * kp, 256, 2), 256, 0, cf::as_stream(stream)>>>(w, n, k, np, kp, blob,
+                                                                                          nullptr);
   return cf::check_launch("cf_pack_weight");
+}
+
+int cf_pack_weight_split(const float* w, int n, int k, uint8_t* blob, uint8_t* blob_lo, void* stream) {
+  if (!w || !blob || !blob_lo || n < 1 || k < 1) return cf::fail(CF_E_BAD_ARG, "cf_pack_weight_split: bad args");
+  const int np = (n + 15) / 16 * 16, kp = (k + 15) / 16 * 16;
+  pack_kernel<<<cf::grid_for((int64_t)np * kp, 256, 2), 256, 0, cf::as_stream(stream)>>>(w, n, k, np, kp, blob,
+                                                                                          blob_lo);
+  return cf::check_launch("cf_pack_weight_split");
 }
 
 }  // extern "C"

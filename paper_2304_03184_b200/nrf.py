@@ -108,14 +108,16 @@ def pad16(n: int) -> int:
     return (n + 15) // 16 * 16
 
 
-def pack_weight(W: np.ndarray) -> np.ndarray:
+def pack_weight(W: np.ndarray, lo: bool = False) -> np.ndarray:
     """(N, K) float -> fp16 bytes in the UMMA canonical K-major layout
-    [n/8][k/8][n%8][k%8] with N, K zero-padded to multiples of 16."""
+    [n/8][k/8][n%8][k%8] with N, K zero-padded to multiples of 16. lo=True packs
+    the residual fp16(W - fp16(W)) instead (the "fp32" precision mode's B halves)."""
     W = np.asarray(W, dtype=np.float32)
     n, k = W.shape
     Np, Kp = pad16(n), pad16(k)
     P = np.zeros((Np, Kp), dtype=np.float16)
-    P[:n, :k] = W.astype(np.float16)
+    h = W.astype(np.float16)
+    P[:n, :k] = (W - h.astype(np.float32)).astype(np.float16) if lo else h
     return P.reshape(Np // 8, 8, Kp // 8, 8).transpose(0, 2, 1, 3).reshape(-1).view(np.uint8)
 
 

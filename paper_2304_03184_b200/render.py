@@ -67,7 +67,17 @@ class RenderConfig:
     obj_occ_res: int = 64
     obj_shell: float = 0.02
     background: tuple = (24 / 255.0, 28 / 255.0, 34 / 255.0)   # config.py bg_r/g/b
+    # "fp32": fp32 hash tables and features, split-fp16 (hi + lo) tensor-core MLP operands —
+    # the SPEC's 32-bit semantics within 1e-4; "fp16": fp16 operands and
+    # features, fp16 copy of the deformation table
+    precision: str = "fp32"
     cuda_graphs: bool = True      # replay the captured frame (False: launch every kernel each view)
+
+
+def _precise(precision: str) -> bool:
+    if precision not in ("fp32", "fp16"):
+        raise ValueError(f"precision must be 'fp32' or 'fp16', not {precision!r}")
+    return precision == "fp32"
 
 
 def _kaiming(rng, n_out, n_in):
@@ -85,7 +95,9 @@ def occ_grid(gmin, size, res) -> _lib.OccGrid:
 
 
 class FieldNets:
-    """Weights of one field: [DeformNet], E_g, E_c (fp16-representable fp32 copies kept on host)."""
+    """Weights of one field: [DeformNet], E_g, E_c (fp32 on the host). The device blobs
+    hold them in the tcgen05 operand layout: `blob` = fp16(W), `blob_lo` =
+    fp16(W - fp16(W)) (used by the "fp32" precision mode)."""
 
     def __init__(self, rng, deform: bool, zero_deform_out: bool = True, theta_dim: int = 72):
         self.deform = deform
@@ -104,13 +116,14 @@ class FieldNets:
         self.repack()
 
     def repack(self) -> None:
-        """Round the host weights to fp16 and upload them in the tcgen05 operand layout."""
-        self.layers = {k: v.astype(np.float16).astype(np.float32) for k, v in self.layers.items()}
+        """Upload the host weights in the tcgen05 operand layout (hi and lo halves)."""
+        self.layers = {k: np.asarray(v, dtype=np.float32) for k, v in self.layers.items()}
         order = (["D1h", "D2", "D3", "D4", "D5"] if self.deform else []) + ["G1", "G2", "C1", "C2", "C3"]
         mats = [self.layers["D1"][:, :32] if k == "D1h" else self.layers[k] for k in order]
         blob = np.concatenate([pack_weight(m) for m in mats])
         self.w_bytes = int(blob.size)
         self.blob = dev(blob.copy(), dtype=torch.uint8)
+        self.blob_lo = dev(np.concatenate([pack_weight(m, lo=True) for m in mats]).copy(), dtype=torch.uint8)
 
     def theta_bias(self, theta) -> np.ndarray:
         """DeformNet layer-1 pose term W1[:, 32:] @ theta, folded into a per-frame bias (fp32)."""
@@ -166,14 +179,17 @@ class HumanField:
                   cfg.ed_k, cfg.ed_radius, cap, self.occ_cells.data_ptr(), self.occ_nbr.data_ptr(),
                   self.occ_w.data_ptr(), self.occ_count.data_ptr(), _lib.stream_ptr())
 
-    def desc(self, dbias: torch.Tensor) -> _lib.FieldDesc:
+    def desc(self, dbias: torch.Tensor, precision: str | None = None) -> _lib.FieldDesc:
+        precise = _precise(precision or self.cfg.precision)
         d = _lib.FieldDesc()
         d.has_deform = 1
         d.dgrid = self.dgrid.desc
-        d.dtable = self.dgrid.table_for_kernels().data_ptr()
+        d.dtable = (self.dgrid.table if precise else self.dgrid.table_for_kernels()).data_ptr()
         d.cgrid = self.cgrid.desc
         d.ctable = self.cgrid.table_for_kernels().data_ptr()
         d.wblob = self.nets.blob.data_ptr()
+        d.wblob_lo = self.nets.blob_lo.data_ptr()
+        d.precise = int(precise)
         d.w_bytes = self.nets.w_bytes
         d.dbias = dbias.data_ptr()
         d.delta_scale = 0.05
@@ -199,12 +215,14 @@ class ObjectField:
         h = (ctypes.c_double * 3)(*self.half)
         _lib.call("cf_occ_box_shell", _lib.byref(self.occ), h, cfg.obj_shell, self.bits.data_ptr(), _lib.stream_ptr())
 
-    def desc(self) -> _lib.FieldDesc:
+    def desc(self, precision: str | None = None) -> _lib.FieldDesc:
         d = _lib.FieldDesc()
         d.has_deform = 0
         d.cgrid = self.cgrid.desc
         d.ctable = self.cgrid.table_for_kernels().data_ptr()
         d.wblob = self.nets.blob.data_ptr()
+        d.wblob_lo = self.nets.blob_lo.data_ptr()
+        d.precise = int(_precise(precision or self.cfg.precision))
         d.w_bytes = self.nets.w_bytes
         d.delta_scale = 0.05
         d.inv_side = self.inv_side
@@ -373,7 +391,7 @@ class Renderer:
             w.anchors = self._anchors.data_ptr()
             w.n_nodes = int(self._anchors.shape[0])
             self.hw = w
-            self.hdesc = h.desc(self.dbias)
+            self.hdesc = h.desc(self.dbias, self.cfg.precision)
         self._setup_pending = True
 
     def _human_setup(self) -> None:
@@ -408,7 +426,7 @@ class Renderer:
         self._frame_host[3:12] = np.asarray(obj_R, dtype=np.float64).reshape(9)
         self._frame_host[12:15] = np.asarray(obj_t, dtype=np.float64).reshape(3)
         if getattr(self, "odesc", None) is None:
-            self.odesc = self.obj.desc()
+            self.odesc = self.obj.desc(self.cfg.precision)
 
     # -- per-view --------------------------------------------------------------
 

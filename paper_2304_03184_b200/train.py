@@ -117,7 +117,8 @@ class ColorParams:
         for k in COLOR_LAYERS:
             w = self.W[k]
             n, kk = w.shape
-            _lib.call("cf_pack_weight", w.data_ptr(), n, kk, self.nets.blob.data_ptr() + o, s)
+            _lib.call("cf_pack_weight_split", w.data_ptr(), n, kk, self.nets.blob.data_ptr() + o,
+                      self.nets.blob_lo.data_ptr() + o, s)
             o += ((n + 15) // 16 * 16) * ((kk + 15) // 16 * 16) * 2
         o = 0
         for k in ("C3", "C2", "C1", "G2", "G1"):
@@ -160,7 +161,8 @@ class DeformParams:
         o = 0
         for w in mats:
             n, kk = w.shape
-            _lib.call("cf_pack_weight", w.data_ptr(), n, kk, self.nets.blob.data_ptr() + o, s)
+            _lib.call("cf_pack_weight_split", w.data_ptr(), n, kk, self.nets.blob.data_ptr() + o,
+                      self.nets.blob_lo.data_ptr() + o, s)
             o += ((n + 15) // 16 * 16) * ((kk + 15) // 16 * 16) * 2
         keep = [self.W["D5"].t().contiguous(), self.W["D4"].t().contiguous(), self.W["D3"].t().contiguous(),
                 self.W["D2"].t().contiguous(), self.W["D1"][:, :32].t().contiguous()]
@@ -259,21 +261,20 @@ class Trainer:
         if st["name"] == "human":
             _lib.call("cf_human_canon", _lib.byref(M), self.dirs.data_ptr(), _lib.byref(buf.mo), _lib.byref(r.hw),
                       r._anchor_buckets.handle, field.lbs.buckets.handle, buf.xu.data_ptr(), s)
-            desc = r.hdesc
+            # the training forward runs the fp16 mode (its backward consumes the fp16 saves)
+            desc = field.desc(r.dbias, "fp16")
             if dp is not None:
-                # a private descriptor: this frame's pose bias from the current W1, forward saves on
+                # this frame's pose bias from the current W1, forward saves on
                 if b.theta is None:
                     raise ValueError("DeformNet training needs FrameBatch.theta")
                 st["dbias"] = dp.bias(b.theta)
-                desc = _lib.FieldDesc()
-                ctypes.memmove(ctypes.byref(desc), ctypes.byref(r.hdesc), ctypes.sizeof(desc))
                 desc.dbias = st["dbias"].data_ptr()
                 desc.save_h = st["dbufs"].save_h.data_ptr()
                 desc.save_o = st["dbufs"].save_o.data_ptr()
                 desc.save_mask = st["dbufs"].save_mask.data_ptr()
         else:
             _lib.call("cf_object_canon", _lib.byref(M), self.dirs.data_ptr(), _lib.byref(buf.mo), buf.xu.data_ptr(), s)
-            desc = r.odesc
+            desc = field.desc("fp16")
         scratch = r._scratch(buf, desc)
         _lib.call("cf_field_forward", _lib.byref(desc), _lib.byref(buf.mo), self.dirs.data_ptr(), buf.xu.data_ptr(),
                   buf.out.data_ptr(), scratch.data_ptr(), s)
@@ -411,10 +412,10 @@ def sync_host_weights(trainer: "Trainer") -> None:
     for st in trainer.fields:
         nets = st["field"].nets
         for k, w in st["params"].W.items():
-            nets.layers[k] = w.cpu().numpy().astype(np.float16).astype(np.float32)
+            nets.layers[k] = w.cpu().numpy().astype(np.float32)
         if "deform" in st:
             for k, w in st["deform"].W.items():
-                nets.layers[k] = w.cpu().numpy().astype(np.float16).astype(np.float32)
+                nets.layers[k] = w.cpu().numpy().astype(np.float32)
 
 
 def allreduce_grads(tensors, group=None):

@@ -51,3 +51,47 @@ def test_mlp_kernel_precision_matches_fp64_loosely():
     x = rng.normal(size=(100, 32))
     ref = np.maximum(x @ Ws[0].T, 0) @ Ws[1].T
     assert np.allclose(on.mlp_forward(Ws, x), ref, rtol=2e-2, atol=2e-2)
+
+
+# ---- volume_render examples and invariants (acceptance 5)
+
+def _uniform_ray(sig, t_near=0.3, t_far=5.0, rgb=(0.2, 0.5, 0.9)):
+    from oracle import render as orr
+    S = len(sig)
+    dt = (t_far - t_near) / S
+    f = np.zeros((S, 4), dtype=np.float32)
+    f[:, 0] = sig
+    f[:, 1:] = rgb
+    return orr.composite(1, np.zeros(S, np.int64), np.arange(S), f, t_near, dt, t_term=0.0), dt
+
+
+def test_volume_render_zero_density():
+    (rgb, depth, op), _ = _uniform_ray(np.zeros(128))
+    assert (rgb == 0).all() and op[0] == 0.0  # black background, opacity 0
+
+
+def test_volume_render_constant_density_analytic():
+    for sigma in (0.05, 0.5, 1.0, 1.9):
+        (rgb, depth, op), dt = _uniform_ray(np.full(128, sigma, np.float32))
+        ell = 128 * dt
+        assert abs(op[0] - (1.0 - np.exp(-float(np.float32(sigma)) * ell))) <= 1e-5
+
+
+def test_volume_render_thin_slab_depth():
+    S, t_near, t_far = 128, 0.3, 5.0
+    dt = (t_far - t_near) / S
+    for t_star in (0.9, 2.35, 4.1):
+        i0 = int((t_star - t_near) / dt)
+        sig = np.zeros(S, np.float32)
+        sig[i0] = 5e3  # near-opaque slab one sample thick
+        (rgb, depth, op), _ = _uniform_ray(sig, t_near, t_far)
+        assert op[0] > 0.999 and abs(depth[0] - t_star) <= dt
+
+
+def test_volume_render_telescoping():
+    rng = np.random.default_rng(5)
+    for _ in range(20):
+        sig = (rng.exponential(0.3, 128) * (rng.random(128) < 0.5)).astype(np.float32)
+        (rgb, depth, op), dt = _uniform_ray(sig)
+        T_end = np.prod(1.0 - (1.0 - np.exp(-sig.astype(np.float64) * float(np.float32(dt)))))
+        assert abs(op[0] + T_end - 1.0) <= 1e-6

@@ -3,7 +3,8 @@ nodes + 6890 skin verts, 16-level 2^19 grid), stage by stage against the
 oracle fed with the previous stage's device output:
   occupancy bits, march sample sets, ED/LBS flags      bit-exact
   canonical coordinates (float32)                      ED: bit-exact; LBS: 1e-6
-  field sigma / rgb (fp16 tensor-core MLPs)            see FIELD_* below
+  field sigma / rgb ("fp16" mode: fp16 tensor-core     see FIELD_* below
+  operands) vs the kernel-precision oracle             (the "fp32" mode: test_precision_gpu.py)
   composite rgb / opacity / depth                      1e-5 abs
   layer choice                                         bit-exact
 """
@@ -29,7 +30,7 @@ def words(t):
 @pytest.fixture(scope="module")
 def setup():
     sc = Scene(SceneConfig(width=64, height=64), seed=0)
-    cfg = RenderConfig(n_samples=64)
+    cfg = RenderConfig(n_samples=64, precision="fp16")
     hf = HumanField(sc.nodes, sc.template_points, sc.skin_verts, sc.skin_weights, cfg, seed=0, zero_deform_out=False,
                     table_scale=0.5)
     of = ObjectField(sc.box_half, cfg, seed=1, table_scale=0.5)
