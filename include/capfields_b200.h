@@ -358,11 +358,14 @@ int cf_keyframe_rays(const cf_camera* cam, const int* fg_pixels, int64_t n_fg, i
 int cf_train_sample(const cf_march_desc* M, const float* gt_depth, const uint8_t* mask, int n_guided, int n_uniform,
                     int n_empty, double sigma_d, uint64_t seed, const cf_march_out* F, double* t_out, void* stream);
 /* masked L2 colour + lambda * L1 depth (lambda_depth = 0.1) and the
- * compositing backward: grad = float4 (dL/dsigma, dL/dr, dL/dg, dL/db) per sample;
- * loss[0] += L_color, loss[1] += L_depth (unweighted), normalised by inv_n_* */
+ * compositing backward: grad = grad_scale * float4 (dL/dsigma, dL/dr, dL/dg, dL/db) per
+ * sample (grad_scale: a power of two keeping the fp16 backward operands in range —
+ * loss scaling; the optimiser divides it out); loss[0] += L_color, loss[1] += L_depth
+ * (unweighted, unscaled), normalised by inv_n_* */
 int cf_loss_composite_bwd(const cf_march_desc* M, const cf_march_out* F, const float* field, float t_term,
                           const float* gt_rgb, const float* gt_depth, const uint8_t* mask, float lambda_depth,
-                          float inv_n_color, float inv_n_depth, float* grad, float* loss, void* stream);
+                          float inv_n_color, float inv_n_depth, float grad_scale, float* grad, float* loss,
+                          void* stream);
 
 /* saved activations (fp16 rows) and gradients of the E_g/E_c backward (S = capacity) */
 typedef struct cf_color_bwd_io {

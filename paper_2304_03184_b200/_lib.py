@@ -213,7 +213,7 @@ _SIGS = {
     "cf_keyframe_rays": [_P(Camera), _p, _i64, _i64, ctypes.c_uint64, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p],
     "cf_train_sample": [_P(MarchDesc), _p, _p, _i32, _i32, _i32, _f64, ctypes.c_uint64, _P(MarchOut), _p, _p],
     "cf_loss_composite_bwd": [_P(MarchDesc), _P(MarchOut), _p, ctypes.c_float, _p, _p, _p, ctypes.c_float,
-                              ctypes.c_float, ctypes.c_float, _p, _p, _p],
+                              ctypes.c_float, ctypes.c_float, ctypes.c_float, _p, _p, _p],
     "cf_color_backward": [_P(FieldDesc), _p, _P(MarchOut), _p, _p, _p, _p, _P(ColorBwdIO), _p],
     "cf_field_hash_backward": [_P(FieldDesc), _P(MarchOut), _p, _p, _p, _p, _p, _p],
     "cf_deform_backward": [_P(FieldDesc), _p, _P(MarchOut), _p, _p, _P(DeformBwdIO), _p],

@@ -833,8 +833,8 @@ __global__ void composite_final_kernel(cf_march_desc M, cf_march_out F, const fl
 __global__ void composite_bwd_kernel(cf_march_desc M, cf_march_out F, const float4* __restrict__ field,
                                      float t_term, const float* __restrict__ gt_rgb,
                                      const float* __restrict__ gt_depth, const uint8_t* __restrict__ mask,
-                                     float lambda, float inv_nm, float inv_nd, float4* __restrict__ grad,
-                                     float* __restrict__ loss) {
+                                     float lambda, float inv_nm, float inv_nd, float gscale,
+                                     float4* __restrict__ grad, float* __restrict__ loss) {
   float lc = 0.f, ld = 0.f;
   for (int64_t ray = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ray < M.n_rays;
        ray += (int64_t)gridDim.x * blockDim.x) {
@@ -861,13 +861,13 @@ __global__ void composite_bwd_kernel(cf_march_desc M, cf_march_out F, const floa
       for (int c = 0; c < 3; ++c) {
         const float e = S[c] - gt_rgb[3 * ray + c];
         lc += e * e * inv_nm;
-        gv[c] = 2.0f * e * inv_nm;
+        gv[c] = 2.0f * e * inv_nm * gscale;
       }
       const float gd = gt_depth[ray];
       if (gd > 0.f) {
         const float O = fmaxf(S[4], 1e-6f), depth = S[3] / O, e = depth - gd;
         ld += fabsf(e) * inv_nd;
-        const float gdep = lambda * inv_nd * (e > 0.f ? 1.f : (e < 0.f ? -1.f : 0.f));
+        const float gdep = lambda * inv_nd * gscale * (e > 0.f ? 1.f : (e < 0.f ? -1.f : 0.f));
         gv[3] = gdep / O;
         gv[4] = S[4] > 1e-6f ? -gdep * S[3] / (S[4] * S[4]) : 0.f;
       }
@@ -1246,13 +1246,14 @@ int cf_train_sample(const cf_march_desc* M, const float* gt_depth, const uint8_t
 
 int cf_loss_composite_bwd(const cf_march_desc* M, const cf_march_out* F, const float* field, float t_term,
                           const float* gt_rgb, const float* gt_depth, const uint8_t* mask, float lambda_depth,
-                          float inv_n_color, float inv_n_depth, float* grad, float* loss, void* stream) {
+                          float inv_n_color, float inv_n_depth, float grad_scale, float* grad, float* loss,
+                          void* stream) {
   if (!M || !F || !field || !gt_rgb || !gt_depth || !mask || !grad)
     return cf::fail(CF_E_BAD_ARG, "cf_loss_composite_bwd: bad args");
   if (M->n_rays == 0) return CF_OK;
   composite_bwd_kernel<<<cf::grid_for(M->n_rays, 128, 8), 128, 0, cf::as_stream(stream)>>>(
       *M, *F, reinterpret_cast<const float4*>(field), t_term, gt_rgb, gt_depth, mask, lambda_depth, inv_n_color,
-      inv_n_depth, reinterpret_cast<float4*>(grad), loss);
+      inv_n_depth, grad_scale, reinterpret_cast<float4*>(grad), loss);
   return cf::check_launch("cf_loss_composite_bwd");
 }
 

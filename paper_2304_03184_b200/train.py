@@ -278,9 +278,11 @@ class Trainer:
         scratch = r._scratch(buf, desc)
         _lib.call("cf_field_forward", _lib.byref(desc), _lib.byref(buf.mo), self.dirs.data_ptr(), buf.xu.data_ptr(),
                   buf.out.data_ptr(), scratch.data_ptr(), s)
+        if st.get("gscale") is None:
+            st["gscale"] = loss_scale(n_m)
         _lib.call("cf_loss_composite_bwd", _lib.byref(M), _lib.byref(buf.mo), buf.out.data_ptr(), r.cfg.t_term,
                   b.gt_rgb.data_ptr(), b.gt_depth.data_ptr(), mask.data_ptr(), cfg.lambda_depth, 1.0 / n_m,
-                  1.0 / max(n_d, 1), bwd.grad.data_ptr(), stats.data_ptr(), s)
+                  1.0 / max(n_d, 1), st["gscale"], bwd.grad.data_ptr(), stats.data_ptr(), s)
         _lib.call("cf_color_backward", _lib.byref(desc), P.wt_blob.data_ptr(), _lib.byref(buf.mo),
                   self.dirs.data_ptr(), buf.xu.data_ptr(), bwd.grad.data_ptr(), scratch.data_ptr(),
                   _lib.byref(bwd.io), s)
@@ -368,6 +370,9 @@ class Trainer:
                 st["dtgrad"].zero_()
                 st["deform"].zero_grad()
             st["stats"] = torch.zeros(2, dtype=torch.float32, device=self.dirs.device)
+        for st in self.fields:  # one loss scale per field and step (every frame's grads add up)
+            mk = [b.mask_h if st["name"] == "human" else b.mask_o for b in batches]
+            st["gscale"] = loss_scale(min(int(m.sum()) for m in mk))
         for b in batches:
             self.set_frame(b)
             for st in self.fields:
@@ -382,24 +387,25 @@ class Trainer:
         cfg, s = self.cfg, _lib.stream_ptr()
         nb = float(len(batches))
         for st in self.fields:
+            unscale = 1.0 / (nb * st["gscale"])  # mean over frames, loss scale divided out
             t = st["field"].cgrid.table
             _lib.call("cf_adam", t.data_ptr(), st["tgrad"].data_ptr(), st["tm"].data_ptr(), st["tv"].data_ptr(),
-                      t.numel(), cfg.lr_hash, cfg.beta1, cfg.beta2, cfg.eps, self.step_count, 1.0 / nb, s)
+                      t.numel(), cfg.lr_hash, cfg.beta1, cfg.beta2, cfg.eps, self.step_count, unscale, s)
             st["field"].cgrid.refresh_f16()
             P = st["params"]
             for k in COLOR_LAYERS:
                 _lib.call("cf_adam", P.W[k].data_ptr(), P.G[k].data_ptr(), P.m[k].data_ptr(), P.v[k].data_ptr(),
-                          P.W[k].numel(), cfg.lr_net, cfg.beta1, cfg.beta2, cfg.eps, self.step_count, 1.0 / nb, s)
+                          P.W[k].numel(), cfg.lr_net, cfg.beta1, cfg.beta2, cfg.eps, self.step_count, unscale, s)
             P.pack()
             if "deform" in st:
                 t = st["field"].dgrid.table
                 _lib.call("cf_adam", t.data_ptr(), st["dtgrad"].data_ptr(), st["dtm"].data_ptr(), st["dtv"].data_ptr(),
-                          t.numel(), cfg.lr_hash, cfg.beta1, cfg.beta2, cfg.eps, self.step_count, 1.0 / nb, s)
+                          t.numel(), cfg.lr_hash, cfg.beta1, cfg.beta2, cfg.eps, self.step_count, unscale, s)
                 st["field"].dgrid.refresh_f16()
                 D = st["deform"]
                 for k in DEFORM_LAYERS:
                     _lib.call("cf_adam", D.W[k].data_ptr(), D.G[k].data_ptr(), D.m[k].data_ptr(), D.v[k].data_ptr(),
-                              D.W[k].numel(), cfg.lr_net, cfg.beta1, cfg.beta2, cfg.eps, self.step_count, 1.0 / nb,
+                              D.W[k].numel(), cfg.lr_net, cfg.beta1, cfg.beta2, cfg.eps, self.step_count, unscale,
                               s)
                 D.pack()
             out[st["name"]] = st["stats"] / nb
@@ -416,6 +422,13 @@ def sync_host_weights(trainer: "Trainer") -> None:
         if "deform" in st:
             for k, w in st["deform"].W.items():
                 nets.layers[k] = w.cpu().numpy().astype(np.float32)
+
+
+def loss_scale(n_masked: int) -> float:
+    """Power-of-two loss scale of a field's backward: the per-sample gradients of the
+    1/n-normalised loss are O(1/n); scaled by 2^floor(log2 n) they are O(1), inside
+    the fp16 range of the backward's tensor-core operands (no subnormal underflow)."""
+    return float(2.0 ** max(0, int(np.floor(np.log2(max(1, n_masked))))))
 
 
 def allreduce_grads(tensors, group=None):
