@@ -468,6 +468,10 @@ int cf_mp_write(const char* path, int create, int32_t n_nodes, int32_t n_theta, 
  * theta (n_frames, 3J) device float64 -> A (n_frames, J, 4, 4) device float64,
  * A_j = G_j(theta) G_j(0)^-1. parents (J) int32 and offsets (J, 3) float64 are HOST
  * arrays (parents[j] < j, -1 = root), J <= 64. */
+/* DeformNet layer-1 pose bias of a frame: out[i] = sum_j W[i * ldw + col0 + j] * (float)theta[j]
+ * (fp32, j ascending) — the theta fold of DESIGN.md §3, run per frame on the device */
+int cf_pose_bias(const float* W, int ldw, int col0, int n_out, const double* theta, int n_theta, float* out,
+                 void* stream);
 int cf_skinning_transforms(const double* theta, int64_t n_frames, const int32_t* parents, const double* offsets,
                            int32_t n_joints, double* A, void* stream);
 

@@ -230,6 +230,7 @@ _SIGS = {
     "cf_mp_read": [ctypes.c_char_p, _i64, _i64, _p, _p, _p, _p, _p],
     "cf_mp_write": [ctypes.c_char_p, _i32, _i32, _i32, _i64, _p, _p, _p, _p, _p],
     "cf_skinning_transforms": [_p, _i64, _p, _p, _i32, _p, _p],
+    "cf_pose_bias": [_p, _i32, _i32, _i32, _p, _i32, _p, _p],
     "cf_blur_score": [_p, _i32, _i32, _p, _p, _p],
     "cf_visibility_map": [_p, _i32, _p, _i32, _i32, _P(VisCamera), ctypes.c_double, _p, _p],
     "cf_pool_scan": [_P(PoolDesc), _P(PoolEntry), _p, _p, _p],

@@ -201,6 +201,17 @@ __global__ void __launch_bounds__(32 * kFkWarps) fk_kernel(const double* __restr
   }
 }
 
+// DeformNet layer-1 pose term of a frame (theta folded into a per-frame bias,
+// DESIGN.md §3): out[i] = sum_j W[i, col0 + j] * (float)theta[j], fp32, j ascending.
+__global__ void pose_bias_kernel(const float* __restrict__ W, int ldw, int col0, int n_out,
+                                 const double* __restrict__ theta, int n_theta, float* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_out) return;
+  float acc = 0.0f;
+  for (int j = 0; j < n_theta; ++j) acc = __fadd_rn(acc, __fmul_rn(W[(int64_t)i * ldw + col0 + j], (float)theta[j]));
+  out[i] = acc;
+}
+
 }  // namespace
 
 extern "C" {
@@ -250,6 +261,16 @@ int cf_mp_write(const char* path, int create, int32_t n_nodes, int32_t n_theta, 
   }
   ok = ok && std::fflush(F.f) == 0;
   return ok ? CF_OK : cf::fail(CF_E_BAD_ARG, std::string(path) + ": write failed");
+}
+
+int cf_pose_bias(const float* W, int ldw, int col0, int n_out, const double* theta, int n_theta, float* out,
+                 void* stream) {
+  if (!W || !theta || !out || n_out < 0 || n_theta < 0 || ldw < col0 + n_theta)
+    return cf::fail(CF_E_BAD_ARG, "cf_pose_bias: bad args");
+  if (n_out == 0) return CF_OK;
+  pose_bias_kernel<<<(unsigned)((n_out + 127) / 128), 128, 0, cf::as_stream(stream)>>>(W, ldw, col0, n_out, theta,
+                                                                                       n_theta, out);
+  return cf::check_launch("cf_pose_bias");
 }
 
 int cf_skinning_transforms(const double* theta, int64_t n_frames, const int32_t* parents, const double* offsets,

@@ -72,6 +72,7 @@ class RenderConfig:
     # features, fp16 copy of the deformation table
     precision: str = "fp32"
     cuda_graphs: bool = True      # replay the captured frame (False: launch every kernel each view)
+    serial: bool = False          # every launch on the caller's stream (per-kernel timing; no side stream)
 
 
 def _precise(precision: str) -> bool:
@@ -124,6 +125,13 @@ class FieldNets:
         self.w_bytes = int(blob.size)
         self.blob = dev(blob.copy(), dtype=torch.uint8)
         self.blob_lo = dev(np.concatenate([pack_weight(m, lo=True) for m in mats]).copy(), dtype=torch.uint8)
+        # DeformNet layer 1 in fp32 on the device: its pose columns give the per-frame
+        # bias on the device (cf_pose_bias); the trainer updates this tensor in place
+        if self.deform:
+            if getattr(self, "d1", None) is None:
+                self.d1 = dev(self.layers["D1"], dtype=torch.float32)
+            else:
+                self.d1.copy_(torch.from_numpy(self.layers["D1"]))
 
     def theta_bias(self, theta) -> np.ndarray:
         """DeformNet layer-1 pose term W1[:, 32:] @ theta, folded into a per-frame bias (fp32)."""
@@ -361,11 +369,23 @@ class Renderer:
         if self.obj is not None:
             self.set_object_pose(obj_R, obj_t)
 
-    def load_prior(self, dqs: torch.Tensor, bone_A: torch.Tensor, dbias: torch.Tensor) -> None:
-        """Per-frame human prior from device-resident tensors (no host sync): node
-        dqs (n,8) f64, bone transforms (J,4,4) f64, DeformNet pose bias (128,) f32.
-        Staged into the renderer's fixed buffers; the setup kernels run with the
-        next view (inside its graph)."""
+    def load_pose(self, dqs: torch.Tensor, theta: torch.Tensor) -> None:
+        """Per-frame human prior as the tracker emits it (a CFMP record, records.py:98-126):
+        node dqs (n,8) f64 and pose theta (72,) f64, device or pinned host tensors. The
+        frame's setup runs the forward kinematics (cf_skinning_transforms, skeleton.py:
+        121-139) and the DeformNet pose bias (cf_pose_bias) on the device, then the warp
+        setup — no host FK, no host matvec."""
+        self._prior_buffers()
+        if getattr(self, "_theta", None) is None:
+            self._theta = torch.empty(self.human.lbs.J * 3, dtype=torch.float64, device=self.dirs.device)
+            from .records import _rig_arrays
+            self._rig = _rig_arrays(None)
+        self._defer_copy(self._dqs, dqs)
+        self._defer_copy(self._theta, theta)
+        self._pose_on_device = True
+        self._setup_pending = True
+
+    def _prior_buffers(self) -> None:
         h = self.human
         if getattr(self, "_dqs", None) is None:
             n = len(h.graph.nodes)
@@ -374,10 +394,6 @@ class Renderer:
             self._A = torch.empty((h.lbs.J, 4, 4), dtype=torch.float64, device=self.dirs.device)
             self.dbias = torch.empty(128, dtype=torch.float32, device=self.dirs.device)
             self._anchor_buckets = Buckets(n)
-        # enqueued with the next view's frame block as one batched copy (sources must
-        # stay valid until that view, or prepare_frame, is issued)
-        for dst, src in ((self._dqs, dqs), (self._A, bone_A), (self.dbias, dbias)):
-            self._defer_copy(dst, src)
         if getattr(self, "hw", None) is None:
             w = _lib.HumanWarp()
             w.dqs = self._dqs.data_ptr()
@@ -392,6 +408,18 @@ class Renderer:
             w.n_nodes = int(self._anchors.shape[0])
             self.hw = w
             self.hdesc = h.desc(self.dbias, self.cfg.precision)
+
+    def load_prior(self, dqs: torch.Tensor, bone_A: torch.Tensor, dbias: torch.Tensor) -> None:
+        """Per-frame human prior from device-resident tensors (no host sync): node
+        dqs (n,8) f64, bone transforms (J,4,4) f64, DeformNet pose bias (128,) f32.
+        Staged into the renderer's fixed buffers; the setup kernels run with the
+        next view (inside its graph)."""
+        self._prior_buffers()
+        self._pose_on_device = False
+        # enqueued with the next view's frame block as one batched copy (sources must
+        # stay valid until that view, or prepare_frame, is issued)
+        for dst, src in ((self._dqs, dqs), (self._A, bone_A), (self.dbias, dbias)):
+            self._defer_copy(dst, src)
         self._setup_pending = True
 
     def _human_setup(self) -> None:
@@ -401,20 +429,27 @@ class Renderer:
         s = _lib.stream_ptr()
         h = self.human
         n = self._dqs.shape[0]
-        # the backward-LBS chain (vertex transforms, posed vertices, their buckets)
-        # is independent of the ED chain: run it on the side stream
-        # (and the deformed nodes + their buckets, which only the canonicalisation reads,
-        # after the same event)
+        # the backward-LBS chain (FK of theta, vertex transforms, posed vertices, their
+        # buckets) is independent of the ED chain: run it on the side stream (and the
+        # pose bias and the deformed nodes, which only the canonicalisation and the
+        # field read, after the same event)
         main = torch.cuda.current_stream()
-        self._fork(main, self.side)
-        with torch.cuda.stream(self.side):
+        side = self._side_stream()
+        self._fork(main, side)
+        with torch.cuda.stream(side):
             ss = _lib.stream_ptr()
+            if getattr(self, "_pose_on_device", False):  # FK + pose bias of the frame's theta
+                parents, offsets = self._rig
+                _lib.call("cf_skinning_transforms", self._theta.data_ptr(), 1, parents.ctypes.data,
+                          offsets.ctypes.data, len(parents), self._A.data_ptr(), ss)
+                _lib.call("cf_pose_bias", h.nets.d1.data_ptr(), 32 + 3 * len(parents), 32, 128,
+                          self._theta.data_ptr(), 3 * len(parents), self.dbias.data_ptr(), ss)
             _lib.call("cf_deform_nodes", h.nodes.data_ptr(), self._dqs.data_ptr(), n, self._anchors.data_ptr(), ss)
             if n > 1024:  # small graphs are scanned from shared memory (no buckets needed)
                 self._anchor_buckets.build(self._anchors)
             h.lbs.set_pose(self._A)
             self._mark("lbs_setup")
-            self._lbs_done.record(self.side)
+            self._lbs_done.record(side)
         _lib.call("cf_occ_splat_cached", h.occ_cells.data_ptr(), h.occ_nbr.data_ptr(), h.occ_w.data_ptr(),
                   h.occ_count.data_ptr(), h.occ_cap, self.cfg.ed_k, self._dqs.data_ptr(), _lib.byref(h.canon_occ),
                   _lib.byref(self.live_occ), self.live_scratch.data_ptr(), self.live_bits.data_ptr(),
@@ -496,8 +531,13 @@ class Renderer:
     def _scratch(self, buf, desc) -> torch.Tensor:
         """Per-field scratch of cf_field_forward (allocated once)."""
         if getattr(buf, "scratch", None) is None:
+            # sized for the larger ("fp32") layout: a view may switch precision
+            # (set_precision) while graphs captured earlier keep pointing here
+            d = _lib.FieldDesc()
+            ctypes.memmove(ctypes.byref(d), ctypes.byref(desc), ctypes.sizeof(d))
+            d.precise = 1
             nb = ctypes.c_int64()
-            _lib.call("cf_field_scratch_bytes", _lib.byref(desc), int(buf.mo.capacity), ctypes.byref(nb))
+            _lib.call("cf_field_scratch_bytes", _lib.byref(d), int(buf.mo.capacity), ctypes.byref(nb))
             buf.scratch = torch.empty(max(int(nb.value), 16), dtype=torch.uint8, device=self.dirs.device)
         return buf.scratch
 
@@ -511,6 +551,20 @@ class Renderer:
             st = torch.cuda.current_stream()
             e.record(st)
             self.marks.append((st.cuda_stream, name, e))
+
+    def _side_stream(self) -> torch.cuda.Stream:
+        """The stream of the LBS chain and the object field: a second stream, or the
+        caller's stream in serial mode (cfg.serial)."""
+        return torch.cuda.current_stream() if self.cfg.serial else self.side
+
+    def set_precision(self, precision: str) -> None:
+        """Switch the field arithmetic ("fp32" / "fp16") of the following views."""
+        _precise(precision)
+        self.cfg.precision = precision
+        if getattr(self, "hdesc", None) is not None:
+            self.hdesc = self.human.desc(self.dbias, precision)
+        if getattr(self, "odesc", None) is not None:
+            self.odesc = self.obj.desc(precision)
 
     @staticmethod
     def _fork(src: torch.cuda.Stream, dst: torch.cuda.Stream) -> None:
@@ -580,7 +634,7 @@ class Renderer:
         self.image = self._images[slot]
         if self._copy_done[slot] is not None:  # this buffer's previous read-back must be done
             torch.cuda.current_stream().wait_event(self._copy_done[slot])
-        key = (setup, timed, slot)
+        key = (setup, timed, slot, self.cfg.serial, self.cfg.precision)
         if not self.cfg.cuda_graphs or (key not in self._graphs and not getattr(self, "_eager_done", False)):
             # eager launches (also the first view: lazily allocated state must exist before capture)
             if timed:
@@ -627,8 +681,9 @@ class Renderer:
         def object_field():
             # the object field is independent of the human one: side stream (running it
             # serially on the main stream measured 330 -> 355 us per frame)
-            self._fork(main, self.side)
-            with torch.cuda.stream(self.side):
+            side = self._side_stream()
+            self._fork(main, side)
+            with torch.cuda.stream(side):
                 so = _lib.stream_ptr()
                 _lib.call("cf_object_canon", _lib.byref(self.M), self.dirs.data_ptr(), _lib.byref(ob.mo),
                           ob.xu.data_ptr(), so)
@@ -639,7 +694,7 @@ class Renderer:
                 _lib.call("cf_composite", _lib.byref(self.M), _lib.byref(ob.mo), ob.out.data_ptr(),
                           self.cfg.t_term, ob.rgb.data_ptr(), ob.depth.data_ptr(), ob.opacity.data_ptr(), so)
                 self._mark("object_composite")
-                self._obj_done.record(self.side)
+                self._obj_done.record(side)
 
         if ob:
             object_field()

@@ -145,6 +145,7 @@ class DeformParams:
     def __init__(self, nets, device):
         self.nets = nets
         self.W = {k: torch.from_numpy(nets.layers[k].astype(np.float32)).to(device).contiguous() for k in DEFORM_LAYERS}
+        self.W["D1"] = nets.d1  # shared with the renderer: its per-frame pose bias reads the trained W1
         self.G = {k: torch.zeros_like(v) for k, v in self.W.items()}
         self.m = {k: torch.zeros_like(v) for k, v in self.W.items()}
         self.v = {k: torch.zeros_like(v) for k, v in self.W.items()}

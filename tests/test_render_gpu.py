@@ -317,3 +317,24 @@ def test_small_copy_entry_points():
     _lib.call("cf_store_to_host", dv.data_ptr(), back.data_ptr(), 4096 * 4, 8, _lib.stream_ptr())
     torch.cuda.synchronize()
     assert torch.equal(back, h)
+
+
+def test_load_pose_device_fk_matches_host_prior(setup):
+    """Renderer.load_pose (node dqs + theta; FK and the DeformNet pose bias on the
+    device) renders the frame the host-side prior (set_frame: host FK, host bias) does."""
+    import torch as _t
+    sc, cfg, hf, of, r, fid, img = setup
+    cam = sc.camera
+    a = img.clone()
+    r.load_pose(_t.from_numpy(sc.node_dqs(fid)).cuda(), _t.from_numpy(sc.theta(fid)).cuda())
+    R, t = sc.object_pose(fid)
+    r.set_object_pose(R, t)
+    b = r.render(cam.R, cam.t, cam.fx, cam.fy, cam.cx, cam.cy).clone()
+    _t.cuda.synchronize()
+    assert np.allclose(r._A.cpu().numpy(), sc.bone_transforms(fid), rtol=0, atol=1e-12)
+    assert np.allclose(r.dbias.cpu().numpy(), hf.nets.theta_bias(sc.theta(fid)), rtol=1e-5, atol=1e-6)
+    assert float((a - b).abs().max()) <= 1e-4
+    # back to the host prior: identical to the first render
+    r.set_frame(sc.node_dqs(fid), sc.theta(fid), sc.bone_transforms(fid), R, t)
+    c = r.render(cam.R, cam.t, cam.fx, cam.fy, cam.cx, cam.cy)
+    assert _t.equal(a, c)
