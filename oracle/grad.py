@@ -23,7 +23,7 @@ DEFORM = (8, 4, 17, 16, 256)
 PRIMES = (1, 2654435761, 805459861)
 
 
-def hash_encode_t(table, x, grid):
+def hash_encode_t(table, x, grid, cell32=False):
     """Trilinear multi-resolution hash features of x (N,3) in
     float64 torch, differentiable in table and x; corner choice as hash_corners."""
     L, F, log2T, nmin, nmax = grid
@@ -33,7 +33,14 @@ def hash_encode_t(table, x, grid):
     feats = []
     for N, dense, off in levels:
         pos = xc * float(N)
-        g = torch.minimum(torch.floor(pos.detach()), torch.tensor(float(N - 1), dtype=x.dtype))
+        if cell32:
+            # the cell chosen from the fp32 product, as the kernels and oracle/nrf.py do
+            # (DESIGN 4's fp32 position): an f64 product can land on the other side of a
+            # cell face, where the interpolant's normal derivative jumps (device checks)
+            p32 = (xc.detach().to(torch.float32) * torch.tensor(float(N), dtype=torch.float32)).to(x.dtype)
+        else:  # exact cell: the interpolant is continuous (finite-difference checks)
+            p32 = pos.detach()
+        g = torch.minimum(torch.floor(p32), torch.tensor(float(N - 1), dtype=x.dtype))
         fr = pos - g
         gi = g.to(torch.int64)
         f = 0
@@ -63,16 +70,32 @@ def _mlp(x, Ws, bias=None):
     return h
 
 
-def field_t(params, xu, dirs, inv_side, theta=None):
-    """(sigma, rgb) of samples xu (N,4: unit coords + flag) as float64 torch."""
+def field_t(params, xu, dirs, inv_side, theta=None, keep=None, xc_value=None, cell32=False):
+    """(sigma, rgb) of samples xu (N,4: unit coords + flag) as float64 torch. keep: an
+    optional dict that receives the intermediates fd, o, xc, fc (gradients retained);
+    xc_value: optional (N,3) canonical positions to evaluate the canonical grid at;
+    cell32: choose hash cells from the fp32 product as the device does."""
     x = torch.as_tensor(xu[:, :3], dtype=torch.float64)
     if "dtable" in params:
-        fd = hash_encode_t(params["dtable"], x, DEFORM)
+        fd = hash_encode_t(params["dtable"], x, DEFORM, cell32)
         th = torch.as_tensor(theta, dtype=torch.float64)
         D1 = params["D1"]
         o = _mlp(fd, [D1[:, :32], params["D2"], params["D3"], params["D4"], params["D5"]], D1[:, 32:] @ th)
         x = x + 0.05 * torch.tanh(o[:, :3]) * inv_side
-    fc = hash_encode_t(params["ctable"], x, CANON)
+        if xc_value is not None:
+            # evaluate the canonical grid at given positions (the device forward's xc),
+            # gradients still flowing through the deformation: the trilinear interpolant's
+            # normal derivative jumps across cell faces, so the backward is compared where
+            # the forward put the sample (xc itself is checked by the forward parity tests)
+            x = torch.as_tensor(np.asarray(xc_value), dtype=torch.float64) + (x - x.detach())
+        if keep is not None:
+            keep.update(fd=fd, o=o)
+    fc = hash_encode_t(params["ctable"], x, CANON, cell32)
+    if keep is not None:
+        keep.update(xc=x, fc=fc)
+        for v in keep.values():
+            if v.requires_grad:
+                v.retain_grad()
     g = _mlp(fc, [params["G1"], params["G2"]])
     sigma = torch.exp(g[:, 0])
     sh = torch.as_tensor(sh16(np.asarray(dirs)), dtype=torch.float64)
@@ -87,7 +110,8 @@ def loss_t(params, batch, lam=0.1, color_only=False):
     depth-valid ray counts, as cf_loss_composite_bwd). batch: dict with xu (N,4), dirs
     (N,3), ray (N,), t (N,) sorted per ray, delta (N,), gt_rgb (R,3), gt_depth (R,),
     mask (R,), inv_side, theta."""
-    sigma, rgb = field_t(params, batch["xu"], batch["dirs"], batch["inv_side"], batch.get("theta"))
+    sigma, rgb = field_t(params, batch["xu"], batch["dirs"], batch["inv_side"], batch.get("theta"),
+                         batch.get("keep"), batch.get("xc_value"), batch.get("cell32", False))
     ray = torch.as_tensor(batch["ray"])
     t = torch.as_tensor(batch["t"], dtype=torch.float64)
     delta = torch.as_tensor(batch["delta"], dtype=torch.float64)

@@ -647,12 +647,17 @@ __device__ __forceinline__ void split_layer(SplitSlot& S, const uint8_t* w_hi, c
   tc::fence_after();
 }
 
-// 32 D columns from col -> (+bias) ReLU -> hi / lo fp16x2 -> A columns col/2
-__device__ __forceinline__ void split_relu32(const SplitSlot& S, int col, const float* bias) {
+// 32 D columns from col -> (+bias) ReLU -> hi / lo fp16x2 -> A columns col/2.
+// Training (save != nullptr): the hi halves (= the fp16 rounding of the activation,
+// what the fp16 backward consumes) also go to the feature-major save block; returns
+// the ReLU derivative bits of the 32 columns.
+__device__ __forceinline__ uint32_t split_relu32(const SplitSlot& S, int col, const float* bias,
+                                                 __half* save = nullptr, int64_t ld = 0) {
   uint32_t r[32];
   tc::tmem_ld32_nowait(S.d + (uint32_t)col, r);
   tc::tmem_wait_ld();
   uint32_t h[16], l[16];
+  uint32_t bits = 0;
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
     float x0 = __uint_as_float(r[2 * i]), x1 = __uint_as_float(r[2 * i + 1]);
@@ -660,20 +665,27 @@ __device__ __forceinline__ void split_relu32(const SplitSlot& S, int col, const 
       x0 += bias[col + 2 * i];
       x1 += bias[col + 2 * i + 1];
     }
+    bits |= (x0 > 0.0f ? 1u : 0u) << (2 * i) | (x1 > 0.0f ? 1u : 0u) << (2 * i + 1);
     tc::split_f16x2(fmaxf(x0, 0.0f), fmaxf(x1, 0.0f), h[i], l[i]);
   }
   tc::tmem_st16(S.ahi + (uint32_t)(col / 2), h);
   tc::tmem_st16(S.alo + (uint32_t)(col / 2), l);
+  if (save) store_cols_f16(reinterpret_cast<uint16_t*>(save), ld, col, h);
+  return bits;
 }
 
 // n4 float4 of fp32 values -> hi / lo halves at A column c0 (2 values per column)
 template <int N4>
-__device__ __forceinline__ void split_store(const SplitSlot& S, const float4* v, int c0) {
+__device__ __forceinline__ void split_store(const SplitSlot& S, const float4* v, int c0, uint32_t* hi_out = nullptr) {
   uint32_t h[2 * N4], l[2 * N4];
 #pragma unroll
   for (int q = 0; q < N4; ++q) {
     tc::split_f16x2(v[q].x, v[q].y, h[2 * q], l[2 * q]);
     tc::split_f16x2(v[q].z, v[q].w, h[2 * q + 1], l[2 * q + 1]);
+  }
+  if (hi_out) {
+#pragma unroll
+    for (int q = 0; q < 2 * N4; ++q) hi_out[q] = h[q];
   }
   if constexpr (N4 == 4) {
     tc::tmem_st8(S.ahi + (uint32_t)c0, h);
@@ -685,11 +697,18 @@ __device__ __forceinline__ void split_store(const SplitSlot& S, const float4* v,
   }
 }
 
+// kSave: the training forward — xc at 32-bit semantics (the canonical hash backward's
+// spatial gradient is evaluated where the 32-bit field puts the sample), plus the
+// fp16 saves the fp16 backward consumes: h1..h4 (hi halves, feature-major), the
+// ReLU bits, o, and the deformation features' hi halves (dfeat16, for dW of layer 1)
+template <bool kSave>
 __global__ void __launch_bounds__(kPrecDeformSlots* kDeformSlotThreads, 1)
     deform_mlp_prec_kernel(const uint8_t* __restrict__ wblob, const uint8_t* __restrict__ wblob_lo,
                            const float* __restrict__ bias1, float delta_scale, float inv_side,
                            const float4* __restrict__ xu, const float4* __restrict__ dfeat,
-                           const int* __restrict__ count, int64_t capacity, float4* __restrict__ xc) {
+                           const int* __restrict__ count, int64_t capacity, float4* __restrict__ xc,
+                           __half* __restrict__ save_h, float4* __restrict__ save_o,
+                           uint32_t* __restrict__ save_mask, uint4* __restrict__ dfeat16) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t mbar[kPrecDeformSlots];
   __shared__ uint32_t tmem_base;
@@ -737,25 +756,34 @@ __global__ void __launch_bounds__(kPrecDeformSlots* kDeformSlotThreads, 1)
       float4 f[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) f[q] = live ? dfeat[s * 8 + 4 * S.half + q] : make_float4(0.f, 0.f, 0.f, 0.f);
-      split_store<4>(S, f, 8 * S.half);  // this half's 16 features
+      uint32_t hi[8];
+      split_store<4>(S, f, 8 * S.half, kSave ? hi : nullptr);  // this half's 16 features
+      if (kSave && live) {
+        dfeat16[s * 4 + 2 * S.half] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+        dfeat16[s * 4 + 2 * S.half + 1] = make_uint4(hi[4], hi[5], hi[6], hi[7]);
+      }
     }
     const float4 xs = (live && S.half == 0) ? xu[s] : make_float4(0.f, 0.f, 0.f, 0.f);
-    split_layer(S, smem + o1, lo + o1, 32, 128);
-    split_relu32(S, 64 * S.half, s_bias);
-    split_relu32(S, 64 * S.half + 32, s_bias);
-    split_layer(S, smem + o2, lo + o2, 128, 128);
-    split_relu32(S, 64 * S.half, nullptr);
-    split_relu32(S, 64 * S.half + 32, nullptr);
-    split_layer(S, smem + o3, lo + o3, 128, 128);
-    split_relu32(S, 64 * S.half, nullptr);
-    split_relu32(S, 64 * S.half + 32, nullptr);
-    split_layer(S, smem + o4, lo + o4, 128, 128);
-    split_relu32(S, 64 * S.half, nullptr);
-    split_relu32(S, 64 * S.half + 32, nullptr);
+    // training saves: h feature-major (512, capacity), ReLU bits [layer][half][2] per sample
+    __half* sv = (kSave && live) ? save_h + s : nullptr;
+    const int64_t L = 128 * capacity;
+    uint32_t* mk = (kSave && live) ? save_mask + s * 16 + 2 * S.half : nullptr;
+    const uint8_t* wo[4] = {smem + o1, smem + o2, smem + o3, smem + o4};
+#pragma unroll 1
+    for (int l = 0; l < 4; ++l) {
+      const int lo_off = (int)(wo[l] - smem);
+      split_layer(S, wo[l], lo + lo_off, l == 0 ? 32 : 128, 128);
+      const uint32_t b0 = split_relu32(S, 64 * S.half, l == 0 ? s_bias : nullptr, sv ? sv + l * L : nullptr,
+                                       capacity);
+      const uint32_t b1 = split_relu32(S, 64 * S.half + 32, l == 0 ? s_bias : nullptr, sv ? sv + l * L : nullptr,
+                                       capacity);
+      if (mk) *reinterpret_cast<uint2*>(mk + 4 * l) = make_uint2(b0, b1);
+    }
     split_layer(S, smem + o5, lo + o5, 128, 16);
     if (S.half == 0) {  // warp-uniform: tcgen05.ld is warp-collective
       float v[16];
       tc::tmem_ld16(S.d, v);
+      if (kSave && live) save_o[s] = make_float4(v[0], v[1], v[2], 0.0f);
       if (live) {
         float4 p = xs;
         if (p.w > 0.0f) {
@@ -781,7 +809,8 @@ __global__ void __launch_bounds__(kColorPrecSlots* kSlotThreads, 1)
     color_mlp_prec_kernel(const uint8_t* __restrict__ wblob, const uint8_t* __restrict__ wblob_lo,
                           const float4* __restrict__ xu, const float4* __restrict__ cfeat,
                           const uint32_t* __restrict__ records, const double* __restrict__ dirs,
-                          const int* __restrict__ count, int64_t capacity, float4* __restrict__ out) {
+                          const int* __restrict__ count, int64_t capacity, float4* __restrict__ out,
+                          uint4* __restrict__ cfeat16) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t mbar[kColorPrecSlots];
   __shared__ uint32_t tmem_base;
@@ -826,7 +855,12 @@ __global__ void __launch_bounds__(kColorPrecSlots* kSlotThreads, 1)
       float4 f[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) f[q] = live ? cfeat[s * 8 + q] : make_float4(0.f, 0.f, 0.f, 0.f);
-      split_store<8>(S, f, 0);
+      uint32_t hi[16];
+      split_store<8>(S, f, 0, cfeat16 ? hi : nullptr);
+      if (cfeat16 && live) {  // training: the features' fp16 halves for the fp16 backward
+#pragma unroll
+        for (int q = 0; q < 4; ++q) cfeat16[s * 4 + q] = make_uint4(hi[4 * q], hi[4 * q + 1], hi[4 * q + 2], hi[4 * q + 3]);
+      }
     }
     const bool valid = live && xu[s].w > 0.0f;
     double ddx = 0.0, ddy = 0.0, ddz = 1.0;
@@ -1392,8 +1426,47 @@ unsigned persistent_grid(int64_t capacity, int slots) {
 int field_stage_precise(const cf_field_desc* FD, const cf_march_out* S, const double* dirs, const float* xu_f,
                         float* out_f, void* scratch, int stage, cudaStream_t st) {
   auto run = [&](int s) { return stage < 0 || stage == s; };
-  if (FD->save_h) return cf::fail(CF_E_BAD_ARG, "cf_field_forward: training saves need the fp16 mode");
   const int64_t cap = S->capacity;
+  if (FD->save_h) {
+    // training forward at 32-bit semantics (fp32 tables and features, split-fp16 MMAs):
+    // xc, sigma and rgb are the 32-bit field's (the L1 depth term's sign and the
+    // spatial gradient dL/dxc are evaluated where the SPEC's field is), plus the fp16
+    // saves the fp16 backward consumes. Scratch: cfeat16 (64 B) | dfeat16 (64 B) |
+    // xc (16 B) | dfeat32 (128 B) | cfeat32 (128 B) per sample (the fp16 layout first).
+    if (!FD->has_deform || !FD->save_o || !FD->save_mask)
+      return cf::fail(CF_E_BAD_ARG, "cf_field_forward: training saves need the human field, save_o and save_mask");
+    uint4* cfeat = reinterpret_cast<uint4*>(scratch);
+    uint4* dfeat16 = cfeat + cap * 4;
+    float4* xc = reinterpret_cast<float4*>(dfeat16 + cap * 4);
+    float4* dfeat32 = xc + cap;
+    const unsigned hgrid = cf::grid_for(cap, 128, 16);
+    const float4* xu = reinterpret_cast<const float4*>(xu_f);
+    if (run(0))
+      cf::launch_pdl(hash_f16_kernel<4, 8, 2, 1, float, true>, hgrid, 128, 0, st, FD->dgrid,
+                     reinterpret_cast<const float*>(FD->dtable), xu, S->counters, cap, reinterpret_cast<uint4*>(dfeat32));
+    if (run(1)) {
+      const int smem = 2 * kDeformW;
+      CF_CHECK_CUDA(cudaFuncSetAttribute(deform_mlp_prec_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      cf::launch_pdl(deform_mlp_prec_kernel<true>, persistent_grid(cap, kPrecDeformSlots),
+                     kPrecDeformSlots * kDeformSlotThreads, smem, st, FD->wblob, FD->wblob_lo, FD->dbias,
+                     FD->delta_scale, FD->inv_side, xu, static_cast<const float4*>(dfeat32), S->counters, cap, xc,
+                     reinterpret_cast<__half*>(FD->save_h), reinterpret_cast<float4*>(FD->save_o), FD->save_mask,
+                     dfeat16);
+    }
+    float4* cfeat32 = dfeat32 + cap * 8;
+    if (run(2))
+      cf::launch_pdl(hash_f16_kernel<2, 16, 4, 1, float, true>, hgrid, 128, 0, st, FD->cgrid,
+                     reinterpret_cast<const float*>(FD->ctable), static_cast<const float4*>(xc), S->counters, cap,
+                     reinterpret_cast<uint4*>(cfeat32));
+    if (run(3)) {
+      const int csmem = 2 * kColorW;
+      CF_CHECK_CUDA(cudaFuncSetAttribute(color_mlp_prec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, csmem));
+      cf::launch_pdl(color_mlp_prec_kernel, persistent_grid(cap, kColorPrecSlots), kColorPrecSlots * kSlotThreads,
+                     csmem, st, FD->wblob + kDeformW, FD->wblob_lo + kDeformW, xu, static_cast<const float4*>(cfeat32),
+                     S->records, dirs, S->counters, cap, reinterpret_cast<float4*>(out_f), cfeat);
+    }
+    return cf::check_launch("cf_field_forward (training)");
+  }
   const float4* xu = reinterpret_cast<const float4*>(xu_f);
   float4* out = reinterpret_cast<float4*>(out_f);
   float4* cfeat = reinterpret_cast<float4*>(scratch);  // (cap, 32) fp32
@@ -1407,10 +1480,12 @@ int field_stage_precise(const cf_field_desc* FD, const cf_march_out* S, const do
                      reinterpret_cast<const float*>(FD->dtable), xu, S->counters, cap, reinterpret_cast<uint4*>(dfeat));
     if (run(1)) {
       const int smem = 2 * kDeformW;
-      CF_CHECK_CUDA(cudaFuncSetAttribute(deform_mlp_prec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      cf::launch_pdl(deform_mlp_prec_kernel, persistent_grid(cap, kPrecDeformSlots),
+      CF_CHECK_CUDA(cudaFuncSetAttribute(deform_mlp_prec_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      cf::launch_pdl(deform_mlp_prec_kernel<false>, persistent_grid(cap, kPrecDeformSlots),
                      kPrecDeformSlots * kDeformSlotThreads, smem, st, FD->wblob, FD->wblob_lo, FD->dbias,
-                     FD->delta_scale, FD->inv_side, xu, static_cast<const float4*>(dfeat), S->counters, cap, xc);
+                     FD->delta_scale, FD->inv_side, xu, static_cast<const float4*>(dfeat), S->counters, cap, xc,
+                     static_cast<__half*>(nullptr), static_cast<float4*>(nullptr), static_cast<uint32_t*>(nullptr),
+                     static_cast<uint4*>(nullptr));
     }
     xcan = xc;
   }
@@ -1429,7 +1504,7 @@ int field_stage_precise(const cf_field_desc* FD, const cf_march_out* S, const do
     CF_CHECK_CUDA(cudaFuncSetAttribute(color_mlp_prec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, csmem));
     cf::launch_pdl(color_mlp_prec_kernel, persistent_grid(cap, kColorPrecSlots), kColorPrecSlots * kSlotThreads, csmem,
                    st, FD->wblob + off, FD->wblob_lo + off, xu, static_cast<const float4*>(cfeat), S->records, dirs,
-                   S->counters, cap, out);
+                   S->counters, cap, out, static_cast<uint4*>(nullptr));
   }
   return cf::check_launch("cf_field_forward (precise)");
 }
@@ -1443,6 +1518,7 @@ int cf_field_scratch_bytes(const cf_field_desc* FD, int64_t capacity, int64_t* b
   // cfeat (64 B fp16 / 128 B fp32) [+ dfeat (same) + xc (16 B)] per sample
   const int64_t feat = FD->precise ? 128 : 64;
   *bytes = capacity * (feat + (FD->has_deform ? feat + 16 : 0));
+  if (FD->has_deform && FD->save_h) *bytes = capacity * (64 + 64 + 16 + 128 + 128);  // training layout
   return CF_OK;
 }
 

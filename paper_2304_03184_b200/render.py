@@ -456,6 +456,27 @@ class Renderer:
                   self.live_bbox.data_ptr(), s)
         self._mark("ed_setup")
 
+    def _save_frame_state(self):
+        """Snapshot of the per-frame state another user of the warp buffers (the
+        trainer's key frames) overwrites: prior buffers (device copies), the pose flag
+        and whether a setup was pending."""
+        if self.human is None or getattr(self, "_dqs", None) is None:
+            return None
+        bufs = [self._dqs, self._A, self.dbias] + ([self._theta] if getattr(self, "_theta", None) is not None else [])
+        self._flush_copies()  # a prior staged but not yet issued belongs to the snapshot
+        return ([(b, b.clone()) for b in bufs], getattr(self, "_pose_on_device", False))
+
+    def _restore_frame_state(self, saved) -> None:
+        """Restore a _save_frame_state snapshot; the frame's setup (deformed nodes,
+        LBS, live occupancy) re-runs with the next view."""
+        if saved is None:
+            return
+        pairs, pose_on_device = saved
+        for dst, src in pairs:
+            dst.copy_(src, non_blocking=True)
+        self._pose_on_device = pose_on_device
+        self._setup_pending = True
+
     def set_object_pose(self, obj_R, obj_t) -> None:
         """Object-to-world pose of the frame (frame block, uploaded with the next view)."""
         self._frame_host[3:12] = np.asarray(obj_R, dtype=np.float64).reshape(9)

@@ -58,6 +58,7 @@ class FrameBatch:
     mask_h: torch.Tensor       # (R,) u8 human mask
     mask_o: torch.Tensor       # (R,) u8 object mask
     theta: torch.Tensor | None = None  # (72,) f32 pose; DeformNet training recomputes dbias from it
+    origin: np.ndarray | None = None   # (3,) f64 camera centre of the key frame (the rays' origin)
 
 
 class KeyFrame:
@@ -74,6 +75,7 @@ class KeyFrame:
         self.cam.fx, self.cam.fy = float(camera.fx), float(camera.fy)
         self.cam.cx, self.cam.cy = float(camera.cx), float(camera.cy)
         self.cam.width, self.cam.height = int(camera.width), int(camera.height)
+        self.origin = np.asarray(camera.t, dtype=np.float64).reshape(3).copy()
         self.rgb = rgb.contiguous()
         self.depth = depth.contiguous()
         self.mask_h = mask_h.contiguous()
@@ -94,7 +96,8 @@ class KeyFrame:
                   self.mask_o.data_ptr(), None, dirs.data_ptr(), rgb.data_ptr(), depth.data_ptr(), mh.data_ptr(),
                   mo.data_ptr(), _lib.stream_ptr())
         return FrameBatch(dqs=self.dqs, bone_A=self.bone_A, dbias=self.dbias, obj_R=self.obj_R, obj_t=self.obj_t,
-                          dirs=dirs, gt_rgb=rgb, gt_depth=depth, mask_h=mh, mask_o=mo, theta=self.theta)
+                          dirs=dirs, gt_rgb=rgb, gt_depth=depth, mask_h=mh, mask_o=mo, theta=self.theta,
+                          origin=self.origin)
 
 
 class ColorParams:
@@ -262,8 +265,9 @@ class Trainer:
         if st["name"] == "human":
             _lib.call("cf_human_canon", _lib.byref(M), self.dirs.data_ptr(), _lib.byref(buf.mo), _lib.byref(r.hw),
                       r._anchor_buckets.handle, field.lbs.buckets.handle, buf.xu.data_ptr(), s)
-            # the training forward runs the fp16 mode (its backward consumes the fp16 saves)
-            desc = field.desc(r.dbias, "fp16")
+            # the training forward: DeformNet at 32-bit semantics with the fp16 saves the
+            # fp16 backward consumes (cf_field_forward with save_h in the "fp32" mode)
+            desc = field.desc(r.dbias, "fp32" if dp is not None else "fp16")
             if dp is not None:
                 # this frame's pose bias from the current W1, forward saves on
                 if b.theta is None:
@@ -345,20 +349,27 @@ class Trainer:
             GD["D1"][:, 32:] += torch.outer(csum, b.theta.to(DP.device, torch.float32))
 
     def set_frame(self, b: FrameBatch):
+        """The key frame's warp state (prior -> deformed nodes, LBS, live occupancy in the
+        renderer's per-frame buffers) and its camera centre / object pose (by value in
+        the trainer's own march descriptor: the renderer's frame block, i.e. its novel
+        view, is never read)."""
+        if b.origin is None:
+            raise ValueError("FrameBatch.origin (the key frame's camera centre) is required")
         r = self.r
-        r.load_prior(b.dqs, b.bone_A, b.dbias)
-        r.set_object_pose(b.obj_R, b.obj_t)
-        r.prepare_frame()
         n = b.dirs.shape[0]
         if n > self.max_rays:
             raise ValueError("frame batch larger than max_rays")
+        r.load_prior(b.dqs, b.bone_A, b.dbias)
+        r.prepare_frame()
         self.dirs[:n].copy_(b.dirs)
-        fr = r._frame_host  # origin[3], obj_R[9], obj_t[3] of the renderer's frame block
+        o = np.asarray(b.origin, dtype=np.float64).reshape(3)
+        oR = np.asarray(b.obj_R, dtype=np.float64).reshape(9)
+        ot = np.asarray(b.obj_t, dtype=np.float64).reshape(3)
         for a in range(3):
-            self.M.origin[a] = fr[a]
-            self.M.obj_t[a] = fr[12 + a]
+            self.M.origin[a] = o[a]
+            self.M.obj_t[a] = ot[a]
         for a in range(9):
-            self.M.obj_R[a] = fr[3 + a]
+            self.M.obj_R[a] = oR[a]
         torch.cuda.current_stream().wait_event(r._lbs_done)
 
     def step(self, batches, allreduce=None):
@@ -374,10 +385,15 @@ class Trainer:
         for st in self.fields:  # one loss scale per field and step (every frame's grads add up)
             mk = [b.mask_h if st["name"] == "human" else b.mask_o for b in batches]
             st["gscale"] = loss_scale(min(int(m.sum()) for m in mk))
-        for b in batches:
-            self.set_frame(b)
-            for st in self.fields:
-                self._frame(b, st, st["stats"])
+        saved = self.r._save_frame_state()
+        try:
+            for b in batches:
+                self.set_frame(b)
+                for st in self.fields:
+                    self._frame(b, st, st["stats"])
+        finally:
+            # the renderer's own frame (prior, pending setup) is back for its next view
+            self.r._restore_frame_state(saved)
         if allreduce is not None:
             bufs = [st["tgrad"] for st in self.fields] + [g for st in self.fields for g in st["params"].G.values()]
             for st in self.fields:

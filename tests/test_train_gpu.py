@@ -32,7 +32,7 @@ def make_batch(sc, hf, fid, n_rays, rng, dev):
                       theta=T(sc.theta(fid), torch.float32),
                       dirs=T(d[pick], torch.float64), gt_rgb=T(rgb[pick], torch.float32),
                       gt_depth=T(depth, torch.float32), mask_h=T(hum[pick], torch.uint8),
-                      mask_o=T(obj[pick], torch.uint8))
+                      mask_o=T(obj[pick], torch.uint8), origin=np.asarray(sc.camera.t, dtype=np.float64))
 
 
 @pytest.fixture(scope="module")
@@ -245,10 +245,11 @@ def test_canonical_hash_spatial_gradient(setup):
 
 
 def test_deform_backward_vs_autograd(setup):
-    """DeformNet weight and feature gradients (tcgen05 backward + fp16 GEMMs) vs
-    autograd of the same fp16-operand graph (activations and the backward's
-    dL/dpre operands rounded to fp16 as the kernels do), driven by the kernel's
-    dL/dxc."""
+    """DeformNet weight and feature gradients (tcgen05 backward + dW GEMMs) vs an fp32
+    restatement of the training graph: the forward at 32-bit semantics (fp32 features
+    and weights; the kernel's split-fp16 MMAs), the backward on fp16 operands as the
+    kernels take them — saved activations, dL/do and dL/dpre rounded to fp16, the
+    transposed weights in fp16 — with fp32 accumulation, driven by the kernel's dL/dxc."""
     sc, hf, of, r, tr, batches = setup
     b = batches[2]
     st = tr.fields[0]
@@ -257,43 +258,45 @@ def test_deform_backward_vs_autograd(setup):
     buf, D, db = st["buf"], st["deform"], st["dbufs"]
     cap = buf.mo.capacity
     scratch = r._scratch(buf, r.hdesc)
-    xd = scratch[cap * 64: cap * 64 + n * 64].view(torch.float16).view(n, 32).float().cpu()
+    # training scratch: cfeat16 | dfeat16 | xc | dfeat32 (cf_field_forward, save_h)
+    x0 = scratch[cap * 144: cap * 144 + n * 128].view(torch.float32).view(n, 32).cpu()
+    xd16 = scratch[cap * 64: cap * 64 + n * 64].view(torch.float16).view(n, 32).float().cpu()
+    h = lambda x: x.half().float()  # noqa: E731  fp16 operand rounding of the kernels
+    assert torch.equal(xd16, h(x0))
     valid = torch.from_numpy(buf.xu[:n].cpu().numpy()[:, 3] > 0).float()
     dxc = db.dxc[:n].cpu()[:, :3]
     theta = b.theta.cpu().float()
-    W = {k: D.W[k].detach().cpu().clone().requires_grad_(True) for k in D.W}
-    h = lambda x: x.half().float()  # noqa: E731  fp16 operand rounding of the kernel
-
-    class GradF16(torch.autograd.Function):  # the backward MMAs take dL/dpre as fp16 operands
-        @staticmethod
-        def forward(ctx, x):
-            return x.view_as(x)
-
-        @staticmethod
-        def backward(ctx, g):
-            return g.half().float()
-
-    q = GradF16.apply
-    Wh = {k: h(W[k]) for k in W}
+    W = {k: D.W[k].detach().cpu().clone() for k in D.W}
     bias = W["D1"][:, 32:] @ theta  # fp32 master weights (Trainer: DeformParams.bias)
-    x0 = xd.clone().requires_grad_(True)
-    a1 = torch.relu(q(h(x0) @ Wh["D1"][:, :32].t() + bias))
-    a2 = torch.relu(q(h(a1) @ Wh["D2"].t()))
-    a3 = torch.relu(q(h(a2) @ Wh["D3"].t()))
-    a4 = torch.relu(q(h(a3) @ Wh["D4"].t()))
-    o = q(h(a4) @ Wh["D5"].t())
-    dv = 0.05 * torch.tanh(o) * hf.inv_side
-    L = (valid[:, None] * dxc * dv).sum()
-    L.backward()
-    # tolerance: fp32 accumulation order (TMEM / cuBLAS vs CPU) and the resulting
-    # one-ulp fp16 flips of saved activations; measured max 1e-3 of the max entry
+    p1 = x0 @ W["D1"][:, :32].t() + bias
+    a1 = torch.relu(p1)
+    p2 = a1 @ W["D2"].t()
+    a2 = torch.relu(p2)
+    p3 = a2 @ W["D3"].t()
+    a3 = torch.relu(p3)
+    p4 = a3 @ W["D4"].t()
+    a4 = torch.relu(p4)
+    o = a4 @ W["D5"].t()
+    go = h(valid[:, None] * dxc * 0.05 * hf.inv_side * (1.0 - torch.tanh(o) ** 2))
+    ref = {"D5": go.t() @ h(a4)}
+    dp4 = h((go @ h(W["D5"])) * (p4 > 0))
+    ref["D4"] = dp4.t() @ h(a3)
+    dp3 = h((dp4 @ h(W["D4"])) * (p3 > 0))
+    ref["D3"] = dp3.t() @ h(a2)
+    dp2 = h((dp3 @ h(W["D3"])) * (p2 > 0))
+    ref["D2"] = dp2.t() @ h(a1)
+    dp1 = h((dp2 @ h(W["D2"])) * (p1 > 0))
+    ref["D1"] = torch.cat([dp1.t() @ h(x0), torch.outer(dp1.sum(0), theta)], 1)
+    dx0 = dp1 @ h(W["D1"][:, :32])
+    # tolerance: fp32 accumulation order (TMEM vs CPU) and the resulting one-ulp fp16
+    # flips of saved activations / dL/dpre; measured max 1e-3 of the max entry
     for k in ("D1", "D2", "D3", "D4", "D5"):
-        ref = W[k].grad.numpy()
+        rk = ref[k].numpy()
         got = D.G[k].cpu().numpy()
-        scale = np.abs(ref).max()
+        scale = np.abs(rk).max()
         assert scale > 0, k
-        assert np.abs(got - ref).max() <= 1e-2 * scale, (k, np.abs(got - ref).max(), scale)
-    ref = x0.grad.numpy()
+        assert np.abs(got - rk).max() <= 1e-2 * scale, (k, np.abs(got - rk).max(), scale)
+    ref = dx0.numpy()
     got = db.d_dfeat[:n].cpu().numpy()
     scale = np.abs(ref).max()
     assert scale > 0
@@ -407,19 +410,23 @@ def test_gemm_kmajor_vs_torch(n_cols, K):
 
 
 def test_device_gradients_vs_f64_oracle(setup):
-    """Every trained parameter's gradient from the device training step (fp16-mode
-    forward + tcgen05 / hash backward kernels) against the 64-bit analytic gradient
-    of the same loss on the same samples (oracle/grad.py, itself pinned to central
-    finite differences within 1e-3 by tests/test_oracle_grad.py). Tolerance: the
-    fp16 operand rounding of the training kernels, GRAD_TOL of the largest entry
-    per parameter. Measured (B200): E_g / E_c 1.1-2.7e-3, canonical table 6.5e-3;
-    DeformNet 1.8-6.4e-2 and deformation table 3.9e-2 — the fp16 forward's xc error
-    (~2e-5, test_precision_gpu) moves samples by ~4 % of a 2048-level cell, which the
-    spatial gradient dL/dxc feeding the DeformNet backward is sensitive to. Without
-    the loss scaling (train.loss_scale) the deformation table was off by 37 %."""
+    """Every trained parameter's gradient from the device training step against the
+    64-bit analytic gradient of the same loss on the same samples (oracle/grad.py,
+    itself pinned to central finite differences within 1e-3 by
+    tests/test_oracle_grad.py). The training forward runs at 32-bit semantics
+    (split-fp16 MMAs, fp32 tables / features: xc, sigma, rgb are the SPEC field's), the
+    backward on fp16 tensor-core operands with fp32 accumulation. Tolerance: GRAD_TOL
+    of the largest entry per parameter. Measured (B200): E_g / E_c 2e-4-1.7e-3,
+    canonical table 2.6e-3, DeformNet 0.7-1.5e-2, deformation table 3.6e-2 — the
+    DeformNet chain starts from the spatial gradient dL/dxc, a sum of 16 levels x 8
+    corners scaled by the level resolution, where the backward's fp16 rounding of
+    dL/dfeat (2-3 % worst-sample error, printed below) is amplified. With the fp16
+    forward (before r2) the L1 depth term's sign flipped on rays whose depth error
+    straddled the target and the DeformNet grads were off by 5-12 %; without the loss
+    scaling (train.loss_scale) the deformation table was off by 37 %."""
     from oracle import grad as og
-    GRAD_TOL = {"ctable": 1e-2, "dtable": 1e-1, "G1": 1e-2, "G2": 1e-2, "C1": 1e-2, "C2": 1e-2, "C3": 1e-2,
-                "D1": 1e-1, "D2": 1e-1, "D3": 1e-1, "D4": 1e-1, "D5": 1e-1}
+    GRAD_TOL = {"ctable": 1e-2, "dtable": 6e-2, "G1": 1e-2, "G2": 1e-2, "C1": 1e-2, "C2": 1e-2, "C3": 1e-2,
+                "D1": 3e-2, "D2": 3e-2, "D3": 3e-2, "D4": 3e-2, "D5": 3e-2}
     sc, hf, of, r, tr, batches = setup
     b = batches[0]
     st = tr.fields[0]
@@ -442,7 +449,27 @@ def test_device_gradients_vs_f64_oracle(setup):
     values = {"ctable": hf.cgrid.table.cpu().numpy(), "dtable": hf.dgrid.table.cpu().numpy()}
     values.update({k: w.cpu().numpy() for k, w in P.W.items()})
     values.update({k: w.cpu().numpy() for k, w in D.W.items()})
+    keep = {}
+    batch["keep"] = keep
+    cap = buf.mo.capacity
+    xc_dev = r._scratch(buf, r.hdesc)[cap * 128: cap * 128 + n * 16].view(torch.float32).view(n, 4).cpu().numpy()
+    batch["xc_value"] = xc_dev[order, :3].astype(np.float64)  # the canonical grid at the forward's positions
+    batch["cell32"] = True  # and its cells chosen as the kernels choose them
     _, ref = og.gradients(values, batch)
+    # stage-wise diagnostics (device vs f64, max err / max |ref|, in the device's sample order)
+    inv = np.argsort(order)
+    gs = st["gscale"]
+    diag = {}
+    for name, dev_val in (("dL/dfc", st["bwd"].dfeat[:n].cpu().numpy()), ("dL/dxc", st["dbufs"].dxc[:n].cpu().numpy()[:, :3]),
+                          ("dL/dfd", st["dbufs"].d_dfeat[:n].cpu().numpy())):
+        key = {"dL/dfc": "fc", "dL/dxc": "xc", "dL/dfd": "fd"}[name]
+        rv = keep[key].grad.numpy()[inv]
+        dv = dev_val / gs
+        diag[name] = float(np.abs(dv - rv).max() / np.abs(rv).max())
+        err = np.abs(dv - rv).max(1)
+        worst_s = np.argsort(err)[-3:]
+        diag[name + " worst"] = [(int(q), float(err[q]), float(np.abs(rv[q]).max())) for q in worst_s]
+    print("stage diagnostics:", diag)
     got = {"ctable": st["tgrad"].cpu().numpy(), "dtable": st["dtgrad"].cpu().numpy()}
     got.update({k: g.cpu().numpy() for k, g in P.G.items()})
     got.update({k: g.cpu().numpy() for k, g in D.G.items()})
@@ -454,3 +481,41 @@ def test_device_gradients_vs_f64_oracle(setup):
     print("device vs f64 gradients, max err / max |grad|:", worst)
     for k, tol in GRAD_TOL.items():
         assert worst[k] <= tol, (k, worst)
+
+
+def test_render_between_steps_does_not_leak(setup):
+    """A novel-view render between training steps must not change what the trainer
+    computes (rays start at the key frame's camera, not the last rendered view), and a
+    training step must not change what the renderer shows afterwards (its frame's prior
+    and object pose are restored) — ADVICE r1 (train.py set_frame)."""
+    sc, hf, of, r, tr, batches = setup
+    b = batches[1]
+    st = tr.fields[0]
+    seed = tr.seed
+    s1 = run_frame(tr, b, st).cpu().numpy()
+    g1 = st["tgrad"].clone()
+    cam = sc.camera
+    # a different view (camera moved 0.7 m sideways, same orientation)
+    t2 = np.asarray(cam.t, dtype=np.float64) + np.array([0.7, 0.0, 0.1])
+    r.set_frame(sc.node_dqs(5), sc.theta(5), sc.bone_transforms(5), *sc.object_pose(5))
+    img_a = r.render(cam.R, t2, cam.fx, cam.fy, cam.cx, cam.cy).clone()
+    tr.seed = seed
+    s2 = run_frame(tr, b, st).cpu().numpy()
+    # (loss sums and table gradients are float atomics: equal up to summation order)
+    assert np.allclose(s1, s2, rtol=1e-5, atol=0), (s1, s2)
+    g2 = st["tgrad"]
+    assert (g1 - g2).abs().max().item() <= 1e-4 * g1.abs().max().item()
+    # a full step with zero learning rates leaves every parameter as it was: the view
+    # rendered after it must be bit-identical to the one before it (run_frame above
+    # drove Trainer.set_frame directly, outside step(): re-register the view's frame)
+    r.set_frame(sc.node_dqs(5), sc.theta(5), sc.bone_transforms(5), *sc.object_pose(5))
+    img_a = r.render(cam.R, t2, cam.fx, cam.fy, cam.cx, cam.cy).clone()
+    lr = (tr.cfg.lr_hash, tr.cfg.lr_net)
+    tr.cfg.lr_hash = tr.cfg.lr_net = 0.0
+    try:
+        tr.step(batches)
+    finally:
+        tr.cfg.lr_hash, tr.cfg.lr_net = lr
+    img_b = r.render(cam.R, t2, cam.fx, cam.fy, cam.cx, cam.cy).clone()
+    torch.cuda.synchronize()
+    assert torch.equal(img_a, img_b)
