@@ -577,16 +577,17 @@ def run_train(args, rank, world, pg):
     """configs[2]: key-frame training step, 2^18 rays (global; sharded over ranks)
     drawn from the 10 key frames, forward + backward + Adam, gradients all-reduced.
     The key frames' images live in HBM; every step draws fresh rays from their
-    foreground pixels on the device (KeyFrame.sample, inside the timed step)."""
+    foreground pixels on the device. The whole step (draw, counts, 10 frames x 2
+    fields of forward / backward / dW, bucket all-reduce, Adam, repack) is one CUDA
+    graph (Trainer.capture). e2e: the public eager API, Trainer.step, on batches
+    uploaded every step from pinned host memory, the losses read back."""
     import torch
-    from paper_2304_03184_b200.train import KeyFrame, Trainer, TrainConfig, allreduce_grads, shard_rays
+    from paper_2304_03184_b200.train import KeyFrame, Trainer, TrainConfig, shard_rays
     sc, cfg, hf, of, r, frames = build_workload(args, rank)
     cam = sc.camera
     r.rays(cam.R, cam.t, cam.fx, cam.fy, cam.cx, cam.cy)
     dev = torch.device("cuda", torch.cuda.current_device())
-    mine = shard_rays(args.train_rays, rank, world)
-    n_local = mine.stop - mine.start
-    per_frame = int(np.ceil(n_local / len(frames)))
+    per_frame = int(np.ceil(args.train_rays / world / len(frames)))
     o, d = cam.all_rays()
     T = lambda x, dt: torch.as_tensor(np.ascontiguousarray(x), dtype=dt, device=dev)  # noqa: E731
     keyframes = []
@@ -599,45 +600,81 @@ def run_train(args, rank, world, pg):
                                   T(sc.bone_transforms(fid), torch.float64),
                                   T(hf.nets.theta_bias(f["theta"]), torch.float32), T(f["theta"], torch.float32),
                                   f["R"], f["t"]))
-    step_no = [0]
-
-    def draw():
-        step_no[0] += 1
-        return [kf.sample(per_frame, seed=(step_no[0] * 1000 + fid) * 64 + rank)
-                for fid, kf in enumerate(keyframes)]
-
-    batches = draw()
     tr = Trainer(r, max_rays=per_frame, cfg=TrainConfig())
-    ar = (lambda ts: allreduce_grads(ts)) if world > 1 else None
-    for _ in range(args.warmup):
-        tr.step(draw(), allreduce=ar)
+    group = None if world == 1 else torch.distributed.group.WORLD
+    step = tr.capture(keyframes, per_frame, group)  # (its warm-up is a real step)
+    for _ in range(max(0, args.warmup - 1)):
+        step()
     torch.cuda.synchronize()
     barrier(pg)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    for _ in range(args.steps):
-        tr.step(draw(), allreduce=ar)
-    b.record()
-    torch.cuda.synchronize()
+    with ClockSampler(torch.cuda.current_device()) as clocks:
+        a.record()
+        for _ in range(args.steps):
+            step()
+        b.record()
+        torch.cuda.synchronize()
+    clk = clocks.summary()
     barrier(pg)
     ms = max_over_ranks(pg, a.elapsed_time(b))
-    # samples processed per step (sum over frames and fields), from one instrumented step
-    per_step = 0
-    for bt in batches:
-        tr.set_frame(bt)
-        for st in tr.fields:
-            tr._frame(bt, st, torch.zeros(2, device=dev))
-            per_step += int(st["buf"].counters[0])
-    per_step = sum_over_ranks(pg, float(per_step))
+    # samples of a step from its (rank-summed) ray counts: 32 guided + 16 uniform per
+    # masked ray with depth, 64 uniform without, per field and frame
+    c = tr.counts.cpu().numpy().astype(np.int64)
+    per_step = float(sum(48 * c[:, 2 * q + 1] + 64 * (c[:, 2 * q] - c[:, 2 * q + 1]) for q in range(2)).sum())
+    ours, other, names = count_launches(step)
+    launches = {"per_step": ours, "foreign_kernels_per_step": other, "kernels": names,
+                "how": "CUPTI (torch.profiler) over one graph replay"}
+    # e2e: eager public API, this step's ray batches uploaded from pinned host memory
+    e2e = None
+    if not args.no_e2e:
+        host = []
+        for kf in keyframes:
+            bt = kf.sample(per_frame, seed=rank + 17)
+            host.append({k: getattr(bt, k).cpu().pin_memory() for k in ("dirs", "gt_rgb", "gt_depth", "mask_h",
+                                                                        "mask_o")})
+        bufs = [kf.batch_buffers(per_frame) for kf in keyframes]
+        for bt in bufs:
+            bt.ray0 = rank * per_frame
+        h2d = sum(v.numel() * v.element_size() for hb in host for v in hb.values())
+        loss_h = torch.empty((2, 2), dtype=torch.float32).pin_memory()
+
+        def e2e_step():
+            for bt, hb in zip(bufs, host):
+                for k, v in hb.items():
+                    getattr(bt, k).copy_(v, non_blocking=True)
+            out = tr.step(bufs, group)
+            loss_h.copy_(tr.stats, non_blocking=True)
+            return out
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        barrier(pg)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        el = max_over_ranks(pg, time.perf_counter() - t0)
+        e2e = {"value": per_step * args.steps / el, "unit": "samples/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": 16, "ms_per_step": el * 1e3 / args.steps,
+               "path": "Trainer.step (eager) on ray batches copied from pinned host memory every step, "
+                       "losses read back"}
     line = {"metric": "training samples/s (fwd+bwd+Adam, warp+hash+MLP+composite)", "value":
             per_step * args.steps / (ms / 1e3), "unit": "samples/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64 deform / f32 hash+grads / fp16-in fp32-acc MLP",
+            "vs_baseline": None,
+            "dtype": "f64 deform / fp32-semantics forward (split-fp16 tcgen05) / fp16-operand fp32-acc backward / "
+                     "f32 tables, grads, Adam",
             "data": "synthetic (analytic ray-cast targets of the scripted scene)",
             "config": {"workload": f"key-frame training step (configs[2]): {args.train_rays} rays over 10 frames "
                                    f"drawn on the device every step from the HBM-resident key-frame images, "
                                    f"32 guided + 16 uniform / 64 empty samples per ray",
-                       "samples_per_step": per_step, "parallelism": f"dp{world} (rays sharded, grads all-reduced)"}}
+                       "samples_per_step": per_step, "rays_per_frame_per_rank": per_frame,
+                       "step": "one CUDA graph: draw + counts + 10 frames x (human, object) fwd/bwd/dW + "
+                               "bucket all-reduce + multi-tensor Adam + repack",
+                       "l2": "inputs (hash tables 64 MB + 47 MB, per-frame activations) larger than L2",
+                       "parallelism": f"dp{world} (rays sharded, ray counts and gradient buckets summed)"},
+            "gpu_launches": launches["per_step"] * args.steps, "gpu_launches_detail": launches,
+            "clocks": clk, "e2e": e2e}
     if rank == 0:
         print(json.dumps(line))
 

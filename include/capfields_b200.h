@@ -327,11 +327,17 @@ typedef struct cf_field_desc {
   int precise;              /* 1 = "fp32" mode: fp32 tables and features, split-fp16 (hi + lo) MLP operands
                                (3 MMA chains per layer); 0 = "fp16" mode (fp16 operands, fp16 deform-table copy) */
   const uint8_t* wblob_lo;  /* precise: the residual blob fp16(W - fp16(W)), same layout as wblob */
+  int train;                /* 1 = the training forward: 32-bit semantics (as precise) plus the fp16 saves of
+                               the backward, feature-major in the scratch (cf_field_train_layout) */
 } cf_field_desc;
 /* device scratch needed by cf_field_forward for `capacity` samples */
 int cf_field_scratch_bytes(const cf_field_desc* F, int64_t capacity, int64_t* bytes);
 /* scratch layout (S = capacity): fp16 mode: cfeat (S,32) fp16 | dfeat (S,32) fp16 | xc (S) float4;
- * precise mode: cfeat (S,32) fp32 | dfeat (S,32) fp32 | xc (S) float4 (dfeat / xc human only) */
+ * precise mode: cfeat (S,32) fp32 | dfeat (S,32) fp32 | xc (S) float4 (dfeat / xc human only);
+ * training (train = 1, S % 8 == 0): byte offsets from cf_field_train_layout:
+ * [0] cfeat16 (32,S) fp16 feature-major, [1] dfeat16 (33,S) fp16 feature-major with row 32 = 1,
+ * [2] xc (S) float4, [3] dfeat32 (S,32) fp32, [4] cfeat32 (S,32) fp32, [5] total bytes */
+int cf_field_train_layout(int64_t capacity, int64_t* offsets);
 /* out: float4 (sigma, r, g, b) per compacted sample of S (count read on device).
  * Stages: hash (fp16 features) [-> DeformNet -> hash] -> E_g/E_c, see field.cu */
 int cf_field_forward(const cf_field_desc* F, const cf_march_out* S, const double* dirs, const float* xu, float* out,
@@ -347,25 +353,29 @@ int cf_field_stage(const cf_field_desc* F, const cf_march_out* S, const double* 
  * uniformly with replacement from fg_pixels (the frame's foreground pixel ids) by a
  * counter-based hash of (seed, i); gathers rgb (H*W,3), depth, masks at those pixels
  * and writes each pixel's exact camera ray (same directions as cf_camera_rays);
- * pix_out (optional) = the drawn pixel ids */
+ * pix_out (optional) = the drawn pixel ids; seed_offset (optional, device) is added to
+ * seed (a captured training step draws new rays every replay) */
 int cf_keyframe_rays(const cf_camera* cam, const int* fg_pixels, int64_t n_fg, int64_t n_rays, uint64_t seed,
-                     const float* rgb, const float* depth, const uint8_t* mask_h, const uint8_t* mask_o, int* pix_out,
+                     const uint64_t* seed_offset, const float* rgb, const float* depth, const uint8_t* mask_h, const uint8_t* mask_o, int* pix_out,
                      double* dirs, float* rgb_out, float* depth_out, uint8_t* mask_h_out, uint8_t* mask_o_out,
                      void* stream);
 /* depth-guided samples of the masked rays: fills F (records, per-ray
  * offset/count, counters) and t_out (float64 depth per compacted sample; pass it as
- * M->sample_t to the canonicalisation / field / composite calls) */
+ * M->sample_t to the canonicalisation / field / composite calls); the stratum jitter of ray i
+ * is a counter-based hash of (seed + *seed_offset, ray_id0 + i): a ray draws the same samples
+ * whichever shard of a data-parallel batch it is in */
 int cf_train_sample(const cf_march_desc* M, const float* gt_depth, const uint8_t* mask, int n_guided, int n_uniform,
-                    int n_empty, double sigma_d, uint64_t seed, const cf_march_out* F, double* t_out, void* stream);
+                    int n_empty, double sigma_d, uint64_t seed, const uint64_t* seed_offset, int64_t ray_id0,
+                    const cf_march_out* F, double* t_out, void* stream);
 /* masked L2 colour + lambda * L1 depth (lambda_depth = 0.1) and the
  * compositing backward: grad = grad_scale * float4 (dL/dsigma, dL/dr, dL/dg, dL/db) per
- * sample (grad_scale: a power of two keeping the fp16 backward operands in range —
- * loss scaling; the optimiser divides it out); loss[0] += L_color, loss[1] += L_depth
- * (unweighted, unscaled), normalised by inv_n_* */
+ * sample; norm (device, 4 floats) = [1 / n_masked, 1 / n_depth_valid, grad_scale, loss weight]
+ * (cf_train_norms; grad_scale: a power of two keeping the fp16 backward operands in
+ * range — loss scaling, divided out by the optimiser); loss[0] += L_color,
+ * loss[1] += L_depth (normalised, times the loss weight, unscaled) */
 int cf_loss_composite_bwd(const cf_march_desc* M, const cf_march_out* F, const float* field, float t_term,
                           const float* gt_rgb, const float* gt_depth, const uint8_t* mask, float lambda_depth,
-                          float inv_n_color, float inv_n_depth, float grad_scale, float* grad, float* loss,
-                          void* stream);
+                          const float* norm, float* grad, float* loss, void* stream);
 
 /* saved activations (fp16 rows) and gradients of the E_g/E_c backward (S = capacity) */
 typedef struct cf_color_bwd_io {
@@ -418,6 +428,62 @@ int cf_adam(float* p, const float* g, float* m, float* v, int64_t n, float lr, f
  * n_cols in {32, 64, 128} */
 int cf_gemm_kmajor_f16(const void* A, int64_t lda, const void* B, int64_t ldb, int n_cols, int64_t K, float* C,
                        int ldc, void* stream);
+/* ---- the training step's device-side control (graph-capturable: no host syncs) */
+/* one weight-gradient problem: C[m x n] += A[m x K] B[n x K]^T, A / B fp16 K-major (the
+ * feature-major saves: row stride lda / ldb elements, 16-byte aligned rows), C fp32
+ * row-major (ldc); m, n in 1..128 */
+typedef struct cf_dw_problem {
+  const void* A;
+  int64_t lda;
+  int m;
+  const void* B;
+  int64_t ldb;
+  int n;
+  float* C;
+  int ldc;
+} cf_dw_problem;
+/* up to 10 problems in one tcgen05 launch, K = min(*count, capacity) read on the
+ * device (the frame's sample count); the operands' columns K .. roundup(K, 64) must be
+ * finite with zero in A or B (the training kernels write every lane of a tile) */
+int cf_dw_grouped(const cf_dw_problem* problems, int n, const int* count, int64_t capacity, void* stream);
+/* masked / depth-valid ray counts of n_frames key-frame batches (frame f's rays at
+ * f * frame_stride): counts (n_frames, 4) int32 = [n_m human, n_d human, n_m object, n_d object] */
+int cf_train_counts(const uint8_t* mask_h, const uint8_t* mask_o, const float* gt_depth, int64_t n_rays,
+                    int n_frames, int64_t frame_stride, int* counts, void* stream);
+/* per-step normalisers from the counts (after the data-parallel sum over ranks):
+ * norms (2 fields, n_frames, 4) = [1/n_m, 1/n_d, loss scale, 1/n_frames] (cf_loss_composite_bwd's
+ * norm), adam_scale (2) = 1 / (n_frames * loss scale), stats (2 fields x 2) zeroed, ++*step,
+ * *seed (optional) = the step's sampling seed offset */
+int cf_train_norms(const int* counts, int n_frames, float* norms, float* adam_scale, float* stats, int* step,
+                   uint64_t* seed, void* stream);
+/* DeformNet layer-1 dW from the GEMM over [features | 1]: G[:, :n_x] += tmp[:, :n_x],
+ * G[:, n_x + j] += tmp[:, n_x] * theta[j]; tmp (rows, ldt) zeroed */
+int cf_dw_pose_cols(float* tmp, int rows, int ldt, int n_x, const float* theta, int n_theta, float* G, int ldg,
+                    void* stream);
+/* one tensor of cf_adam_multi; p16 (optional) receives fp16(p) after the update */
+typedef struct cf_adam_tensor {
+  float* p;
+  float* g;
+  float* m;
+  float* v;
+  void* p16;
+  int64_t n;
+  float lr;
+  int scale_idx;  /* gradient scale = scale[scale_idx] */
+} cf_adam_tensor;
+/* Adam over up to 24 tensors in one launch: bias corrections from the device step
+ * counter, gradients multiplied by the device scale (NULL = 1) and zeroed after use */
+int cf_adam_multi(const cf_adam_tensor* tensors, int n, float beta1, float beta2, float eps, const int* step,
+                  const float* scale, void* stream);
+/* one matrix of cf_pack_multi: the packed matrix P (rows x cols) is W[r][col0 + c]
+ * (transpose = 0) or W[c][col0 + r] (transpose = 1), W row stride ldw; blob_lo optional */
+typedef struct cf_pack_item {
+  const float* w;
+  uint8_t* blob;
+  uint8_t* blob_lo;
+  int rows, cols, ldw, col0, transpose;
+} cf_pack_item;
+int cf_pack_multi(const cf_pack_item* items, int n, void* stream);
 /* fp32 (n x k) row-major weight -> fp16 UMMA canonical K-major blob (n, k padded to 16) */
 int cf_pack_weight(const float* w, int n, int k, uint8_t* blob, void* stream);
 /* as cf_pack_weight, plus the residual fp16(W - fp16(W)) into blob_lo (same layout):

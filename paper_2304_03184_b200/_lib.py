@@ -87,7 +87,23 @@ class FieldDesc(ctypes.Structure):
                 ("cgrid", HashGridDesc), ("ctable", ctypes.c_void_p), ("wblob", ctypes.c_void_p),
                 ("w_bytes", ctypes.c_int), ("dbias", ctypes.c_void_p), ("delta_scale", ctypes.c_float),
                 ("inv_side", ctypes.c_float), ("save_h", ctypes.c_void_p), ("save_o", ctypes.c_void_p),
-                ("save_mask", ctypes.c_void_p), ("precise", ctypes.c_int), ("wblob_lo", ctypes.c_void_p)]
+                ("save_mask", ctypes.c_void_p), ("precise", ctypes.c_int), ("wblob_lo", ctypes.c_void_p),
+                ("train", ctypes.c_int)]
+
+
+class DwProblem(ctypes.Structure):
+    _fields_ = [("A", ctypes.c_void_p), ("lda", ctypes.c_int64), ("m", ctypes.c_int), ("B", ctypes.c_void_p),
+                ("ldb", ctypes.c_int64), ("n", ctypes.c_int), ("C", ctypes.c_void_p), ("ldc", ctypes.c_int)]
+
+
+class AdamTensor(ctypes.Structure):
+    _fields_ = [("p", ctypes.c_void_p), ("g", ctypes.c_void_p), ("m", ctypes.c_void_p), ("v", ctypes.c_void_p),
+                ("p16", ctypes.c_void_p), ("n", ctypes.c_int64), ("lr", ctypes.c_float), ("scale_idx", ctypes.c_int)]
+
+
+class PackItem(ctypes.Structure):
+    _fields_ = [("w", ctypes.c_void_p), ("blob", ctypes.c_void_p), ("blob_lo", ctypes.c_void_p), ("rows", ctypes.c_int),
+                ("cols", ctypes.c_int), ("ldw", ctypes.c_int), ("col0", ctypes.c_int), ("transpose", ctypes.c_int)]
 
 
 class MpInfo(ctypes.Structure):
@@ -210,10 +226,19 @@ _SIGS = {
     "cf_field_forward": [_P(FieldDesc), _P(MarchOut), _p, _p, _p, _p, _p],
     "cf_field_scratch_bytes": [_P(FieldDesc), _i64, _P(_i64)],
     "cf_field_stage": [_P(FieldDesc), _P(MarchOut), _p, _p, _p, _p, _i32, _p],
-    "cf_keyframe_rays": [_P(Camera), _p, _i64, _i64, ctypes.c_uint64, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p],
-    "cf_train_sample": [_P(MarchDesc), _p, _p, _i32, _i32, _i32, _f64, ctypes.c_uint64, _P(MarchOut), _p, _p],
-    "cf_loss_composite_bwd": [_P(MarchDesc), _P(MarchOut), _p, ctypes.c_float, _p, _p, _p, ctypes.c_float,
-                              ctypes.c_float, ctypes.c_float, ctypes.c_float, _p, _p, _p],
+    "cf_keyframe_rays": [_P(Camera), _p, _i64, _i64, ctypes.c_uint64, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p,
+                         _p],
+    "cf_train_sample": [_P(MarchDesc), _p, _p, _i32, _i32, _i32, _f64, ctypes.c_uint64, _p, _i64, _P(MarchOut), _p,
+                        _p],
+    "cf_loss_composite_bwd": [_P(MarchDesc), _P(MarchOut), _p, ctypes.c_float, _p, _p, _p, ctypes.c_float, _p, _p,
+                              _p, _p],
+    "cf_field_train_layout": [_i64, _p],
+    "cf_dw_grouped": [_p, _i32, _p, _i64, _p],
+    "cf_train_counts": [_p, _p, _p, _i64, _i32, _i64, _p, _p],
+    "cf_train_norms": [_p, _i32, _p, _p, _p, _p, _p, _p],
+    "cf_dw_pose_cols": [_p, _i32, _i32, _i32, _p, _i32, _p, _i32, _p],
+    "cf_adam_multi": [_p, _i32, ctypes.c_float, ctypes.c_float, ctypes.c_float, _p, _p, _p],
+    "cf_pack_multi": [_p, _i32, _p],
     "cf_color_backward": [_P(FieldDesc), _p, _P(MarchOut), _p, _p, _p, _p, _P(ColorBwdIO), _p],
     "cf_field_hash_backward": [_P(FieldDesc), _P(MarchOut), _p, _p, _p, _p, _p, _p],
     "cf_deform_backward": [_P(FieldDesc), _p, _P(MarchOut), _p, _p, _P(DeformBwdIO), _p],

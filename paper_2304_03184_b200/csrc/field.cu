@@ -207,13 +207,6 @@ __device__ __forceinline__ void relu_to_abuf(Slot& S, const float* bias) {
 }
 
 // copy one 64-byte fp16 feature row into the A buffer (K = 32)
-__device__ __forceinline__ void row_to_abuf(Slot& S, const uint4* __restrict__ feat, int64_t s, bool live) {
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const uint4 v = live ? feat[s * 4 + q] : make_uint4(0, 0, 0, 0);
-    *reinterpret_cast<uint4*>(S.abuf + tc::core_offset(S.r, 8 * q, 32)) = v;
-  }
-}
 
 template <int SLOTS, int TMEM_COLS>
 __device__ __forceinline__ void slots_setup(const uint8_t* __restrict__ wblob, int w_bytes, uint8_t* smem,
@@ -302,13 +295,18 @@ __device__ __forceinline__ void store_cols_f16(uint16_t* dst, int64_t ld, int co
   }
 }
 
+// 16 fp16 values (8 packed pairs) of sample s as columns col .. col+15 of a
+// feature-major block (column c at dst[c * ld + s])
+__device__ __forceinline__ void store_cols16_f16(uint16_t* dst, int64_t ld, int64_t s, int col, const uint32_t* h) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    dst[(int64_t)(col + 2 * i) * ld + s] = (uint16_t)(h[i] & 0xffffu);
+    dst[(int64_t)(col + 2 * i + 1) * ld + s] = (uint16_t)(h[i] >> 16);
+  }
+}
+
 // hidden epilogue of a 128-wide layer: this warp's 64 columns -> (+bias) ReLU -> fp16 -> A
-// (training: also -> save, this layer's activations of the sample in the feature-major
-// (128, ld) block at save (column c at save[c * ld]), and mask = the ReLU derivative
-// bits of these 64 columns, 2 x uint32)
-__device__ __forceinline__ void ts_relu128(const TsSlot& S, const float* bias, __half* save,
-                                           uint32_t* mask = nullptr, int64_t ld = 0) {
-  uint32_t mw[2];
+__device__ __forceinline__ void ts_relu128(const TsSlot& S, const float* bias) {
 #pragma unroll
   for (int c = 0; c < 2; ++c) {
     const int col = 64 * S.half + 32 * c;
@@ -316,7 +314,6 @@ __device__ __forceinline__ void ts_relu128(const TsSlot& S, const float* bias, _
     tc::tmem_ld32_nowait(S.d + (uint32_t)col, r);
     tc::tmem_wait_ld();
     uint32_t h[16];
-    uint32_t bits = 0;
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       float x0 = __uint_as_float(r[2 * i]), x1 = __uint_as_float(r[2 * i + 1]);
@@ -324,10 +321,8 @@ __device__ __forceinline__ void ts_relu128(const TsSlot& S, const float* bias, _
         x0 += bias[col + 2 * i];
         x1 += bias[col + 2 * i + 1];
       }
-      bits |= (x0 > 0.0f ? 1u : 0u) << (2 * i) | (x1 > 0.0f ? 1u : 0u) << (2 * i + 1);
       h[i] = tc::relu_f16x2(x0, x1);
     }
-    mw[c] = bits;
     if (S.abuf) {
 #pragma unroll
       for (int q = 0; q < 4; ++q)
@@ -336,19 +331,14 @@ __device__ __forceinline__ void ts_relu128(const TsSlot& S, const float* bias, _
     } else {
       tc::tmem_st16(S.a + (uint32_t)(col / 2), h);
     }
-    if (save) store_cols_f16(reinterpret_cast<uint16_t*>(save), ld, col, h);
   }
-  if (mask) *reinterpret_cast<uint2*>(mask) = make_uint2(mw[0], mw[1]);
 }
 
-// kSave: the training forward (saves h, o and the ReLU bits); the render path
-// compiles without them
-template <bool kSave>
+// the fp16-mode render forward (the training forward is deform_mlp_prec_kernel<true>)
 __global__ void __launch_bounds__(kDeformSlots* kDeformSlotThreads, 1)
     deform_mlp_kernel(const uint8_t* __restrict__ wblob, const float* __restrict__ bias1, float delta_scale,
                       float inv_side, const float4* __restrict__ xu, const uint4* __restrict__ dfeat,
-                      const int* __restrict__ count, int64_t capacity, float4* __restrict__ xc,
-                      __half* __restrict__ save_h, float4* __restrict__ save_o, uint32_t* __restrict__ save_mask) {
+                      const int* __restrict__ count, int64_t capacity, float4* __restrict__ xc) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t mbar[kDeformSlots];
   __shared__ uint32_t tmem_base;
@@ -411,23 +401,17 @@ __global__ void __launch_bounds__(kDeformSlots* kDeformSlotThreads, 1)
 #pragma unroll
       for (int q = 0; q < 2; ++q) nxt[q] = (sn < n) ? dfeat[sn * 4 + 2 * S.half + q] : make_uint4(0, 0, 0, 0);
     }
-    // activations h1..h4 feature-major: save_h (512, capacity), row = layer * 128 + column
-    __half* sv = (kSave && live) ? save_h + s : nullptr;
-    const int64_t L = 128 * capacity;
-    // ReLU masks: per sample 4 layers x 2 halves x 64 bits
-    uint32_t* mk = (kSave && live) ? save_mask + s * 16 + 2 * S.half : nullptr;  // [layer][half][2]
-    ts_relu128(S, s_bias, sv, mk, capacity);
+    ts_relu128(S, s_bias);
     ts_layer(S, smem + o2, 128, 128);
-    ts_relu128(S, nullptr, sv ? sv + L : nullptr, mk ? mk + 4 : nullptr, capacity);
+    ts_relu128(S, nullptr);
     ts_layer(S, smem + o3, 128, 128);
-    ts_relu128(S, nullptr, sv ? sv + 2 * L : nullptr, mk ? mk + 8 : nullptr, capacity);
+    ts_relu128(S, nullptr);
     ts_layer(S, smem + o4, 128, 128);
-    ts_relu128(S, nullptr, sv ? sv + 3 * L : nullptr, mk ? mk + 12 : nullptr, capacity);
+    ts_relu128(S, nullptr);
     ts_layer(S, smem + o5, 128, 16);
     if (S.half == 0) {
       float v[16];
       tc::tmem_ld16(S.d, v);
-      if (kSave && live) save_o[s] = make_float4(v[0], v[1], v[2], 0.0f);
       if (live) {
         float4 p = xs;
         if (p.w > 0.0f) {
@@ -708,7 +692,7 @@ __global__ void __launch_bounds__(kPrecDeformSlots* kDeformSlotThreads, 1)
                            const float4* __restrict__ xu, const float4* __restrict__ dfeat,
                            const int* __restrict__ count, int64_t capacity, float4* __restrict__ xc,
                            __half* __restrict__ save_h, float4* __restrict__ save_o,
-                           uint32_t* __restrict__ save_mask, uint4* __restrict__ dfeat16) {
+                           uint32_t* __restrict__ save_mask, __half* __restrict__ dfeat16) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t mbar[kPrecDeformSlots];
   __shared__ uint32_t tmem_base;
@@ -758,14 +742,16 @@ __global__ void __launch_bounds__(kPrecDeformSlots* kDeformSlotThreads, 1)
       for (int q = 0; q < 4; ++q) f[q] = live ? dfeat[s * 8 + 4 * S.half + q] : make_float4(0.f, 0.f, 0.f, 0.f);
       uint32_t hi[8];
       split_store<4>(S, f, 8 * S.half, kSave ? hi : nullptr);  // this half's 16 features
-      if (kSave && live) {
-        dfeat16[s * 4 + 2 * S.half] = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-        dfeat16[s * 4 + 2 * S.half + 1] = make_uint4(hi[4], hi[5], hi[6], hi[7]);
+      if (kSave && s < capacity) {
+        // feature-major (33, capacity): this half's 16 feature rows, + row 32 = 1 (the
+        // layer-1 dW GEMM's extra column: sum_s dpre1, for the pose columns)
+        store_cols16_f16(reinterpret_cast<uint16_t*>(dfeat16), capacity, s, 16 * S.half, hi);
+        if (S.half == 0) reinterpret_cast<uint16_t*>(dfeat16)[32 * capacity + s] = 0x3C00u;  // 1.0
       }
     }
     const float4 xs = (live && S.half == 0) ? xu[s] : make_float4(0.f, 0.f, 0.f, 0.f);
     // training saves: h feature-major (512, capacity), ReLU bits [layer][half][2] per sample
-    __half* sv = (kSave && live) ? save_h + s : nullptr;
+    __half* sv = (kSave && s < capacity) ? save_h + s : nullptr;
     const int64_t L = 128 * capacity;
     uint32_t* mk = (kSave && live) ? save_mask + s * 16 + 2 * S.half : nullptr;
     const uint8_t* wo[4] = {smem + o1, smem + o2, smem + o3, smem + o4};
@@ -810,7 +796,7 @@ __global__ void __launch_bounds__(kColorPrecSlots* kSlotThreads, 1)
                           const float4* __restrict__ xu, const float4* __restrict__ cfeat,
                           const uint32_t* __restrict__ records, const double* __restrict__ dirs,
                           const int* __restrict__ count, int64_t capacity, float4* __restrict__ out,
-                          uint4* __restrict__ cfeat16) {
+                          __half* __restrict__ cfeat16) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t mbar[kColorPrecSlots];
   __shared__ uint32_t tmem_base;
@@ -857,9 +843,9 @@ __global__ void __launch_bounds__(kColorPrecSlots* kSlotThreads, 1)
       for (int q = 0; q < 8; ++q) f[q] = live ? cfeat[s * 8 + q] : make_float4(0.f, 0.f, 0.f, 0.f);
       uint32_t hi[16];
       split_store<8>(S, f, 0, cfeat16 ? hi : nullptr);
-      if (cfeat16 && live) {  // training: the features' fp16 halves for the fp16 backward
-#pragma unroll
-        for (int q = 0; q < 4; ++q) cfeat16[s * 4 + q] = make_uint4(hi[4 * q], hi[4 * q + 1], hi[4 * q + 2], hi[4 * q + 3]);
+      if (cfeat16 && s < capacity) {  // training: the features' fp16 halves, feature-major (32, capacity)
+        store_cols16_f16(reinterpret_cast<uint16_t*>(cfeat16), capacity, s, 0, hi);
+        store_cols16_f16(reinterpret_cast<uint16_t*>(cfeat16), capacity, s, 16, hi + 8);
       }
     }
     const bool valid = live && xu[s].w > 0.0f;
@@ -928,20 +914,17 @@ struct ColorBwdIO {
   float* dfeat;  // (S,32) dL/d(hash features)
 };
 
-__device__ __forceinline__ void store_row_f16(__half* dst, int64_t s, int width, const float* v) {
-  uint4* d = reinterpret_cast<uint4*>(dst + s * width);
-#pragma unroll 4
-  for (int q = 0; q < width / 8; ++q) {
-    __half2 h[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) h[i] = __floats2half2_rn(v[8 * q + 2 * i], v[8 * q + 2 * i + 1]);
-    d[q] = *reinterpret_cast<uint4*>(h);
-  }
+// width fp16 values of sample s into a feature-major (width, ld) block: column c at
+// dst[c * ld + s] (lanes = consecutive samples: coalesced 64-byte warp segments)
+__device__ __forceinline__ void store_fm_f16(__half* dst, int64_t s, int64_t ld, int width, const float* v) {
+#pragma unroll 8
+  for (int c = 0; c < width; ++c) dst[(int64_t)c * ld + s] = __float2half_rn(v[c]);
 }
 
-// forward hidden layer with ReLU: keep the activation mask, write fp16 to A buffer (+ HBM copy)
+// forward hidden layer with ReLU: keep the activation mask, write fp16 to A buffer (+ the
+// feature-major HBM copy, row stride ld)
 template <int N>
-__device__ __forceinline__ uint64_t fwd_relu(Slot& S, __half* save, int64_t s, bool live) {
+__device__ __forceinline__ uint64_t fwd_relu(Slot& S, __half* save, int64_t s, bool live, int64_t ld) {
   uint64_t mask = 0;
 #pragma unroll
   for (int c0 = 0; c0 < N; c0 += 32) {
@@ -954,23 +937,14 @@ __device__ __forceinline__ uint64_t fwd_relu(Slot& S, __half* save, int64_t s, b
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q) tc::st_row8(S.abuf, S.r, c0 + 8 * q, N, v + 8 * q);
-    if (live) {
-      uint4* d = reinterpret_cast<uint4*>(save + s * N + c0);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        __half2 h[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) h[i] = __floats2half2_rn(v[8 * q + 2 * i], v[8 * q + 2 * i + 1]);
-        d[q] = *reinterpret_cast<uint4*>(h);
-      }
-    }
+    if (live) store_fm_f16(save + (int64_t)c0 * ld, s, ld, 32, v);
   }
   return mask;
 }
 
 // backward through a ReLU layer: dpre = dact (from TMEM) * relu'(mask) -> A buffer (+ HBM)
 template <int N>
-__device__ __forceinline__ void bwd_relu(Slot& S, uint64_t mask, __half* save, int64_t s, bool live) {
+__device__ __forceinline__ void bwd_relu(Slot& S, uint64_t mask, __half* save, int64_t s, bool live, int64_t ld) {
 #pragma unroll
   for (int c0 = 0; c0 < N; c0 += 32) {
     float v[32];
@@ -980,22 +954,13 @@ __device__ __forceinline__ void bwd_relu(Slot& S, uint64_t mask, __half* save, i
       if (!((mask >> (c0 + i)) & 1ull)) v[i] = 0.0f;
 #pragma unroll
     for (int q = 0; q < 4; ++q) tc::st_row8(S.abuf, S.r, c0 + 8 * q, N, v + 8 * q);
-    if (live) {
-      uint4* d = reinterpret_cast<uint4*>(save + s * N + c0);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        __half2 h[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) h[i] = __floats2half2_rn(v[8 * q + 2 * i], v[8 * q + 2 * i + 1]);
-        d[q] = *reinterpret_cast<uint4*>(h);
-      }
-    }
+    if (live) store_fm_f16(save + (int64_t)c0 * ld, s, ld, 32, v);
   }
 }
 
 __global__ void __launch_bounds__(kBwdSlots* kSlotThreads, 1)
     color_bwd_kernel(const uint8_t* __restrict__ wblob, const uint8_t* __restrict__ wtblob,
-                     const float4* __restrict__ xu, const uint4* __restrict__ cfeat,
+                     const float4* __restrict__ xu, const __half* __restrict__ cfeat,
                      const uint32_t* __restrict__ records, const double* __restrict__ dirs,
                      const float4* __restrict__ gout, const int* __restrict__ count, int64_t capacity,
                      ColorBwdIO io) {
@@ -1015,11 +980,23 @@ __global__ void __launch_bounds__(kBwdSlots* kSlotThreads, 1)
   for (int64_t tile = (int64_t)blockIdx.x * kBwdSlots + S.slot; tile < n_tiles; tile += (int64_t)gridDim.x * kBwdSlots) {
     const int64_t s = tile * 128 + S.r;
     const bool live = s < n;
+    // the saves (feature-major, row stride = capacity) are written for every lane of
+    // the tile inside the capacity: the dW GEMMs' last K tile reads past n, where the
+    // dead lanes' dL/d terms are zero and their activations finite
+    const bool keep = s < capacity;
+    const int64_t ld = capacity;
     const bool valid = live && xu[s].w > 0.0f;
-    // ---- forward recompute, saving what the weight gradients need
-    row_to_abuf(S, cfeat, s, live);
+    // ---- forward recompute from the features (fp16, feature-major (32, capacity)),
+    // saving what the weight gradients need
+    {
+      float x[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) x[c] = live ? __half2float(cfeat[(int64_t)c * ld + s]) : 0.0f;
+#pragma unroll
+      for (int k0 = 0; k0 < 32; k0 += 8) tc::st_row8(S.abuf, S.r, k0, 32, x + k0);
+    }
     run_layer(S, g1, 32, 64);
-    const uint64_t m_h1 = fwd_relu<64>(S, io.h1, s, live);
+    const uint64_t m_h1 = fwd_relu<64>(S, io.h1, s, keep, ld);
     run_layer(S, g2, 64, 16);
     float gv[16];
     tc::tmem_ld16(S.tmem_row, gv);
@@ -1038,11 +1015,11 @@ __global__ void __launch_bounds__(kBwdSlots* kSlotThreads, 1)
     cin[31] = 0.0f;
 #pragma unroll
     for (int k0 = 0; k0 < 32; k0 += 8) tc::st_row8(S.abuf, S.r, k0, 32, cin + k0);
-    if (live) store_row_f16(io.cin, s, 32, cin);
+    if (keep) store_fm_f16(io.cin, s, ld, 32, cin);
     run_layer(S, c1, 32, 64);
-    const uint64_t m_c1 = fwd_relu<64>(S, io.c1, s, live);
+    const uint64_t m_c1 = fwd_relu<64>(S, io.c1, s, keep, ld);
     run_layer(S, c2, 64, 64);
-    const uint64_t m_c2 = fwd_relu<64>(S, io.c2, s, live);
+    const uint64_t m_c2 = fwd_relu<64>(S, io.c2, s, keep, ld);
     run_layer(S, c3, 64, 16);
     float ov[16];
     tc::tmem_ld16(S.tmem_row, ov);
@@ -1061,11 +1038,11 @@ __global__ void __launch_bounds__(kBwdSlots* kSlotThreads, 1)
     }
     tc::st_row8(S.abuf, S.r, 0, 16, d_o);
     tc::st_row8(S.abuf, S.r, 8, 16, d_o + 8);
-    if (live) store_row_f16(io.d_o, s, 16, d_o);
+    if (keep) store_fm_f16(io.d_o, s, ld, 16, d_o);
     run_layer(S, t_c3, 16, 64);  // dC2act = dO . C3
-    bwd_relu<64>(S, m_c2, io.dc2, s, live);
+    bwd_relu<64>(S, m_c2, io.dc2, s, keep, ld);
     run_layer(S, t_c2, 64, 64);  // dC1act = dC2 . C2
-    bwd_relu<64>(S, m_c1, io.dc1, s, live);
+    bwd_relu<64>(S, m_c1, io.dc1, s, keep, ld);
     run_layer(S, t_c1, 64, 32);  // dCin = dC1 . C1
     float dcin[32];
     tc::tmem_ld32(S.tmem_row, dcin);
@@ -1075,9 +1052,9 @@ __global__ void __launch_bounds__(kBwdSlots* kSlotThreads, 1)
     for (int i = 1; i < 16; ++i) dg[i] = dcin[i - 1];
     tc::st_row8(S.abuf, S.r, 0, 16, dg);
     tc::st_row8(S.abuf, S.r, 8, 16, dg + 8);
-    if (live) store_row_f16(io.dg, s, 16, dg);
+    if (keep) store_fm_f16(io.dg, s, ld, 16, dg);
     run_layer(S, t_g2, 16, 64);  // dH1act = dG . G2
-    bwd_relu<64>(S, m_h1, io.dh1, s, live);
+    bwd_relu<64>(S, m_h1, io.dh1, s, keep, ld);
     run_layer(S, t_g1, 64, 32);  // dX0 = dH1 . G1
     float dfx[32];
     tc::tmem_ld32(S.tmem_row, dfx);
@@ -1293,9 +1270,12 @@ __global__ void __launch_bounds__(kDBwdSlots* kDeformSlotThreads, 1)
       } else {
         tc::tmem_st8(S.a, h);
       }
-      if (live) {
-        reinterpret_cast<uint4*>(d_o_out + s * 16)[0] = make_uint4(h[0], h[1], h[2], h[3]);
-        reinterpret_cast<uint4*>(d_o_out + s * 16)[1] = make_uint4(h[4], h[5], h[6], h[7]);
+      if (s < capacity) {  // feature-major (16, capacity); dead lanes write zeros
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          d_o_out[(int64_t)(2 * i) * capacity + s] = __ushort_as_half((uint16_t)(h[i] & 0xffffu));
+          d_o_out[(int64_t)(2 * i + 1) * capacity + s] = __ushort_as_half((uint16_t)(h[i] >> 16));
+        }
       }
     }
     // the 4 layers' ReLU bits for this half, fetched once per tile
@@ -1307,8 +1287,9 @@ __global__ void __launch_bounds__(kDBwdSlots* kDeformSlotThreads, 1)
         mk[l] = (uint64_t)v.x | (uint64_t)v.y << 32;
       }
     }
-    // dpre1..4 feature-major: (512, capacity), row = layer * 128 + column
-    __half* dp = live ? dpre + s : nullptr;
+    // dpre1..4 feature-major: (512, capacity), row = layer * 128 + column; dead lanes
+    // of the tile (mask 0) write zeros, read by the dW GEMMs' last K tile
+    __half* dp = s < capacity ? dpre + s : nullptr;
     const int64_t L = 128 * capacity;
     ts_layer(S, smem + t5, 16, 128);  // dh4 = d_o . W5
     ts_bwd_mask128(S, mk[3], dp ? dp + 3 * L : nullptr, capacity);
@@ -1421,52 +1402,84 @@ unsigned persistent_grid(int64_t capacity, int slots) {
   return (unsigned)(g < 1 ? 1 : g);
 }
 
+// Scratch of the training forward (cf_field_desc.train), S = capacity: the fp16
+// features feature-major for the backward and the dW GEMMs, then the fp32 working
+// set of the 32-bit forward. Offsets in bytes; S % 8 == 0 keeps every block 16-byte
+// aligned (TMA rows, float4).
+struct TrainLayout {
+  int64_t cfeat16, dfeat16, xc, dfeat32, cfeat32, total;
+};
+inline TrainLayout train_layout(int64_t S) {
+  TrainLayout L;
+  L.cfeat16 = 0;               // (32, S) fp16 canonical features
+  L.dfeat16 = S * 64;          // (33, S) fp16 deformation features + a row of ones
+  L.xc = L.dfeat16 + S * 66;   // (S) float4 canonical positions
+  L.dfeat32 = L.xc + S * 16;   // (S, 32) fp32 deformation features
+  L.cfeat32 = L.dfeat32 + S * 128;  // (S, 32) fp32 canonical features
+  L.total = L.cfeat32 + S * 128;
+  return L;
+}
+
 // "fp32" precision mode of cf_field_stage: fp32 tables (the deformation grid's fp32
 // parameters, not its fp16 copy), fp32 features, split-fp16 MLPs
 int field_stage_precise(const cf_field_desc* FD, const cf_march_out* S, const double* dirs, const float* xu_f,
                         float* out_f, void* scratch, int stage, cudaStream_t st) {
   auto run = [&](int s) { return stage < 0 || stage == s; };
   const int64_t cap = S->capacity;
-  if (FD->save_h) {
+  if (FD->train) {
     // training forward at 32-bit semantics (fp32 tables and features, split-fp16 MMAs):
     // xc, sigma and rgb are the 32-bit field's (the L1 depth term's sign and the
     // spatial gradient dL/dxc are evaluated where the SPEC's field is), plus the fp16
-    // saves the fp16 backward consumes. Scratch: cfeat16 (64 B) | dfeat16 (64 B) |
-    // xc (16 B) | dfeat32 (128 B) | cfeat32 (128 B) per sample (the fp16 layout first).
-    if (!FD->has_deform || !FD->save_o || !FD->save_mask)
-      return cf::fail(CF_E_BAD_ARG, "cf_field_forward: training saves need the human field, save_o and save_mask");
-    uint4* cfeat = reinterpret_cast<uint4*>(scratch);
-    uint4* dfeat16 = cfeat + cap * 4;
-    float4* xc = reinterpret_cast<float4*>(dfeat16 + cap * 4);
-    float4* dfeat32 = xc + cap;
-    const unsigned hgrid = cf::grid_for(cap, 128, 16);
+    // feature-major saves the fp16 backward and the dW GEMMs consume (train_layout)
+    if (cap % 8 != 0) return cf::fail(CF_E_BAD_ARG, "cf_field_forward: training needs capacity % 8 == 0");
+    if (FD->has_deform && (!FD->save_h || !FD->save_o || !FD->save_mask))
+      return cf::fail(CF_E_BAD_ARG, "cf_field_forward: training the human field needs save_h, save_o, save_mask");
+    const TrainLayout TL = train_layout(cap);
+    uint8_t* sb = static_cast<uint8_t*>(scratch);
+    __half* cfeat16 = reinterpret_cast<__half*>(sb + TL.cfeat16);
+    float4* cfeat32 = reinterpret_cast<float4*>(sb + TL.cfeat32);
     const float4* xu = reinterpret_cast<const float4*>(xu_f);
-    if (run(0))
-      cf::launch_pdl(hash_f16_kernel<4, 8, 2, 1, float, true>, hgrid, 128, 0, st, FD->dgrid,
-                     reinterpret_cast<const float*>(FD->dtable), xu, S->counters, cap, reinterpret_cast<uint4*>(dfeat32));
-    if (run(1)) {
-      const int smem = 2 * kDeformW;
-      CF_CHECK_CUDA(cudaFuncSetAttribute(deform_mlp_prec_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      cf::launch_pdl(deform_mlp_prec_kernel<true>, persistent_grid(cap, kPrecDeformSlots),
-                     kPrecDeformSlots * kDeformSlotThreads, smem, st, FD->wblob, FD->wblob_lo, FD->dbias,
-                     FD->delta_scale, FD->inv_side, xu, static_cast<const float4*>(dfeat32), S->counters, cap, xc,
-                     reinterpret_cast<__half*>(FD->save_h), reinterpret_cast<float4*>(FD->save_o), FD->save_mask,
-                     dfeat16);
+    const float4* xcan = xu;
+    const unsigned hgrid = cf::grid_for(cap, 128, 16);
+    if (FD->has_deform) {
+      float4* xc = reinterpret_cast<float4*>(sb + TL.xc);
+      float4* dfeat32 = reinterpret_cast<float4*>(sb + TL.dfeat32);
+      if (run(0))
+        cf::launch_pdl(hash_f16_kernel<4, 8, 2, 1, float, true>, hgrid, 128, 0, st, FD->dgrid,
+                       reinterpret_cast<const float*>(FD->dtable), xu, S->counters, cap,
+                       reinterpret_cast<uint4*>(dfeat32));
+      if (run(1)) {
+        const int smem = 2 * kDeformW;
+        CF_CHECK_CUDA(cudaFuncSetAttribute(deform_mlp_prec_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        cf::launch_pdl(deform_mlp_prec_kernel<true>, persistent_grid(cap, kPrecDeformSlots),
+                       kPrecDeformSlots * kDeformSlotThreads, smem, st, FD->wblob, FD->wblob_lo, FD->dbias,
+                       FD->delta_scale, FD->inv_side, xu, static_cast<const float4*>(dfeat32), S->counters, cap, xc,
+                       reinterpret_cast<__half*>(FD->save_h), reinterpret_cast<float4*>(FD->save_o), FD->save_mask,
+                       reinterpret_cast<__half*>(sb + TL.dfeat16));
+      }
+      xcan = xc;
     }
-    float4* cfeat32 = dfeat32 + cap * 8;
-    if (run(2))
-      cf::launch_pdl(hash_f16_kernel<2, 16, 4, 1, float, true>, hgrid, 128, 0, st, FD->cgrid,
-                     reinterpret_cast<const float*>(FD->ctable), static_cast<const float4*>(xc), S->counters, cap,
-                     reinterpret_cast<uint4*>(cfeat32));
+    if (run(2)) {
+      if (FD->has_deform)
+        cf::launch_pdl(hash_f16_kernel<2, 16, 4, 1, float, true>, hgrid, 128, 0, st, FD->cgrid,
+                       reinterpret_cast<const float*>(FD->ctable), xcan, S->counters, cap,
+                       reinterpret_cast<uint4*>(cfeat32));
+      else
+        cf::launch_pdl(hash_f16_kernel<2, 16, 4, 4, float, true>, cf::grid_for(cap * 4, 128, 16), 128, 0, st,
+                       FD->cgrid, reinterpret_cast<const float*>(FD->ctable), xcan, S->counters, cap,
+                       reinterpret_cast<uint4*>(cfeat32));
+    }
     if (run(3)) {
+      const int off = FD->has_deform ? kDeformW : 0;
       const int csmem = 2 * kColorW;
       CF_CHECK_CUDA(cudaFuncSetAttribute(color_mlp_prec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, csmem));
       cf::launch_pdl(color_mlp_prec_kernel, persistent_grid(cap, kColorPrecSlots), kColorPrecSlots * kSlotThreads,
-                     csmem, st, FD->wblob + kDeformW, FD->wblob_lo + kDeformW, xu, static_cast<const float4*>(cfeat32),
-                     S->records, dirs, S->counters, cap, reinterpret_cast<float4*>(out_f), cfeat);
+                     csmem, st, FD->wblob + off, FD->wblob_lo + off, xu, static_cast<const float4*>(cfeat32),
+                     S->records, dirs, S->counters, cap, reinterpret_cast<float4*>(out_f), cfeat16);
     }
     return cf::check_launch("cf_field_forward (training)");
   }
+  if (FD->save_h) return cf::fail(CF_E_BAD_ARG, "cf_field_forward: saves are a training-mode (train = 1) output");
   const float4* xu = reinterpret_cast<const float4*>(xu_f);
   float4* out = reinterpret_cast<float4*>(out_f);
   float4* cfeat = reinterpret_cast<float4*>(scratch);  // (cap, 32) fp32
@@ -1485,7 +1498,7 @@ int field_stage_precise(const cf_field_desc* FD, const cf_march_out* S, const do
                      kPrecDeformSlots * kDeformSlotThreads, smem, st, FD->wblob, FD->wblob_lo, FD->dbias,
                      FD->delta_scale, FD->inv_side, xu, static_cast<const float4*>(dfeat), S->counters, cap, xc,
                      static_cast<__half*>(nullptr), static_cast<float4*>(nullptr), static_cast<uint32_t*>(nullptr),
-                     static_cast<uint4*>(nullptr));
+                     static_cast<__half*>(nullptr));
     }
     xcan = xc;
   }
@@ -1504,7 +1517,7 @@ int field_stage_precise(const cf_field_desc* FD, const cf_march_out* S, const do
     CF_CHECK_CUDA(cudaFuncSetAttribute(color_mlp_prec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, csmem));
     cf::launch_pdl(color_mlp_prec_kernel, persistent_grid(cap, kColorPrecSlots), kColorPrecSlots * kSlotThreads, csmem,
                    st, FD->wblob + off, FD->wblob_lo + off, xu, static_cast<const float4*>(cfeat), S->records, dirs,
-                   S->counters, cap, out, static_cast<uint4*>(nullptr));
+                   S->counters, cap, out, static_cast<__half*>(nullptr));
   }
   return cf::check_launch("cf_field_forward (precise)");
 }
@@ -1513,12 +1526,24 @@ int field_stage_precise(const cf_field_desc* FD, const cf_march_out* S, const do
 
 extern "C" {
 
+int cf_field_train_layout(int64_t capacity, int64_t* offsets) {
+  if (capacity < 0 || !offsets) return cf::fail(CF_E_BAD_ARG, "cf_field_train_layout: bad args");
+  const TrainLayout L = train_layout(capacity);
+  offsets[0] = L.cfeat16;
+  offsets[1] = L.dfeat16;
+  offsets[2] = L.xc;
+  offsets[3] = L.dfeat32;
+  offsets[4] = L.cfeat32;
+  offsets[5] = L.total;
+  return CF_OK;
+}
+
 int cf_field_scratch_bytes(const cf_field_desc* FD, int64_t capacity, int64_t* bytes) {
   if (!FD || !bytes || capacity < 0) return cf::fail(CF_E_BAD_ARG, "cf_field_scratch_bytes: bad args");
   // cfeat (64 B fp16 / 128 B fp32) [+ dfeat (same) + xc (16 B)] per sample
   const int64_t feat = FD->precise ? 128 : 64;
   *bytes = capacity * (feat + (FD->has_deform ? feat + 16 : 0));
-  if (FD->has_deform && FD->save_h) *bytes = capacity * (64 + 64 + 16 + 128 + 128);  // training layout
+  if (FD->train) *bytes = train_layout(capacity).total;
   return CF_OK;
 }
 
@@ -1532,6 +1557,7 @@ int cf_color_backward(const cf_field_desc* FD, const uint8_t* wt_blob, const cf_
                       void* stream) {
   if (!FD || !wt_blob || !S || !dirs || !xu || !grad_out || !scratch || !io || !io->dfeat)
     return cf::fail(CF_E_BAD_ARG, "cf_color_backward: bad args");
+  if (!FD->train) return cf::fail(CF_E_BAD_ARG, "cf_color_backward: needs the training forward's scratch (train = 1)");
   const int64_t cap = S->capacity;
   if (cap == 0) return CF_OK;
   ColorBwdIO o{reinterpret_cast<__half*>(io->h1),  reinterpret_cast<__half*>(io->cin),
@@ -1543,7 +1569,7 @@ int cf_color_backward(const cf_field_desc* FD, const uint8_t* wt_blob, const cf_
   CF_CHECK_CUDA(cudaFuncSetAttribute(color_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const uint8_t* cw = FD->wblob + (FD->has_deform ? kDeformW : 0);
   color_bwd_kernel<<<persistent_grid(cap, kBwdSlots), kBwdSlots * kSlotThreads, smem, cf::as_stream(stream)>>>(
-      cw, wt_blob, reinterpret_cast<const float4*>(xu), reinterpret_cast<const uint4*>(scratch), S->records, dirs,
+      cw, wt_blob, reinterpret_cast<const float4*>(xu), reinterpret_cast<const __half*>(scratch), S->records, dirs,
       reinterpret_cast<const float4*>(grad_out), S->counters, cap, o);
   return cf::check_launch("cf_color_backward");
 }
@@ -1556,8 +1582,9 @@ int cf_field_hash_backward(const cf_field_desc* FD, const cf_march_out* S, const
   if (cap == 0) return CF_OK;
   // the canonical grid saw xc (human: after DeformNet, stored in scratch) or xu (object)
   const float4* x = reinterpret_cast<const float4*>(xu);
+  if (!FD->train) return cf::fail(CF_E_BAD_ARG, "cf_field_hash_backward: needs the training forward's scratch");
   if (FD->has_deform)
-    x = reinterpret_cast<const float4*>(reinterpret_cast<const uint4*>(scratch) + cap * 8);
+    x = reinterpret_cast<const float4*>(static_cast<const uint8_t*>(scratch) + train_layout(cap).xc);
   if (dx_out)
     hash_bwd_dx_kernel<2, 16><<<cf::grid_for(cap, 128, 16), 128, 0, cf::as_stream(stream)>>>(
         FD->cgrid, reinterpret_cast<const float*>(FD->ctable), x, dfeat, S->counters, cap, table_grad,
@@ -1607,11 +1634,12 @@ int cf_field_stage(const cf_field_desc* FD, const cf_march_out* S, const double*
     return cf::fail(CF_E_BAD_ARG, "cf_field_forward: grids must be 16x F2 (canonical) and 8x F4 (deform)");
   if (FD->w_bytes != (FD->has_deform ? kDeformW : 0) + kColorW)
     return cf::fail(CF_E_BAD_ARG, "cf_field_forward: weight blob size mismatch");
-  if (FD->precise && !FD->wblob_lo) return cf::fail(CF_E_BAD_ARG, "cf_field_forward: precise mode needs wblob_lo");
+  if ((FD->precise || FD->train) && !FD->wblob_lo)
+    return cf::fail(CF_E_BAD_ARG, "cf_field_forward: precise / training mode needs wblob_lo");
   cudaStream_t st = cf::as_stream(stream);
   const int64_t cap = S->capacity;
   if (cap == 0) return CF_OK;
-  if (FD->precise) return field_stage_precise(FD, S, dirs, xu_f, out_f, scratch, stage, st);
+  if (FD->precise || FD->train) return field_stage_precise(FD, S, dirs, xu_f, out_f, scratch, stage, st);
   const float4* xu = reinterpret_cast<const float4*>(xu_f);
   float4* out = reinterpret_cast<float4*>(out_f);
   uint4* cfeat = reinterpret_cast<uint4*>(scratch);
@@ -1624,13 +1652,9 @@ int cf_field_stage(const cf_field_desc* FD, const cf_march_out* S, const double*
       cf::launch_pdl(hash_f16_kernel<4, 8, 2, 1, __half>, hgrid, 128, 0, st, FD->dgrid, reinterpret_cast<const __half*>(FD->dtable), xu, S->counters, cap, dfeat);
     if (run(1)) {
       const int smem = kDeformW + kDeformA;
-      const bool save = FD->save_h != nullptr;
-      if (save && (!FD->save_o || !FD->save_mask))
-        return cf::fail(CF_E_BAD_ARG, "cf_field_forward: save_h needs save_o and save_mask");
-      auto kern = save ? deform_mlp_kernel<true> : deform_mlp_kernel<false>;
-      CF_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      cf::launch_pdl(kern, persistent_grid(cap, kDeformSlots), kDeformSlots * kDeformSlotThreads, smem, st, FD->wblob, FD->dbias, FD->delta_scale, FD->inv_side, xu, dfeat, S->counters, cap, xc,
-          reinterpret_cast<__half*>(FD->save_h), reinterpret_cast<float4*>(FD->save_o), FD->save_mask);
+      CF_CHECK_CUDA(cudaFuncSetAttribute(deform_mlp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      cf::launch_pdl(deform_mlp_kernel, persistent_grid(cap, kDeformSlots), kDeformSlots * kDeformSlotThreads, smem,
+                     st, FD->wblob, FD->dbias, FD->delta_scale, FD->inv_side, xu, dfeat, S->counters, cap, xc);
     }
     xcan = xc;
   }

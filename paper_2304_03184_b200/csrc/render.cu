@@ -833,8 +833,11 @@ __global__ void composite_final_kernel(cf_march_desc M, cf_march_out F, const fl
 __global__ void composite_bwd_kernel(cf_march_desc M, cf_march_out F, const float4* __restrict__ field,
                                      float t_term, const float* __restrict__ gt_rgb,
                                      const float* __restrict__ gt_depth, const uint8_t* __restrict__ mask,
-                                     float lambda, float inv_nm, float inv_nd, float gscale,
+                                     float lambda, const float* __restrict__ norm,
                                      float4* __restrict__ grad, float* __restrict__ loss) {
+  // normalisers from the device (cf_train_norms: the frame's masked / depth-valid ray
+  // counts, summed over ranks) and the field's power-of-two loss scale
+  const float inv_nm = norm[0], inv_nd = norm[1], gscale = norm[2], wl = norm[3];
   float lc = 0.f, ld = 0.f;
   for (int64_t ray = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ray < M.n_rays;
        ray += (int64_t)gridDim.x * blockDim.x) {
@@ -860,13 +863,13 @@ __global__ void composite_bwd_kernel(cf_march_desc M, cf_march_out F, const floa
     if (mask[ray]) {
       for (int c = 0; c < 3; ++c) {
         const float e = S[c] - gt_rgb[3 * ray + c];
-        lc += e * e * inv_nm;
+        lc += e * e * inv_nm * wl;
         gv[c] = 2.0f * e * inv_nm * gscale;
       }
       const float gd = gt_depth[ray];
       if (gd > 0.f) {
         const float O = fmaxf(S[4], 1e-6f), depth = S[3] / O, e = depth - gd;
-        ld += fabsf(e) * inv_nd;
+        ld += fabsf(e) * inv_nd * wl;
         const float gdep = lambda * inv_nd * gscale * (e > 0.f ? 1.f : (e < 0.f ? -1.f : 0.f));
         gv[3] = gdep / O;
         gv[4] = S[4] > 1e-6f ? -gdep * S[3] / (S[4] * S[4]) : 0.f;
@@ -921,7 +924,7 @@ __device__ __forceinline__ double u01(uint64_t seed, uint64_t ray, uint64_t j) {
 // pixel list (u01 of (seed, i)); their targets are gathered from the frame's
 // HBM-resident images and their exact camera rays generated (pixel_dir).
 __global__ void keyframe_rays_kernel(cf_camera cam, const int* __restrict__ fg, int64_t n_fg, int64_t n,
-                                     uint64_t seed, const float* __restrict__ rgb, const float* __restrict__ depth,
+                                     uint64_t seed, const uint64_t* __restrict__ seed_off, const float* __restrict__ rgb, const float* __restrict__ depth,
                                      const uint8_t* __restrict__ mask_h, const uint8_t* __restrict__ mask_o,
                                      int* __restrict__ pix_out, double* __restrict__ dirs, float* __restrict__ rgb_o,
                                      float* __restrict__ depth_o, uint8_t* __restrict__ mh_o,
@@ -929,6 +932,7 @@ __global__ void keyframe_rays_kernel(cf_camera cam, const int* __restrict__ fg, 
   __shared__ double s_cam[13];
   load_camera(cam, s_cam);
   const ExactDiv by_fx(s_cam[9]), by_fy(s_cam[10]);
+  if (seed_off) seed += *seed_off;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t k = min((int64_t)(u01(seed, (uint64_t)i, 0) * (double)n_fg), n_fg - 1);
     const int px = fg[k];
@@ -952,7 +956,9 @@ __global__ void keyframe_rays_kernel(cf_camera cam, const int* __restrict__ fg, 
 __global__ void __launch_bounds__(128) train_sample_kernel(cf_march_desc M, const float* __restrict__ gt_depth,
                                                            const uint8_t* __restrict__ mask, int n_guided,
                                                            int n_uniform, int n_empty, double sigma_d,
-                                                           uint64_t seed, cf_march_out F, double* __restrict__ t_out) {
+                                                           uint64_t seed, const uint64_t* __restrict__ seed_off,
+                                                           int64_t ray0, cf_march_out F, double* __restrict__ t_out) {
+  if (seed_off) seed += *seed_off;
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < M.n_rays; base += (int64_t)gridDim.x * blockDim.x) {
     const int64_t ray = base + threadIdx.x;
     const bool live = ray < M.n_rays && mask[ray] != 0;
@@ -975,7 +981,7 @@ __global__ void __launch_bounds__(128) train_sample_kernel(cf_march_desc M, cons
     }
     if (c == 0) continue;
     auto strat = [&](double lo, double hi, int n, int j, int slot) {
-      return x_add(lo, x_mul(x_div((double)j + u01(seed, ray, slot), (double)n), x_sub(hi, lo)));
+      return x_add(lo, x_mul(x_div((double)j + u01(seed, (uint64_t)(ray0 + ray), slot), (double)n), x_sub(hi, lo)));
     };
     if (!guided) {
       for (int j = 0; j < n_empty; ++j) {
@@ -1218,7 +1224,7 @@ int cf_composite(const cf_march_desc* M, const cf_march_out* F, const float* fie
 }
 
 int cf_keyframe_rays(const cf_camera* cam, const int* fg_pixels, int64_t n_fg, int64_t n_rays, uint64_t seed,
-                     const float* rgb, const float* depth, const uint8_t* mask_h, const uint8_t* mask_o, int* pix_out,
+                     const uint64_t* seed_offset, const float* rgb, const float* depth, const uint8_t* mask_h, const uint8_t* mask_o, int* pix_out,
                      double* dirs, float* rgb_out, float* depth_out, uint8_t* mask_h_out, uint8_t* mask_o_out,
                      void* stream) {
   if (!cam || !fg_pixels || n_fg < 1 || n_rays < 0 || !rgb || !depth || !mask_h || !mask_o || !dirs || !rgb_out ||
@@ -1226,13 +1232,14 @@ int cf_keyframe_rays(const cf_camera* cam, const int* fg_pixels, int64_t n_fg, i
     return cf::fail(CF_E_BAD_ARG, "cf_keyframe_rays: bad args");
   if (n_rays == 0) return CF_OK;
   keyframe_rays_kernel<<<cf::grid_for(n_rays, 256, 4), 256, 0, cf::as_stream(stream)>>>(
-      *cam, fg_pixels, n_fg, n_rays, seed, rgb, depth, mask_h, mask_o, pix_out, dirs, rgb_out, depth_out, mask_h_out,
+      *cam, fg_pixels, n_fg, n_rays, seed, seed_offset, rgb, depth, mask_h, mask_o, pix_out, dirs, rgb_out, depth_out, mask_h_out,
       mask_o_out);
   return cf::check_launch("cf_keyframe_rays");
 }
 
 int cf_train_sample(const cf_march_desc* M, const float* gt_depth, const uint8_t* mask, int n_guided, int n_uniform,
-                    int n_empty, double sigma_d, uint64_t seed, const cf_march_out* F, double* t_out, void* stream) {
+                    int n_empty, double sigma_d, uint64_t seed, const uint64_t* seed_offset, int64_t ray_id0,
+                    const cf_march_out* F, double* t_out, void* stream) {
   if (!M || !F || !gt_depth || !mask || !t_out || n_guided < 1 || n_uniform < 1 || n_empty < 1 ||
       n_guided + n_uniform > 128 || n_empty > 128 || n_guided > 32)
     return cf::fail(CF_E_BAD_ARG, "cf_train_sample: bad args");
@@ -1240,20 +1247,20 @@ int cf_train_sample(const cf_march_desc* M, const float* gt_depth, const uint8_t
   cf::fill_list(st, {{F->counters, 0u, 4}});
   if (M->n_rays == 0) return CF_OK;
   train_sample_kernel<<<cf::grid_for(M->n_rays, 128, 8), 128, 0, st>>>(*M, gt_depth, mask, n_guided, n_uniform,
-                                                                        n_empty, sigma_d, seed, *F, t_out);
+                                                                        n_empty, sigma_d, seed, seed_offset, ray_id0, *F,
+                                                                        t_out);
   return cf::check_launch("cf_train_sample");
 }
 
 int cf_loss_composite_bwd(const cf_march_desc* M, const cf_march_out* F, const float* field, float t_term,
                           const float* gt_rgb, const float* gt_depth, const uint8_t* mask, float lambda_depth,
-                          float inv_n_color, float inv_n_depth, float grad_scale, float* grad, float* loss,
-                          void* stream) {
-  if (!M || !F || !field || !gt_rgb || !gt_depth || !mask || !grad)
+                          const float* norm, float* grad, float* loss, void* stream) {
+  if (!M || !F || !field || !gt_rgb || !gt_depth || !mask || !grad || !norm)
     return cf::fail(CF_E_BAD_ARG, "cf_loss_composite_bwd: bad args");
   if (M->n_rays == 0) return CF_OK;
   composite_bwd_kernel<<<cf::grid_for(M->n_rays, 128, 8), 128, 0, cf::as_stream(stream)>>>(
-      *M, *F, reinterpret_cast<const float4*>(field), t_term, gt_rgb, gt_depth, mask, lambda_depth, inv_n_color,
-      inv_n_depth, grad_scale, reinterpret_cast<float4*>(grad), loss);
+      *M, *F, reinterpret_cast<const float4*>(field), t_term, gt_rgb, gt_depth, mask, lambda_depth, norm,
+      reinterpret_cast<float4*>(grad), loss);
   return cf::check_launch("cf_loss_composite_bwd");
 }
 

@@ -156,6 +156,251 @@ __global__ void __launch_bounds__(128, 1) gemm_kmajor_kernel(const __grid_consta
   if (warp == 2) tc::tmem_free<N < 32 ? 32 : N>(tmem_base);
 }
 
+// ---------------------------------------------------------------- grouped dW, K on the device
+// Up to kMaxDw weight-gradient problems of one field in ONE launch (blockIdx.y =
+// problem): C_p[m_p x n_p] += A_p[m_p x K] B_p[n_p x K]^T, both operands K-major
+// fp16 (feature-major saves, K = samples), K = min(*count, capacity) read on the
+// device — no host sync, and the launch is graph-capturable. Same pipeline as
+// gemm_kmajor_kernel with runtime shapes: the A box is always 128 rows (TMA fills
+// rows >= m_p with zeros, the MMA is M = 128), the B box n_mma rows (n_p rounded up
+// to 16), the epilogue adds only rows < m_p and columns < n_p.
+constexpr int kMaxDw = 10;
+struct DwProb {
+  CUtensorMap a, b;
+  float* C;
+  int ldc, m, n, n_mma;
+};
+struct DwGroup {
+  DwProb p[kMaxDw];
+  const int* count;
+  int64_t capacity;
+};
+
+__global__ void __launch_bounds__(128, 1) dw_grouped_kernel(const __grid_constant__ DwGroup G) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t full[kGStages], empty[kGStages], done;
+  __shared__ uint32_t tmem_base;
+  const DwProb& P = G.p[blockIdx.y];
+  const int N = P.n_mma;
+  constexpr int kStageA = 128 * kGKT * 2, kStage = kStageA + 128 * kGKT * 2;
+  const uint32_t tx = (uint32_t)(kStageA + N * kGKT * 2);
+  const int tid = threadIdx.x, warp = tid / 32;
+  const int64_t K = min((int64_t)*G.count, G.capacity);
+  const int64_t T = (K + kGKT - 1) / kGKT;
+  const int64_t per = (T + gridDim.x - 1) / gridDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * per, nt = max((int64_t)0, min(per, T - t0));
+  if (nt == 0) return;
+  if (tid == 0) {
+    for (int q = 0; q < kGStages; ++q) {
+      tc::bar_init(&full[q], 1);
+      tc::bar_init(&empty[q], 1);
+    }
+    tc::bar_init(&done, 1);
+    tc::bar_fence_init();
+  }
+  if (warp == 2) tc::tmem_alloc<128>(&tmem_base);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t sbase = tc::smem_u32(smem);
+  if (tid == 0) {
+    for (int64_t i = 0; i < nt; ++i) {
+      const int st = (int)(i % kGStages);
+      if (i >= kGStages) tc::bar_wait(&empty[st], (uint32_t)(((i / kGStages) - 1) & 1));
+      bar_expect_tx(&full[st], tx);
+      const int k0 = (int)((t0 + i) * kGKT);
+      const uint32_t sa = sbase + st * kStage, sb = sa + kStageA;
+      tma_load_2d(sa, &P.a, k0, 0, &full[st]);
+      tma_load_2d(sb, &P.b, k0, 0, &full[st]);
+    }
+  } else if (tid == 32) {
+    const uint32_t idesc = tc::idesc_f16(128, N);
+    for (int64_t i = 0; i < nt; ++i) {
+      const int st = (int)(i % kGStages);
+      tc::bar_wait(&full[st], (uint32_t)((i / kGStages) & 1));
+      tc::fence_after();
+      const uint32_t sa = sbase + st * kStage, sb = sa + kStageA;
+#pragma unroll
+      for (int ks = 0; ks < kGKT / 16; ++ks)
+        tc::mma_f16(tmem_base, sdesc_sw128(sa + ks * 32), sdesc_sw128(sb + ks * 32), idesc,
+                    (i > 0 || ks > 0) ? 1u : 0u);
+      tc::mma_commit(&empty[st]);
+    }
+    tc::mma_commit(&done);
+  }
+  tc::bar_wait(&done, 0);
+  __syncwarp();
+  tc::fence_after();
+  const int row = warp * 32 + (tid & 31);
+#pragma unroll 1
+  for (int c0 = 0; c0 < N; c0 += 32) {  // warp-uniform: tcgen05.ld is warp-collective
+    float v[32];
+    tc::tmem_ld32(tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+    if (row < P.m) {
+      float* dst = P.C + (int64_t)row * P.ldc + c0;
+      const int nc = min(32, P.n - c0);
+#pragma unroll
+      for (int c = 0; c < 32; ++c)
+        if (c < nc) atomicAdd(dst + c, v[c]);
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 2) tc::tmem_free<128>(tmem_base);
+}
+
+// ---------------------------------------------------------------- step control on the device
+// Masked / depth-valid ray counts of every key frame of the step: one CTA per frame
+// (frame f's rays at f * stride); counts (F, 4) = [n_m human, n_d human, n_m object,
+// n_d object]. Exact integer sums, written (no accumulation: no reset needed).
+__global__ void __launch_bounds__(1024) train_counts_kernel(const uint8_t* __restrict__ mask_h,
+                                                            const uint8_t* __restrict__ mask_o,
+                                                            const float* __restrict__ depth, int64_t n_rays,
+                                                            int64_t stride, int* __restrict__ counts) {
+  const int64_t base = (int64_t)blockIdx.x * stride;
+  int c[4] = {0, 0, 0, 0};
+  for (int64_t i = threadIdx.x; i < n_rays; i += blockDim.x) {
+    const bool h = mask_h[base + i] != 0, o = mask_o[base + i] != 0, d = depth[base + i] > 0.f;
+    c[0] += h;
+    c[1] += h && d;
+    c[2] += o;
+    c[3] += o && d;
+  }
+  __shared__ int red[32][4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    for (int o = 16; o > 0; o >>= 1) c[q] += __shfl_xor_sync(0xffffffffu, c[q], o);
+  if ((threadIdx.x & 31) == 0)
+    for (int q = 0; q < 4; ++q) red[threadIdx.x / 32][q] = c[q];
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    int t = 0;
+    for (int w = 0; w < (int)(blockDim.x / 32); ++w) t += red[w][threadIdx.x];
+    counts[blockIdx.x * 4 + threadIdx.x] = t;
+  }
+}
+
+// Per-step normalisers from the (rank-summed) counts: norms (2 fields, F, 3) =
+// [1/max(n_m,1), 1/max(n_d,1), loss scale]; the loss scale of a field is the power of
+// two 2^floor(log2(min over its frames with n_m > 0 of n_m)) (the per-sample
+// gradients of the 1/n-normalised loss are O(1/n): scaled they sit inside the fp16
+// range of the backward operands); adam_scale[q] = 1 / (F * scale_q) divides it and
+// the mean over frames out; stats (2 fields x 2) zeroed; ++step (Adam's bias
+// correction). One thread per field.
+__global__ void train_norms_kernel(const int* __restrict__ counts, int n_frames, float* __restrict__ norms,
+                                   float* __restrict__ adam_scale, float* __restrict__ stats, int* __restrict__ step,
+                                   uint64_t* __restrict__ seed) {
+  const int q = threadIdx.x;
+  if (q >= 2) return;
+  int mn = 0;
+  for (int f = 0; f < n_frames; ++f) {
+    const int m = counts[f * 4 + 2 * q];
+    if (m > 0 && (mn == 0 || m < mn)) mn = m;
+  }
+  const float scale = mn > 0 ? ldexpf(1.0f, 31 - __clz(mn)) : 1.0f;
+  for (int f = 0; f < n_frames; ++f) {
+    const int m = counts[f * 4 + 2 * q], d = counts[f * 4 + 2 * q + 1];
+    float* o = norms + ((int64_t)q * n_frames + f) * 4;
+    o[0] = 1.0f / (float)max(m, 1);
+    o[1] = 1.0f / (float)max(d, 1);
+    o[2] = scale;
+    o[3] = 1.0f / (float)n_frames;  // the reported losses: mean over frames
+  }
+  adam_scale[q] = 1.0f / ((float)n_frames * scale);
+  stats[2 * q] = 0.f;
+  stats[2 * q + 1] = 0.f;
+  __syncwarp(0x3u);
+  if (q == 0) {
+    const int st = *step + 1;
+    *step = st;
+    if (seed) *seed = (uint64_t)st * 0x9E3779B97F4A7C15ull;  // the step's sampling seed offset
+  }
+}
+
+// dW of DeformNet layer 1 from the GEMM over [features | 1] (tmp (rows, ldt), columns
+// 0..n_x-1 the feature part, column n_x = sum_s dpre1): G[:, :n_x] += tmp[:, :n_x],
+// G[:, n_x + j] += tmp[:, n_x] * theta[j] (theta is the same for every sample of the
+// frame); tmp is zeroed for the next frame.
+__global__ void dw_pose_cols_kernel(float* __restrict__ tmp, int rows, int ldt, int n_x,
+                                    const float* __restrict__ theta, int n_theta, float* __restrict__ G, int ldg) {
+  const int r = blockIdx.x;
+  if (r >= rows) return;
+  const float cs = tmp[(int64_t)r * ldt + n_x];
+  for (int c = threadIdx.x; c < n_x + n_theta; c += blockDim.x)
+    G[(int64_t)r * ldg + c] += c < n_x ? tmp[(int64_t)r * ldt + c] : cs * theta[c - n_x];
+  __syncthreads();
+  for (int c = threadIdx.x; c <= n_x; c += blockDim.x) tmp[(int64_t)r * ldt + c] = 0.f;
+}
+
+// Multi-tensor Adam: every trained tensor of the step in one launch (blockIdx.y =
+// tensor). Bias corrections from the device step counter, the gradient scale from
+// the device (cf_train_norms), grads zeroed after use (the next step accumulates
+// into them), optional fp16 copy of the updated parameters.
+constexpr int kMaxAdam = 24;
+struct AdamT {
+  float* p;
+  float* g;
+  float* m;
+  float* v;
+  __half* p16;
+  int64_t n;
+  float lr;
+  int scale_idx;
+};
+struct AdamGroup {
+  AdamT t[kMaxAdam];
+  const int* step;
+  const float* scale;
+  float b1, b2, eps;
+};
+
+__global__ void adam_multi_kernel(const __grid_constant__ AdamGroup A) {
+  const AdamT& T = A.t[blockIdx.y];
+  const int step = *A.step;
+  const float c1 = 1.0f / (1.0f - powf(A.b1, (float)step)), c2 = 1.0f / (1.0f - powf(A.b2, (float)step));
+  const float gs = A.scale ? A.scale[T.scale_idx] : 1.0f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < T.n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float gi = T.g[i] * gs;
+    const float mi = A.b1 * T.m[i] + (1.f - A.b1) * gi;
+    const float vi = A.b2 * T.v[i] + (1.f - A.b2) * gi * gi;
+    T.m[i] = mi;
+    T.v[i] = vi;
+    T.g[i] = 0.f;
+    const float p = T.p[i] - T.lr * (mi * c1) / (sqrtf(vi * c2) + A.eps);
+    T.p[i] = p;
+    if (T.p16) T.p16[i] = __float2half_rn(p);
+  }
+}
+
+// Multi-matrix fp32 -> fp16 UMMA canonical repack (forward blobs with their split
+// residual, transposed blobs of the backward) in one launch (blockIdx.y = item).
+// Packed matrix P (rows x cols, padded to 16): P[r][c] = W[r][col0 + c] or, when
+// transposed, W[c][col0 + r] (W row stride ldw).
+constexpr int kMaxPack = 32;
+struct PackItem {
+  const float* w;
+  uint8_t* blob;
+  uint8_t* blob_lo;
+  int rows, cols, ldw, col0, transpose;
+};
+struct PackGroup {
+  PackItem it[kMaxPack];
+};
+
+__global__ void pack_multi_kernel(const __grid_constant__ PackGroup G) {
+  const PackItem& I = G.it[blockIdx.y];
+  const int rp = (I.rows + 15) / 16 * 16, cp = (I.cols + 15) / 16 * 16;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < rp * cp; e += gridDim.x * blockDim.x) {
+    const int r = e / cp, c = e % cp;
+    float x = 0.0f;
+    if (r < I.rows && c < I.cols)
+      x = I.transpose ? I.w[(int64_t)c * I.ldw + I.col0 + r] : I.w[(int64_t)r * I.ldw + I.col0 + c];
+    const __half h = __float2half_rn(x);
+    *reinterpret_cast<__half*>(I.blob + tc::core_offset(r, c, cp)) = h;
+    if (I.blob_lo) *reinterpret_cast<__half*>(I.blob_lo + tc::core_offset(r, c, cp)) = __float2half_rn(x - __half2float(h));
+  }
+}
+
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -169,13 +414,14 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// rows x K fp16, row stride ld elements; boxes of 64 halves (128 B) x rows, 128B swizzle
-bool make_map(CUtensorMap* map, const void* base, int rows, int64_t K, int64_t ld) {
+// rows x K fp16, row stride ld elements; boxes of 64 halves (128 B) x box_rows (default
+// rows; more than rows = zero-filled), 128B swizzle
+bool make_map(CUtensorMap* map, const void* base, int rows, int64_t K, int64_t ld, int box_rows = 0) {
   auto fn = encode_fn();
   if (!fn) return false;
   const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
   const cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
-  const cuuint32_t box[2] = {64, (cuuint32_t)rows};
+  const cuuint32_t box[2] = {64, (cuuint32_t)(box_rows > 0 ? box_rows : rows)};
   const cuuint32_t estr[2] = {1, 1};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -211,6 +457,102 @@ int cf_gemm_kmajor_f16(const void* A, int64_t lda, const void* B, int64_t ldb, i
                          : (n_cols == 64 ? run(gemm_kmajor_kernel<64>, 64) : run(gemm_kmajor_kernel<32>, 32));
   if (rc) return rc;
   return cf::check_launch("cf_gemm_kmajor_f16");
+}
+
+int cf_dw_grouped(const cf_dw_problem* probs, int n, const int* count, int64_t capacity, void* stream) {
+  if (!probs || n < 1 || n > kMaxDw || !count || capacity < 0)
+    return cf::fail(CF_E_BAD_ARG, "cf_dw_grouped: bad args (1..10 problems, count, capacity)");
+  if (capacity == 0) return CF_OK;
+  if (capacity >= (int64_t)1 << 31) return cf::fail(CF_E_BAD_ARG, "cf_dw_grouped: capacity must be < 2^31");
+  DwGroup G{};
+  G.count = count;
+  G.capacity = capacity;
+  for (int i = 0; i < n; ++i) {
+    const cf_dw_problem& q = probs[i];
+    if (!q.A || !q.B || !q.C || q.m < 1 || q.m > 128 || q.n < 1 || q.n > 128 || q.lda < capacity ||
+        q.ldb < capacity || q.ldc < q.n)
+      return cf::fail(CF_E_BAD_ARG, "cf_dw_grouped: problem shape (m, n in 1..128, lda/ldb >= capacity)");
+    if ((q.lda | q.ldb) % 8 != 0 || (reinterpret_cast<uintptr_t>(q.A) | reinterpret_cast<uintptr_t>(q.B)) % 16 != 0)
+      return cf::fail(CF_E_BAD_ARG, "cf_dw_grouped: operands need 16-byte aligned rows");
+    DwProb& P = G.p[i];
+    P.n_mma = (q.n + 15) / 16 * 16;
+    if (!make_map(&P.a, q.A, q.m, capacity, q.lda, 128) || !make_map(&P.b, q.B, q.n, capacity, q.ldb, P.n_mma))
+      return cf::fail(CF_E_CUDA, "cf_dw_grouped: cuTensorMapEncodeTiled failed");
+    P.C = q.C;
+    P.ldc = q.ldc;
+    P.m = q.m;
+    P.n = q.n;
+  }
+  const int64_t T = (capacity + kGKT - 1) / kGKT;
+  const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(T, cf::sm_count()));
+  const int smem = kGStages * 2 * 128 * kGKT * 2;
+  CF_CHECK_CUDA(cudaFuncSetAttribute(dw_grouped_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  dw_grouped_kernel<<<dim3(gx, (unsigned)n), 128, smem, cf::as_stream(stream)>>>(G);
+  return cf::check_launch("cf_dw_grouped");
+}
+
+int cf_train_counts(const uint8_t* mask_h, const uint8_t* mask_o, const float* gt_depth, int64_t n_rays,
+                    int n_frames, int64_t frame_stride, int* counts, void* stream) {
+  if (!mask_h || !mask_o || !gt_depth || !counts || n_rays < 0 || n_frames < 1 || frame_stride < n_rays)
+    return cf::fail(CF_E_BAD_ARG, "cf_train_counts: bad args");
+  train_counts_kernel<<<n_frames, 1024, 0, cf::as_stream(stream)>>>(mask_h, mask_o, gt_depth, n_rays, frame_stride,
+                                                                   counts);
+  return cf::check_launch("cf_train_counts");
+}
+
+int cf_train_norms(const int* counts, int n_frames, float* norms, float* adam_scale, float* stats, int* step,
+                   uint64_t* seed, void* stream) {
+  if (!counts || n_frames < 1 || !norms || !adam_scale || !stats || !step)
+    return cf::fail(CF_E_BAD_ARG, "cf_train_norms: bad args");
+  train_norms_kernel<<<1, 32, 0, cf::as_stream(stream)>>>(counts, n_frames, norms, adam_scale, stats, step, seed);
+  return cf::check_launch("cf_train_norms");
+}
+
+int cf_dw_pose_cols(float* tmp, int rows, int ldt, int n_x, const float* theta, int n_theta, float* G, int ldg,
+                    void* stream) {
+  if (!tmp || !theta || !G || rows < 1 || n_x < 1 || ldt <= n_x || n_theta < 0 || ldg < n_x + n_theta)
+    return cf::fail(CF_E_BAD_ARG, "cf_dw_pose_cols: bad args");
+  dw_pose_cols_kernel<<<rows, 128, 0, cf::as_stream(stream)>>>(tmp, rows, ldt, n_x, theta, n_theta, G, ldg);
+  return cf::check_launch("cf_dw_pose_cols");
+}
+
+int cf_adam_multi(const cf_adam_tensor* ts, int n, float beta1, float beta2, float eps, const int* step,
+                  const float* scale, void* stream) {
+  if (!ts || n < 1 || n > kMaxAdam || !step) return cf::fail(CF_E_BAD_ARG, "cf_adam_multi: bad args (1..24 tensors)");
+  AdamGroup A{};
+  int64_t nmax = 0;
+  for (int i = 0; i < n; ++i) {
+    const cf_adam_tensor& t = ts[i];
+    if (!t.p || !t.g || !t.m || !t.v || t.n < 0 || (scale && t.scale_idx < 0))
+      return cf::fail(CF_E_BAD_ARG, "cf_adam_multi: bad tensor");
+    A.t[i] = AdamT{t.p, t.g, t.m, t.v, reinterpret_cast<__half*>(t.p16), t.n, t.lr, t.scale_idx};
+    nmax = std::max(nmax, t.n);
+  }
+  A.step = step;
+  A.scale = scale;
+  A.b1 = beta1;
+  A.b2 = beta2;
+  A.eps = eps;
+  if (nmax == 0) return CF_OK;
+  const unsigned gx = (unsigned)std::min<int64_t>((nmax + 255) / 256, (int64_t)cf::sm_count() * 8);
+  adam_multi_kernel<<<dim3(gx, (unsigned)n), 256, 0, cf::as_stream(stream)>>>(A);
+  return cf::check_launch("cf_adam_multi");
+}
+
+int cf_pack_multi(const cf_pack_item* items, int n, void* stream) {
+  if (!items || n < 1 || n > kMaxPack) return cf::fail(CF_E_BAD_ARG, "cf_pack_multi: bad args (1..32 items)");
+  PackGroup G{};
+  int emax = 0;
+  for (int i = 0; i < n; ++i) {
+    const cf_pack_item& q = items[i];
+    if (!q.w || !q.blob || q.rows < 1 || q.cols < 1 || q.col0 < 0 ||
+        (q.transpose ? q.ldw < q.col0 + q.rows : q.ldw < q.col0 + q.cols))
+      return cf::fail(CF_E_BAD_ARG, "cf_pack_multi: bad item");
+    G.it[i] = PackItem{q.w, q.blob, q.blob_lo, q.rows, q.cols, q.ldw, q.col0, q.transpose};
+    emax = std::max(emax, (q.rows + 15) / 16 * 16 * ((q.cols + 15) / 16 * 16));
+  }
+  pack_multi_kernel<<<dim3((unsigned)((emax + 255) / 256), (unsigned)n), 256, 0, cf::as_stream(stream)>>>(G);
+  return cf::check_launch("cf_pack_multi");
 }
 
 int cf_adam(float* p, const float* g, float* m, float* v, int64_t n, float lr, float beta1, float beta2, float eps,

@@ -286,6 +286,16 @@ def gather_row_shards(part, width: int, height: int, group=None):
     return assemble_row_shards(parts, width, height)
 
 
+def _copy_list(pairs) -> None:
+    """Device-to-device copies (src, dst) of contiguous tensors as one cf_copy_batch launch."""
+    L = _lib.CopyList()
+    for src, dst in pairs:
+        L.src[L.n], L.dst[L.n] = src.data_ptr(), dst.data_ptr()
+        L.bytes[L.n] = src.numel() * src.element_size()
+        L.n += 1
+    _lib.call("cf_copy_batch", _lib.byref(L), _lib.stream_ptr())
+
+
 class Renderer:
     """render_view for one human + one rigid object."""
 
@@ -458,22 +468,25 @@ class Renderer:
 
     def _save_frame_state(self):
         """Snapshot of the per-frame state another user of the warp buffers (the
-        trainer's key frames) overwrites: prior buffers (device copies), the pose flag
-        and whether a setup was pending."""
+        trainer's key frames) overwrites: the prior buffers (one batched device copy
+        into buffers kept for this) and the pose flag."""
         if self.human is None or getattr(self, "_dqs", None) is None:
             return None
-        bufs = [self._dqs, self._A, self.dbias] + ([self._theta] if getattr(self, "_theta", None) is not None else [])
         self._flush_copies()  # a prior staged but not yet issued belongs to the snapshot
-        return ([(b, b.clone()) for b in bufs], getattr(self, "_pose_on_device", False))
+        bufs = [self._dqs, self._A, self.dbias] + ([self._theta] if getattr(self, "_theta", None) is not None else [])
+        snap = getattr(self, "_snap", None)
+        if snap is None or len(snap) != len(bufs):
+            snap = self._snap = [torch.empty_like(b) for b in bufs]
+        _copy_list(list(zip(bufs, snap)))
+        return (list(zip(snap, bufs)), getattr(self, "_pose_on_device", False))
 
     def _restore_frame_state(self, saved) -> None:
-        """Restore a _save_frame_state snapshot; the frame's setup (deformed nodes,
-        LBS, live occupancy) re-runs with the next view."""
+        """Restore a _save_frame_state snapshot (one batched device copy); the frame's
+        setup (deformed nodes, LBS, live occupancy) re-runs with the next view."""
         if saved is None:
             return
         pairs, pose_on_device = saved
-        for dst, src in pairs:
-            dst.copy_(src, non_blocking=True)
+        _copy_list(pairs)
         self._pose_on_device = pose_on_device
         self._setup_pending = True
 

@@ -8,17 +8,29 @@ Trained: the canonical hash grids and E_g/E_c of both fields, and the human's
 DeformNet with its deformation grid (TrainConfig.train_deform): the canonical
 hash backward also returns dL/dxc (spatial gradient of the trilinear
 interpolation), which flows through xc = xu + 0.05 tanh(o) / side into the
-tcgen05 DeformNet backward and on into the deformation-grid hash backward. The
-weight-gradient reductions dW = dY^T X over the saved fp16 activations are plain
-GEMMs (cuBLAS via torch.mm); every other step is a kernel of this package.
+tcgen05 DeformNet backward and on into the deformation-grid hash backward.
 
-Multi-GPU: rays are sharded across ranks; `allreduce_grads` sums the flat
-gradient buckets over NCCL (NVLink) and each rank applies the same Adam update.
+Every launch of a step is a kernel of this package and nothing in it waits on the
+host: the frames' masked / depth-valid ray counts, the loss normalisers and the
+power-of-two loss scale are computed on the device (cf_train_counts /
+cf_train_norms), the weight gradients dW = dY^T X are one grouped tcgen05 launch
+per field and frame with the sample count read on the device (cf_dw_grouped over
+the feature-major fp16 saves), Adam is one multi-tensor launch that also zeroes the
+gradients, and the fp16 weight blobs are repacked by one launch. So the whole step
+(key-frame ray draw included, `Trainer.capture`) replays as one CUDA graph.
+
+Multi-GPU: rays are sharded across ranks (`shard_batch`; the sampler's jitter is a
+hash of the GLOBAL ray id, so a ray draws the same samples in any shard); the
+per-frame ray counts are summed over ranks before the loss is normalised, so the
+sum of the ranks' gradients is the gradient of the global batch's loss; each
+field's gradients live in one flat bucket that is all-reduced (sum, NCCL over
+NVLink) as soon as that field's last backward is enqueued — the human bucket while
+the last frame's object backward still runs.
 """
 from __future__ import annotations
 
 import ctypes
-from dataclasses import dataclass
+from dataclasses import dataclass, replace
 
 import numpy as np
 import torch
@@ -27,6 +39,8 @@ from . import _lib
 from .render import Renderer, _FieldBuffers
 
 COLOR_LAYERS = ("G1", "G2", "C1", "C2", "C3")
+DEFORM_LAYERS = ("D1", "D2", "D3", "D4", "D5")
+_FIELD_INDEX = {"human": 0, "object": 1}
 
 
 @dataclass
@@ -59,6 +73,20 @@ class FrameBatch:
     mask_o: torch.Tensor       # (R,) u8 object mask
     theta: torch.Tensor | None = None  # (72,) f32 pose; DeformNet training recomputes dbias from it
     origin: np.ndarray | None = None   # (3,) f64 camera centre of the key frame (the rays' origin)
+    ray0: int = 0                      # global id of the first ray (data-parallel shards)
+    theta64: torch.Tensor | None = None  # (72,) f64 copy of theta (made once, reused by every step)
+
+    def pose64(self) -> torch.Tensor:
+        if self.theta64 is None:
+            self.theta64 = self.theta.to(torch.float64).contiguous()
+        return self.theta64
+
+
+def shard_batch(b: FrameBatch, rank: int, world: int) -> FrameBatch:
+    """A rank's contiguous share of a key frame's rays (ray0 = their global id)."""
+    sl = shard_rays(b.dirs.shape[0], rank, world)
+    return replace(b, dirs=b.dirs[sl], gt_rgb=b.gt_rgb[sl], gt_depth=b.gt_depth[sl], mask_h=b.mask_h[sl],
+                   mask_o=b.mask_o[sl], ray0=b.ray0 + sl.start)
 
 
 class KeyFrame:
@@ -82,123 +110,123 @@ class KeyFrame:
         self.mask_o = mask_o.contiguous()
         self.fg = torch.nonzero((self.mask_h | self.mask_o).view(-1)).view(-1).to(torch.int32)
         self.dqs, self.bone_A, self.theta, self.dbias = dqs, bone_A, theta, dbias
+        self.theta64 = theta.to(torch.float64).contiguous() if theta is not None else None
         self.obj_R, self.obj_t = obj_R, obj_t
 
-    def sample(self, n_rays: int, seed: int) -> FrameBatch:
+    def batch_buffers(self, n_rays: int) -> FrameBatch:
         d = self.rgb.device
-        dirs = torch.empty((n_rays, 3), dtype=torch.float64, device=d)
-        rgb = torch.empty((n_rays, 3), dtype=torch.float32, device=d)
-        depth = torch.empty(n_rays, dtype=torch.float32, device=d)
-        mh = torch.empty(n_rays, dtype=torch.uint8, device=d)
-        mo = torch.empty(n_rays, dtype=torch.uint8, device=d)
-        _lib.call("cf_keyframe_rays", _lib.byref(self.cam), self.fg.data_ptr(), int(self.fg.numel()), int(n_rays),
-                  ctypes.c_uint64(seed), self.rgb.data_ptr(), self.depth.data_ptr(), self.mask_h.data_ptr(),
-                  self.mask_o.data_ptr(), None, dirs.data_ptr(), rgb.data_ptr(), depth.data_ptr(), mh.data_ptr(),
-                  mo.data_ptr(), _lib.stream_ptr())
         return FrameBatch(dqs=self.dqs, bone_A=self.bone_A, dbias=self.dbias, obj_R=self.obj_R, obj_t=self.obj_t,
-                          dirs=dirs, gt_rgb=rgb, gt_depth=depth, mask_h=mh, mask_o=mo, theta=self.theta,
-                          origin=self.origin)
+                          dirs=torch.empty((n_rays, 3), dtype=torch.float64, device=d),
+                          gt_rgb=torch.empty((n_rays, 3), dtype=torch.float32, device=d),
+                          gt_depth=torch.empty(n_rays, dtype=torch.float32, device=d),
+                          mask_h=torch.empty(n_rays, dtype=torch.uint8, device=d),
+                          mask_o=torch.empty(n_rays, dtype=torch.uint8, device=d), theta=self.theta,
+                          origin=self.origin, theta64=self.theta64)
+
+    def draw(self, b: FrameBatch, seed: int, seed_offset: torch.Tensor | None = None) -> FrameBatch:
+        """Fill b's rays (fresh pixels every call: seed, + *seed_offset on the device)."""
+        n = b.dirs.shape[0]
+        _lib.call("cf_keyframe_rays", _lib.byref(self.cam), self.fg.data_ptr(), int(self.fg.numel()), int(n),
+                  ctypes.c_uint64(seed), seed_offset.data_ptr() if seed_offset is not None else None,
+                  self.rgb.data_ptr(), self.depth.data_ptr(), self.mask_h.data_ptr(), self.mask_o.data_ptr(), None,
+                  b.dirs.data_ptr(), b.gt_rgb.data_ptr(), b.gt_depth.data_ptr(), b.mask_h.data_ptr(),
+                  b.mask_o.data_ptr(), _lib.stream_ptr())
+        return b
+
+    def sample(self, n_rays: int, seed: int) -> FrameBatch:
+        return self.draw(self.batch_buffers(n_rays), seed)
+
+
+def _pad16(x: int) -> int:
+    return (x + 15) // 16 * 16
+
+
+def _item(w, rows, cols, ldw, col0, transpose, blob, blob_lo):
+    return _lib.PackItem(w.data_ptr(), blob, blob_lo, rows, cols, ldw, col0, transpose)
 
 
 class ColorParams:
-    """fp32 master weights of E_g/E_c on the device, their grads and Adam moments;
-    repacks the fp16 forward and transposed blobs after every update."""
+    """fp32 master weights of E_g/E_c on the device, their grads (views into the
+    field's flat gradient bucket) and Adam moments; the fp16 forward / transposed
+    blobs are repacked from them after every update (pack_items)."""
 
-    def __init__(self, nets, device):
+    def __init__(self, nets, device, grads: dict):
         self.nets = nets
         self.W = {k: torch.from_numpy(nets.layers[k].astype(np.float32)).to(device).contiguous() for k in COLOR_LAYERS}
-        self.G = {k: torch.zeros_like(v) for k, v in self.W.items()}
+        self.G = {k: grads[k] for k in COLOR_LAYERS}
         self.m = {k: torch.zeros_like(v) for k, v in self.W.items()}
         self.v = {k: torch.zeros_like(v) for k, v in self.W.items()}
         self.off = nets.w_bytes - 20480  # colour part of the forward blob (after DeformNet)
         self.wt_blob = torch.empty(20480, dtype=torch.uint8, device=device)
-        self.pack()
 
-    def pack(self):
-        s = _lib.stream_ptr()
+    def pack_items(self):
+        it = []
         o = self.off
-        for k in COLOR_LAYERS:
+        for k in COLOR_LAYERS:  # forward blob: W (n_out x n_in) with its split residual
             w = self.W[k]
             n, kk = w.shape
-            _lib.call("cf_pack_weight_split", w.data_ptr(), n, kk, self.nets.blob.data_ptr() + o,
-                      self.nets.blob_lo.data_ptr() + o, s)
-            o += ((n + 15) // 16 * 16) * ((kk + 15) // 16 * 16) * 2
+            it.append(_item(w, n, kk, kk, 0, 0, self.nets.blob.data_ptr() + o, self.nets.blob_lo.data_ptr() + o))
+            o += _pad16(n) * _pad16(kk) * 2
         o = 0
-        for k in ("C3", "C2", "C1", "G2", "G1"):
-            wt = self.W[k].t().contiguous()
-            self._keep = getattr(self, "_keep", []) + [wt]
-            n, kk = wt.shape
-            _lib.call("cf_pack_weight", wt.data_ptr(), n, kk, self.wt_blob.data_ptr() + o, s)
-            o += ((n + 15) // 16 * 16) * ((kk + 15) // 16 * 16) * 2
-        self._keep = []
-
-    def zero_grad(self):
-        for g in self.G.values():
-            g.zero_()
-
-
-DEFORM_LAYERS = ("D1", "D2", "D3", "D4", "D5")
+        for k in ("C3", "C2", "C1", "G2", "G1"):  # backward blob: W^T
+            w = self.W[k]
+            n, kk = w.shape
+            it.append(_item(w, kk, n, kk, 0, 1, self.wt_blob.data_ptr() + o, None))
+            o += _pad16(kk) * _pad16(n) * 2
+        return it
 
 
 class DeformParams:
     """fp32 master weights of DeformNet (D1 = [hash(32) | theta(72)] columns), their
-    grads and Adam moments; repacks the forward blob's DeformNet part and the
-    transposed blob of the backward kernel after every update."""
+    grads (views into the human field's bucket) and Adam moments."""
 
-    def __init__(self, nets, device):
+    def __init__(self, nets, device, grads: dict):
         self.nets = nets
         self.W = {k: torch.from_numpy(nets.layers[k].astype(np.float32)).to(device).contiguous() for k in DEFORM_LAYERS}
         self.W["D1"] = nets.d1  # shared with the renderer: its per-frame pose bias reads the trained W1
-        self.G = {k: torch.zeros_like(v) for k, v in self.W.items()}
+        self.G = {k: grads[k] for k in DEFORM_LAYERS}
         self.m = {k: torch.zeros_like(v) for k, v in self.W.items()}
         self.v = {k: torch.zeros_like(v) for k, v in self.W.items()}
         self.wt_blob = torch.empty(110592, dtype=torch.uint8, device=device)
-        self.pack()
+        self.d1_tmp = torch.zeros((128, 48), dtype=torch.float32, device=device)  # [dW1 features | sum dpre1]
 
-    def bias(self, theta: torch.Tensor) -> torch.Tensor:
-        """Per-frame layer-1 pose term W1[:, 32:] @ theta (fp32, device)."""
-        return (self.W["D1"][:, 32:] @ theta.to(self.W["D1"].device, torch.float32)).contiguous()
-
-    def pack(self):
-        s = _lib.stream_ptr()
-        mats = [self.W["D1"][:, :32].contiguous(), self.W["D2"], self.W["D3"], self.W["D4"], self.W["D5"]]
+    def pack_items(self):
+        W = self.W
+        ld1 = int(W["D1"].shape[1])
+        it = []
         o = 0
-        for w in mats:
-            n, kk = w.shape
-            _lib.call("cf_pack_weight_split", w.data_ptr(), n, kk, self.nets.blob.data_ptr() + o,
-                      self.nets.blob_lo.data_ptr() + o, s)
-            o += ((n + 15) // 16 * 16) * ((kk + 15) // 16 * 16) * 2
-        keep = [self.W["D5"].t().contiguous(), self.W["D4"].t().contiguous(), self.W["D3"].t().contiguous(),
-                self.W["D2"].t().contiguous(), self.W["D1"][:, :32].t().contiguous()]
+        for w, rows, cols, ldw in ((W["D1"], 128, 32, ld1), (W["D2"], 128, 128, 128), (W["D3"], 128, 128, 128),
+                                   (W["D4"], 128, 128, 128), (W["D5"], 3, 128, 128)):
+            it.append(_item(w, rows, cols, ldw, 0, 0, self.nets.blob.data_ptr() + o, self.nets.blob_lo.data_ptr() + o))
+            o += _pad16(rows) * _pad16(cols) * 2
         o = 0
-        for wt in keep:
-            n, kk = wt.shape
-            _lib.call("cf_pack_weight", wt.data_ptr(), n, kk, self.wt_blob.data_ptr() + o, s)
-            o += ((n + 15) // 16 * 16) * ((kk + 15) // 16 * 16) * 2
-
-    def zero_grad(self):
-        for g in self.G.values():
-            g.zero_()
+        for w, rows, cols, ldw in ((W["D5"], 128, 3, 128), (W["D4"], 128, 128, 128), (W["D3"], 128, 128, 128),
+                                   (W["D2"], 128, 128, 128), (W["D1"], 32, 128, ld1)):
+            it.append(_item(w, rows, cols, ldw, 0, 1, self.wt_blob.data_ptr() + o, None))
+            o += _pad16(rows) * _pad16(cols) * 2
+        return it
 
 
 class _DeformBuffers:
     def __init__(self, cap, device):
-        # feature-major (512, capacity): the kernels' stores coalesce across samples
+        # feature-major (rows, capacity): the kernels' stores coalesce across samples and
+        # the dW GEMMs read them K-major
         self.save_h = torch.empty((512, cap), dtype=torch.float16, device=device)
         self.save_o = torch.empty((cap, 4), dtype=torch.float32, device=device)
         self.save_mask = torch.empty((cap, 16), dtype=torch.int32, device=device)
-        self.d_o = torch.empty((cap, 16), dtype=torch.float16, device=device)
+        self.d_o = torch.empty((16, cap), dtype=torch.float16, device=device)
         self.dpre = torch.empty((512, cap), dtype=torch.float16, device=device)
         self.d_dfeat = torch.empty((cap, 32), dtype=torch.float32, device=device)
         self.dxc = torch.empty((cap, 4), dtype=torch.float32, device=device)
         self.io = _lib.DeformBwdIO(self.save_h.data_ptr(), self.save_o.data_ptr(), self.save_mask.data_ptr(),
-                                   self.d_o.data_ptr(),
-                                   self.dpre.data_ptr(), self.d_dfeat.data_ptr())
+                                   self.d_o.data_ptr(), self.dpre.data_ptr(), self.d_dfeat.data_ptr())
 
 
 class _BwdBuffers:
+    """E_g/E_c backward saves, feature-major (width, capacity) fp16."""
+
     def __init__(self, cap, device):
-        h = lambda w: torch.empty((cap, w), dtype=torch.float16, device=device)  # noqa: E731
+        h = lambda w: torch.empty((w, cap), dtype=torch.float16, device=device)  # noqa: E731
         self.h1, self.cin, self.c1, self.c2 = h(64), h(32), h(64), h(64)
         self.d_o, self.dc2, self.dc1, self.dg, self.dh1 = h(16), h(64), h(64), h(16), h(64)
         self.dfeat = torch.empty((cap, 32), dtype=torch.float32, device=device)
@@ -208,145 +236,191 @@ class _BwdBuffers:
                                     ("h1", "cin", "c1", "c2", "d_o", "dc2", "dc1", "dg", "dh1", "dfeat")])
 
 
+def _flat_bucket(shapes: dict, device) -> tuple[torch.Tensor, dict]:
+    """One zeroed fp32 buffer holding every gradient of a field (the all-reduce bucket)."""
+    total = sum(int(np.prod(s)) for s in shapes.values())
+    flat = torch.zeros(total, dtype=torch.float32, device=device)
+    views, o = {}, 0
+    for k, s in shapes.items():
+        n = int(np.prod(s))
+        views[k] = flat[o:o + n].view(s)
+        o += n
+    return flat, views
+
+
 class Trainer:
     """SPEC train_step for the human + object fields of a Renderer."""
 
     def __init__(self, renderer: Renderer, max_rays: int, cfg: TrainConfig | None = None):
         self.r = renderer
-        self.cfg = cfg or TrainConfig()
+        self.cfg = cfg = cfg or TrainConfig()
         d = renderer.dirs.device
+        self.device = d
         self.max_rays = int(max_rays)
-        cap = self.max_rays * max(self.cfg.n_guided + self.cfg.n_uniform, self.cfg.n_empty)
+        per_ray = max(cfg.n_guided + cfg.n_uniform, cfg.n_empty)
+        cap = -(-self.max_rays * per_ray // 128) * 128  # whole 128-sample tiles (the saves' last K tile)
+        self.cap = cap
+        offs = (ctypes.c_int64 * 6)()
+        _lib.call("cf_field_train_layout", cap, offs)
+        self.layout = list(offs)
         self.fields = []
         for name, field in (("human", renderer.human), ("object", renderer.obj)):
             if field is None:
                 continue
-            st = {"name": name, "field": field, "buf": _FieldBuffers(self.max_rays, cap, d),
-                  "bwd": _BwdBuffers(cap, d), "params": ColorParams(field.nets, d)}
-            st["tgrad"] = torch.zeros_like(field.cgrid.table)
-            st["tm"] = torch.zeros_like(field.cgrid.table)
-            st["tv"] = torch.zeros_like(field.cgrid.table)
-            if name == "human" and self.cfg.train_deform:
-                st["deform"] = DeformParams(field.nets, d)
+            deform = name == "human" and cfg.train_deform
+            shapes = {"ctable": tuple(field.cgrid.table.shape)}
+            shapes.update({k: tuple(field.nets.layers[k].shape) for k in COLOR_LAYERS})
+            if deform:
+                shapes["dtable"] = tuple(field.dgrid.table.shape)
+                shapes.update({k: tuple(field.nets.layers[k].shape) for k in DEFORM_LAYERS})
+            flat, g = _flat_bucket(shapes, d)
+            buf = _FieldBuffers(self.max_rays, cap, d)
+            buf.scratch = torch.empty(self.layout[5], dtype=torch.uint8, device=d)
+            st = {"name": name, "q": _FIELD_INDEX[name], "field": field, "buf": buf, "bwd": _BwdBuffers(cap, d),
+                  "flat": flat, "tgrad": g["ctable"], "params": ColorParams(field.nets, d, g),
+                  "tm": torch.zeros_like(field.cgrid.table), "tv": torch.zeros_like(field.cgrid.table)}
+            if deform:
+                st["deform"] = DeformParams(field.nets, d, g)
                 st["dbufs"] = _DeformBuffers(cap, d)
-                st["dtgrad"] = torch.zeros_like(field.dgrid.table)
+                st["dtgrad"] = g["dtable"]
                 st["dtm"] = torch.zeros_like(field.dgrid.table)
                 st["dtv"] = torch.zeros_like(field.dgrid.table)
+                st["dbias"] = torch.empty(128, dtype=torch.float32, device=d)
             self.fields.append(st)
-        self.dirs = torch.empty((self.max_rays, 3), dtype=torch.float64, device=d)
         self.M = _lib.MarchDesc()
         ctypes.memmove(ctypes.byref(self.M), ctypes.byref(renderer.M), ctypes.sizeof(self.M))
         self.M.frame = None  # the trainer passes its frame (origin, object pose) by value
-        self.loss = torch.zeros(2, dtype=torch.float32, device=d)
+        # device-side step control
+        self.step_dev = torch.zeros(1, dtype=torch.int32, device=d)
+        self.seed_dev = torch.zeros(1, dtype=torch.int64, device=d)
+        self.adam_scale = torch.ones(2, dtype=torch.float32, device=d)
+        self.stats = torch.zeros((2, 2), dtype=torch.float32, device=d)
+        self.counts = None
+        self.norms = None
         self.step_count = 0
         self.seed = 1234
+        self._adam = None
+        self._pack = None
+        self._pack_weights()
+
+    # -- per-step control ------------------------------------------------------
+
+    def _ensure_frames(self, n_frames: int):
+        if self.counts is None or self.counts.shape[0] != n_frames:
+            self.counts = torch.zeros((n_frames, 4), dtype=torch.int32, device=self.device)
+            self.norms = torch.zeros((2, n_frames, 4), dtype=torch.float32, device=self.device)
+
+    def prepare(self, batches, group=None):
+        """Count the masked / depth-valid rays of every frame, sum them over ranks
+        (data parallel) and derive the step's normalisers and loss scales on the device."""
+        self._ensure_frames(len(batches))
+        s = _lib.stream_ptr()
+        for f, b in enumerate(batches):
+            n = int(b.dirs.shape[0])
+            _lib.call("cf_train_counts", b.mask_h.data_ptr(), b.mask_o.data_ptr(), b.gt_depth.data_ptr(), n, 1,
+                      max(n, 1), self.counts[f].data_ptr(), s)
+        if _world(group) > 1:
+            import torch.distributed as dist
+            dist.all_reduce(self.counts, group=group)
+        _lib.call("cf_train_norms", self.counts.data_ptr(), len(batches), self.norms.data_ptr(),
+                  self.adam_scale.data_ptr(), self.stats.data_ptr(), self.step_dev.data_ptr(),
+                  self.seed_dev.data_ptr(), s)
+
+    def grad_scale(self, name: str) -> float:
+        """The field's loss scale of the last prepared step (host read: tests / tools)."""
+        return float(self.norms[_FIELD_INDEX[name], 0, 2])
 
     # -- one key frame -----------------------------------------------------------
 
-    def _frame(self, b: FrameBatch, st, stats):
+    def _frame(self, f: int, b: FrameBatch, st):
         r, cfg, s = self.r, self.cfg, _lib.stream_ptr()
         buf, bwd, P = st["buf"], st["bwd"], st["params"]
-        field = st["field"]
-        n_rays = b.dirs.shape[0]
+        field, q = st["field"], st["q"]
+        n_rays = int(b.dirs.shape[0])
+        if n_rays > self.max_rays:
+            raise ValueError("frame batch larger than max_rays")
         mask = b.mask_h if st["name"] == "human" else b.mask_o
-        n_m = int(mask.sum())
-        if n_m == 0:
-            return
-        n_d = int(((b.gt_depth > 0) & (mask > 0)).sum())
         M = self.M
         M.n_rays = n_rays
         M.sample_t = None
-        self.seed += 1
+        norm = self.norms[q, f].data_ptr()
         _lib.call("cf_train_sample", _lib.byref(M), b.gt_depth.data_ptr(), mask.data_ptr(), cfg.n_guided,
-                  cfg.n_uniform, cfg.n_empty, cfg.depth_sigma, ctypes.c_uint64(self.seed), _lib.byref(buf.mo),
-                  bwd.t.data_ptr(), s)
+                  cfg.n_uniform, cfg.n_empty, cfg.depth_sigma, ctypes.c_uint64(self.seed + 7919 * f + 104729 * q),
+                  self.seed_dev.data_ptr(), int(b.ray0), _lib.byref(buf.mo), bwd.t.data_ptr(), s)
         M.sample_t = bwd.t.data_ptr()
         dp = st.get("deform")
+        dirs = b.dirs.data_ptr()
         if st["name"] == "human":
-            _lib.call("cf_human_canon", _lib.byref(M), self.dirs.data_ptr(), _lib.byref(buf.mo), _lib.byref(r.hw),
+            _lib.call("cf_human_canon", _lib.byref(M), dirs, _lib.byref(buf.mo), _lib.byref(r.hw),
                       r._anchor_buckets.handle, field.lbs.buckets.handle, buf.xu.data_ptr(), s)
-            # the training forward: DeformNet at 32-bit semantics with the fp16 saves the
-            # fp16 backward consumes (cf_field_forward with save_h in the "fp32" mode)
-            desc = field.desc(r.dbias, "fp32" if dp is not None else "fp16")
+            desc = field.desc(r.dbias, "fp32")
             if dp is not None:
-                # this frame's pose bias from the current W1, forward saves on
                 if b.theta is None:
                     raise ValueError("DeformNet training needs FrameBatch.theta")
-                st["dbias"] = dp.bias(b.theta)
+                # this frame's pose bias W1[:, 32:] theta from the current (trained) W1
+                th = b.pose64()
+                _lib.call("cf_pose_bias", dp.W["D1"].data_ptr(), int(dp.W["D1"].shape[1]), 32, 128, th.data_ptr(),
+                          int(th.numel()), st["dbias"].data_ptr(), s)
                 desc.dbias = st["dbias"].data_ptr()
                 desc.save_h = st["dbufs"].save_h.data_ptr()
                 desc.save_o = st["dbufs"].save_o.data_ptr()
                 desc.save_mask = st["dbufs"].save_mask.data_ptr()
         else:
-            _lib.call("cf_object_canon", _lib.byref(M), self.dirs.data_ptr(), _lib.byref(buf.mo), buf.xu.data_ptr(), s)
-            desc = field.desc("fp16")
-        scratch = r._scratch(buf, desc)
-        _lib.call("cf_field_forward", _lib.byref(desc), _lib.byref(buf.mo), self.dirs.data_ptr(), buf.xu.data_ptr(),
-                  buf.out.data_ptr(), scratch.data_ptr(), s)
-        if st.get("gscale") is None:
-            st["gscale"] = loss_scale(n_m)
+            _lib.call("cf_object_canon", _lib.byref(M), dirs, _lib.byref(buf.mo), buf.xu.data_ptr(), s)
+            desc = field.desc("fp32")
+        desc.train = 1  # 32-bit forward + the fp16 feature-major saves of the backward
+        st["desc"] = desc
+        scratch = buf.scratch.data_ptr()
+        _lib.call("cf_field_forward", _lib.byref(desc), _lib.byref(buf.mo), dirs, buf.xu.data_ptr(),
+                  buf.out.data_ptr(), scratch, s)
         _lib.call("cf_loss_composite_bwd", _lib.byref(M), _lib.byref(buf.mo), buf.out.data_ptr(), r.cfg.t_term,
-                  b.gt_rgb.data_ptr(), b.gt_depth.data_ptr(), mask.data_ptr(), cfg.lambda_depth, 1.0 / n_m,
-                  1.0 / max(n_d, 1), st["gscale"], bwd.grad.data_ptr(), stats.data_ptr(), s)
-        _lib.call("cf_color_backward", _lib.byref(desc), P.wt_blob.data_ptr(), _lib.byref(buf.mo),
-                  self.dirs.data_ptr(), buf.xu.data_ptr(), bwd.grad.data_ptr(), scratch.data_ptr(),
-                  _lib.byref(bwd.io), s)
+                  b.gt_rgb.data_ptr(), b.gt_depth.data_ptr(), mask.data_ptr(), cfg.lambda_depth, norm,
+                  bwd.grad.data_ptr(), self.stats[q].data_ptr(), s)
+        _lib.call("cf_color_backward", _lib.byref(desc), P.wt_blob.data_ptr(), _lib.byref(buf.mo), dirs,
+                  buf.xu.data_ptr(), bwd.grad.data_ptr(), scratch, _lib.byref(bwd.io), s)
         db = st.get("dbufs")
-        _lib.call("cf_field_hash_backward", _lib.byref(desc), _lib.byref(buf.mo), buf.xu.data_ptr(),
-                  scratch.data_ptr(), bwd.dfeat.data_ptr(), st["tgrad"].data_ptr(),
-                  db.dxc.data_ptr() if dp is not None else None, s)
+        _lib.call("cf_field_hash_backward", _lib.byref(desc), _lib.byref(buf.mo), buf.xu.data_ptr(), scratch,
+                  bwd.dfeat.data_ptr(), st["tgrad"].data_ptr(), db.dxc.data_ptr() if dp is not None else None, s)
         if dp is not None:
             _lib.call("cf_deform_backward", _lib.byref(desc), dp.wt_blob.data_ptr(), _lib.byref(buf.mo),
                       buf.xu.data_ptr(), db.dxc.data_ptr(), _lib.byref(db.io), s)
             _lib.call("cf_deform_hash_backward", _lib.byref(desc), _lib.byref(buf.mo), buf.xu.data_ptr(),
                       db.d_dfeat.data_ptr(), st["dtgrad"].data_ptr(), s)
-        # weight gradients dW = dY^T X over this frame's samples (plain GEMMs)
-        n = int(buf.counters[0])
-        if n == 0:
-            return
-        # The GEMM row count is rounded up to one of 8 sizes per power of two (within
-        # the buffers) so that frames with different sample counts reuse cuBLASLt's
-        # cached plans (a new shape costs ~4 ms of host-side heuristics); the padding
-        # rows of both operands are zeroed, so they add nothing (zero dY alone is not
-        # enough: stale X rows may hold inf/NaN bit patterns, and 0 * NaN = NaN).
-        q = 1 << max(n.bit_length() - 4, 10)
-        cap = buf.mo.capacity
-        n_pad = min(-(-n // q) * q, cap)
-        pads = [bwd.d_o, bwd.dc2, bwd.dc1, bwd.dg, bwd.dh1, bwd.c2, bwd.c1, bwd.cin, bwd.h1]
-        pads += [scratch[n * 64: n_pad * 64]]  # colour-MLP input rows (x0 below)
+        # weight gradients dW = dY^T X over the frame's samples: one grouped tcgen05
+        # launch, both operands feature-major (K = samples), K read on the device
+        probs = self._dw_problems(st)
+        arr = (_lib.DwProblem * len(probs))(*probs)
+        _lib.call("cf_dw_grouped", arr, len(probs), buf.counters.data_ptr(), self.cap, s)
         if dp is not None:
-            pads += [db.d_o, scratch[cap * 64 + n * 64: cap * 64 + n_pad * 64]]
-            db.dpre[:, n:n_pad].zero_()
-            db.save_h[:, n:n_pad].zero_()
-        for t in pads:
-            (t[n:n_pad] if t.dim() == 2 else t).zero_()
-        n, n_true = n_pad, n
-        x0 = scratch[: n * 64].view(torch.float16).view(n, 32)
-        # fp16 operands on the tensor cores, fp32 accumulation (reduced-precision
-        # split-K reduction disabled), fp32 gradient accumulation across frames
-        torch.backends.cuda.matmul.allow_fp16_reduced_precision_reduction = False
-        f = lambda t: t[:n]  # noqa: E731
-        G = P.G
-        G["C3"] += (f(bwd.d_o).t() @ f(bwd.c2)).float()[:3]
-        G["C2"] += (f(bwd.dc2).t() @ f(bwd.c1)).float()
-        G["C1"] += (f(bwd.dc1).t() @ f(bwd.cin)).float()[:, :31]
-        G["G2"] += (f(bwd.dg).t() @ f(bwd.h1)).float()
-        G["G1"] += (f(bwd.dh1).t() @ x0).float()
+            # theta is the same for every sample of the frame: dW1[:, 32:] = (sum_s dpre1) theta^T
+            th = b.theta
+            _lib.call("cf_dw_pose_cols", dp.d1_tmp.data_ptr(), 128, 48, 32, th.data_ptr(), int(th.numel()),
+                      dp.G["D1"].data_ptr(), int(dp.G["D1"].shape[1]), s)
+
+    def _dw_problems(self, st):
+        cap, bwd, G = self.cap, st["bwd"], st["params"].G
+        x0 = st["buf"].scratch.data_ptr() + self.layout[0]  # canonical features (32, cap)
+
+        def prob(A, m, B, n, C, ldc):
+            return _lib.DwProblem(A, cap, m, B, cap, n, C.data_ptr(), ldc)
+
+        ps = [prob(bwd.dh1.data_ptr(), 64, x0, 32, G["G1"], 32),
+              prob(bwd.dg.data_ptr(), 16, bwd.h1.data_ptr(), 64, G["G2"], 64),
+              prob(bwd.dc1.data_ptr(), 64, bwd.cin.data_ptr(), 31, G["C1"], 31),
+              prob(bwd.dc2.data_ptr(), 64, bwd.c1.data_ptr(), 64, G["C2"], 64),
+              prob(bwd.d_o.data_ptr(), 3, bwd.c2.data_ptr(), 64, G["C3"], 64)]
+        dp = st.get("deform")
         if dp is not None:
-            xd = scratch[cap * 64: cap * 64 + n * 64].view(torch.float16).view(n, 32)  # deform-grid features
-            H, DP, DO = db.save_h[:, :n], db.dpre[:, :n], db.d_o[:n]  # H, DP feature-major
-            GD = dp.G
-            GD["D5"] += (DO.t() @ H[384:512].t()).float()[:3]
-            # dW_l = dpre_l h_{l-1}^T over the frame's samples: both operands feature-major
-            # (K = samples contiguous), split-K on tcgen05 accumulating into the fp32 grads
-            ld = db.save_h.stride(0)
-            for l, key in ((3, "D4"), (2, "D3"), (1, "D2")):
-                _lib.call("cf_gemm_kmajor_f16", db.dpre[128 * l].data_ptr(), ld, db.save_h[128 * (l - 1)].data_ptr(),
-                          ld, 128, n, GD[key].data_ptr(), 128, s)
-            GD["D1"][:, :32] += (DP[0:128] @ xd).float()
-            # theta is the same for every sample of the frame: dW1_theta = (sum_s dpre1) theta^T
-            csum = DP[0:128, :n_true].sum(1, dtype=torch.float32)
-            GD["D1"][:, 32:] += torch.outer(csum, b.theta.to(DP.device, torch.float32))
+            db, GD = st["dbufs"], dp.G
+            h = lambda l: db.save_h[128 * l].data_ptr()  # noqa: E731  h_{l+1}, (128, cap)
+            dpre = lambda l: db.dpre[128 * l].data_ptr()  # noqa: E731
+            xd = st["buf"].scratch.data_ptr() + self.layout[1]  # [deform features | 1] (33, cap)
+            ps += [prob(db.d_o.data_ptr(), 3, h(3), 128, GD["D5"], 128),
+                   prob(dpre(3), 128, h(2), 128, GD["D4"], 128),
+                   prob(dpre(2), 128, h(1), 128, GD["D3"], 128),
+                   prob(dpre(1), 128, h(0), 128, GD["D2"], 128),
+                   prob(dpre(0), 128, xd, 33, dp.d1_tmp, 48)]
+        return ps
 
     def set_frame(self, b: FrameBatch):
         """The key frame's warp state (prior -> deformed nodes, LBS, live occupancy in the
@@ -356,12 +430,8 @@ class Trainer:
         if b.origin is None:
             raise ValueError("FrameBatch.origin (the key frame's camera centre) is required")
         r = self.r
-        n = b.dirs.shape[0]
-        if n > self.max_rays:
-            raise ValueError("frame batch larger than max_rays")
         r.load_prior(b.dqs, b.bone_A, b.dbias)
         r.prepare_frame()
-        self.dirs[:n].copy_(b.dirs)
         o = np.asarray(b.origin, dtype=np.float64).reshape(3)
         oR = np.asarray(b.obj_R, dtype=np.float64).reshape(9)
         ot = np.asarray(b.obj_t, dtype=np.float64).reshape(3)
@@ -372,61 +442,133 @@ class Trainer:
             self.M.obj_R[a] = oR[a]
         torch.cuda.current_stream().wait_event(r._lbs_done)
 
-    def step(self, batches, allreduce=None):
-        """One optimisation step over the key-frame batches -> {field: (L_color, L_depth)}."""
-        out = {}
-        for st in self.fields:
-            st["tgrad"].zero_()
-            st["params"].zero_grad()
-            if "deform" in st:
-                st["dtgrad"].zero_()
-                st["deform"].zero_grad()
-            st["stats"] = torch.zeros(2, dtype=torch.float32, device=self.dirs.device)
-        for st in self.fields:  # one loss scale per field and step (every frame's grads add up)
-            mk = [b.mask_h if st["name"] == "human" else b.mask_o for b in batches]
-            st["gscale"] = loss_scale(min(int(m.sum()) for m in mk))
+    # -- the step ------------------------------------------------------------------
+
+    def step(self, batches, group=None, update: bool = True):
+        """One optimisation step over the key-frame batches -> {field: (L_color, L_depth)}
+        (device tensors, means over the frames). Data parallel (torch.distributed
+        initialised with world > 1, or `group`): the batches are this rank's shards; ray
+        counts and gradient buckets are summed over ranks. update=False stops before
+        Adam (the summed, loss-scaled gradients stay in the buckets)."""
+        self.prepare(batches, group)
+        world = _world(group)
+        works = []
         saved = self.r._save_frame_state()
         try:
-            for b in batches:
+            for f, b in enumerate(batches):
                 self.set_frame(b)
                 for st in self.fields:
-                    self._frame(b, st, st["stats"])
+                    self._frame(f, b, st)
+                    if world > 1 and f == len(batches) - 1:
+                        works.append(_allreduce_async(st["flat"], group))
         finally:
             # the renderer's own frame (prior, pending setup) is back for its next view
             self.r._restore_frame_state(saved)
-        if allreduce is not None:
-            bufs = [st["tgrad"] for st in self.fields] + [g for st in self.fields for g in st["params"].G.values()]
-            for st in self.fields:
-                if "deform" in st:
-                    bufs += [st["dtgrad"]] + list(st["deform"].G.values())
-            allreduce(bufs)
+        for w in works:
+            w.wait()
         self.step_count += 1
-        cfg, s = self.cfg, _lib.stream_ptr()
-        nb = float(len(batches))
-        for st in self.fields:
-            unscale = 1.0 / (nb * st["gscale"])  # mean over frames, loss scale divided out
-            t = st["field"].cgrid.table
-            _lib.call("cf_adam", t.data_ptr(), st["tgrad"].data_ptr(), st["tm"].data_ptr(), st["tv"].data_ptr(),
-                      t.numel(), cfg.lr_hash, cfg.beta1, cfg.beta2, cfg.eps, self.step_count, unscale, s)
-            st["field"].cgrid.refresh_f16()
-            P = st["params"]
-            for k in COLOR_LAYERS:
-                _lib.call("cf_adam", P.W[k].data_ptr(), P.G[k].data_ptr(), P.m[k].data_ptr(), P.v[k].data_ptr(),
-                          P.W[k].numel(), cfg.lr_net, cfg.beta1, cfg.beta2, cfg.eps, self.step_count, unscale, s)
-            P.pack()
-            if "deform" in st:
-                t = st["field"].dgrid.table
-                _lib.call("cf_adam", t.data_ptr(), st["dtgrad"].data_ptr(), st["dtm"].data_ptr(), st["dtv"].data_ptr(),
-                          t.numel(), cfg.lr_hash, cfg.beta1, cfg.beta2, cfg.eps, self.step_count, unscale, s)
-                st["field"].dgrid.refresh_f16()
-                D = st["deform"]
-                for k in DEFORM_LAYERS:
-                    _lib.call("cf_adam", D.W[k].data_ptr(), D.G[k].data_ptr(), D.m[k].data_ptr(), D.v[k].data_ptr(),
-                              D.W[k].numel(), cfg.lr_net, cfg.beta1, cfg.beta2, cfg.eps, self.step_count, unscale,
-                              s)
-                D.pack()
-            out[st["name"]] = st["stats"] / nb
-        return out
+        if update:
+            self._update()
+        return {st["name"]: self.stats[st["q"]] for st in self.fields}
+
+    def _update(self):
+        """Adam over every trained tensor (one launch, grads zeroed) and the fp16 repack
+        of the networks' weight blobs (one launch)."""
+        cfg = self.cfg
+        if self._adam is None:
+            ts = []
+            for st in self.fields:
+                q = st["q"]
+                t = st["field"].cgrid.table
+                ts.append(_lib.AdamTensor(t.data_ptr(), st["tgrad"].data_ptr(), st["tm"].data_ptr(),
+                                          st["tv"].data_ptr(), None, t.numel(), cfg.lr_hash, q))
+                P = st["params"]
+                for k in COLOR_LAYERS:
+                    ts.append(_lib.AdamTensor(P.W[k].data_ptr(), P.G[k].data_ptr(), P.m[k].data_ptr(),
+                                              P.v[k].data_ptr(), None, P.W[k].numel(), cfg.lr_net, q))
+                if "deform" in st:
+                    g = st["field"].dgrid
+                    ts.append(_lib.AdamTensor(g.table.data_ptr(), st["dtgrad"].data_ptr(), st["dtm"].data_ptr(),
+                                              st["dtv"].data_ptr(), g.table_f16.data_ptr() if g.read_half else None,
+                                              g.table.numel(), cfg.lr_hash, q))
+                    D = st["deform"]
+                    for k in DEFORM_LAYERS:
+                        ts.append(_lib.AdamTensor(D.W[k].data_ptr(), D.G[k].data_ptr(), D.m[k].data_ptr(),
+                                                  D.v[k].data_ptr(), None, D.W[k].numel(), cfg.lr_net, q))
+            self._adam = (_lib.AdamTensor * len(ts))(*ts)
+        _lib.call("cf_adam_multi", self._adam, len(self._adam), cfg.beta1, cfg.beta2, cfg.eps,
+                  self.step_dev.data_ptr(), self.adam_scale.data_ptr(), _lib.stream_ptr())
+        self._pack_weights()
+
+    def _pack_weights(self):
+        if self._pack is None:
+            items = []
+            for st in self.fields:
+                items += st["params"].pack_items()
+                if "deform" in st:
+                    items += st["deform"].pack_items()
+            self._pack = (_lib.PackItem * len(items))(*items)
+        _lib.call("cf_pack_multi", self._pack, len(self._pack), _lib.stream_ptr())
+
+    def set_learning_rates(self, lr_hash: float, lr_net: float):
+        """New learning rates (the Adam launch table is rebuilt; a captured step must be
+        captured again)."""
+        self.cfg.lr_hash, self.cfg.lr_net = float(lr_hash), float(lr_net)
+        self._adam = None
+
+    # -- the captured step -----------------------------------------------------------
+
+    def capture(self, keyframes, rays_per_frame: int, group=None):
+        """CUDA-graph the whole step over `keyframes` — ray draw (fresh pixels and
+        samples every replay: the seeds advance on the device), counts, forward,
+        backward, dW, Adam, repack — and return a callable that replays it and returns
+        the step's {field: (L_color, L_depth)} device tensors. The draw gives rank r the
+        rays [r R, (r + 1) R) of each frame's global batch (R = rays_per_frame).
+        Data-parallel capture needs an NCCL group (the collectives are captured with the
+        kernels). The warm-up run before the capture is a real optimisation step."""
+        world = _world(group)
+        rank = 0
+        if world > 1:
+            import torch.distributed as dist
+            if dist.get_backend(group) != "nccl":
+                raise ValueError("Trainer.capture with world > 1 needs an NCCL process group")
+            rank = dist.get_rank(group)
+        bufs = [kf.batch_buffers(rays_per_frame) for kf in keyframes]
+        for b in bufs:
+            b.ray0 = rank * rays_per_frame
+
+        def body():
+            for f, (kf, b) in enumerate(zip(keyframes, bufs)):
+                kf.draw(b, seed=(f * 64 + rank) * 1000003, seed_offset=self.seed_dev)
+            return self.step(bufs, group)
+
+        side = torch.cuda.Stream(device=self.device)  # warm-up: lazy state exists before the capture
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            body()
+        torch.cuda.current_stream().wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            out = body()
+
+        def replay():
+            g.replay()
+            self.step_count += 1
+            return out
+        replay.graph = g
+        return replay
+
+
+def _world(group=None) -> int:
+    import torch.distributed as dist
+    if not dist.is_available() or not dist.is_initialized():
+        return 1
+    return dist.get_world_size(group)
+
+
+def _allreduce_async(flat: torch.Tensor, group=None):
+    import torch.distributed as dist
+    return dist.all_reduce(flat, group=group, async_op=True)
 
 
 def sync_host_weights(trainer: "Trainer") -> None:
@@ -441,26 +583,15 @@ def sync_host_weights(trainer: "Trainer") -> None:
                 nets.layers[k] = w.cpu().numpy().astype(np.float32)
 
 
-def loss_scale(n_masked: int) -> float:
-    """Power-of-two loss scale of a field's backward: the per-sample gradients of the
-    1/n-normalised loss are O(1/n); scaled by 2^floor(log2 n) they are O(1), inside
-    the fp16 range of the backward's tensor-core operands (no subnormal underflow)."""
-    return float(2.0 ** max(0, int(np.floor(np.log2(max(1, n_masked))))))
-
-
 def allreduce_grads(tensors, group=None):
-    """Sum gradient buckets over ranks (NCCL on GPUs, gloo on CPU), then average."""
+    """Sum gradient buckets over ranks (NCCL on GPUs, gloo on CPU). The training loss
+    is normalised by the GLOBAL ray counts (Trainer.prepare), so the sum is the
+    global batch's gradient."""
     import torch.distributed as dist
-    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size() == 1:
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
         return
-    flat = torch.cat([t.reshape(-1) for t in tensors])
-    dist.all_reduce(flat, group=group)
-    flat /= dist.get_world_size()
-    o = 0
     for t in tensors:
-        n = t.numel()
-        t.copy_(flat[o:o + n].view_as(t))
-        o += n
+        dist.all_reduce(t, group=group)
 
 
 def shard_rays(n_rays: int, rank: int, world: int) -> slice:

@@ -1,5 +1,5 @@
 """Multi-rank host logic on CPU (gloo, world size 2): training-ray sharding
-covers the global batch exactly once, the gradient-bucket all-reduce averages
+covers the global batch exactly once, the gradient-bucket all-reduce sums
 every bucket across ranks, and the row-sharded multi-GPU render reassembles the
 frame from the ranks' round-robin rows."""
 import os
@@ -56,8 +56,8 @@ def test_allreduce_and_sharding_world2():
         p.join(timeout=60)
         assert p.exitcode == 0
     for rank, g0, gw, a, b, ok in res:
-        assert g0 == pytest.approx(1.5)  # mean of 1 and 2
-        assert gw == (torch.arange(12, dtype=torch.float32).view(3, 4) * 1.5).tolist()
+        assert g0 == pytest.approx(3.0)  # sum of 1 and 2 (the loss is normalised by global counts)
+        assert gw == (torch.arange(12, dtype=torch.float32).view(3, 4) * 3.0).tolist()
         assert ok, f"rank {rank}: row-sharded frame not reassembled"
     spans = [(a, b) for _, _, _, a, b, _ in res]
     assert spans[0][0] == 0 and spans[-1][1] == 10001 and spans[0][1] == spans[1][0]

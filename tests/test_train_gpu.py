@@ -55,16 +55,28 @@ def setup():
 
 
 def run_frame(tr, b, st):
-    st["tgrad"].zero_()
-    st["params"].zero_grad()
+    """One key frame's forward + backward of one field into zeroed gradient buckets
+    (device counts / normalisers of this batch alone); returns its (L_color, L_depth)."""
+    st["flat"].zero_()
     if "deform" in st:
-        st["dtgrad"].zero_()
-        st["deform"].zero_grad()
-    stats = torch.zeros(2, device="cuda")
+        st["deform"].d1_tmp.zero_()
+    tr.prepare([b])
     tr.set_frame(b)
-    tr._frame(b, st, stats)
+    tr._frame(0, b, st)
     torch.cuda.synchronize()
-    return stats
+    return tr.stats[st["q"]].clone()
+
+
+def scratch_block(tr, st, k, rows_or_n, width, dtype, feature_major):
+    """A block of the training scratch (cf_field_train_layout offset k): feature-major
+    (width, cap)[:, :n] returned as (n, width), or sample-major (n, width)."""
+    sc = st["buf"].scratch
+    cap = tr.cap
+    es = torch.tensor([], dtype=dtype).element_size()
+    o = tr.layout[k]
+    if feature_major:
+        return sc[o: o + width * cap * es].view(dtype).view(width, cap)[:, :rows_or_n].t().cpu()
+    return sc[o: o + rows_or_n * width * es].view(dtype).view(rows_or_n, width).cpu()
 
 
 def samples_of(st):
@@ -82,8 +94,9 @@ def test_sampler_bitexact(setup):
     n, ray, i = samples_of(st)
     t = st["bwd"].t[:n].cpu().numpy()
     c = tr.cfg
+    seed = (tr.seed + int(tr.seed_dev.item())) % (1 << 64)  # frame 0, human field; + the step's device offset
     ref = orr.train_samples(b.gt_depth.cpu().numpy(), b.mask_h.cpu().numpy(), 0.3, 5.0, c.n_guided, c.n_uniform,
-                            c.n_empty, c.depth_sigma, tr.seed)
+                            c.n_empty, c.depth_sigma, seed)
     off = st["buf"].ray_offset.cpu().numpy()
     cnt = st["buf"].ray_count.cpu().numpy()
     for q, rt in enumerate(ref):
@@ -143,7 +156,7 @@ def test_loss_composite_backward(setup):
     ref = torch_composite_loss(out[sel], t[sel], ray[sel], b.dirs.shape[0], b.gt_rgb.cpu().numpy(),
                                b.gt_depth.cpu().numpy(), mask, (5.0 - 0.3) / 64, 0.1, 1.0 / n_m, 1.0 / max(n_d, 1),
                                1e-4)
-    got = st["bwd"].grad[:n].cpu().numpy()[sel] / st["gscale"]  # loss scaling divided out
+    got = st["bwd"].grad[:n].cpu().numpy()[sel] / tr.grad_scale("object")  # loss scaling divided out
     scale = np.abs(ref).max()
     assert scale > 0
     assert np.abs(got - ref).max() <= 1e-4 * scale + 1e-7
@@ -156,11 +169,10 @@ def test_color_backward_vs_autograd(setup):
     run_frame(tr, b, st)
     n, ray, i = samples_of(st)
     buf, bwd, P = st["buf"], st["bwd"], st["params"]
-    scratch = r._scratch(buf, r.hdesc)
-    x0 = scratch[: n * 64].view(torch.float16).view(n, 32).float().cpu()
+    x0 = scratch_block(tr, st, 0, n, 32, torch.float16, True).float()  # the fp16 features, feature-major
     valid = torch.from_numpy(buf.xu[:n].cpu().numpy()[:, 3] > 0)
     g = bwd.grad[:n].cpu()  # scaled by the loss scale, as every gradient of the backward below
-    dirs = torch.from_numpy(tr.dirs[:b.dirs.shape[0]].cpu().numpy()[ray].astype(np.float32))
+    dirs = torch.from_numpy(b.dirs.cpu().numpy()[ray].astype(np.float32))
     W = {k: P.W[k].detach().cpu().half().float().requires_grad_(True) for k in P.W}
     h = lambda x: x.half().float()  # noqa: E731  fp16 operand rounding of the kernel
     h1 = torch.relu(h(x0) @ W["G1"].t())
@@ -225,10 +237,7 @@ def test_canonical_hash_spatial_gradient(setup):
     assert "deform" in st
     run_frame(tr, b, st)
     n, _, _ = samples_of(st)
-    buf = st["buf"]
-    cap = buf.mo.capacity
-    scratch = r._scratch(buf, r.hdesc)
-    xc = scratch[cap * 128: cap * 128 + n * 16].view(torch.float32).view(n, 4).cpu()
+    xc = scratch_block(tr, st, 2, n, 4, torch.float32, False)
     keep = (xc[:, 3] > 0).numpy()
     sel = np.nonzero(keep)[0][:3000]
     x = xc[sel, :3].clone().requires_grad_(True)
@@ -256,13 +265,12 @@ def test_deform_backward_vs_autograd(setup):
     run_frame(tr, b, st)
     n, _, _ = samples_of(st)
     buf, D, db = st["buf"], st["deform"], st["dbufs"]
-    cap = buf.mo.capacity
-    scratch = r._scratch(buf, r.hdesc)
-    # training scratch: cfeat16 | dfeat16 | xc | dfeat32 (cf_field_forward, save_h)
-    x0 = scratch[cap * 144: cap * 144 + n * 128].view(torch.float32).view(n, 32).cpu()
-    xd16 = scratch[cap * 64: cap * 64 + n * 64].view(torch.float16).view(n, 32).float().cpu()
+    # training scratch (cf_field_train_layout): fp32 deformation features, and their fp16
+    # halves feature-major with a row of ones (the layer-1 dW GEMM's pose column)
+    x0 = scratch_block(tr, st, 3, n, 32, torch.float32, False)
+    xd16 = scratch_block(tr, st, 1, n, 33, torch.float16, True).float()
     h = lambda x: x.half().float()  # noqa: E731  fp16 operand rounding of the kernels
-    assert torch.equal(xd16, h(x0))
+    assert torch.equal(xd16[:, :32], h(x0)) and bool((xd16[:, 32] == 1).all())
     valid = torch.from_numpy(buf.xu[:n].cpu().numpy()[:, 3] > 0).float()
     dxc = db.dxc[:n].cpu()[:, :3]
     theta = b.theta.cpu().float()
@@ -340,7 +348,7 @@ def test_pack_and_adam():
 
 def test_training_reduces_loss(setup):
     sc, hf, of, r, tr, batches = setup
-    first = tr.step(batches)
+    first = {k: v.clone() for k, v in tr.step(batches).items()}  # (views of the trainer's stats buffer)
     for _ in range(40):
         last = tr.step(batches)
     torch.cuda.synchronize()
@@ -373,7 +381,7 @@ def test_keyframe_ray_sampler(setup):
     mh = torch.empty(n, dtype=torch.uint8, device="cuda")
     mo = torch.empty(n, dtype=torch.uint8, device="cuda")
     _lib.call("cf_keyframe_rays", _lib.byref(kf.cam), kf.fg.data_ptr(), int(kf.fg.numel()), n,
-              _lib.ctypes.c_uint64(7), kf.rgb.data_ptr(), kf.depth.data_ptr(), kf.mask_h.data_ptr(),
+              _lib.ctypes.c_uint64(7), None, kf.rgb.data_ptr(), kf.depth.data_ptr(), kf.mask_h.data_ptr(),
               kf.mask_o.data_ptr(), pix.data_ptr(), dirs.data_ptr(), g_rgb.data_ptr(), g_d.data_ptr(),
               mh.data_ptr(), mo.data_ptr(), _lib.stream_ptr())
     p = pix.cpu().numpy()
@@ -441,7 +449,7 @@ def test_device_gradients_vs_f64_oracle(setup):
     delta[:-1] = t[1:] - t[:-1]
     delta[last] = r.M.dt
     mask = b.mask_h.cpu().numpy()
-    batch = {"xu": buf.xu[:n].cpu().numpy()[order], "dirs": tr.dirs[:b.dirs.shape[0]].cpu().numpy()[ray], "ray": ray,
+    batch = {"xu": buf.xu[:n].cpu().numpy()[order], "dirs": b.dirs.cpu().numpy()[ray], "ray": ray,
              "t": t, "delta": delta, "gt_rgb": b.gt_rgb.cpu().numpy().astype(np.float64),
              "gt_depth": b.gt_depth.cpu().numpy(), "mask": mask, "inv_side": hf.inv_side,
              "theta": b.theta.cpu().numpy()}
@@ -451,14 +459,13 @@ def test_device_gradients_vs_f64_oracle(setup):
     values.update({k: w.cpu().numpy() for k, w in D.W.items()})
     keep = {}
     batch["keep"] = keep
-    cap = buf.mo.capacity
-    xc_dev = r._scratch(buf, r.hdesc)[cap * 128: cap * 128 + n * 16].view(torch.float32).view(n, 4).cpu().numpy()
+    xc_dev = scratch_block(tr, st, 2, n, 4, torch.float32, False).numpy()
     batch["xc_value"] = xc_dev[order, :3].astype(np.float64)  # the canonical grid at the forward's positions
     batch["cell32"] = True  # and its cells chosen as the kernels choose them
     _, ref = og.gradients(values, batch)
     # stage-wise diagnostics (device vs f64, max err / max |ref|, in the device's sample order)
     inv = np.argsort(order)
-    gs = st["gscale"]
+    gs = tr.grad_scale("human")
     diag = {}
     for name, dev_val in (("dL/dfc", st["bwd"].dfeat[:n].cpu().numpy()), ("dL/dxc", st["dbufs"].dxc[:n].cpu().numpy()[:, :3]),
                           ("dL/dfd", st["dbufs"].d_dfeat[:n].cpu().numpy())):
@@ -473,7 +480,7 @@ def test_device_gradients_vs_f64_oracle(setup):
     got = {"ctable": st["tgrad"].cpu().numpy(), "dtable": st["dtgrad"].cpu().numpy()}
     got.update({k: g.cpu().numpy() for k, g in P.G.items()})
     got.update({k: g.cpu().numpy() for k, g in D.G.items()})
-    got = {k: v / st["gscale"] for k, v in got.items()}  # loss scaling divided out
+    got = {k: v / gs for k, v in got.items()}  # loss scaling divided out
     worst = {}
     for k in GRAD_TOL:
         scale = np.abs(ref[k]).max()
@@ -491,7 +498,7 @@ def test_render_between_steps_does_not_leak(setup):
     sc, hf, of, r, tr, batches = setup
     b = batches[1]
     st = tr.fields[0]
-    seed = tr.seed
+    step0 = int(tr.step_dev.item())  # the sampling seed advances with the device step counter
     s1 = run_frame(tr, b, st).cpu().numpy()
     g1 = st["tgrad"].clone()
     cam = sc.camera
@@ -499,7 +506,7 @@ def test_render_between_steps_does_not_leak(setup):
     t2 = np.asarray(cam.t, dtype=np.float64) + np.array([0.7, 0.0, 0.1])
     r.set_frame(sc.node_dqs(5), sc.theta(5), sc.bone_transforms(5), *sc.object_pose(5))
     img_a = r.render(cam.R, t2, cam.fx, cam.fy, cam.cx, cam.cy).clone()
-    tr.seed = seed
+    tr.step_dev.fill_(step0)
     s2 = run_frame(tr, b, st).cpu().numpy()
     # (loss sums and table gradients are float atomics: equal up to summation order)
     assert np.allclose(s1, s2, rtol=1e-5, atol=0), (s1, s2)
@@ -511,11 +518,11 @@ def test_render_between_steps_does_not_leak(setup):
     r.set_frame(sc.node_dqs(5), sc.theta(5), sc.bone_transforms(5), *sc.object_pose(5))
     img_a = r.render(cam.R, t2, cam.fx, cam.fy, cam.cx, cam.cy).clone()
     lr = (tr.cfg.lr_hash, tr.cfg.lr_net)
-    tr.cfg.lr_hash = tr.cfg.lr_net = 0.0
+    tr.set_learning_rates(0.0, 0.0)
     try:
         tr.step(batches)
     finally:
-        tr.cfg.lr_hash, tr.cfg.lr_net = lr
+        tr.set_learning_rates(*lr)
     img_b = r.render(cam.R, t2, cam.fx, cam.fy, cam.cx, cam.cy).clone()
     torch.cuda.synchronize()
     assert torch.equal(img_a, img_b)
