@@ -65,6 +65,11 @@ int cf_selftest_exact_div(int64_t n, uint64_t seed, int64_t* mismatches);
 /* anchors[i] = dq_apply(dqs[i], nodes[i]) in float64, bit-identical to the
  * reference's numpy evaluation order (edgraph.py:134-136). */
 int cf_deform_nodes(const double* nodes, const double* dqs, int64_t n, double* anchors, void* stream);
+/* graphs of n <= 1024 nodes: the deformed nodes plus the frame's anchor block read by
+ * cf_human_canon (float64 + fp32 copies, bbox; cf_anchor_block_bytes(n) bytes, 16-byte aligned) */
+int cf_anchor_block_bytes(int64_t n, int64_t* bytes);
+int cf_deform_nodes_block(const double* nodes, const double* dqs, int64_t n, double* anchors, void* block,
+                          void* stream);
 
 /* Coarse voxel buckets over a point set (ED anchors or posed skin vertices):
  * counting sort of point ids into a uniform grid, rebuilt per frame into
@@ -250,9 +255,10 @@ typedef struct cf_human_warp {
   double lbs_max_d2;
   double canon_min[3];      /* canonical unit-cube normalisation */
   double inv_side;
-  const double* anchors;    /* (n,3) deformed nodes of the frame; with n_nodes <= 1024 the
-                               k-NN scans them from shared memory (anchor_buckets may be NULL) */
+  const double* anchors;    /* (n,3) deformed nodes of the frame */
   int n_nodes;
+  const void* anchor_block; /* n_nodes <= 1024: the frame's anchor block (cf_deform_nodes_block), which the
+                               k-NN scans with warp-cooperative culling (anchor_buckets may be NULL) */
 } cf_human_warp;
 
 int cf_camera_rays(const cf_camera* cam, double* dirs, void* stream);

@@ -27,6 +27,81 @@ __global__ void deform_nodes_kernel(const double* __restrict__ nodes, const doub
   pdl_trigger();
 }
 
+// Small graphs (n <= 1024, one CTA): the deformed nodes plus the per-frame anchor
+// block the canonicalisation reads straight from L1 — float64 copies (double4), fp32
+// copies (float4, [0].w = max |coordinate|) and the float64 bbox — built once per
+// frame instead of once per CTA of every canonicalisation launch.
+__global__ void __launch_bounds__(1024) deform_nodes_block_kernel(const double* __restrict__ nodes,
+                                                                  const double* __restrict__ dqs, int n,
+                                                                  double* __restrict__ anchors,
+                                                                  uint8_t* __restrict__ block) {
+  pdl_wait();
+  double4* a64 = reinterpret_cast<double4*>(block);
+  float4* a32 = reinterpret_cast<float4*>(block + 32 * (size_t)n);
+  double* box = reinterpret_cast<double*>(block + 48 * (size_t)n);
+  __shared__ double s_lo[32][3], s_hi[32][3];
+  __shared__ float s_mag[32];
+  const int i = threadIdx.x, lane = i & 31, warp = i >> 5;
+  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  float mag = 0.f;
+  float4 af = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (i < n) {
+    const d3 a = dq_apply(load_dq(dqs + 8 * (int64_t)i), load_d3(nodes + 3 * (int64_t)i));
+    store_d3(anchors + 3 * (int64_t)i, a);
+    a64[i] = make_double4(a.x, a.y, a.z, 0.0);
+    af = make_float4((float)a.x, (float)a.y, (float)a.z, 0.f);
+    mag = fmaxf(fabsf(af.x), fmaxf(fabsf(af.y), fabsf(af.z)));
+    lo[0] = hi[0] = a.x;
+    lo[1] = hi[1] = a.y;
+    lo[2] = hi[2] = a.z;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mag = fmaxf(mag, __shfl_xor_sync(0xffffffffu, mag, o));
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = fmin(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+      hi[a] = fmax(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+    }
+  }
+  if (lane == 0) {
+    s_mag[warp] = mag;
+    for (int a = 0; a < 3; ++a) {
+      s_lo[warp][a] = lo[a];
+      s_hi[warp][a] = hi[a];
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = (int)(blockDim.x >> 5);
+    mag = lane < nw ? s_mag[lane] : 0.f;
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = lane < nw ? s_lo[lane][a] : INFINITY;
+      hi[a] = lane < nw ? s_hi[lane][a] : -INFINITY;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mag = fmaxf(mag, __shfl_xor_sync(0xffffffffu, mag, o));
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        lo[a] = fmin(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+        hi[a] = fmax(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+      }
+    }
+    if (lane == 0) {
+      for (int a = 0; a < 3; ++a) {
+        box[a] = lo[a];
+        box[3 + a] = hi[a];
+      }
+      s_mag[0] = mag;
+    }
+  }
+  __syncthreads();
+  if (i == 0) af.w = s_mag[0];
+  if (i < n) a32[i] = af;
+  pdl_trigger();
+}
+
 // ------------------------------------------------------------------ buckets
 
 // grid of G cells along the longest extent of the bbox [mn, mx]
@@ -647,6 +722,21 @@ int cf_deform_nodes(const double* nodes, const double* dqs, int64_t n, double* a
   if (n == 0) return CF_OK;
   cf::launch_pdl(deform_nodes_kernel, cf::grid_for(n, 128, 4), 128, 0, cf::as_stream(stream), nodes, dqs, n, anchors);
   return cf::check_launch("cf_deform_nodes");
+}
+
+int cf_anchor_block_bytes(int64_t n, int64_t* bytes) {
+  if (n < 0 || !bytes) return cf::fail(CF_E_BAD_ARG, "cf_anchor_block_bytes: bad args");
+  *bytes = 48 * n + 48;
+  return CF_OK;
+}
+
+int cf_deform_nodes_block(const double* nodes, const double* dqs, int64_t n, double* anchors, void* block,
+                          void* stream) {
+  if (n < 1 || n > 1024 || !nodes || !dqs || !anchors || !block || reinterpret_cast<uintptr_t>(block) % 16 != 0)
+    return cf::fail(CF_E_BAD_ARG, "cf_deform_nodes_block: bad args (1 <= n <= 1024, 16-byte aligned block)");
+  cf::launch_pdl(deform_nodes_block_kernel, 1, 1024, 0, cf::as_stream(stream), nodes, dqs, (int)n, anchors,
+                 static_cast<uint8_t*>(block));
+  return cf::check_launch("cf_deform_nodes_block");
 }
 
 int cf_buckets_create(int64_t max_points, int max_grid_res, cf_buckets_t** out) {

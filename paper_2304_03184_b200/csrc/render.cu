@@ -13,7 +13,7 @@
 namespace {
 
 #ifndef CF_CANON_MINB
-#define CF_CANON_MINB 4  // resident CTAs/SM the canonicalisation kernel is compiled for
+#define CF_CANON_MINB 5  // resident CTAs/SM the canonicalisation kernel is compiled for
 #endif
 // graphs up to this many nodes are scanned exhaustively from shared memory
 // (cheaper than the bucket ring search's divergent loops at render sizes)
@@ -598,9 +598,16 @@ __device__ __forceinline__ float4 canon_out(const cf_human_warp& W, d3 pt, float
                      __double2float_rn(x_mul(x_sub(pt.z, W.canon_min[2]), W.inv_side)), flag);
 }
 
-// human samples: live point -> ED backward warp (exact bucketed k-NN + DQB^-1),
-// falling back to backward LBS outside the ED support; -> canonical unit cube
-template <int K, bool kSmem>
+// human samples: live point -> ED backward warp (exact k-NN + DQB^-1), falling back
+// to backward LBS outside the ED support; -> canonical unit cube.
+// kBlock (graphs of <= 1024 nodes): the k-NN scans the frame's anchor block
+// (cf_deform_nodes_block: float64 + fp32 copies, bbox; 48 B per node), copied into
+// shared memory once per CTA (one barrier; reading it through L1 instead measured
+// 72 -> 82 us), with the warp-cooperative culling; else the coarse buckets. Warps
+// pull 32-sample chunks from a ticket
+// (count[2]; per-chunk cost varies with the LBS fallback and the candidate-set
+// size), fetching the next ticket while the current chunk runs.
+template <int K, bool kBlock>
 __global__ void __launch_bounds__(128, CF_CANON_MINB) human_canon_kernel(cf_march_desc M, const double* __restrict__ dirs,
                                                           const uint32_t* __restrict__ records,
                                                           int* count, int64_t capacity,
@@ -609,71 +616,34 @@ __global__ void __launch_bounds__(128, CF_CANON_MINB) human_canon_kernel(cf_marc
                                                           const BucketParams* __restrict__ LPp,
                                                           const int* __restrict__ lcs, const double4* __restrict__ ls,
                                                           float4* __restrict__ xu) {
+  extern __shared__ __align__(16) uint8_t s_blk[];  // kBlock: the anchor block (48 n + 48 B)
   pdl_wait();
-  __shared__ BucketParams sE, sL;
-  extern __shared__ double4 s_anchors[];  // kSmem: the frame's deformed nodes (+ fp32 copies)
-  float4* s_af = reinterpret_cast<float4*>(s_anchors + (kSmem ? W.n_nodes : 0));
-  __shared__ unsigned s_mag;
-  __shared__ double s_box[6];
-  if (threadIdx.x == 0) {
-    if (!kSmem) sE = *EPp;
-    if (LPp) sL = *LPp;
-    s_mag = 0u;
-  }
-  __syncthreads();
-  if (kSmem) {
-    float mag = 0.f;
-    for (int i = threadIdx.x; i < W.n_nodes; i += blockDim.x) {
-      const double x = W.anchors[3 * i], y = W.anchors[3 * i + 1], z = W.anchors[3 * i + 2];
-      s_anchors[i] = make_double4(x, y, z, 0.0);
-      s_af[i] = make_float4((float)x, (float)y, (float)z, 0.f);
-      mag = fmaxf(mag, fmaxf(fabsf((float)x), fmaxf(fabsf((float)y), fabsf((float)z))));
-    }
-    atomicMax(&s_mag, __float_as_uint(mag));  // non-negative floats order as their bits
+  if (kBlock) {  // one coalesced copy of the prebuilt block, one barrier
+    const int words = (48 * W.n_nodes + 48) / 16;
+    const uint4* src = static_cast<const uint4*>(W.anchor_block);
+    for (int i = threadIdx.x; i < words; i += blockDim.x) reinterpret_cast<uint4*>(s_blk)[i] = src[i];
     __syncthreads();
-    if (threadIdx.x == 0) s_af[0].w = __uint_as_float(s_mag);
-    // float64 bbox of the anchors (warp 0), for the ED-support early-out below
-    if (threadIdx.x < 32) {
-      double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
-      for (int i = threadIdx.x; i < W.n_nodes; i += 32) {
-        const double4 a = s_anchors[i];
-        lo[0] = fmin(lo[0], a.x), lo[1] = fmin(lo[1], a.y), lo[2] = fmin(lo[2], a.z);
-        hi[0] = fmax(hi[0], a.x), hi[1] = fmax(hi[1], a.y), hi[2] = fmax(hi[2], a.z);
-      }
-#pragma unroll
-      for (int a = 0; a < 3; ++a)
-        for (int off = 16; off > 0; off >>= 1) {
-          lo[a] = fmin(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], off));
-          hi[a] = fmax(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], off));
-        }
-      if (threadIdx.x == 0)
-        for (int a = 0; a < 3; ++a) {
-          s_box[a] = lo[a];
-          s_box[3 + a] = hi[a];
-        }
-    }
   }
-  __syncthreads();
+  const double4* a64 = reinterpret_cast<const double4*>(s_blk);
+  const float4* a32 = reinterpret_cast<const float4*>(s_blk + 32 * (size_t)W.n_nodes);
+  const double* box = reinterpret_cast<const double*>(s_blk + 48 * (size_t)W.n_nodes);
   // A sample farther than R from the anchors' bbox has every Gaussian weight
   // below the validity floor: d^2 / r^2 > -ln(1e-6) (1 + 1e-5) => w < 1e-6. Such
   // samples skip the k-NN (ED invalid, as the exact evaluation would find) and
   // stay out of the warp's culling box — training's uniform samples along the
   // whole ray [0.3 m, 5 m] are mostly of this kind.
   const double rsup2 = 13.815510557964274 * W.r2 * (1.0 + 1e-5);
-  __shared__ double s_fr[15];
-  load_frame(M, s_fr);
+  const d3 o = M.frame ? d3{M.frame[0], M.frame[1], M.frame[2]} : d3{M.origin[0], M.origin[1], M.origin[2]};
   const int64_t n = min((int64_t)count[0], capacity);
-  const d3 o{s_fr[0], s_fr[1], s_fr[2]};
-  // warps pull 32-sample chunks from a ticket (count[2]): per-chunk cost varies
-  // (LBS fallback, candidate-set size), so static striding leaves a long tail.
-  // Warp-uniform trip count: the culled scan is warp-cooperative.
+  const int lane = threadIdx.x & 31;
   int* ticket = count + 2;
-  for (;;) {
-    int64_t base = 0;
-    if ((threadIdx.x & 31) == 0) base = atomicAdd(ticket, 32);
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (base >= n) break;
-    const int64_t s = base + (threadIdx.x & 31);
+  int64_t base = 0;
+  if (lane == 0) base = atomicAdd(ticket, 32);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  while (base < n) {  // warp-uniform: the culled scan is warp-cooperative
+    int64_t next = 0;
+    if (lane == 0) next = atomicAdd(ticket, 32);  // in flight while this chunk runs
+    const int64_t s = base + lane;
     const bool live = s < n;
     const uint32_t rec = live ? records[s] : 0u;
     const int64_t ray = rec >> 8;
@@ -681,28 +651,29 @@ __global__ void __launch_bounds__(128, CF_CANON_MINB) human_canon_kernel(cf_marc
     d3 pt;
     float flag = 0.0f;
     bool near = live;
-    if (kSmem && live) {
+    if (kBlock && live) {
       const double q[3] = {p.x, p.y, p.z};
       double d2 = 0.0;
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
-        const double e = fmax(fmax(s_box[a] - q[a], q[a] - s_box[3 + a]), 0.0);
+        const double e = fmax(fmax(box[a] - q[a], q[a] - box[3 + a]), 0.0);
         d2 += e * e;
       }
       near = d2 <= rsup2;
     }
-    const bool ed_ok = kSmem ? ed_warp_point_cull<K>(s_anchors, s_af, W.n_nodes, W.dqs, W.k, W.r2, true, p, near, pt)
-                             : (live && ed_warp_point<K>(sE, ecs, es, W.dqs, W.k, W.r2, true, p, pt));
-    if (!live) continue;
-    if (ed_ok) flag = 1.0f;
-    else if (LPp && lbs_fallback(sL, lcs, ls, W, p, pt)) flag = 2.0f;
-    xu[s] = canon_out(W, pt, flag);
+    const bool ed_ok = kBlock ? ed_warp_point_cull<K>(a64, a32, W.n_nodes, W.dqs, W.k, W.r2, true, p, near, pt)
+                              : (live && ed_warp_point<K>(*EPp, ecs, es, W.dqs, W.k, W.r2, true, p, pt));
+    if (live) {
+      if (ed_ok) flag = 1.0f;
+      else if (LPp && lbs_fallback(*LPp, lcs, ls, W, p, pt)) flag = 2.0f;
+      xu[s] = canon_out(W, pt, flag);
+    }
+    base = __shfl_sync(0xffffffffu, next, 0);
   }
-  // the last CTA out re-arms the ticket for the next launch on these counters
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  // the last warp out re-arms the ticket for the next launch on these counters
+  if (lane == 0) {
     __threadfence();
-    if (atomicAdd(ticket + 1, 1) == (int)gridDim.x - 1) {
+    if (atomicAdd(ticket + 1, 1) == (int)(gridDim.x * (blockDim.x >> 5)) - 1) {
       ticket[0] = 0;
       ticket[1] = 0;
     }
@@ -1178,12 +1149,14 @@ int cf_rays_march(const cf_camera* cam, const cf_march_desc* M, double* dirs, co
 int cf_human_canon(const cf_march_desc* M, const double* dirs, const cf_march_out* F, const cf_human_warp* W,
                    const cf_buckets_t* anchor_buckets, const cf_buckets_t* vert_buckets, float* xu_f, void* stream) {
   float4* xu = reinterpret_cast<float4*>(xu_f);
-  const bool smem = W && W->anchors && W->n_nodes > 0 && W->n_nodes <= kSmemAnchors;
+  const bool smem = W && W->anchor_block && W->n_nodes > 0 && W->n_nodes <= kSmemAnchors;
   if (!M || !F || !W || W->k < 1 || W->k > 8 || (!smem && (!anchor_buckets || anchor_buckets->grid_res == 0)))
     return cf::fail(CF_E_BAD_ARG, "cf_human_canon: bad args");
+  if (W->n_nodes > 0 && W->n_nodes <= kSmemAnchors && !W->anchor_block)
+    return cf::fail(CF_E_BAD_ARG, "cf_human_canon: graphs of <= 1024 nodes need the anchor block (cf_deform_nodes_block)");
   const bool lbs = vert_buckets && W->vert_Tinv;
   cudaStream_t st = cf::as_stream(stream);
-  const size_t dsm = smem ? (sizeof(double4) + sizeof(float4)) * W->n_nodes : 0;
+  const size_t dsm = smem ? (size_t)(48 * W->n_nodes + 48) : 0;
   // persistent: exactly the resident CTAs (the ticket balances the work)
 #define CF_HC(KK, SM)                                                                                             \
   int per_sm = 0;                                                                                                \

@@ -416,6 +416,11 @@ class Renderer:
             w.inv_side = h.inv_side
             w.anchors = self._anchors.data_ptr()
             w.n_nodes = int(self._anchors.shape[0])
+            if w.n_nodes <= 1024:  # the frame's anchor block for the culled k-NN (cf_deform_nodes_block)
+                nb = ctypes.c_int64()
+                _lib.call("cf_anchor_block_bytes", w.n_nodes, ctypes.byref(nb))
+                self._anchor_block = torch.empty(int(nb.value), dtype=torch.uint8, device=self.dirs.device)
+                w.anchor_block = self._anchor_block.data_ptr()
             self.hw = w
             self.hdesc = h.desc(self.dbias, self.cfg.precision)
 
@@ -454,7 +459,11 @@ class Renderer:
                           offsets.ctypes.data, len(parents), self._A.data_ptr(), ss)
                 _lib.call("cf_pose_bias", h.nets.d1.data_ptr(), 32 + 3 * len(parents), 32, 128,
                           self._theta.data_ptr(), 3 * len(parents), self.dbias.data_ptr(), ss)
-            _lib.call("cf_deform_nodes", h.nodes.data_ptr(), self._dqs.data_ptr(), n, self._anchors.data_ptr(), ss)
+            if n <= 1024:
+                _lib.call("cf_deform_nodes_block", h.nodes.data_ptr(), self._dqs.data_ptr(), n,
+                          self._anchors.data_ptr(), self._anchor_block.data_ptr(), ss)
+            else:
+                _lib.call("cf_deform_nodes", h.nodes.data_ptr(), self._dqs.data_ptr(), n, self._anchors.data_ptr(), ss)
             if n > 1024:  # small graphs are scanned from shared memory (no buckets needed)
                 self._anchor_buckets.build(self._anchors)
             h.lbs.set_pose(self._A)
