@@ -336,6 +336,16 @@ typedef struct cf_field_desc {
   int train;                /* 1 = the training forward: 32-bit semantics (as precise) plus the fp16 saves of
                                the backward, feature-major in the scratch (cf_field_train_layout) */
 } cf_field_desc;
+/* occupancy from the trained density (the builder's K12; SPEC.md:429 leaves ray-marching
+ * acceleration open): per cell of a res^3 grid over the field's unit cube, the E_g density
+ * logit g0 at the centre u = (i + 0.5) / res, exact fp32 (hash features as cf_hash_encode,
+ * W1 (64 x 32) / W2 (16 x 64, row 0) fp32 master weights, un-contracted sequential sums);
+ * logits (res^3, init -inf) = max(logits + log_decay, g0); bits = (logits > log_threshold)
+ * dilated by `dilate` cells per axis (Chebyshev; the DeformNet offset bound for the human).
+ * x-major cells ((x * res + y) * res + z), 32 z-cells per word; res % 32 == 0; scratch = res^3/32 words */
+int cf_density_grid_update(const cf_hashgrid_desc* G, const float* table, const float* W1, const float* W2, int res,
+                           float log_decay, float log_threshold, int dilate, float* logits, uint32_t* bits,
+                           uint32_t* scratch, void* stream);
 /* device scratch needed by cf_field_forward for `capacity` samples */
 int cf_field_scratch_bytes(const cf_field_desc* F, int64_t capacity, int64_t* bytes);
 /* scratch layout (S = capacity): fp16 mode: cfeat (S,32) fp16 | dfeat (S,32) fp16 | xc (S) float4;

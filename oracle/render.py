@@ -274,3 +274,52 @@ def train_samples(gt_depth, mask, t_near, t_far, n_guided, n_uniform, n_empty, s
                 merged.append(b[k]); k += 1
         out.append(np.array(merged))
     return out
+
+
+def density_logits(table, W1, W2, res):
+    """E_g density logit g0 at every cell centre u = (i + 0.5) / res of a res^3 grid,
+    x-major, restating density_grid_kernel (field.cu) bit for bit: hash features as
+    hash_encode (fp32, bit-exact with the kernels), then un-contracted fp32 sums in the
+    kernel's order: a_j = sum_i W1[j, i] f_i (i ascending), g0 = sum_j W2[0, j] relu(a_j)."""
+    u = ((np.arange(res, dtype=np.float64) + 0.5) / res).astype(np.float32)
+    x, y, z = np.meshgrid(u, u, u, indexing="ij")
+    pts = np.stack([x.ravel(), y.ravel(), z.ravel()], 1)
+    f = on.hash_encode(table, pts).astype(np.float32)
+    W1 = np.asarray(W1, dtype=np.float32)
+    W2 = np.asarray(W2, dtype=np.float32)
+    g0 = None
+    for j in range(64):
+        a = W1[j, 0] * f[:, 0]
+        for i in range(1, 32):
+            a = a + W1[j, i] * f[:, i]
+        h = np.maximum(a, np.float32(0))
+        g0 = W2[0, 0] * h if j == 0 else g0 + W2[0, j] * h
+    return g0
+
+
+def dilate_box(on_grid, r):
+    """Chebyshev (box) dilation of a (res, res, res) bool grid by r cells per axis, no wrap."""
+    out = on_grid.copy()
+    for axis in range(3):
+        src = out.copy()
+        n = src.shape[axis]
+        for k in range(1, r + 1):
+            if k >= n:
+                break
+            sl_dst = [slice(None)] * 3
+            sl_src = [slice(None)] * 3
+            sl_dst[axis], sl_src[axis] = slice(k, None), slice(0, n - k)
+            out[tuple(sl_dst)] |= src[tuple(sl_src)]
+            sl_dst[axis], sl_src[axis] = slice(0, n - k), slice(k, None)
+            out[tuple(sl_dst)] |= src[tuple(sl_src)]
+    return out
+
+
+def density_grid_update(logits, g0, log_decay, log_thr, res, dilate):
+    """cf_density_grid_update's decisions: g = max(logits + log_decay, g0) in fp32,
+    occupied = g > log_threshold, box-dilated by `dilate` cells -> (g, flat bool bits)."""
+    g = np.maximum(np.asarray(logits, dtype=np.float32) + np.float32(log_decay), np.asarray(g0, dtype=np.float32))
+    occ = (g > np.float32(log_thr)).reshape(res, res, res)
+    if dilate > 0:
+        occ = dilate_box(occ, dilate)
+    return g, occ.ravel()

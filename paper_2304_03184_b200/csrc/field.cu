@@ -1395,6 +1395,82 @@ __global__ void __launch_bounds__(128) hash_bwd_dx_kernel(cf_hashgrid_desc D, co
   }
 }
 
+// ---------------------------------------------------------------- density grid (occupancy refresh)
+// Occupancy from the trained density (K12; the SPEC leaves ray-marching acceleration
+// open): per cell of a res^3 grid over the field's unit cube, the E_g
+// density logit g0 (sigma = exp(g0)) at the cell centre u = (i + 0.5) / res (fp32 of
+// the float64 quotient), hash features exactly as hash_features, the MLP in fp32 with
+// un-contracted sequential sums (a_j = sum_i W1[j][i] f_i in i order, then
+// g0 = sum_j W2[0][j] relu(a_j) in j order). Kept as a log-density with a max-decay
+// update g = max(g + log_decay, g0) (an EMA of the max density in log space), the
+// cell is occupied when g > log_threshold. Every operation is an exact fp32 op, so
+// the oracle restates it bit for bit. One warp = 32 consecutive z cells = one word.
+__global__ void __launch_bounds__(256) density_grid_kernel(cf_hashgrid_desc D, const float* __restrict__ table,
+                                                           const float* __restrict__ W1, const float* __restrict__ W2,
+                                                           int res, float log_decay, float log_thr,
+                                                           float* __restrict__ logits, uint32_t* __restrict__ raw) {
+  __shared__ float sW1[64 * 32], sW2[64];
+  for (int i = threadIdx.x; i < 64 * 32; i += blockDim.x) sW1[i] = W1[i];
+  if (threadIdx.x < 64) sW2[threadIdx.x] = W2[threadIdx.x];
+  __syncthreads();
+  const int64_t total = (int64_t)res * res * res;
+  const double inv = 1.0 / (double)res;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c - (threadIdx.x & 31) < total;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    bool on = false;
+    if (c < total) {
+      const int64_t x = c / ((int64_t)res * res), y = (c / res) % res, z = c % res;
+      const float ux = __double2float_rn(((double)x + 0.5) * inv), uy = __double2float_rn(((double)y + 0.5) * inv),
+                  uz = __double2float_rn(((double)z + 0.5) * inv);
+      float f[32];
+      hash_features<2, 16, 4, float>(D, table, ux, uy, uz, f);
+      float g0 = 0.0f;
+      for (int j = 0; j < 64; ++j) {
+        float a = f_mul(sW1[j * 32], f[0]);
+#pragma unroll
+        for (int i = 1; i < 32; ++i) a = f_add(a, f_mul(sW1[j * 32 + i], f[i]));
+        const float h = fmaxf(a, 0.0f);
+        g0 = j == 0 ? f_mul(sW2[0], h) : f_add(g0, f_mul(sW2[j], h));
+      }
+      const float g = fmaxf(f_add(logits[c], log_decay), g0);
+      logits[c] = g;
+      on = g > log_thr;
+    }
+    const unsigned word = __ballot_sync(0xffffffffu, on);
+    if ((threadIdx.x & 31) == 0 && c < total) raw[c >> 5] = word;
+  }
+}
+
+// Chebyshev (box) dilation of a bit grid by r cells along one axis (0 = z, within and
+// across the 32-cell words; 1 = y; 2 = x), no wrap. res % 32 == 0.
+__global__ void bits_dilate_kernel(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst, int res, int axis,
+                                   int r) {
+  const int wpr = res / 32;  // words per z row
+  const int64_t words = (int64_t)res * res * wpr;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < words; w += (int64_t)gridDim.x * blockDim.x) {
+    const int zw = (int)(w % wpr);
+    const int64_t row = w / wpr;  // x * res + y
+    const int y = (int)(row % res), x = (int)(row / res);
+    uint32_t v = src[w];
+    if (axis == 0) {
+      const uint64_t lo = zw > 0 ? src[w - 1] : 0u, hi = zw + 1 < wpr ? src[w + 1] : 0u;
+      const uint64_t cur = src[w];
+      for (int k = 1; k <= r; ++k) {
+        // bit b of the result sees bits b - k (from lower z) and b + k (from higher z)
+        v |= (uint32_t)((cur << k) | (lo >> (32 - k)));
+        v |= (uint32_t)((cur >> k) | (hi << (32 - k)));
+      }
+    } else {
+      for (int k = -r; k <= r; ++k) {
+        const int yy = axis == 1 ? y + k : y, xx = axis == 2 ? x + k : x;
+        if (k == 0 || yy < 0 || yy >= res || xx < 0 || xx >= res) continue;
+        v |= src[((int64_t)xx * res + yy) * wpr + zw];
+      }
+    }
+    dst[w] = v;
+  }
+}
+
 unsigned persistent_grid(int64_t capacity, int slots) {
   const int64_t tiles = (capacity + 127) / 128;
   int64_t g = (tiles + slots - 1) / slots;
@@ -1525,6 +1601,26 @@ int field_stage_precise(const cf_field_desc* FD, const cf_march_out* S, const do
 }  // namespace
 
 extern "C" {
+
+int cf_density_grid_update(const cf_hashgrid_desc* G, const float* table, const float* W1, const float* W2, int res,
+                           float log_decay, float log_threshold, int dilate, float* logits, uint32_t* bits,
+                           uint32_t* scratch, void* stream) {
+  if (!G || !table || !W1 || !W2 || res < 32 || res % 32 != 0 || dilate < 0 || dilate > 32 || !logits || !bits ||
+      !scratch || G->n_features != 2 || G->n_levels != 16)
+    return cf::fail(CF_E_BAD_ARG, "cf_density_grid_update: bad args (16 x F2 grid, res % 32 == 0)");
+  cudaStream_t st = cf::as_stream(stream);
+  const int64_t total = (int64_t)res * res * res, words = total / 32;
+  uint32_t* raw = dilate > 0 ? scratch : bits;
+  density_grid_kernel<<<cf::grid_for(total, 256, 8), 256, 0, st>>>(*G, table, W1, W2, res, log_decay, log_threshold,
+                                                                   logits, raw);
+  if (dilate > 0) {
+    const unsigned g = cf::grid_for(words, 256, 8);
+    bits_dilate_kernel<<<g, 256, 0, st>>>(scratch, bits, res, 0, dilate);
+    bits_dilate_kernel<<<g, 256, 0, st>>>(bits, scratch, res, 1, dilate);
+    bits_dilate_kernel<<<g, 256, 0, st>>>(scratch, bits, res, 2, dilate);
+  }
+  return cf::check_launch("cf_density_grid_update");
+}
 
 int cf_field_train_layout(int64_t capacity, int64_t* offsets) {
   if (capacity < 0 || !offsets) return cf::fail(CF_E_BAD_ARG, "cf_field_train_layout: bad args");

@@ -66,6 +66,11 @@ class RenderConfig:
     canon_occ_radius: float = 0.03   # geometry-initialised density bits
     obj_occ_res: int = 64
     obj_shell: float = 0.02
+    # occupancy refresh from the trained density (refresh_occupancy): a cell is occupied
+    # when its max-decayed density keeps one sample's opacity 1 - exp(-sigma dt) above
+    # occ_alpha; the log-density decays by occ_decay per refresh
+    occ_alpha: float = 0.01
+    occ_decay: float = 0.95
     background: tuple = (24 / 255.0, 28 / 255.0, 34 / 255.0)   # config.py bg_r/g/b
     # "fp32": fp32 hash tables and features, split-fp16 (hi + lo) tensor-core MLP operands —
     # the SPEC's 32-bit semantics within 1e-4; "fp16": fp16 operands and
@@ -84,6 +89,22 @@ def _precise(precision: str) -> bool:
 def _kaiming(rng, n_out, n_in):
     b = np.sqrt(6.0 / n_in)
     return rng.uniform(-b, b, size=(n_out, n_in))
+
+
+def _refresh_density(field, W1, W2, dt, dilate, bits) -> None:
+    cfg = field.cgrid.table.device
+    res = field.occ.res if isinstance(field, ObjectField) else field.cfg.canon_occ_res
+    if getattr(field, "density_logits", None) is None:
+        field.density_logits = torch.full((res ** 3,), float("-inf"), dtype=torch.float32, device=cfg)
+        field._density_scratch = torch.empty(res ** 3 // 32, dtype=torch.int32, device=cfg)
+    c = field.cfg
+    log_thr = float(np.log(-np.log1p(-c.occ_alpha) / dt))  # sigma_thr = -ln(1 - alpha) / dt
+    W1 = W1.to(torch.float32).contiguous()
+    W2 = W2.to(torch.float32).contiguous()
+    _lib.call("cf_density_grid_update", _lib.byref(field.cgrid.desc), field.cgrid.table.data_ptr(), W1.data_ptr(),
+              W2.data_ptr(), res, float(np.log(c.occ_decay)), log_thr, dilate, field.density_logits.data_ptr(),
+              bits.data_ptr(), field._density_scratch.data_ptr(), _lib.stream_ptr())
+    field._density_keep = (W1, W2)  # alive until the stream-ordered kernel ran
 
 
 def occ_grid(gmin, size, res) -> _lib.OccGrid:
@@ -172,20 +193,33 @@ class HumanField:
         self.build_occ_cache()
 
     def build_occ_cache(self) -> None:
-        """Static canonical k-NN of the occupied cells (re-run when canon_bits change)."""
+        """Static canonical k-NN of the occupied cells (re-run when canon_bits change; the
+        buffers hold every cell of the grid, so a refresh never reallocates them and views
+        captured in CUDA graphs stay valid; the count lives on the device)."""
         cfg = self.cfg
-        n_on = int(torch.bitwise_count(self.canon_bits).sum()) if hasattr(torch, "bitwise_count") else \
-            int(np.unpackbits(self.canon_bits.cpu().numpy().view(np.uint8)).sum())
-        cap = max(n_on, 1)
         d = self.nodes.device
-        self.occ_cells = torch.empty(cap, dtype=torch.int32, device=d)
-        self.occ_nbr = torch.empty((cap, cfg.ed_k), dtype=torch.int32, device=d)
-        self.occ_w = torch.empty((cap, cfg.ed_k), dtype=torch.float64, device=d)
-        self.occ_count = torch.zeros(1, dtype=torch.int32, device=d)
-        self.occ_cap = cap
+        if getattr(self, "occ_cells", None) is None:
+            cap = cfg.canon_occ_res ** 3
+            self.occ_cells = torch.empty(cap, dtype=torch.int32, device=d)
+            self.occ_nbr = torch.empty((cap, cfg.ed_k), dtype=torch.int32, device=d)
+            self.occ_w = torch.empty((cap, cfg.ed_k), dtype=torch.float64, device=d)
+            self.occ_count = torch.zeros(1, dtype=torch.int32, device=d)
+            self.occ_cap = cap
+        cap = self.occ_cap
         _lib.call("cf_occ_cache", self.canon_bits.data_ptr(), _lib.byref(self.canon_occ), self.node_buckets.handle,
                   cfg.ed_k, cfg.ed_radius, cap, self.occ_cells.data_ptr(), self.occ_nbr.data_ptr(),
                   self.occ_w.data_ptr(), self.occ_count.data_ptr(), _lib.stream_ptr())
+
+    def refresh_occupancy(self, W1: torch.Tensor, W2: torch.Tensor, dt: float) -> None:
+        """Canonical density bits from the trained field (cf_density_grid_update): the
+        E_g density at the canonical cell centres, max-decayed, thresholded at the
+        density whose one-sample opacity is cfg.occ_alpha (sample spacing dt), dilated
+        by the DeformNet offset bound (|dv| <= 0.05 m per axis: a sample's canonical
+        point xu + dv is within that many cells of xu's cell), then the cached canonical
+        k-NN of the occupied cells is rebuilt. Replaces the geometry shell."""
+        _refresh_density(self, W1, W2, dt, int(np.ceil(0.05 / (self.side / self.cfg.canon_occ_res))),
+                         self.canon_bits)
+        self.build_occ_cache()
 
     def desc(self, dbias: torch.Tensor, precision: str | None = None) -> _lib.FieldDesc:
         precise = _precise(precision or self.cfg.precision)
@@ -222,6 +256,11 @@ class ObjectField:
         self.bits = torch.empty(nwords, dtype=torch.int32, device=self.cgrid.table.device)
         h = (ctypes.c_double * 3)(*self.half)
         _lib.call("cf_occ_box_shell", _lib.byref(self.occ), h, cfg.obj_shell, self.bits.data_ptr(), _lib.stream_ptr())
+
+    def refresh_occupancy(self, W1: torch.Tensor, W2: torch.Tensor, dt: float) -> None:
+        """Object density bits from the trained field (cf_density_grid_update, no dilation:
+        the object field has no deformation). Replaces the box shell."""
+        _refresh_density(self, W1, W2, dt, 0, self.bits)
 
     def desc(self, precision: str | None = None) -> _lib.FieldDesc:
         d = _lib.FieldDesc()

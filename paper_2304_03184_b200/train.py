@@ -510,6 +510,18 @@ class Trainer:
             self._pack = (_lib.PackItem * len(items))(*items)
         _lib.call("cf_pack_multi", self._pack, len(self._pack), _lib.stream_ptr())
 
+    def update_occupancy(self):
+        """Refresh both fields' occupancy bits from their trained density (the renderer's
+        march then skips what the field learned to be empty and keeps what it learned
+        to fill, instead of the geometry-initialised grids); run every few steps,
+        outside a captured step. The renderer's live occupancy is rebuilt with its next
+        view."""
+        dt = float(self.r.M.dt)
+        for st in self.fields:
+            W = st["params"].W
+            st["field"].refresh_occupancy(W["G1"], W["G2"], dt)
+        self.r._setup_pending = self.r.human is not None and getattr(self.r, "_dqs", None) is not None
+
     def set_learning_rates(self, lr_hash: float, lr_net: float):
         """New learning rates (the Adam launch table is rebuilt; a captured step must be
         captured again)."""

@@ -526,3 +526,23 @@ def test_render_between_steps_does_not_leak(setup):
     img_b = r.render(cam.R, t2, cam.fx, cam.fy, cam.cx, cam.cy).clone()
     torch.cuda.synchronize()
     assert torch.equal(img_a, img_b)
+
+
+def test_occupancy_refresh_after_training(setup):
+    """Trainer.update_occupancy: the fields' occupancy bits come from their trained
+    density (runs last: it replaces the geometry-initialised grids of the fixture)."""
+    sc, hf, of, r, tr, batches = setup
+    for _ in range(5):
+        tr.step(batches)
+    tr.update_occupancy()
+    torch.cuda.synchronize()
+    on_h = orr.unpack_bits(hf.canon_bits.cpu().numpy(), hf.cfg.canon_occ_res ** 3)
+    on_o = orr.unpack_bits(of.bits.cpu().numpy(), of.cfg.obj_occ_res ** 3)
+    # (45 steps from a random init have not taught the field where space is empty:
+    # most cells stay occupied; test_occupancy_gpu.py checks the decisions themselves)
+    assert on_h.sum() > 0 and on_o.sum() > 0
+    cam = sc.camera
+    r.set_frame(sc.node_dqs(2), sc.theta(2), sc.bone_transforms(2), *sc.object_pose(2))
+    img = r.render(cam.R, cam.t, cam.fx, cam.fy, cam.cx, cam.cy)
+    torch.cuda.synchronize()
+    assert torch.isfinite(img).all() and r.sample_counts()[0] > 0
