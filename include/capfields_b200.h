@@ -19,6 +19,8 @@
  * Reference interfaces replaced (the reference has no FFI; these are the Python
  * functions whose bodies the calls stand in for — see INTEGRATION.md):
  *   cf_deform_nodes            <- edgraph.deformed_nodes            edgraph.py:134-136
+ *   cf_dq_blend / cf_dq_status <- transforms.dq_blend                transforms.py:180-196
+ *   cf_dq_apply                <- transforms.dq_apply                transforms.py:174-177
  *   cf_knn_warp                <- edgraph.warp_backward_batch       edgraph.py:174-183
  *                                 edgraph.warp_forward_batch        edgraph.py:154-162
  *                                 knnfield.brute_force_query        knnfield.py:32-42
@@ -65,6 +67,17 @@ int cf_selftest_exact_div(int64_t n, uint64_t seed, int64_t* mismatches);
 /* anchors[i] = dq_apply(dqs[i], nodes[i]) in float64, bit-identical to the
  * reference's numpy evaluation order (edgraph.py:134-136). */
 int cf_deform_nodes(const double* nodes, const double* dqs, int64_t n, double* anchors, void* stream);
+/* dq_blend drop-in (transforms.py:180-196): n rows of k (weight, dq) pairs -> (n, 8) unit dual
+ * quaternions, bit-exact with the reference's numpy evaluation order; *err (device int, zeroed
+ * by the caller, optional) receives 2 for a negative weight, 1 for a row summing to <= 0 */
+int cf_dq_blend(const double* weights, const double* dqs, int64_t n, int k, double* out, int* err, void* stream);
+/* synchronises the stream and maps cf_dq_blend's *err to a status: CF_E_BAD_ARG (ValueError,
+ * negative weights), CF_E_DEGENERATE (DegenerateWeightsError, zero weights) or CF_OK */
+int cf_dq_status(const int* err, void* stream);
+/* dq_apply drop-in (transforms.py:174-177): row i = dq[i * dq_stride] applied to p[i * p_stride]
+ * (a stride of 0 broadcasts one dq / one point) */
+int cf_dq_apply(const double* dq, int64_t dq_stride, const double* p, int64_t p_stride, int64_t n, double* out,
+                void* stream);
 /* graphs of n <= 1024 nodes: the deformed nodes plus the frame's anchor block read by
  * cf_human_canon (float64 + fp32 copies, bbox; cf_anchor_block_bytes(n) bytes, 16-byte aligned) */
 int cf_anchor_block_bytes(int64_t n, int64_t* bytes);
@@ -77,6 +90,8 @@ int cf_deform_nodes_block(const double* nodes, const double* dqs, int64_t n, dou
 typedef struct cf_buckets cf_buckets_t;
 int cf_buckets_create(int64_t max_points, int max_grid_res, cf_buckets_t** out);
 int cf_buckets_destroy(cf_buckets_t* b);
+/* stream-ordered destroy: the buffers are freed after the work queued on `stream`, no host sync */
+int cf_buckets_destroy_async(cf_buckets_t* b, void* stream);
 /* grid_res <= 0 picks a resolution from n (~4 points per occupied cell). */
 int cf_buckets_build(cf_buckets_t* b, const double* pts, int64_t n, int grid_res, void* stream);
 /* Optional second level, after cf_buckets_build: per cell, the exact candidate

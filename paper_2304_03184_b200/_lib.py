@@ -192,9 +192,13 @@ _SIGS = {
     "cf_selftest_exact_div": [_i64, ctypes.c_uint64, ctypes.POINTER(_i64)],
     "cf_deform_nodes": [_p, _p, _i64, _p, _p],
     "cf_anchor_block_bytes": [_i64, _P(_i64)],
+    "cf_dq_blend": [_p, _p, _i64, _i32, _p, _p, _p],
+    "cf_dq_status": [_p, _p],
+    "cf_dq_apply": [_p, _i64, _p, _i64, _i64, _p, _p],
     "cf_deform_nodes_block": [_p, _p, _i64, _p, _p, _p],
     "cf_buckets_create": [_i64, _i32, ctypes.POINTER(_p)],
     "cf_buckets_destroy": [_p],
+    "cf_buckets_destroy_async": [_p, _p],
     "cf_buckets_build": [_p, _p, _i64, _i32, _p],
     "cf_buckets_build_candidates": [_p, _i32, _p],
     "cf_knn_warp": [_p, _p, _p, _i64, _i32, _f64, _i32, _p, _i64, _p, _p, _p, _p, _p],

@@ -102,6 +102,42 @@ __global__ void __launch_bounds__(1024) deform_nodes_block_kernel(const double* 
   pdl_trigger();
 }
 
+// ------------------------------------------------------------------ transforms drop-ins
+// dq_blend (transforms.py:180-196) over n rows of k neighbours, in the reference's
+// evaluation order (DqbAcc: sign-aligned to the row's first real part, sequential
+// weighted sum, dq_normalize). Argument errors are flagged per row into *err (the
+// largest code wins, as the reference checks the negative weights first):
+// 2 = a negative weight (ValueError), 1 = a row whose weights sum to <= 0
+// (DegenerateWeightsError); cf_dq_status turns the flag into the status.
+__global__ void dq_blend_kernel(const double* __restrict__ w, const double* __restrict__ dqs, int64_t n, int k,
+                                double* __restrict__ out, int* __restrict__ err) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    bool neg = false;
+    double wsum = 0.0;
+    DqbAcc acc;
+    for (int j = 0; j < k; ++j) {
+      const double wj = w[i * k + j];
+      neg |= wj < 0.0;
+      wsum = j == 0 ? wj : x_add(wsum, wj);
+      acc.add(wj, load_dq(dqs + 8 * (i * k + j)));
+    }
+    if (err && (neg || wsum <= 0.0 || k == 0)) atomicMax(err, neg ? 2 : 1);
+    const dq8 b = acc.result();
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      out[8 * i + c] = b.r[c];
+      out[8 * i + 4 + c] = b.d[c];
+    }
+  }
+}
+
+// dq_apply (transforms.py:174-177): rotate by the real part, add the translation
+__global__ void dq_apply_kernel(const double* __restrict__ dq, int64_t dq_stride, const double* __restrict__ p,
+                                int64_t p_stride, int64_t n, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    store_d3(out + 3 * i, dq_apply(load_dq(dq + dq_stride * i), load_d3(p + p_stride * i)));
+}
+
 // ------------------------------------------------------------------ buckets
 
 // grid of G cells along the longest extent of the bbox [mn, mx]
@@ -724,6 +760,33 @@ int cf_deform_nodes(const double* nodes, const double* dqs, int64_t n, double* a
   return cf::check_launch("cf_deform_nodes");
 }
 
+int cf_dq_blend(const double* weights, const double* dqs, int64_t n, int k, double* out, int* err, void* stream) {
+  if (n < 0 || k < 0 || (n > 0 && (!out || (k > 0 && (!weights || !dqs)))))
+    return cf::fail(CF_E_BAD_ARG, "cf_dq_blend: bad args");
+  if (n == 0) return CF_OK;
+  dq_blend_kernel<<<cf::grid_for(n, 128, 8), 128, 0, cf::as_stream(stream)>>>(weights, dqs, n, k, out, err);
+  return cf::check_launch("cf_dq_blend");
+}
+
+int cf_dq_status(const int* err, void* stream) {
+  if (!err) return cf::fail(CF_E_BAD_ARG, "cf_dq_status: bad args");
+  int h = 0;
+  CF_CHECK_CUDA(cudaMemcpyAsync(&h, err, sizeof(int), cudaMemcpyDeviceToHost, cf::as_stream(stream)));
+  CF_CHECK_CUDA(cudaStreamSynchronize(cf::as_stream(stream)));
+  if (h == 2) return cf::fail(CF_E_BAD_ARG, "blend weights must be nonnegative");
+  if (h == 1) return cf::fail(CF_E_DEGENERATE, "all blend weights are zero");
+  return CF_OK;
+}
+
+int cf_dq_apply(const double* dq, int64_t dq_stride, const double* p, int64_t p_stride, int64_t n, double* out,
+                void* stream) {
+  if (n < 0 || (n > 0 && (!dq || !p || !out)) || dq_stride < 0 || p_stride < 0)
+    return cf::fail(CF_E_BAD_ARG, "cf_dq_apply: bad args");
+  if (n == 0) return CF_OK;
+  dq_apply_kernel<<<cf::grid_for(n, 128, 8), 128, 0, cf::as_stream(stream)>>>(dq, dq_stride, p, p_stride, n, out);
+  return cf::check_launch("cf_dq_apply");
+}
+
 int cf_anchor_block_bytes(int64_t n, int64_t* bytes) {
   if (n < 0 || !bytes) return cf::fail(CF_E_BAD_ARG, "cf_anchor_block_bytes: bad args");
   *bytes = 48 * n + 48;
@@ -739,6 +802,9 @@ int cf_deform_nodes_block(const double* nodes, const double* dqs, int64_t n, dou
   return cf::check_launch("cf_deform_nodes_block");
 }
 
+// The handle's buffers come from the stream-ordered allocator, so a handle can be
+// destroyed on a stream without a host synchronisation (cf_buckets_destroy_async):
+// the frees are ordered after the work already queued on that stream.
 int cf_buckets_create(int64_t max_points, int max_grid_res, cf_buckets_t** out) {
   if (!out || max_points < 1 || max_grid_res < 1 || max_grid_res > 256)
     return cf::fail(CF_E_BAD_ARG, "cf_buckets_create: bad args");
@@ -746,15 +812,18 @@ int cf_buckets_create(int64_t max_points, int max_grid_res, cf_buckets_t** out) 
   b->max_points = max_points;
   b->max_grid_res = max_grid_res;
   const int64_t cells = (int64_t)max_grid_res * max_grid_res * max_grid_res;
-  cudaError_t e = cudaMalloc(&b->params, sizeof(BucketParams));
-  if (e == cudaSuccess) e = cudaMalloc(&b->cell_start, sizeof(int) * (cells + 1));
-  if (e == cudaSuccess) e = cudaMalloc(&b->point_cell, sizeof(int) * max_points);
-  if (e == cudaSuccess) e = cudaMalloc(&b->point_slot, sizeof(int) * max_points);
-  if (e == cudaSuccess) e = cudaMalloc(&b->sorted, sizeof(double4) * max_points);
+  cudaStream_t st = 0;
+  auto alloc = [&](void** p, size_t bytes) { return cudaMallocAsync(p, bytes, st); };
+  cudaError_t e = alloc(reinterpret_cast<void**>(&b->params), sizeof(BucketParams));
+  if (e == cudaSuccess) e = alloc(reinterpret_cast<void**>(&b->cell_start), sizeof(int) * (cells + 1));
+  if (e == cudaSuccess) e = alloc(reinterpret_cast<void**>(&b->point_cell), sizeof(int) * max_points);
+  if (e == cudaSuccess) e = alloc(reinterpret_cast<void**>(&b->point_slot), sizeof(int) * max_points);
+  if (e == cudaSuccess) e = alloc(reinterpret_cast<void**>(&b->sorted), sizeof(double4) * max_points);
   b->ccl_cap = std::max<int64_t>(max_points * 64, 1 << 20);
-  if (e == cudaSuccess) e = cudaMalloc(&b->ccl_count, sizeof(int) * (cells + 1));
-  if (e == cudaSuccess) e = cudaMalloc(&b->ccl_len, sizeof(int) * cells);
-  if (e == cudaSuccess) e = cudaMalloc(&b->ccl_ids, sizeof(int) * b->ccl_cap);
+  if (e == cudaSuccess) e = alloc(reinterpret_cast<void**>(&b->ccl_count), sizeof(int) * (cells + 1));
+  if (e == cudaSuccess) e = alloc(reinterpret_cast<void**>(&b->ccl_len), sizeof(int) * cells);
+  if (e == cudaSuccess) e = alloc(reinterpret_cast<void**>(&b->ccl_ids), sizeof(int) * b->ccl_cap);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // usable from every stream
   if (e != cudaSuccess) {
     cf_buckets_destroy(b);
     return cf::fail(CF_E_CUDA, std::string("cf_buckets_create: ") + cudaGetErrorString(e));
@@ -763,18 +832,22 @@ int cf_buckets_create(int64_t max_points, int max_grid_res, cf_buckets_t** out) 
   return CF_OK;
 }
 
+int cf_buckets_destroy_async(cf_buckets_t* b, void* stream) {
+  if (!b) return CF_OK;
+  cudaStream_t st = cf::as_stream(stream);
+  void* ptrs[] = {b->params, b->cell_start, b->point_cell, b->point_slot, b->sorted, b->ccl_count, b->ccl_len,
+                  b->ccl_ids};
+  for (void* p : ptrs)
+    if (p) cudaFreeAsync(p, st);
+  delete b;
+  return cf::check_launch("cf_buckets_destroy_async");
+}
+
 int cf_buckets_destroy(cf_buckets_t* b) {
   if (!b) return CF_OK;
-  cudaFree(b->params);
-  cudaFree(b->cell_start);
-  cudaFree(b->point_cell);
-  cudaFree(b->point_slot);
-  cudaFree(b->sorted);
-  cudaFree(b->ccl_count);
-  cudaFree(b->ccl_len);
-  cudaFree(b->ccl_ids);
-  delete b;
-  return CF_OK;
+  const int rc = cf_buckets_destroy_async(b, nullptr);
+  cudaStreamSynchronize(0);
+  return rc;
 }
 
 int cf_buckets_build_candidates(cf_buckets_t* b, int k, void* stream) {

@@ -8,6 +8,7 @@ inputs give CUDA tensor outputs with no host round trip.
 """
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
@@ -109,10 +110,10 @@ class Buckets:
                       _lib.stream_ptr())
 
     def __del__(self):
+        # stream-ordered: the frees follow the work queued on the current stream (no host sync)
         h = getattr(self, "handle", None)
         if h and _lib._lib is not None:
-            torch.cuda.current_stream().synchronize()
-            _lib._lib.cf_buckets_destroy(h)
+            _lib._lib.cf_buckets_destroy_async(h, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
             self.handle = None
 
 

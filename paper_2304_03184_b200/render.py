@@ -693,6 +693,8 @@ class Renderer:
         that use the frame's warp state without rendering a view (training)."""
         if self._setup_pending and self.human is not None:
             self._human_setup()
+            # the side-stream LBS chain is done before the caller's next launch
+            torch.cuda.current_stream().wait_event(self._lbs_done)
         self._setup_pending = False
 
     def render(self, R, t, fx, fy, cx, cy):

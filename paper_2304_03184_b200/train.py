@@ -440,7 +440,6 @@ class Trainer:
             self.M.obj_t[a] = ot[a]
         for a in range(9):
             self.M.obj_R[a] = oR[a]
-        torch.cuda.current_stream().wait_event(r._lbs_done)
 
     # -- the step ------------------------------------------------------------------
 
