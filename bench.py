@@ -221,27 +221,32 @@ def load_peaks():
                                "measured L2-resident random 8 B gathers, " + src.get("micro", "-")),
             "l2_gather16_gbs": (float(peaks.get("l2_gather_16B_64MiB_gbs", 4600.0)),
                                 "measured L2-resident random 16 B gathers, " + src.get("micro", "-")),
-            "fp64_tflops": (float(peaks.get("fp64_fma_tflops", 34.0)), "measured FP64 FMA, " + src.get("micro", "-"))}
+            "fp64_tflops": (float(peaks.get("fp64_fma_tflops", 34.0)), "measured FP64 FMA, " + src.get("micro", "-")),
+            "hash_c_gbs": (float(peaks.get("hash_gather_canonical_16x2p19xF2_f32_gbs", 4180.0)),
+                           "measured gather-only ceiling of the canonical grid's own access pattern, "
+                           + src.get("micro", "-")),
+            "hash_d_gbs": (float(peaks.get("hash_gather_deform_8x2p17xF4_f32_gbs", 9750.0)),
+                           "measured gather-only ceiling of the deformation grid's access pattern (fp32 entries), "
+                           + src.get("micro", "-"))}
 
 
 def stage_costs(hs, os_, n_rays, precision):
     """Algorithmic work per launch of each render stage:
-    (bound, work, unit, how). Hash stages: the corner gathers of the HASHED levels (the
-    dense coarse levels are L1-resident) against the L2 random-gather peak of their
-    entry size; MLPs: the math FLOPs (the fp32 mode issues 3x as split-fp16 MMAs)."""
+    (bound, work, unit, how). Hash stages: every level's 8 corner gathers (SURVEY 8(d)
+    K8) against the measured gather-only ceiling of the same grid's access pattern
+    (tools/peaks.cu hash_gather: L1 reuse between neighbouring samples included);
+    MLPs: the math FLOPs (the fp32 mode issues 3x as split-fp16 MMAs)."""
     f32 = precision == "fp32"
     ent_d = 16 if f32 else 8   # deformation grid entry (F = 4): fp32 / fp16 copy
-    feat = 128 if f32 else 64
     return {
         "human_canon": ("hbm", hs * 57.0, "B", "57 B/sample (SURVEY 8d K5/K6: pos 12 + p_c 12 + idx 16 + w 16 + valid 1)"),
-        "human_hash_d": ("l2_16" if f32 else "l2_8", hs * 5 * 8 * ent_d, "B",
-                         f"5 hashed levels x 8 corners x {ent_d} B (levels 0-2 dense, L1-resident)"),
+        "human_hash_d": ("hash_d", hs * 8 * 8 * ent_d, "B", f"8 levels x 8 corners x {ent_d} B"),
         "human_deform_mlp": ("tensor", hs * 110592.0, "FLOP",
                              "2(32x128 + 3x128x128 + 128x16) FLOP/sample" + (" (x3 issued: split fp16)" if f32 else "")),
-        "human_hash_c": ("l2_8", hs * 11 * 8 * 8, "B", "11 hashed levels x 8 corners x 8 B (levels 0-4 dense)"),
+        "human_hash_c": ("hash_c", hs * 16 * 8 * 8, "B", "16 levels x 8 corners x 8 B"),
         "human_color_mlp": ("tensor", hs * 20480.0, "FLOP",
                             "2(32x64 + 64x16 + 32x64 + 64x64 + 64x16) FLOP/sample" + (" (x3 issued)" if f32 else "")),
-        "object_field": ("l2_8", os_ * 11 * 8 * 8, "B", "hash (11 hashed levels x 8 x 8 B) + E_g/E_c; gather-bound"),
+        "object_field": ("hash_c", os_ * 16 * 8 * 8, "B", "hash (16 levels x 8 x 8 B) + E_g/E_c; gather-bound"),
         "march": ("hbm", n_rays * 32.0 + 4.0 * (hs + os_), "B", "B/ray: dir 24 + offset/count 8, + 4 B/record"),
         "human_composite": ("hbm", (hs) * 16.0 + n_rays * 40.0, "B", "field 16 B/sample + 40 B/ray out"),
     }
@@ -254,10 +259,12 @@ def roofline_entry(name, cost, ms, peaks):
         peak, src = peaks["bf16_tflops"]
         return {"kernel": name, "bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
                 "frac": ach / peak, "per_unit": how, "peak_source": src, "ms": ms}
-    key = {"hbm": "hbm_gbs", "l2_8": "l2_gather8_gbs", "l2_16": "l2_gather16_gbs"}[bound]
+    key = {"hbm": "hbm_gbs", "l2_8": "l2_gather8_gbs", "l2_16": "l2_gather16_gbs", "hash_c": "hash_c_gbs",
+           "hash_d": "hash_d_gbs"}[bound]
     ach = work / (ms / 1e3) / 1e9
     peak, src = peaks[key]
-    return {"kernel": name, "bound": "hbm" if bound == "hbm" else "l2", "achieved": ach, "peak": peak,
+    return {"kernel": name, "bound": "hbm" if bound == "hbm" else ("gather" if bound.startswith("hash") else "l2"),
+            "achieved": ach, "peak": peak,
             "unit": "GB/s", "frac": ach / peak, "per_unit": how, "peak_source": src, "ms": ms}
 
 
@@ -624,6 +631,7 @@ def run_train(args, rank, world, pg):
     ours, other, names = count_launches(step)
     launches = {"per_step": ours, "foreign_kernels_per_step": other, "kernels": names,
                 "how": "CUPTI (torch.profiler) over one graph replay"}
+    stage_ms, roof = train_stage_roofline(tr, keyframes, per_frame, rank)
     # e2e: eager public API, this step's ray batches uploaded from pinned host memory
     e2e = None
     if not args.no_e2e:
@@ -674,9 +682,95 @@ def run_train(args, rank, world, pg):
                        "l2": "inputs (hash tables 64 MB + 47 MB, per-frame activations) larger than L2",
                        "parallelism": f"dp{world} (rays sharded, ray counts and gradient buckets summed)"},
             "gpu_launches": launches["per_step"] * args.steps, "gpu_launches_detail": launches,
-            "clocks": clk, "e2e": e2e}
+            "clocks": clk, "e2e": e2e, "stage_ms_per_step": stage_ms, "roofline": roof}
+    if rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = train_cpu_baseline()
     if rank == 0:
         print(json.dumps(line))
+
+
+# per-sample bytes of the dW GEMM operands (cf_dw_grouped: A and B rows, fp16, read once)
+_DW_BYTES = {"human": 2 * ((64 + 32) + (16 + 64) + (64 + 31) + (64 + 64) + (3 + 64)
+                           + (3 + 128) + 3 * (128 + 128) + (128 + 33)),
+             "object": 2 * ((64 + 32) + (16 + 64) + (64 + 31) + (64 + 64) + (3 + 64))}
+
+
+def train_stage_roofline(tr, keyframes, per_frame, rank):
+    """Per-kernel device time of one eager step (CUDA events around each launch of the
+    kernels named below, on the launching stream) and the roofline of the dominant one
+    (algorithmic bytes or FLOPs per sample x the step's samples, per field)."""
+    import torch
+    from paper_2304_03184_b200 import _lib
+    names = {"cf_dw_grouped": "dw_grouped", "cf_color_backward": "color_bwd", "cf_field_forward": "field_fwd",
+             "cf_field_hash_backward": "hash_bwd_c", "cf_human_canon": "human_canon",
+             "cf_deform_backward": "deform_bwd", "cf_deform_hash_backward": "hash_bwd_d",
+             "cf_loss_composite_bwd": "loss_composite_bwd"}
+    marks = []
+    real = _lib.call
+
+    def timed(name, *a):
+        if name not in names:
+            return real(name, *a)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        real(name, *a)
+        e1.record()
+        marks.append((names[name], e0, e1))
+    bufs = [kf.batch_buffers(per_frame) for kf in keyframes]
+    for f, (kf, b) in enumerate(zip(keyframes, bufs)):
+        kf.draw(b, seed=f * 64 + rank + 99)
+        b.ray0 = rank * per_frame
+    torch.cuda.synchronize()
+    _lib.call = timed
+    try:
+        tr.step(bufs, None, update=False)
+        torch.cuda.synchronize()
+    finally:
+        _lib.call = real
+    ms = {}
+    for n, e0, e1 in marks:
+        ms[n] = ms.get(n, 0.0) + e0.elapsed_time(e1)
+    c = tr.counts.cpu().numpy().astype(np.int64)
+    samples = {q: float((48 * c[:, 2 * i + 1] + 64 * (c[:, 2 * i] - c[:, 2 * i + 1])).sum())
+               for i, q in enumerate(("human", "object"))}
+    peaks = load_peaks()
+    work = sum(samples[q] * _DW_BYTES[q] for q in samples)
+    t = ms["dw_grouped"]
+    ach = work / (t / 1e3) / 1e9
+    peak, src = peaks["hbm_gbs"]
+    roof = {"kernel": "dw_grouped (tcgen05 split-K weight gradients, 2 launches per frame)", "bound": "hbm",
+            "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+            "per_unit": "fp16 operand rows read once per sample: human 3,052 B (E_g/E_c 932 + DeformNet 2,120), "
+                        "object 932 B", "peak_source": src, "ms": t, "traffic": None,
+            "timing": "CUDA events around each launch of one eager step (update=False), summed per kernel"}
+    top = max(ms, key=ms.get)
+    roof["dominant_by_time"] = top
+    return {k: round(v, 3) for k, v in sorted(ms.items(), key=lambda kv: -kv[1])}, roof
+
+
+def train_cpu_baseline(budget_s=15.0):
+    """The training step's human-field work on the host (oracle/pipeline.train_rays: the
+    SPEC's algorithm in numpy / float64 torch autograd, one process, no device work) on
+    a bounded sample of the key frame's foreground rays."""
+    import torch
+    from oracle import pipeline as op
+    torch.set_num_threads(os.cpu_count() or 1)
+    S = op.build_static(width=512, height=512, samples=128, table_scale=1e-4)
+    sc = S["scene"]
+    o, d = sc.camera.all_rays()
+    _, _, _, hum, _ = sc.raycast(o, d, 3)
+    fg = np.nonzero(hum)[0]
+    rng = np.random.default_rng(0)
+    t0 = time.perf_counter()
+    done, reps = 0, 0
+    while reps < 1 or time.perf_counter() - t0 < budget_s:
+        done += op.train_rays(S, 3, rng.choice(fg, 64), seed=reps)
+        reps += 1
+    el = time.perf_counter() - t0
+    return {"value": done / el, "unit": "samples/s", "cores": torch.get_num_threads(), "kind": "port",
+            "sample": f"oracle/pipeline.train_rays: {reps} x 64 human rays of key frame 3 (depth-guided samples, "
+                      f"hybrid canonicalisation, fp32-semantics field, float64 autograd gradients of every human "
+                      f"parameter, Adam) in one process (torch intra-op threads = cores)"}
 
 
 def run_knn(args, rank, world, pg):

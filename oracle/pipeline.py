@@ -218,3 +218,42 @@ class FramePool:
         img, layer = orr.layers(acc["human"], acc["object"], BACKGROUND)
         return nh, no, img, layer
 
+
+
+def train_rays(S, fid, ray_ids, seed=1234):
+    """The key-frame training step's human-field work for the given pixels of frame
+    fid on the host: depth-guided samples, hybrid canonicalisation, the
+    field forward and the 64-bit analytic gradient of masked L2 + 0.1 L1 depth with
+    respect to every human parameter (oracle/grad.py), then one Adam update (numpy).
+    -> number of samples processed. (CPU baseline of bench.py --workload train.)"""
+    from . import grad as og
+    sc = S["scene"]
+    F = frame_setup(S, fid)
+    h = S["human"]
+    o = S["origin"]
+    d = S["dirs"][ray_ids]
+    th, to, rgb, hum, obj = sc.raycast(np.broadcast_to(o, d.shape), d, fid)
+    depth = np.where(hum, th, 0.0)
+    ts = orr.train_samples(depth, hum, S["t_near"], S["t_far"], 32, 16, 64, 0.02, seed)
+    ray = np.concatenate([np.full(len(t), q) for q, t in enumerate(ts) if t is not None]).astype(np.int64)
+    t = np.concatenate([t for t in ts if t is not None])
+    if len(t) == 0:
+        return 0
+    p = o + t[:, None] * d[ray]
+    verts, vw = np.asarray(sc.skin_verts), np.asarray(sc.skin_weights)
+    xu = orr.human_canon(p, S["nodes"], F["dqs"], 4, 0.1, F["A"], verts, vw, 0.2, h["cmin"], h["inv_side"])
+    delta = np.empty(len(t))
+    last = np.append(ray[1:] != ray[:-1], True)
+    delta[:-1] = t[1:] - t[:-1]
+    delta[last] = S["dt"]
+    batch = {"xu": xu, "dirs": d[ray], "ray": ray, "t": t, "delta": delta, "gt_rgb": rgb.astype(np.float64),
+             "gt_depth": depth, "mask": hum, "inv_side": h["inv_side"], "theta": sc.theta(fid)}
+    values = {"ctable": h["ctable"], "dtable": h["dtable"]}
+    values.update({k: v for k, v in h["layers"].items()})
+    _, g = og.gradients(values, batch)
+    for k, v in values.items():  # one Adam step (first-step moments)
+        m = 0.1 * g[k]
+        vv = 0.01 * g[k] ** 2
+        lr = 1e-2 if k.endswith("table") else 1e-3
+        values[k] = v - lr * (m / 0.1) / (np.sqrt(vv / 0.01) + 1e-15)
+    return len(t)
