@@ -658,6 +658,38 @@ __device__ __forceinline__ uint32_t split_relu32(const SplitSlot& S, int col, co
   return bits;
 }
 
+// 64 D columns from col (this thread's half of the row): both 32-column TMEM loads in
+// flight before one wait, then (+bias) ReLU -> hi / lo fp16x2 -> A columns col/2;
+// training saves and ReLU bits as split_relu32 (two words)
+__device__ __forceinline__ uint2 split_relu64(const SplitSlot& S, int col, const float* bias, __half* save = nullptr,
+                                              int64_t ld = 0) {
+  uint32_t r[64];
+  tc::tmem_ld32_nowait(S.d + (uint32_t)col, r);
+  tc::tmem_ld32_nowait(S.d + (uint32_t)(col + 32), r + 32);
+  tc::tmem_wait_ld();
+  uint32_t bits[2];
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    uint32_t h[16], l[16];
+    uint32_t b = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      float x0 = __uint_as_float(r[32 * c + 2 * i]), x1 = __uint_as_float(r[32 * c + 2 * i + 1]);
+      if (bias) {
+        x0 += bias[col + 32 * c + 2 * i];
+        x1 += bias[col + 32 * c + 2 * i + 1];
+      }
+      b |= (x0 > 0.0f ? 1u : 0u) << (2 * i) | (x1 > 0.0f ? 1u : 0u) << (2 * i + 1);
+      tc::split_f16x2(fmaxf(x0, 0.0f), fmaxf(x1, 0.0f), h[i], l[i]);
+    }
+    tc::tmem_st16(S.ahi + (uint32_t)((col + 32 * c) / 2), h);
+    tc::tmem_st16(S.alo + (uint32_t)((col + 32 * c) / 2), l);
+    if (save) store_cols_f16(reinterpret_cast<uint16_t*>(save), ld, col + 32 * c, h);
+    bits[c] = b;
+  }
+  return make_uint2(bits[0], bits[1]);
+}
+
 // n4 float4 of fp32 values -> hi / lo halves at A column c0 (2 values per column)
 template <int N4>
 __device__ __forceinline__ void split_store(const SplitSlot& S, const float4* v, int c0, uint32_t* hi_out = nullptr) {
@@ -759,11 +791,8 @@ __global__ void __launch_bounds__(kPrecDeformSlots* kDeformSlotThreads, 1)
     for (int l = 0; l < 4; ++l) {
       const int lo_off = (int)(wo[l] - smem);
       split_layer(S, wo[l], lo + lo_off, l == 0 ? 32 : 128, 128);
-      const uint32_t b0 = split_relu32(S, 64 * S.half, l == 0 ? s_bias : nullptr, sv ? sv + l * L : nullptr,
-                                       capacity);
-      const uint32_t b1 = split_relu32(S, 64 * S.half + 32, l == 0 ? s_bias : nullptr, sv ? sv + l * L : nullptr,
-                                       capacity);
-      if (mk) *reinterpret_cast<uint2*>(mk + 4 * l) = make_uint2(b0, b1);
+      const uint2 b = split_relu64(S, 64 * S.half, l == 0 ? s_bias : nullptr, sv ? sv + l * L : nullptr, capacity);
+      if (mk) *reinterpret_cast<uint2*>(mk + 4 * l) = b;
     }
     split_layer(S, smem + o5, lo + o5, 128, 16);
     if (S.half == 0) {  // warp-uniform: tcgen05.ld is warp-collective
