@@ -81,6 +81,13 @@ int cf_dq_apply(const double* dq, int64_t dq_stride, const double* p, int64_t p_
 /* graphs of n <= 1024 nodes: the deformed nodes plus the frame's anchor block read by
  * cf_human_canon (float64 + fp32 copies, bbox; cf_anchor_block_bytes(n) bytes, 16-byte aligned) */
 int cf_anchor_block_bytes(int64_t n, int64_t* bytes);
+/* candidate grid of a frame's anchors (n <= 1024), hierarchical k-NN: grid_res cells along the
+ * longest side of the anchors' bbox grown by the ED support radius sqrt(-ln 1e-6) radius; per cell
+ * the nodes that can be among the k nearest of any point in it (float64, ties included), up to
+ * cmax ids (fuller cells fall back to every node). Reads the anchor block (cf_deform_nodes_block). */
+int cf_cand_grid_bytes(int grid_res, int cmax, int64_t* bytes);
+int cf_cand_grid_build(const void* block, int64_t n, int k, double radius, int grid_res, int cmax, void* cand,
+                       void* stream);
 int cf_deform_nodes_block(const double* nodes, const double* dqs, int64_t n, double* anchors, void* block,
                           void* stream);
 
@@ -274,6 +281,8 @@ typedef struct cf_human_warp {
   int n_nodes;
   const void* anchor_block; /* n_nodes <= 1024: the frame's anchor block (cf_deform_nodes_block), which the
                                k-NN scans with warp-cooperative culling (anchor_buckets may be NULL) */
+  const void* cand_grid;    /* optional, with anchor_block: the frame's candidate grid (cf_cand_grid_build);
+                               each sample then ranks only its cell's candidate nodes */
 } cf_human_warp;
 
 int cf_camera_rays(const cf_camera* cam, double* dirs, void* stream);

@@ -79,7 +79,8 @@ class HumanWarp(ctypes.Structure):
     _fields_ = [("dqs", ctypes.c_void_p), ("k", ctypes.c_int), ("r2", ctypes.c_double),
                 ("vert_Tinv", ctypes.c_void_p), ("lbs_max_d2", ctypes.c_double),
                 ("canon_min", ctypes.c_double * 3), ("inv_side", ctypes.c_double),
-                ("anchors", ctypes.c_void_p), ("n_nodes", ctypes.c_int), ("anchor_block", ctypes.c_void_p)]
+                ("anchors", ctypes.c_void_p), ("n_nodes", ctypes.c_int), ("anchor_block", ctypes.c_void_p),
+                ("cand_grid", ctypes.c_void_p)]
 
 
 class FieldDesc(ctypes.Structure):
@@ -192,6 +193,8 @@ _SIGS = {
     "cf_selftest_exact_div": [_i64, ctypes.c_uint64, ctypes.POINTER(_i64)],
     "cf_deform_nodes": [_p, _p, _i64, _p, _p],
     "cf_anchor_block_bytes": [_i64, _P(_i64)],
+    "cf_cand_grid_bytes": [_i32, _i32, _P(_i64)],
+    "cf_cand_grid_build": [_p, _i64, _i32, _f64, _i32, _i32, _p, _p],
     "cf_dq_blend": [_p, _p, _i64, _i32, _p, _p, _p],
     "cf_dq_status": [_p, _p],
     "cf_dq_apply": [_p, _i64, _p, _i64, _i64, _p, _p],

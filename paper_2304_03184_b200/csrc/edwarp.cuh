@@ -6,6 +6,16 @@
 #include "buckets.cuh"
 #include "dq.cuh"
 
+// header of a candidate grid (cf_cand_grid_build, knn.cu), followed at byte 64 by the
+// per-cell lists: uint16 count (0xFFFF = more than cmax) then cmax node ids
+struct CandGridHdr {
+  double origin[3];
+  double h, inv_h;
+  int dims[3];
+  int cmax;
+};
+static_assert(sizeof(CandGridHdr) <= 64, "candidate-grid header");
+
 template <int K>
 __device__ __forceinline__ bool blend_apply(const TopK<K>& top, const double* __restrict__ dqs, int k, double r2,
                                             bool inverse, d3 p, d3& out);

@@ -102,6 +102,93 @@ __global__ void __launch_bounds__(1024) deform_nodes_block_kernel(const double* 
   pdl_trigger();
 }
 
+// Candidate grid of a small graph (the render path's k-NN, n <= 1024): a per-frame
+// grid of cells over the anchors' bbox grown by the ED support radius R (a sample
+// farther than R from every node has all Gaussian weights below the validity
+// floor); per cell the nodes that can be among the k nearest of ANY point of the
+// cell: U = the k-th smallest (with multiplicity) over all nodes of the farthest
+// distance^2 from the cell box to the node bounds the k-th neighbour distance^2 of
+// every point in the cell, and a node whose nearest distance^2 to the box exceeds U
+// cannot be closer than that (ties included: <=). The bounds are taken in fp32 with
+// margins that only grow the lists (see the kernel); lists hold node ids ascending,
+// up to cmax; a fuller cell is marked 0xFFFF (its samples scan every node).
+
+__device__ __forceinline__ void cand_grid_geometry(const double* box, double r2, int G, CandGridHdr& H) {
+  const double R = sqrt(13.815510557964274 * r2 * (1.0 + 1e-5)) * (1.0 + 1e-9) + 1e-9;
+  double ext[3], mx = 0.0;
+  for (int a = 0; a < 3; ++a) {
+    H.origin[a] = box[a] - R;
+    ext[a] = (box[3 + a] + R) - H.origin[a];
+    mx = fmax(mx, ext[a]);
+  }
+  H.h = mx / G;
+  H.inv_h = 1.0 / H.h;
+  for (int a = 0; a < 3; ++a) H.dims[a] = max(1, min(G, (int)ceil(ext[a] * H.inv_h)));
+}
+
+template <int K>
+__global__ void __launch_bounds__(64) cand_grid_kernel(const uint8_t* __restrict__ block, int n, int k, double r2,
+                                                       int G, int cmax, uint8_t* __restrict__ cand) {
+  extern __shared__ float4 s_a[];  // the frame's nodes (fp32 copies)
+  pdl_wait();
+  const float4* a32 = reinterpret_cast<const float4*>(block + 32 * (size_t)n);
+  const double* box = reinterpret_cast<const double*>(block + 48 * (size_t)n);
+  CandGridHdr H;
+  cand_grid_geometry(box, r2, G, H);
+  H.cmax = cmax;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *reinterpret_cast<CandGridHdr*>(cand) = H;
+  if ((int64_t)blockIdx.x * blockDim.x >= (int64_t)H.dims[0] * H.dims[1] * H.dims[2]) return;  // (CTA-uniform)
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s_a[i] = a32[i];
+  __syncthreads();
+  uint16_t* lists = reinterpret_cast<uint16_t*>(cand + 64);
+  const int64_t cells = (int64_t)H.dims[0] * H.dims[1] * H.dims[2];
+  const float INF = __int_as_float(0x7f800000);
+  // one thread per cell, the nodes broadcast from shared memory. fp32 with margins that
+  // keep the list a superset: U is rounded up (an upper bound of the k-th neighbour
+  // distance^2 of every point of the cell), each node's nearest distance^2 to the cell
+  // rounded down (fp32 coordinates of ~1 m carry < 1e-7 relative error, the margins
+  // are 1e-4 relative + 1e-9 m^2); the samples then rank the list exactly in float64.
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < cells; c += (int64_t)gridDim.x * blockDim.x) {
+    const int cx = (int)(c / ((int64_t)H.dims[1] * H.dims[2])), cy = (int)((c / H.dims[2]) % H.dims[1]),
+              cz = (int)(c % H.dims[2]);
+    const float lo[3] = {(float)(H.origin[0] + cx * H.h), (float)(H.origin[1] + cy * H.h),
+                         (float)(H.origin[2] + cz * H.h)};
+    const float hf = (float)H.h;
+    const float hi[3] = {lo[0] + hf, lo[1] + hf, lo[2] + hf};
+    float best[K];  // the K smallest farthest-distances^2 (with multiplicity), ascending
+#pragma unroll
+    for (int j = 0; j < K; ++j) best[j] = INF;
+    for (int i = 0; i < n; ++i) {
+      const float4 a = s_a[i];
+      const float ex = fmaxf(fabsf(a.x - lo[0]), fabsf(a.x - hi[0]));
+      const float ey = fmaxf(fabsf(a.y - lo[1]), fabsf(a.y - hi[1]));
+      const float ez = fmaxf(fabsf(a.z - lo[2]), fabsf(a.z - hi[2]));
+      float v = ex * ex + ey * ey + ez * ez;
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        const float lo_v = fminf(v, best[j]);
+        v = fmaxf(v, best[j]);
+        best[j] = lo_v;
+      }
+    }
+    const float cut = best[K - 1] * (1.0f + 1e-4f) + 1e-9f;
+    uint16_t* L = lists + c * (int64_t)(cmax + 1);
+    int cnt = 0;
+    for (int i = 0; i < n; ++i) {
+      const float4 a = s_a[i];
+      const float dx = fmaxf(fmaxf(lo[0] - a.x, a.x - hi[0]), 0.f);
+      const float dy = fmaxf(fmaxf(lo[1] - a.y, a.y - hi[1]), 0.f);
+      const float dz = fmaxf(fmaxf(lo[2] - a.z, a.z - hi[2]), 0.f);
+      if ((dx * dx + dy * dy + dz * dz) * (1.0f - 1e-4f) - 1e-9f <= cut) {
+        if (cnt < cmax) L[1 + cnt] = (uint16_t)i;
+        ++cnt;
+      }
+    }
+    L[0] = cnt <= cmax ? (uint16_t)cnt : (uint16_t)0xFFFF;
+  }
+  pdl_trigger();
+}
+
 // ------------------------------------------------------------------ transforms drop-ins
 // dq_blend (transforms.py:180-196) over n rows of k neighbours, in the reference's
 // evaluation order (DqbAcc: sign-aligned to the row's first real part, sequential
@@ -785,6 +872,31 @@ int cf_dq_apply(const double* dq, int64_t dq_stride, const double* p, int64_t p_
   if (n == 0) return CF_OK;
   dq_apply_kernel<<<cf::grid_for(n, 128, 8), 128, 0, cf::as_stream(stream)>>>(dq, dq_stride, p, p_stride, n, out);
   return cf::check_launch("cf_dq_apply");
+}
+
+int cf_cand_grid_bytes(int grid_res, int cmax, int64_t* bytes) {
+  if (grid_res < 1 || grid_res > 128 || cmax < 1 || cmax > 4096 || !bytes)
+    return cf::fail(CF_E_BAD_ARG, "cf_cand_grid_bytes: bad args");
+  *bytes = 64 + (int64_t)grid_res * grid_res * grid_res * (cmax + 1) * 2;
+  return CF_OK;
+}
+
+int cf_cand_grid_build(const void* block, int64_t n, int k, double radius, int grid_res, int cmax, void* cand,
+                       void* stream) {
+  if (!block || !cand || n < 1 || n > 1024 || k < 1 || k > 8 || !(radius > 0) || grid_res < 1 || grid_res > 128 ||
+      cmax < 1 || cmax > 4096)
+    return cf::fail(CF_E_BAD_ARG, "cf_cand_grid_build: bad args");
+  const int64_t cells = (int64_t)grid_res * grid_res * grid_res;  // (upper bound of the grid's cells)
+  // one thread per cell, 64-thread CTAs over the grid's upper bound of cells (the
+  // frame's actual grid is known on the device only; surplus CTAs exit at once)
+  const unsigned grid = (unsigned)std::max<int64_t>(1, (cells + 63) / 64);
+  cudaStream_t st = cf::as_stream(stream);
+  dispatch_k(k, [&]<int K>() {
+    cf::launch_pdl(cand_grid_kernel<K>, grid, 64, (size_t)n * sizeof(float4), st, static_cast<const uint8_t*>(block),
+                   (int)n, k, radius * radius, grid_res, cmax, static_cast<uint8_t*>(cand));
+    return 0;
+  });
+  return cf::check_launch("cf_cand_grid_build");
 }
 
 int cf_anchor_block_bytes(int64_t n, int64_t* bytes) {

@@ -627,6 +627,9 @@ __global__ void __launch_bounds__(128, CF_CANON_MINB) human_canon_kernel(cf_marc
   const double4* a64 = reinterpret_cast<const double4*>(s_blk);
   const float4* a32 = reinterpret_cast<const float4*>(s_blk + 32 * (size_t)W.n_nodes);
   const double* box = reinterpret_cast<const double*>(s_blk + 48 * (size_t)W.n_nodes);
+  const CandGridHdr* cgrid = static_cast<const CandGridHdr*>(W.cand_grid);
+  const uint16_t* clists = cgrid ? reinterpret_cast<const uint16_t*>(static_cast<const uint8_t*>(W.cand_grid) + 64)
+                                 : nullptr;
   // A sample farther than R from the anchors' bbox has every Gaussian weight
   // below the validity floor: d^2 / r^2 > -ln(1e-6) (1 + 1e-5) => w < 1e-6. Such
   // samples skip the k-NN (ED invalid, as the exact evaluation would find) and
@@ -661,8 +664,44 @@ __global__ void __launch_bounds__(128, CF_CANON_MINB) human_canon_kernel(cf_marc
       }
       near = d2 <= rsup2;
     }
-    const bool ed_ok = kBlock ? ed_warp_point_cull<K>(a64, a32, W.n_nodes, W.dqs, W.k, W.r2, true, p, near, pt)
-                              : (live && ed_warp_point<K>(*EPp, ecs, es, W.dqs, W.k, W.r2, true, p, pt));
+    bool ed_ok;
+    if (kBlock && cgrid) {
+      // the cell's candidate list (cf_cand_grid_build): exact float64 ranking of the few
+      // nodes that can be among the k nearest of any point of the cell
+      ed_ok = false;
+      if (live && near) {
+        const double q[3] = {p.x, p.y, p.z};
+        int64_t cell = 0;
+        bool in = true;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          const double f = floor(x_mul(x_sub(q[a], cgrid->origin[a]), cgrid->inv_h));
+          const int ca = f < 0.0 ? 0 : (f >= (double)cgrid->dims[a] ? cgrid->dims[a] - 1 : (int)f);
+          in &= f >= 0.0 && f < (double)cgrid->dims[a];  // (outside: rounding at the grid's edge -> every node)
+          cell = cell * cgrid->dims[a] + ca;
+        }
+        TopK<K> top;
+        top.init(W.k);
+        const uint16_t* L = clists + cell * (int64_t)(cgrid->cmax + 1);
+        const int cnt = in ? (int)L[0] : 0xFFFF;
+        if (cnt == 0xFFFF) {  // a crowded cell: every node
+          for (int i = 0; i < W.n_nodes; ++i) {
+            const double4 a = a64[i];
+            top.insert(sqdist(p, d3{a.x, a.y, a.z}), i);
+          }
+        } else {
+          for (int j = 0; j < cnt; ++j) {
+            const int i = L[1 + j];
+            const double4 a = a64[i];
+            top.insert(sqdist(p, d3{a.x, a.y, a.z}), i);
+          }
+        }
+        ed_ok = blend_apply<K>(top, W.dqs, W.k, W.r2, true, p, pt);
+      }
+    } else {
+      ed_ok = kBlock ? ed_warp_point_cull<K>(a64, a32, W.n_nodes, W.dqs, W.k, W.r2, true, p, near, pt)
+                     : (live && ed_warp_point<K>(*EPp, ecs, es, W.dqs, W.k, W.r2, true, p, pt));
+    }
     if (live) {
       if (ed_ok) flag = 1.0f;
       else if (LPp && lbs_fallback(*LPp, lcs, ls, W, p, pt)) flag = 2.0f;

@@ -69,6 +69,11 @@ class RenderConfig:
     # occupancy refresh from the trained density (refresh_occupancy): a cell is occupied
     # when its max-decayed density keeps one sample's opacity 1 - exp(-sigma dt) above
     # occ_alpha; the log-density decays by occ_decay per refresh
+    # hierarchical k-NN of the canonicalisation (graphs <= 1024 nodes): a per-frame grid of
+    # cand_grid_res cells along the longest side with per-cell candidate lists (0 = the
+    # warp-cooperative culled scan instead)
+    cand_grid_res: int = 48
+    cand_grid_cmax: int = 64
     occ_alpha: float = 0.01
     occ_decay: float = 0.95
     background: tuple = (24 / 255.0, 28 / 255.0, 34 / 255.0)   # config.py bg_r/g/b
@@ -390,8 +395,11 @@ class Renderer:
         # human chain (stream priorities and a later object fork were measured: no gain)
         self.side = torch.cuda.Stream(device=d)
         self._lbs_done = torch.cuda.Event()
+        self._ed_done = torch.cuda.Event()
+        self.side_ed = torch.cuda.Stream(device=d)
         self._obj_done = torch.cuda.Event()
         self._lbs_done.record(torch.cuda.current_stream())
+        self._ed_done.record(torch.cuda.current_stream())
         # frame block: origin[3], obj_R[9], obj_t[3] | camera R[9], fx, fy, cx, cy
         self.frame_dev = torch.zeros(_FRAME_DOUBLES, dtype=torch.float64, device=d)
         self._frame_host = np.zeros(_FRAME_DOUBLES)
@@ -460,6 +468,11 @@ class Renderer:
                 _lib.call("cf_anchor_block_bytes", w.n_nodes, ctypes.byref(nb))
                 self._anchor_block = torch.empty(int(nb.value), dtype=torch.uint8, device=self.dirs.device)
                 w.anchor_block = self._anchor_block.data_ptr()
+                if self.cfg.cand_grid_res > 0:  # the per-frame candidate grid of the k-NN
+                    _lib.call("cf_cand_grid_bytes", self.cfg.cand_grid_res, self.cfg.cand_grid_cmax,
+                              ctypes.byref(nb))
+                    self._cand_grid = torch.empty(int(nb.value), dtype=torch.uint8, device=self.dirs.device)
+                    w.cand_grid = self._cand_grid.data_ptr()
             self.hw = w
             self.hdesc = h.desc(self.dbias, self.cfg.precision)
 
@@ -498,16 +511,27 @@ class Renderer:
                           offsets.ctypes.data, len(parents), self._A.data_ptr(), ss)
                 _lib.call("cf_pose_bias", h.nets.d1.data_ptr(), 32 + 3 * len(parents), 32, 128,
                           self._theta.data_ptr(), 3 * len(parents), self.dbias.data_ptr(), ss)
-            if n <= 1024:
-                _lib.call("cf_deform_nodes_block", h.nodes.data_ptr(), self._dqs.data_ptr(), n,
-                          self._anchors.data_ptr(), self._anchor_block.data_ptr(), ss)
-            else:
-                _lib.call("cf_deform_nodes", h.nodes.data_ptr(), self._dqs.data_ptr(), n, self._anchors.data_ptr(), ss)
-            if n > 1024:  # small graphs are scanned from shared memory (no buckets needed)
-                self._anchor_buckets.build(self._anchors)
             h.lbs.set_pose(self._A)
             self._mark("lbs_setup")
             self._lbs_done.record(side)
+        # the ED chain (deformed nodes, their anchor block and candidate grid, or buckets)
+        # on a third stream, next to the LBS chain and the main stream's occupancy + march
+        ed = self._ed_stream()
+        self._fork(main, ed)
+        with torch.cuda.stream(ed):
+            es = _lib.stream_ptr()
+            if n <= 1024:
+                _lib.call("cf_deform_nodes_block", h.nodes.data_ptr(), self._dqs.data_ptr(), n,
+                          self._anchors.data_ptr(), self._anchor_block.data_ptr(), es)
+                if getattr(self, "_cand_grid", None) is not None:
+                    _lib.call("cf_cand_grid_build", self._anchor_block.data_ptr(), n, self.cfg.ed_k,
+                              self.cfg.ed_radius, self.cfg.cand_grid_res, self.cfg.cand_grid_cmax,
+                              self._cand_grid.data_ptr(), es)
+            else:
+                _lib.call("cf_deform_nodes", h.nodes.data_ptr(), self._dqs.data_ptr(), n, self._anchors.data_ptr(), es)
+                self._anchor_buckets.build(self._anchors)
+            self._mark("ed_warp_setup")
+            self._ed_done.record(ed)
         _lib.call("cf_occ_splat_cached", h.occ_cells.data_ptr(), h.occ_nbr.data_ptr(), h.occ_w.data_ptr(),
                   h.occ_count.data_ptr(), h.occ_cap, self.cfg.ed_k, self._dqs.data_ptr(), _lib.byref(h.canon_occ),
                   _lib.byref(self.live_occ), self.live_scratch.data_ptr(), self.live_bits.data_ptr(),
@@ -634,6 +658,10 @@ class Renderer:
             e.record(st)
             self.marks.append((st.cuda_stream, name, e))
 
+    def _ed_stream(self) -> torch.cuda.Stream:
+        """The stream of the per-frame ED chain (or the caller's, in serial mode)."""
+        return torch.cuda.current_stream() if self.cfg.serial else self.side_ed
+
     def _side_stream(self) -> torch.cuda.Stream:
         """The stream of the LBS chain and the object field: a second stream, or the
         caller's stream in serial mode (cfg.serial)."""
@@ -693,8 +721,9 @@ class Renderer:
         that use the frame's warp state without rendering a view (training)."""
         if self._setup_pending and self.human is not None:
             self._human_setup()
-            # the side-stream LBS chain is done before the caller's next launch
+            # the side-stream LBS and ED chains are done before the caller's next launch
             torch.cuda.current_stream().wait_event(self._lbs_done)
+            torch.cuda.current_stream().wait_event(self._ed_done)
         self._setup_pending = False
 
     def render(self, R, t, fx, fy, cx, cy):
@@ -786,6 +815,7 @@ class Renderer:
             h = self.human
             if setup:
                 main.wait_event(self._lbs_done)
+                main.wait_event(self._ed_done)
             _lib.call("cf_human_canon", _lib.byref(self.M), self.dirs.data_ptr(), _lib.byref(hb.mo),
                       _lib.byref(self.hw), self._anchor_buckets.handle, h.lbs.buckets.handle, hb.xu.data_ptr(), s)
             self._mark("human_canon")

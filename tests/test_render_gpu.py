@@ -338,3 +338,28 @@ def test_load_pose_device_fk_matches_host_prior(setup):
     r.set_frame(sc.node_dqs(fid), sc.theta(fid), sc.bone_transforms(fid), R, t)
     c = r.render(cam.R, cam.t, cam.fx, cam.fy, cam.cx, cam.cy)
     assert _t.equal(a, c)
+
+
+@pytest.mark.parametrize("fid", [0, 7])
+def test_candidate_grid_equals_culled_scan(fid):
+    """The hierarchical k-NN of the canonicalisation (per-frame candidate grid,
+    cf_cand_grid_build) gives bit-identical canonical coordinates and flags to the
+    warp-cooperative culled scan over every node, on a full 256^2 view."""
+    sc = Scene(SceneConfig(width=256, height=256), seed=0)
+    out = []
+    for res in (48, 0):
+        cfg = RenderConfig(n_samples=128, cand_grid_res=res)
+        hf = HumanField(sc.nodes, sc.template_points, sc.skin_verts, sc.skin_weights, cfg, table_scale=0.1)
+        r = Renderer(hf, None, 256, 256, cfg)
+        r.set_frame(sc.node_dqs(fid), sc.theta(fid), sc.bone_transforms(fid))
+        cam = sc.camera
+        r.render(cam.R, cam.t, cam.fx, cam.fy, cam.cx, cam.cy)
+        torch.cuda.synchronize()
+        n, ray, i = field_samples(r.hb)
+        xu = r.hb.xu[:n].cpu().numpy()
+        order = np.lexsort((i, ray))
+        out.append((ray[order], i[order], xu[order]))
+    (r0, i0, x0), (r1, i1, x1) = out
+    assert len(r0) > 10000
+    assert np.array_equal(r0, r1) and np.array_equal(i0, i1)
+    assert np.array_equal(x0.view(np.uint32), x1.view(np.uint32))
