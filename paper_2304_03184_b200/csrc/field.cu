@@ -944,10 +944,23 @@ struct ColorBwdIO {
 };
 
 // width fp16 values of sample s into a feature-major (width, ld) block: column c at
-// dst[c * ld + s] (lanes = consecutive samples: coalesced 64-byte warp segments)
-__device__ __forceinline__ void store_fm_f16(__half* dst, int64_t s, int64_t ld, int width, const float* v) {
+// dst[c * ld + s]. Lanes are consecutive samples (s even on even lanes, ld even): the
+// lane pair (2j, 2j+1) swaps one value per column pair so that the even lane writes
+// column c and the odd lane column c+1 for both samples as one 32-bit store — two
+// coalesced 64-byte segments per warp store, half the store instructions of 2-byte
+// stores. All 32 lanes call it (shuffles); ok gates the lane's store (the pair's
+// lanes share it: a tile's lanes are all inside the capacity, a multiple of 128).
+__device__ __forceinline__ void store_fm_f16(__half* dst, int64_t s, int64_t ld, int width, const float* v, bool ok) {
+  const bool odd = threadIdx.x & 1;
+  const int64_t s0 = s & ~(int64_t)1;
 #pragma unroll 8
-  for (int c = 0; c < width; ++c) dst[(int64_t)c * ld + s] = __float2half_rn(v[c]);
+  for (int c = 0; c < width; c += 2) {
+    // even lane (sample s0) keeps v[c], sends v[c+1]; odd lane (s0 + 1) keeps v[c+1], sends v[c]
+    const float mine = odd ? v[c + 1] : v[c];
+    const float other = __shfl_xor_sync(0xffffffffu, odd ? v[c] : v[c + 1], 1);
+    const __half2 h = odd ? __floats2half2_rn(other, mine) : __floats2half2_rn(mine, other);
+    if (ok) *reinterpret_cast<__half2*>(dst + (int64_t)(c + (odd ? 1 : 0)) * ld + s0) = h;
+  }
 }
 
 // forward hidden layer with ReLU: keep the activation mask, write fp16 to A buffer (+ the
@@ -966,7 +979,7 @@ __device__ __forceinline__ uint64_t fwd_relu(Slot& S, __half* save, int64_t s, b
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q) tc::st_row8(S.abuf, S.r, c0 + 8 * q, N, v + 8 * q);
-    if (live) store_fm_f16(save + (int64_t)c0 * ld, s, ld, 32, v);
+    store_fm_f16(save + (int64_t)c0 * ld, s, ld, 32, v, live);
   }
   return mask;
 }
@@ -983,13 +996,13 @@ __device__ __forceinline__ void bwd_relu(Slot& S, uint64_t mask, __half* save, i
       if (!((mask >> (c0 + i)) & 1ull)) v[i] = 0.0f;
 #pragma unroll
     for (int q = 0; q < 4; ++q) tc::st_row8(S.abuf, S.r, c0 + 8 * q, N, v + 8 * q);
-    if (live) store_fm_f16(save + (int64_t)c0 * ld, s, ld, 32, v);
+    store_fm_f16(save + (int64_t)c0 * ld, s, ld, 32, v, live);
   }
 }
 
 __global__ void __launch_bounds__(kBwdSlots* kSlotThreads, 1)
     color_bwd_kernel(const uint8_t* __restrict__ wblob, const uint8_t* __restrict__ wtblob,
-                     const float4* __restrict__ xu, const __half* __restrict__ cfeat,
+                     const float4* __restrict__ xu, const float4* __restrict__ cfeat32,
                      const uint32_t* __restrict__ records, const double* __restrict__ dirs,
                      const float4* __restrict__ gout, const int* __restrict__ count, int64_t capacity,
                      ColorBwdIO io) {
@@ -1015,14 +1028,15 @@ __global__ void __launch_bounds__(kBwdSlots* kSlotThreads, 1)
     const bool keep = s < capacity;
     const int64_t ld = capacity;
     const bool valid = live && xu[s].w > 0.0f;
-    // ---- forward recompute from the features (fp16, feature-major (32, capacity)),
-    // saving what the weight gradients need
+    // ---- forward recompute from the features (the training forward's fp32 features,
+    // sample-major: 8 vector loads; st_row8 rounds them to the same fp16 values the
+    // feature-major copy for the dW GEMM holds), saving what the weight gradients need
     {
-      float x[32];
+      float4 x[8];
 #pragma unroll
-      for (int c = 0; c < 32; ++c) x[c] = live ? __half2float(cfeat[(int64_t)c * ld + s]) : 0.0f;
+      for (int q = 0; q < 8; ++q) x[q] = live ? cfeat32[s * 8 + q] : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-      for (int k0 = 0; k0 < 32; k0 += 8) tc::st_row8(S.abuf, S.r, k0, 32, x + k0);
+      for (int k0 = 0; k0 < 32; k0 += 8) tc::st_row8(S.abuf, S.r, k0, 32, reinterpret_cast<const float*>(x) + k0);
     }
     run_layer(S, g1, 32, 64);
     const uint64_t m_h1 = fwd_relu<64>(S, io.h1, s, keep, ld);
@@ -1044,7 +1058,7 @@ __global__ void __launch_bounds__(kBwdSlots* kSlotThreads, 1)
     cin[31] = 0.0f;
 #pragma unroll
     for (int k0 = 0; k0 < 32; k0 += 8) tc::st_row8(S.abuf, S.r, k0, 32, cin + k0);
-    if (keep) store_fm_f16(io.cin, s, ld, 32, cin);
+    store_fm_f16(io.cin, s, ld, 32, cin, keep);
     run_layer(S, c1, 32, 64);
     const uint64_t m_c1 = fwd_relu<64>(S, io.c1, s, keep, ld);
     run_layer(S, c2, 64, 64);
@@ -1067,7 +1081,7 @@ __global__ void __launch_bounds__(kBwdSlots* kSlotThreads, 1)
     }
     tc::st_row8(S.abuf, S.r, 0, 16, d_o);
     tc::st_row8(S.abuf, S.r, 8, 16, d_o + 8);
-    if (keep) store_fm_f16(io.d_o, s, ld, 16, d_o);
+    store_fm_f16(io.d_o, s, ld, 16, d_o, keep);
     run_layer(S, t_c3, 16, 64);  // dC2act = dO . C3
     bwd_relu<64>(S, m_c2, io.dc2, s, keep, ld);
     run_layer(S, t_c2, 64, 64);  // dC1act = dC2 . C2
@@ -1081,7 +1095,7 @@ __global__ void __launch_bounds__(kBwdSlots* kSlotThreads, 1)
     for (int i = 1; i < 16; ++i) dg[i] = dcin[i - 1];
     tc::st_row8(S.abuf, S.r, 0, 16, dg);
     tc::st_row8(S.abuf, S.r, 8, 16, dg + 8);
-    if (keep) store_fm_f16(io.dg, s, ld, 16, dg);
+    store_fm_f16(io.dg, s, ld, 16, dg, keep);
     run_layer(S, t_g2, 16, 64);  // dH1act = dG . G2
     bwd_relu<64>(S, m_h1, io.dh1, s, keep, ld);
     run_layer(S, t_g1, 64, 32);  // dX0 = dH1 . G1
@@ -1594,7 +1608,7 @@ int field_stage_precise(const cf_field_desc* FD, const cf_march_out* S, const do
     float4* dfeat = cfeat + cap * 8;
     float4* xc = dfeat + cap * 8;
     if (run(0))
-      cf::launch_pdl(hash_f16_kernel<4, 8, 2, 1, float, true>, hgrid, 128, 0, st, FD->dgrid,
+      cf::launch_pdl(hash_f16_kernel<4, 8, 2, 2, float, true>, cf::grid_for(cap * 2, 128, 16), 128, 0, st, FD->dgrid,
                      reinterpret_cast<const float*>(FD->dtable), xu, S->counters, cap, reinterpret_cast<uint4*>(dfeat));
     if (run(1)) {
       const int smem = 2 * kDeformW;
@@ -1694,7 +1708,8 @@ int cf_color_backward(const cf_field_desc* FD, const uint8_t* wt_blob, const cf_
   CF_CHECK_CUDA(cudaFuncSetAttribute(color_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const uint8_t* cw = FD->wblob + (FD->has_deform ? kDeformW : 0);
   color_bwd_kernel<<<persistent_grid(cap, kBwdSlots), kBwdSlots * kSlotThreads, smem, cf::as_stream(stream)>>>(
-      cw, wt_blob, reinterpret_cast<const float4*>(xu), reinterpret_cast<const __half*>(scratch), S->records, dirs,
+      cw, wt_blob, reinterpret_cast<const float4*>(xu),
+      reinterpret_cast<const float4*>(static_cast<const uint8_t*>(scratch) + train_layout(cap).cfeat32), S->records, dirs,
       reinterpret_cast<const float4*>(grad_out), S->counters, cap, o);
   return cf::check_launch("cf_color_backward");
 }
