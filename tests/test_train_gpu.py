@@ -546,3 +546,52 @@ def test_occupancy_refresh_after_training(setup):
     img = r.render(cam.R, cam.t, cam.fx, cam.fy, cam.cx, cam.cy)
     torch.cuda.synchronize()
     assert torch.isfinite(img).all() and r.sample_counts()[0] > 0
+
+
+def test_captured_step_equals_eager_steps():
+    """Trainer.capture (the whole step — ray draw, counts, forward, backward, dW, Adam,
+    repack — as one CUDA graph) computes what the eager steps compute: two trainers
+    from the same initial state, one replaying the captured step, one stepping eagerly
+    with the same draws (the device seed offset advances identically)."""
+    from paper_2304_03184_b200.train import KeyFrame
+    dev = torch.device("cuda")
+    sc = Scene(SceneConfig(width=96, height=96), seed=0)
+    cam = sc.camera
+    o, d = cam.all_rays()
+    T = lambda x, dt: torch.as_tensor(np.ascontiguousarray(x), dtype=dt, device=dev)  # noqa: E731
+    outs = []
+    for mode in ("graph", "eager"):
+        cfg = RenderConfig(n_samples=64)
+        hf = HumanField(sc.nodes, sc.template_points, sc.skin_verts, sc.skin_weights, cfg, zero_deform_out=False,
+                        table_scale=0.1)
+        of = ObjectField(sc.box_half, cfg, table_scale=0.1)
+        r = Renderer(hf, of, 96, 96, cfg)
+        r.set_frame(sc.node_dqs(0), sc.theta(0), sc.bone_transforms(0), *sc.object_pose(0))
+        kfs = []
+        for fid in (1, 4):
+            th, to, rgb, hum, obj = sc.raycast(o, d, fid)
+            depth = np.where(hum, th, np.where(obj, to, 0.0))
+            kfs.append(KeyFrame(cam, T(rgb, torch.float32), T(depth, torch.float32), T(hum, torch.uint8),
+                                T(obj, torch.uint8), T(sc.node_dqs(fid), torch.float64),
+                                T(sc.bone_transforms(fid), torch.float64),
+                                T(hf.nets.theta_bias(sc.theta(fid)), torch.float32), T(sc.theta(fid), torch.float32),
+                                *sc.object_pose(fid)))
+        tr = Trainer(r, max_rays=1024, cfg=TrainConfig())
+        if mode == "graph":
+            step = tr.capture(kfs, 1024)  # its warm-up is step 1
+            for _ in range(2):
+                loss = step()
+        else:
+            bufs = [kf.batch_buffers(1024) for kf in kfs]
+            for _ in range(3):  # the captured step's draws: seed (f * 64 + rank) * 1000003 + the device offset
+                for f, (kf, b) in enumerate(zip(kfs, bufs)):
+                    kf.draw(b, seed=f * 64 * 1000003, seed_offset=tr.seed_dev)
+                loss = tr.step(bufs)
+        torch.cuda.synchronize()
+        outs.append(({k: v.clone() for k, v in loss.items()}, hf.cgrid.table.clone(), tr.fields[0]["params"].W["G1"].clone()))
+    (lg, tg, wg), (le, te, we) = outs
+    for k in lg:
+        assert torch.allclose(lg[k], le[k], rtol=1e-4, atol=1e-7), (k, lg[k], le[k])
+    # (float-atomic summation order: Adam's ~lr * sign(g) can differ where g ~ 0)
+    assert ((tg - te).abs() > 1e-6).float().mean().item() < 1e-3
+    assert ((wg - we).abs() > 1e-6).float().mean().item() < 1e-2
