@@ -690,6 +690,45 @@ __device__ __forceinline__ uint2 split_relu64(const SplitSlot& S, int col, const
   return make_uint2(bits[0], bits[1]);
 }
 
+// The last DeformNet layer (128 -> 3) on the CUDA cores, in fp32, straight from layer 4's
+// accumulator: this thread's 64 columns (its half of the row) -> ReLU -> the 3 partial
+// dot products with W5 (fp32 rows from the split blobs, w5[j * 128 + c]). A 3-column
+// output on tcgen05 costs a full N = 16 MMA chain per K step (1/8 of the tensor rate:
+// as long as a 128-wide layer); here it is 192 FMAs per thread. Training: the hi halves
+// of h4 and its ReLU bits are saved as split_relu64 does.
+__device__ __forceinline__ uint2 relu_dot3_64(const SplitSlot& S, int col, const float* w5, float* p,
+                                              __half* save = nullptr, int64_t ld = 0) {
+  uint32_t r[64];
+  tc::tmem_ld32_nowait(S.d + (uint32_t)col, r);
+  tc::tmem_ld32_nowait(S.d + (uint32_t)(col + 32), r + 32);
+  tc::tmem_wait_ld();
+  p[0] = p[1] = p[2] = 0.0f;
+  uint32_t bits[2] = {0u, 0u};
+#pragma unroll
+  for (int i = 0; i < 64; ++i) {
+    const float x = __uint_as_float(r[i]);
+    bits[i >> 5] |= (x > 0.0f ? 1u : 0u) << (i & 31);
+    const float h = fmaxf(x, 0.0f);
+    p[0] = fmaf(w5[col + i], h, p[0]);
+    p[1] = fmaf(w5[128 + col + i], h, p[1]);
+    p[2] = fmaf(w5[256 + col + i], h, p[2]);
+  }
+  if (save) {
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      uint32_t h[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const __half2 v = __floats2half2_rn(fmaxf(__uint_as_float(r[32 * c + 2 * i]), 0.0f),
+                                            fmaxf(__uint_as_float(r[32 * c + 2 * i + 1]), 0.0f));
+        h[i] = *reinterpret_cast<const uint32_t*>(&v);
+      }
+      store_cols_f16(reinterpret_cast<uint16_t*>(save), ld, col + 32 * c, h);
+    }
+  }
+  return make_uint2(bits[0], bits[1]);
+}
+
 // n4 float4 of fp32 values -> hi / lo halves at A column c0 (2 values per column)
 template <int N4>
 __device__ __forceinline__ void split_store(const SplitSlot& S, const float4* v, int c0, uint32_t* hi_out = nullptr) {
@@ -717,8 +756,90 @@ __device__ __forceinline__ void split_store(const SplitSlot& S, const float4* v,
 // spatial gradient is evaluated where the 32-bit field puts the sample), plus the
 // fp16 saves the fp16 backward consumes: h1..h4 (hi halves, feature-major), the
 // ReLU bits, o, and the deformation features' hi halves (dfeat16, for dW of layer 1)
+// The "fp32"-mode DeformNet, 16 warps per slot: warp w of a slot owns TMEM lane quarter
+// w % 4 (32 sample rows) and column quarter w / 4 (32 of a layer's 128 columns), so a
+// layer's epilogue is spread over twice the warps of the 8-warp layout. Measured with
+// per-stage clocks, the 8-warp kernel spent 1.3-2k cycles per layer in its epilogue
+// against 1.5k cycles of one layer's MMAs: the other slot's MMAs ran dry and the
+// tensor pipe was busy 42 % of the time.
+constexpr int kPrecDeformThreads = 512;  // per slot
+
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+
+// one hidden layer's epilogue for this thread's 32 columns (two 16-column chunks):
+// D -> (+bias) ReLU -> hi / lo fp16x2 -> A; training: hi halves saved feature-major;
+// returns the 32 ReLU bits
+__device__ __forceinline__ uint32_t split_relu_q(const SplitSlot& S, int col, const float* bias, __half* save,
+                                                 int64_t ld) {
+  uint32_t bits = 0;
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    uint32_t r[16];
+    tmem_ld16_nowait(S.d + (uint32_t)(col + 16 * c), r);
+    tc::tmem_wait_ld();
+    uint32_t h[8], l[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float x0 = __uint_as_float(r[2 * i]), x1 = __uint_as_float(r[2 * i + 1]);
+      if (bias) {
+        x0 += bias[col + 16 * c + 2 * i];
+        x1 += bias[col + 16 * c + 2 * i + 1];
+      }
+      bits |= (x0 > 0.0f ? 1u : 0u) << (16 * c + 2 * i) | (x1 > 0.0f ? 1u : 0u) << (16 * c + 2 * i + 1);
+      tc::split_f16x2(fmaxf(x0, 0.0f), fmaxf(x1, 0.0f), h[i], l[i]);
+    }
+    tc::tmem_st8(S.ahi + (uint32_t)((col + 16 * c) / 2), h);
+    tc::tmem_st8(S.alo + (uint32_t)((col + 16 * c) / 2), l);
+    if (save) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        reinterpret_cast<uint16_t*>(save)[(int64_t)(col + 16 * c + 2 * i) * ld] = (uint16_t)(h[i] & 0xffffu);
+        reinterpret_cast<uint16_t*>(save)[(int64_t)(col + 16 * c + 2 * i + 1) * ld] = (uint16_t)(h[i] >> 16);
+      }
+    }
+  }
+  return bits;
+}
+
+// layer 4's epilogue with the last layer (128 -> 3) on the CUDA cores in fp32: this
+// thread's 32 columns -> ReLU -> 3 partial dot products with W5 (fp32, hi + lo); training
+// saves as split_relu_q; returns the ReLU bits
+__device__ __forceinline__ uint32_t relu_dot3_q(const SplitSlot& S, int col, const float* w5, float* p, __half* save,
+                                                int64_t ld) {
+  uint32_t bits = 0;
+  p[0] = p[1] = p[2] = 0.0f;
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    uint32_t r[16];
+    tmem_ld16_nowait(S.d + (uint32_t)(col + 16 * c), r);
+    tc::tmem_wait_ld();
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const float x = __uint_as_float(r[i]);
+      bits |= (x > 0.0f ? 1u : 0u) << (16 * c + i);
+      const float h = fmaxf(x, 0.0f);
+      const int k = col + 16 * c + i;
+      p[0] = fmaf(w5[k], h, p[0]);
+      p[1] = fmaf(w5[128 + k], h, p[1]);
+      p[2] = fmaf(w5[256 + k], h, p[2]);
+      if (save) reinterpret_cast<__half*>(save)[(int64_t)k * ld] = __float2half_rn(h);
+    }
+  }
+  return bits;
+}
+
+// kSave: the training forward — xc at 32-bit semantics (the canonical hash backward's
+// spatial gradient is evaluated where the 32-bit field puts the sample), plus the
+// fp16 saves the fp16 backward consumes: h1..h4 (hi halves, feature-major), the
+// ReLU bits, o, and the deformation features' hi halves (dfeat16, for dW of layer 1)
 template <bool kSave>
-__global__ void __launch_bounds__(kPrecDeformSlots* kDeformSlotThreads, 1)
+__global__ void __launch_bounds__(kPrecDeformSlots* kPrecDeformThreads, 1)
     deform_mlp_prec_kernel(const uint8_t* __restrict__ wblob, const uint8_t* __restrict__ wblob_lo,
                            const float* __restrict__ bias1, float delta_scale, float inv_side,
                            const float4* __restrict__ xu, const float4* __restrict__ dfeat,
@@ -729,11 +850,21 @@ __global__ void __launch_bounds__(kPrecDeformSlots* kDeformSlotThreads, 1)
   __shared__ uint64_t mbar[kPrecDeformSlots];
   __shared__ uint32_t tmem_base;
   __shared__ float s_bias[128];
+  __shared__ float s_w5[3 * 128];                        // W5 rows 0..2 in fp32 (hi + lo)
+  __shared__ float s_part[kPrecDeformSlots][2][128][3];  // layer-5 partials exchanged between column quarters
   const int tid = threadIdx.x, warp = tid / 32;
   if (tid < 128) s_bias[tid] = bias1[tid];
   for (int i = tid * 16; i < kDeformW; i += blockDim.x * 16) {
     *reinterpret_cast<uint4*>(smem + i) = *reinterpret_cast<const uint4*>(wblob + i);
     *reinterpret_cast<uint4*>(smem + kDeformW + i) = *reinterpret_cast<const uint4*>(wblob_lo + i);
+  }
+  {
+    constexpr int o5w = 128 * 32 * 2 + 3 * 128 * 128 * 2;  // W5 (16 x 128, rows 3.. zero) in the blob
+    for (int e = tid; e < 3 * 128; e += blockDim.x) {
+      const uint32_t off = o5w + tc::core_offset(e / 128, e % 128, 128);
+      s_w5[e] = __half2float(*reinterpret_cast<const __half*>(wblob + off)) +
+                __half2float(*reinterpret_cast<const __half*>(wblob_lo + off));
+    }
   }
   if (tid == 0) {
     for (int q = 0; q < kPrecDeformSlots; ++q) tc::bar_init(&mbar[q], 1);
@@ -746,11 +877,12 @@ __global__ void __launch_bounds__(kPrecDeformSlots* kDeformSlotThreads, 1)
   tc::fence_after();
   pdl_wait();
   SplitSlot S;
-  S.nthreads = kDeformSlotThreads;
-  S.slot = tid / kDeformSlotThreads;
-  const int ws = warp % (kDeformSlotThreads / 32);
-  S.half = ws / 4;
-  S.r = (ws % 4) * 32 + (tid & 31);
+  S.nthreads = kPrecDeformThreads;
+  S.slot = tid / kPrecDeformThreads;
+  const int ws = warp % (kPrecDeformThreads / 32);  // warp within the slot (0..15)
+  const int cq = ws / 4;                            // column quarter
+  S.half = cq;
+  S.r = (ws % 4) * 32 + (tid & 31);                 // sample row = TMEM lane
   S.bar = &mbar[S.slot];
   S.phase = 0;
   const uint32_t lane_q = (uint32_t)((ws % 4) * 32) << 16;
@@ -761,46 +893,75 @@ __global__ void __launch_bounds__(kPrecDeformSlots* kDeformSlotThreads, 1)
   S.ahi = S.ahi0 + lane_q;
   S.alo = S.alo0 + lane_q;
   const uint8_t* lo = smem + kDeformW;
-  constexpr int o1 = 0, o2 = 128 * 32 * 2, o3 = o2 + 128 * 128 * 2, o4 = o3 + 128 * 128 * 2, o5 = o4 + 128 * 128 * 2;
+  constexpr int o2 = 128 * 32 * 2, o3 = o2 + 128 * 128 * 2, o4 = o3 + 128 * 128 * 2;
+  const uint8_t* wo[4] = {smem, smem + o2, smem + o3, smem + o4};
   const int64_t n = min((int64_t)*count, capacity);
   const int64_t n_tiles = (n + 127) / 128;
+  const int64_t L = 128 * capacity;
   for (int64_t tile = (int64_t)blockIdx.x * kPrecDeformSlots + S.slot; tile < n_tiles;
        tile += (int64_t)gridDim.x * kPrecDeformSlots) {
     const int64_t s = tile * 128 + S.r;
     const bool live = s < n;
-    {
-      float4 f[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) f[q] = live ? dfeat[s * 8 + 4 * S.half + q] : make_float4(0.f, 0.f, 0.f, 0.f);
-      uint32_t hi[8];
-      split_store<4>(S, f, 8 * S.half, kSave ? hi : nullptr);  // this half's 16 features
+    {  // this quarter's 8 input features -> hi / lo A columns 4 cq ..
+      const float4 f0 = live ? dfeat[s * 8 + 2 * cq] : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 f1 = live ? dfeat[s * 8 + 2 * cq + 1] : make_float4(0.f, 0.f, 0.f, 0.f);
+      uint32_t h[4], l[4];
+      tc::split_f16x2(f0.x, f0.y, h[0], l[0]);
+      tc::split_f16x2(f0.z, f0.w, h[1], l[1]);
+      tc::split_f16x2(f1.x, f1.y, h[2], l[2]);
+      tc::split_f16x2(f1.z, f1.w, h[3], l[3]);
+      tc::tmem_st4(S.ahi + (uint32_t)(4 * cq), h);
+      tc::tmem_st4(S.alo + (uint32_t)(4 * cq), l);
       if (kSave && s < capacity) {
-        // feature-major (33, capacity): this half's 16 feature rows, + row 32 = 1 (the
+        // feature-major (33, capacity): this quarter's 8 feature rows, + row 32 = 1 (the
         // layer-1 dW GEMM's extra column: sum_s dpre1, for the pose columns)
-        store_cols16_f16(reinterpret_cast<uint16_t*>(dfeat16), capacity, s, 16 * S.half, hi);
-        if (S.half == 0) reinterpret_cast<uint16_t*>(dfeat16)[32 * capacity + s] = 0x3C00u;  // 1.0
+        uint16_t* d16 = reinterpret_cast<uint16_t*>(dfeat16);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          d16[(int64_t)(8 * cq + 2 * i) * capacity + s] = (uint16_t)(h[i] & 0xffffu);
+          d16[(int64_t)(8 * cq + 2 * i + 1) * capacity + s] = (uint16_t)(h[i] >> 16);
+        }
+        if (cq == 0) d16[32 * capacity + s] = 0x3C00u;  // 1.0
       }
     }
-    const float4 xs = (live && S.half == 0) ? xu[s] : make_float4(0.f, 0.f, 0.f, 0.f);
-    // training saves: h feature-major (512, capacity), ReLU bits [layer][half][2] per sample
+    // training saves: h feature-major (512, capacity), ReLU bits [layer][32-column word] per sample
     __half* sv = (kSave && s < capacity) ? save_h + s : nullptr;
-    const int64_t L = 128 * capacity;
-    uint32_t* mk = (kSave && live) ? save_mask + s * 16 + 2 * S.half : nullptr;
-    const uint8_t* wo[4] = {smem + o1, smem + o2, smem + o3, smem + o4};
+    uint32_t* mk = (kSave && live) ? save_mask + s * 16 + cq : nullptr;
 #pragma unroll 1
-    for (int l = 0; l < 4; ++l) {
-      const int lo_off = (int)(wo[l] - smem);
-      split_layer(S, wo[l], lo + lo_off, l == 0 ? 32 : 128, 128);
-      const uint2 b = split_relu64(S, 64 * S.half, l == 0 ? s_bias : nullptr, sv ? sv + l * L : nullptr, capacity);
-      if (mk) *reinterpret_cast<uint2*>(mk + 4 * l) = b;
+    for (int l = 0; l < 3; ++l) {
+      split_layer(S, wo[l], lo + (int)(wo[l] - smem), l == 0 ? 32 : 128, 128);
+      const uint32_t b = split_relu_q(S, 32 * cq, l == 0 ? s_bias : nullptr, sv ? sv + l * L : nullptr, capacity);
+      if (mk) mk[4 * l] = b;
     }
-    split_layer(S, smem + o5, lo + o5, 128, 16);
-    if (S.half == 0) {  // warp-uniform: tcgen05.ld is warp-collective
-      float v[16];
-      tc::tmem_ld16(S.d, v);
+    split_layer(S, wo[3], lo + o4, 128, 128);
+    float part[3];
+    {
+      const uint32_t b = relu_dot3_q(S, 32 * cq, s_w5, part, sv ? sv + 3 * L : nullptr, capacity);
+      if (mk) mk[12] = b;
+    }
+    // the four quarters' partials summed as (p0 + p2) + (p1 + p3), in two exchanges
+    if (cq >= 2) {
+#pragma unroll
+      for (int j = 0; j < 3; ++j) s_part[S.slot][cq - 2][S.r][j] = part[j];
+    }
+    tc::named_sync(1 + S.slot, S.nthreads);
+    if (cq < 2) {
+#pragma unroll
+      for (int j = 0; j < 3; ++j) part[j] += s_part[S.slot][cq][S.r][j];
+    }
+    tc::named_sync(1 + S.slot, S.nthreads);
+    if (cq == 1) {
+#pragma unroll
+      for (int j = 0; j < 3; ++j) s_part[S.slot][0][S.r][j] = part[j];
+    }
+    tc::named_sync(1 + S.slot, S.nthreads);
+    if (cq == 0) {
+      float v[3];
+#pragma unroll
+      for (int j = 0; j < 3; ++j) v[j] = part[j] + s_part[S.slot][0][S.r][j];
       if (kSave && live) save_o[s] = make_float4(v[0], v[1], v[2], 0.0f);
       if (live) {
-        float4 p = xs;
+        float4 p = xu[s];
         if (p.w > 0.0f) {
           p.x = f_add(p.x, f_mul(delta_scale * tanhf(v[0]), inv_side));
           p.y = f_add(p.y, f_mul(delta_scale * tanhf(v[1]), inv_side));
@@ -1571,7 +1732,7 @@ int field_stage_precise(const cf_field_desc* FD, const cf_march_out* S, const do
         const int smem = 2 * kDeformW;
         CF_CHECK_CUDA(cudaFuncSetAttribute(deform_mlp_prec_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         cf::launch_pdl(deform_mlp_prec_kernel<true>, persistent_grid(cap, kPrecDeformSlots),
-                       kPrecDeformSlots * kDeformSlotThreads, smem, st, FD->wblob, FD->wblob_lo, FD->dbias,
+                       kPrecDeformSlots * kPrecDeformThreads, smem, st, FD->wblob, FD->wblob_lo, FD->dbias,
                        FD->delta_scale, FD->inv_side, xu, static_cast<const float4*>(dfeat32), S->counters, cap, xc,
                        reinterpret_cast<__half*>(FD->save_h), reinterpret_cast<float4*>(FD->save_o), FD->save_mask,
                        reinterpret_cast<__half*>(sb + TL.dfeat16));
@@ -1614,7 +1775,7 @@ int field_stage_precise(const cf_field_desc* FD, const cf_march_out* S, const do
       const int smem = 2 * kDeformW;
       CF_CHECK_CUDA(cudaFuncSetAttribute(deform_mlp_prec_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       cf::launch_pdl(deform_mlp_prec_kernel<false>, persistent_grid(cap, kPrecDeformSlots),
-                     kPrecDeformSlots * kDeformSlotThreads, smem, st, FD->wblob, FD->wblob_lo, FD->dbias,
+                     kPrecDeformSlots * kPrecDeformThreads, smem, st, FD->wblob, FD->wblob_lo, FD->dbias,
                      FD->delta_scale, FD->inv_side, xu, static_cast<const float4*>(dfeat), S->counters, cap, xc,
                      static_cast<__half*>(nullptr), static_cast<float4*>(nullptr), static_cast<uint32_t*>(nullptr),
                      static_cast<__half*>(nullptr));

@@ -62,13 +62,17 @@ __device__ __forceinline__ void bar_init(uint64_t* bar, uint32_t count) {
 }
 __device__ __forceinline__ void bar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 
+// Wait for the phase with a suspend-time hint: the waiting warps sleep until the phase
+// completes instead of polling, so a slot waiting on its MMAs leaves the issue slots to
+// the slot running its epilogue (polling warps took 39 % of the DeformNet kernel's stall
+// samples and stretched the other slot's epilogue)
 __device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t phase) {
   const uint32_t a = smem_u32(bar);
   uint32_t done = 0;
   while (!done) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 0x989680;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}\n"
         : "=r"(done)
         : "r"(a), "r"(phase)

@@ -593,5 +593,6 @@ def test_captured_step_equals_eager_steps():
     for k in lg:
         assert torch.allclose(lg[k], le[k], rtol=1e-4, atol=1e-7), (k, lg[k], le[k])
     # (float-atomic summation order: Adam's ~lr * sign(g) can differ where g ~ 0)
-    assert ((tg - te).abs() > 1e-6).float().mean().item() < 1e-3
-    assert ((wg - we).abs() > 1e-6).float().mean().item() < 1e-2
+    # (a gradient entry that is ~0 can take either sign: Adam then moves it by ~lr either way)
+    assert ((tg - te).abs() > 1e-4).float().mean().item() < 1e-3
+    assert ((wg - we).abs() > 1e-4).float().mean().item() < 1e-3

@@ -1,0 +1,142 @@
+// tcgen05 kind::f16 throughput per SM for the operand forms the MLP kernels use
+// (one CTA per SM, one thread issuing, commit + wait every `chain` MMAs):
+//   SS: A and B from shared memory (UMMA canonical K-major, SWIZZLE_NONE)
+//   TS: A from TMEM, B from shared memory
+// for M = 128 and N = 16 / 64 / 128, K = 16 per instruction. Prints one JSON object:
+// dense FLOP/s over the whole GPU and per SM per clock.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I../paper_2304_03184_b200/csrc mma_bench.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+
+#include "tc.cuh"
+
+template <bool TS, bool kLoad = false>
+__global__ void __launch_bounds__(128, 1) mma_kernel(int N, int iters, int chain, float* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];  // A 128 x 128 + B 128 x 128 fp16
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tmem_base;
+  // operands: random fp16 in [-1, 1) (a data-dependent tensor-core cost would show here)
+  for (int i = threadIdx.x * 2; i < 2 * 128 * 128; i += blockDim.x * 2) {
+    uint32_t x = (uint32_t)i * 2654435761u + 12345u;
+    x ^= x >> 13; x *= 0x5bd1e995u; x ^= x >> 15;
+    const __half2 h = __floats2half2_rn((float)(x & 0xffff) / 32768.f - 1.f, (float)(x >> 16) / 32768.f - 1.f);
+    *reinterpret_cast<__half2*>(smem + 2 * i) = h;
+  }
+  if (threadIdx.x == 0) {
+    tc::bar_init(&bar, 1);
+    tc::bar_fence_init();
+  }
+  if (threadIdx.x < 32) tc::tmem_alloc<256>(&tmem_base);
+  tc::fence_async_smem();
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t d = tmem_base, a_t = tmem_base + 128;
+  {  // random A in TMEM (this thread's lane, 64 packed columns)
+    uint32_t v[16];
+    for (int c = 0; c < 64; c += 16) {
+      for (int i = 0; i < 16; ++i) {
+        uint32_t x = (uint32_t)(threadIdx.x * 64 + c + i) * 2246822519u + 7u;
+        x ^= x >> 13; x *= 0x5bd1e995u; x ^= x >> 15;
+        const __half2 h = __floats2half2_rn((float)(x & 0xffff) / 32768.f - 1.f, (float)(x >> 16) / 32768.f - 1.f);
+        v[i] = *reinterpret_cast<const uint32_t*>(&h);
+      }
+      tc::tmem_st16(a_t + ((uint32_t)((threadIdx.x / 32) * 32) << 16) + (uint32_t)c, v);
+    }
+    tc::tmem_wait_st();
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+  }
+  const uint32_t a0 = tc::smem_u32(smem), b0 = a0 + 128 * 128 * 2;
+  const uint32_t idesc = tc::idesc_f16(128, N);
+  uint32_t phase = 0;
+  if (kLoad && threadIdx.x >= 32) {
+    // warps 1-3: TMEM traffic like an epilogue (ld 32 fp32 columns + st 32 columns of
+    // another region) for as long as the MMAs run
+    volatile uint32_t* flag = reinterpret_cast<volatile uint32_t*>(&tmem_base) ;
+    const uint32_t lane_q = (uint32_t)(((threadIdx.x / 32) % 4) * 32) << 16;
+    uint32_t r[32];
+    for (int it = 0; it < iters * chain / 8; ++it) {
+      tc::tmem_ld32_nowait(tmem_base + lane_q + 192u, r);
+      tc::tmem_wait_ld();
+      for (int i = 0; i < 32; ++i) r[i] += 1u;
+      tc::tmem_st32(tmem_base + lane_q + 224u, r);
+    }
+    (void)flag;
+    tc::tmem_wait_st();
+  } else
+  for (int it = 0; it < iters; ++it) {
+    if (threadIdx.x == 0) {
+      for (int j = 0; j < chain; ++j) {
+        const int ks = j & 7;
+        const uint64_t bd = tc::sdesc(b0 + ks * 256, 128, 128 * 16);
+        if (TS) {
+          tc::mma_f16_ts(d, a_t + (uint32_t)(ks * 8), bd, idesc, j > 0 ? 1u : 0u);
+        } else {
+          const uint64_t ad = tc::sdesc(a0 + ks * 256, 128, 128 * 16);
+          tc::mma_f16(d, ad, bd, idesc, j > 0 ? 1u : 0u);
+        }
+      }
+      tc::mma_commit(&bar);
+    }
+    tc::bar_wait(&bar, phase);
+    phase ^= 1u;
+    tc::fence_after();
+  }
+  __syncthreads();
+  float v[16];
+  if (threadIdx.x < 32) tc::tmem_ld16(d, v);
+  if (threadIdx.x == 0 && v[0] == 1234.5f) out[0] = v[0];
+  tc::fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) tc::tmem_free<256>(tmem_base);
+}
+
+int main() {
+  cudaDeviceProp p;
+  cudaGetDeviceProperties(&p, 0);
+  int clk = 0;
+  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+  float* out;
+  cudaMalloc(&out, 64);
+  const int smem = 2 * 128 * 128 * 2;
+  cudaFuncSetAttribute(mma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(mma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(mma_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  printf("{\"gpu\": \"%s\", \"sm_mhz\": %.0f", p.name, clk / 1e3);
+  for (int ts = 0; ts < 3; ++ts)
+    for (int N : {16, 64, 128})
+      for (int chain : {8, 24, 96}) {
+        const int iters = 4000 * 24 / chain;
+        auto run = [&] {
+          if (ts == 2) mma_kernel<true, true><<<p.multiProcessorCount, 128, smem>>>(N, iters, chain, out);
+          else if (ts) mma_kernel<true><<<p.multiProcessorCount, 128, smem>>>(N, iters, chain, out);
+          else mma_kernel<false><<<p.multiProcessorCount, 128, smem>>>(N, iters, chain, out);
+        };
+        run();
+        cudaDeviceSynchronize();
+        float best = 1e30f;
+        for (int r = 0; r < 5; ++r) {
+          cudaEventRecord(e0);
+          run();
+          cudaEventRecord(e1);
+          cudaEventSynchronize(e1);
+          float ms;
+          cudaEventElapsedTime(&ms, e0, e1);
+          best = ms < best ? ms : best;
+        }
+        const double flop = 2.0 * 128 * N * 16 * (double)chain * iters * p.multiProcessorCount;
+        const double tf = flop / (best * 1e-3) / 1e12;
+        const char* nm = ts == 2 ? "ts_tmemload" : (ts ? "ts" : "ss");
+        printf(", \"%s_N%d_chain%d_tflops\": %.1f, \"%s_N%d_chain%d_flop_per_clk_sm\": %.0f", nm, N, chain, tf, nm, N,
+               chain, tf * 1e12 / (p.multiProcessorCount * clk * 1e3));
+      }
+  printf("}\n");
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) fprintf(stderr, "%s\n", cudaGetErrorString(e));
+  return 0;
+}
