@@ -990,10 +990,19 @@ __global__ void __launch_bounds__(kColorPrecSlots* kSlotThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t mbar[kColorPrecSlots];
   __shared__ uint32_t tmem_base;
+  __shared__ float s_w3[3 * 64];  // E_c's last layer (64 -> 3) in fp32 (hi + lo), on the CUDA cores
   const int tid = threadIdx.x, warp = tid / 32;
   for (int i = tid * 16; i < kColorW; i += blockDim.x * 16) {
     *reinterpret_cast<uint4*>(smem + i) = *reinterpret_cast<const uint4*>(wblob + i);
     *reinterpret_cast<uint4*>(smem + kColorW + i) = *reinterpret_cast<const uint4*>(wblob_lo + i);
+  }
+  {
+    constexpr int c3w = 64 * 32 * 2 + 16 * 64 * 2 + 64 * 32 * 2 + 64 * 64 * 2;
+    for (int e = tid; e < 3 * 64; e += blockDim.x) {
+      const uint32_t off = c3w + tc::core_offset(e / 64, e % 64, 64);
+      s_w3[e] = __half2float(*reinterpret_cast<const __half*>(wblob + off)) +
+                __half2float(*reinterpret_cast<const __half*>(wblob_lo + off));
+    }
   }
   if (tid == 0) {
     for (int q = 0; q < kColorPrecSlots; ++q) tc::bar_init(&mbar[q], 1);
@@ -1020,7 +1029,7 @@ __global__ void __launch_bounds__(kColorPrecSlots* kSlotThreads, 1)
   S.ahi = S.ahi0 + lane_q;
   S.alo = S.alo0 + lane_q;
   const uint8_t* lo = smem + kColorW;
-  constexpr int g1 = 0, g2 = 64 * 32 * 2, c1 = g2 + 16 * 64 * 2, c2 = c1 + 64 * 32 * 2, c3 = c2 + 64 * 64 * 2;
+  constexpr int g1 = 0, g2 = 64 * 32 * 2, c1 = g2 + 16 * 64 * 2, c2 = c1 + 64 * 32 * 2;
   const int64_t n = min((int64_t)*count, capacity);
   const int64_t n_tiles = (n + 127) / 128;
   for (int64_t tile = (int64_t)blockIdx.x * kColorPrecSlots + S.slot; tile < n_tiles;
@@ -1065,11 +1074,22 @@ __global__ void __launch_bounds__(kColorPrecSlots* kSlotThreads, 1)
     split_relu32(S, 0, nullptr);
     split_relu32(S, 32, nullptr);
     split_layer(S, smem + c2, lo + c2, 64, 64);
-    split_relu32(S, 0, nullptr);
-    split_relu32(S, 32, nullptr);
-    split_layer(S, smem + c3, lo + c3, 64, 16);
-    float cv[16];
-    tc::tmem_ld16(S.d, cv);
+    // the last layer (64 -> 3) in fp32 on the CUDA cores: an N = 16 MMA chain runs at
+    // 1/8 of the tensor rate (tools/mma_bench.cu), as long as a full-width layer
+    float cv[3] = {0.f, 0.f, 0.f};
+    {
+      uint32_t r[64];
+      tc::tmem_ld32_nowait(S.d, r);
+      tc::tmem_ld32_nowait(S.d + 32u, r + 32);
+      tc::tmem_wait_ld();
+#pragma unroll
+      for (int k = 0; k < 64; ++k) {
+        const float h = fmaxf(__uint_as_float(r[k]), 0.0f);
+        cv[0] = fmaf(s_w3[k], h, cv[0]);
+        cv[1] = fmaf(s_w3[64 + k], h, cv[1]);
+        cv[2] = fmaf(s_w3[128 + k], h, cv[2]);
+      }
+    }
     if (live) {
       const float r = 1.0f / (1.0f + expf(-cv[0])), g = 1.0f / (1.0f + expf(-cv[1])),
                   b = 1.0f / (1.0f + expf(-cv[2]));

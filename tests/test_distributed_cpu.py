@@ -82,3 +82,21 @@ def test_row_shards_cover_and_assemble():
     full = torch.arange(H * W * 3, dtype=torch.float32).view(H * W, 3)
     parts = [full.view(H, W, 3)[r::w].reshape(-1, 3) for r in range(w)]
     assert torch.equal(assemble_row_shards(parts, W, H), full)
+
+
+def test_shard_batch_keeps_global_ray_ids():
+    """shard_batch: the ranks' shards cover a key frame's rays once, in order, and each
+    carries the global id of its first ray (the sampler hashes global ids)."""
+    import numpy as np
+
+    from paper_2304_03184_b200.train import FrameBatch, shard_batch
+    R = 1001
+    t = lambda *shape: torch.arange(int(np.prod(shape)), dtype=torch.float32).reshape(*shape)  # noqa: E731
+    b = FrameBatch(dqs=None, bone_A=None, dbias=None, obj_R=None, obj_t=None, dirs=t(R, 3), gt_rgb=t(R, 3),
+                   gt_depth=t(R), mask_h=t(R), mask_o=t(R), ray0=5)
+    for world in (1, 2, 3, 8):
+        parts = [shard_batch(b, r, world) for r in range(world)]
+        assert torch.equal(torch.cat([p.dirs for p in parts]), b.dirs)
+        assert torch.equal(torch.cat([p.gt_depth for p in parts]), b.gt_depth)
+        starts = [p.ray0 for p in parts]
+        assert starts[0] == 5 and all(p.ray0 + p.dirs.shape[0] == q.ray0 for p, q in zip(parts, parts[1:]))

@@ -340,15 +340,16 @@ def test_load_pose_device_fk_matches_host_prior(setup):
     assert _t.equal(a, c)
 
 
-@pytest.mark.parametrize("fid", [0, 7])
-def test_candidate_grid_equals_culled_scan(fid):
+@pytest.mark.parametrize("fid,cmax", [(0, 64), (7, 64), (7, 6)])
+def test_candidate_grid_equals_culled_scan(fid, cmax):
     """The hierarchical k-NN of the canonicalisation (per-frame candidate grid,
     cf_cand_grid_build) gives bit-identical canonical coordinates and flags to the
-    warp-cooperative culled scan over every node, on a full 256^2 view."""
+    warp-cooperative culled scan over every node, on a full 256^2 view (cmax = 6: most
+    cells overflow their list and take the every-node path)."""
     sc = Scene(SceneConfig(width=256, height=256), seed=0)
     out = []
     for res in (48, 0):
-        cfg = RenderConfig(n_samples=128, cand_grid_res=res)
+        cfg = RenderConfig(n_samples=128, cand_grid_res=res, cand_grid_cmax=cmax)
         hf = HumanField(sc.nodes, sc.template_points, sc.skin_verts, sc.skin_weights, cfg, table_scale=0.1)
         r = Renderer(hf, None, 256, 256, cfg)
         r.set_frame(sc.node_dqs(fid), sc.theta(fid), sc.bone_transforms(fid))
