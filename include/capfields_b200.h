@@ -389,6 +389,17 @@ int cf_field_stage(const cf_field_desc* F, const cf_march_out* S, const double* 
 
 /* ------------------------------------------------------------------ training (SPEC train_step) */
 
+/* valid-sample compaction (training): C gets the samples of F whose flag (xu.w) > 0 —
+ * records and xu, in C->records / xu_c, count in C->counters[0] (reset here) — with
+ * vidx[j] = the full index of compacted sample j and inv[s] = the compacted index of
+ * sample s or -1. The field forward / backward then run on C; cf_scatter_rows puts
+ * their per-sample outputs (float4) back in F's order (zero for invalid samples) and
+ * cf_gather_rows takes per-sample float4 rows of F (the composite's gradients) to C. */
+int cf_compact_valid(const cf_march_out* F, const float* xu, const cf_march_out* C, float* xu_c, int* vidx, int* inv,
+                     void* stream);
+int cf_scatter_rows(const cf_march_out* F, const int* inv, const float* src, float* dst, void* stream);
+int cf_gather_rows(const cf_march_out* C, const int* vidx, const float* src, float* dst, void* stream);
+
 /* training rays of one key frame (device ray-batch sampler): n_rays pixels drawn
  * uniformly with replacement from fg_pixels (the frame's foreground pixel ids) by a
  * counter-based hash of (seed, i); gathers rgb (H*W,3), depth, masks at those pixels

@@ -242,6 +242,9 @@ _SIGS = {
     "cf_loss_composite_bwd": [_P(MarchDesc), _P(MarchOut), _p, ctypes.c_float, _p, _p, _p, ctypes.c_float, _p, _p,
                               _p, _p],
     "cf_field_train_layout": [_i64, _p],
+    "cf_compact_valid": [_P(MarchOut), _p, _P(MarchOut), _p, _p, _p, _p],
+    "cf_scatter_rows": [_P(MarchOut), _p, _p, _p, _p],
+    "cf_gather_rows": [_P(MarchOut), _p, _p, _p, _p],
     "cf_density_grid_update": [_P(HashGridDesc), _p, _p, _p, _i32, ctypes.c_float, ctypes.c_float, _i32, _p, _p, _p,
                                _p],
     "cf_dw_grouped": [_p, _i32, _p, _i64, _p],

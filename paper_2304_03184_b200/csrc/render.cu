@@ -720,6 +720,56 @@ __global__ void __launch_bounds__(128, CF_CANON_MINB) human_canon_kernel(cf_marc
   pdl_trigger();
 }
 
+// ------------------------------------------------------------ valid-sample compaction
+// The training step's human samples with no warp (flag 0: ~26 % of them at configs[2],
+// mostly the uniform samples far from the body) have sigma = 0 and no gradient: the
+// field forward / backward run on the compacted valid ones (records, xu) and only the
+// composite sees every sample. Per warp: ballot + one atomic; vidx[j] = the full index of
+// compacted sample j, inv[s] = its compacted index or -1.
+__global__ void compact_valid_kernel(const int* __restrict__ count, int64_t capacity,
+                                     const uint32_t* __restrict__ records, const float4* __restrict__ xu,
+                                     uint32_t* __restrict__ rec_c, float4* __restrict__ xu_c, int* __restrict__ vidx,
+                                     int* __restrict__ inv, int* __restrict__ count_c) {
+  const int64_t n = min((int64_t)*count, capacity);
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = base + threadIdx.x;
+    const bool live = s < n;
+    const float4 x = live ? xu[s] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const bool ok = live && x.w > 0.0f;
+    const unsigned m = __ballot_sync(0xffffffffu, ok);
+    int wbase = 0;
+    if (lane == 0 && m) wbase = atomicAdd(count_c, __popc(m));
+    wbase = __shfl_sync(0xffffffffu, wbase, 0);
+    if (!live) continue;
+    const int pos = wbase + __popc(m & ((1u << lane) - 1u));
+    if (ok) {
+      rec_c[pos] = records[s];
+      xu_c[pos] = x;
+      vidx[pos] = (int)s;
+    }
+    inv[s] = ok ? pos : -1;
+  }
+}
+
+// out[s] = out_c[inv[s]] for the valid samples, zero for the others
+__global__ void scatter_rows_kernel(const int* __restrict__ count, int64_t capacity, const int* __restrict__ inv,
+                                    const float4* __restrict__ src, float4* __restrict__ dst) {
+  const int64_t n = min((int64_t)*count, capacity);
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
+    const int j = inv[s];
+    dst[s] = j >= 0 ? src[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+// dst[j] = src[vidx[j]] over the compacted samples
+__global__ void gather_rows_kernel(const int* __restrict__ count_c, int64_t capacity, const int* __restrict__ vidx,
+                                   const float4* __restrict__ src, float4* __restrict__ dst) {
+  const int64_t n = min((int64_t)*count_c, capacity);
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+    dst[j] = src[vidx[j]];
+}
+
 // rigid object samples: live point -> object-local frame -> unit cube
 __global__ void object_canon_kernel(cf_march_desc M, const double* __restrict__ dirs,
                                     const uint32_t* __restrict__ records, const int* __restrict__ count,
@@ -1216,6 +1266,35 @@ int cf_human_canon(const cf_march_desc* M, const double* dirs, const cf_march_ou
   });
 #undef CF_HC
   return cf::check_launch("cf_human_canon");
+}
+
+int cf_compact_valid(const cf_march_out* F, const float* xu, const cf_march_out* C, float* xu_c, int* vidx, int* inv,
+                     void* stream) {
+  if (!F || !C || !xu || !xu_c || !vidx || !inv || !C->records || !C->counters || C->capacity < F->capacity)
+    return cf::fail(CF_E_BAD_ARG, "cf_compact_valid: bad args");
+  cudaStream_t st = cf::as_stream(stream);
+  cf::fill_list(st, {{C->counters, 0u, 4}});
+  if (F->capacity == 0) return CF_OK;
+  compact_valid_kernel<<<cf::grid_for(F->capacity, 256, 8), 256, 0, st>>>(
+      F->counters, F->capacity, F->records, reinterpret_cast<const float4*>(xu), C->records,
+      reinterpret_cast<float4*>(xu_c), vidx, inv, C->counters);
+  return cf::check_launch("cf_compact_valid");
+}
+
+int cf_scatter_rows(const cf_march_out* F, const int* inv, const float* src, float* dst, void* stream) {
+  if (!F || !inv || !src || !dst) return cf::fail(CF_E_BAD_ARG, "cf_scatter_rows: bad args");
+  if (F->capacity == 0) return CF_OK;
+  scatter_rows_kernel<<<cf::grid_for(F->capacity, 256, 8), 256, 0, cf::as_stream(stream)>>>(
+      F->counters, F->capacity, inv, reinterpret_cast<const float4*>(src), reinterpret_cast<float4*>(dst));
+  return cf::check_launch("cf_scatter_rows");
+}
+
+int cf_gather_rows(const cf_march_out* C, const int* vidx, const float* src, float* dst, void* stream) {
+  if (!C || !vidx || !src || !dst) return cf::fail(CF_E_BAD_ARG, "cf_gather_rows: bad args");
+  if (C->capacity == 0) return CF_OK;
+  gather_rows_kernel<<<cf::grid_for(C->capacity, 256, 8), 256, 0, cf::as_stream(stream)>>>(
+      C->counters, C->capacity, vidx, reinterpret_cast<const float4*>(src), reinterpret_cast<float4*>(dst));
+  return cf::check_launch("cf_gather_rows");
 }
 
 int cf_object_canon(const cf_march_desc* M, const double* dirs, const cf_march_out* F, float* xu_f, void* stream) {

@@ -236,6 +236,22 @@ class _BwdBuffers:
                                     ("h1", "cin", "c1", "c2", "d_o", "dc2", "dc1", "dg", "dh1", "dfeat")])
 
 
+class _CompactBuffers:
+    """The human field's valid samples (flag > 0), compacted (cf_compact_valid): the
+    field forward / backward run on these; vidx / inv map them to the full sample set
+    the composite sees."""
+
+    def __init__(self, cap, device):
+        self.records = torch.empty(cap, dtype=torch.int32, device=device)
+        self.counters = torch.zeros(4, dtype=torch.int32, device=device)
+        self.xu = torch.empty((cap, 4), dtype=torch.float32, device=device)
+        self.out = torch.empty((cap, 4), dtype=torch.float32, device=device)
+        self.grad = torch.empty((cap, 4), dtype=torch.float32, device=device)
+        self.vidx = torch.empty(cap, dtype=torch.int32, device=device)
+        self.inv = torch.empty(cap, dtype=torch.int32, device=device)
+        self.mo = _lib.MarchOut(self.records.data_ptr(), None, None, self.counters.data_ptr(), int(cap))
+
+
 def _flat_bucket(shapes: dict, device) -> tuple[torch.Tensor, dict]:
     """One zeroed fp32 buffer holding every gradient of a field (the all-reduce bucket)."""
     total = sum(int(np.prod(s)) for s in shapes.values())
@@ -286,6 +302,8 @@ class Trainer:
                 st["dtm"] = torch.zeros_like(field.dgrid.table)
                 st["dtv"] = torch.zeros_like(field.dgrid.table)
                 st["dbias"] = torch.empty(128, dtype=torch.float32, device=d)
+            if name == "human":
+                st["cbuf"] = _CompactBuffers(cap, d)
             self.fields.append(st)
         self.M = _lib.MarchDesc()
         ctypes.memmove(ctypes.byref(self.M), ctypes.byref(renderer.M), ctypes.sizeof(self.M))
@@ -371,26 +389,40 @@ class Trainer:
         desc.train = 1  # 32-bit forward + the fp16 feature-major saves of the backward
         st["desc"] = desc
         scratch = buf.scratch.data_ptr()
-        _lib.call("cf_field_forward", _lib.byref(desc), _lib.byref(buf.mo), dirs, buf.xu.data_ptr(),
-                  buf.out.data_ptr(), scratch, s)
+        # the field runs on the samples a warp reached (the human's compacted valid set;
+        # every object sample is valid), the composite on all of them
+        cb = st.get("cbuf")
+        if cb is not None:
+            _lib.call("cf_compact_valid", _lib.byref(buf.mo), buf.xu.data_ptr(), _lib.byref(cb.mo), cb.xu.data_ptr(),
+                      cb.vidx.data_ptr(), cb.inv.data_ptr(), s)
+            fmo, fxu, fout, fgrad, fcount = cb.mo, cb.xu, cb.out, cb.grad, cb.counters
+        else:
+            fmo, fxu, fout, fgrad, fcount = buf.mo, buf.xu, buf.out, bwd.grad, buf.counters
+        _lib.call("cf_field_forward", _lib.byref(desc), _lib.byref(fmo), dirs, fxu.data_ptr(), fout.data_ptr(), scratch,
+                  s)
+        if cb is not None:
+            _lib.call("cf_scatter_rows", _lib.byref(buf.mo), cb.inv.data_ptr(), cb.out.data_ptr(), buf.out.data_ptr(), s)
         _lib.call("cf_loss_composite_bwd", _lib.byref(M), _lib.byref(buf.mo), buf.out.data_ptr(), r.cfg.t_term,
                   b.gt_rgb.data_ptr(), b.gt_depth.data_ptr(), mask.data_ptr(), cfg.lambda_depth, norm,
                   bwd.grad.data_ptr(), self.stats[q].data_ptr(), s)
-        _lib.call("cf_color_backward", _lib.byref(desc), P.wt_blob.data_ptr(), _lib.byref(buf.mo), dirs,
-                  buf.xu.data_ptr(), bwd.grad.data_ptr(), scratch, _lib.byref(bwd.io), s)
+        if cb is not None:
+            _lib.call("cf_gather_rows", _lib.byref(cb.mo), cb.vidx.data_ptr(), bwd.grad.data_ptr(), cb.grad.data_ptr(),
+                      s)
+        _lib.call("cf_color_backward", _lib.byref(desc), P.wt_blob.data_ptr(), _lib.byref(fmo), dirs,
+                  fxu.data_ptr(), fgrad.data_ptr(), scratch, _lib.byref(bwd.io), s)
         db = st.get("dbufs")
-        _lib.call("cf_field_hash_backward", _lib.byref(desc), _lib.byref(buf.mo), buf.xu.data_ptr(), scratch,
+        _lib.call("cf_field_hash_backward", _lib.byref(desc), _lib.byref(fmo), fxu.data_ptr(), scratch,
                   bwd.dfeat.data_ptr(), st["tgrad"].data_ptr(), db.dxc.data_ptr() if dp is not None else None, s)
         if dp is not None:
-            _lib.call("cf_deform_backward", _lib.byref(desc), dp.wt_blob.data_ptr(), _lib.byref(buf.mo),
-                      buf.xu.data_ptr(), db.dxc.data_ptr(), _lib.byref(db.io), s)
-            _lib.call("cf_deform_hash_backward", _lib.byref(desc), _lib.byref(buf.mo), buf.xu.data_ptr(),
+            _lib.call("cf_deform_backward", _lib.byref(desc), dp.wt_blob.data_ptr(), _lib.byref(fmo),
+                      fxu.data_ptr(), db.dxc.data_ptr(), _lib.byref(db.io), s)
+            _lib.call("cf_deform_hash_backward", _lib.byref(desc), _lib.byref(fmo), fxu.data_ptr(),
                       db.d_dfeat.data_ptr(), st["dtgrad"].data_ptr(), s)
-        # weight gradients dW = dY^T X over the frame's samples: one grouped tcgen05
+        # weight gradients dW = dY^T X over the field's samples: one grouped tcgen05
         # launch, both operands feature-major (K = samples), K read on the device
         probs = self._dw_problems(st)
         arr = (_lib.DwProblem * len(probs))(*probs)
-        _lib.call("cf_dw_grouped", arr, len(probs), buf.counters.data_ptr(), self.cap, s)
+        _lib.call("cf_dw_grouped", arr, len(probs), fcount.data_ptr(), self.cap, s)
         if dp is not None:
             # theta is the same for every sample of the frame: dW1[:, 32:] = (sum_s dpre1) theta^T
             th = b.theta

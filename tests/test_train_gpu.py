@@ -79,6 +79,20 @@ def scratch_block(tr, st, k, rows_or_n, width, dtype, feature_major):
     return sc[o: o + rows_or_n * width * es].view(dtype).view(rows_or_n, width).cpu()
 
 
+def field_samples(st):
+    """The samples the field kernels ran on — the human's compacted valid set
+    (cf_compact_valid; vidx = their full indices), every sample for the object:
+    (n, ray, xu, grad, vidx)."""
+    cb = st.get("cbuf")
+    if cb is None:
+        n, ray, _ = samples_of(st)
+        return n, ray, st["buf"].xu[:n].cpu().numpy(), st["bwd"].grad[:n].cpu(), np.arange(n)
+    n = int(cb.counters[0])
+    rec = cb.records[:n].cpu().numpy().view(np.uint32)
+    return (n, (rec >> 8).astype(np.int64), cb.xu[:n].cpu().numpy(), cb.grad[:n].cpu(),
+            cb.vidx[:n].cpu().numpy().astype(np.int64))
+
+
 def samples_of(st):
     buf = st["buf"]
     n = int(buf.counters[0])
@@ -167,11 +181,10 @@ def test_color_backward_vs_autograd(setup):
     b = batches[2]
     st = tr.fields[0]
     run_frame(tr, b, st)
-    n, ray, i = samples_of(st)
-    buf, bwd, P = st["buf"], st["bwd"], st["params"]
+    n, ray, xu, g, _ = field_samples(st)  # g: scaled by the loss scale, as every gradient below
+    bwd, P = st["bwd"], st["params"]
     x0 = scratch_block(tr, st, 0, n, 32, torch.float16, True).float()  # the fp16 features, feature-major
-    valid = torch.from_numpy(buf.xu[:n].cpu().numpy()[:, 3] > 0)
-    g = bwd.grad[:n].cpu()  # scaled by the loss scale, as every gradient of the backward below
+    valid = torch.from_numpy(xu[:, 3] > 0)
     dirs = torch.from_numpy(b.dirs.cpu().numpy()[ray].astype(np.float32))
     W = {k: P.W[k].detach().cpu().half().float().requires_grad_(True) for k in P.W}
     h = lambda x: x.half().float()  # noqa: E731  fp16 operand rounding of the kernel
@@ -236,7 +249,7 @@ def test_canonical_hash_spatial_gradient(setup):
     st = tr.fields[0]
     assert "deform" in st
     run_frame(tr, b, st)
-    n, _, _ = samples_of(st)
+    n, _, _, _, _ = field_samples(st)
     xc = scratch_block(tr, st, 2, n, 4, torch.float32, False)
     keep = (xc[:, 3] > 0).numpy()
     sel = np.nonzero(keep)[0][:3000]
@@ -263,15 +276,15 @@ def test_deform_backward_vs_autograd(setup):
     b = batches[2]
     st = tr.fields[0]
     run_frame(tr, b, st)
-    n, _, _ = samples_of(st)
-    buf, D, db = st["buf"], st["deform"], st["dbufs"]
+    n, _, xu, _, _ = field_samples(st)
+    D, db = st["deform"], st["dbufs"]
     # training scratch (cf_field_train_layout): fp32 deformation features, and their fp16
     # halves feature-major with a row of ones (the layer-1 dW GEMM's pose column)
     x0 = scratch_block(tr, st, 3, n, 32, torch.float32, False)
     xd16 = scratch_block(tr, st, 1, n, 33, torch.float16, True).float()
     h = lambda x: x.half().float()  # noqa: E731  fp16 operand rounding of the kernels
     assert torch.equal(xd16[:, :32], h(x0)) and bool((xd16[:, 32] == 1).all())
-    valid = torch.from_numpy(buf.xu[:n].cpu().numpy()[:, 3] > 0).float()
+    valid = torch.from_numpy(xu[:, 3] > 0).float()
     dxc = db.dxc[:n].cpu()[:, :3]
     theta = b.theta.cpu().float()
     W = {k: D.W[k].detach().cpu().clone() for k in D.W}
@@ -459,16 +472,23 @@ def test_device_gradients_vs_f64_oracle(setup):
     values.update({k: w.cpu().numpy() for k, w in D.W.items()})
     keep = {}
     batch["keep"] = keep
-    xc_dev = scratch_block(tr, st, 2, n, 4, torch.float32, False).numpy()
-    batch["xc_value"] = xc_dev[order, :3].astype(np.float64)  # the canonical grid at the forward's positions
+    nf, _, _, _, vidx = field_samples(st)
+    xc_full = buf.xu[:n].cpu().numpy().copy()  # (invalid samples: no warp, sigma = 0 either way)
+    xc_full[vidx] = scratch_block(tr, st, 2, nf, 4, torch.float32, False).numpy()
+    batch["xc_value"] = xc_full[order, :3].astype(np.float64)  # the canonical grid at the forward's positions
     batch["cell32"] = True  # and its cells chosen as the kernels choose them
     _, ref = og.gradients(values, batch)
     # stage-wise diagnostics (device vs f64, max err / max |ref|, in the device's sample order)
     inv = np.argsort(order)
     gs = tr.grad_scale("human")
     diag = {}
-    for name, dev_val in (("dL/dfc", st["bwd"].dfeat[:n].cpu().numpy()), ("dL/dxc", st["dbufs"].dxc[:n].cpu().numpy()[:, :3]),
-                          ("dL/dfd", st["dbufs"].d_dfeat[:n].cpu().numpy())):
+    def full(a):  # the field's compacted per-sample rows -> the full sample order (0 where invalid)
+        o = np.zeros((n,) + a.shape[1:], a.dtype)
+        o[vidx] = a
+        return o
+    for name, dev_val in (("dL/dfc", full(st["bwd"].dfeat[:nf].cpu().numpy())),
+                          ("dL/dxc", full(st["dbufs"].dxc[:nf].cpu().numpy()[:, :3])),
+                          ("dL/dfd", full(st["dbufs"].d_dfeat[:nf].cpu().numpy()))):
         key = {"dL/dfc": "fc", "dL/dxc": "xc", "dL/dfd": "fd"}[name]
         rv = keep[key].grad.numpy()[inv]
         dv = dev_val / gs
