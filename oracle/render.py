@@ -133,9 +133,13 @@ def human_canon(p, nodes, dqs, k, radius, A, verts, vweights, max_dist, cmin, in
 
 
 def object_canon(p, R, t, omin, inv_side):
+    """Object-local unit-cube coordinates + flag: the object field is defined on its box
+    (the render's object grid); a sample outside [0, 1]^3 is empty (flag 0, xu 0)."""
     q = to_object(p, R, t)
     xu = ((q - np.asarray(omin)) * inv_side).astype(np.float32)
-    return np.concatenate([xu, np.ones((len(q), 1), np.float32)], axis=1)
+    inside = np.all((xu >= 0) & (xu <= 1), axis=1)
+    xu[~inside] = 0.0
+    return np.concatenate([xu, inside[:, None].astype(np.float32)], axis=1)
 
 
 def sh16(d):

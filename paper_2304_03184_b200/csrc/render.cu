@@ -721,10 +721,10 @@ __global__ void __launch_bounds__(128, CF_CANON_MINB) human_canon_kernel(cf_marc
 }
 
 // ------------------------------------------------------------ valid-sample compaction
-// The training step's human samples with no warp (flag 0: ~26 % of them at configs[2],
-// mostly the uniform samples far from the body) have sigma = 0 and no gradient: the
-// field forward / backward run on the compacted valid ones (records, xu) and only the
-// composite sees every sample. Per warp: ballot + one atomic; vidx[j] = the full index of
+// The training step's empty samples (flag 0: human samples no warp reaches, ~26 % at
+// configs[2], object samples outside the object's box — mostly the uniform samples
+// along the rays) have sigma = 0 and no gradient: the field forward / backward run on
+// the compacted valid ones (records, xu) and only the composite sees every sample. Per warp: ballot + one atomic; vidx[j] = the full index of
 // compacted sample j, inv[s] = its compacted index or -1.
 __global__ void compact_valid_kernel(const int* __restrict__ count, int64_t capacity,
                                      const uint32_t* __restrict__ records, const float4* __restrict__ xu,
@@ -784,9 +784,13 @@ __global__ void object_canon_kernel(cf_march_desc M, const double* __restrict__ 
     const uint32_t rec = records[s];
     const int64_t ray = rec >> 8;
     const d3 p = to_object(s_fr + 3, s_fr + 12, sample_p(o, load_d3(dirs + 3 * ray), rec_t(M, s, rec)));
-    xu[s] = make_float4(__double2float_rn(x_mul(x_sub(p.x, M.obj_min[0]), M.obj_inv_side)),
-                        __double2float_rn(x_mul(x_sub(p.y, M.obj_min[1]), M.obj_inv_side)),
-                        __double2float_rn(x_mul(x_sub(p.z, M.obj_min[2]), M.obj_inv_side)), 1.0f);
+    const float4 u = make_float4(__double2float_rn(x_mul(x_sub(p.x, M.obj_min[0]), M.obj_inv_side)),
+                                 __double2float_rn(x_mul(x_sub(p.y, M.obj_min[1]), M.obj_inv_side)),
+                                 __double2float_rn(x_mul(x_sub(p.z, M.obj_min[2]), M.obj_inv_side)), 1.0f);
+    // the object field is defined on its box (the render's object grid): a sample
+    // outside [0, 1]^3 (training's uniform samples) is empty
+    const bool in = u.x >= 0.f && u.x <= 1.f && u.y >= 0.f && u.y <= 1.f && u.z >= 0.f && u.z <= 1.f;
+    xu[s] = in ? u : make_float4(0.f, 0.f, 0.f, 0.f);
   }
   pdl_trigger();
 }

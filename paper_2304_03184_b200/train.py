@@ -237,9 +237,9 @@ class _BwdBuffers:
 
 
 class _CompactBuffers:
-    """The human field's valid samples (flag > 0), compacted (cf_compact_valid): the
-    field forward / backward run on these; vidx / inv map them to the full sample set
-    the composite sees."""
+    """A field's valid samples (flag > 0), compacted (cf_compact_valid): the field
+    forward / backward run on these; vidx / inv map them to the full sample set the
+    composite sees. (Human: samples no warp reaches; object: samples outside its box.)"""
 
     def __init__(self, cap, device):
         self.records = torch.empty(cap, dtype=torch.int32, device=device)
@@ -302,8 +302,7 @@ class Trainer:
                 st["dtm"] = torch.zeros_like(field.dgrid.table)
                 st["dtv"] = torch.zeros_like(field.dgrid.table)
                 st["dbias"] = torch.empty(128, dtype=torch.float32, device=d)
-            if name == "human":
-                st["cbuf"] = _CompactBuffers(cap, d)
+            st["cbuf"] = _CompactBuffers(cap, d)
             self.fields.append(st)
         self.M = _lib.MarchDesc()
         ctypes.memmove(ctypes.byref(self.M), ctypes.byref(renderer.M), ctypes.sizeof(self.M))
@@ -389,8 +388,8 @@ class Trainer:
         desc.train = 1  # 32-bit forward + the fp16 feature-major saves of the backward
         st["desc"] = desc
         scratch = buf.scratch.data_ptr()
-        # the field runs on the samples a warp reached (the human's compacted valid set;
-        # every object sample is valid), the composite on all of them
+        # the field runs on the compacted valid samples (human: reached by a warp; object:
+        # inside its box), the composite on all of them
         cb = st.get("cbuf")
         if cb is not None:
             _lib.call("cf_compact_valid", _lib.byref(buf.mo), buf.xu.data_ptr(), _lib.byref(cb.mo), cb.xu.data_ptr(),

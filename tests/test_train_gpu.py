@@ -329,8 +329,7 @@ def test_hash_backward(setup):
     b = batches[0]
     st = tr.fields[1]
     run_frame(tr, b, st)
-    n, _, _ = samples_of(st)
-    x = st["buf"].xu[:n].cpu().numpy()
+    n, _, x, _, _ = field_samples(st)
     df = st["bwd"].dfeat[:n].cpu().numpy()
     keep = x[:, 3] > 0
     ref = on.hash_encode_bwd(x[keep, :3], df[keep])
