@@ -706,7 +706,9 @@ def train_stage_roofline(tr, keyframes, per_frame, rank):
              "cf_deform_backward": "deform_bwd", "cf_deform_hash_backward": "hash_bwd_d",
              "cf_loss_composite_bwd": "loss_composite_bwd"}
     marks = []
+    dw_samples = []  # (field, the dW launch's K: the field's compacted sample count) per launch
     real = _lib.call
+    count_of = {st["cbuf"].counters.data_ptr(): st for st in tr.fields}
 
     def timed(name, *a):
         if name not in names:
@@ -716,6 +718,9 @@ def train_stage_roofline(tr, keyframes, per_frame, rank):
         real(name, *a)
         e1.record()
         marks.append((names[name], e0, e1))
+        if name == "cf_dw_grouped":
+            st = count_of[a[2]]
+            dw_samples.append((st["name"], st["cbuf"].counters[0].clone()))
     bufs = [kf.batch_buffers(per_frame) for kf in keyframes]
     for f, (kf, b) in enumerate(zip(keyframes, bufs)):
         kf.draw(b, seed=f * 64 + rank + 99)
@@ -730,18 +735,16 @@ def train_stage_roofline(tr, keyframes, per_frame, rank):
     ms = {}
     for n, e0, e1 in marks:
         ms[n] = ms.get(n, 0.0) + e0.elapsed_time(e1)
-    c = tr.counts.cpu().numpy().astype(np.int64)
-    samples = {q: float((48 * c[:, 2 * i + 1] + 64 * (c[:, 2 * i] - c[:, 2 * i + 1])).sum())
-               for i, q in enumerate(("human", "object"))}
     peaks = load_peaks()
-    work = sum(samples[q] * _DW_BYTES[q] for q in samples)
+    work = float(sum(int(k) * _DW_BYTES[q] for q, k in dw_samples))
     t = ms["dw_grouped"]
     ach = work / (t / 1e3) / 1e9
     peak, src = peaks["hbm_gbs"]
     roof = {"kernel": "dw_grouped (tcgen05 split-K weight gradients, 2 launches per frame)", "bound": "hbm",
             "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-            "per_unit": "fp16 operand rows read once per sample: human 3,052 B (E_g/E_c 932 + DeformNet 2,120), "
-                        "object 932 B", "peak_source": src, "ms": t, "traffic": None,
+            "per_unit": "fp16 operand rows read once per field sample (the compacted valid ones, the GEMMs' K): "
+                        "human 3,052 B (E_g/E_c 932 + DeformNet 2,120), object 932 B",
+            "peak_source": src, "ms": t, "traffic": None,
             "timing": "CUDA events around each launch of one eager step (update=False), summed per kernel"}
     top = max(ms, key=ms.get)
     roof["dominant_by_time"] = top
