@@ -438,15 +438,18 @@ def run_ours(args, rank, world, pg):
     stages = {k: roofline_entry(k, costs[k], stage_ms[k], peaks) for k in costs if k in stage_ms}
     dom = max(stages, key=lambda k: stages[k]["ms"])
     roof = dict(stages[dom])
-    traffic = None
-    try:
-        t = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(f"{args.precision}:{dom}")
-        traffic = float(t["dram_bytes_per_launch"]) if isinstance(t, dict) else t
+    try:  # DRAM bytes per launch from the committed ncu --set full capture (profiles/)
+        tr_map = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
     except Exception:
-        pass
-    roof["traffic"] = traffic
-    roof["all_stages"] = {k: {x: v[x] for x in ("ms", "bound", "achieved", "peak", "unit", "frac")}
-                          for k, v in stages.items()}
+        tr_map = {}
+
+    def traffic_of(k):
+        t = tr_map.get(f"{args.precision}:{k}")
+        return float(t["dram_bytes_per_launch"]) if isinstance(t, dict) else None
+    roof["traffic"] = traffic_of(dom)
+    roof["traffic_source"] = "profiles/ncu_traffic.json (dram__bytes_read.sum + dram__bytes_write.sum of one launch)"
+    roof["all_stages"] = {k: dict({x: v[x] for x in ("ms", "bound", "achieved", "peak", "unit", "frac")},
+                                  traffic=traffic_of(k)) for k, v in stages.items()}
     roof["timing"] = (f"per-kernel CUDA events of the frame replayed serialised on one stream (sum {serial_ms:.3f} "
                       f"ms vs {ms_per_step:.3f} ms overlapped)")
 
