@@ -742,7 +742,8 @@ typedef struct cf_nr_system {
   double* val;
   int* col;
   double* res;
-  double* energy;
+  double* energy;   /* [data, bind, reg, pose] energies, each a fixed-order sum (deterministic) */
+  int jac_terms;    /* with val: bit 0 data, 1 bind, 2 reg, 3 pose = write that term's Jacobian rows */
 } cf_nr_system;
 int cf_nr_warp(const double* dqs, const int* idx, const double* w, int k, const double* pts, const double* normals,
                int64_t n, double* out_pts, double* out_normals, void* stream);

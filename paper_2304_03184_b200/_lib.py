@@ -171,7 +171,8 @@ class NrSystem(ctypes.Structure):
                 ("reg_row0", ctypes.c_int64), ("reg_entry0", ctypes.c_int64),
                 ("pose_lbs", _p), ("pose_u", _p), ("pose_n", _p), ("pose_jth", _p), ("n_pose", ctypes.c_int64),
                 ("w_pose", ctypes.c_double), ("pose_row0", ctypes.c_int64), ("pose_entry0", ctypes.c_int64),
-                ("val", _p), ("col", _p), ("res", _p), ("energy", _p)]
+                ("val", _p), ("col", _p), ("res", _p), ("energy", _p),
+                ("jac_terms", ctypes.c_int)]
 
 
 class DeformBwdIO(ctypes.Structure):

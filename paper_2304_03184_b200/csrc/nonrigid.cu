@@ -41,9 +41,23 @@ __global__ void __launch_bounds__(128) nr_warp_kernel(const double* __restrict__
   }
 }
 
+// Energy of a term: one CTA per term (grid-stride over its rows), each thread's partial
+// in a fixed order, then a fixed-order tree over the block and a plain store — the same
+// sum every run (the LM accept test compares energies; atomics made near-ties flip).
+__device__ __forceinline__ void block_energy_store(double e, double* __restrict__ energy) {
+  __shared__ double red[1024];
+  red[threadIdx.x] = e;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *energy = red[0];
+}
+
 // data term: r = n . (v - u) on the blended warp; row c: 6 entries per neighbour
 // [s g wn_j, s n wn_j] at columns 6 nbr_j + 0..5 (g = v x n, s = sqrt(w huber_weight(r)))
-__global__ void __launch_bounds__(128) nr_data_kernel(const double* __restrict__ warped, const int64_t* __restrict__ ci,
+__global__ void __launch_bounds__(1024) nr_data_kernel(const double* __restrict__ warped, const int64_t* __restrict__ ci,
                                                       const double* __restrict__ cu, const double* __restrict__ cn,
                                                       int64_t C, const int* __restrict__ bidx,
                                                       const double* __restrict__ bwn, int k, double wdata,
@@ -73,12 +87,12 @@ __global__ void __launch_bounds__(128) nr_data_kernel(const double* __restrict__
     }
     res[c] = s * r;
   }
-  atomicAdd(energy, e);
+  block_energy_store(e, energy);
 }
 
 // bind term per node i (rows 3i .. 3i+2 of the block): r = dq_apply(dq_i, x_i) - LBS(x_i);
 // row a: -s [v]_x[a] (cols 6i..6i+2), s I[a] (cols 6i+3..6i+5), -s Jth[i,a,:] (cols 6n..)
-__global__ void __launch_bounds__(128) nr_bind_kernel(const double* __restrict__ dqs, const double* __restrict__ nodes,
+__global__ void __launch_bounds__(1024) nr_bind_kernel(const double* __restrict__ dqs, const double* __restrict__ nodes,
                                                       const double* __restrict__ node_lbs,
                                                       const double* __restrict__ jth, int n, int T, double s,
                                                       double* __restrict__ val, int* __restrict__ col,
@@ -105,11 +119,11 @@ __global__ void __launch_bounds__(128) nr_bind_kernel(const double* __restrict__
       res[3 * i + a] = s * r[a];
     }
   }
-  atomicAdd(energy, e);
+  block_energy_store(e, energy);
 }
 
 // reg term per edge (i, j): a = dq_i(x_j), b = dq_j(x_j), r = a - b; 12 entries per row
-__global__ void __launch_bounds__(128) nr_reg_kernel(const double* __restrict__ dqs, const double* __restrict__ nodes,
+__global__ void __launch_bounds__(1024) nr_reg_kernel(const double* __restrict__ dqs, const double* __restrict__ nodes,
                                                      const int64_t* __restrict__ edges, int64_t E, double s,
                                                      double* __restrict__ val, int* __restrict__ col,
                                                      double* __restrict__ res, double* __restrict__ energy) {
@@ -138,11 +152,11 @@ __global__ void __launch_bounds__(128) nr_reg_kernel(const double* __restrict__ 
       res[3 * q + row] = s * r[row];
     }
   }
-  atomicAdd(energy, e);
+  block_energy_store(e, energy);
 }
 
 // pose term per correspondence p: r = n . (LBS(x_p) - u); row: s (n . Jth[p]) over theta
-__global__ void __launch_bounds__(128) nr_pose_kernel(const double* __restrict__ lbs_pts, const double* __restrict__ pu,
+__global__ void __launch_bounds__(1024) nr_pose_kernel(const double* __restrict__ lbs_pts, const double* __restrict__ pu,
                                                       const double* __restrict__ pn, const double* __restrict__ jth,
                                                       int64_t P, int T, int n_nodes, double wpose,
                                                       double* __restrict__ val, int* __restrict__ col,
@@ -161,7 +175,7 @@ __global__ void __launch_bounds__(128) nr_pose_kernel(const double* __restrict__
     }
     res[p] = s * r;
   }
-  atomicAdd(energy, e);
+  block_energy_store(e, energy);
 }
 
 // _apply_step: dq_i <- normalize(dq(quat(xi_i[:3]), xi_i[3:]) * dq_i)
@@ -215,25 +229,27 @@ int cf_nr_terms(const cf_nr_system* S, void* stream) {
   cudaStream_t st = cf::as_stream(stream);
   cf::fill_u32(S->energy, 0u, 2 * 4, st);  // data, bind, reg, pose
   const bool J = S->val != nullptr;
-  auto V = [&](int64_t e) { return J ? S->val + e : nullptr; };
-  auto Cc = [&](int64_t e) { return J ? S->col + e : nullptr; };
-  auto R = [&](int64_t r) { return J ? S->res + r : nullptr; };
+  // a term's Jacobian rows are written only when val is set and its jac_terms bit is on;
+  // its energy is always evaluated (the reference's energy_terms computes every term)
+  auto on = [&](int bit) { return J && (S->jac_terms & (1 << bit)); };
+  auto V = [&](int64_t e, int bit) { return on(bit) ? S->val + e : nullptr; };
+  auto Cc = [&](int64_t e, int bit) { return on(bit) ? S->col + e : nullptr; };
+  auto R = [&](int64_t r, int bit) { return on(bit) ? S->res + r : nullptr; };
   if (S->n_data > 0)
-    nr_data_kernel<<<cf::grid_for(S->n_data, 128, 4), 128, 0, st>>>(
-        S->warped, S->data_idx, S->data_u, S->data_n, S->n_data, S->blend_idx, S->blend_wn, S->k, S->w_data,
-        V(S->data_entry0), Cc(S->data_entry0), R(S->data_row0), S->energy + 0);
+    nr_data_kernel<<<1, 1024, 0, st>>>(S->warped, S->data_idx, S->data_u, S->data_n, S->n_data, S->blend_idx,
+                                       S->blend_wn, S->k, S->w_data, V(S->data_entry0, 0), Cc(S->data_entry0, 0),
+                                       R(S->data_row0, 0), S->energy + 0);
   if (S->do_bind)
-    nr_bind_kernel<<<cf::grid_for(S->n_nodes, 128, 4), 128, 0, st>>>(
-        S->dqs, S->nodes, S->node_lbs, S->node_jth, S->n_nodes, S->n_theta, S->s_bind, V(S->bind_entry0),
-        Cc(S->bind_entry0), R(S->bind_row0), S->energy + 1);
+    nr_bind_kernel<<<1, 1024, 0, st>>>(S->dqs, S->nodes, S->node_lbs, S->node_jth, S->n_nodes, S->n_theta,
+                                       S->s_bind, V(S->bind_entry0, 1), Cc(S->bind_entry0, 1), R(S->bind_row0, 1),
+                                       S->energy + 1);
   if (S->n_edges > 0)
-    nr_reg_kernel<<<cf::grid_for(S->n_edges, 128, 4), 128, 0, st>>>(S->dqs, S->nodes, S->edges, S->n_edges,
-                                                                     S->s_reg, V(S->reg_entry0), Cc(S->reg_entry0),
-                                                                     R(S->reg_row0), S->energy + 2);
+    nr_reg_kernel<<<1, 1024, 0, st>>>(S->dqs, S->nodes, S->edges, S->n_edges, S->s_reg, V(S->reg_entry0, 2),
+                                      Cc(S->reg_entry0, 2), R(S->reg_row0, 2), S->energy + 2);
   if (S->n_pose > 0)
-    nr_pose_kernel<<<cf::grid_for(S->n_pose, 128, 4), 128, 0, st>>>(
-        S->pose_lbs, S->pose_u, S->pose_n, S->pose_jth, S->n_pose, S->n_theta, S->n_nodes, S->w_pose,
-        V(S->pose_entry0), Cc(S->pose_entry0), R(S->pose_row0), S->energy + 3);
+    nr_pose_kernel<<<1, 1024, 0, st>>>(S->pose_lbs, S->pose_u, S->pose_n, S->pose_jth, S->n_pose, S->n_theta,
+                                       S->n_nodes, S->w_pose, V(S->pose_entry0, 3), Cc(S->pose_entry0, 3),
+                                       R(S->pose_row0, 3), S->energy + 3);
   return cf::check_launch("cf_nr_terms");
 }
 

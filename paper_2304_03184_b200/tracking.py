@@ -442,7 +442,8 @@ class NonrigidTracker:
                      ("inter", int(inter[4].numel()) if use["inter"] else 0, 6)]
             rows = sum(s[1] for s in sizes)
             if rows == 0:
-                return self._energy(state), None, None
+                _lib.call("cf_nr_terms", _lib.byref(S), _lib.stream_ptr())
+                return self._energy(state, lim_r), None, None
             nnz = sum(s[1] * s[2] for s in sizes)
             d = self.d_nodes.device
             val = torch.zeros(nnz, dtype=torch.float64, device=d)
@@ -458,12 +459,9 @@ class NonrigidTracker:
             S.bind_row0, S.bind_entry0 = off["bind"]
             S.reg_row0, S.reg_entry0 = off["reg"]
             S.pose_row0, S.pose_entry0 = off["pose"]
-            if not use["data"]:
-                S.n_data = 0
-            if not use["bind"]:
-                S.do_bind = 0
-            if not use["reg"]:
-                S.n_edges = 0
+            # every energy is evaluated; only the used terms write Jacobian rows
+            S.jac_terms = (int(bool(use["data"])) | int(bool(use["bind"])) << 1 | int(bool(use["reg"])) << 2
+                           | int(bool(use["pose"])) << 3)
             if use["bind"]:
                 jn = lbs_theta_jacobian(self.skel, state.theta, self.d_nodes, self.d_node_w, as_tensor=True)
                 S.node_jth = jn.data_ptr()
@@ -471,8 +469,6 @@ class NonrigidTracker:
                 jp = lbs_theta_jacobian(self.skel, state.theta, self.d_pts[pi].contiguous(),
                                         self.d_lbs[pi].contiguous(), as_tensor=True)
                 S.pose_jth = jp.data_ptr()
-            else:
-                S.n_pose = 0
             _lib.call("cf_nr_terms", _lib.byref(S), _lib.stream_ptr())
             if use["prior"]:  # quadratic joint-limit rows (tracking.py:445-456)
                 s = np.sqrt(w.prior)

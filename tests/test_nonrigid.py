@@ -126,3 +126,41 @@ def test_interpenetration_term(ref):
     assert info["iterations"] >= 1
     for before, after in info["accepted"]:
         assert after <= before + 1e-12
+
+
+def test_energies_evaluated_with_zero_weights_and_deterministic(ref):
+    """A zero weight drops a term's Jacobian rows but not its energy (the reference's
+    energy_terms computes every term, tracking.py:288-336), and each energy is a
+    fixed-order sum: bit-identical across evaluations (the LM accept test compares them)."""
+    from paper_2304_03184_b200.tracking import EnergyWeights, NonrigidTracker, SolveState
+    model, cam = _model(ref)
+    tr = NonrigidTracker(model, cam, surface_samples=1500)
+    n = len(ref["nodes"])
+    rng = np.random.default_rng(3)
+    dq = np.zeros((n, 8))
+    dq[:, 0] = 1.0
+    dq[:, 5:8] = rng.normal(scale=0.01, size=(n, 3))
+    st = SolveState(dq, np.zeros(72))  # no joint-limit rows
+    m = len(tr.sub_pts)
+    idx = np.arange(m, dtype=np.int64)
+    nrm = rng.normal(size=(m, 3))
+    nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
+    data = (idx, tr.sub_pts + rng.normal(scale=0.01, size=(m, 3)), nrm)
+    empty = (np.zeros(0, dtype=np.int64), np.zeros((0, 3)), np.zeros((0, 3)))
+    full = tr.energy_terms(st, data, empty)
+    again = [tr.energy_terms(st, data, empty) for _ in range(3)]
+    assert all(a == full for a in again)
+    assert full["data"] > 0 and full["reg"] > 0 and full["bind"] > 0
+    base = tr.weights
+    for term in ("data", "bind", "reg"):
+        kw = {k: getattr(base, k) for k in ("data", "bind", "reg", "prior", "pose", "inter")}
+        kw[term] = 0.0
+        tr.weights = EnergyWeights(**kw)
+        e, J, r = tr._system(st, data, empty, True)
+        for k in ("data", "bind", "reg", "pose"):
+            assert e[k] == full[k], (term, k)
+        rows = J[3][0]
+        want = (m if term != "data" else 0) + (3 * n if term != "bind" else 0) + \
+            (3 * len(ref["edges"]) if term != "reg" else 0)
+        assert rows == want, (term, rows, want)
+    tr.weights = base
