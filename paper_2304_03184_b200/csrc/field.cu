@@ -182,10 +182,9 @@ __device__ __forceinline__ void run_layer(Slot& S, int w_off, int K, int N) {
   tc::fence_async_smem();
   tc::fence_before();
   tc::named_sync(1 + S.slot, kSlotThreads);
-  if (S.r == 0) {
+  if (S.r < 32) {  // the slot's first warp issues (tc::layer_ss_warp)
     tc::fence_after();
-    tc::issue_layer(S.tmem, S.abuf, S.w_s + w_off, K, N);
-    tc::mma_commit(S.bar);
+    tc::layer_ss_warp(S.tmem, S.abuf, S.w_s + w_off, K, N, S.bar);
   }
   tc::bar_wait(S.bar, S.phase);
   S.phase ^= 1u;
@@ -273,11 +272,10 @@ __device__ __forceinline__ void ts_layer(TsSlot& S, const uint8_t* w, int K, int
   else tc::tmem_wait_st();
   tc::fence_before();
   tc::named_sync(1 + S.slot, kDeformSlotThreads);
-  if (threadIdx.x % kDeformSlotThreads == 0) {
+  if (threadIdx.x % kDeformSlotThreads < 32) {  // the slot's first warp issues
     tc::fence_after();
-    if (S.abuf) tc::issue_layer(S.d0, S.abuf, w, K, N);
-    else tc::issue_layer_ts(S.d0, S.a0, w, K, N);
-    tc::mma_commit(S.bar);
+    if (S.abuf) tc::layer_ss_warp(S.d0, S.abuf, w, K, N, S.bar);
+    else tc::layer_ts_warp(S.d0, S.a0, w, K, N, S.bar);
   }
   tc::bar_wait(S.bar, S.phase);
   S.phase ^= 1u;
@@ -476,10 +474,9 @@ __device__ __forceinline__ void cts_layer(CSlot& S, const uint8_t* w, int K, int
   tc::tmem_wait_st();
   tc::fence_before();
   tc::named_sync(1 + S.slot, kSlotThreads);
-  if (S.r == 0) {
+  if (S.r < 32) {  // the slot's first warp issues
     tc::fence_after();
-    tc::issue_layer_ts(S.d0, S.a0, w, K, N);
-    tc::mma_commit(S.bar);
+    tc::layer_ts_warp(S.d0, S.a0, w, K, N, S.bar);
   }
   tc::bar_wait(S.bar, S.phase);
   S.phase ^= 1u;
@@ -600,7 +597,7 @@ __global__ void __launch_bounds__(kColorTsSlots* kSlotThreads, 1)
 
 // ---------------------------------------------------------------- "fp32" precision mode
 // The same networks with every operand split into fp16 hi + lo halves and three
-// MMA chains per layer (tc::issue_layer_ts_split): ~22-bit operands, fp32 TMEM
+// MMA chains per layer (tc::issue_split_warp): ~22-bit operands, fp32 TMEM
 // accumulation, fp32 hash features in. This is the mode that meets the SPEC's
 // 32-bit semantics within 1e-4 (tests/test_precision_gpu.py);
 // the fp16-operand kernels above are the "fp16" mode.
@@ -617,116 +614,32 @@ struct SplitSlot {
   int slot, r, half, nthreads;
 };
 
-__device__ __forceinline__ void split_layer(SplitSlot& S, const uint8_t* w_hi, const uint8_t* w_lo, int K, int N) {
+// one split layer of a slot: the slot's threads finish their TMEM stores, its first
+// warp issues the three chains and the commit (tc::issue_split_warp), all wait for D
+template <int K>
+__device__ __forceinline__ void split_layer(SplitSlot& S, const uint8_t* w_hi, const uint8_t* w_lo, int N) {
   tc::tmem_wait_st();
   tc::fence_before();
   tc::named_sync(1 + S.slot, S.nthreads);
-  if (threadIdx.x % S.nthreads == 0) {
+  if ((threadIdx.x % S.nthreads) < 32) {
     tc::fence_after();
-    tc::issue_layer_ts_split(S.d0, S.ahi0, S.alo0, w_hi, w_lo, K, N);
-    tc::mma_commit(S.bar);
+    tc::issue_split_warp<K>(S.d0, S.ahi0, S.alo0, w_hi, w_lo, N, S.bar);
   }
   tc::bar_wait(S.bar, S.phase);
   S.phase ^= 1u;
   tc::fence_after();
 }
 
-// 32 D columns from col -> (+bias) ReLU -> hi / lo fp16x2 -> A columns col/2.
-// Training (save != nullptr): the hi halves (= the fp16 rounding of the activation,
-// what the fp16 backward consumes) also go to the feature-major save block; returns
-// the ReLU derivative bits of the 32 columns.
-__device__ __forceinline__ uint32_t split_relu32(const SplitSlot& S, int col, const float* bias,
-                                                 __half* save = nullptr, int64_t ld = 0) {
+// 32 D columns from col -> ReLU -> hi / lo fp16x2 -> A columns col/2 (tc::split_relu_rz)
+__device__ __forceinline__ void split_relu32(const SplitSlot& S, int col) {
   uint32_t r[32];
   tc::tmem_ld32_nowait(S.d + (uint32_t)col, r);
   tc::tmem_wait_ld();
   uint32_t h[16], l[16];
-  uint32_t bits = 0;
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    float x0 = __uint_as_float(r[2 * i]), x1 = __uint_as_float(r[2 * i + 1]);
-    if (bias) {
-      x0 += bias[col + 2 * i];
-      x1 += bias[col + 2 * i + 1];
-    }
-    bits |= (x0 > 0.0f ? 1u : 0u) << (2 * i) | (x1 > 0.0f ? 1u : 0u) << (2 * i + 1);
-    tc::split_f16x2(fmaxf(x0, 0.0f), fmaxf(x1, 0.0f), h[i], l[i]);
-  }
+  for (int i = 0; i < 16; ++i) tc::split_relu_rz(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]), h[i], l[i]);
   tc::tmem_st16(S.ahi + (uint32_t)(col / 2), h);
   tc::tmem_st16(S.alo + (uint32_t)(col / 2), l);
-  if (save) store_cols_f16(reinterpret_cast<uint16_t*>(save), ld, col, h);
-  return bits;
-}
-
-// 64 D columns from col (this thread's half of the row): both 32-column TMEM loads in
-// flight before one wait, then (+bias) ReLU -> hi / lo fp16x2 -> A columns col/2;
-// training saves and ReLU bits as split_relu32 (two words)
-__device__ __forceinline__ uint2 split_relu64(const SplitSlot& S, int col, const float* bias, __half* save = nullptr,
-                                              int64_t ld = 0) {
-  uint32_t r[64];
-  tc::tmem_ld32_nowait(S.d + (uint32_t)col, r);
-  tc::tmem_ld32_nowait(S.d + (uint32_t)(col + 32), r + 32);
-  tc::tmem_wait_ld();
-  uint32_t bits[2];
-#pragma unroll
-  for (int c = 0; c < 2; ++c) {
-    uint32_t h[16], l[16];
-    uint32_t b = 0;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      float x0 = __uint_as_float(r[32 * c + 2 * i]), x1 = __uint_as_float(r[32 * c + 2 * i + 1]);
-      if (bias) {
-        x0 += bias[col + 32 * c + 2 * i];
-        x1 += bias[col + 32 * c + 2 * i + 1];
-      }
-      b |= (x0 > 0.0f ? 1u : 0u) << (2 * i) | (x1 > 0.0f ? 1u : 0u) << (2 * i + 1);
-      tc::split_f16x2(fmaxf(x0, 0.0f), fmaxf(x1, 0.0f), h[i], l[i]);
-    }
-    tc::tmem_st16(S.ahi + (uint32_t)((col + 32 * c) / 2), h);
-    tc::tmem_st16(S.alo + (uint32_t)((col + 32 * c) / 2), l);
-    if (save) store_cols_f16(reinterpret_cast<uint16_t*>(save), ld, col + 32 * c, h);
-    bits[c] = b;
-  }
-  return make_uint2(bits[0], bits[1]);
-}
-
-// The last DeformNet layer (128 -> 3) on the CUDA cores, in fp32, straight from layer 4's
-// accumulator: this thread's 64 columns (its half of the row) -> ReLU -> the 3 partial
-// dot products with W5 (fp32 rows from the split blobs, w5[j * 128 + c]). A 3-column
-// output on tcgen05 costs a full N = 16 MMA chain per K step (1/8 of the tensor rate:
-// as long as a 128-wide layer); here it is 192 FMAs per thread. Training: the hi halves
-// of h4 and its ReLU bits are saved as split_relu64 does.
-__device__ __forceinline__ uint2 relu_dot3_64(const SplitSlot& S, int col, const float* w5, float* p,
-                                              __half* save = nullptr, int64_t ld = 0) {
-  uint32_t r[64];
-  tc::tmem_ld32_nowait(S.d + (uint32_t)col, r);
-  tc::tmem_ld32_nowait(S.d + (uint32_t)(col + 32), r + 32);
-  tc::tmem_wait_ld();
-  p[0] = p[1] = p[2] = 0.0f;
-  uint32_t bits[2] = {0u, 0u};
-#pragma unroll
-  for (int i = 0; i < 64; ++i) {
-    const float x = __uint_as_float(r[i]);
-    bits[i >> 5] |= (x > 0.0f ? 1u : 0u) << (i & 31);
-    const float h = fmaxf(x, 0.0f);
-    p[0] = fmaf(w5[col + i], h, p[0]);
-    p[1] = fmaf(w5[128 + col + i], h, p[1]);
-    p[2] = fmaf(w5[256 + col + i], h, p[2]);
-  }
-  if (save) {
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      uint32_t h[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const __half2 v = __floats2half2_rn(fmaxf(__uint_as_float(r[32 * c + 2 * i]), 0.0f),
-                                            fmaxf(__uint_as_float(r[32 * c + 2 * i + 1]), 0.0f));
-        h[i] = *reinterpret_cast<const uint32_t*>(&v);
-      }
-      store_cols_f16(reinterpret_cast<uint16_t*>(save), ld, col + 32 * c, h);
-    }
-  }
-  return make_uint2(bits[0], bits[1]);
 }
 
 // n4 float4 of fp32 values -> hi / lo halves at A column c0 (2 values per column)
@@ -775,6 +688,10 @@ __device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t* r) {
 // one hidden layer's epilogue for this thread's 32 columns (two 16-column chunks):
 // D -> (+bias) ReLU -> hi / lo fp16x2 -> A; training: hi halves saved feature-major;
 // returns the 32 ReLU bits
+// The render (kTrain false) splits with tc::split_relu_rz (5 instructions per pair); the
+// training forward keeps the round-to-nearest hi half, the fp16 activation its backward
+// consumes, and computes the ReLU bits.
+template <bool kTrain>
 __device__ __forceinline__ uint32_t split_relu_q(const SplitSlot& S, int col, const float* bias, __half* save,
                                                  int64_t ld) {
   uint32_t bits = 0;
@@ -785,18 +702,28 @@ __device__ __forceinline__ uint32_t split_relu_q(const SplitSlot& S, int col, co
     tc::tmem_wait_ld();
     uint32_t h[8], l[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      float x0 = __uint_as_float(r[2 * i]), x1 = __uint_as_float(r[2 * i + 1]);
+    for (int i = 0; i < 8; i += 2) {
+      float x[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) x[j] = __uint_as_float(r[2 * i + j]);
       if (bias) {
-        x0 += bias[col + 16 * c + 2 * i];
-        x1 += bias[col + 16 * c + 2 * i + 1];
+        const float4 bv = *reinterpret_cast<const float4*>(bias + col + 16 * c + 2 * i);
+        x[0] += bv.x, x[1] += bv.y, x[2] += bv.z, x[3] += bv.w;
       }
-      bits |= (x0 > 0.0f ? 1u : 0u) << (16 * c + 2 * i) | (x1 > 0.0f ? 1u : 0u) << (16 * c + 2 * i + 1);
-      tc::split_f16x2(fmaxf(x0, 0.0f), fmaxf(x1, 0.0f), h[i], l[i]);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        if constexpr (kTrain) {
+          bits |= (x[2 * q] > 0.0f ? 1u : 0u) << (16 * c + 2 * (i + q)) |
+                  (x[2 * q + 1] > 0.0f ? 1u : 0u) << (16 * c + 2 * (i + q) + 1);
+          tc::split_f16x2(fmaxf(x[2 * q], 0.0f), fmaxf(x[2 * q + 1], 0.0f), h[i + q], l[i + q]);
+        } else {
+          tc::split_relu_rz(x[2 * q], x[2 * q + 1], h[i + q], l[i + q]);
+        }
+      }
     }
     tc::tmem_st8(S.ahi + (uint32_t)((col + 16 * c) / 2), h);
     tc::tmem_st8(S.alo + (uint32_t)((col + 16 * c) / 2), l);
-    if (save) {
+    if (kTrain && save) {
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         reinterpret_cast<uint16_t*>(save)[(int64_t)(col + 16 * c + 2 * i) * ld] = (uint16_t)(h[i] & 0xffffu);
@@ -810,6 +737,7 @@ __device__ __forceinline__ uint32_t split_relu_q(const SplitSlot& S, int col, co
 // layer 4's epilogue with the last layer (128 -> 3) on the CUDA cores in fp32: this
 // thread's 32 columns -> ReLU -> 3 partial dot products with W5 (fp32, hi + lo); training
 // saves as split_relu_q; returns the ReLU bits
+template <bool kTrain>
 __device__ __forceinline__ uint32_t relu_dot3_q(const SplitSlot& S, int col, const float* w5, float* p, __half* save,
                                                 int64_t ld) {
   uint32_t bits = 0;
@@ -820,15 +748,21 @@ __device__ __forceinline__ uint32_t relu_dot3_q(const SplitSlot& S, int col, con
     tmem_ld16_nowait(S.d + (uint32_t)(col + 16 * c), r);
     tc::tmem_wait_ld();
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const float x = __uint_as_float(r[i]);
-      bits |= (x > 0.0f ? 1u : 0u) << (16 * c + i);
-      const float h = fmaxf(x, 0.0f);
+    for (int i = 0; i < 16; i += 4) {
       const int k = col + 16 * c + i;
-      p[0] = fmaf(w5[k], h, p[0]);
-      p[1] = fmaf(w5[128 + k], h, p[1]);
-      p[2] = fmaf(w5[256 + k], h, p[2]);
-      if (save) reinterpret_cast<__half*>(save)[(int64_t)k * ld] = __float2half_rn(h);
+      const float4 w0 = *reinterpret_cast<const float4*>(w5 + k), w1 = *reinterpret_cast<const float4*>(w5 + 128 + k),
+                   w2 = *reinterpret_cast<const float4*>(w5 + 256 + k);
+      const float a0[4] = {w0.x, w0.y, w0.z, w0.w}, a1[4] = {w1.x, w1.y, w1.z, w1.w}, a2[4] = {w2.x, w2.y, w2.z, w2.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float x = __uint_as_float(r[i + j]);
+        if constexpr (kTrain) bits |= (x > 0.0f ? 1u : 0u) << (16 * c + i + j);
+        const float h = fmaxf(x, 0.0f);
+        p[0] = fmaf(a0[j], h, p[0]);
+        p[1] = fmaf(a1[j], h, p[1]);
+        p[2] = fmaf(a2[j], h, p[2]);
+        if (kTrain && save) reinterpret_cast<__half*>(save)[(int64_t)(k + j) * ld] = __float2half_rn(h);
+      }
     }
   }
   return bits;
@@ -849,8 +783,8 @@ __global__ void __launch_bounds__(kPrecDeformSlots* kPrecDeformThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t mbar[kPrecDeformSlots];
   __shared__ uint32_t tmem_base;
-  __shared__ float s_bias[128];
-  __shared__ float s_w5[3 * 128];                        // W5 rows 0..2 in fp32 (hi + lo)
+  __shared__ __align__(16) float s_bias[128];
+  __shared__ __align__(16) float s_w5[3 * 128];                        // W5 rows 0..2 in fp32 (hi + lo)
   __shared__ float s_part[kPrecDeformSlots][2][128][3];  // layer-5 partials exchanged between column quarters
   const int tid = threadIdx.x, warp = tid / 32;
   if (tid < 128) s_bias[tid] = bias1[tid];
@@ -894,7 +828,6 @@ __global__ void __launch_bounds__(kPrecDeformSlots* kPrecDeformThreads, 1)
   S.alo = S.alo0 + lane_q;
   const uint8_t* lo = smem + kDeformW;
   constexpr int o2 = 128 * 32 * 2, o3 = o2 + 128 * 128 * 2, o4 = o3 + 128 * 128 * 2;
-  const uint8_t* wo[4] = {smem, smem + o2, smem + o3, smem + o4};
   const int64_t n = min((int64_t)*count, capacity);
   const int64_t n_tiles = (n + 127) / 128;
   const int64_t L = 128 * capacity;
@@ -925,21 +858,27 @@ __global__ void __launch_bounds__(kPrecDeformSlots* kPrecDeformThreads, 1)
       }
     }
     // training saves: h feature-major (512, capacity), ReLU bits [layer][32-column word] per sample
+    // the sample's position, needed at the end of the tile: loaded now, under the layers
+    const float4 xu_s = (cq == 0 && live) ? xu[s] : make_float4(0.f, 0.f, 0.f, 0.f);
     __half* sv = (kSave && s < capacity) ? save_h + s : nullptr;
     uint32_t* mk = (kSave && live) ? save_mask + s * 16 + cq : nullptr;
 #pragma unroll 1
     for (int l = 0; l < 3; ++l) {
-      split_layer(S, wo[l], lo + (int)(wo[l] - smem), l == 0 ? 32 : 128, 128);
-      const uint32_t b = split_relu_q(S, 32 * cq, l == 0 ? s_bias : nullptr, sv ? sv + l * L : nullptr, capacity);
+      if (l == 0)
+        split_layer<32>(S, smem, lo, 128);
+      else
+        split_layer<128>(S, smem + o2 + (l - 1) * (o3 - o2), lo + o2 + (l - 1) * (o3 - o2), 128);
+      const uint32_t b = split_relu_q<kSave>(S, 32 * cq, l == 0 ? s_bias : nullptr, sv ? sv + l * L : nullptr, capacity);
       if (mk) mk[4 * l] = b;
     }
-    split_layer(S, wo[3], lo + o4, 128, 128);
+    split_layer<128>(S, smem + o4, lo + o4, 128);
     float part[3];
     {
-      const uint32_t b = relu_dot3_q(S, 32 * cq, s_w5, part, sv ? sv + 3 * L : nullptr, capacity);
+      const uint32_t b = relu_dot3_q<kSave>(S, 32 * cq, s_w5, part, sv ? sv + 3 * L : nullptr, capacity);
       if (mk) mk[12] = b;
     }
-    // the four quarters' partials summed as (p0 + p2) + (p1 + p3), in two exchanges
+    // the four quarters' partials summed as (p0 + p2) + (p1 + p3), in two exchanges: the
+    // second goes through quarter 1's own first-exchange entry (read by the same thread)
     if (cq >= 2) {
 #pragma unroll
       for (int j = 0; j < 3; ++j) s_part[S.slot][cq - 2][S.r][j] = part[j];
@@ -949,19 +888,18 @@ __global__ void __launch_bounds__(kPrecDeformSlots* kPrecDeformThreads, 1)
 #pragma unroll
       for (int j = 0; j < 3; ++j) part[j] += s_part[S.slot][cq][S.r][j];
     }
-    tc::named_sync(1 + S.slot, S.nthreads);
     if (cq == 1) {
 #pragma unroll
-      for (int j = 0; j < 3; ++j) s_part[S.slot][0][S.r][j] = part[j];
+      for (int j = 0; j < 3; ++j) s_part[S.slot][1][S.r][j] = part[j];
     }
     tc::named_sync(1 + S.slot, S.nthreads);
     if (cq == 0) {
       float v[3];
 #pragma unroll
-      for (int j = 0; j < 3; ++j) v[j] = part[j] + s_part[S.slot][0][S.r][j];
+      for (int j = 0; j < 3; ++j) v[j] = part[j] + s_part[S.slot][1][S.r][j];
       if (kSave && live) save_o[s] = make_float4(v[0], v[1], v[2], 0.0f);
       if (live) {
-        float4 p = xu[s];
+        float4 p = xu_s;
         if (p.w > 0.0f) {
           p.x = f_add(p.x, f_mul(delta_scale * tanhf(v[0]), inv_side));
           p.y = f_add(p.y, f_mul(delta_scale * tanhf(v[1]), inv_side));
@@ -1055,10 +993,10 @@ __global__ void __launch_bounds__(kColorPrecSlots* kSlotThreads, 1)
       ddy = dirs[3 * ray + 1];
       ddz = dirs[3 * ray + 2];
     }
-    split_layer(S, smem + g1, lo + g1, 32, 64);
-    split_relu32(S, 0, nullptr);
-    split_relu32(S, 32, nullptr);
-    split_layer(S, smem + g2, lo + g2, 64, 16);
+    split_layer<32>(S, smem + g1, lo + g1, 64);
+    split_relu32(S, 0);
+    split_relu32(S, 32);
+    split_layer<64>(S, smem + g2, lo + g2, 16);
     float gv[16];
     tc::tmem_ld16(S.d, gv);
     const float sigma = valid ? expf(gv[0]) : 0.0f;
@@ -1070,10 +1008,10 @@ __global__ void __launch_bounds__(kColorPrecSlots* kSlotThreads, 1)
       cin[31] = 0.0f;
       split_store<8>(S, reinterpret_cast<const float4*>(cin), 0);
     }
-    split_layer(S, smem + c1, lo + c1, 32, 64);
-    split_relu32(S, 0, nullptr);
-    split_relu32(S, 32, nullptr);
-    split_layer(S, smem + c2, lo + c2, 64, 64);
+    split_layer<32>(S, smem + c1, lo + c1, 64);
+    split_relu32(S, 0);
+    split_relu32(S, 32);
+    split_layer<64>(S, smem + c2, lo + c2, 64);
     // the last layer (64 -> 3) in fp32 on the CUDA cores: an N = 16 MMA chain runs at
     // 1/8 of the tensor rate (tools/mma_bench.cu), as long as a full-width layer
     float cv[3] = {0.f, 0.f, 0.f};

@@ -83,10 +83,9 @@ __global__ void __launch_bounds__(kSlots* kSlotThreads, 1)
       tc::fence_async_smem();
       tc::fence_before();
       tc::named_sync(1 + slot, kSlotThreads);
-      if (r == 0) {
+      if (r < 32) {  // the slot's first warp issues
         tc::fence_after();
-        tc::issue_layer(tmem_slot, abuf, w_s + D.w_off[l], D.k[l], D.n[l]);
-        tc::mma_commit(&mbar[slot]);
+        tc::layer_ss_warp(tmem_slot, abuf, w_s + D.w_off[l], D.k[l], D.n[l], &mbar[slot]);
       }
       tc::bar_wait(&mbar[slot], phase);
       phase ^= 1u;

@@ -136,24 +136,44 @@ __device__ __forceinline__ void mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uin
       "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
-__device__ __forceinline__ void issue_layer_ts(uint32_t tmem_d, uint32_t tmem_a, const uint8_t* b_buf, int K, int N,
-                                               bool accumulate = false) {
-  const uint32_t b0 = smem_u32(b_buf);
-  const uint32_t idesc = idesc_f16(128, N);
-  for (int ks = 0; ks < K / 16; ++ks)
-    mma_f16_ts(tmem_d, tmem_a + (uint32_t)(ks * 8), sdesc(b0 + ks * 256, 128, (uint32_t)K * 16), idesc,
-               (accumulate || ks > 0) ? 1u : 0u);
-}
-
 // Split-fp16 layer ("fp32" precision mode): with A = Ah + Al and B = Bh + Bl
-// (hi = fp16(x), lo = fp16(x - hi)), D = Ah.Bh + Ah.Bl + Al.Bh accumulated in fp32
-// TMEM — three kind::f16 MMA chains, ~22 significant bits per operand (the
-// dropped Al.Bl term is 2^-22 relative). A halves in TMEM (TS form), B halves in smem.
-__device__ __forceinline__ void issue_layer_ts_split(uint32_t tmem_d, uint32_t a_hi, uint32_t a_lo,
-                                                     const uint8_t* b_hi, const uint8_t* b_lo, int K, int N) {
-  issue_layer_ts(tmem_d, a_hi, b_hi, K, N, false);
-  issue_layer_ts(tmem_d, a_hi, b_lo, K, N, true);
-  issue_layer_ts(tmem_d, a_lo, b_hi, K, N, true);
+// (hi/lo fp16 halves), D = Ah.Bh + Ah.Bl + Al.Bh accumulated in fp32 TMEM — three
+// kind::f16 MMA chains, ~22 significant bits per operand (the dropped Al.Bl term is
+// 2^-22 relative). A halves in TMEM (TS form), B halves in smem. Issued by a whole
+// (converged) warp from one elected lane, the three chains and the commit in one asm
+// block: the operands stay in uniform registers and the MMAs go out back to back.
+// Issued from one divergent thread, each MMA cost ~14 instructions of convergence
+// loops and R2UR broadcasts, and the issue stream stalled behind the other slot's
+// epilogue warps (DeformNet fp32 mode 118 -> 96 us).
+#define CF_MMA_STEP(ACC)                                              \
+  "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ta], tb, %5, " ACC ";\n\t" \
+  "add.u32 ta, ta, 8;\n\tadd.s64 tb, tb, 16;\n\t"
+#define CF_CHAIN2(ACC) CF_MMA_STEP(ACC) CF_MMA_STEP("pt")
+#define CF_CHAIN4(ACC) CF_CHAIN2(ACC) CF_CHAIN2("pt")
+#define CF_CHAIN8(ACC) CF_CHAIN4(ACC) CF_CHAIN4("pt")
+#define CF_SPLIT_ASM(CHAIN)                                                                          \
+  "{\n\t.reg .pred e, pf, pt;\n\t.reg .b32 ta;\n\t.reg .b64 tb;\n\t"                              \
+  "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 pf, 0, 0;\n\tsetp.eq.b32 pt, 0, 0;\n\t"                 \
+  "mov.b32 ta, %1;\n\tmov.b64 tb, %3;\n\t" CHAIN("pf")                                             \
+  "mov.b32 ta, %1;\n\tmov.b64 tb, %4;\n\t" CHAIN("pt")                                             \
+  "mov.b32 ta, %2;\n\tmov.b64 tb, %3;\n\t" CHAIN("pt")                                             \
+  "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n\t}\n"
+template <int K>
+__device__ __forceinline__ void issue_split_warp(uint32_t tmem_d, uint32_t a_hi, uint32_t a_lo, const uint8_t* b_hi,
+                                                 const uint8_t* b_lo, int N, uint64_t* bar) {
+  const uint64_t dh = sdesc(smem_u32(b_hi), 128, (uint32_t)K * 16), dl = sdesc(smem_u32(b_lo), 128, (uint32_t)K * 16);
+  const uint32_t idesc = idesc_f16(128, N), b = smem_u32(bar);
+  if constexpr (K == 32)
+    asm volatile(CF_SPLIT_ASM(CF_CHAIN2)::"r"(tmem_d), "r"(a_hi), "r"(a_lo), "l"(dh), "l"(dl), "r"(idesc), "r"(b)
+                 : "memory");
+  else if constexpr (K == 64)
+    asm volatile(CF_SPLIT_ASM(CF_CHAIN4)::"r"(tmem_d), "r"(a_hi), "r"(a_lo), "l"(dh), "l"(dl), "r"(idesc), "r"(b)
+                 : "memory");
+  else {
+    static_assert(K == 128, "K = 32, 64 or 128");
+    asm volatile(CF_SPLIT_ASM(CF_CHAIN8)::"r"(tmem_d), "r"(a_hi), "r"(a_lo), "l"(dh), "l"(dl), "r"(idesc), "r"(b)
+                 : "memory");
+  }
 }
 
 // (a, b) -> packed fp16x2 hi = fp16(x) and lo = fp16(x - hi) (low halves = a)
@@ -163,6 +183,19 @@ __device__ __forceinline__ void split_f16x2(float a, float b, uint32_t& hi, uint
   const __half2 l = __floats2half2_rn(a - hf.x, b - hf.y);
   hi = *reinterpret_cast<const uint32_t*>(&h);
   lo = *reinterpret_cast<const uint32_t*>(&l);
+}
+
+// ReLU fused into the split, 5 instructions per pair: hi = fp16x2 of relu(a, b) rounded
+// toward zero (so x - hi >= 0 for x > 0), lo = fp16x2 of relu(x - hi) with x - hi from
+// the mixed-precision f32 += f16 add (FHADD) on the negated hi halves; for x <= 0 both
+// halves are 0. hi + lo carries relu(x) to ~2^-21 relative (lo < one fp16 ulp of hi).
+__device__ __forceinline__ void split_relu_rz(float a, float b, uint32_t& hi, uint32_t& lo) {
+  asm("cvt.rz.relu.f16x2.f32 %0, %1, %2;" : "=r"(hi) : "f"(b), "f"(a));
+  const uint32_t nh = hi ^ 0x80008000u;
+  float la, lb;
+  asm("add.f32.f16 %0, %1, %2;" : "=f"(la) : "h"((unsigned short)(nh & 0xffffu)), "f"(a));
+  asm("add.f32.f16 %0, %1, %2;" : "=f"(lb) : "h"((unsigned short)(nh >> 16)), "f"(b));
+  asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(lb), "f"(la));
 }
 
 // 32 fp32 columns without the wait (issue several, then tmem_wait_ld once)
@@ -224,16 +257,51 @@ __device__ __forceinline__ void st_row8(uint8_t* buf, int r, int k0, int K, cons
   *reinterpret_cast<uint4*>(buf + core_offset(r, k0, K)) = *reinterpret_cast<uint4*>(h);
 }
 
-// Issue D[128 x N] (+)= A[128 x K] * B[N x K]^T from canonical smem buffers.
-__device__ __forceinline__ void issue_layer(uint32_t tmem_d, const uint8_t* a_buf, const uint8_t* b_buf, int K,
-                                            int N) {
-  const uint32_t a0 = smem_u32(a_buf), b0 = smem_u32(b_buf);
+// Whole-warp issue: the calling warp is converged, one elected lane issues. The
+// operands stay warp-uniform (uniform registers, no per-MMA convergence loop), so the
+// issue stream is a few instructions per MMA even while other warps of the CTA run
+// their epilogues. Commit from the same elected lane (tcgen05.commit tracks the MMAs
+// of the executing thread).
+__device__ __forceinline__ void mma_ts_elect(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_ss_elect(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(smem_u32(bar))
+      : "memory");
+}
+// a layer (TS: A from TMEM / SS: A from a canonical smem buffer) + commit, by one warp
+__device__ __forceinline__ void layer_ts_warp(uint32_t tmem_d, uint32_t tmem_a, const uint8_t* b_buf, int K, int N,
+                                              uint64_t* bar) {
+  const uint64_t b0 = sdesc(smem_u32(b_buf), 128, (uint32_t)K * 16);
   const uint32_t idesc = idesc_f16(128, N);
-  for (int ks = 0; ks < K / 16; ++ks) {
-    const uint64_t ad = sdesc(a0 + ks * 256, 128, (uint32_t)K * 16);
-    const uint64_t bd = sdesc(b0 + ks * 256, 128, (uint32_t)K * 16);
-    mma_f16(tmem_d, ad, bd, idesc, ks > 0 ? 1u : 0u);
-  }
+  for (int ks = 0; ks < K / 16; ++ks)
+    mma_ts_elect(tmem_d, tmem_a + (uint32_t)(ks * 8), b0 + (uint64_t)(ks * 16), idesc, ks > 0 ? 1u : 0u);
+  commit_elect(bar);
+}
+__device__ __forceinline__ void layer_ss_warp(uint32_t tmem_d, const uint8_t* a_buf, const uint8_t* b_buf, int K,
+                                              int N, uint64_t* bar) {
+  const uint64_t a0 = sdesc(smem_u32(a_buf), 128, (uint32_t)K * 16), b0 = sdesc(smem_u32(b_buf), 128, (uint32_t)K * 16);
+  const uint32_t idesc = idesc_f16(128, N);
+  for (int ks = 0; ks < K / 16; ++ks)
+    mma_ss_elect(tmem_d, a0 + (uint64_t)(ks * 16), b0 + (uint64_t)(ks * 16), idesc, ks > 0 ? 1u : 0u);
+  commit_elect(bar);
 }
 
 }  // namespace tc
