@@ -35,6 +35,21 @@ __device__ __forceinline__ bool occ_test(const cf_occ_grid& g, const uint32_t* _
   return (__ldg(bits + (flat >> 5)) >> (flat & 31)) & 1u;
 }
 
+// occ_test split in two for batched lookups: the flat cell index (-1 outside the
+// grid), branch-free, with the reciprocal hoisted by the caller (same arithmetic)
+__device__ __forceinline__ int64_t occ_flat(const cf_occ_grid& g, double inv, d3 p) {
+  const double q[3] = {p.x, p.y, p.z};
+  bool ok = true;
+  int64_t c[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double f = floor(x_mul(x_sub(q[a], g.min[a]), inv));
+    ok = ok && (f >= 0.0) && f < (double)g.res;
+    c[a] = ok ? (int64_t)f : 0;
+  }
+  return ok ? (c[0] * g.res + c[1]) * g.res + c[2] : -1;
+}
+
 __device__ __forceinline__ d3 cell_center(const cf_occ_grid& g, int64_t flat) {
   const int64_t r = g.res;
   const int64_t x = flat / (r * r), y = (flat / r) % r, z = flat % r;
@@ -451,17 +466,33 @@ __device__ __forceinline__ int warp_excl_scan(int v, int& total) {
   return x - v;
 }
 
-// occupancy-skipped sample compaction, one thread per ray, up to two fields
-// occupancy masks of samples i0..i1 (< 128), word loop unrolled so the masks
-// stay in registers (a runtime word index would put them in local memory)
-template <class Test>
-__device__ __forceinline__ void scan_samples(int i0, int i1, Test test, uint32_t (&m)[4]) {
+// occupancy-skipped sample compaction, one thread per ray, up to two fields:
+// occupancy masks of samples i0..i1 (< 128). Samples go in batches of 4 — cell
+// indices first, then the 4 bit-word loads in flight together (one dependent load
+// per sample was the march's latency chain) — and each hit is merged into the mask
+// word by selects, so the masks stay in registers without unrolling a loop per word
+// (a runtime word index would put them in local memory; four unrolled word loops
+// blew the instruction cache).
+template <class Flat>
+__device__ __forceinline__ void scan_samples(int i0, int i1, Flat flat_of, const uint32_t* __restrict__ bits,
+                                             uint32_t (&m)[4]) {
+  m[0] = m[1] = m[2] = m[3] = 0u;
+  for (int i = i0; i <= i1; i += 4) {
+    int64_t f[4];
 #pragma unroll
-  for (int w = 0; w < 4; ++w) {
-    uint32_t mw = 0;
-    const int lo = max(i0, 32 * w), hi = min(i1, 32 * w + 31);
-    for (int i = lo; i <= hi; ++i) mw |= (uint32_t)test(i) << (i & 31);
-    m[w] = mw;
+    for (int j = 0; j < 4; ++j) f[j] = i + j <= i1 ? flat_of(i + j) : -1;
+    uint32_t v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v[j] = f[j] >= 0 ? __ldg(bits + (f[j] >> 5)) : 0u;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t b = (f[j] >= 0 ? (v[j] >> (f[j] & 31)) & 1u : 0u) << ((i + j) & 31);
+      const int w = (i + j) >> 5;
+      m[0] |= w == 0 ? b : 0u;
+      m[1] |= w == 1 ? b : 0u;
+      m[2] |= w == 2 ? b : 0u;
+      m[3] |= w == 3 ? b : 0u;
+    }
   }
 }
 
@@ -514,7 +545,9 @@ __global__ void __launch_bounds__(128) march_kernel(cf_march_desc M, cf_camera c
     if (live && hbits && !hempty) {
       int i0, i1;
       sample_range(M, o, d, hlo, hhi, i0, i1);
-      scan_samples(i0, i1, [&](int i) { return occ_test(M.human_grid, hbits, sample_p(o, d, sample_t(M, i))); }, hm);
+      const double inv = 1.0 / M.human_grid.cell;
+      scan_samples(
+          i0, i1, [&](int i) { return occ_flat(M.human_grid, inv, sample_p(o, d, sample_t(M, i))); }, hbits, hm);
       hc = __popc(hm[0]) + __popc(hm[1]) + __popc(hm[2]) + __popc(hm[3]);
     }
     if (live && obits) {
@@ -524,12 +557,11 @@ __global__ void __launch_bounds__(128) march_kernel(cf_march_desc M, cf_camera c
                   d.x * obj_R[2] + d.y * obj_R[5] + d.z * obj_R[8]};
       int i0, i1;
       sample_range(M, oo, od, olo, ohi, i0, i1);
+      const double inv = 1.0 / M.object_grid.cell;
       scan_samples(
           i0, i1,
-          [&](int i) {
-            return occ_test(M.object_grid, obits, to_object(obj_R, obj_t, sample_p(o, d, sample_t(M, i))));
-          },
-          om);
+          [&](int i) { return occ_flat(M.object_grid, inv, to_object(obj_R, obj_t, sample_p(o, d, sample_t(M, i)))); },
+          obits, om);
       oc = __popc(om[0]) + __popc(om[1]) + __popc(om[2]) + __popc(om[3]);
     }
 #pragma unroll
