@@ -164,9 +164,11 @@ int cf_lbs_theta_jacobian(const double* A_pm, int n_theta, int J, const double* 
 int cf_lbs_vertex_transforms(const double* A, int J, const double* vert_weights, int64_t n_verts, double* T_out,
                              double* Tinv_out, void* stream);
 /* per-frame skin setup in one kernel: cf_lbs_vertex_transforms (T, Tinv) plus
- * the posed vertices of cf_lbs_forward with the same weights (J <= 64) */
+ * the posed vertices of cf_lbs_forward with the same weights (J <= 64); posed_box
+ * (6 x uint64, may be NULL) receives the posed vertices' bounding box in the
+ * order-preserving key form cf_human_lbs_fallback reads */
 int cf_lbs_setup(const double* A, int J, const double* verts, const double* vert_weights, int64_t n_verts,
-                 double* T_out, double* Tinv_out, double* posed_out, void* stream);
+                 double* T_out, double* Tinv_out, double* posed_out, uint64_t* posed_box, void* stream);
 /* backward LBS (builder-defined): nearest posed skin vertex
  * v* (exact 1-NN, ties by index; vert_buckets built over verts_posed, or NULL
  * for an exhaustive scan) -> p_c = Tinv_{v*} [p, 1];
@@ -322,6 +324,16 @@ int cf_rays_march(const cf_camera* cam, const cf_march_desc* M, double* dirs, co
 /* human samples -> canonical unit cube (xu: float4 x,y,z,flag; flag 1 = ED, 2 = LBS, 0 = invalid) */
 int cf_human_canon(const cf_march_desc* M, const double* dirs, const cf_march_out* F, const cf_human_warp* W,
                    const cf_buckets_t* anchor_buckets, const cf_buckets_t* vert_buckets, float* xu, void* stream);
+/* the backward-LBS fallback of cf_human_canon as a separate pass: with vert_buckets = NULL
+ * cf_human_canon leaves the samples no ED warp reaches at flag 0; this pass gives them
+ * their LBS canonical position (flag 2) — output identical to the fused call. It needs
+ * no vertex buckets: a warp scans the posed vertices (verts_posed, n_verts) for each
+ * flag-0 sample within lbs_max_dist of their box (posed_box of cf_lbs_setup); exact
+ * 1-NN with ties by index, as the bucket search. The render runs the canonicalisation
+ * as soon as the march and the ED chain are done and this pass after the LBS setup. */
+int cf_human_lbs_fallback(const cf_march_desc* M, const double* dirs, const cf_march_out* F, const cf_human_warp* W,
+                          const double* verts_posed, int64_t n_verts, const uint64_t* posed_box, float* xu,
+                          void* stream);
 int cf_object_canon(const cf_march_desc* M, const double* dirs, const cf_march_out* F, float* xu, void* stream);
 /* front-to-back compositing of field outputs (float4 sigma,r,g,b per sample) */
 int cf_composite(const cf_march_desc* M, const cf_march_out* F, const float* field, float t_term, float* rgb,

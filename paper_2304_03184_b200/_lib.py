@@ -212,7 +212,7 @@ _SIGS = {
     "cf_knnfield_query": [_p, _p, _p, _p, _i32, _i32, _p, _f64, _f64, _p, _i64, _p, _p, _p, _p, _p],
     "cf_lbs_forward": [_p, _i32, _p, _p, _i64, _p, _p],
     "cf_lbs_vertex_transforms": [_p, _i32, _p, _i64, _p, _p, _p],
-    "cf_lbs_setup": [_p, _i32, _p, _p, _i64, _p, _p, _p, _p],
+    "cf_lbs_setup": [_p, _i32, _p, _p, _i64, _p, _p, _p, _p, _p],
     "cf_lbs_backward": [_p, _p, _p, _i64, _f64, _p, _i64, _p, _p, _p, _p],
     "cf_hashgrid_init": [ctypes.POINTER(HashGridDesc), _i32, _i32, _i32, _i32, _i32],
     "cf_hashgrid_encode": [ctypes.POINTER(HashGridDesc), _p, _p, _i64, _p, _p],
@@ -230,6 +230,7 @@ _SIGS = {
     "cf_occ_cache": [_p, _P(OccGrid), _p, _i32, _f64, _i64, _p, _p, _p, _p, _p],
     "cf_occ_splat_cached": [_p, _p, _p, _p, _i64, _i32, _p, _P(OccGrid), _P(OccGrid), _p, _p, _p, _p],
     "cf_human_canon": [_P(MarchDesc), _p, _P(MarchOut), _P(HumanWarp), _p, _p, _p, _p],
+    "cf_human_lbs_fallback": [_P(MarchDesc), _p, _P(MarchOut), _P(HumanWarp), _p, _i64, _p, _p, _p],
     "cf_object_canon": [_P(MarchDesc), _p, _P(MarchOut), _p, _p],
     "cf_composite": [_P(MarchDesc), _P(MarchOut), _p, ctypes.c_float, _p, _p, _p, _p],
     "cf_composite_layers": [_i64, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p],

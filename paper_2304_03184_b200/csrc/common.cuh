@@ -127,6 +127,16 @@ __device__ __forceinline__ double sqdist(d3 a, d3 b) {
   return x_add(x_add(x_mul(dx, dx), x_mul(dy, dy)), x_mul(dz, dz));
 }
 
+// Order-preserving uint64 keys of doubles (x < y <=> key(x) < key(y); no NaNs): a
+// float64 bounding box by integer atomicMin / atomicMax
+__device__ __forceinline__ unsigned long long dkey(double x) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(x);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double dkey_inv(unsigned long long k) {
+  return __longlong_as_double((long long)((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k));
+}
+
 namespace cf {
 // Several fills in ONE launch, launched with PDL (waits for the stream predecessor
 // before writing): the frame's counter / bit-grid resets between its kernels.

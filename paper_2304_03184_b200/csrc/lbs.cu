@@ -75,7 +75,8 @@ __global__ void __launch_bounds__(128) lbs_setup_kernel(const double* __restrict
                                                         const double* __restrict__ verts,
                                                         const double* __restrict__ W, int64_t V,
                                                         double* __restrict__ T, double* __restrict__ Tinv,
-                                                        double* __restrict__ posed) {
+                                                        double* __restrict__ posed,
+                                                        unsigned long long* __restrict__ box) {
   __shared__ double sA[kMaxBones * 16];
   pdl_wait();
   for (int i = threadIdx.x; i < J * 16; i += blockDim.x) sA[i] = A[i];
@@ -104,6 +105,24 @@ __global__ void __launch_bounds__(128) lbs_setup_kernel(const double* __restrict
     posed[3 * v] = o[0];
     posed[3 * v + 1] = o[1];
     posed[3 * v + 2] = o[2];
+    if (box) {  // the posed vertices' bounding box (keys, cf_lbs_setup); lanes with no vertex are inert
+      const unsigned act = __activemask();
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        unsigned long long lo = dkey(o[a]), hi = lo;
+        for (int off = 16; off > 0; off >>= 1) {
+          const unsigned long long l2 = __shfl_xor_sync(act, lo, off), h2 = __shfl_xor_sync(act, hi, off);
+          if ((act >> ((threadIdx.x ^ off) & 31)) & 1u) {
+            lo = l2 < lo ? l2 : lo;
+            hi = h2 > hi ? h2 : hi;
+          }
+        }
+        if ((threadIdx.x & 31) == __ffs(act) - 1) {
+          atomicMin(box + a, lo);
+          atomicMax(box + 3 + a, hi);
+        }
+      }
+    }
     const double a = m[0], b = m[1], c = m[2], d = m[4], e = m[5], f = m[6], g = m[8], h = m[9], k = m[10];
     const double A00 = e * k - f * h, A01 = c * h - b * k, A02 = b * f - c * e;
     const double A10 = f * g - d * k, A11 = a * k - c * g, A12 = c * d - a * f;
@@ -216,12 +235,18 @@ int cf_lbs_vertex_transforms(const double* A, int J, const double* vert_weights,
 }
 
 int cf_lbs_setup(const double* A, int J, const double* verts, const double* vert_weights, int64_t n_verts,
-                 double* T_out, double* Tinv_out, double* posed_out, void* stream) {
+                 double* T_out, double* Tinv_out, double* posed_out, uint64_t* posed_box, void* stream) {
   if (J < 1 || J > kMaxBones || n_verts < 1 || !A || !verts || !vert_weights || !Tinv_out || !posed_out)
     return cf::fail(CF_E_BAD_ARG, "cf_lbs_setup: bad args");
+  cudaStream_t st = cf::as_stream(stream);
+  unsigned long long* box = reinterpret_cast<unsigned long long*>(posed_box);
+  if (box) {  // lo keys to all-ones, hi keys to zero
+    uint32_t* w = reinterpret_cast<uint32_t*>(box);
+    cf::fill_list(st, {{w, 0xffffffffu, 6}, {w + 6, 0u, 6}});
+  }
   // 64 threads per CTA: a few thousand vertices still spread over ~all SMs
-  cf::launch_pdl(lbs_setup_kernel, cf::grid_for(n_verts, 64, 4), 64, 0, cf::as_stream(stream), A, J, verts,
-                 vert_weights, n_verts, T_out, Tinv_out, posed_out);
+  cf::launch_pdl(lbs_setup_kernel, cf::grid_for(n_verts, 64, 4), 64, 0, st, A, J, verts, vert_weights, n_verts, T_out,
+                 Tinv_out, posed_out, box);
   return cf::check_launch("cf_lbs_setup");
 }
 

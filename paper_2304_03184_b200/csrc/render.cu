@@ -599,6 +599,12 @@ __global__ void __launch_bounds__(128) march_kernel(cf_march_desc M, cf_camera c
   pdl_trigger();
 }
 
+// p_c = Tinv [p, 1] (Tinv: (3,4) row-major)
+__device__ __forceinline__ d3 lbs_apply(const double* __restrict__ T, d3 p) {
+  return d3{T[0] * p.x + T[1] * p.y + T[2] * p.z + T[3], T[4] * p.x + T[5] * p.y + T[6] * p.z + T[7],
+            T[8] * p.x + T[9] * p.y + T[10] * p.z + T[11]};
+}
+
 // backward-LBS fallback of a sample outside the ED support: its nearest posed
 // skin vertex (exact 1-NN on the vertex buckets) within lbs_max_dist -> that
 // vertex's inverse blended transform. No vertex can be that close when the
@@ -616,9 +622,7 @@ __device__ __forceinline__ bool lbs_fallback(const BucketParams& sL, const int* 
   top.init(1);
   if (d2b <= W.lbs_max_d2 * (1.0 + 1e-9)) bucket_knn<1>(sL, lcs, ls, p, top, W.lbs_max_d2);
   if (!(top.d[0] <= W.lbs_max_d2)) return false;
-  const double* T = W.vert_Tinv + 12 * (int64_t)top.i[0];
-  pt = d3{T[0] * p.x + T[1] * p.y + T[2] * p.z + T[3], T[4] * p.x + T[5] * p.y + T[6] * p.z + T[7],
-          T[8] * p.x + T[9] * p.y + T[10] * p.z + T[11]};
+  pt = lbs_apply(W.vert_Tinv + 12 * (int64_t)top.i[0], p);
   return true;
 }
 
@@ -747,6 +751,79 @@ __global__ void __launch_bounds__(128, CF_CANON_MINB) human_canon_kernel(cf_marc
     if (atomicAdd(ticket + 1, 1) == (int)(gridDim.x * (blockDim.x >> 5)) - 1) {
       ticket[0] = 0;
       ticket[1] = 0;
+    }
+  }
+  pdl_trigger();
+}
+
+// The backward-LBS fallback as its own pass, for the render: the canonicalisation runs
+// without it (samples the ED warp does not reach get flag 0) as soon as the march and
+// the ED chain are done, and this pass completes those samples after the per-frame LBS
+// setup (posed vertices, inverse transforms and their box, on the side stream) — that
+// chain no longer sits between the march and the canonicalisation, and the render
+// needs no vertex buckets. Per warp: the samples of flag 0 within lbs_max_dist of the
+// posed vertices' box (lbs_fallback's rejection) are taken one at a time, the 32 lanes
+// scan the vertices and reduce (d^2, index) — the exact 1-NN with ties by index that
+// bucket_knn<1> finds — and the owner lane applies that vertex's inverse transform
+// (lbs_apply, as lbs_fallback): bit-identical to the fused call.
+__global__ void __launch_bounds__(128) human_lbs_fallback_kernel(cf_march_desc M, const double* __restrict__ dirs,
+                                                                 const uint32_t* __restrict__ records,
+                                                                 const int* __restrict__ count, int64_t capacity,
+                                                                 cf_human_warp W, const double* __restrict__ posed,
+                                                                 int64_t V, const unsigned long long* __restrict__ box,
+                                                                 float4* __restrict__ xu) {
+  pdl_wait();
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const d3 o = M.frame ? d3{M.frame[0], M.frame[1], M.frame[2]} : d3{M.origin[0], M.origin[1], M.origin[2]};
+  double lo[3], hi[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    lo[a] = dkey_inv(box[a]);
+    hi[a] = dkey_inv(box[3 + a]);
+  }
+  const int64_t n = min((int64_t)count[0], capacity);
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t base = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; base < n;
+       base += warps * 32) {
+    const int64_t s = base + lane;
+    bool need = s < n && xu[s].w == 0.0f;
+    d3 p{0.0, 0.0, 0.0};
+    if (need) {
+      const uint32_t rec = records[s];
+      p = sample_p(o, load_d3(dirs + 3 * (int64_t)(rec >> 8)), rec_t(M, s, rec));
+      const double q[3] = {p.x, p.y, p.z};
+      double d2b = 0.0;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const double e = fmax(fmax(lo[a] - q[a], q[a] - hi[a]), 0.0);
+        d2b += e * e;
+      }
+      need = d2b <= W.lbs_max_d2 * (1.0 + 1e-9);
+    }
+    unsigned todo = __ballot_sync(FULL, need);
+    while (todo) {
+      const int j = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const d3 pj{__shfl_sync(FULL, p.x, j), __shfl_sync(FULL, p.y, j), __shfl_sync(FULL, p.z, j)};
+      double bd = __longlong_as_double(0x7ff0000000000000LL);
+      int bi = 0x7fffffff;
+      for (int64_t v = lane; v < V; v += 32) {
+        const double d = sqdist(pj, load_d3(posed + 3 * v));
+        if (key_less(d, (int)v, bd, bi)) {
+          bd = d;
+          bi = (int)v;
+        }
+      }
+      for (int off = 16; off > 0; off >>= 1) {
+        const double d2 = __shfl_xor_sync(FULL, bd, off);
+        const int i2 = __shfl_xor_sync(FULL, bi, off);
+        if (key_less(d2, i2, bd, bi)) {
+          bd = d2;
+          bi = i2;
+        }
+      }
+      if (lane == j && bd <= W.lbs_max_d2) xu[s] = canon_out(W, lbs_apply(W.vert_Tinv + 12 * (int64_t)bi, p), 2.0f);
     }
   }
   pdl_trigger();
@@ -1302,6 +1379,17 @@ int cf_human_canon(const cf_march_desc* M, const double* dirs, const cf_march_ou
   });
 #undef CF_HC
   return cf::check_launch("cf_human_canon");
+}
+
+int cf_human_lbs_fallback(const cf_march_desc* M, const double* dirs, const cf_march_out* F, const cf_human_warp* W,
+                          const double* verts_posed, int64_t n_verts, const uint64_t* posed_box, float* xu_f,
+                          void* stream) {
+  if (!M || !F || !W || !verts_posed || n_verts < 1 || n_verts >= 0x7fffffff || !posed_box || !W->vert_Tinv || !xu_f)
+    return cf::fail(CF_E_BAD_ARG, "cf_human_lbs_fallback: bad args");
+  cf::launch_pdl(human_lbs_fallback_kernel, cf::grid_for(F->capacity, 128 * 32, 8), 128, 0, cf::as_stream(stream), *M,
+                 dirs, F->records, F->counters, F->capacity, *W, verts_posed, n_verts,
+                 reinterpret_cast<const unsigned long long*>(posed_box), reinterpret_cast<float4*>(xu_f));
+  return cf::check_launch("cf_human_lbs_fallback");
 }
 
 int cf_compact_valid(const cf_march_out* F, const float* xu, const cf_march_out* C, float* xu_c, int* vidx, int* inv,

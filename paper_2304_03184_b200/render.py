@@ -489,9 +489,11 @@ class Renderer:
             self._defer_copy(dst, src)
         self._setup_pending = True
 
-    def _human_setup(self) -> None:
+    def _human_setup(self, lbs_buckets: bool = True) -> None:
         """The frame's human setup kernels: backward-LBS chain on the side stream,
-        deformed nodes + live occupancy splat on the current stream."""
+        deformed nodes + live occupancy splat on the current stream. lbs_buckets=False
+        (the view): no posed-vertex buckets — the view's fallback pass scans the
+        posed vertices; prepare_frame adds the buckets for the fused callers."""
         self._flush_copies()
         s = _lib.stream_ptr()
         h = self.human
@@ -511,7 +513,8 @@ class Renderer:
                           offsets.ctypes.data, len(parents), self._A.data_ptr(), ss)
                 _lib.call("cf_pose_bias", h.nets.d1.data_ptr(), 32 + 3 * len(parents), 32, 128,
                           self._theta.data_ptr(), 3 * len(parents), self.dbias.data_ptr(), ss)
-            h.lbs.set_pose(self._A)
+            h.lbs.set_pose(self._A, buckets=lbs_buckets)
+            self._lbs_buckets_current = lbs_buckets
             self._mark("lbs_setup")
             self._lbs_done.record(side)
         # the ED chain (deformed nodes, their anchor block and candidate grid, or buckets)
@@ -724,6 +727,10 @@ class Renderer:
             # the side-stream LBS and ED chains are done before the caller's next launch
             torch.cuda.current_stream().wait_event(self._lbs_done)
             torch.cuda.current_stream().wait_event(self._ed_done)
+        elif self.human is not None and not getattr(self, "_lbs_buckets_current", True):
+            # the frame's setup ran with a view (no vertex buckets): add them now
+            self.human.lbs.build_buckets()
+            self._lbs_buckets_current = True
         self._setup_pending = False
 
     def render(self, R, t, fx, fy, cx, cy):
@@ -781,7 +788,7 @@ class Renderer:
     def _launch_view(self, setup: bool):
         s = _lib.stream_ptr()
         if setup:
-            self._human_setup()
+            self._human_setup(lbs_buckets=False)
         hb, ob = self.hb, self.ob
         # ray generation fused into the march (directions written for the later stages)
         self.M.n_rays = self.n_rays
@@ -813,11 +820,18 @@ class Renderer:
             object_field()
         if hb:
             h = self.human
+            # the canonicalisation needs the ED chain; the backward-LBS fallback (posed
+            # vertices + buckets from the side stream's LBS chain) runs as its own pass
+            # after it, so the LBS chain overlaps the march and the ED canonicalisation
             if setup:
-                main.wait_event(self._lbs_done)
                 main.wait_event(self._ed_done)
             _lib.call("cf_human_canon", _lib.byref(self.M), self.dirs.data_ptr(), _lib.byref(hb.mo),
-                      _lib.byref(self.hw), self._anchor_buckets.handle, h.lbs.buckets.handle, hb.xu.data_ptr(), s)
+                      _lib.byref(self.hw), self._anchor_buckets.handle, None, hb.xu.data_ptr(), s)
+            if setup:
+                main.wait_event(self._lbs_done)
+            _lib.call("cf_human_lbs_fallback", _lib.byref(self.M), self.dirs.data_ptr(), _lib.byref(hb.mo),
+                      _lib.byref(self.hw), h.lbs.posed.data_ptr(), h.lbs.V, h.lbs.box.data_ptr(),
+                      hb.xu.data_ptr(), s)
             self._mark("human_canon")
             scratch = self._scratch(hb, self.hdesc).data_ptr()
             for stage, name in enumerate(("human_hash_d", "human_deform_mlp", "human_hash_c", "human_color_mlp")):

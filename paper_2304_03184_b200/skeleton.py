@@ -50,14 +50,21 @@ class BackwardLBS:
         self.T = torch.empty((self.V, 12), dtype=torch.float64, device=self.verts.device)
         self.Tinv = torch.empty_like(self.T)
         self.buckets = Buckets(self.V)
+        self.box = torch.empty(6, dtype=torch.int64, device=self.verts.device)  # posed bbox keys (cf_lbs_setup)
 
-    def set_pose(self, A) -> None:
-        """Per-frame setup from bone transforms A (J,4,4): numpy, or a CUDA tensor used in place."""
+    def set_pose(self, A, buckets: bool = True) -> None:
+        """Per-frame setup from bone transforms A (J,4,4): numpy, or a CUDA tensor used in
+        place. buckets=False skips the vertex buckets (the render's fallback pass scans
+        the posed vertices instead); build_buckets() adds them later."""
         self.A = A.contiguous() if is_device(A) else dev(np.asarray(A, dtype=np.float64))
         s = _lib.stream_ptr()
-        # blended vertex transforms + inverses + posed vertices in one kernel
+        # blended vertex transforms + inverses + posed vertices (+ their box) in one kernel
         _lib.call("cf_lbs_setup", self.A.data_ptr(), self.J, self.verts.data_ptr(), self.W.data_ptr(), self.V,
-                  self.T.data_ptr(), self.Tinv.data_ptr(), self.posed.data_ptr(), s)
+                  self.T.data_ptr(), self.Tinv.data_ptr(), self.posed.data_ptr(), self.box.data_ptr(), s)
+        if buckets:
+            self.build_buckets()
+
+    def build_buckets(self) -> None:
         self.buckets.build(self.posed)
 
     def warp(self, pts: torch.Tensor):

@@ -364,3 +364,42 @@ def test_candidate_grid_equals_culled_scan(fid, cmax):
     assert len(r0) > 10000
     assert np.array_equal(r0, r1) and np.array_equal(i0, i1)
     assert np.array_equal(x0.view(np.uint32), x1.view(np.uint32))
+
+
+def test_lbs_fallback_pass_equals_fused(setup):
+    """The render's separate backward-LBS pass (cf_human_lbs_fallback: a warp scan of
+    the posed vertices, no buckets) gives the fused cf_human_canon output (bucket
+    1-NN) bit for bit. The ED radius is shrunk so every sample falls back; points
+    near the posed skin and far away (rejected by the posed box)."""
+    import ctypes
+
+    from paper_2304_03184_b200 import _lib, spec
+    sc, cfg, hf, of, r = setup[:5]
+    r.set_frame(sc.node_dqs(4), sc.theta(4), sc.bone_transforms(4), *sc.object_pose(4))
+    r.prepare_frame()
+    h = r.human
+    rng = np.random.default_rng(7)
+    posed = h.lbs.posed.cpu().numpy()
+    near = posed[rng.integers(0, len(posed), 6000)] + rng.normal(scale=0.08, size=(6000, 3))
+    far = rng.uniform(-4, 4, size=(1000, 3))
+    p = torch.as_tensor(np.concatenate([near, far]), dtype=torch.float64, device="cuda")
+    n = p.shape[0]
+    buf, M, tt = spec._batch(r, p, torch.ones((n, 1), dtype=torch.float64, device="cuda"))
+    for a in range(3):
+        M.origin[a] = 0.0
+    hw = _lib.HumanWarp()
+    ctypes.memmove(ctypes.byref(hw), ctypes.byref(r.hw), ctypes.sizeof(hw))
+    hw.r2 = 1e-12  # no sample within any ED node's support
+    s = _lib.stream_ptr()
+    _lib.call("cf_human_canon", _lib.byref(M), p.data_ptr(), _lib.byref(buf.mo), _lib.byref(hw),
+              r._anchor_buckets.handle, h.lbs.buckets.handle, buf.xu.data_ptr(), s)
+    fused = buf.xu[:n].clone()
+    buf.xu.fill_(123.0)
+    _lib.call("cf_human_canon", _lib.byref(M), p.data_ptr(), _lib.byref(buf.mo), _lib.byref(hw),
+              r._anchor_buckets.handle, None, buf.xu.data_ptr(), s)
+    assert int((buf.xu[:n, 3] != 0).sum()) == 0
+    _lib.call("cf_human_lbs_fallback", _lib.byref(M), p.data_ptr(), _lib.byref(buf.mo), _lib.byref(hw),
+              h.lbs.posed.data_ptr(), h.lbs.V, h.lbs.box.data_ptr(), buf.xu.data_ptr(), s)
+    split = buf.xu[:n]
+    assert int((fused[:, 3] == 2).sum()) > 4000 and int((fused[:, 3] == 0).sum()) >= 1000
+    assert torch.equal(fused, split)
