@@ -1,5 +1,5 @@
 #!/bin/bash
-# round-2 measurement set: bench lines (render, reference arm, train, knn), the render launch list
+# measurement set: bench lines (render, reference arm, train, knn), the render launch list
 # and one ncu --set full capture of the render kernels; outputs in gpurun_out/
 set -x
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/m_smi.txt
