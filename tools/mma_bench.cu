@@ -2,7 +2,7 @@
 // (one CTA per SM, one thread issuing, commit + wait every `chain` MMAs):
 //   SS: A and B from shared memory (UMMA canonical K-major, SWIZZLE_NONE)
 //   TS: A from TMEM, B from shared memory
-// for M = 128 and N = 16 / 64 / 128, K = 16 per instruction. Prints one JSON object:
+// for M = 128 (and M = 64, SS) and N = 16 / 64 / 128, K = 16 per instruction. Prints one JSON object:
 // dense FLOP/s over the whole GPU and per SM per clock.
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I../paper_2304_03184_b200/csrc mma_bench.cu
 #include <cstdio>
@@ -11,7 +11,7 @@
 #include "tc.cuh"
 
 template <bool TS, bool kLoad = false>
-__global__ void __launch_bounds__(128, 1) mma_kernel(int N, int iters, int chain, float* out) {
+__global__ void __launch_bounds__(128, 1) mma_kernel(int N, int iters, int chain, float* out, int M = 128) {
   extern __shared__ __align__(1024) uint8_t smem[];  // A 128 x 128 + B 128 x 128 fp16
   __shared__ uint64_t bar;
   __shared__ uint32_t tmem_base;
@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(128, 1) mma_kernel(int N, int iters, int chain
     tc::fence_after();
   }
   const uint32_t a0 = tc::smem_u32(smem), b0 = a0 + 128 * 128 * 2;
-  const uint32_t idesc = tc::idesc_f16(128, N);
+  const uint32_t idesc = tc::idesc_f16(M, N);
   uint32_t phase = 0;
   if (kLoad && threadIdx.x >= 32) {
     // warps 1-3: TMEM traffic like an epilogue (ld 32 fp32 columns + st 32 columns of
@@ -108,12 +108,13 @@ int main() {
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   printf("{\"gpu\": \"%s\", \"sm_mhz\": %.0f", p.name, clk / 1e3);
-  for (int ts = 0; ts < 3; ++ts)
+  for (int ts = 0; ts < 4; ++ts)
     for (int N : {16, 64, 128})
       for (int chain : {8, 24, 96}) {
         const int iters = 4000 * 24 / chain;
         auto run = [&] {
-          if (ts == 2) mma_kernel<true, true><<<p.multiProcessorCount, 128, smem>>>(N, iters, chain, out);
+          if (ts == 3) mma_kernel<false><<<p.multiProcessorCount, 128, smem>>>(N, iters, chain, out, 64);
+          else if (ts == 2) mma_kernel<true, true><<<p.multiProcessorCount, 128, smem>>>(N, iters, chain, out);
           else if (ts) mma_kernel<true><<<p.multiProcessorCount, 128, smem>>>(N, iters, chain, out);
           else mma_kernel<false><<<p.multiProcessorCount, 128, smem>>>(N, iters, chain, out);
         };
@@ -129,9 +130,9 @@ int main() {
           cudaEventElapsedTime(&ms, e0, e1);
           best = ms < best ? ms : best;
         }
-        const double flop = 2.0 * 128 * N * 16 * (double)chain * iters * p.multiProcessorCount;
+        const double flop = 2.0 * (ts == 3 ? 64 : 128) * N * 16 * (double)chain * iters * p.multiProcessorCount;
         const double tf = flop / (best * 1e-3) / 1e12;
-        const char* nm = ts == 2 ? "ts_tmemload" : (ts ? "ts" : "ss");
+        const char* nm = ts == 3 ? "ss_m64" : ts == 2 ? "ts_tmemload" : (ts ? "ts" : "ss");
         printf(", \"%s_N%d_chain%d_tflops\": %.1f, \"%s_N%d_chain%d_flop_per_clk_sm\": %.0f", nm, N, chain, tf, nm, N,
                chain, tf * 1e12 / (p.multiProcessorCount * clk * 1e3));
       }
