@@ -148,6 +148,25 @@ int cf_knnfield_query(const int32_t* live, const int32_t* neighbor_idx, const do
                       const double* anchors_frame, int s, int res, const double* bbox_min, double voxel_size,
                       double radius, const double* pts, int64_t n_pts, int64_t* nbr_out, double* w_out,
                       double* pc_out, uint8_t* valid_out, void* stream);
+/* Sparse live maps (a frame's map is mostly empty space: 512 MiB dense per frame at
+ * 512^3): bricks of 8^3 voxels. brick_index: B^3 int32 (B = ceil(res / 8), brick
+ * (bi, bj, bk) at (bi*B + bj)*B + bk) = the brick's block in `bricks` (512 int32, voxel
+ * (x, y, z) of the brick at (x*8 + y)*8 + z) or -1 if all its voxels are empty.
+ * cf_knnfield_brick_count: B^3. cf_knnfield_brick_index: brick_index and the number of
+ * set bricks (device int32) from a dense map; cf_knnfield_brick_pack: the set bricks;
+ * cf_knnfield_brick_unpack: back to the dense map. cf_knnfield_query_sparse: the
+ * query of cf_knnfield_query on a sparse map (same results). */
+int cf_knnfield_brick_count(int res, int64_t* n_bricks_total);
+int cf_knnfield_brick_index(const int32_t* live_dense, int res, int32_t* brick_index, int32_t* n_set, void* stream);
+int cf_knnfield_brick_pack(const int32_t* live_dense, int res, const int32_t* brick_index, int32_t* bricks,
+                           void* stream);
+int cf_knnfield_brick_unpack(const int32_t* brick_index, const int32_t* bricks, int res, int32_t* live_dense,
+                             void* stream);
+int cf_knnfield_query_sparse(const int32_t* brick_index, const int32_t* bricks, const int32_t* neighbor_idx,
+                             const double* dqs_frame, const double* anchors_frame, int s, int res,
+                             const double* bbox_min, double voxel_size, double radius, const double* pts,
+                             int64_t n_pts, int64_t* nbr_out, double* w_out, double* pc_out, uint8_t* valid_out,
+                             void* stream);
 
 /* ------------------------------------------------------------------ skeleton */
 

@@ -210,6 +210,11 @@ _SIGS = {
     "cf_knnfield_build": [_p, _i64, _i32, _i32, _p, _f64, _f64, _p, _p],
     "cf_knnfield_update": [_p, _p, _i64, _p, _i32, _i32, _p, _f64, _f64, _p, _p, _p, _p],
     "cf_knnfield_query": [_p, _p, _p, _p, _i32, _i32, _p, _f64, _f64, _p, _i64, _p, _p, _p, _p, _p],
+    "cf_knnfield_query_sparse": [_p, _p, _p, _p, _p, _i32, _i32, _p, _f64, _f64, _p, _i64, _p, _p, _p, _p, _p],
+    "cf_knnfield_brick_count": [_i32, _P(_i64)],
+    "cf_knnfield_brick_index": [_p, _i32, _p, _p, _p],
+    "cf_knnfield_brick_pack": [_p, _i32, _p, _p, _p],
+    "cf_knnfield_brick_unpack": [_p, _p, _i32, _p, _p],
     "cf_lbs_forward": [_p, _i32, _p, _p, _i64, _p, _p],
     "cf_lbs_vertex_transforms": [_p, _i32, _p, _i64, _p, _p, _p],
     "cf_lbs_setup": [_p, _i32, _p, _p, _i64, _p, _p, _p, _p, _p],

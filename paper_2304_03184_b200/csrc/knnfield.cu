@@ -4,7 +4,8 @@
 //   one-ring dilation               KnnField._dilate_once            knnfield.py:169-188
 //   O(1) per-sample query           KnnField.query_motion_batch      knnfield.py:197-222
 // Layout in HBM: neighbor_idx (r^3, s) int32 x-major (flat = i*r*r + j*r + k),
-// live map (r^3) int32, -1 = empty. The collision rule "nearest warped centre
+// live map (r^3) int32, -1 = empty — built dense in a scratch buffer shared by all
+// frames and kept per frame as 8^3 bricks (brick table + the occupied bricks). The collision rule "nearest warped centre
 // wins, ties -> smaller canonical voxel" is a two-phase atomicMin: first on the
 // float64 distance bits (order-preserving for non-negative doubles), then on the
 // canonical index among the exact-distance winners.
@@ -163,18 +164,101 @@ __global__ void live_dilate_kernel(const uint32_t* __restrict__ winner, int res,
   }
 }
 
-template <int K>
+// ---- sparse live maps: bricks of 8^3 voxels. brick_index (B^3 int32, B = ceil(res / 8),
+// brick (bi, bj, bk) at (bi * B + bj) * B + bk) holds the brick's block number in
+// `bricks` (512 int32 each, voxel (x, y, z) of the brick at (x * 8 + y) * 8 + z) or -1
+// when every voxel of the brick is empty. A live map is mostly empty space (the body
+// fills a few % of its bbox): 512 MiB dense per frame at 512^3 -> the occupied bricks.
+constexpr int kBrick = 8;
+
+__device__ __forceinline__ int32_t sparse_lookup(const int32_t* __restrict__ bidx, const int32_t* __restrict__ bricks,
+                                                 int res, int64_t f) {
+  const int64_t r = res, B = (r + kBrick - 1) / kBrick;
+  const int64_t i = f / (r * r), j = (f / r) % r, k = f % r;
+  const int32_t b = bidx[((i / kBrick) * B + j / kBrick) * B + k / kBrick];
+  return b < 0 ? -1 : bricks[(int64_t)b * (kBrick * kBrick * kBrick) + ((i % kBrick) * kBrick + j % kBrick) * kBrick + k % kBrick];
+}
+
+// warp per brick: flag[b] = any voxel of the brick set
+__global__ void brick_flag_kernel(const int32_t* __restrict__ live, int res, int32_t* __restrict__ flag) {
+  const int64_t r = res, B = (r + kBrick - 1) / kBrick, nb = B * B * B;
+  const int lane = threadIdx.x & 31;
+  for (int64_t b = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; b < nb;
+       b += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t bi = b / (B * B), bj = (b / B) % B, bk = b % B;
+    bool any = false;
+    for (int v = lane; v < kBrick * kBrick * kBrick; v += 32) {
+      const int64_t i = bi * kBrick + v / (kBrick * kBrick), j = bj * kBrick + (v / kBrick) % kBrick,
+                    k = bk * kBrick + v % kBrick;
+      if (i < r && j < r && k < r) any |= live[(i * r + j) * r + k] >= 0;
+    }
+    any = __any_sync(0xffffffffu, any);
+    if (lane == 0) flag[b] = any ? 1 : 0;
+  }
+}
+
+// one CTA: exclusive scan of the flags -> block numbers (or -1), count -> n_out
+__global__ void __launch_bounds__(1024) brick_scan_kernel(int32_t* __restrict__ idx, int64_t nb, int32_t* n_out) {
+  __shared__ int32_t s_sum[1024];
+  const int64_t per = (nb + blockDim.x - 1) / blockDim.x, lo = threadIdx.x * per, hi = min(lo + per, nb);
+  int32_t c = 0;
+  for (int64_t b = lo; b < hi; ++b) c += idx[b];
+  s_sum[threadIdx.x] = c;
+  __syncthreads();
+  for (int o = 1; o < (int)blockDim.x; o <<= 1) {  // inclusive Hillis-Steele
+    const int32_t v = threadIdx.x >= (unsigned)o ? s_sum[threadIdx.x - o] : 0;
+    __syncthreads();
+    s_sum[threadIdx.x] += v;
+    __syncthreads();
+  }
+  int32_t run = s_sum[threadIdx.x] - c;
+  for (int64_t b = lo; b < hi; ++b) {
+    const int32_t f = idx[b];
+    idx[b] = f ? run : -1;
+    run += f;
+  }
+  if (threadIdx.x == blockDim.x - 1) *n_out = s_sum[threadIdx.x];
+}
+
+// warp per brick: copy the set bricks' 512 voxels (voxels past the grid edge: -1)
+__global__ void brick_pack_kernel(const int32_t* __restrict__ live, int res, const int32_t* __restrict__ bidx,
+                                  int32_t* __restrict__ bricks) {
+  const int64_t r = res, B = (r + kBrick - 1) / kBrick, nb = B * B * B;
+  const int lane = threadIdx.x & 31;
+  for (int64_t b = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; b < nb;
+       b += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int32_t o = bidx[b];
+    if (o < 0) continue;
+    const int64_t bi = b / (B * B), bj = (b / B) % B, bk = b % B;
+    for (int v = lane; v < kBrick * kBrick * kBrick; v += 32) {
+      const int64_t i = bi * kBrick + v / (kBrick * kBrick), j = bj * kBrick + (v / kBrick) % kBrick,
+                    k = bk * kBrick + v % kBrick;
+      bricks[(int64_t)o * (kBrick * kBrick * kBrick) + v] = (i < r && j < r && k < r) ? live[(i * r + j) * r + k] : -1;
+    }
+  }
+}
+
+__global__ void brick_unpack_kernel(const int32_t* __restrict__ bidx, const int32_t* __restrict__ bricks, int res,
+                                    int32_t* __restrict__ live) {
+  const int64_t r = res, total = r * r * r;
+  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < total; f += (int64_t)gridDim.x * blockDim.x)
+    live[f] = sparse_lookup(bidx, bricks, res, f);
+}
+
+// kSparse: the live map as brick_index (live) + bricks
+template <int K, bool kSparse = false>
 __global__ void __launch_bounds__(128, 4) query_kernel(const int32_t* __restrict__ live, const int32_t* __restrict__ nidx,
                                                     const double* __restrict__ dqs,
                                                     const double* __restrict__ anchors, int s, Grid g, double r2,
                                                     const double* __restrict__ pts, int64_t n, int64_t* nbr_out,
-                                                    double* w_out, double* pc_out, uint8_t* valid_out) {
+                                                    double* w_out, double* pc_out, uint8_t* valid_out,
+                                                    const int32_t* __restrict__ bricks = nullptr) {
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
     const d3 p = load_d3(pts + 3 * q);
     bool inside;
     int64_t ijk[3];
     const int64_t f = flat_index(g, p, inside, ijk);
-    int64_t kv = inside ? (int64_t)live[f] : -1;
+    int64_t kv = inside ? (int64_t)(kSparse ? sparse_lookup(live, bricks, g.res, f) : live[f]) : -1;
     bool valid = kv >= 0;
     const int64_t ks = valid ? kv : 0;
     int nb[K];
@@ -258,10 +342,10 @@ int cf_knnfield_update(const double* nodes, const double* dqs, int64_t n, const 
   return cf::check_launch("cf_knnfield_update");
 }
 
-int cf_knnfield_query(const int32_t* live, const int32_t* neighbor_idx, const double* dqs_frame,
-                      const double* anchors_frame, int s, int res, const double* bbox_min, double voxel_size,
-                      double radius, const double* pts, int64_t n_pts, int64_t* nbr_out, double* w_out,
-                      double* pc_out, uint8_t* valid_out, void* stream) {
+static int knnfield_query(const int32_t* live, const int32_t* bricks, const int32_t* neighbor_idx,
+                          const double* dqs_frame, const double* anchors_frame, int s, int res, const double* bbox_min,
+                          double voxel_size, double radius, const double* pts, int64_t n_pts, int64_t* nbr_out,
+                          double* w_out, double* pc_out, uint8_t* valid_out, void* stream) {
   if (res < 8 || s < 1 || s > 16 || !live || !neighbor_idx || !dqs_frame || !anchors_frame)
     return cf::fail(CF_E_BAD_ARG, "cf_knnfield_query: bad args");
   if (n_pts == 0) return CF_OK;
@@ -269,9 +353,15 @@ int cf_knnfield_query(const int32_t* live, const int32_t* neighbor_idx, const do
   cudaStream_t st = cf::as_stream(stream);
   const unsigned grid = cf::grid_for(n_pts, 128, 8);
   const double r2 = radius * radius;
-#define CF_Q(KK)                                                                                              \
-  query_kernel<KK><<<grid, 128, 0, st>>>(live, neighbor_idx, dqs_frame, anchors_frame, s, g, r2, pts, n_pts, \
-                                         nbr_out, w_out, pc_out, valid_out)
+#define CF_Q(KK)                                                                                                    \
+  do {                                                                                                              \
+    if (bricks)                                                                                                     \
+      query_kernel<KK, true><<<grid, 128, 0, st>>>(live, neighbor_idx, dqs_frame, anchors_frame, s, g, r2, pts,     \
+                                                   n_pts, nbr_out, w_out, pc_out, valid_out, bricks);               \
+    else                                                                                                            \
+      query_kernel<KK, false><<<grid, 128, 0, st>>>(live, neighbor_idx, dqs_frame, anchors_frame, s, g, r2, pts,    \
+                                                    n_pts, nbr_out, w_out, pc_out, valid_out);                      \
+  } while (0)
   if (s <= 1) CF_Q(1);
   else if (s <= 2) CF_Q(2);
   else if (s <= 4) CF_Q(4);
@@ -279,6 +369,58 @@ int cf_knnfield_query(const int32_t* live, const int32_t* neighbor_idx, const do
   else CF_Q(16);
 #undef CF_Q
   return cf::check_launch("cf_knnfield_query");
+}
+
+int cf_knnfield_query(const int32_t* live, const int32_t* neighbor_idx, const double* dqs_frame,
+                      const double* anchors_frame, int s, int res, const double* bbox_min, double voxel_size,
+                      double radius, const double* pts, int64_t n_pts, int64_t* nbr_out, double* w_out,
+                      double* pc_out, uint8_t* valid_out, void* stream) {
+  return knnfield_query(live, nullptr, neighbor_idx, dqs_frame, anchors_frame, s, res, bbox_min, voxel_size, radius,
+                        pts, n_pts, nbr_out, w_out, pc_out, valid_out, stream);
+}
+
+int cf_knnfield_query_sparse(const int32_t* brick_index, const int32_t* bricks, const int32_t* neighbor_idx,
+                             const double* dqs_frame, const double* anchors_frame, int s, int res,
+                             const double* bbox_min, double voxel_size, double radius, const double* pts,
+                             int64_t n_pts, int64_t* nbr_out, double* w_out, double* pc_out, uint8_t* valid_out,
+                             void* stream) {
+  if (!bricks) return cf::fail(CF_E_BAD_ARG, "cf_knnfield_query_sparse: bad args");
+  return knnfield_query(brick_index, bricks, neighbor_idx, dqs_frame, anchors_frame, s, res, bbox_min, voxel_size,
+                        radius, pts, n_pts, nbr_out, w_out, pc_out, valid_out, stream);
+}
+
+int cf_knnfield_brick_count(int res, int64_t* n_bricks_total) {
+  if (res < 8 || !n_bricks_total) return cf::fail(CF_E_BAD_ARG, "cf_knnfield_brick_count: bad args");
+  const int64_t B = (res + kBrick - 1) / kBrick;
+  *n_bricks_total = B * B * B;
+  return CF_OK;
+}
+
+int cf_knnfield_brick_index(const int32_t* live_dense, int res, int32_t* brick_index, int32_t* n_set, void* stream) {
+  if (res < 8 || !live_dense || !brick_index || !n_set) return cf::fail(CF_E_BAD_ARG, "cf_knnfield_brick_index: bad args");
+  const int64_t B = (res + kBrick - 1) / kBrick, nb = B * B * B;
+  cudaStream_t st = cf::as_stream(stream);
+  brick_flag_kernel<<<cf::grid_for(nb * 32, 256, 8), 256, 0, st>>>(live_dense, res, brick_index);
+  brick_scan_kernel<<<1, 1024, 0, st>>>(brick_index, nb, n_set);
+  return cf::check_launch("cf_knnfield_brick_index");
+}
+
+int cf_knnfield_brick_pack(const int32_t* live_dense, int res, const int32_t* brick_index, int32_t* bricks,
+                           void* stream) {
+  if (res < 8 || !live_dense || !brick_index || !bricks) return cf::fail(CF_E_BAD_ARG, "cf_knnfield_brick_pack: bad args");
+  const int64_t B = (res + kBrick - 1) / kBrick, nb = B * B * B;
+  brick_pack_kernel<<<cf::grid_for(nb * 32, 256, 8), 256, 0, cf::as_stream(stream)>>>(live_dense, res, brick_index,
+                                                                                        bricks);
+  return cf::check_launch("cf_knnfield_brick_pack");
+}
+
+int cf_knnfield_brick_unpack(const int32_t* brick_index, const int32_t* bricks, int res, int32_t* live_dense,
+                             void* stream) {
+  if (res < 8 || !brick_index || !live_dense) return cf::fail(CF_E_BAD_ARG, "cf_knnfield_brick_unpack: bad args");
+  const int64_t total = (int64_t)res * res * res;
+  brick_unpack_kernel<<<cf::grid_for(total, 256, 8), 256, 0, cf::as_stream(stream)>>>(brick_index, bricks, res,
+                                                                                       live_dense);
+  return cf::check_launch("cf_knnfield_brick_unpack");
 }
 
 }  // extern "C"

@@ -53,13 +53,14 @@ def brute_force_query(graph, motion, pts_live, s: int, search: str = "brute"):
 
 
 class _LiveMaps(Mapping):
-    """dict-like view of per-frame live maps; values copied to host on access."""
+    """dict-like view of per-frame live maps; values expanded from the frame's bricks
+    and copied to host on access."""
 
     def __init__(self, field: "KnnField"):
         self._f = field
 
     def __getitem__(self, fid):
-        return host(self._f._live_dev[fid])
+        return host(self._f.live_map_dense(fid))
 
     def __iter__(self):
         return iter(self._f._live_dev)
@@ -105,6 +106,10 @@ class KnnField:
         self._anchors_dev: dict[int, torch.Tensor] = {}
         self._scratch_u64 = None
         self._scratch_i32 = None
+        self._scratch_live = None
+        nb = _lib.ctypes.c_int64()
+        _lib.call("cf_knnfield_brick_count", self.resolution, _lib.ctypes.byref(nb))
+        self._n_bricks = int(nb.value)
         self.live_maps = _LiveMaps(self)
 
     # -- reference attributes -------------------------------------------------
@@ -159,13 +164,23 @@ class KnnField:
         r3 = self.resolution ** 3
         d = self._nodes_dev.device
         if self._scratch_u64 is None:
+            # dense scratch shared by every frame's update (2 GiB at 512^3, freed by
+            # release_scratch); a frame keeps only its bricks (SURVEY §7 hard part 6)
             self._scratch_u64 = torch.empty(r3, dtype=torch.int64, device=d)
             self._scratch_i32 = torch.empty(r3, dtype=torch.int32, device=d)
+            self._scratch_live = torch.empty(r3, dtype=torch.int32, device=d)
         dqs = dev(dqs_np, shape_last=8)
-        live = torch.empty(r3, dtype=torch.int32, device=d)
+        dense = self._scratch_live
+        s = _lib.stream_ptr()
         _lib.call("cf_knnfield_update", self._nodes_dev.data_ptr(), dqs.data_ptr(), n, self._nidx_dev.data_ptr(),
-                  self.s, self.resolution, self._bmin_c, self.voxel_size, float(self.graph.radius), live.data_ptr(),
-                  self._scratch_u64.data_ptr(), self._scratch_i32.data_ptr(), _lib.stream_ptr())
+                  self.s, self.resolution, self._bmin_c, self.voxel_size, float(self.graph.radius), dense.data_ptr(),
+                  self._scratch_u64.data_ptr(), self._scratch_i32.data_ptr(), s)
+        bidx = torch.empty(self._n_bricks, dtype=torch.int32, device=d)
+        n_set = torch.empty(1, dtype=torch.int32, device=d)
+        _lib.call("cf_knnfield_brick_index", dense.data_ptr(), self.resolution, bidx.data_ptr(), n_set.data_ptr(), s)
+        bricks = torch.empty(max(int(n_set.item()), 1) * 512, dtype=torch.int32, device=d)  # one sync per registration
+        _lib.call("cf_knnfield_brick_pack", dense.data_ptr(), self.resolution, bidx.data_ptr(), bricks.data_ptr(), s)
+        live = (bidx, bricks)
         anchors = torch.empty_like(self._nodes_dev)
         _lib.call("cf_deform_nodes", self._nodes_dev.data_ptr(), dqs.data_ptr(), n, anchors.data_ptr(),
                   _lib.stream_ptr())
@@ -174,6 +189,23 @@ class KnnField:
         self._anchors_dev[fid] = anchors
         self._frame_slots[fid] = len(self._frame_slots)
         self._lut_blocks.append(dqs_np.copy())
+
+    def live_map_dense(self, frame_id: int) -> torch.Tensor:
+        """The frame's live map as the reference's dense (r^3,) int32 array (device)."""
+        bidx, bricks = self._live_dev[frame_id]
+        out = torch.empty(self.resolution ** 3, dtype=torch.int32, device=bidx.device)
+        _lib.call("cf_knnfield_brick_unpack", bidx.data_ptr(), bricks.data_ptr(), self.resolution, out.data_ptr(),
+                  _lib.stream_ptr())
+        return out
+
+    def live_map_bytes(self, frame_id: int) -> int:
+        """Device bytes the frame's live map occupies (brick table + set bricks)."""
+        bidx, bricks = self._live_dev[frame_id]
+        return bidx.numel() * 4 + bricks.numel() * 4
+
+    def release_scratch(self) -> None:
+        """Free the dense update scratch (re-allocated by the next update_live_map)."""
+        self._scratch_u64 = self._scratch_i32 = self._scratch_live = None
 
     # -- queries --------------------------------------------------------------
 
@@ -188,7 +220,8 @@ class KnnField:
         w = torch.empty((n_pts, self.s), dtype=torch.float64, device=d)
         pc = torch.empty((n_pts, 3), dtype=torch.float64, device=d)
         valid = torch.empty(n_pts, dtype=torch.uint8, device=d)
-        _lib.call("cf_knnfield_query", self._live_dev[frame_id].data_ptr(), self._nidx_dev.data_ptr(),
+        bidx, bricks = self._live_dev[frame_id]
+        _lib.call("cf_knnfield_query_sparse", bidx.data_ptr(), bricks.data_ptr(), self._nidx_dev.data_ptr(),
                   self._lut_dev[frame_id].data_ptr(), self._anchors_dev[frame_id].data_ptr(), self.s, self.resolution,
                   self._bmin_c, self.voxel_size, float(self.graph.radius), p.data_ptr(), n_pts, nbr.data_ptr(),
                   w.data_ptr(), pc.data_ptr(), valid.data_ptr(), _lib.stream_ptr())

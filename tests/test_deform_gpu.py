@@ -258,3 +258,36 @@ def test_shared_denominator_division_is_ieee_exact():
     bad = _lib.ctypes.c_int64(-1)
     _lib.call("cf_selftest_exact_div", 1 << 24, 20240607, _lib.ctypes.byref(bad))
     assert bad.value == 0
+
+
+def test_knnfield_sparse_live_maps():
+    """Per-frame live maps are kept as 8^3 bricks: far below the dense r^3 int32 map,
+    expanding back to it exactly, and queries on the bricks equal queries on the dense
+    map (cf_knnfield_query) — at a resolution that is not a multiple of 8."""
+    from paper_2304_03184_b200 import _lib
+    from paper_2304_03184_b200.knnfield import KnnField
+    from paper_2304_03184_b200.scene import Scene, SceneConfig
+    sc = Scene(SceneConfig(width=32, height=32), seed=0)
+    g = eg.EDGraph(sc.nodes)
+    f = KnnField(g, resolution=100, s=4)
+    f.update_live_map(eg.GraphMotion(3, sc.node_dqs(3)))
+    r = f.resolution
+    assert f.live_map_bytes(3) < 0.25 * r ** 3 * 4
+    dense = f.live_map_dense(3)
+    assert int((dense >= 0).sum()) > 1000
+    rng = np.random.default_rng(5)
+    anchors = od.deformed_nodes(sc.nodes, sc.node_dqs(3))
+    q = anchors[rng.integers(0, len(anchors), 4000)] + rng.normal(scale=0.05, size=(4000, 3))
+    nbr, w, pc, valid = f.query_motion_batch(q, 3)
+    p = torch.as_tensor(q, dtype=torch.float64, device="cuda")
+    n = len(q)
+    nb2 = torch.empty((n, f.s), dtype=torch.int64, device="cuda")
+    w2 = torch.empty((n, f.s), dtype=torch.float64, device="cuda")
+    pc2 = torch.empty((n, 3), dtype=torch.float64, device="cuda")
+    v2 = torch.empty(n, dtype=torch.uint8, device="cuda")
+    _lib.call("cf_knnfield_query", dense.data_ptr(), f._nidx_dev.data_ptr(), f._lut_dev[3].data_ptr(),
+              f._anchors_dev[3].data_ptr(), f.s, r, f._bmin_c, f.voxel_size, float(g.radius), p.data_ptr(), n,
+              nb2.data_ptr(), w2.data_ptr(), pc2.data_ptr(), v2.data_ptr(), _lib.stream_ptr())
+    assert np.array_equal(nbr, nb2.cpu().numpy()) and np.array_equal(valid, v2.bool().cpu().numpy())
+    assert np.array_equal(w, w2.cpu().numpy()) and np.array_equal(pc, pc2.cpu().numpy())
+    assert valid.mean() > 0.5
