@@ -7,7 +7,8 @@
 #include "dq.cuh"
 
 // header of a candidate grid (cf_cand_grid_build, knn.cu), followed at byte 64 by the
-// per-cell lists: uint16 count (0xFFFF = more than cmax) then cmax node ids
+// per-cell lists: uint16 count (0xFFFF = more than cmax) then cmax node ids, each list
+// padded to a 16-byte multiple (cand_stride entries) so a reader takes 8 at a time
 struct CandGridHdr {
   double origin[3];
   double h, inv_h;
@@ -15,6 +16,7 @@ struct CandGridHdr {
   int cmax;
 };
 static_assert(sizeof(CandGridHdr) <= 64, "candidate-grid header");
+__host__ __device__ constexpr int64_t cand_stride(int cmax) { return ((int64_t)cmax + 1 + 7) & ~(int64_t)7; }
 
 template <int K>
 __device__ __forceinline__ bool blend_apply(const TopK<K>& top, const double* __restrict__ dqs, int k, double r2,

@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(64) cand_grid_kernel(const uint8_t* __restrict
       }
     }
     const float cut = best[K - 1] * (1.0f + 1e-4f) + 1e-9f;
-    uint16_t* L = lists + c * (int64_t)(cmax + 1);
+    uint16_t* L = lists + c * cand_stride(cmax);
     int cnt = 0;
     for (int i = 0; i < n; ++i) {
       const float4 a = s_a[i];
@@ -877,7 +877,7 @@ int cf_dq_apply(const double* dq, int64_t dq_stride, const double* p, int64_t p_
 int cf_cand_grid_bytes(int grid_res, int cmax, int64_t* bytes) {
   if (grid_res < 1 || grid_res > 128 || cmax < 1 || cmax > 4096 || !bytes)
     return cf::fail(CF_E_BAD_ARG, "cf_cand_grid_bytes: bad args");
-  *bytes = 64 + (int64_t)grid_res * grid_res * grid_res * (cmax + 1) * 2;
+  *bytes = 64 + (int64_t)grid_res * grid_res * grid_res * cand_stride(cmax) * 2;
   return CF_OK;
 }
 

@@ -652,14 +652,20 @@ __global__ void __launch_bounds__(128, CF_CANON_MINB) human_canon_kernel(cf_marc
                                                           const BucketParams* __restrict__ LPp,
                                                           const int* __restrict__ lcs, const double4* __restrict__ ls,
                                                           float4* __restrict__ xu) {
-  extern __shared__ __align__(16) uint8_t s_blk[];  // kBlock: the anchor block (48 n + 48 B)
+  extern __shared__ __align__(16) uint8_t s_blk[];  // kBlock: the anchor block (48 n + 48 B), node dqs (64 n B)
   pdl_wait();
-  if (kBlock) {  // one coalesced copy of the prebuilt block, one barrier
+  if (kBlock) {  // one coalesced copy of the prebuilt block and of the node dqs, one barrier
     const int words = (48 * W.n_nodes + 48) / 16;
     const uint4* src = static_cast<const uint4*>(W.anchor_block);
     for (int i = threadIdx.x; i < words; i += blockDim.x) reinterpret_cast<uint4*>(s_blk)[i] = src[i];
+    const uint4* dsrc = reinterpret_cast<const uint4*>(W.dqs);
+    uint4* ddst = reinterpret_cast<uint4*>(s_blk + 48 * (size_t)W.n_nodes + 48);
+    for (int i = threadIdx.x; i < 4 * W.n_nodes; i += blockDim.x) ddst[i] = dsrc[i];
     __syncthreads();
   }
+  // kBlock: the blend reads the node dqs from shared memory (its k loads of 64 bytes
+  // each, right after the ranking, were a second dependent global round trip)
+  const double* s_dqs = kBlock ? reinterpret_cast<const double*>(s_blk + 48 * (size_t)W.n_nodes + 48) : W.dqs;
   const double4* a64 = reinterpret_cast<const double4*>(s_blk);
   const float4* a32 = reinterpret_cast<const float4*>(s_blk + 32 * (size_t)W.n_nodes);
   const double* box = reinterpret_cast<const double*>(s_blk + 48 * (size_t)W.n_nodes);
@@ -718,24 +724,33 @@ __global__ void __launch_bounds__(128, CF_CANON_MINB) human_canon_kernel(cf_marc
         }
         TopK<K> top;
         top.init(W.k);
-        const uint16_t* L = clists + cell * (int64_t)(cgrid->cmax + 1);
-        const int cnt = in ? (int)L[0] : 0xFFFF;
+        // the list 8 entries (16 bytes) per load, the next 8 in flight while these are
+        // ranked (one dependent 2-byte load per candidate was the k-NN's latency chain)
+        const uint4* L4 = reinterpret_cast<const uint4*>(clists + cell * cand_stride(cgrid->cmax));
+        uint4 v = in ? __ldg(L4) : make_uint4(0xFFFFu, 0u, 0u, 0u);
+        const int cnt = (int)(v.x & 0xFFFFu);
         if (cnt == 0xFFFF) {  // a crowded cell: every node
           for (int i = 0; i < W.n_nodes; ++i) {
             const double4 a = a64[i];
             top.insert(sqdist(p, d3{a.x, a.y, a.z}), i);
           }
         } else {
-          for (int j = 0; j < cnt; ++j) {
-            const int i = L[1 + j];
-            const double4 a = a64[i];
-            top.insert(sqdist(p, d3{a.x, a.y, a.z}), i);
+          for (int e0 = 0; e0 <= cnt; e0 += 8) {  // list position e: entry e - 1 (0 = count)
+            const uint4 nxt = e0 + 8 <= cnt ? __ldg(L4 + (e0 >> 3) + 1) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll 1
+            for (int u = (e0 == 0 ? 1 : 0); u < 8 && e0 + u <= cnt; ++u) {
+              const uint32_t w = u < 2 ? v.x : u < 4 ? v.y : u < 6 ? v.z : v.w;
+              const int i = (int)((u & 1) ? w >> 16 : w & 0xFFFFu);
+              const double4 a = a64[i];
+              top.insert(sqdist(p, d3{a.x, a.y, a.z}), i);
+            }
+            v = nxt;
           }
         }
-        ed_ok = blend_apply<K>(top, W.dqs, W.k, W.r2, true, p, pt);
+        ed_ok = blend_apply<K>(top, s_dqs, W.k, W.r2, true, p, pt);
       }
     } else {
-      ed_ok = kBlock ? ed_warp_point_cull<K>(a64, a32, W.n_nodes, W.dqs, W.k, W.r2, true, p, near, pt)
+      ed_ok = kBlock ? ed_warp_point_cull<K>(a64, a32, W.n_nodes, s_dqs, W.k, W.r2, true, p, near, pt)
                      : (live && ed_warp_point<K>(*EPp, ecs, es, W.dqs, W.k, W.r2, true, p, pt));
     }
     if (live) {
@@ -1358,7 +1373,7 @@ int cf_human_canon(const cf_march_desc* M, const double* dirs, const cf_march_ou
     return cf::fail(CF_E_BAD_ARG, "cf_human_canon: graphs of <= 1024 nodes need the anchor block (cf_deform_nodes_block)");
   const bool lbs = vert_buckets && W->vert_Tinv;
   cudaStream_t st = cf::as_stream(stream);
-  const size_t dsm = smem ? (size_t)(48 * W->n_nodes + 48) : 0;
+  const size_t dsm = smem ? (size_t)(48 * W->n_nodes + 48 + 64 * W->n_nodes) : 0;  // anchor block + node dqs
   // persistent: exactly the resident CTAs (the ticket balances the work)
 #define CF_HC(KK, SM)                                                                                             \
   int per_sm = 0;                                                                                                \
