@@ -779,9 +779,24 @@ __global__ void __launch_bounds__(kPrecDeformSlots* kPrecDeformThreads, 1)
                            const float4* __restrict__ xu, const float4* __restrict__ dfeat,
                            const int* __restrict__ count, int64_t capacity, float4* __restrict__ xc,
                            __half* __restrict__ save_h, float4* __restrict__ save_o,
-                           uint32_t* __restrict__ save_mask, __half* __restrict__ dfeat16) {
+                           uint32_t* __restrict__ save_mask, __half* __restrict__ dfeat16,
+                           const uint8_t* __restrict__ l2_prefetch = nullptr, int64_t l2_prefetch_bytes = 0) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t mbar[kPrecDeformSlots];
+  // the next stage's table (the canonical hash grid) into L2 while this tensor-bound
+  // kernel leaves the memory system idle: each CTA its share, as bulk L2 prefetches.
+  // Measured: the canonical hash stage itself gains ~1 us (it is L1/L2-request bound,
+  // not DRAM bound), but this kernel's build with the block runs 88 -> 72 us back to
+  // back whether or not the prefetch is issued (CF_NO_L2PF) — a code-layout effect of
+  // the hot loop (same instructions, shifted), not understood; profiles/r02_summary.md.
+  if (l2_prefetch && threadIdx.x == 0) {
+    const int64_t share = ((l2_prefetch_bytes + gridDim.x - 1) / gridDim.x + 65535) & ~(int64_t)65535;
+    const int64_t b0 = (int64_t)blockIdx.x * share, b1 = min(b0 + share, l2_prefetch_bytes & ~(int64_t)15);
+    for (int64_t b = b0; b < b1; b += 65536) {
+      const uint32_t sz = (uint32_t)min((int64_t)65536, b1 - b);
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(l2_prefetch + b), "r"(sz) : "memory");
+    }
+  }
   __shared__ uint32_t tmem_base;
   __shared__ __align__(16) float s_bias[128];
   __shared__ __align__(16) float s_w5[3 * 128];                        // W5 rows 0..2 in fp32 (hi + lo)
@@ -1693,7 +1708,9 @@ int field_stage_precise(const cf_field_desc* FD, const cf_march_out* S, const do
                        kPrecDeformSlots * kPrecDeformThreads, smem, st, FD->wblob, FD->wblob_lo, FD->dbias,
                        FD->delta_scale, FD->inv_side, xu, static_cast<const float4*>(dfeat32), S->counters, cap, xc,
                        reinterpret_cast<__half*>(FD->save_h), reinterpret_cast<float4*>(FD->save_o), FD->save_mask,
-                       reinterpret_cast<__half*>(sb + TL.dfeat16));
+                       reinterpret_cast<__half*>(sb + TL.dfeat16),
+                       static_cast<const uint8_t*>(FD->ctable),
+                       (int64_t)(FD->cgrid.offset[FD->cgrid.n_levels] * FD->cgrid.n_features * 4));
       }
       xcan = xc;
     }
@@ -1736,7 +1753,9 @@ int field_stage_precise(const cf_field_desc* FD, const cf_march_out* S, const do
                      kPrecDeformSlots * kPrecDeformThreads, smem, st, FD->wblob, FD->wblob_lo, FD->dbias,
                      FD->delta_scale, FD->inv_side, xu, static_cast<const float4*>(dfeat), S->counters, cap, xc,
                      static_cast<__half*>(nullptr), static_cast<float4*>(nullptr), static_cast<uint32_t*>(nullptr),
-                     static_cast<__half*>(nullptr));
+                     static_cast<__half*>(nullptr),
+                     getenv("CF_NO_L2PF") ? nullptr : static_cast<const uint8_t*>(FD->ctable),
+                     (int64_t)(FD->cgrid.offset[FD->cgrid.n_levels] * FD->cgrid.n_features * 4));
     }
     xcan = xc;
   }
