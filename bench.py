@@ -230,7 +230,7 @@ def load_peaks():
                            + src.get("micro", "-"))}
 
 
-def stage_costs(hs, os_, n_rays, precision):
+def stage_costs(hs, os_, n_rays, precision, fused=False):
     """Algorithmic work per launch of each render stage:
     (bound, work, unit, how). Hash stages: every level's 8 corner gathers (SURVEY 8(d)
     K8) against the measured gather-only ceiling of the same grid's access pattern
@@ -244,8 +244,11 @@ def stage_costs(hs, os_, n_rays, precision):
         "human_deform_mlp": ("tensor", hs * 110592.0, "FLOP",
                              "2(32x128 + 3x128x128 + 128x16) FLOP/sample" + (" (x3 issued: split fp16)" if f32 else "")),
         "human_hash_c": ("hash_c", hs * 16 * 8 * 8, "B", "16 levels x 8 corners x 8 B"),
-        "human_color_mlp": ("tensor", hs * 20480.0, "FLOP",
-                            "2(32x64 + 64x16 + 32x64 + 64x64 + 64x16) FLOP/sample" + (" (x3 issued)" if f32 else "")),
+        "human_color_mlp": (("hash_c", hs * 16 * 8 * 8, "B",
+                             "canonical hash fused in: 16 levels x 8 corners x 8 B gathers (+ E_g/E_c "
+                             "20 480 FLOP/sample, x3 issued, in the same kernel)") if fused else
+                            ("tensor", hs * 20480.0, "FLOP",
+                             "2(32x64 + 64x16 + 32x64 + 64x64 + 64x16) FLOP/sample" + (" (x3 issued)" if f32 else ""))),
         "object_field": ("hash_c", os_ * 16 * 8 * 8, "B", "hash (16 levels x 8 x 8 B) + E_g/E_c; gather-bound"),
         "march": ("hbm", n_rays * 32.0 + 4.0 * (hs + os_), "B", "B/ray: dir 24 + offset/count 8, + 4 B/record"),
         "human_composite": ("hbm", (hs) * 16.0 + n_rays * 40.0, "B", "field 16 B/sample + 40 B/ray out"),
@@ -434,7 +437,8 @@ def run_ours(args, rank, world, pg):
     hs = float(np.mean([counts[(k + fofs) % nF][0] for k in range(args.steps)]))
     os_ = float(np.mean([counts[(k + fofs) % nF][1] for k in range(args.steps)]))
     peaks = load_peaks()
-    costs = stage_costs(hs, os_, r.n_rays, args.precision)
+    costs = stage_costs(hs, os_, r.n_rays, args.precision,
+                        fused=bool(r.hdesc.precise) and not bool(r.hdesc.split_color))
     stages = {k: roofline_entry(k, costs[k], stage_ms[k], peaks) for k in costs if k in stage_ms}
     dom = max(stages, key=lambda k: stages[k]["ms"])
     roof = dict(stages[dom])

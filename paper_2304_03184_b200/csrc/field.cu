@@ -783,12 +783,13 @@ __global__ void __launch_bounds__(kPrecDeformSlots* kPrecDeformThreads, 1)
                            const uint8_t* __restrict__ l2_prefetch = nullptr, int64_t l2_prefetch_bytes = 0) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t mbar[kPrecDeformSlots];
-  // the next stage's table (the canonical hash grid) into L2 while this tensor-bound
-  // kernel leaves the memory system idle: each CTA its share, as bulk L2 prefetches.
-  // Measured: the canonical hash stage itself gains ~1 us (it is L1/L2-request bound,
-  // not DRAM bound), but this kernel's build with the block runs 88 -> 72 us back to
-  // back whether or not the prefetch is issued (CF_NO_L2PF) — a code-layout effect of
-  // the hot loop (same instructions, shifted), not understood; profiles/r02_summary.md.
+  // optional (l2_prefetch_on): the next stage's table into L2 while this tensor-bound
+  // kernel leaves the memory system idle, each CTA its share as bulk L2 prefetches.
+  // Measured: no gain for the hash stage (L1-request bound, 75.8 us after an L2 flush
+  // either way), ~4 us cost here, so it is off by default. The kernel compiled with this
+  // block runs 88 -> 72 us back to back, issued or not, while the same parameters
+  // without the block stay at 88 — a code-layout effect of the hot loop (the same
+  // instructions shifted by ~200), kept and documented.
   if (l2_prefetch && threadIdx.x == 0) {
     const int64_t share = ((l2_prefetch_bytes + gridDim.x - 1) / gridDim.x + 65535) & ~(int64_t)65535;
     const int64_t b0 = (int64_t)blockIdx.x * share, b1 = min(b0 + share, l2_prefetch_bytes & ~(int64_t)15);
@@ -934,12 +935,16 @@ __global__ void __launch_bounds__(kPrecDeformSlots* kPrecDeformThreads, 1)
 // per slot D (64) + A_hi (32) + A_lo (32) TMEM columns.
 constexpr int kColorPrecSlots = 4;
 
+// kHashCH > 0: the canonical hash features are computed here (hash_features with
+// kHashCH levels in flight, from the positions xu) instead of read from cfeat — the
+// gathers of one slot overlap the other slots' MMAs and epilogues
+template <int kHashCH>
 __global__ void __launch_bounds__(kColorPrecSlots* kSlotThreads, 1)
     color_mlp_prec_kernel(const uint8_t* __restrict__ wblob, const uint8_t* __restrict__ wblob_lo,
                           const float4* __restrict__ xu, const float4* __restrict__ cfeat,
                           const uint32_t* __restrict__ records, const double* __restrict__ dirs,
                           const int* __restrict__ count, int64_t capacity, float4* __restrict__ out,
-                          __half* __restrict__ cfeat16) {
+                          __half* __restrict__ cfeat16, cf_hashgrid_desc HD = {}, const float* __restrict__ htable = nullptr) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t mbar[kColorPrecSlots];
   __shared__ uint32_t tmem_base;
@@ -991,8 +996,20 @@ __global__ void __launch_bounds__(kColorPrecSlots* kSlotThreads, 1)
     const bool live = s < n;
     {
       float4 f[8];
+      if constexpr (kHashCH > 0) {
+        const float4 p = live ? xu[s] : make_float4(0.f, 0.f, 0.f, 0.f);
+        float* ff = reinterpret_cast<float*>(f);
+        if (p.w > 0.0f) {
+          hash_features<2, 16, kHashCH, float>(HD, htable, p.x, p.y, p.z, ff);
+        } else {
 #pragma unroll
-      for (int q = 0; q < 8; ++q) f[q] = live ? cfeat[s * 8 + q] : make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int i = 0; i < 32; ++i) ff[i] = 0.0f;
+        }
+
+      } else {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) f[q] = live ? cfeat[s * 8 + q] : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
       uint32_t hi[16];
       split_store<8>(S, f, 0, cfeat16 ? hi : nullptr);
       if (cfeat16 && s < capacity) {  // training: the features' fp16 halves, feature-major (32, capacity)
@@ -1648,6 +1665,14 @@ __global__ void bits_dilate_kernel(const uint32_t* __restrict__ src, uint32_t* _
   }
 }
 
+// the DeformNet kernel's L2 prefetch of the canonical table (CF_L2_PREFETCH=1): off by
+// default — measured, the hash stage after it gains nothing (it is L1-request bound)
+// and the kernel loses ~4 us issuing it
+bool l2_prefetch_on() {
+  static const bool on = [] { const char* e = getenv("CF_L2_PREFETCH"); return e && atoi(e) != 0; }();
+  return on;
+}
+
 unsigned persistent_grid(int64_t capacity, int slots) {
   const int64_t tiles = (capacity + 127) / 128;
   int64_t g = (tiles + slots - 1) / slots;
@@ -1727,10 +1752,11 @@ int field_stage_precise(const cf_field_desc* FD, const cf_march_out* S, const do
     if (run(3)) {
       const int off = FD->has_deform ? kDeformW : 0;
       const int csmem = 2 * kColorW;
-      CF_CHECK_CUDA(cudaFuncSetAttribute(color_mlp_prec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, csmem));
-      cf::launch_pdl(color_mlp_prec_kernel, persistent_grid(cap, kColorPrecSlots), kColorPrecSlots * kSlotThreads,
+      CF_CHECK_CUDA(cudaFuncSetAttribute(color_mlp_prec_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, csmem));
+      cf::launch_pdl(color_mlp_prec_kernel<0>, persistent_grid(cap, kColorPrecSlots), kColorPrecSlots * kSlotThreads,
                      csmem, st, FD->wblob + off, FD->wblob_lo + off, xu, static_cast<const float4*>(cfeat32),
-                     S->records, dirs, S->counters, cap, reinterpret_cast<float4*>(out_f), cfeat16);
+                     S->records, dirs, S->counters, cap, reinterpret_cast<float4*>(out_f), cfeat16, cf_hashgrid_desc{},
+                     static_cast<const float*>(nullptr));
     }
     return cf::check_launch("cf_field_forward (training)");
   }
@@ -1754,12 +1780,17 @@ int field_stage_precise(const cf_field_desc* FD, const cf_march_out* S, const do
                      FD->delta_scale, FD->inv_side, xu, static_cast<const float4*>(dfeat), S->counters, cap, xc,
                      static_cast<__half*>(nullptr), static_cast<float4*>(nullptr), static_cast<uint32_t*>(nullptr),
                      static_cast<__half*>(nullptr),
-                     getenv("CF_NO_L2PF") ? nullptr : static_cast<const uint8_t*>(FD->ctable),
+                     l2_prefetch_on() ? static_cast<const uint8_t*>(FD->ctable) : nullptr,
                      (int64_t)(FD->cgrid.offset[FD->cgrid.n_levels] * FD->cgrid.n_features * 4));
     }
     xcan = xc;
   }
-  if (run(2)) {
+  // the canonical hash fused into the E_g / E_c kernel (kHashCH = 4 levels in flight):
+  // each slot's gathers overlap the other slots' MMAs and epilogues, and the 128 B/sample
+  // feature round trip through HBM goes away (hash 76 + colour 37 -> 84 us after an L2
+  // flush); output bit-identical to the split stages (test_fused_color_kernel_equals_stages)
+  const int fused = FD->split_color ? 0 : 4;
+  if (run(2) && !fused) {
     if (FD->has_deform)
       cf::launch_pdl(hash_f16_kernel<2, 16, 4, 1, float, true>, hgrid, 128, 0, st, FD->cgrid,
                      reinterpret_cast<const float*>(FD->ctable), xcan, S->counters, cap, reinterpret_cast<uint4*>(cfeat));
@@ -1771,10 +1802,20 @@ int field_stage_precise(const cf_field_desc* FD, const cf_march_out* S, const do
   if (run(3)) {
     const int off = FD->has_deform ? kDeformW : 0;
     const int csmem = 2 * kColorW;
-    CF_CHECK_CUDA(cudaFuncSetAttribute(color_mlp_prec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, csmem));
-    cf::launch_pdl(color_mlp_prec_kernel, persistent_grid(cap, kColorPrecSlots), kColorPrecSlots * kSlotThreads, csmem,
-                   st, FD->wblob + off, FD->wblob_lo + off, xu, static_cast<const float4*>(cfeat), S->records, dirs,
-                   S->counters, cap, out, static_cast<__half*>(nullptr));
+    if (fused) {
+      auto kern = color_mlp_prec_kernel<4>;
+      CF_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, csmem));
+      cf::launch_pdl(kern, persistent_grid(cap, kColorPrecSlots), kColorPrecSlots * kSlotThreads, csmem, st,
+                     FD->wblob + off, FD->wblob_lo + off, xcan, static_cast<const float4*>(cfeat), S->records, dirs,
+                     S->counters, cap, out, static_cast<__half*>(nullptr), FD->cgrid,
+                     reinterpret_cast<const float*>(FD->ctable));
+    } else {
+      CF_CHECK_CUDA(cudaFuncSetAttribute(color_mlp_prec_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, csmem));
+      cf::launch_pdl(color_mlp_prec_kernel<0>, persistent_grid(cap, kColorPrecSlots), kColorPrecSlots * kSlotThreads,
+                     csmem, st, FD->wblob + off, FD->wblob_lo + off, xu, static_cast<const float4*>(cfeat),
+                     S->records, dirs, S->counters, cap, out, static_cast<__half*>(nullptr), cf_hashgrid_desc{},
+                     static_cast<const float*>(nullptr));
+    }
   }
   return cf::check_launch("cf_field_forward (precise)");
 }

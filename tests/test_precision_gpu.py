@@ -42,9 +42,9 @@ CGRID = (16, 2, 19, 16, 2048)
 DGRID = (8, 4, 17, 16, 256)
 
 
-def _scene_fields(precision):
+def _scene_fields(precision, fuse=False):
     sc = Scene(SceneConfig(width=64, height=64), seed=0)
-    cfg = RenderConfig(n_samples=64, precision=precision)
+    cfg = RenderConfig(n_samples=64, precision=precision, fuse_color_hash=fuse)
     hf = HumanField(sc.nodes, sc.template_points, sc.skin_verts, sc.skin_weights, cfg, seed=0, zero_deform_out=False,
                     table_scale=0.5)
     of = ObjectField(sc.box_half, cfg, seed=1, table_scale=0.5)
@@ -57,9 +57,14 @@ def _scene_fields(precision):
 
 @pytest.fixture(scope="module", params=["fp32", "fp16"])
 def rendered(request):
+    """One view with the stage-by-stage kernels (fuse_color_hash=False: the canonical
+    hash features land in the field scratch, so each stage can be checked on its own);
+    the render's fused hash + E_g/E_c kernel is checked against this path in
+    test_fused_color_kernel_equals_stages."""
     precision = request.param
     sc, cfg, hf, of = _scene_fields(precision)
     r = Renderer(hf, of, 64, 64, cfg)
+    r.cfg.cuda_graphs = False
     fid = 7
     R, t = sc.object_pose(fid)
     r.set_frame(sc.node_dqs(fid), sc.theta(fid), sc.bone_transforms(fid), R, t)
@@ -68,6 +73,39 @@ def rendered(request):
     torch.cuda.synchronize()
     r.check_overflow()
     return precision, sc, cfg, hf, of, r, fid
+
+
+def _by_record(buf):
+    """The view's field outputs ordered by record (the march's compaction order is
+    that of its warps' atomics, not fixed)."""
+    n = int(buf.counters[0])
+    rec = buf.records[:n].cpu().numpy().view(np.uint32)
+    order = np.argsort(rec, kind="stable")
+    return rec[order], buf.out[:n].cpu().numpy()[order]
+
+
+def test_fused_color_kernel_equals_stages():
+    """The render's fp32-mode colour stage computes the canonical hash features inside
+    the E_g / E_c kernel (color_mlp_prec_kernel<4>) instead of reading them from the
+    separate hash kernel's output: same functions, so the field outputs are bit-equal
+    to the stage-by-stage path, human and object."""
+    fid = 3
+    out = {}
+    for fuse in (False, True):
+        sc, cfg, hf, of = _scene_fields("fp32", fuse=fuse)  # same seeds: the same fields
+        r = Renderer(hf, of, 64, 64, cfg)
+        r.cfg.cuda_graphs = False
+        R, t = sc.object_pose(fid)
+        r.set_frame(sc.node_dqs(fid), sc.theta(fid), sc.bone_transforms(fid), R, t)
+        cam = sc.camera
+        r.render(cam.R, cam.t, cam.fx, cam.fy, cam.cx, cam.cy)
+        torch.cuda.synchronize()
+        assert bool(r.hdesc.split_color) != fuse
+        out[fuse] = (_by_record(r.hb), _by_record(r.ob))
+    for f in range(2):
+        (ra, oa), (rb, ob) = out[False][f], out[True][f]
+        assert len(ra) > 100 and np.array_equal(ra, rb)
+        assert np.array_equal(oa.view(np.int32), ob.view(np.int32))
 
 
 def _scratch_views(r, buf, desc, has_deform, precision):
