@@ -241,14 +241,15 @@ def stage_costs(hs, os_, n_rays, precision, fused=False):
     return {
         "human_canon": ("hbm", hs * 57.0, "B", "57 B/sample (SURVEY 8d K5/K6: pos 12 + p_c 12 + idx 16 + w 16 + valid 1)"),
         "human_hash_d": ("hash_d", hs * 8 * 8 * ent_d, "B", f"8 levels x 8 corners x {ent_d} B"),
-        "human_deform_mlp": ("tensor", hs * 110592.0, "FLOP",
-                             "2(32x128 + 3x128x128 + 128x16) FLOP/sample" + (" (x3 issued: split fp16)" if f32 else "")),
+        "human_deform_mlp": [("tensor", hs * 110592.0, "FLOP",
+                              "2(32x128 + 3x128x128 + 128x16) FLOP/sample" + (" (x3 issued: split fp16)" if f32 else ""))]
+                            + ([("hash_d", hs * 8 * 8 * ent_d, "B",
+                                 f"deformation-grid hash fused in: 8 levels x 8 corners x {ent_d} B")] if fused else []),
         "human_hash_c": ("hash_c", hs * 16 * 8 * 8, "B", "16 levels x 8 corners x 8 B"),
-        "human_color_mlp": (("hash_c", hs * 16 * 8 * 8, "B",
-                             "canonical hash fused in: 16 levels x 8 corners x 8 B gathers (+ E_g/E_c "
-                             "20 480 FLOP/sample, x3 issued, in the same kernel)") if fused else
-                            ("tensor", hs * 20480.0, "FLOP",
-                             "2(32x64 + 64x16 + 32x64 + 64x64 + 64x16) FLOP/sample" + (" (x3 issued)" if f32 else ""))),
+        "human_color_mlp": [("tensor", hs * 20480.0, "FLOP",
+                             "2(32x64 + 64x16 + 32x64 + 64x64 + 64x16) FLOP/sample" + (" (x3 issued)" if f32 else ""))]
+                           + ([("hash_c", hs * 16 * 8 * 8, "B", "canonical hash fused in: 16 levels x 8 corners x 8 B")]
+                              if fused else []),
         "object_field": ("hash_c", os_ * 16 * 8 * 8, "B", "hash (16 levels x 8 x 8 B) + E_g/E_c; gather-bound"),
         "march": ("hbm", n_rays * 32.0 + 4.0 * (hs + os_), "B", "B/ray: dir 24 + offset/count 8, + 4 B/record"),
         "human_composite": ("hbm", (hs) * 16.0 + n_rays * 40.0, "B", "field 16 B/sample + 40 B/ray out"),
@@ -256,6 +257,18 @@ def stage_costs(hs, os_, n_rays, precision, fused=False):
 
 
 def roofline_entry(name, cost, ms, peaks):
+    """One stage against its bound. A fused stage (a list of costs: e.g. the MLP's
+    FLOPs and the hash gathers it does itself) is bound by the resource whose ideal
+    time is the longest; that resource's entry is reported, the others listed."""
+    if isinstance(cost, list):
+        parts = [roofline_entry(name, c, ms, peaks) for c in cost]
+        if len(parts) == 1:
+            return parts[0]
+        best = dict(max(parts, key=lambda e: e["frac"]))
+        best["components"] = [{x: e[x] for x in ("bound", "achieved", "peak", "unit", "frac", "per_unit")}
+                              for e in parts]
+        best["per_unit"] = " + ".join(e["per_unit"] for e in parts) + " (one kernel; bound = the slower resource)"
+        return best
     bound, work, unit, how = cost
     if bound == "tensor":
         ach = work / (ms / 1e3) / 1e12
@@ -438,7 +451,7 @@ def run_ours(args, rank, world, pg):
     os_ = float(np.mean([counts[(k + fofs) % nF][1] for k in range(args.steps)]))
     peaks = load_peaks()
     costs = stage_costs(hs, os_, r.n_rays, args.precision,
-                        fused=bool(r.hdesc.precise) and not bool(r.hdesc.split_color))
+                        fused=bool(r.hdesc.precise) and not bool(r.hdesc.split_stages))
     stages = {k: roofline_entry(k, costs[k], stage_ms[k], peaks) for k in costs if k in stage_ms}
     dom = max(stages, key=lambda k: stages[k]["ms"])
     roof = dict(stages[dom])

@@ -390,9 +390,9 @@ typedef struct cf_field_desc {
   const uint8_t* wblob_lo;  /* precise: the residual blob fp16(W - fp16(W)), same layout as wblob */
   int train;                /* 1 = the training forward: 32-bit semantics (as precise) plus the fp16 saves of
                                the backward, feature-major in the scratch (cf_field_train_layout) */
-  int split_color;          /* precise render: 0 = the canonical hash features are computed inside the E_g / E_c
-                               kernel (stage 2 is empty, stage 3 does both); 1 = separate kernels, the
-                               features in the scratch (stage-by-stage inspection) */
+  int split_stages;         /* precise render: 0 = the hash lookups run inside the MLP kernels (the deformation
+                               grid in DeformNet, the canonical grid in E_g / E_c: stages 0 and 2 are empty);
+                               1 = separate hash kernels, features in the scratch (stage-by-stage inspection) */
 } cf_field_desc;
 /* occupancy from the trained density (the builder's K12; SPEC.md:429 leaves ray-marching
  * acceleration open): per cell of a res^3 grid over the field's unit cube, the E_g density

@@ -772,7 +772,7 @@ __device__ __forceinline__ uint32_t relu_dot3_q(const SplitSlot& S, int col, con
 // spatial gradient is evaluated where the 32-bit field puts the sample), plus the
 // fp16 saves the fp16 backward consumes: h1..h4 (hi halves, feature-major), the
 // ReLU bits, o, and the deformation features' hi halves (dfeat16, for dW of layer 1)
-template <bool kSave>
+template <bool kSave, int kHash = 0>
 __global__ void __launch_bounds__(kPrecDeformSlots* kPrecDeformThreads, 1)
     deform_mlp_prec_kernel(const uint8_t* __restrict__ wblob, const uint8_t* __restrict__ wblob_lo,
                            const float* __restrict__ bias1, float delta_scale, float inv_side,
@@ -780,7 +780,8 @@ __global__ void __launch_bounds__(kPrecDeformSlots* kPrecDeformThreads, 1)
                            const int* __restrict__ count, int64_t capacity, float4* __restrict__ xc,
                            __half* __restrict__ save_h, float4* __restrict__ save_o,
                            uint32_t* __restrict__ save_mask, __half* __restrict__ dfeat16,
-                           const uint8_t* __restrict__ l2_prefetch = nullptr, int64_t l2_prefetch_bytes = 0) {
+                           const uint8_t* __restrict__ l2_prefetch = nullptr, int64_t l2_prefetch_bytes = 0,
+                           cf_hashgrid_desc DG = {}, const float* __restrict__ dtable = nullptr) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t mbar[kPrecDeformSlots];
   // optional (l2_prefetch_on): the next stage's table into L2 while this tensor-bound
@@ -851,9 +852,25 @@ __global__ void __launch_bounds__(kPrecDeformSlots* kPrecDeformThreads, 1)
        tile += (int64_t)gridDim.x * kPrecDeformSlots) {
     const int64_t s = tile * 128 + S.r;
     const bool live = s < n;
-    {  // this quarter's 8 input features -> hi / lo A columns 4 cq ..
-      const float4 f0 = live ? dfeat[s * 8 + 2 * cq] : make_float4(0.f, 0.f, 0.f, 0.f);
-      const float4 f1 = live ? dfeat[s * 8 + 2 * cq + 1] : make_float4(0.f, 0.f, 0.f, 0.f);
+    // the sample's position (quarter 0: the output at the end of the tile; kHash: every
+    // quarter, the deformation-grid lookup), loaded now, under the layers
+    const float4 xu_s = ((kHash > 0 || cq == 0) && live) ? xu[s] : make_float4(0.f, 0.f, 0.f, 0.f);
+    {  // this quarter's 8 input features (levels 2 cq, 2 cq + 1) -> hi / lo A columns 4 cq ..
+      float4 f0, f1;
+      if constexpr (kHash > 0) {  // the deformation-grid hash here, as hash_f16_kernel computes it
+        float ft[8];
+        if (xu_s.w > 0.0f) {
+          hash_features<4, 2, kHash, float>(DG, dtable, xu_s.x, xu_s.y, xu_s.z, ft, 2 * cq);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) ft[i] = 0.0f;
+        }
+        f0 = make_float4(ft[0], ft[1], ft[2], ft[3]);
+        f1 = make_float4(ft[4], ft[5], ft[6], ft[7]);
+      } else {
+        f0 = live ? dfeat[s * 8 + 2 * cq] : make_float4(0.f, 0.f, 0.f, 0.f);
+        f1 = live ? dfeat[s * 8 + 2 * cq + 1] : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
       uint32_t h[4], l[4];
       tc::split_f16x2(f0.x, f0.y, h[0], l[0]);
       tc::split_f16x2(f0.z, f0.w, h[1], l[1]);
@@ -874,8 +891,6 @@ __global__ void __launch_bounds__(kPrecDeformSlots* kPrecDeformThreads, 1)
       }
     }
     // training saves: h feature-major (512, capacity), ReLU bits [layer][32-column word] per sample
-    // the sample's position, needed at the end of the tile: loaded now, under the layers
-    const float4 xu_s = (cq == 0 && live) ? xu[s] : make_float4(0.f, 0.f, 0.f, 0.f);
     __half* sv = (kSave && s < capacity) ? save_h + s : nullptr;
     uint32_t* mk = (kSave && live) ? save_mask + s * 16 + cq : nullptr;
 #pragma unroll 1
@@ -1734,8 +1749,8 @@ int field_stage_precise(const cf_field_desc* FD, const cf_march_out* S, const do
                        FD->delta_scale, FD->inv_side, xu, static_cast<const float4*>(dfeat32), S->counters, cap, xc,
                        reinterpret_cast<__half*>(FD->save_h), reinterpret_cast<float4*>(FD->save_o), FD->save_mask,
                        reinterpret_cast<__half*>(sb + TL.dfeat16),
-                       static_cast<const uint8_t*>(FD->ctable),
-                       (int64_t)(FD->cgrid.offset[FD->cgrid.n_levels] * FD->cgrid.n_features * 4));
+                       static_cast<const uint8_t*>(nullptr), (int64_t)0, cf_hashgrid_desc{},
+                       static_cast<const float*>(nullptr));
       }
       xcan = xc;
     }
@@ -1769,19 +1784,26 @@ int field_stage_precise(const cf_field_desc* FD, const cf_march_out* S, const do
   if (FD->has_deform) {
     float4* dfeat = cfeat + cap * 8;
     float4* xc = dfeat + cap * 8;
-    if (run(0))
+    // the deformation-grid hash inside DeformNet (render, split_stages = 0): each thread
+    // looks up its quarter's 2 levels at the tile head (2 levels of gathers in flight)
+    // instead of reading the 128 B/sample the hash kernel wrote — hash 46 + DeformNet 82
+    // -> 121 us serialised, 0.403 -> 0.391 ms per frame; bit-identical to the split path
+    const int dfused = FD->split_stages ? 0 : 2;
+    if (run(0) && !dfused)
       cf::launch_pdl(hash_f16_kernel<4, 8, 2, 2, float, true>, cf::grid_for(cap * 2, 128, 16), 128, 0, st, FD->dgrid,
                      reinterpret_cast<const float*>(FD->dtable), xu, S->counters, cap, reinterpret_cast<uint4*>(dfeat));
     if (run(1)) {
       const int smem = 2 * kDeformW;
-      CF_CHECK_CUDA(cudaFuncSetAttribute(deform_mlp_prec_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      cf::launch_pdl(deform_mlp_prec_kernel<false>, persistent_grid(cap, kPrecDeformSlots),
+      auto kern = dfused ? deform_mlp_prec_kernel<false, 2> : deform_mlp_prec_kernel<false, 0>;
+      CF_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      cf::launch_pdl(kern, persistent_grid(cap, kPrecDeformSlots),
                      kPrecDeformSlots * kPrecDeformThreads, smem, st, FD->wblob, FD->wblob_lo, FD->dbias,
                      FD->delta_scale, FD->inv_side, xu, static_cast<const float4*>(dfeat), S->counters, cap, xc,
                      static_cast<__half*>(nullptr), static_cast<float4*>(nullptr), static_cast<uint32_t*>(nullptr),
                      static_cast<__half*>(nullptr),
                      l2_prefetch_on() ? static_cast<const uint8_t*>(FD->ctable) : nullptr,
-                     (int64_t)(FD->cgrid.offset[FD->cgrid.n_levels] * FD->cgrid.n_features * 4));
+                     (int64_t)(FD->cgrid.offset[FD->cgrid.n_levels] * FD->cgrid.n_features * 4), FD->dgrid,
+                     reinterpret_cast<const float*>(FD->dtable));
     }
     xcan = xc;
   }
@@ -1789,7 +1811,7 @@ int field_stage_precise(const cf_field_desc* FD, const cf_march_out* S, const do
   // each slot's gathers overlap the other slots' MMAs and epilogues, and the 128 B/sample
   // feature round trip through HBM goes away (hash 76 + colour 37 -> 84 us after an L2
   // flush); output bit-identical to the split stages (test_fused_color_kernel_equals_stages)
-  const int fused = FD->split_color ? 0 : 4;
+  const int fused = FD->split_stages ? 0 : 4;
   if (run(2) && !fused) {
     if (FD->has_deform)
       cf::launch_pdl(hash_f16_kernel<2, 16, 4, 1, float, true>, hgrid, 128, 0, st, FD->cgrid,

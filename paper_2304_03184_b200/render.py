@@ -74,7 +74,7 @@ class RenderConfig:
     # warp-cooperative culled scan instead)
     cand_grid_res: int = 48
     cand_grid_cmax: int = 64
-    fuse_color_hash: bool = True  # fp32 mode: canonical hash inside the E_g/E_c kernel (cf_field_desc.split_color)
+    fuse_hash: bool = True  # fp32 mode: hash lookups inside the MLP kernels (cf_field_desc.split_stages = 0)
     occ_alpha: float = 0.01
     occ_decay: float = 0.95
     background: tuple = (24 / 255.0, 28 / 255.0, 34 / 255.0)   # config.py bg_r/g/b
@@ -231,7 +231,7 @@ class HumanField:
         precise = _precise(precision or self.cfg.precision)
         d = _lib.FieldDesc()
         d.has_deform = 1
-        d.split_color = int(not self.cfg.fuse_color_hash)
+        d.split_stages = int(not self.cfg.fuse_hash)
         d.dgrid = self.dgrid.desc
         d.dtable = (self.dgrid.table if precise else self.dgrid.table_for_kernels()).data_ptr()
         d.cgrid = self.cgrid.desc
@@ -272,7 +272,7 @@ class ObjectField:
     def desc(self, precision: str | None = None) -> _lib.FieldDesc:
         d = _lib.FieldDesc()
         d.has_deform = 0
-        d.split_color = int(not self.cfg.fuse_color_hash)
+        d.split_stages = int(not self.cfg.fuse_hash)
         d.cgrid = self.cgrid.desc
         d.ctable = self.cgrid.table_for_kernels().data_ptr()
         d.wblob = self.nets.blob.data_ptr()
@@ -837,9 +837,9 @@ class Renderer:
                       hb.xu.data_ptr(), s)
             self._mark("human_canon")
             scratch = self._scratch(hb, self.hdesc).data_ptr()
-            fused = self.hdesc.precise and not self.hdesc.split_color  # stage 2 runs inside stage 3
+            fused = self.hdesc.precise and not self.hdesc.split_stages  # stages 0 / 2 run inside 1 / 3
             for stage, name in enumerate(("human_hash_d", "human_deform_mlp", "human_hash_c", "human_color_mlp")):
-                if stage == 2 and fused:
+                if stage in (0, 2) and fused:
                     continue
                 _lib.call("cf_field_stage", _lib.byref(self.hdesc), _lib.byref(hb.mo), self.dirs.data_ptr(),
                           hb.xu.data_ptr(), hb.out.data_ptr(), scratch, stage, s)

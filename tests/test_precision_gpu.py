@@ -44,7 +44,7 @@ DGRID = (8, 4, 17, 16, 256)
 
 def _scene_fields(precision, fuse=False):
     sc = Scene(SceneConfig(width=64, height=64), seed=0)
-    cfg = RenderConfig(n_samples=64, precision=precision, fuse_color_hash=fuse)
+    cfg = RenderConfig(n_samples=64, precision=precision, fuse_hash=fuse)
     hf = HumanField(sc.nodes, sc.template_points, sc.skin_verts, sc.skin_weights, cfg, seed=0, zero_deform_out=False,
                     table_scale=0.5)
     of = ObjectField(sc.box_half, cfg, seed=1, table_scale=0.5)
@@ -57,10 +57,10 @@ def _scene_fields(precision, fuse=False):
 
 @pytest.fixture(scope="module", params=["fp32", "fp16"])
 def rendered(request):
-    """One view with the stage-by-stage kernels (fuse_color_hash=False: the canonical
-    hash features land in the field scratch, so each stage can be checked on its own);
-    the render's fused hash + E_g/E_c kernel is checked against this path in
-    test_fused_color_kernel_equals_stages."""
+    """One view with the stage-by-stage kernels (fuse_hash=False: both grids' hash
+    features land in the field scratch, so each stage can be checked on its own); the
+    render's fused hash + MLP kernels are checked against this path in
+    test_fused_hash_kernels_equal_stages."""
     precision = request.param
     sc, cfg, hf, of = _scene_fields(precision)
     r = Renderer(hf, of, 64, 64, cfg)
@@ -84,11 +84,12 @@ def _by_record(buf):
     return rec[order], buf.out[:n].cpu().numpy()[order]
 
 
-def test_fused_color_kernel_equals_stages():
-    """The render's fp32-mode colour stage computes the canonical hash features inside
-    the E_g / E_c kernel (color_mlp_prec_kernel<4>) instead of reading them from the
-    separate hash kernel's output: same functions, so the field outputs are bit-equal
-    to the stage-by-stage path, human and object."""
+def test_fused_hash_kernels_equal_stages():
+    """The render's fp32 mode looks the hash grids up inside the MLP kernels (the
+    deformation grid in DeformNet, deform_mlp_prec_kernel<false, 2>; the canonical grid
+    in E_g / E_c, color_mlp_prec_kernel<4>) instead of reading the separate hash
+    kernels' output: same functions, so the field outputs are bit-equal to the
+    stage-by-stage path, human and object."""
     fid = 3
     out = {}
     for fuse in (False, True):
@@ -100,7 +101,7 @@ def test_fused_color_kernel_equals_stages():
         cam = sc.camera
         r.render(cam.R, cam.t, cam.fx, cam.fy, cam.cx, cam.cy)
         torch.cuda.synchronize()
-        assert bool(r.hdesc.split_color) != fuse
+        assert bool(r.hdesc.split_stages) != fuse
         out[fuse] = (_by_record(r.hb), _by_record(r.ob))
     for f in range(2):
         (ra, oa), (rb, ob) = out[False][f], out[True][f]

@@ -20,12 +20,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SRC = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "gpurun_out")
 OUT = os.path.join(ROOT, "profiles")
 
-# bench stage -> the kernel (name prefix, template args) whose ncu capture it uses
+# bench stage -> the kernel (name prefix) whose ncu capture it uses (the longest launch
+# of that name: the human field's, not the object's)
 STAGE_KERNEL = {
     "human_canon": "human_canon_kernel",
-    "human_hash_d": "hash_f16_kernel<4, 8, 2, 2, float, 1>",
-    "human_deform_mlp": "deform_mlp_prec_kernel<0>",
-    "human_hash_c": "hash_f16_kernel<2, 16, 4, 1, float, 1>",
+    "human_deform_mlp": "deform_mlp_prec_kernel",
     "human_color_mlp": "color_mlp_prec_kernel",
     "march": "march_kernel",
 }
@@ -101,7 +100,7 @@ def main():
     for stage, kname in STAGE_KERNEL.items():
         hits = [k for k in kern if k["name"].startswith(kname)]
         if hits:
-            k = hits[0]
+            k = max(hits, key=lambda h: h["us"])
             traffic["fp32:" + stage] = {
                 "dram_bytes_per_launch": (k["rd"] + k["wr"]),
                 "source": "profiles/r02_render_kernels_ncu_full.csv (dram__bytes_read.sum + dram__bytes_write.sum, "
