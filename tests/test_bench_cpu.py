@@ -61,3 +61,25 @@ def test_gpu_arm_refuses_without_devices():
     cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1"]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
     assert out.returncode != 0 and "CUDA device" in (out.stderr + out.stdout)
+
+
+def test_roofline_of_fused_stages_is_the_slower_resource():
+    """A fused stage (MLP FLOPs + the hash gathers it does itself) reports the resource
+    with the longer ideal time, the other one listed; unfused stages keep one bound."""
+    sys.path.insert(0, ROOT)
+    import bench
+    peaks = {"bf16_tflops": (1600.0, "t"), "hash_c_gbs": (4000.0, "t"), "hash_d_gbs": (10000.0, "t"),
+             "hbm_gbs": (6500.0, "t")}
+    hs = 300_000
+    fused = bench.stage_costs(hs, 40_000, 512 * 512, "fp32", fused=True)
+    split = bench.stage_costs(hs, 40_000, 512 * 512, "fp32", fused=False)
+    e = bench.roofline_entry("human_color_mlp", fused["human_color_mlp"], 0.08, peaks)
+    gather = hs * 16 * 8 * 8 / 0.08e-3 / 1e9 / 4000.0
+    tensor = hs * 20480.0 / 0.08e-3 / 1e12 / 1600.0
+    assert e["bound"] == "gather" and abs(e["frac"] - gather) < 1e-9
+    assert sorted(c["bound"] for c in e["components"]) == ["gather", "tensor"]
+    assert abs(min(c["frac"] for c in e["components"]) - tensor) < 1e-9
+    d = bench.roofline_entry("human_deform_mlp", fused["human_deform_mlp"], 0.12, peaks)
+    assert d["frac"] == max(c["frac"] for c in d["components"])
+    s = bench.roofline_entry("human_deform_mlp", split["human_deform_mlp"], 0.08, peaks)
+    assert s["bound"] == "tensor" and "components" not in s
