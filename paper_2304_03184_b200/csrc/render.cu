@@ -933,6 +933,40 @@ __device__ __forceinline__ void seg_t_delta(const cf_march_desc& M, const cf_mar
   }
 }
 
+// One ray's front-to-back accumulation, 4 samples per step: their field values and
+// depths are loaded together before the sequential accumulation (the loop's loads were
+// one dependent round trip per sample); same operations in the same order as sample by
+// sample, stopping after the sample that takes T below t_term.
+__device__ __forceinline__ void ray_accumulate(const cf_march_desc& M, const cf_march_out& F,
+                                               const float4* __restrict__ field, float t_term, int off, int cnt,
+                                               float& T, float& r, float& g, float& b, float& dep) {
+  for (int j0 = 0; j0 < cnt; j0 += 4) {
+    float4 f[4];
+    float t[4], delta[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (j0 + u < cnt) {
+        f[u] = field[off + j0 + u];
+        seg_t_delta(M, F, off, cnt, j0 + u, t[u], delta[u]);
+      }
+    }
+    bool stop = false;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (stop || j0 + u >= cnt) break;
+      const float alpha = 1.0f - expf(-f[u].x * delta[u]);
+      const float w = T * alpha;
+      r += w * f[u].y;
+      g += w * f[u].z;
+      b += w * f[u].w;
+      dep += w * t[u];
+      T *= 1.0f - alpha;
+      stop = T < t_term;
+    }
+    if (stop) break;
+  }
+}
+
 // front-to-back alpha compositing: alpha_i = 1 - exp(-sigma_i * dt),
 // T_i = prod_{j<i} (1 - alpha_j); stops once T < t_term
 __global__ void composite_kernel(cf_march_desc M, cf_march_out F, const float4* __restrict__ field, float t_term,
@@ -942,19 +976,7 @@ __global__ void composite_kernel(cf_march_desc M, cf_march_out F, const float4* 
        ray += (int64_t)gridDim.x * blockDim.x) {
     const int off = F.ray_offset[ray], cnt = F.ray_count[ray];
     float T = 1.0f, r = 0.f, g = 0.f, b = 0.f, dep = 0.f, op = 0.f;
-    for (int j = 0; j < cnt; ++j) {
-      const float4 f = field[off + j];
-      float t, delta;
-      seg_t_delta(M, F, off, cnt, j, t, delta);
-      const float alpha = 1.0f - expf(-f.x * delta);
-      const float w = T * alpha;
-      r += w * f.y;
-      g += w * f.z;
-      b += w * f.w;
-      dep += w * t;
-      T *= 1.0f - alpha;
-      if (T < t_term) break;
-    }
+    ray_accumulate(M, F, field, t_term, off, cnt, T, r, g, b, dep);
     op = 1.0f - T;  // = sum T_i alpha_i (telescoping), without its rounding drift
     rgb[3 * ray] = r;
     rgb[3 * ray + 1] = g;
@@ -978,19 +1000,7 @@ __global__ void composite_final_kernel(cf_march_desc M, cf_march_out F, const fl
        ray += (int64_t)gridDim.x * blockDim.x) {
     const int off = F.ray_offset[ray], cnt = F.ray_count[ray];
     float T = 1.0f, r = 0.f, g = 0.f, b = 0.f, dep = 0.f, op = 0.f;
-    for (int j = 0; j < cnt; ++j) {
-      const float4 f = field[off + j];
-      float t, delta;
-      seg_t_delta(M, F, off, cnt, j, t, delta);
-      const float alpha = 1.0f - expf(-f.x * delta);
-      const float w = T * alpha;
-      r += w * f.y;
-      g += w * f.z;
-      b += w * f.w;
-      dep += w * t;
-      T *= 1.0f - alpha;
-      if (T < t_term) break;
-    }
+    ray_accumulate(M, F, field, t_term, off, cnt, T, r, g, b, dep);
     op = 1.0f - T;  // = sum T_i alpha_i (telescoping), without its rounding drift
     const float hd = dep / fmaxf(op, 1e-6f);
     rgb[3 * ray] = r;
