@@ -1116,11 +1116,15 @@ struct ColorBwdIO {
 // coalesced 64-byte segments per warp store, half the store instructions of 2-byte
 // stores. All 32 lanes call it (shuffles); ok gates the lane's store (the pair's
 // lanes share it: a tile's lanes are all inside the capacity, a multiple of 128).
-__device__ __forceinline__ void store_fm_f16(__half* dst, int64_t s, int64_t ld, int width, const float* v, bool ok) {
+// (width a template parameter and the loop fully unrolled: with a runtime width and a
+// partial unroll, v[] was indexed at run time and lived in local memory — 256 bytes of
+// stack per thread in the colour backward)
+template <int kWidth>
+__device__ __forceinline__ void store_fm_f16(__half* dst, int64_t s, int64_t ld, const float* v, bool ok) {
   const bool odd = threadIdx.x & 1;
   const int64_t s0 = s & ~(int64_t)1;
-#pragma unroll 8
-  for (int c = 0; c < width; c += 2) {
+#pragma unroll
+  for (int c = 0; c < kWidth; c += 2) {
     // even lane (sample s0) keeps v[c], sends v[c+1]; odd lane (s0 + 1) keeps v[c+1], sends v[c]
     const float mine = odd ? v[c + 1] : v[c];
     const float other = __shfl_xor_sync(0xffffffffu, odd ? v[c] : v[c + 1], 1);
@@ -1145,7 +1149,7 @@ __device__ __forceinline__ uint64_t fwd_relu(Slot& S, __half* save, int64_t s, b
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q) tc::st_row8(S.abuf, S.r, c0 + 8 * q, N, v + 8 * q);
-    store_fm_f16(save + (int64_t)c0 * ld, s, ld, 32, v, live);
+    store_fm_f16<32>(save + (int64_t)c0 * ld, s, ld, v, live);
   }
   return mask;
 }
@@ -1162,7 +1166,7 @@ __device__ __forceinline__ void bwd_relu(Slot& S, uint64_t mask, __half* save, i
       if (!((mask >> (c0 + i)) & 1ull)) v[i] = 0.0f;
 #pragma unroll
     for (int q = 0; q < 4; ++q) tc::st_row8(S.abuf, S.r, c0 + 8 * q, N, v + 8 * q);
-    store_fm_f16(save + (int64_t)c0 * ld, s, ld, 32, v, live);
+    store_fm_f16<32>(save + (int64_t)c0 * ld, s, ld, v, live);
   }
 }
 
@@ -1224,7 +1228,7 @@ __global__ void __launch_bounds__(kBwdSlots* kSlotThreads, 1)
     cin[31] = 0.0f;
 #pragma unroll
     for (int k0 = 0; k0 < 32; k0 += 8) tc::st_row8(S.abuf, S.r, k0, 32, cin + k0);
-    store_fm_f16(io.cin, s, ld, 32, cin, keep);
+    store_fm_f16<32>(io.cin, s, ld, cin, keep);
     run_layer(S, c1, 32, 64);
     const uint64_t m_c1 = fwd_relu<64>(S, io.c1, s, keep, ld);
     run_layer(S, c2, 64, 64);
@@ -1247,7 +1251,7 @@ __global__ void __launch_bounds__(kBwdSlots* kSlotThreads, 1)
     }
     tc::st_row8(S.abuf, S.r, 0, 16, d_o);
     tc::st_row8(S.abuf, S.r, 8, 16, d_o + 8);
-    store_fm_f16(io.d_o, s, ld, 16, d_o, keep);
+    store_fm_f16<16>(io.d_o, s, ld, d_o, keep);
     run_layer(S, t_c3, 16, 64);  // dC2act = dO . C3
     bwd_relu<64>(S, m_c2, io.dc2, s, keep, ld);
     run_layer(S, t_c2, 64, 64);  // dC1act = dC2 . C2
@@ -1261,7 +1265,7 @@ __global__ void __launch_bounds__(kBwdSlots* kSlotThreads, 1)
     for (int i = 1; i < 16; ++i) dg[i] = dcin[i - 1];
     tc::st_row8(S.abuf, S.r, 0, 16, dg);
     tc::st_row8(S.abuf, S.r, 8, 16, dg + 8);
-    store_fm_f16(io.dg, s, ld, 16, dg, keep);
+    store_fm_f16<16>(io.dg, s, ld, dg, keep);
     run_layer(S, t_g2, 16, 64);  // dH1act = dG . G2
     bwd_relu<64>(S, m_h1, io.dh1, s, keep, ld);
     run_layer(S, t_g1, 64, 32);  // dX0 = dH1 . G1
