@@ -643,7 +643,7 @@ __device__ __forceinline__ float4 canon_out(const cf_human_warp& W, d3 pt, float
 // pull 32-sample chunks from a ticket
 // (count[2]; per-chunk cost varies with the LBS fallback and the candidate-set
 // size), fetching the next ticket while the current chunk runs.
-template <int K, bool kBlock>
+template <int K, bool kBlock, bool kGrid = false>  // kGrid: the candidate-grid path only (the render)
 __global__ void __launch_bounds__(128, CF_CANON_MINB) human_canon_kernel(cf_march_desc M, const double* __restrict__ dirs,
                                                           const uint32_t* __restrict__ records,
                                                           int* count, int64_t capacity,
@@ -707,7 +707,7 @@ __global__ void __launch_bounds__(128, CF_CANON_MINB) human_canon_kernel(cf_marc
       near = d2 <= rsup2;
     }
     bool ed_ok;
-    if (kBlock && cgrid) {
+    if (kGrid || (kBlock && cgrid)) {
       // the cell's candidate list (cf_cand_grid_build): exact float64 ranking of the few
       // nodes that can be among the k nearest of any point of the cell
       ed_ok = false;
@@ -749,7 +749,7 @@ __global__ void __launch_bounds__(128, CF_CANON_MINB) human_canon_kernel(cf_marc
         }
         ed_ok = blend_apply<K>(top, s_dqs, W.k, W.r2, true, p, pt);
       }
-    } else {
+    } else if constexpr (!kGrid) {
       ed_ok = kBlock ? ed_warp_point_cull<K>(a64, a32, W.n_nodes, s_dqs, W.k, W.r2, true, p, near, pt)
                      : (live && ed_warp_point<K>(*EPp, ecs, es, W.dqs, W.k, W.r2, true, p, pt));
     }
@@ -1385,20 +1385,22 @@ int cf_human_canon(const cf_march_desc* M, const double* dirs, const cf_march_ou
   cudaStream_t st = cf::as_stream(stream);
   const size_t dsm = smem ? (size_t)(48 * W->n_nodes + 48 + 64 * W->n_nodes) : 0;  // anchor block + node dqs
   // persistent: exactly the resident CTAs (the ticket balances the work)
-#define CF_HC(KK, SM)                                                                                             \
+#define CF_HC(KK, SM, GR)                                                                                         \
   int per_sm = 0;                                                                                                \
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, human_canon_kernel<KK, SM>, 128, dsm);                  \
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, human_canon_kernel<KK, SM, GR>, 128, dsm);              \
   const unsigned grid = cf::grid_for(F->capacity, 128, per_sm > 0 ? per_sm : 1);                                 \
-  cf::launch_pdl(human_canon_kernel<KK, SM>, grid, 128, dsm, st, \
+  cf::launch_pdl(human_canon_kernel<KK, SM, GR>, grid, 128, dsm, st, \
       *M, dirs, F->records, F->counters, F->capacity, *W, anchor_buckets ? anchor_buckets->params : nullptr,    \
       anchor_buckets ? anchor_buckets->cell_start : nullptr, anchor_buckets ? anchor_buckets->sorted : nullptr, \
       lbs ? vert_buckets->params : nullptr, lbs ? vert_buckets->cell_start : nullptr,                            \
       lbs ? vert_buckets->sorted : nullptr, xu)
   dispatch_k(W->k, [&]<int K>() {
-    if (smem) {
-      CF_HC(K, true);
+    if (smem && W->cand_grid) {
+      CF_HC(K, true, true);
+    } else if (smem) {
+      CF_HC(K, true, false);
     } else {
-      CF_HC(K, false);
+      CF_HC(K, false, false);
     }
     return 0;
   });
