@@ -848,8 +848,20 @@ __global__ void __launch_bounds__(kPrecDeformSlots* kPrecDeformThreads, 1)
   const int64_t n = min((int64_t)*count, capacity);
   const int64_t n_tiles = (n + 127) / 128;
   const int64_t L = 128 * capacity;
-  for (int64_t tile = (int64_t)blockIdx.x * kPrecDeformSlots + S.slot; tile < n_tiles;
-       tile += (int64_t)gridDim.x * kPrecDeformSlots) {
+  // the render (kSave false): tiles taken from a ticket (counters[2]) instead of a fixed
+  // stride, so slots that start late (their SM still busy with the previous kernel or
+  // the object field) take fewer tiles; the last slot out re-arms counters[2..3]
+  constexpr bool kDyn = !kSave;
+  __shared__ int s_next[kPrecDeformSlots];
+  int* const ticket = const_cast<int*>(count) + 2;
+  const bool slot_lead = (threadIdx.x % S.nthreads) == 0;
+  int64_t tile = (int64_t)blockIdx.x * kPrecDeformSlots + S.slot;
+  if constexpr (kDyn) {
+    if (slot_lead) s_next[S.slot] = atomicAdd(ticket, 1);
+    tc::named_sync(1 + S.slot, S.nthreads);
+    tile = s_next[S.slot];
+  }
+  for (; tile < n_tiles;) {
     const int64_t s = tile * 128 + S.r;
     const bool live = s < n;
     // the sample's position (quarter 0: the output at the end of the tile; kHash: every
@@ -895,9 +907,11 @@ __global__ void __launch_bounds__(kPrecDeformSlots* kPrecDeformThreads, 1)
     uint32_t* mk = (kSave && live) ? save_mask + s * 16 + cq : nullptr;
 #pragma unroll 1
     for (int l = 0; l < 3; ++l) {
-      if (l == 0)
+      if (l == 0) {
         split_layer<32>(S, smem, lo, 128);
-      else
+        // every thread of the slot has read this tile's number: fetch the next one
+        if (kDyn && slot_lead) s_next[S.slot] = atomicAdd(ticket, 1);
+      } else
         split_layer<128>(S, smem + o2 + (l - 1) * (o3 - o2), lo + o2 + (l - 1) * (o3 - o2), 128);
       const uint32_t b = split_relu_q<kSave>(S, 32 * cq, l == 0 ? s_bias : nullptr, sv ? sv + l * L : nullptr, capacity);
       if (mk) mk[4 * l] = b;
@@ -938,6 +952,17 @@ __global__ void __launch_bounds__(kPrecDeformSlots* kPrecDeformThreads, 1)
         }
         xc[s] = p;
       }
+    }
+    if constexpr (kDyn)
+      tile = s_next[S.slot];  // written after this tile's first barrier
+    else
+      tile += (int64_t)gridDim.x * kPrecDeformSlots;
+  }
+  if (kDyn && slot_lead) {
+    __threadfence();
+    if (atomicAdd(ticket + 1, 1) == (int)(gridDim.x * kPrecDeformSlots) - 1) {
+      ticket[0] = 0;
+      ticket[1] = 0;
     }
   }
   pdl_trigger();
@@ -1005,8 +1030,18 @@ __global__ void __launch_bounds__(kColorPrecSlots* kSlotThreads, 1)
   constexpr int g1 = 0, g2 = 64 * 32 * 2, c1 = g2 + 16 * 64 * 2, c2 = c1 + 64 * 32 * 2;
   const int64_t n = min((int64_t)*count, capacity);
   const int64_t n_tiles = (n + 127) / 128;
-  for (int64_t tile = (int64_t)blockIdx.x * kColorPrecSlots + S.slot; tile < n_tiles;
-       tile += (int64_t)gridDim.x * kColorPrecSlots) {
+  // the render's fused instance: tiles from a ticket (counters[2]), as DeformNet's
+  constexpr bool kDyn = kHashCH > 0;
+  __shared__ int s_next[kColorPrecSlots];
+  int* const ticket = const_cast<int*>(count) + 2;
+  const bool slot_lead = (threadIdx.x % S.nthreads) == 0;
+  int64_t tile = (int64_t)blockIdx.x * kColorPrecSlots + S.slot;
+  if constexpr (kDyn) {
+    if (slot_lead) s_next[S.slot] = atomicAdd(ticket, 1);
+    tc::named_sync(1 + S.slot, S.nthreads);
+    tile = s_next[S.slot];
+  }
+  for (; tile < n_tiles;) {
     const int64_t s = tile * 128 + S.r;
     const bool live = s < n;
     {
@@ -1041,6 +1076,7 @@ __global__ void __launch_bounds__(kColorPrecSlots* kSlotThreads, 1)
       ddz = dirs[3 * ray + 2];
     }
     split_layer<32>(S, smem + g1, lo + g1, 64);
+    if (kDyn && slot_lead) s_next[S.slot] = atomicAdd(ticket, 1);  // all have read this tile's
     split_relu32(S, 0);
     split_relu32(S, 32);
     split_layer<64>(S, smem + g2, lo + g2, 16);
@@ -1079,6 +1115,17 @@ __global__ void __launch_bounds__(kColorPrecSlots* kSlotThreads, 1)
       const float r = 1.0f / (1.0f + expf(-cv[0])), g = 1.0f / (1.0f + expf(-cv[1])),
                   b = 1.0f / (1.0f + expf(-cv[2]));
       out[s] = valid ? make_float4(sigma, r, g, b) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    if constexpr (kDyn)
+      tile = s_next[S.slot];
+    else
+      tile += (int64_t)gridDim.x * kColorPrecSlots;
+  }
+  if (kDyn && slot_lead) {
+    __threadfence();
+    if (atomicAdd(ticket + 1, 1) == (int)(gridDim.x * kColorPrecSlots) - 1) {
+      ticket[0] = 0;
+      ticket[1] = 0;
     }
   }
   tc::fence_before();
