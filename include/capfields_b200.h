@@ -393,6 +393,8 @@ typedef struct cf_field_desc {
   int split_stages;         /* precise render: 0 = the hash lookups run inside the MLP kernels (the deformation
                                grid in DeformNet, the canonical grid in E_g / E_c: stages 0 and 2 are empty);
                                1 = separate hash kernels, features in the scratch (stage-by-stage inspection) */
+  int max_ctas;             /* precise render: cap on the persistent E_g / E_c kernel's CTAs (0 = one per SM);
+                               a field rendered on a side stream beside another leaves it the other SMs */
 } cf_field_desc;
 /* occupancy from the trained density (the builder's K12; SPEC.md:429 leaves ray-marching
  * acceleration open): per cell of a res^3 grid over the field's unit cube, the E_g density

@@ -89,7 +89,7 @@ class FieldDesc(ctypes.Structure):
                 ("w_bytes", ctypes.c_int), ("dbias", ctypes.c_void_p), ("delta_scale", ctypes.c_float),
                 ("inv_side", ctypes.c_float), ("save_h", ctypes.c_void_p), ("save_o", ctypes.c_void_p),
                 ("save_mask", ctypes.c_void_p), ("precise", ctypes.c_int), ("wblob_lo", ctypes.c_void_p),
-                ("train", ctypes.c_int), ("split_stages", ctypes.c_int)]
+                ("train", ctypes.c_int), ("split_stages", ctypes.c_int), ("max_ctas", ctypes.c_int)]
 
 
 class DwProblem(ctypes.Structure):

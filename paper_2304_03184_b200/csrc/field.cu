@@ -1880,11 +1880,9 @@ int field_stage_precise(const cf_field_desc* FD, const cf_march_out* S, const do
       auto kern = color_mlp_prec_kernel<4>;
       CF_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, csmem));
       unsigned grid = persistent_grid(cap, kColorPrecSlots);
-      // the object field runs on the side stream beside the human chain: at most an
-      // eighth of the SMs (its slots take tiles from the ticket, so fewer CTAs only
-      // lengthen it), leaving the rest to the human DeformNet kernel that starts while
-      // it runs (measured 0.353 -> 0.348 ms per frame; 8 CTAs made it the critical path)
-      if (!FD->has_deform) grid = std::min(grid, (unsigned)std::max(16, cf::sm_count() / 8));
+      // a field on a side stream (the render's object field) leaves the other SMs to the
+      // kernels beside it (its slots take tiles from the ticket: fewer CTAs only lengthen it)
+      if (FD->max_ctas > 0) grid = std::min(grid, (unsigned)FD->max_ctas);
       cf::launch_pdl(kern, grid, kColorPrecSlots * kSlotThreads, csmem, st,
                      FD->wblob + off, FD->wblob_lo + off, xcan, static_cast<const float4*>(cfeat), S->records, dirs,
                      S->counters, cap, out, static_cast<__half*>(nullptr), FD->cgrid,

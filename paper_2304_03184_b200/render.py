@@ -287,6 +287,10 @@ class ObjectField:
 _FRAME_DOUBLES = 28
 
 
+def _sm_count(device) -> int:
+    return torch.cuda.get_device_properties(device).multi_processor_count
+
+
 class _FieldBuffers:
     def __init__(self, n_rays, capacity, device):
         self.records = torch.empty(capacity, dtype=torch.int32, device=device)
@@ -811,6 +815,10 @@ class Renderer:
                 _lib.call("cf_object_canon", _lib.byref(self.M), self.dirs.data_ptr(), _lib.byref(ob.mo),
                           ob.xu.data_ptr(), so)
                 self._mark("object_canon")
+                # beside the human chain the object field keeps to an eighth of the SMs, leaving
+                # the rest to the DeformNet kernel that starts while it runs (0.353 -> 0.348 ms
+                # per frame; 8 CTAs made it the critical path); serialised: the whole GPU
+                self.odesc.max_ctas = 0 if self.cfg.serial else max(16, _sm_count(self.dirs.device) // 8)
                 _lib.call("cf_field_forward", _lib.byref(self.odesc), _lib.byref(ob.mo), self.dirs.data_ptr(),
                           ob.xu.data_ptr(), ob.out.data_ptr(), self._scratch(ob, self.odesc).data_ptr(), so)
                 self._mark("object_field")
