@@ -176,22 +176,28 @@ struct DwGroup {
   int64_t capacity;
 };
 
+// A stage holds kDwBoxes consecutive 64-wide K boxes of each operand, loaded back to
+// back: every operand row (one feature, K contiguous) is then read kDwBoxes x 128 B at
+// a time instead of 128 B per stage period (DRAM row-buffer locality).
+constexpr int kDwBoxes = 2, kDwStages = kGStages / kDwBoxes, kDwKT = kGKT * kDwBoxes;
+constexpr int kDwBox = 128 * kGKT * 2;  // one 64 x 128-row box, 16 KB
+
 __global__ void __launch_bounds__(128, 1) dw_grouped_kernel(const __grid_constant__ DwGroup G) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t full[kGStages], empty[kGStages], done;
+  __shared__ uint64_t full[kDwStages], empty[kDwStages], done;
   __shared__ uint32_t tmem_base;
   const DwProb& P = G.p[blockIdx.y];
   const int N = P.n_mma;
-  constexpr int kStageA = 128 * kGKT * 2, kStage = kStageA + 128 * kGKT * 2;
-  const uint32_t tx = (uint32_t)(kStageA + N * kGKT * 2);
+  constexpr int kStageA = kDwBoxes * kDwBox, kStage = 2 * kStageA;
+  const uint32_t tx = (uint32_t)(kDwBox + N * kGKT * 2);  // one box pair
   const int tid = threadIdx.x, warp = tid / 32;
   const int64_t K = min((int64_t)*G.count, G.capacity);
-  const int64_t T = (K + kGKT - 1) / kGKT;
+  const int64_t T = (K + kDwKT - 1) / kDwKT;
   const int64_t per = (T + gridDim.x - 1) / gridDim.x;
   const int64_t t0 = (int64_t)blockIdx.x * per, nt = max((int64_t)0, min(per, T - t0));
   if (nt == 0) return;
   if (tid == 0) {
-    for (int q = 0; q < kGStages; ++q) {
+    for (int q = 0; q < kDwStages; ++q) {
       tc::bar_init(&full[q], 1);
       tc::bar_init(&empty[q], 1);
     }
@@ -203,27 +209,37 @@ __global__ void __launch_bounds__(128, 1) dw_grouped_kernel(const __grid_constan
   __syncthreads();
   tc::fence_after();
   const uint32_t sbase = tc::smem_u32(smem);
+  // boxes of the stage that hold columns < roundup(K, 64) (the caller's zero-padded range)
+  auto nbox = [&](int64_t i) {
+    const int64_t k0 = (t0 + i) * kDwKT;
+    return (int)min((int64_t)kDwBoxes, (K - k0 + kGKT - 1) / kGKT);
+  };
   if (tid == 0) {
     for (int64_t i = 0; i < nt; ++i) {
-      const int st = (int)(i % kGStages);
-      if (i >= kGStages) tc::bar_wait(&empty[st], (uint32_t)(((i / kGStages) - 1) & 1));
-      bar_expect_tx(&full[st], tx);
-      const int k0 = (int)((t0 + i) * kGKT);
+      const int st = (int)(i % kDwStages);
+      if (i >= kDwStages) tc::bar_wait(&empty[st], (uint32_t)(((i / kDwStages) - 1) & 1));
+      const int nb = nbox(i);
+      bar_expect_tx(&full[st], tx * (uint32_t)nb);
+      const int k0 = (int)((t0 + i) * kDwKT);
       const uint32_t sa = sbase + st * kStage, sb = sa + kStageA;
-      tma_load_2d(sa, &P.a, k0, 0, &full[st]);
-      tma_load_2d(sb, &P.b, k0, 0, &full[st]);
+      for (int b = 0; b < nb; ++b) {
+        tma_load_2d(sa + b * kDwBox, &P.a, k0 + b * kGKT, 0, &full[st]);
+        tma_load_2d(sb + b * kDwBox, &P.b, k0 + b * kGKT, 0, &full[st]);
+      }
     }
   } else if (tid == 32) {
     const uint32_t idesc = tc::idesc_f16(128, N);
     for (int64_t i = 0; i < nt; ++i) {
-      const int st = (int)(i % kGStages);
-      tc::bar_wait(&full[st], (uint32_t)((i / kGStages) & 1));
+      const int st = (int)(i % kDwStages);
+      tc::bar_wait(&full[st], (uint32_t)((i / kDwStages) & 1));
       tc::fence_after();
       const uint32_t sa = sbase + st * kStage, sb = sa + kStageA;
+      const int nb = nbox(i);
+      for (int b = 0; b < nb; ++b)
 #pragma unroll
-      for (int ks = 0; ks < kGKT / 16; ++ks)
-        tc::mma_f16(tmem_base, sdesc_sw128(sa + ks * 32), sdesc_sw128(sb + ks * 32), idesc,
-                    (i > 0 || ks > 0) ? 1u : 0u);
+        for (int ks = 0; ks < kGKT / 16; ++ks)
+          tc::mma_f16(tmem_base, sdesc_sw128(sa + b * kDwBox + ks * 32), sdesc_sw128(sb + b * kDwBox + ks * 32),
+                      idesc, (i > 0 || b > 0 || ks > 0) ? 1u : 0u);
       tc::mma_commit(&empty[st]);
     }
     tc::mma_commit(&done);
@@ -483,9 +499,9 @@ int cf_dw_grouped(const cf_dw_problem* probs, int n, const int* count, int64_t c
     P.m = q.m;
     P.n = q.n;
   }
-  const int64_t T = (capacity + kGKT - 1) / kGKT;
+  const int64_t T = (capacity + kDwKT - 1) / kDwKT;
   const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(T, cf::sm_count()));
-  const int smem = kGStages * 2 * 128 * kGKT * 2;
+  const int smem = kDwStages * 2 * kDwBoxes * kDwBox;
   CF_CHECK_CUDA(cudaFuncSetAttribute(dw_grouped_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   dw_grouped_kernel<<<dim3(gx, (unsigned)n), 128, smem, cf::as_stream(stream)>>>(G);
   return cf::check_launch("cf_dw_grouped");
