@@ -516,21 +516,23 @@ int cf_adam(float* p, const float* g, float* m, float* v, int64_t n, float lr, f
 int cf_gemm_kmajor_f16(const void* A, int64_t lda, const void* B, int64_t ldb, int n_cols, int64_t K, float* C,
                        int ldc, void* stream);
 /* ---- the training step's device-side control (graph-capturable: no host syncs) */
-/* one weight-gradient problem: C[m x n] += A[m x K] B[n x K]^T, A / B fp16 K-major (the
- * feature-major saves: row stride lda / ldb elements, 16-byte aligned rows), C fp32
- * row-major (ldc); m, n in 1..128 */
+/* one weight-gradient problem: C[m x n] += A[m x K] B[n x K]^T, A / B fp16 K-blocked
+ * feature-major (the training saves): a matrix of a_rows (b_rows) rows stored as
+ * capacity / 64 blocks of (rows, 64), element (r, k) at ((k / 64) * rows + r) * 64 + k % 64,
+ * 16-byte aligned; the first m (n) rows are the operand; C fp32 row-major (ldc);
+ * m, n in 1..128 */
 typedef struct cf_dw_problem {
   const void* A;
-  int64_t lda;
+  int64_t a_rows;
   int m;
   const void* B;
-  int64_t ldb;
+  int64_t b_rows;
   int n;
   float* C;
   int ldc;
 } cf_dw_problem;
-/* up to 10 problems in one tcgen05 launch, K = min(*count, capacity) read on the
- * device (the frame's sample count); the operands' columns K .. roundup(K, 64) must be
+/* up to 10 problems in one tcgen05 launch (capacity % 64 == 0), K = min(*count, capacity)
+ * read on the device (the frame's sample count); the operands' columns K .. roundup(K, 64) must be
  * finite with zero in A or B (the training kernels write every lane of a tile) */
 int cf_dw_grouped(const cf_dw_problem* problems, int n, const int* count, int64_t capacity, void* stream);
 /* masked / depth-valid ray counts of n_frames key-frame batches (frame f's rays at

@@ -93,8 +93,8 @@ class FieldDesc(ctypes.Structure):
 
 
 class DwProblem(ctypes.Structure):
-    _fields_ = [("A", ctypes.c_void_p), ("lda", ctypes.c_int64), ("m", ctypes.c_int), ("B", ctypes.c_void_p),
-                ("ldb", ctypes.c_int64), ("n", ctypes.c_int), ("C", ctypes.c_void_p), ("ldc", ctypes.c_int)]
+    _fields_ = [("A", ctypes.c_void_p), ("a_rows", ctypes.c_int64), ("m", ctypes.c_int),
+                ("B", ctypes.c_void_p), ("b_rows", ctypes.c_int64), ("n", ctypes.c_int), ("C", ctypes.c_void_p), ("ldc", ctypes.c_int)]
 
 
 class AdamTensor(ctypes.Structure):

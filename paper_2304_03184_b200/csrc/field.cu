@@ -283,6 +283,13 @@ __device__ __forceinline__ void ts_layer(TsSlot& S, const uint8_t* w, int K, int
   tc::fence_after();
 }
 
+// The training saves (the dW GEMMs' operands) are K-blocked feature-major: a (rows, S)
+// fp16 matrix stored as S / 64 blocks of (rows, 64), element (c, s) at
+// kb_col(s, rows) + 64 c — one dW TMA box (64 samples x the operand's rows) is then one
+// contiguous run of HBM instead of a 128-byte piece of every feature row.
+__device__ __forceinline__ int64_t kb_col(int64_t s, int rows) { return (s >> 6) * rows * 64 + (s & 63); }
+constexpr int64_t kKbLd = 64;  // column stride inside a block
+
 // Store this thread's 32 fp16 values (16 packed pairs, columns col .. col+31) into a
 // column-major (feature-major) matrix: column c of the sample at dst[c * ld]. Lanes
 // are consecutive samples, so every store is a coalesced 64-byte warp segment.
@@ -892,19 +899,20 @@ __global__ void __launch_bounds__(kPrecDeformSlots* kPrecDeformThreads, 1)
       tc::tmem_st4(S.ahi + (uint32_t)(4 * cq), h);
       tc::tmem_st4(S.alo + (uint32_t)(4 * cq), l);
       if (kSave && s < capacity) {
-        // feature-major (33, capacity): this quarter's 8 feature rows, + row 32 = 1 (the
+        // K-blocked (33, capacity): this quarter's 8 feature rows, + row 32 = 1 (the
         // layer-1 dW GEMM's extra column: sum_s dpre1, for the pose columns)
-        uint16_t* d16 = reinterpret_cast<uint16_t*>(dfeat16);
+        uint16_t* d16 = reinterpret_cast<uint16_t*>(dfeat16) + kb_col(s, 33);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          d16[(int64_t)(8 * cq + 2 * i) * capacity + s] = (uint16_t)(h[i] & 0xffffu);
-          d16[(int64_t)(8 * cq + 2 * i + 1) * capacity + s] = (uint16_t)(h[i] >> 16);
+          d16[(8 * cq + 2 * i) * kKbLd] = (uint16_t)(h[i] & 0xffffu);
+          d16[(8 * cq + 2 * i + 1) * kKbLd] = (uint16_t)(h[i] >> 16);
         }
-        if (cq == 0) d16[32 * capacity + s] = 0x3C00u;  // 1.0
+        if (cq == 0) d16[32 * kKbLd] = 0x3C00u;  // 1.0
       }
     }
-    // training saves: h feature-major (512, capacity), ReLU bits [layer][32-column word] per sample
-    __half* sv = (kSave && s < capacity) ? save_h + s : nullptr;
+    // training saves: h as four K-blocked (128, capacity) matrices, ReLU bits
+    // [layer][32-column word] per sample
+    __half* sv = (kSave && s < capacity) ? save_h + kb_col(s, 128) : nullptr;
     uint32_t* mk = (kSave && live) ? save_mask + s * 16 + cq : nullptr;
 #pragma unroll 1
     for (int l = 0; l < 3; ++l) {
@@ -914,13 +922,13 @@ __global__ void __launch_bounds__(kPrecDeformSlots* kPrecDeformThreads, 1)
         if (kDyn && slot_lead) s_next[S.slot] = atomicAdd(ticket, 1);
       } else
         split_layer<128>(S, smem + o2 + (l - 1) * (o3 - o2), lo + o2 + (l - 1) * (o3 - o2), 128);
-      const uint32_t b = split_relu_q<kSave>(S, 32 * cq, l == 0 ? s_bias : nullptr, sv ? sv + l * L : nullptr, capacity);
+      const uint32_t b = split_relu_q<kSave>(S, 32 * cq, l == 0 ? s_bias : nullptr, sv ? sv + l * L : nullptr, kKbLd);
       if (mk) mk[4 * l] = b;
     }
     split_layer<128>(S, smem + o4, lo + o4, 128);
     float part[3];
     {
-      const uint32_t b = relu_dot3_q<kSave>(S, 32 * cq, s_w5, part, sv ? sv + 3 * L : nullptr, capacity);
+      const uint32_t b = relu_dot3_q<kSave>(S, 32 * cq, s_w5, part, sv ? sv + 3 * L : nullptr, kKbLd);
       if (mk) mk[12] = b;
     }
     // the four quarters' partials summed as (p0 + p2) + (p1 + p3), in two exchanges: the
@@ -1063,9 +1071,10 @@ __global__ void __launch_bounds__(kColorPrecSlots* kSlotThreads, 1)
       }
       uint32_t hi[16];
       split_store<8>(S, f, 0, cfeat16 ? hi : nullptr);
-      if (cfeat16 && s < capacity) {  // training: the features' fp16 halves, feature-major (32, capacity)
-        store_cols16_f16(reinterpret_cast<uint16_t*>(cfeat16), capacity, s, 0, hi);
-        store_cols16_f16(reinterpret_cast<uint16_t*>(cfeat16), capacity, s, 16, hi + 8);
+      if (cfeat16 && s < capacity) {  // training: the features' fp16 halves, K-blocked (32, capacity)
+        uint16_t* d16 = reinterpret_cast<uint16_t*>(cfeat16) + kb_col(s, 32);
+        store_cols16_f16(d16, kKbLd, 0, 0, hi);
+        store_cols16_f16(d16, kKbLd, 0, 16, hi + 8);
       }
     }
     const bool valid = live && xu[s].w > 0.0f;
@@ -1168,23 +1177,24 @@ struct ColorBwdIO {
 // partial unroll, v[] was indexed at run time and lived in local memory — 256 bytes of
 // stack per thread in the colour backward)
 template <int kWidth>
-__device__ __forceinline__ void store_fm_f16(__half* dst, int64_t s, int64_t ld, const float* v, bool ok) {
+__device__ __forceinline__ void store_fm_f16(__half* dst, int64_t s, int rows, const float* v, bool ok) {
   const bool odd = threadIdx.x & 1;
   const int64_t s0 = s & ~(int64_t)1;
+  dst += kb_col(s0, rows);  // s0, s0 + 1: adjacent in one block
 #pragma unroll
   for (int c = 0; c < kWidth; c += 2) {
     // even lane (sample s0) keeps v[c], sends v[c+1]; odd lane (s0 + 1) keeps v[c+1], sends v[c]
     const float mine = odd ? v[c + 1] : v[c];
     const float other = __shfl_xor_sync(0xffffffffu, odd ? v[c] : v[c + 1], 1);
     const __half2 h = odd ? __floats2half2_rn(other, mine) : __floats2half2_rn(mine, other);
-    if (ok) *reinterpret_cast<__half2*>(dst + (int64_t)(c + (odd ? 1 : 0)) * ld + s0) = h;
+    if (ok) *reinterpret_cast<__half2*>(dst + (c + (odd ? 1 : 0)) * kKbLd) = h;
   }
 }
 
 // forward hidden layer with ReLU: keep the activation mask, write fp16 to A buffer (+ the
 // feature-major HBM copy, row stride ld)
 template <int N>
-__device__ __forceinline__ uint64_t fwd_relu(Slot& S, __half* save, int64_t s, bool live, int64_t ld) {
+__device__ __forceinline__ uint64_t fwd_relu(Slot& S, __half* save, int64_t s, bool live) {
   uint64_t mask = 0;
 #pragma unroll
   for (int c0 = 0; c0 < N; c0 += 32) {
@@ -1197,14 +1207,14 @@ __device__ __forceinline__ uint64_t fwd_relu(Slot& S, __half* save, int64_t s, b
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q) tc::st_row8(S.abuf, S.r, c0 + 8 * q, N, v + 8 * q);
-    store_fm_f16<32>(save + (int64_t)c0 * ld, s, ld, v, live);
+    store_fm_f16<32>(save + c0 * kKbLd, s, N, v, live);
   }
   return mask;
 }
 
 // backward through a ReLU layer: dpre = dact (from TMEM) * relu'(mask) -> A buffer (+ HBM)
 template <int N>
-__device__ __forceinline__ void bwd_relu(Slot& S, uint64_t mask, __half* save, int64_t s, bool live, int64_t ld) {
+__device__ __forceinline__ void bwd_relu(Slot& S, uint64_t mask, __half* save, int64_t s, bool live) {
 #pragma unroll
   for (int c0 = 0; c0 < N; c0 += 32) {
     float v[32];
@@ -1214,7 +1224,7 @@ __device__ __forceinline__ void bwd_relu(Slot& S, uint64_t mask, __half* save, i
       if (!((mask >> (c0 + i)) & 1ull)) v[i] = 0.0f;
 #pragma unroll
     for (int q = 0; q < 4; ++q) tc::st_row8(S.abuf, S.r, c0 + 8 * q, N, v + 8 * q);
-    store_fm_f16<32>(save + (int64_t)c0 * ld, s, ld, v, live);
+    store_fm_f16<32>(save + c0 * kKbLd, s, N, v, live);
   }
 }
 
@@ -1240,11 +1250,10 @@ __global__ void __launch_bounds__(kBwdSlots* kSlotThreads, 1)
   for (int64_t tile = (int64_t)blockIdx.x * kBwdSlots + S.slot; tile < n_tiles; tile += (int64_t)gridDim.x * kBwdSlots) {
     const int64_t s = tile * 128 + S.r;
     const bool live = s < n;
-    // the saves (feature-major, row stride = capacity) are written for every lane of
-    // the tile inside the capacity: the dW GEMMs' last K tile reads past n, where the
-    // dead lanes' dL/d terms are zero and their activations finite
+    // the saves (K-blocked feature-major, kb_col) are written for every lane of the
+    // tile inside the capacity: the dW GEMMs' last K tile reads past n, where the dead
+    // lanes' dL/d terms are zero and their activations finite
     const bool keep = s < capacity;
-    const int64_t ld = capacity;
     const bool valid = live && xu[s].w > 0.0f;
     // ---- forward recompute from the features (the training forward's fp32 features,
     // sample-major: 8 vector loads; st_row8 rounds them to the same fp16 values the
@@ -1257,7 +1266,7 @@ __global__ void __launch_bounds__(kBwdSlots* kSlotThreads, 1)
       for (int k0 = 0; k0 < 32; k0 += 8) tc::st_row8(S.abuf, S.r, k0, 32, reinterpret_cast<const float*>(x) + k0);
     }
     run_layer(S, g1, 32, 64);
-    const uint64_t m_h1 = fwd_relu<64>(S, io.h1, s, keep, ld);
+    const uint64_t m_h1 = fwd_relu<64>(S, io.h1, s, keep);
     run_layer(S, g2, 64, 16);
     float gv[16];
     tc::tmem_ld16(S.tmem_row, gv);
@@ -1276,11 +1285,11 @@ __global__ void __launch_bounds__(kBwdSlots* kSlotThreads, 1)
     cin[31] = 0.0f;
 #pragma unroll
     for (int k0 = 0; k0 < 32; k0 += 8) tc::st_row8(S.abuf, S.r, k0, 32, cin + k0);
-    store_fm_f16<32>(io.cin, s, ld, cin, keep);
+    store_fm_f16<32>(io.cin, s, 32, cin, keep);
     run_layer(S, c1, 32, 64);
-    const uint64_t m_c1 = fwd_relu<64>(S, io.c1, s, keep, ld);
+    const uint64_t m_c1 = fwd_relu<64>(S, io.c1, s, keep);
     run_layer(S, c2, 64, 64);
-    const uint64_t m_c2 = fwd_relu<64>(S, io.c2, s, keep, ld);
+    const uint64_t m_c2 = fwd_relu<64>(S, io.c2, s, keep);
     run_layer(S, c3, 64, 16);
     float ov[16];
     tc::tmem_ld16(S.tmem_row, ov);
@@ -1299,11 +1308,11 @@ __global__ void __launch_bounds__(kBwdSlots* kSlotThreads, 1)
     }
     tc::st_row8(S.abuf, S.r, 0, 16, d_o);
     tc::st_row8(S.abuf, S.r, 8, 16, d_o + 8);
-    store_fm_f16<16>(io.d_o, s, ld, d_o, keep);
+    store_fm_f16<16>(io.d_o, s, 16, d_o, keep);
     run_layer(S, t_c3, 16, 64);  // dC2act = dO . C3
-    bwd_relu<64>(S, m_c2, io.dc2, s, keep, ld);
+    bwd_relu<64>(S, m_c2, io.dc2, s, keep);
     run_layer(S, t_c2, 64, 64);  // dC1act = dC2 . C2
-    bwd_relu<64>(S, m_c1, io.dc1, s, keep, ld);
+    bwd_relu<64>(S, m_c1, io.dc1, s, keep);
     run_layer(S, t_c1, 64, 32);  // dCin = dC1 . C1
     float dcin[32];
     tc::tmem_ld32(S.tmem_row, dcin);
@@ -1313,9 +1322,9 @@ __global__ void __launch_bounds__(kBwdSlots* kSlotThreads, 1)
     for (int i = 1; i < 16; ++i) dg[i] = dcin[i - 1];
     tc::st_row8(S.abuf, S.r, 0, 16, dg);
     tc::st_row8(S.abuf, S.r, 8, 16, dg + 8);
-    store_fm_f16<16>(io.dg, s, ld, dg, keep);
+    store_fm_f16<16>(io.dg, s, 16, dg, keep);
     run_layer(S, t_g2, 16, 64);  // dH1act = dG . G2
-    bwd_relu<64>(S, m_h1, io.dh1, s, keep, ld);
+    bwd_relu<64>(S, m_h1, io.dh1, s, keep);
     run_layer(S, t_g1, 64, 32);  // dX0 = dH1 . G1
     float dfx[32];
     tc::tmem_ld32(S.tmem_row, dfx);
@@ -1531,11 +1540,12 @@ __global__ void __launch_bounds__(kDBwdSlots* kDeformSlotThreads, 1)
       } else {
         tc::tmem_st8(S.a, h);
       }
-      if (s < capacity) {  // feature-major (16, capacity); dead lanes write zeros
+      if (s < capacity) {  // K-blocked (16, capacity); dead lanes write zeros
+        __half* d = d_o_out + kb_col(s, 16);
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          d_o_out[(int64_t)(2 * i) * capacity + s] = __ushort_as_half((uint16_t)(h[i] & 0xffffu));
-          d_o_out[(int64_t)(2 * i + 1) * capacity + s] = __ushort_as_half((uint16_t)(h[i] >> 16));
+          d[(2 * i) * kKbLd] = __ushort_as_half((uint16_t)(h[i] & 0xffffu));
+          d[(2 * i + 1) * kKbLd] = __ushort_as_half((uint16_t)(h[i] >> 16));
         }
       }
     }
@@ -1548,18 +1558,18 @@ __global__ void __launch_bounds__(kDBwdSlots* kDeformSlotThreads, 1)
         mk[l] = (uint64_t)v.x | (uint64_t)v.y << 32;
       }
     }
-    // dpre1..4 feature-major: (512, capacity), row = layer * 128 + column; dead lanes
+    // dpre1..4: four K-blocked (128, capacity) matrices (layer l at dpre + l * L); dead lanes
     // of the tile (mask 0) write zeros, read by the dW GEMMs' last K tile
-    __half* dp = s < capacity ? dpre + s : nullptr;
+    __half* dp = s < capacity ? dpre + kb_col(s, 128) : nullptr;
     const int64_t L = 128 * capacity;
     ts_layer(S, smem + t5, 16, 128);  // dh4 = d_o . W5
-    ts_bwd_mask128(S, mk[3], dp ? dp + 3 * L : nullptr, capacity);
+    ts_bwd_mask128(S, mk[3], dp ? dp + 3 * L : nullptr, kKbLd);
     ts_layer(S, smem + t4, 128, 128);  // dh3 = dpre4 . W4
-    ts_bwd_mask128(S, mk[2], dp ? dp + 2 * L : nullptr, capacity);
+    ts_bwd_mask128(S, mk[2], dp ? dp + 2 * L : nullptr, kKbLd);
     ts_layer(S, smem + t3, 128, 128);  // dh2 = dpre3 . W3
-    ts_bwd_mask128(S, mk[1], dp ? dp + L : nullptr, capacity);
+    ts_bwd_mask128(S, mk[1], dp ? dp + L : nullptr, kKbLd);
     ts_layer(S, smem + t2, 128, 128);  // dh1 = dpre2 . W2
-    ts_bwd_mask128(S, mk[0], dp, capacity);
+    ts_bwd_mask128(S, mk[0], dp, kKbLd);
     ts_layer(S, smem + t1, 128, 32);  // dL/dfeat = dpre1 . W1x
     if (S.half == 0) {
       float dfx[32];

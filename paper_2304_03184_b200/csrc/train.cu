@@ -62,6 +62,14 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(tc::smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int x, int y, int z,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+          "r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(tc::smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void bar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tc::smem_u32(bar)), "r"(bytes)
                : "memory");
@@ -222,9 +230,9 @@ __global__ void __launch_bounds__(128, 1) dw_grouped_kernel(const __grid_constan
       bar_expect_tx(&full[st], tx * (uint32_t)nb);
       const int k0 = (int)((t0 + i) * kDwKT);
       const uint32_t sa = sbase + st * kStage, sb = sa + kStageA;
-      for (int b = 0; b < nb; ++b) {
-        tma_load_2d(sa + b * kDwBox, &P.a, k0 + b * kGKT, 0, &full[st]);
-        tma_load_2d(sb + b * kDwBox, &P.b, k0 + b * kGKT, 0, &full[st]);
+      for (int b = 0; b < nb; ++b) {  // K-blocked operands: block k0 / 64 + b, all rows
+        tma_load_3d(sa + b * kDwBox, &P.a, 0, 0, k0 / kGKT + b, &full[st]);
+        tma_load_3d(sb + b * kDwBox, &P.b, 0, 0, k0 / kGKT + b, &full[st]);
       }
     }
   } else if (tid == 32) {
@@ -444,6 +452,21 @@ bool make_map(CUtensorMap* map, const void* base, int rows, int64_t K, int64_t l
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// the K-blocked operand of cf_dw_grouped: a (rows_stored, K) fp16 matrix as K / 64
+// blocks of (rows_stored, 64); the map exposes its first `rows` rows (rows beyond them,
+// up to the box, read as zeros) and a box of 64 x box_rows x 1 block, 128-byte swizzle
+bool make_map_kb(CUtensorMap* map, const void* base, int rows, int64_t rows_stored, int64_t K, int box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[3] = {64, (cuuint64_t)rows, (cuuint64_t)(K / 64)};
+  const cuuint64_t strides[2] = {128, (cuuint64_t)rows_stored * 128};
+  const cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace
 
 extern "C" {
@@ -479,20 +502,21 @@ int cf_dw_grouped(const cf_dw_problem* probs, int n, const int* count, int64_t c
   if (!probs || n < 1 || n > kMaxDw || !count || capacity < 0)
     return cf::fail(CF_E_BAD_ARG, "cf_dw_grouped: bad args (1..10 problems, count, capacity)");
   if (capacity == 0) return CF_OK;
-  if (capacity >= (int64_t)1 << 31) return cf::fail(CF_E_BAD_ARG, "cf_dw_grouped: capacity must be < 2^31");
+  if (capacity >= (int64_t)1 << 31 || capacity % 64 != 0)
+    return cf::fail(CF_E_BAD_ARG, "cf_dw_grouped: capacity must be a multiple of 64 below 2^31");
   DwGroup G{};
   G.count = count;
   G.capacity = capacity;
   for (int i = 0; i < n; ++i) {
     const cf_dw_problem& q = probs[i];
-    if (!q.A || !q.B || !q.C || q.m < 1 || q.m > 128 || q.n < 1 || q.n > 128 || q.lda < capacity ||
-        q.ldb < capacity || q.ldc < q.n)
-      return cf::fail(CF_E_BAD_ARG, "cf_dw_grouped: problem shape (m, n in 1..128, lda/ldb >= capacity)");
-    if ((q.lda | q.ldb) % 8 != 0 || (reinterpret_cast<uintptr_t>(q.A) | reinterpret_cast<uintptr_t>(q.B)) % 16 != 0)
-      return cf::fail(CF_E_BAD_ARG, "cf_dw_grouped: operands need 16-byte aligned rows");
+    if (!q.A || !q.B || !q.C || q.m < 1 || q.m > 128 || q.n < 1 || q.n > 128 || q.a_rows < q.m ||
+        q.b_rows < q.n || q.ldc < q.n)
+      return cf::fail(CF_E_BAD_ARG, "cf_dw_grouped: problem shape (m, n in 1..128, a_rows >= m, b_rows >= n)");
+    if ((reinterpret_cast<uintptr_t>(q.A) | reinterpret_cast<uintptr_t>(q.B)) % 16 != 0)
+      return cf::fail(CF_E_BAD_ARG, "cf_dw_grouped: operands need 16-byte alignment");
     DwProb& P = G.p[i];
     P.n_mma = (q.n + 15) / 16 * 16;
-    if (!make_map(&P.a, q.A, q.m, capacity, q.lda, 128) || !make_map(&P.b, q.B, q.n, capacity, q.ldb, P.n_mma))
+    if (!make_map_kb(&P.a, q.A, q.m, q.a_rows, capacity, 128) || !make_map_kb(&P.b, q.B, q.n, q.b_rows, capacity, P.n_mma))
       return cf::fail(CF_E_CUDA, "cf_dw_grouped: cuTensorMapEncodeTiled failed");
     P.C = q.C;
     P.ldc = q.ldc;

@@ -15,7 +15,7 @@ host: the frames' masked / depth-valid ray counts, the loss normalisers and the
 power-of-two loss scale are computed on the device (cf_train_counts /
 cf_train_norms), the weight gradients dW = dY^T X are one grouped tcgen05 launch
 per field and frame with the sample count read on the device (cf_dw_grouped over
-the feature-major fp16 saves), Adam is one multi-tensor launch that also zeroes the
+the K-blocked feature-major fp16 saves), Adam is one multi-tensor launch that also zeroes the
 gradients, and the fp16 weight blobs are repacked by one launch. So the whole step
 (key-frame ray draw included, `Trainer.capture`) replays as one CUDA graph.
 
@@ -432,25 +432,25 @@ class Trainer:
         cap, bwd, G = self.cap, st["bwd"], st["params"].G
         x0 = st["buf"].scratch.data_ptr() + self.layout[0]  # canonical features (32, cap)
 
-        def prob(A, m, B, n, C, ldc):
-            return _lib.DwProblem(A, cap, m, B, cap, n, C.data_ptr(), ldc)
+        def prob(A, ra, m, B, rb, n, C, ldc):  # K-blocked operands of ra / rb stored rows
+            return _lib.DwProblem(A, ra, m, B, rb, n, C.data_ptr(), ldc)
 
-        ps = [prob(bwd.dh1.data_ptr(), 64, x0, 32, G["G1"], 32),
-              prob(bwd.dg.data_ptr(), 16, bwd.h1.data_ptr(), 64, G["G2"], 64),
-              prob(bwd.dc1.data_ptr(), 64, bwd.cin.data_ptr(), 31, G["C1"], 31),
-              prob(bwd.dc2.data_ptr(), 64, bwd.c1.data_ptr(), 64, G["C2"], 64),
-              prob(bwd.d_o.data_ptr(), 3, bwd.c2.data_ptr(), 64, G["C3"], 64)]
+        ps = [prob(bwd.dh1.data_ptr(), 64, 64, x0, 32, 32, G["G1"], 32),
+              prob(bwd.dg.data_ptr(), 16, 16, bwd.h1.data_ptr(), 64, 64, G["G2"], 64),
+              prob(bwd.dc1.data_ptr(), 64, 64, bwd.cin.data_ptr(), 32, 31, G["C1"], 31),
+              prob(bwd.dc2.data_ptr(), 64, 64, bwd.c1.data_ptr(), 64, 64, G["C2"], 64),
+              prob(bwd.d_o.data_ptr(), 16, 3, bwd.c2.data_ptr(), 64, 64, G["C3"], 64)]
         dp = st.get("deform")
         if dp is not None:
             db, GD = st["dbufs"], dp.G
-            h = lambda l: db.save_h[128 * l].data_ptr()  # noqa: E731  h_{l+1}, (128, cap)
+            h = lambda l: db.save_h[128 * l].data_ptr()  # noqa: E731  h_{l+1}: K-blocked (128, cap)
             dpre = lambda l: db.dpre[128 * l].data_ptr()  # noqa: E731
             xd = st["buf"].scratch.data_ptr() + self.layout[1]  # [deform features | 1] (33, cap)
-            ps += [prob(db.d_o.data_ptr(), 3, h(3), 128, GD["D5"], 128),
-                   prob(dpre(3), 128, h(2), 128, GD["D4"], 128),
-                   prob(dpre(2), 128, h(1), 128, GD["D3"], 128),
-                   prob(dpre(1), 128, h(0), 128, GD["D2"], 128),
-                   prob(dpre(0), 128, xd, 33, dp.d1_tmp, 48)]
+            ps += [prob(db.d_o.data_ptr(), 16, 3, h(3), 128, 128, GD["D5"], 128),
+                   prob(dpre(3), 128, 128, h(2), 128, 128, GD["D4"], 128),
+                   prob(dpre(2), 128, 128, h(1), 128, 128, GD["D3"], 128),
+                   prob(dpre(1), 128, 128, h(0), 128, 128, GD["D2"], 128),
+                   prob(dpre(0), 128, 128, xd, 33, 33, dp.d1_tmp, 48)]
         return ps
 
     def set_frame(self, b: FrameBatch):

@@ -68,14 +68,16 @@ def run_frame(tr, b, st):
 
 
 def scratch_block(tr, st, k, rows_or_n, width, dtype, feature_major):
-    """A block of the training scratch (cf_field_train_layout offset k): feature-major
-    (width, cap)[:, :n] returned as (n, width), or sample-major (n, width)."""
+    """A block of the training scratch (cf_field_train_layout offset k): K-blocked
+    feature-major (cap / 64 blocks of (width, 64)) returned as (n, width), or
+    sample-major (n, width)."""
     sc = st["buf"].scratch
     cap = tr.cap
     es = torch.tensor([], dtype=dtype).element_size()
     o = tr.layout[k]
     if feature_major:
-        return sc[o: o + width * cap * es].view(dtype).view(width, cap)[:, :rows_or_n].t().cpu()
+        blocks = sc[o: o + width * cap * es].view(dtype).view(cap // 64, width, 64)
+        return blocks.permute(0, 2, 1).reshape(cap, width)[:rows_or_n].cpu()
     return sc[o: o + rows_or_n * width * es].view(dtype).view(rows_or_n, width).cpu()
 
 
